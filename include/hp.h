@@ -1,0 +1,206 @@
+/* hp.h -- C ABI of libhp, the B200-native (sm_100a) per-tile nuclei segmentation +
+ * feature pipeline of Teodoro et al., "High-throughput Execution of Hierarchical Analysis
+ * Pipelines on Hybrid Cluster Platforms" (arXiv 1209.3332).
+ *
+ * The paper's model: a data chunk (a 4K x 4K tile,
+ * PAPER.md:649-650) flows through a hierarchical pipeline -- two coarse stages,
+ * segmentation then feature computation, each a chain of fine
+ * operations (Table I) -- and the output is "a set of features for each
+ * segmented nucleus".  The calls below are those two stage instances
+ * per tile (hp_segment_tile, hp_features_tile; fused as hp_process_tile), the demand-driven
+ * multi-tile driver with upload/process/download overlap (hp_run_tiles; PAPER.md:370-389,
+ * 550-571) and a per-operation verification entry (hp_stage_run).
+ *
+ * Conventions (all entry points):
+ *  - No C++ exception crosses the ABI.  Every call returns an hp_status.
+ *  - Pointers documented "device" are CUDA device memory of the context's device; "host"
+ *    pointers are host memory (pinned where stated).  The CALLER owns every image, label
+ *    and table buffer; the context owns scratch sized at creation (max_width x max_height
+ *    x n_slots), lookup tables, streams and graphs.  Hot calls never allocate.
+ *  - Tile calls are asynchronous on the given stream (NULL = legacy default stream);
+ *    outputs are valid once the stream has completed.  Counts (n_objects, n_rows) stay on
+ *    the device, so no host synchronisation happens inside a tile.
+ *  - A slot has at most one call in flight; the caller serialises per slot (the paper's
+ *    "window").  Different slots may run concurrently on different streams.
+ *  - Arguments are validated before any launch -> HP_ERR_INVALID.  A CUDA error ->
+ *    HP_ERR_CUDA and the context is poisoned (every later call returns HP_ERR_CUDA).  More
+ *    objects than a table holds -> HP_ERR_CAPACITY is NOT detectable without a host sync:
+ *    the count is always written, rows beyond capacity are dropped, and hp_run_tiles
+ *    reports HP_ERR_CAPACITY per tile.
+ *  - Images are row-major.  Internal planes and the per-stage I/O of hp_stage_run are dense
+ *    (pitch = width elements).
+ */
+#ifndef HP_H
+#define HP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+struct CUstream_st;                       /* = cudaStream_t, without the CUDA headers */
+typedef struct CUstream_st* hp_stream;
+
+typedef enum {
+    HP_OK = 0,
+    HP_ERR_INVALID = 1,     /* bad argument or parameter; nothing was launched */
+    HP_ERR_CUDA = 2,        /* CUDA runtime error; the context is poisoned */
+    HP_ERR_NOMEM = 3,       /* device or pinned allocation failed at create time */
+    HP_ERR_CAPACITY = 4,    /* more objects than the table capacity (count still written) */
+    HP_ERR_UNSUPPORTED = 5  /* device is not sm_100 (B200) */
+} hp_status;
+
+/* Per-pixel flag bits of S1 (plane 'flags'). */
+enum { HP_FLAG_RBC_HI = 1, HP_FLAG_RBC_LO = 2, HP_FLAG_R_GT_B = 4, HP_FLAG_BG = 8 };
+/* Per-object flag bits of S11. */
+enum { HP_OBJ_TOUCHES_BORDER = 1 };
+/* Columns of a feature row (DESIGN.md "Feature table" gives the definitions). */
+enum {
+    HP_F_AREA = 0, HP_F_PERIMETER, HP_F_CENTROID_X, HP_F_CENTROID_Y, HP_F_BBOX_W, HP_F_BBOX_H,
+    HP_F_MAJOR, HP_F_MINOR, HP_F_ECCENTRICITY, HP_F_ORIENTATION, HP_F_EQDIAM, HP_F_COMPACTNESS,
+    HP_F_EXTENT,                                                           /* shape: 13 */
+    HP_F_INT_MEAN, HP_F_INT_STD, HP_F_INT_MIN, HP_F_INT_MAX, HP_F_INT_MEDIAN, HP_F_INT_SKEW,
+    HP_F_INT_KURT, HP_F_INT_ENTROPY, HP_F_INT_ENERGY,                      /* intensity: 9 */
+    HP_F_GRAD_MEAN, HP_F_GRAD_STD, HP_F_GRAD_SKEW, HP_F_GRAD_KURT,          /* gradient: 4 */
+    HP_F_GLCM_ASM, HP_F_GLCM_CONTRAST, HP_F_GLCM_CORRELATION, HP_F_GLCM_HOMOGENEITY,
+    HP_F_GLCM_ENTROPY, HP_F_GLCM_SHADE, HP_F_GLCM_PROMINENCE, HP_F_GLCM_MAXPROB, /* Haralick: 8 */
+    HP_NFEAT = 34
+};
+
+/* Every constant of the method (readings C3-C12 of DESIGN.md; defaults from
+ * hp_default_params).  The layout is part of the ABI. */
+typedef struct hp_params {
+    float   q[3][3];        /* q[k][j]: optical density of channel k (R,G,B) -> stain j
+                               (H, E, residual); c_j = sum_k OD_k q[k][j] */
+    float   g_scale;        /* g = clamp(rint(g_scale * c_H), 0, 255); default 170 */
+    int32_t bg_rgb_min;     /* flag BG iff min(R,G,B) > bg_rgb_min; default 220 */
+    float   bg_skip_frac;   /* tile skipped (0 objects) iff BG count >= frac * N; > 1 = off
+                               (default 2.0).  When on, hp_segment_tile syncs its stream once. */
+    int32_t rbc_t1, rbc_t2; /* RBC_HI iff R > t1*G, RBC_LO iff R > t2*G (defaults 5, 4) */
+    int32_t open_diam;      /* odd in [1, 63]; OpenCV MORPH_ELLIPSE diam x diam (default 19,
+                               "a 19x19 disk") */
+    int32_t g1;             /* candidate iff g - recon > g1 (default 50) */
+    int32_t cand_min_area, cand_max_area;  /* S5 inclusive area bounds (11, 1000) */
+    float   h;              /* h-maxima height on the distance map, > 0 (default 1.0) */
+    int32_t obj_min_area, obj_max_area;    /* S10 inclusive area bounds (21, 1000) */
+    int32_t glcm_levels;    /* must be 8 (q = g >> 5) */
+} hp_params;
+
+typedef struct hp_config {
+    int32_t   device;       /* CUDA device ordinal */
+    int32_t   max_width;    /* largest tile width  (>= 1, <= 16384) */
+    int32_t   max_height;   /* largest tile height (>= 1, <= 16384) */
+    int32_t   n_slots;      /* independent in-flight tiles (>= 1, <= 64) */
+    int32_t   max_objects;  /* feature-table rows per tile (>= 1) */
+    hp_params params;
+} hp_config;
+
+/* RGB u8, channels interleaved R,G,B; pitch_bytes >= 3*width.  Device or host per call. */
+typedef struct hp_image {
+    const uint8_t* data;
+    int32_t        width, height;
+    int64_t        pitch_bytes;
+} hp_image;
+
+/* Output of segmentation (S10): labels[y*pitch + x] = 1 + min linear index (y*width + x)
+ * of the pixel's object, 0 = background.  Device memory. */
+typedef struct hp_labels {
+    int32_t* labels;
+    int64_t  labels_pitch_elems;  /* >= width */
+    int32_t* n_objects_dev;       /* one int32 (device) */
+} hp_labels;
+
+/* Output of feature computation (S11): rows in ascending label order.  Device memory. */
+typedef struct hp_feature_table {
+    int32_t* label;       /* [capacity] */
+    int32_t* flags;       /* [capacity] HP_OBJ_* bits */
+    float*   feat;        /* [capacity][HP_NFEAT] row-major */
+    int32_t  capacity;
+    int32_t* n_rows_dev;  /* one int32 (device): number of objects (may exceed capacity) */
+} hp_feature_table;
+
+typedef struct hp_ctx hp_ctx;
+
+void        hp_default_params(hp_params* out);
+hp_status   hp_ctx_create(const hp_config* cfg, hp_ctx** out);
+hp_status   hp_ctx_destroy(hp_ctx* ctx);
+const char* hp_status_str(hp_status st);
+const char* hp_last_error(const hp_ctx* ctx);   /* ctx-local message, never NULL */
+int32_t     hp_version(void);                   /* ABI version, currently 1 */
+
+/* Segmentation stage (S1..S10) of one tile.  rgb: device image.  out: device labels. */
+hp_status hp_segment_tile(hp_ctx* ctx, int32_t slot, const hp_image* rgb, hp_labels* out,
+                          hp_stream s);
+/* Feature stage (S11) of one tile: recomputes g (S1) from rgb, then the per-object rows of
+ * the objects in lab.  rgb: device image; lab: device labels as produced by
+ * hp_segment_tile; out: device table. */
+hp_status hp_features_tile(hp_ctx* ctx, int32_t slot, const hp_image* rgb,
+                           const hp_labels* lab, hp_feature_table* out, hp_stream s);
+/* Both stages with the intermediate g shared (the hot path bench.py times). */
+hp_status hp_process_tile(hp_ctx* ctx, int32_t slot, const hp_image* rgb, hp_labels* lab,
+                          hp_feature_table* out, hp_stream s);
+
+/* Demand-driven multi-tile driver (PAPER.md:370-389 window dispatch; 550-571 upload /
+ * process / download overlap).  next() returns 0 and fills a HOST pointer to a pinned RGB
+ * tile of exactly (width, height) with the given pitch and its id, or 1 when drained.
+ * For each tile, done() is called (on the calling thread) with the tile's rows in HOST
+ * memory owned by the context and valid only during the callback (n_rows <= max_objects
+ * rows; st = HP_ERR_CAPACITY if the tile had more).  Up to n_slots tiles are in flight;
+ * each slot runs H2D -> process -> D2H on its own stream.  Blocks until drained. */
+typedef struct hp_tile_source {
+    int   (*next)(void* user, const uint8_t** host_rgb, int64_t* pitch_bytes, int64_t* tile_id);
+    void*   user;
+    int32_t width, height;
+} hp_tile_source;
+typedef struct hp_result_sink {
+    void (*done)(void* user, int64_t tile_id, int32_t n_rows, const int32_t* label,
+                 const int32_t* flags, const float* feat, hp_status st);
+    void* user;
+} hp_result_sink;
+hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_sink* sink);
+
+/* Verification ABI: run ONE operation on caller-provided DEVICE buffers (dense planes of
+ * width x height).  Layouts per stage (in -> out):
+ *  CD        in0 rgb u8x3 (pitch 3w)            -> out0 g u8, out1 flags u8, out2 bg count i64[1]
+ *  RBC       in0 flags u8                       -> out0 rbc u8 (0/1)
+ *  OPEN      in0 g u8                           -> out0 open u8
+ *  RECON     in0 g u8, in1 open u8, in2 rbc u8  -> out0 cand u8 (0/1), out1 recon u8
+ *  AREA      in0 cand u8                        -> out0 big0 u8 (0/1)
+ *  FILL      in0 big0 u8                        -> out0 F u8 (0/1)
+ *  EDT       in0 F u8                           -> out0 d2 u32, out1 dist f32
+ *  MARKERS   in0 dist f32, in1 F u8             -> out0 ML i32, out1 J f32 (0 outside F)
+ *  WATERSHED in0 dist f32, in1 ML i32, in2 F u8 -> out0 split u8, out1 c f32, out2 d i32,
+ *                                                  out3 L i32 (c, d, L: 0 outside F)
+ *  BWLABEL   in0 split u8                       -> out0 labels i32, out1 n_objects i32[1]
+ *  FEATURES  in0 labels i32, in1 g u8           -> out0 label i32[cap], out1 flags i32[cap],
+ *                                                  out2 feat f32[cap][34], out3 n_rows i32[1]
+ *                                                  (cap = max_objects)
+ *  IWPP_RAW  in0 marker u8, in1 mask u8         -> out0 recon u8, out1 stats i64[4]
+ *                                                  (tiles processed, rounds, -, -)
+ *  CCL8/CCL4 in0 fg u8                          -> out0 labels i32 (1 + min index, 0 = bg)
+ *  RECON_F32 in0 marker f32, in1 mask f32, in2 domain u8 (may be NULL) -> out0 recon f32
+ */
+typedef enum {
+    HP_STAGE_CD = 0, HP_STAGE_RBC, HP_STAGE_OPEN, HP_STAGE_RECON, HP_STAGE_AREA,
+    HP_STAGE_FILL, HP_STAGE_EDT, HP_STAGE_MARKERS, HP_STAGE_WATERSHED, HP_STAGE_BWLABEL,
+    HP_STAGE_FEATURES, HP_STAGE_IWPP_RAW, HP_STAGE_CCL8, HP_STAGE_CCL4, HP_STAGE_RECON_F32,
+    HP_STAGE_COUNT
+} hp_stage;
+typedef struct hp_stage_io {
+    const void* in[4];
+    void*       out[4];
+    int32_t     width, height;
+} hp_stage_io;
+hp_status hp_stage_run(hp_ctx* ctx, int32_t slot, hp_stage st, const hp_stage_io* io,
+                       hp_stream s);
+
+/* Per-stage timing of the last hp_segment_tile / hp_process_tile on a slot, recorded with
+ * CUDA events when enabled (adds events to the stream; off by default).  ms[11] = S1..S11. */
+hp_status hp_set_stage_timing(hp_ctx* ctx, int32_t enable);
+hp_status hp_get_stage_times(hp_ctx* ctx, int32_t slot, float* ms11);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HP_H */

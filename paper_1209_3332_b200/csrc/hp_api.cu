@@ -1,0 +1,574 @@
+// hp_api.cu -- the C ABI of include/hp.h: context, scratch arena, stage sequencing
+// (Table I order; reading C1), per-stage verification entry, and the
+// demand-driven multi-tile driver with per-slot upload/process/download streams
+// (PAPER.md:370-389 window, 550-571 prefetch and asynchronous copy).
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "hp_internal.cuh"
+
+namespace hp {
+void launch_zero_outside_f32(const float* src, const uint8_t* F, int64_t n, float* dst, cudaStream_t s);
+void launch_recon_init_f32(const float* marker, const float* mask, const uint8_t* dom, int64_t n, float* R,
+                           cudaStream_t s);
+}
+
+using namespace hp;
+
+struct hp_ctx {
+    hp_config cfg;
+    int device = 0;
+    bool poisoned = false;
+    bool timing = false;
+    std::string err;
+    float* lut = nullptr;
+    std::vector<Slot> slots;
+    std::vector<void*> dev_blocks;
+    std::vector<void*> host_blocks;
+    int rows_copied = 0;  // rows copied back per tile in hp_run_tiles
+};
+
+namespace {
+
+constexpr int kAbiVersion = 1;
+constexpr int kRowsAsync = 4096;
+
+void set_err(hp_ctx* ctx, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    ctx->err = buf;
+}
+
+hp_status cuda_fail(hp_ctx* ctx, cudaError_t e, const char* where) {
+    set_err(ctx, "%s: %s", where, cudaGetErrorString(e));
+    ctx->poisoned = true;
+    return HP_ERR_CUDA;
+}
+
+hp_status check_launch(hp_ctx* ctx, const char* where) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(ctx, e, where);
+    return HP_OK;
+}
+
+bool params_ok(const hp_params& p, std::string* why) {
+    auto bad = [&](const char* m) { *why = m; return false; };
+    for (int k = 0; k < 3; ++k)
+        for (int j = 0; j < 3; ++j)
+            if (!std::isfinite(p.q[k][j])) return bad("q must be finite");
+    if (!(p.g_scale > 0.0f) || !std::isfinite(p.g_scale)) return bad("g_scale must be > 0");
+    if (p.bg_rgb_min < -1 || p.bg_rgb_min > 255) return bad("bg_rgb_min out of [-1, 255]");
+    if (!(p.bg_skip_frac >= 0.0f)) return bad("bg_skip_frac must be >= 0");
+    if (p.rbc_t1 < 0 || p.rbc_t2 < 0 || p.rbc_t1 > 255 || p.rbc_t2 > 255) return bad("rbc_t1/t2 out of [0, 255]");
+    if (p.open_diam < 1 || p.open_diam > 63 || p.open_diam % 2 == 0) return bad("open_diam must be odd in [1, 63]");
+    if (p.g1 < -256 || p.g1 > 255) return bad("g1 out of range");
+    if (p.cand_min_area < 0 || p.cand_min_area > p.cand_max_area) return bad("cand area bounds");
+    if (p.obj_min_area < 0 || p.obj_min_area > p.obj_max_area) return bad("obj area bounds");
+    if (!(p.h > 0.0f) || !std::isfinite(p.h)) return bad("h must be finite and > 0");
+    if (p.glcm_levels != 8) return bad("glcm_levels must be 8");
+    return true;
+}
+
+hp_status enter(hp_ctx* ctx, int32_t slot) {
+    if (!ctx) return HP_ERR_INVALID;
+    if (ctx->poisoned) return HP_ERR_CUDA;
+    if (slot < 0 || slot >= ctx->cfg.n_slots) {
+        set_err(ctx, "slot %d out of [0, %d)", slot, ctx->cfg.n_slots);
+        return HP_ERR_INVALID;
+    }
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+    return HP_OK;
+}
+
+hp_status check_image(hp_ctx* ctx, const hp_image* im) {
+    if (!im || !im->data) { set_err(ctx, "null image"); return HP_ERR_INVALID; }
+    if (im->width < 1 || im->height < 1 || im->width > ctx->cfg.max_width || im->height > ctx->cfg.max_height) {
+        set_err(ctx, "image %dx%d outside [1, %d] x [1, %d]", im->width, im->height, ctx->cfg.max_width, ctx->cfg.max_height);
+        return HP_ERR_INVALID;
+    }
+    if (im->pitch_bytes < 3LL * im->width) { set_err(ctx, "pitch < 3*width"); return HP_ERR_INVALID; }
+    return HP_OK;
+}
+
+void ev(hp_ctx* ctx, Slot& sl, int k, cudaStream_t s) {
+    if (ctx->timing) cudaEventRecord(sl.ev[k], s);
+}
+
+// S1..S10 on device buffers (the segmentation stage instance)
+hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, int64_t lpitch,
+                  int32_t* n_objects, cudaStream_t s) {
+    const hp_params& p = ctx->cfg.params;
+    const int w = rgb->width, h = rgb->height;
+    ev(ctx, sl, 0, s);
+    launch_cd(rgb->data, w, h, rgb->pitch_bytes, ctx->lut, p, sl.g, sl.flags, &sl.counters[0], s);   // S1
+    ev(ctx, sl, 1, s);
+    if (p.bg_skip_frac <= 1.0f) {
+        unsigned long long nbg = 0;
+        cudaMemcpyAsync(&nbg, &sl.counters[0], sizeof(nbg), cudaMemcpyDeviceToHost, s);
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "bg skip sync");
+        if ((double)nbg >= (double)p.bg_skip_frac * (double)w * (double)h) {
+            cudaMemset2DAsync(labels, lpitch * sizeof(int32_t), 0, w * sizeof(int32_t), h, s);
+            cudaMemsetAsync(n_objects, 0, sizeof(int32_t), s);
+            for (int k = 2; k <= 10; ++k) ev(ctx, sl, k, s);
+            return check_launch(ctx, "bg skip");
+        }
+    }
+    launch_rbc(sl.flags, w, h, sl.lab, sl.aux, sl.rbc, s);                                           // S2
+    ev(ctx, sl, 2, s);
+    launch_open(sl.g, w, h, p.open_diam, sl.u8b, sl.u8a, s);                                          // S3
+    ev(ctx, sl, 3, s);
+    launch_recon_init_u8(sl.u8a, sl.g, sl.u8b, w, h, s);                                              // S4
+    launch_recon_u8(sl.g, sl.u8b, w, h, sl.wl, s);
+    launch_tophat(sl.g, sl.u8b, sl.rbc, p.g1, w, h, sl.cand, s);
+    ev(ctx, sl, 4, s);
+    CclSrc cs{sl.cand, 0, false, nullptr};                                                            // S5
+    launch_ccl(cs, w, h, 8, sl.lab, sl.aux, s);
+    launch_ccl_count(cs, w, h, sl.lab, sl.aux, s);
+    launch_ccl_area_filter(cs, w, h, sl.lab, sl.aux, p.cand_min_area, p.cand_max_area, sl.big0, s);
+    ev(ctx, sl, 5, s);
+    launch_fill_holes(sl.big0, w, h, sl.lab, sl.aux, sl.F, s);                                       // S6
+    ev(ctx, sl, 6, s);
+    launch_edt(sl.F, w, h, sl, nullptr, sl.dist, s);                                                 // S7
+    ev(ctx, sl, 7, s);
+    launch_markers(sl.dist, sl.F, p.h, w, h, sl, sl.ML, sl.J, s);                                   // S8
+    ev(ctx, sl, 8, s);
+    launch_watershed(sl.dist, sl.ML, sl.F, w, h, sl, sl.split, nullptr, nullptr, nullptr, s);       // S9
+    ev(ctx, sl, 9, s);
+    launch_bwlabel(sl.split, w, h, p.obj_min_area, p.obj_max_area, sl, labels, lpitch, n_objects, s); // S10
+    ev(ctx, sl, 10, s);
+    return check_launch(ctx, "segment");
+}
+
+hp_status features(hp_ctx* ctx, Slot& sl, int w, int h, const int32_t* labels, int64_t lpitch,
+                   hp_feature_table* out, cudaStream_t s) {
+    launch_features(labels, lpitch, sl.g, w, h, sl, ctx->cfg.max_objects, out->label, out->flags,
+                    out->feat, out->capacity, out->n_rows_dev, s);                                   // S11
+    ev(ctx, sl, 11, s);
+    return check_launch(ctx, "features");
+}
+
+hp_status check_table(hp_ctx* ctx, const hp_feature_table* t) {
+    if (!t || !t->label || !t->flags || !t->feat || !t->n_rows_dev || t->capacity < 0) {
+        set_err(ctx, "invalid feature table");
+        return HP_ERR_INVALID;
+    }
+    return HP_OK;
+}
+
+hp_status check_labels(hp_ctx* ctx, const hp_labels* l, int w) {
+    if (!l || !l->labels || !l->n_objects_dev || l->labels_pitch_elems < w) {
+        set_err(ctx, "invalid labels");
+        return HP_ERR_INVALID;
+    }
+    return HP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t hp_version(void) { return kAbiVersion; }
+
+void hp_default_params(hp_params* p) {
+    if (!p) return;
+    std::memset(p, 0, sizeof(*p));
+    // Q = M^-1, M rows = unit Ruifrok-Johnston H, E and H x E (reading C3); float hex-exact
+    // (column 0 -> c_H and column 1 -> c_E as listed in SURVEY.md §8(c) S1; column 2 is the
+    // float rounding of numpy.linalg.inv(M) in fp64 -- unused by the pipeline)
+    const float q[3][3] = {{0x1.7d33d0p+0f, -0x1.15103ap+0f, -0x1.53d24ap-2f},
+                           {-0x1.4d1a58p-3f, 0x1.1e3064p+0f, -0x1.35a158p-4f},
+                           {0x1.066118p-1f, -0x1.2b1a70p-2f, 0x1.e16e7cp-1f}};
+    std::memcpy(p->q, q, sizeof(q));
+    p->g_scale = 170.0f;
+    p->bg_rgb_min = 220;
+    p->bg_skip_frac = 2.0f;
+    p->rbc_t1 = 5;
+    p->rbc_t2 = 4;
+    p->open_diam = 19;
+    p->g1 = 50;
+    p->cand_min_area = 11;
+    p->cand_max_area = 1000;
+    p->h = 1.0f;
+    p->obj_min_area = 21;
+    p->obj_max_area = 1000;
+    p->glcm_levels = 8;
+}
+
+const char* hp_status_str(hp_status st) {
+    switch (st) {
+        case HP_OK: return "ok";
+        case HP_ERR_INVALID: return "invalid argument";
+        case HP_ERR_CUDA: return "CUDA error";
+        case HP_ERR_NOMEM: return "out of memory";
+        case HP_ERR_CAPACITY: return "object capacity exceeded";
+        case HP_ERR_UNSUPPORTED: return "unsupported device (need sm_100)";
+    }
+    return "unknown status";
+}
+
+const char* hp_last_error(const hp_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
+    if (!cfg || !out) return HP_ERR_INVALID;
+    *out = nullptr;
+    if (cfg->max_width < 1 || cfg->max_height < 1 || cfg->max_width > 16384 || cfg->max_height > 16384 ||
+        cfg->n_slots < 1 || cfg->n_slots > 64 || cfg->max_objects < 1)
+        return HP_ERR_INVALID;
+    std::string why;
+    if (!params_ok(cfg->params, &why)) return HP_ERR_INVALID;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) return HP_ERR_UNSUPPORTED;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess) return HP_ERR_CUDA;
+    if (prop.major != 10) return HP_ERR_UNSUPPORTED;
+    if (cudaSetDevice(cfg->device) != cudaSuccess) return HP_ERR_CUDA;
+
+    hp_ctx* ctx = new (std::nothrow) hp_ctx();
+    if (!ctx) return HP_ERR_NOMEM;
+    ctx->cfg = *cfg;
+    ctx->device = cfg->device;
+    ctx->rows_copied = std::min(cfg->max_objects, kRowsAsync);
+    auto dalloc = [&](size_t bytes) -> void* {
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes ? bytes : 16) != cudaSuccess) return nullptr;
+        ctx->dev_blocks.push_back(p);
+        return p;
+    };
+    auto halloc = [&](size_t bytes) -> void* {
+        void* p = nullptr;
+        if (cudaMallocHost(&p, bytes ? bytes : 16) != cudaSuccess) return nullptr;
+        ctx->host_blocks.push_back(p);
+        return p;
+    };
+    ctx->lut = (float*)dalloc(256 * sizeof(float));
+    if (!ctx->lut) { hp_ctx_destroy(ctx); return HP_ERR_NOMEM; }
+    upload_od_lut(ctx->lut, 0);
+
+    const int64_t N = (int64_t)cfg->max_width * cfg->max_height;
+    const int ntx = (cfg->max_width + kTile - 1) / kTile, nty = (cfg->max_height + kTile - 1) / kTile;
+    const int ntiles = ntx * nty;
+    const int cap = 2 * ntiles + 65536;
+    const int nseg = (cfg->max_height + 63) / 64;
+    const int mo = cfg->max_objects;
+    ctx->slots.resize(cfg->n_slots);
+    for (int i = 0; i < cfg->n_slots; ++i) {
+        Slot& s = ctx->slots[i];
+        std::memset(&s, 0, sizeof(Slot));
+        auto A = [&](size_t b) { return dalloc((b + 255) & ~size_t(255)); };
+        s.g = (uint8_t*)A(N); s.flags = (uint8_t*)A(N); s.rbc = (uint8_t*)A(N); s.u8a = (uint8_t*)A(N);
+        s.u8b = (uint8_t*)A(N); s.cand = (uint8_t*)A(N); s.big0 = (uint8_t*)A(N); s.F = (uint8_t*)A(N);
+        s.split = (uint8_t*)A(N); s.pmask = (uint8_t*)A(N);
+        s.lab = (int32_t*)A(4 * N); s.aux = (int32_t*)A(4 * N); s.ML = (int32_t*)A(4 * N);
+        s.d = (int32_t*)A(4 * N); s.L = (int32_t*)A(4 * N);
+        s.dist = (float*)A(4 * N); s.J = (float*)A(4 * N); s.c = (float*)A(4 * N);
+        s.gcol = (uint16_t*)A(2 * N);
+        s.seg_top = (int16_t*)A(2 * (size_t)nseg * cfg->max_width);
+        s.seg_bot = (int16_t*)A(2 * (size_t)nseg * cfg->max_width);
+        s.wl.state = (uint32_t*)A(4 * (size_t)ntiles);
+        s.wl.queue = (int32_t*)A(4 * (size_t)cap);
+        s.wl.ctr = (unsigned long long*)A(8 * 8);
+        s.wl.cap = cap;
+        s.obj_root = (int32_t*)A(4 * (size_t)mo);
+        s.obj_rank = (int32_t*)A(4 * (size_t)mo);
+        s.obj_bbox = (int32_t*)A(16 * (size_t)mo);
+        s.counters = (unsigned long long*)A(8 * 4);
+        s.cnt32 = (int32_t*)A(4 * 8);
+        s.rgb_dev = (uint8_t*)A(3 * N);
+        s.lab_dev = (int32_t*)A(4 * N);
+        s.tab_label = (int32_t*)A(4 * (size_t)mo);
+        s.tab_flags = (int32_t*)A(4 * (size_t)mo);
+        s.tab_feat = (float*)A(4 * (size_t)mo * HP_NFEAT);
+        s.tab_nrows = (int32_t*)A(16);
+        s.h_label = (int32_t*)halloc(4 * (size_t)mo);
+        s.h_flags = (int32_t*)halloc(4 * (size_t)mo);
+        s.h_feat = (float*)halloc(4 * (size_t)mo * HP_NFEAT);
+        s.h_nrows = (int32_t*)halloc(16);
+        void* all[] = {s.g, s.flags, s.rbc, s.u8a, s.u8b, s.cand, s.big0, s.F, s.split, s.pmask, s.lab, s.aux,
+                       s.ML, s.d, s.L, s.dist, s.J, s.c, s.gcol, s.seg_top, s.seg_bot, s.wl.state, s.wl.queue,
+                       s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
+                       s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows};
+        for (void* p : all)
+            if (!p) { hp_ctx_destroy(ctx); return HP_ERR_NOMEM; }
+        if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.done_ev, cudaEventDisableTiming) != cudaSuccess) {
+            hp_ctx_destroy(ctx);
+            return HP_ERR_CUDA;
+        }
+        for (int k = 0; k < 12; ++k)
+            if (cudaEventCreate(&s.ev[k]) != cudaSuccess) { hp_ctx_destroy(ctx); return HP_ERR_CUDA; }
+        cudaMemset(s.counters, 0, 32);
+        cudaMemset(s.cnt32, 0, 32);
+        cudaMemset(s.wl.ctr, 0, 64);
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) { hp_ctx_destroy(ctx); return HP_ERR_CUDA; }
+    *out = ctx;
+    return HP_OK;
+}
+
+hp_status hp_ctx_destroy(hp_ctx* ctx) {
+    if (!ctx) return HP_ERR_INVALID;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    for (Slot& s : ctx->slots) {
+        if (s.stream) cudaStreamDestroy(s.stream);
+        if (s.done_ev) cudaEventDestroy(s.done_ev);
+        for (int k = 0; k < 12; ++k)
+            if (s.ev[k]) cudaEventDestroy(s.ev[k]);
+    }
+    for (void* p : ctx->dev_blocks) cudaFree(p);
+    for (void* p : ctx->host_blocks) cudaFreeHost(p);
+    delete ctx;
+    return HP_OK;
+}
+
+hp_status hp_segment_tile(hp_ctx* ctx, int32_t slot, const hp_image* rgb, hp_labels* out, hp_stream s) {
+    hp_status st = enter(ctx, slot);
+    if (st) return st;
+    if ((st = check_image(ctx, rgb)) || (st = check_labels(ctx, out, rgb->width))) return st;
+    return segment(ctx, ctx->slots[slot], rgb, out->labels, out->labels_pitch_elems, out->n_objects_dev,
+                   (cudaStream_t)s);
+}
+
+hp_status hp_features_tile(hp_ctx* ctx, int32_t slot, const hp_image* rgb, const hp_labels* lab,
+                           hp_feature_table* out, hp_stream s) {
+    hp_status st = enter(ctx, slot);
+    if (st) return st;
+    if ((st = check_image(ctx, rgb)) || (st = check_labels(ctx, lab, rgb->width)) || (st = check_table(ctx, out)))
+        return st;
+    Slot& sl = ctx->slots[slot];
+    cudaStream_t cs = (cudaStream_t)s;
+    launch_cd(rgb->data, rgb->width, rgb->height, rgb->pitch_bytes, ctx->lut, ctx->cfg.params, sl.g, sl.flags,
+              nullptr, cs);
+    return features(ctx, sl, rgb->width, rgb->height, lab->labels, lab->labels_pitch_elems, out, cs);
+}
+
+hp_status hp_process_tile(hp_ctx* ctx, int32_t slot, const hp_image* rgb, hp_labels* lab,
+                          hp_feature_table* out, hp_stream s) {
+    hp_status st = enter(ctx, slot);
+    if (st) return st;
+    if ((st = check_image(ctx, rgb)) || (st = check_labels(ctx, lab, rgb->width)) || (st = check_table(ctx, out)))
+        return st;
+    Slot& sl = ctx->slots[slot];
+    cudaStream_t cs = (cudaStream_t)s;
+    st = segment(ctx, sl, rgb, lab->labels, lab->labels_pitch_elems, lab->n_objects_dev, cs);
+    if (st) return st;
+    return features(ctx, sl, rgb->width, rgb->height, lab->labels, lab->labels_pitch_elems, out, cs);
+}
+
+hp_status hp_set_stage_timing(hp_ctx* ctx, int32_t enable) {
+    if (!ctx) return HP_ERR_INVALID;
+    ctx->timing = enable != 0;
+    return HP_OK;
+}
+
+hp_status hp_get_stage_times(hp_ctx* ctx, int32_t slot, float* ms11) {
+    hp_status st = enter(ctx, slot);
+    if (st) return st;
+    if (!ms11) return HP_ERR_INVALID;
+    Slot& sl = ctx->slots[slot];
+    cudaError_t e = cudaEventSynchronize(sl.ev[11]);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "stage times");
+    for (int k = 0; k < 11; ++k) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, sl.ev[k], sl.ev[k + 1]) != cudaSuccess) ms = -1.f;
+        ms11[k] = ms;
+    }
+    cudaGetLastError();
+    return HP_OK;
+}
+
+hp_status hp_stage_run(hp_ctx* ctx, int32_t slot, hp_stage stage, const hp_stage_io* io, hp_stream strm) {
+    hp_status st = enter(ctx, slot);
+    if (st) return st;
+    if (!io || io->width < 1 || io->height < 1 || io->width > ctx->cfg.max_width || io->height > ctx->cfg.max_height) {
+        set_err(ctx, "invalid stage io");
+        return HP_ERR_INVALID;
+    }
+    Slot& sl = ctx->slots[slot];
+    const hp_params& p = ctx->cfg.params;
+    const int w = io->width, h = io->height;
+    const int64_t n = (int64_t)w * h;
+    cudaStream_t s = (cudaStream_t)strm;
+    auto need = [&](std::initializer_list<const void*> ptrs) {
+        for (const void* q : ptrs)
+            if (!q) return false;
+        return true;
+    };
+    auto in8 = [&](int k) { return (const uint8_t*)io->in[k]; };
+    switch (stage) {
+        case HP_STAGE_CD:
+            if (!need({io->in[0], io->out[0], io->out[1]})) break;
+            launch_cd(in8(0), w, h, 3LL * w, ctx->lut, p, (uint8_t*)io->out[0], (uint8_t*)io->out[1],
+                      (unsigned long long*)io->out[2], s);
+            return check_launch(ctx, "stage cd");
+        case HP_STAGE_RBC:
+            if (!need({io->in[0], io->out[0]})) break;
+            launch_rbc(in8(0), w, h, sl.lab, sl.aux, (uint8_t*)io->out[0], s);
+            return check_launch(ctx, "stage rbc");
+        case HP_STAGE_OPEN:
+            if (!need({io->in[0], io->out[0]})) break;
+            launch_open(in8(0), w, h, p.open_diam, sl.u8b, (uint8_t*)io->out[0], s);
+            return check_launch(ctx, "stage open");
+        case HP_STAGE_RECON: {
+            if (!need({io->in[0], io->in[1], io->in[2], io->out[0]})) break;
+            launch_recon_init_u8(in8(1), in8(0), sl.u8b, w, h, s);
+            launch_recon_u8(in8(0), sl.u8b, w, h, sl.wl, s);
+            launch_tophat(in8(0), sl.u8b, in8(2), p.g1, w, h, (uint8_t*)io->out[0], s);
+            if (io->out[1]) cudaMemcpyAsync(io->out[1], sl.u8b, n, cudaMemcpyDeviceToDevice, s);
+            return check_launch(ctx, "stage recon");
+        }
+        case HP_STAGE_AREA: {
+            if (!need({io->in[0], io->out[0]})) break;
+            CclSrc cs{in8(0), 0, false, nullptr};
+            launch_ccl(cs, w, h, 8, sl.lab, sl.aux, s);
+            launch_ccl_count(cs, w, h, sl.lab, sl.aux, s);
+            launch_ccl_area_filter(cs, w, h, sl.lab, sl.aux, p.cand_min_area, p.cand_max_area,
+                                   (uint8_t*)io->out[0], s);
+            return check_launch(ctx, "stage area");
+        }
+        case HP_STAGE_FILL:
+            if (!need({io->in[0], io->out[0]})) break;
+            launch_fill_holes(in8(0), w, h, sl.lab, sl.aux, (uint8_t*)io->out[0], s);
+            return check_launch(ctx, "stage fill");
+        case HP_STAGE_EDT:
+            if (!need({io->in[0], io->out[1]})) break;
+            launch_edt(in8(0), w, h, sl, (uint32_t*)io->out[0], (float*)io->out[1], s);
+            return check_launch(ctx, "stage edt");
+        case HP_STAGE_MARKERS: {
+            if (!need({io->in[0], io->in[1], io->out[0]})) break;
+            launch_markers((const float*)io->in[0], in8(1), p.h, w, h, sl, (int32_t*)io->out[0], sl.J, s);
+            if (io->out[1]) launch_zero_outside_f32(sl.J, in8(1), n, (float*)io->out[1], s);
+            return check_launch(ctx, "stage markers");
+        }
+        case HP_STAGE_WATERSHED:
+            if (!need({io->in[0], io->in[1], io->in[2], io->out[0]})) break;
+            launch_watershed((const float*)io->in[0], (const int32_t*)io->in[1], in8(2), w, h, sl,
+                             (uint8_t*)io->out[0], (float*)io->out[1], (int32_t*)io->out[2], (int32_t*)io->out[3], s);
+            return check_launch(ctx, "stage watershed");
+        case HP_STAGE_BWLABEL:
+            if (!need({io->in[0], io->out[0], io->out[1]})) break;
+            launch_bwlabel(in8(0), w, h, p.obj_min_area, p.obj_max_area, sl, (int32_t*)io->out[0], w,
+                           (int32_t*)io->out[1], s);
+            return check_launch(ctx, "stage bwlabel");
+        case HP_STAGE_FEATURES:
+            if (!need({io->in[0], io->in[1], io->out[0], io->out[1], io->out[2], io->out[3]})) break;
+            launch_features((const int32_t*)io->in[0], w, in8(1), w, h, sl, ctx->cfg.max_objects,
+                            (int32_t*)io->out[0], (int32_t*)io->out[1], (float*)io->out[2], ctx->cfg.max_objects,
+                            (int32_t*)io->out[3], s);
+            return check_launch(ctx, "stage features");
+        case HP_STAGE_IWPP_RAW: {
+            if (!need({io->in[0], io->in[1], io->out[0]})) break;
+            launch_recon_init_u8(in8(0), in8(1), (uint8_t*)io->out[0], w, h, s);
+            launch_recon_u8(in8(1), (uint8_t*)io->out[0], w, h, sl.wl, s);
+            if (io->out[1]) cudaMemcpyAsync(io->out[1], sl.wl.ctr + 3, 2 * sizeof(unsigned long long),
+                                            cudaMemcpyDeviceToDevice, s);
+            return check_launch(ctx, "stage iwpp");
+        }
+        case HP_STAGE_CCL8:
+        case HP_STAGE_CCL4: {
+            if (!need({io->in[0], io->out[0]})) break;
+            CclSrc cs{in8(0), 0, false, nullptr};
+            launch_ccl(cs, w, h, stage == HP_STAGE_CCL8 ? 8 : 4, sl.lab, nullptr, s);
+            launch_ccl_to_labels(cs, w, h, sl.lab, (int32_t*)io->out[0], s);
+            return check_launch(ctx, "stage ccl");
+        }
+        case HP_STAGE_RECON_F32: {
+            if (!need({io->in[0], io->in[1], io->out[0]})) break;
+            // R = min(marker, mask) on the domain, then IWPP
+            const float* mk = (const float*)io->in[0];
+            const float* ms = (const float*)io->in[1];
+            launch_recon_init_f32(mk, ms, in8(2), n, (float*)io->out[0], s);
+            launch_recon_f32(ms, in8(2), (float*)io->out[0], w, h, sl.wl, false, s);
+            return check_launch(ctx, "stage recon f32");
+        }
+        default:
+            break;
+    }
+    set_err(ctx, "stage %d: missing buffer or unknown stage", (int)stage);
+    return HP_ERR_INVALID;
+}
+
+hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_sink* sink) {
+    hp_status st = enter(ctx, 0);
+    if (st) return st;
+    if (!src || !src->next || !sink || !sink->done) return HP_ERR_INVALID;
+    const int w = src->width, h = src->height;
+    if (w < 1 || h < 1 || w > ctx->cfg.max_width || h > ctx->cfg.max_height) return HP_ERR_INVALID;
+    const int ns = ctx->cfg.n_slots;
+    const int mo = ctx->cfg.max_objects;
+    std::vector<int64_t> tile_of(ns, -1);
+    std::vector<hp_status> st_of(ns, HP_OK);
+    bool drained = false;
+    int inflight = 0;
+    auto deliver = [&](int i) -> hp_status {
+        Slot& sl = ctx->slots[i];
+        cudaError_t e = cudaEventSynchronize(sl.done_ev);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "run_tiles sync");
+        int nrows = *sl.h_nrows;
+        hp_status ts = st_of[i];
+        if (nrows > mo) ts = HP_ERR_CAPACITY;
+        int nr = std::min(nrows, mo);
+        if (nr > ctx->rows_copied) {  // rare: more rows than the async window
+            int extra = nr - ctx->rows_copied;
+            cudaMemcpy(sl.h_label + ctx->rows_copied, sl.tab_label + ctx->rows_copied, 4 * (size_t)extra, cudaMemcpyDeviceToHost);
+            cudaMemcpy(sl.h_flags + ctx->rows_copied, sl.tab_flags + ctx->rows_copied, 4 * (size_t)extra, cudaMemcpyDeviceToHost);
+            cudaMemcpy(sl.h_feat + (size_t)ctx->rows_copied * HP_NFEAT, sl.tab_feat + (size_t)ctx->rows_copied * HP_NFEAT,
+                       4 * (size_t)extra * HP_NFEAT, cudaMemcpyDeviceToHost);
+        }
+        sink->done(sink->user, tile_of[i], nr, sl.h_label, sl.h_flags, sl.h_feat, ts);
+        tile_of[i] = -1;
+        --inflight;
+        return HP_OK;
+    };
+    int next_slot = 0;
+    while (true) {
+        int i = next_slot;
+        next_slot = (next_slot + 1) % ns;
+        if (tile_of[i] >= 0) {
+            if ((st = deliver(i))) return st;
+        }
+        if (drained) {
+            if (inflight == 0) break;
+            continue;
+        }
+        const uint8_t* host = nullptr;
+        int64_t pitch = 0, tid = -1;
+        if (src->next(src->user, &host, &pitch, &tid) != 0) {
+            drained = true;
+            if (inflight == 0) break;
+            continue;
+        }
+        if (!host || pitch < 3LL * w) return HP_ERR_INVALID;
+        Slot& sl = ctx->slots[i];
+        cudaStream_t s = sl.stream;
+        cudaMemcpy2DAsync(sl.rgb_dev, 3 * (size_t)w, host, (size_t)pitch, 3 * (size_t)w, h, cudaMemcpyHostToDevice, s);
+        hp_image im{sl.rgb_dev, w, h, 3LL * w};
+        hp_feature_table tab{sl.tab_label, sl.tab_flags, sl.tab_feat, mo, sl.tab_nrows};
+        st = segment(ctx, sl, &im, sl.lab_dev, w, sl.cnt32 + 4, s);
+        if (!st) st = features(ctx, sl, w, h, sl.lab_dev, w, &tab, s);
+        if (st) return st;
+        cudaMemcpyAsync(sl.h_nrows, sl.tab_nrows, 4, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(sl.h_label, sl.tab_label, 4 * (size_t)ctx->rows_copied, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(sl.h_flags, sl.tab_flags, 4 * (size_t)ctx->rows_copied, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(sl.h_feat, sl.tab_feat, 4 * (size_t)ctx->rows_copied * HP_NFEAT, cudaMemcpyDeviceToHost, s);
+        cudaEventRecord(sl.done_ev, s);
+        if ((st = check_launch(ctx, "run_tiles"))) return st;
+        tile_of[i] = tid;
+        st_of[i] = HP_OK;
+        ++inflight;
+    }
+    return HP_OK;
+}
+
+}  // extern "C"

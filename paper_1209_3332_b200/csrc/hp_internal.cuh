@@ -1,0 +1,155 @@
+// hp_internal.cuh -- shared device helpers and host launcher declarations of libhp.
+// Product code: shares nothing with oracle/ (test infrastructure).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hp.h"
+
+namespace hp {
+
+constexpr int kTile = 32;          // worklist / CCL tile edge (one warp = one tile row)
+constexpr int kHalo = kTile + 2;   // tile plus a 1-pixel halo on each side
+constexpr int32_t kInfI = 0x3fffffff;
+
+// ---------------------------------------------------------------- memory helpers
+template <class T>
+__device__ __forceinline__ T ldcg(const T* p) { return __ldcg(p); }
+template <>
+__device__ __forceinline__ uint8_t ldcg<uint8_t>(const uint8_t* p) {
+    return (uint8_t)__ldcg(reinterpret_cast<const unsigned char*>(p));
+}
+template <class T>
+__device__ __forceinline__ void stcg(T* p, T v) { __stcg(p, v); }
+template <>
+__device__ __forceinline__ void stcg<uint8_t>(uint8_t* p, uint8_t v) {
+    __stcg(reinterpret_cast<unsigned char*>(p), (unsigned char)v);
+}
+
+__device__ __forceinline__ int sat_add(int a, int b) {
+    long long s = (long long)a + (long long)b;
+    return s >= kInfI ? kInfI : (int)s;
+}
+
+// N8 neighbour order of the watershed parent bitmask: bit j <-> (dx8(j), dy8(j)) =
+// (-1,-1) (0,-1) (1,-1) (-1,0) (1,0) (-1,1) (0,1) (1,1).
+__host__ __device__ __forceinline__ int dx8(int j) { return (j == 0 || j == 3 || j == 5) ? -1 : (j == 1 || j == 6) ? 0 : 1; }
+__host__ __device__ __forceinline__ int dy8(int j) { return j < 3 ? -1 : (j < 5 ? 0 : 1); }
+// index j of offset (dx, dy), dx, dy in {-1, 0, 1}, (0, 0) excluded
+__host__ __device__ __forceinline__ int nb_index(int dx, int dy) {
+    int k = (dy + 1) * 3 + (dx + 1);   // 0..8, 4 = centre
+    return k < 4 ? k : k - 1;
+}
+
+// ---------------------------------------------------------------- worklist
+// Asynchronous tile worklist (the "hierarchical queue" of PAPER.md:633, at tile grain):
+// state[t] in {IDLE, QUEUED, BUSY, BUSY_DIRTY}; queue = ring of tile ids with EMPTY
+// sentinels; ctr[0] head, ctr[1] tail, ctr[2] pending (queued or busy tiles),
+// ctr[3] tiles processed, ctr[4] local rounds.
+struct Worklist {
+    uint32_t* state;
+    int32_t* queue;
+    unsigned long long* ctr;
+    int32_t cap;      // ring capacity (>= ntiles + max warps)
+    int32_t ntx, nty; // tile grid
+};
+
+// ---------------------------------------------------------------- scratch of one slot
+struct Slot {
+    // u8 planes
+    uint8_t *g, *flags, *rbc, *u8a, *u8b, *cand, *big0, *F, *split, *pmask;
+    // 32-bit planes
+    int32_t *lab, *aux, *ML, *d, *L;
+    float *dist, *J, *c;
+    uint32_t* d2;
+    uint16_t* gcol;
+    // EDT segment summaries
+    int16_t *seg_top, *seg_bot;
+    // worklist
+    Worklist wl;
+    // objects
+    int32_t *obj_root, *obj_bbox, *obj_rank;
+    // small device counters: [0] bg count (u64), [1] any-bg flag, [2] n objects, ...
+    unsigned long long* counters;
+    int32_t* cnt32;  // [0] n_obj raw, [1] edt pathological rows, [2..] misc
+    // per-stage timing events
+    cudaEvent_t ev[12];
+    // run_tiles staging
+    uint8_t* rgb_dev;
+    int32_t* lab_dev;
+    int32_t *tab_label, *tab_flags, *tab_nrows;
+    float* tab_feat;
+    cudaStream_t stream;
+    // pinned host staging for run_tiles results
+    int32_t *h_label, *h_flags, *h_nrows;
+    float* h_feat;
+    cudaEvent_t done_ev;
+};
+
+// ---------------------------------------------------------------- launchers (host)
+// S1
+void launch_cd(const uint8_t* rgb, int w, int h, int64_t pitch, const float* lut,
+               const hp_params& p, uint8_t* g, uint8_t* flags, unsigned long long* bg_count,
+               cudaStream_t s);
+void upload_od_lut(float* lut_dev, cudaStream_t s);
+// S3
+void launch_open(const uint8_t* g, int w, int h, int diam, uint8_t* tmp, uint8_t* out,
+                 cudaStream_t s);
+// CCL engine: fg from a u8 plane (nonzero, or zero when invert), optional flag bit mask,
+// optional float equality plane (flat zones).  lab = root index (min linear index) or -1.
+struct CclSrc {
+    const uint8_t* plane;  // foreground plane
+    uint8_t bitmask;       // 0: fg = plane != 0 ; else fg = (plane & bitmask) != 0
+    bool invert;           // fg = !fg
+    const float* eq;       // if non-null: connected iff eq[p] == eq[q]
+};
+void launch_ccl(const CclSrc& src, int w, int h, int conn, int32_t* lab, int32_t* aux_zero,
+                cudaStream_t s);
+void launch_ccl_count(const CclSrc& src, int w, int h, const int32_t* lab, int32_t* aux,
+                      cudaStream_t s);
+void launch_ccl_area_filter(const CclSrc& src, int w, int h, const int32_t* lab,
+                            const int32_t* area, int amin, int amax, uint8_t* out,
+                            cudaStream_t s);
+void launch_ccl_to_labels(const CclSrc& src, int w, int h, const int32_t* lab, int32_t* out,
+                          cudaStream_t s);
+// S2
+void launch_rbc(const uint8_t* flags, int w, int h, int32_t* lab, int32_t* aux, uint8_t* rbc,
+                cudaStream_t s);
+// S6
+void launch_fill_holes(const uint8_t* big0, int w, int h, int32_t* lab, int32_t* aux,
+                       uint8_t* F, cudaStream_t s);
+// IWPP / worklist engine
+void wl_init_all(const Worklist& wl, cudaStream_t s);
+void wl_init_from_mask(const Worklist& wl, const uint8_t* mask, int w, int h, cudaStream_t s);
+void launch_recon_u8(const uint8_t* mask, uint8_t* R, int w, int h, const Worklist& wl,
+                     cudaStream_t s);
+void launch_recon_f32(const float* mask, const uint8_t* dom, float* R, int w, int h,
+                      const Worklist& wl, bool init_from_mask_tiles, cudaStream_t s);
+void launch_plateau_dist(const float* c, int32_t* d, int w, int h, const Worklist& wl,
+                         const uint8_t* F, cudaStream_t s);
+void launch_parent_min(const uint8_t* pm, int32_t* L, int w, int h, const Worklist& wl,
+                       const uint8_t* F, cudaStream_t s);
+// S4 helpers
+void launch_recon_init_u8(const uint8_t* marker, const uint8_t* mask, uint8_t* R, int w, int h,
+                          cudaStream_t s);
+void launch_tophat(const uint8_t* g, const uint8_t* R, const uint8_t* rbc, int g1, int w, int h,
+                   uint8_t* cand, cudaStream_t s);
+// S7
+void launch_edt(const uint8_t* F, int w, int h, Slot& sl, uint32_t* d2_out, float* dist,
+                cudaStream_t s);
+// S8, S9
+void launch_markers(const float* dist, const uint8_t* F, float hh, int w, int h, Slot& sl,
+                    int32_t* ML, float* J, cudaStream_t s);
+void launch_watershed(const float* dist, const int32_t* ML, const uint8_t* F, int w, int h,
+                      Slot& sl, uint8_t* split, float* c_out, int32_t* d_out, int32_t* L_out,
+                      cudaStream_t s);
+// S10
+void launch_bwlabel(const uint8_t* split, int w, int h, int amin, int amax, Slot& sl,
+                    int32_t* labels, int64_t lpitch, int32_t* n_objects, cudaStream_t s);
+// S11
+void launch_features(const int32_t* labels, int64_t lpitch, const uint8_t* g, int w, int h,
+                     Slot& sl, int32_t max_objects, int32_t* row_label, int32_t* row_flags,
+                     float* feat, int32_t capacity, int32_t* n_rows, cudaStream_t s);
+
+}  // namespace hp

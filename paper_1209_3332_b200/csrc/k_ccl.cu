@@ -1,0 +1,345 @@
+// k_ccl.cu -- connected-component labelling engine (BWLabel PAPER.md:602; used by RBC
+// detection S2, AreaThreshold S5, FillHoles S6, markers S8 and S10).
+//
+// Union-find with atomic hooking, canonical root = minimum linear index (reading C14):
+//   k_ccl_local   one 32x32 tile per CTA: shared-memory union-find over the in-tile N+
+//                 neighbours (atomicMin hooking of the larger root under the smaller),
+//                 then every pixel gets the global index of its local root (= the local
+//                 component's minimum linear index, since local and global order agree);
+//   k_ccl_merge   cross-tile edges only (top row / left / right columns): the same hooking
+//                 on the global label plane with atomicMin (L2 atomics);
+//   k_ccl_flatten every pixel points straight at its root; roots zero an aux slot so the
+//                 per-component reductions that follow need no memset.
+// Because a hook always links the larger root under the smaller, the surviving root of a
+// component is its minimum linear index -- the canonical label, in any schedule.
+#include "hp_internal.cuh"
+
+namespace hp {
+
+namespace {
+
+struct Src {
+    const uint8_t* plane;
+    uint8_t bitmask;
+    bool invert;
+    const float* eq;
+    int w, h;
+    __device__ __forceinline__ bool fg(int64_t p) const {
+        uint8_t v = plane[p];
+        bool f = bitmask ? (v & bitmask) != 0 : v != 0;
+        return f != invert;
+    }
+    __device__ __forceinline__ bool conn(int64_t p, int64_t q) const {
+        return eq == nullptr || eq[p] == eq[q];
+    }
+};
+
+Src mk(const CclSrc& s, int w, int h) { return Src{s.plane, s.bitmask, s.invert, s.eq, w, h}; }
+
+// N+ neighbours (already-visited in raster order): left, up-left, up, up-right (8-conn);
+// left, up (4-conn)
+__device__ __forceinline__ int nplus(int conn, int k, int& dx, int& dy) {
+    if (conn == 8) {
+        const int DX[4] = {-1, -1, 0, 1}, DY[4] = {0, -1, -1, -1};
+        dx = DX[k];
+        dy = DY[k];
+        return 4;
+    }
+    const int DX[2] = {-1, 0}, DY[2] = {0, -1};
+    dx = DX[k];
+    dy = DY[k];
+    return 2;
+}
+
+__device__ __forceinline__ int find_s(const int* s, int x) {
+    int p = s[x];
+    while (p != x) {
+        x = p;
+        p = s[x];
+    }
+    return x;
+}
+
+__device__ __forceinline__ void union_s(int* s, int a, int b) {
+    while (true) {
+        a = find_s(s, a);
+        b = find_s(s, b);
+        if (a == b) return;
+        if (a < b) {
+            int t = a;
+            a = b;
+            b = t;
+        }
+        int old = atomicMin(&s[a], b);
+        if (old == a) return;
+        a = old;
+    }
+}
+
+__device__ __forceinline__ int32_t find_g(const int32_t* lab, int32_t x) {
+    int32_t p = __ldcg(lab + x);
+    while (p != x) {
+        x = p;
+        p = __ldcg(lab + x);
+    }
+    return x;
+}
+
+__device__ __forceinline__ void union_g(int32_t* lab, int32_t a, int32_t b) {
+    while (true) {
+        a = find_g(lab, a);
+        b = find_g(lab, b);
+        if (a == b) return;
+        if (a < b) {
+            int32_t t = a;
+            a = b;
+            b = t;
+        }
+        int32_t old = atomicMin(&lab[a], b);
+        if (old == a) return;
+        a = old;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_ccl_local(Src src, int conn, int32_t* __restrict__ lab) {
+    __shared__ int s[kTile * kTile];
+    const int tx0 = blockIdx.x * kTile, ty0 = blockIdx.y * kTile;
+    const int lx = threadIdx.x & 31;
+    const int w = src.w, h = src.h;
+    bool fgv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        int ly = (threadIdx.x >> 5) + 8 * k;
+        int gx = tx0 + lx, gy = ty0 + ly;
+        bool f = gx < w && gy < h && src.fg((int64_t)gy * w + gx);
+        fgv[k] = f;
+        s[ly * kTile + lx] = f ? ly * kTile + lx : -1;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (!fgv[k]) continue;
+        int ly = (threadIdx.x >> 5) + 8 * k;
+        int li = ly * kTile + lx;
+        int64_t p = (int64_t)(ty0 + ly) * w + tx0 + lx;
+        int nn = conn == 8 ? 4 : 2;
+        for (int j = 0; j < nn; ++j) {
+            int dx, dy;
+            nplus(conn, j, dx, dy);
+            int nx = lx + dx, ny = ly + dy;
+            if (nx < 0 || nx >= kTile || ny < 0) continue;
+            int ni = ny * kTile + nx;
+            if (s[ni] < 0) continue;  // background never changes
+            int64_t q = (int64_t)(ty0 + ny) * w + tx0 + nx;
+            if (!src.conn(p, q)) continue;
+            union_s(s, li, ni);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        int ly = (threadIdx.x >> 5) + 8 * k;
+        int gx = tx0 + lx, gy = ty0 + ly;
+        if (gx >= w || gy >= h) continue;
+        int64_t p = (int64_t)gy * w + gx;
+        if (!fgv[k]) {
+            lab[p] = -1;
+            continue;
+        }
+        int r = find_s(s, ly * kTile + lx);
+        lab[p] = (int32_t)((int64_t)(ty0 + r / kTile) * w + tx0 + r % kTile);
+    }
+}
+
+// 96 threads per tile: top row, left column, right column; each checks its N+ neighbours
+// that fall outside the tile.
+__global__ void __launch_bounds__(96) k_ccl_merge(Src src, int conn, int32_t* __restrict__ lab) {
+    const int tx0 = blockIdx.x * kTile, ty0 = blockIdx.y * kTile;
+    const int w = src.w, h = src.h;
+    int side = threadIdx.x >> 5, i = threadIdx.x & 31;
+    int lx, ly;
+    if (side == 0) {
+        lx = i;
+        ly = 0;
+    } else if (side == 1) {
+        lx = 0;
+        ly = i;
+    } else {
+        lx = kTile - 1;
+        ly = i;
+    }
+    int gx = tx0 + lx, gy = ty0 + ly;
+    if (gx >= w || gy >= h) return;
+    int64_t p = (int64_t)gy * w + gx;
+    if (!src.fg(p)) return;
+    int nn = conn == 8 ? 4 : 2;
+    for (int j = 0; j < nn; ++j) {
+        int dx, dy;
+        nplus(conn, j, dx, dy);
+        int nx = lx + dx, ny = ly + dy;
+        if (nx >= 0 && nx < kTile && ny >= 0) continue;  // in-tile edge: done locally
+        int qx = gx + dx, qy = gy + dy;
+        if (qx < 0 || qx >= w || qy < 0) continue;
+        int64_t q = (int64_t)qy * w + qx;
+        if (!src.fg(q) || !src.conn(p, q)) continue;
+        union_g(lab, (int32_t)p, (int32_t)q);
+    }
+}
+
+__global__ void k_ccl_flatten(int32_t* __restrict__ lab, int64_t n, int32_t* __restrict__ aux) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int32_t l = lab[p];
+        if (l < 0) continue;
+        int32_t r = find_g(lab, l);
+        if (r != l) lab[p] = r;
+        if (aux && r == (int32_t)p) aux[p] = 0;
+    }
+}
+
+// per-component pixel count at the root, warp-aggregated by equal root
+__global__ void k_ccl_count(const int32_t* __restrict__ lab, int64_t n, int32_t* __restrict__ aux) {
+    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n;
+         base += (int64_t)gridDim.x * blockDim.x) {
+        int64_t p = base + threadIdx.x;
+        int32_t r = p < n ? lab[p] : -1;
+        unsigned peers = __match_any_sync(0xffffffffu, r);
+        int leader = __ffs(peers) - 1;
+        if (r >= 0 && (int)(threadIdx.x & 31) == leader) atomicAdd(&aux[r], __popc(peers));
+    }
+}
+
+__global__ void k_ccl_area_filter(Src src, const int32_t* __restrict__ lab,
+                                  const int32_t* __restrict__ area, int amin, int amax,
+                                  uint8_t* __restrict__ out) {
+    const int64_t n = (int64_t)src.w * src.h;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int32_t r = lab[p];
+        uint8_t v = 0;
+        if (r >= 0) {
+            int a = area[r];
+            v = (a >= amin && a <= amax) ? 1 : 0;
+        }
+        out[p] = v;
+    }
+}
+
+__global__ void k_ccl_to_labels(const int32_t* __restrict__ lab, int64_t n, int32_t* __restrict__ out) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int32_t r = lab[p];
+        out[p] = r >= 0 ? r + 1 : 0;
+    }
+}
+
+// S2 helpers: roots hit by an RBC_HI pixel; output = hit & R_GT_B
+__global__ void k_rbc_hit(const uint8_t* __restrict__ flags, const int32_t* __restrict__ lab,
+                          int64_t n, int32_t* __restrict__ aux) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        if ((flags[p] & (HP_FLAG_RBC_HI | HP_FLAG_RBC_LO)) == (HP_FLAG_RBC_HI | HP_FLAG_RBC_LO))
+            aux[lab[p]] = 1;
+    }
+}
+__global__ void k_rbc_out(const uint8_t* __restrict__ flags, const int32_t* __restrict__ lab,
+                          int64_t n, const int32_t* __restrict__ aux, uint8_t* __restrict__ rbc) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int32_t r = lab[p];
+        rbc[p] = (r >= 0 && aux[r] && (flags[p] & HP_FLAG_R_GT_B)) ? 1 : 0;
+    }
+}
+
+// S6 helpers: background components touching the tile border; F = big0 | enclosed bg
+__global__ void k_fill_border(const int32_t* __restrict__ lab, int w, int h, int32_t* __restrict__ aux) {
+    int64_t nb = 2LL * w + 2LL * h;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int x, y;
+        if (i < w) { x = (int)i; y = 0; }
+        else if (i < 2LL * w) { x = (int)(i - w); y = h - 1; }
+        else if (i < 2LL * w + h) { x = 0; y = (int)(i - 2LL * w); }
+        else { x = w - 1; y = (int)(i - 2LL * w - h); }
+        int32_t r = lab[(int64_t)y * w + x];
+        if (r >= 0) aux[r] = 1;
+    }
+}
+__global__ void k_fill_out(const uint8_t* __restrict__ big0, const int32_t* __restrict__ lab,
+                           int64_t n, const int32_t* __restrict__ aux, uint8_t* __restrict__ F) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        uint8_t v = big0[p] ? 1 : 0;
+        if (!v) {
+            int32_t r = lab[p];
+            v = (r >= 0 && aux[r] == 0) ? 1 : 0;
+        }
+        F[p] = v;
+    }
+}
+
+inline int grid_for(int64_t n) {
+    int64_t b = (n + 255) / 256;
+    return (int)std::min<int64_t>(b, 148 * 16);
+}
+
+}  // namespace
+
+void launch_ccl(const CclSrc& cs, int w, int h, int conn, int32_t* lab, int32_t* aux_zero,
+                cudaStream_t s) {
+    const int64_t n = (int64_t)w * h;
+    if (n == 0) return;
+    Src src = mk(cs, w, h);
+    dim3 grid((w + kTile - 1) / kTile, (h + kTile - 1) / kTile);
+    k_ccl_local<<<grid, 256, 0, s>>>(src, conn, lab);
+    k_ccl_merge<<<grid, 96, 0, s>>>(src, conn, lab);
+    k_ccl_flatten<<<grid_for(n), 256, 0, s>>>(lab, n, aux_zero);
+}
+
+void launch_ccl_count(const CclSrc&, int w, int h, const int32_t* lab, int32_t* aux,
+                      cudaStream_t s) {
+    const int64_t n = (int64_t)w * h;
+    if (n == 0) return;
+    k_ccl_count<<<grid_for(n), 256, 0, s>>>(lab, n, aux);
+}
+
+void launch_ccl_area_filter(const CclSrc& cs, int w, int h, const int32_t* lab,
+                            const int32_t* area, int amin, int amax, uint8_t* out,
+                            cudaStream_t s) {
+    const int64_t n = (int64_t)w * h;
+    if (n == 0) return;
+    k_ccl_area_filter<<<grid_for(n), 256, 0, s>>>(mk(cs, w, h), lab, area, amin, amax, out);
+}
+
+void launch_ccl_to_labels(const CclSrc&, int w, int h, const int32_t* lab, int32_t* out,
+                          cudaStream_t s) {
+    const int64_t n = (int64_t)w * h;
+    if (n == 0) return;
+    k_ccl_to_labels<<<grid_for(n), 256, 0, s>>>(lab, n, out);
+}
+
+// S2 -- RBC detection: rbc = BinRecon8(RBC_HI, RBC_LO) & R_GT_B, as CCL-select: the
+// RBC_LO components that contain an RBC_HI pixel.
+void launch_rbc(const uint8_t* flags, int w, int h, int32_t* lab, int32_t* aux, uint8_t* rbc,
+                cudaStream_t s) {
+    const int64_t n = (int64_t)w * h;
+    if (n == 0) return;
+    CclSrc cs{flags, (uint8_t)HP_FLAG_RBC_LO, false, nullptr};
+    launch_ccl(cs, w, h, 8, lab, aux, s);
+    k_rbc_hit<<<grid_for(n), 256, 0, s>>>(flags, lab, n, aux);
+    k_rbc_out<<<grid_for(n), 256, 0, s>>>(flags, lab, n, aux, rbc);
+}
+
+// S6 -- FillHolles: 4-connected background components that contain no
+// tile-border pixel are holes (reading C8).
+void launch_fill_holes(const uint8_t* big0, int w, int h, int32_t* lab, int32_t* aux,
+                       uint8_t* F, cudaStream_t s) {
+    const int64_t n = (int64_t)w * h;
+    if (n == 0) return;
+    CclSrc cs{big0, 0, true, nullptr};
+    launch_ccl(cs, w, h, 4, lab, aux, s);
+    k_fill_border<<<grid_for(2LL * (w + h)), 256, 0, s>>>(lab, w, h, aux);
+    k_fill_out<<<grid_for(n), 256, 0, s>>>(big0, lab, n, aux, F);
+}
+
+}  // namespace hp

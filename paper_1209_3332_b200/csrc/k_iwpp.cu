@@ -1,0 +1,588 @@
+// k_iwpp.cu -- irregular wavefront propagation (IWPP) engine: morphological reconstruction
+// (Vincent MR) and the watershed's monotone relaxations (W2
+// plateau distance, W3 parent-min labels).
+//
+// The paper's GPU MR is "a hierarchical queue-based wave-propagation framework"
+// (PAPER.md:632-636).  Here the hierarchy is: a device-wide asynchronous queue of 32x32
+// TILES (one warp per tile, persistent kernel, device-side termination, no host sync) and,
+// inside a tile, warp-synchronous raster / anti-raster row sweeps in shared memory in which
+// every row is closed horizontally by a warp-shuffle prefix scan of the row's per-pixel
+// update functions (Kogge-Stone over 32 lanes):
+//   MR:  f_x(t) = min(mask_x, max(b_x, t))       -- clamps compose into clamps;
+//   W2:  f_x(t) = min(a_x, t + k_x), k in {1,inf} -- min-plus along equal-c edges;
+//   W3:  f_x(t) = min(a_x, t + k_x), k in {0,inf} -- min along parent edges.
+// so a whole row propagates in 5 shuffle steps instead of 32 dependent steps.  A tile is
+// re-swept until it is locally stable; then each border pixel that can still improve a
+// halo neighbour activates that neighbour tile.  Tile states IDLE/QUEUED/BUSY/BUSY_DIRTY
+// guarantee one owner per tile, so tile data are written with plain (L2) stores.
+// Every update is a valid monotone propagation, hence any schedule reaches the same unique
+// fixed point as the oracle's sequential Vincent / BFS algorithms.
+#include <cfloat>
+#include <cmath>
+
+#include "hp_internal.cuh"
+
+namespace hp {
+
+namespace {
+
+constexpr uint32_t ST_IDLE = 0, ST_QUEUED = 1, ST_BUSY = 2, ST_DIRTY = 3;
+constexpr int32_t EMPTY = -1;
+constexpr int P = kHalo + 1;          // smem row pitch (35 words)
+constexpr int kWarps = 4;             // warps per CTA
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ unsigned long long vload(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+__device__ __forceinline__ void wl_push(const Worklist& wl, int32_t t) {
+    unsigned long long pos = atomicAdd(&wl.ctr[1], 1ull);
+    int slot = (int)(pos % (unsigned long long)wl.cap);
+    while (atomicCAS(&wl.queue[slot], EMPTY, t) != EMPTY) __nanosleep(64);
+}
+
+__device__ __forceinline__ int32_t wl_pop(const Worklist& wl) {
+    while (true) {
+        unsigned long long h = vload(&wl.ctr[0]);
+        unsigned long long t = vload(&wl.ctr[1]);
+        if (h >= t) return -1;
+        if (atomicCAS(&wl.ctr[0], h, h + 1) == h) {
+            int slot = (int)(h % (unsigned long long)wl.cap);
+            int32_t v;
+            while ((v = atomicExch(&wl.queue[slot], EMPTY)) == EMPTY) __nanosleep(32);
+            return v;
+        }
+    }
+}
+
+__device__ __forceinline__ void wl_activate(const Worklist& wl, int32_t t) {
+    uint32_t s = *reinterpret_cast<volatile uint32_t*>(&wl.state[t]);
+    while (true) {
+        if (s == ST_IDLE) {
+            uint32_t o = atomicCAS(&wl.state[t], ST_IDLE, ST_QUEUED);
+            if (o == ST_IDLE) {
+                atomicAdd(&wl.ctr[2], 1ull);
+                wl_push(wl, t);
+                return;
+            }
+            s = o;
+        } else if (s == ST_BUSY) {
+            uint32_t o = atomicCAS(&wl.state[t], ST_BUSY, ST_DIRTY);
+            if (o == ST_BUSY) return;
+            s = o;
+        } else {
+            return;  // already queued or already marked dirty
+        }
+    }
+}
+
+// ------------------------------------------------------------------ warp scans
+template <class T>
+__device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }
+template <class T>
+__device__ __forceinline__ T tmax(T a, T b) { return a > b ? a : b; }
+
+// inclusive prefix (left->right) of clamp functions; returns F_x(-inf) = lo
+template <class T>
+__device__ __forceinline__ T clamp_scan_lr(T lo, T hi, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        T lo_o = __shfl_up_sync(FULL, lo, off), hi_o = __shfl_up_sync(FULL, hi, off);
+        if (lane >= off) {
+            T nlo = tmin(hi, tmax(lo, lo_o));
+            T nhi = tmin(hi, tmax(lo, hi_o));
+            lo = nlo;
+            hi = nhi;
+        }
+    }
+    return lo;
+}
+template <class T>
+__device__ __forceinline__ T clamp_scan_rl(T lo, T hi, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        T lo_o = __shfl_down_sync(FULL, lo, off), hi_o = __shfl_down_sync(FULL, hi, off);
+        if (lane + off < 32) {
+            T nlo = tmin(hi, tmax(lo, lo_o));
+            T nhi = tmin(hi, tmax(lo, hi_o));
+            lo = nlo;
+            hi = nhi;
+        }
+    }
+    return lo;
+}
+__device__ __forceinline__ int minplus_scan_lr(int a, int k, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        int a_o = __shfl_up_sync(FULL, a, off), k_o = __shfl_up_sync(FULL, k, off);
+        if (lane >= off) {
+            a = min(a, sat_add(a_o, k));
+            k = sat_add(k, k_o);
+        }
+    }
+    return a;
+}
+__device__ __forceinline__ int minplus_scan_rl(int a, int k, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        int a_o = __shfl_down_sync(FULL, a, off), k_o = __shfl_down_sync(FULL, k, off);
+        if (lane + off < 32) {
+            a = min(a, sat_add(a_o, k));
+            k = sat_add(k, k_o);
+        }
+    }
+    return a;
+}
+
+// tile geometry of a warp job
+struct TileGeo {
+    int x0, y0, w, h;
+    __device__ __forceinline__ bool inimg(int r, int c) const {  // smem coords (halo = 0 / 33)
+        int gx = x0 - 1 + c, gy = y0 - 1 + r;
+        return gx >= 0 && gy >= 0 && gx < w && gy < h;
+    }
+    __device__ __forceinline__ int64_t gidx(int r, int c) const {
+        return (int64_t)(y0 - 1 + r) * w + (x0 - 1 + c);
+    }
+};
+
+// neighbour-tile bit for a halo cell (r, c) of the 34x34 window
+__device__ __forceinline__ uint32_t halo_bit(int r, int c) {
+    int dx = c == 0 ? -1 : (c == kHalo - 1 ? 1 : 0);
+    int dy = r == 0 ? -1 : (r == kHalo - 1 ? 1 : 0);
+    return 1u << nb_index(dx, dy);
+}
+
+// Walk the border: for each interior border pixel p and each of its halo neighbours q,
+// call f(pr, pc, qr, qc); collect the tile bits for which f returned true.
+template <class F>
+__device__ __forceinline__ uint32_t border_scan(int lane, F f) {
+    uint32_t bits = 0;
+    const int c = lane + 1;
+    // top and bottom rows
+    for (int d = -1; d <= 1; ++d) {
+        if (f(1, c, 0, c + d)) bits |= halo_bit(0, c + d);
+        if (f(kTile, c, kHalo - 1, c + d)) bits |= halo_bit(kHalo - 1, c + d);
+    }
+    // left and right columns (corners counted by the rows above)
+    const int r = lane + 1;
+    for (int d = -1; d <= 1; ++d) {
+        if (f(r, 1, r + d, 0)) bits |= halo_bit(r + d, 0);
+        if (f(r, kTile, r + d, kHalo - 1)) bits |= halo_bit(r + d, kHalo - 1);
+    }
+    return __reduce_or_sync(FULL, bits);
+}
+
+// ------------------------------------------------------------------ rules
+// Morphological reconstruction by dilation.  T = int (u8 planes, -1 = absent) or float
+// (-inf = absent: outside the image or outside the domain).
+template <class T, class PT>
+struct RuleMR {
+    static constexpr int kWords = 2 * kHalo * P;
+    const PT* mask;
+    PT* R;
+    const uint8_t* dom;  // may be null
+    int w, h;
+    __device__ static T neg();
+
+    __device__ uint32_t process(int x0, int y0, T* sm, int lane, unsigned long long* rounds) const {
+        T* sR = sm;
+        T* sM = sm + kHalo * P;
+        TileGeo g{x0, y0, w, h};
+        for (int r = 0; r < kHalo; ++r)
+            for (int c = lane; c < kHalo; c += 32) {
+                T rv = neg(), mv = neg();
+                if (g.inimg(r, c)) {
+                    int64_t i = g.gidx(r, c);
+                    if (dom == nullptr || ldcg(dom + i)) {
+                        rv = (T)ldcg(R + i);
+                        mv = (T)ldcg(mask + i);
+                    }
+                }
+                sR[r * P + c] = rv;
+                sM[r * P + c] = mv;
+            }
+        __syncwarp();
+        const int c = lane + 1;
+        bool changed_any = false;
+        int nrounds = 0;
+        while (true) {
+            bool ch = false;
+            for (int pass = 0; pass < 2; ++pass) {
+                for (int k = 0; k < kTile; ++k) {
+                    int y = pass == 0 ? 1 + k : kTile - k;
+                    T m = sM[y * P + c], rr = sR[y * P + c];
+                    T b = rr;
+                    b = tmax(b, tmax(sR[(y - 1) * P + c - 1], tmax(sR[(y - 1) * P + c], sR[(y - 1) * P + c + 1])));
+                    b = tmax(b, tmax(sR[(y + 1) * P + c - 1], tmax(sR[(y + 1) * P + c], sR[(y + 1) * P + c + 1])));
+                    if (lane == 0) b = tmax(b, sR[y * P]);
+                    if (lane == 31) b = tmax(b, sR[y * P + kHalo - 1]);
+                    T lo = tmin(b, m);
+                    T v = clamp_scan_lr<T>(lo, m, lane);
+                    T u = clamp_scan_rl<T>(v, m, lane);
+                    __syncwarp();
+                    if (u != rr) {
+                        sR[y * P + c] = u;
+                        ch = true;
+                    }
+                    __syncwarp();
+                }
+            }
+            ++nrounds;
+            if (!__any_sync(FULL, ch)) break;
+            changed_any = true;
+        }
+        if (lane == 0 && rounds) atomicAdd(rounds, (unsigned long long)nrounds);
+        if (changed_any) {
+            for (int r = 1; r <= kTile; ++r) {
+                if (!g.inimg(r, c)) continue;
+                T m = sM[r * P + c];
+                if (m == neg()) continue;  // outside the domain: never written
+                stcg(R + g.gidx(r, c), (PT)sR[r * P + c]);
+            }
+        }
+        return border_scan(lane, [&](int pr, int pc, int qr, int qc) {
+            T qm = sM[qr * P + qc];
+            if (qm == neg()) return false;
+            return tmin(sR[pr * P + pc], qm) > sR[qr * P + qc];
+        });
+    }
+};
+template <>
+__device__ int RuleMR<int, uint8_t>::neg() { return -1; }
+template <>
+__device__ float RuleMR<float, float>::neg() { return -INFINITY; }
+
+// W2: least fixed point of d(p) = min(d(p), 1 + d(q)) over N8 neighbours q with c(q) ==
+// c(p) (c is NaN outside F, so no edge leaves F).  Initial d: 0 markers, 1 pixels with a
+// higher neighbour, inf otherwise (k_ws_d_init).
+struct RuleW2 {
+    static constexpr int kWords = 2 * kHalo * P;
+    const float* cpl;
+    int32_t* d;
+    int w, h;
+    __device__ uint32_t process(int x0, int y0, int* sm, int lane, unsigned long long* rounds) const {
+        int* sD = sm;
+        float* sC = reinterpret_cast<float*>(sm + kHalo * P);
+        TileGeo g{x0, y0, w, h};
+        for (int r = 0; r < kHalo; ++r)
+            for (int c = lane; c < kHalo; c += 32) {
+                int dv = kInfI;
+                float cv = NAN;
+                if (g.inimg(r, c)) {
+                    int64_t i = g.gidx(r, c);
+                    dv = ldcg(d + i);
+                    cv = ldcg(cpl + i);
+                }
+                sD[r * P + c] = dv;
+                sC[r * P + c] = cv;
+            }
+        __syncwarp();
+        const int c = lane + 1;
+        bool changed_any = false;
+        int nrounds = 0;
+        while (true) {
+            bool ch = false;
+            for (int pass = 0; pass < 2; ++pass) {
+                for (int k = 0; k < kTile; ++k) {
+                    int y = pass == 0 ? 1 + k : kTile - k;
+                    float cp = sC[y * P + c];
+                    int dp = sD[y * P + c];
+                    int a = kInfI, kl = kInfI, kr = kInfI;
+                    if (cp == cp) {  // in F
+                        a = dp;
+#pragma unroll
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            if (sC[(y - 1) * P + c + dx] == cp) a = min(a, sat_add(sD[(y - 1) * P + c + dx], 1));
+                            if (sC[(y + 1) * P + c + dx] == cp) a = min(a, sat_add(sD[(y + 1) * P + c + dx], 1));
+                        }
+                        if (lane == 0 && sC[y * P] == cp) a = min(a, sat_add(sD[y * P], 1));
+                        if (lane == 31 && sC[y * P + kHalo - 1] == cp) a = min(a, sat_add(sD[y * P + kHalo - 1], 1));
+                        if (lane > 0 && sC[y * P + c - 1] == cp) kl = 1;
+                        if (lane < 31 && sC[y * P + c + 1] == cp) kr = 1;
+                    }
+                    int v = minplus_scan_lr(a, kl, lane);
+                    int u = minplus_scan_rl(v, kr, lane);
+                    __syncwarp();
+                    if (u < dp) {
+                        sD[y * P + c] = u;
+                        ch = true;
+                    }
+                    __syncwarp();
+                }
+            }
+            ++nrounds;
+            if (!__any_sync(FULL, ch)) break;
+            changed_any = true;
+        }
+        if (lane == 0 && rounds) atomicAdd(rounds, (unsigned long long)nrounds);
+        if (changed_any)
+            for (int r = 1; r <= kTile; ++r)
+                if (g.inimg(r, c) && sC[r * P + c] == sC[r * P + c]) stcg(d + g.gidx(r, c), sD[r * P + c]);
+        return border_scan(lane, [&](int pr, int pc, int qr, int qc) {
+            float cq = sC[qr * P + qc];
+            return cq == sC[pr * P + pc] && sat_add(sD[pr * P + pc], 1) < sD[qr * P + qc];
+        });
+    }
+};
+
+// W3: least fixed point (from +inf) of L(p) = min(L(p), L(q)) over the parents q of p
+// (bit j of pm[p] <-> neighbour (dx8(j), dy8(j))).  Markers have no parents.
+struct RuleW3 {
+    static constexpr int kWords = 2 * kHalo * P;
+    const uint8_t* pm;
+    int32_t* L;
+    int w, h;
+    __device__ uint32_t process(int x0, int y0, int* sm, int lane, unsigned long long* rounds) const {
+        int* sL = sm;
+        int* sP = sm + kHalo * P;
+        TileGeo g{x0, y0, w, h};
+        for (int r = 0; r < kHalo; ++r)
+            for (int c = lane; c < kHalo; c += 32) {
+                int lv = kInfI, pv = 0;
+                if (g.inimg(r, c)) {
+                    int64_t i = g.gidx(r, c);
+                    lv = ldcg(L + i);
+                    pv = ldcg(pm + i);
+                }
+                sL[r * P + c] = lv;
+                sP[r * P + c] = pv;
+            }
+        __syncwarp();
+        const int c = lane + 1;
+        bool changed_any = false;
+        int nrounds = 0;
+        while (true) {
+            bool ch = false;
+            for (int pass = 0; pass < 2; ++pass) {
+                for (int k = 0; k < kTile; ++k) {
+                    int y = pass == 0 ? 1 + k : kTile - k;
+                    int pmk = sP[y * P + c];
+                    int lp = sL[y * P + c];
+                    int a = lp, kl = kInfI, kr = kInfI;
+                    if (pmk) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            if (!((pmk >> j) & 1)) continue;
+                            int dx = dx8(j), dy = dy8(j);
+                            if (dy == 0) {
+                                if (dx < 0 && lane > 0) { kl = 0; continue; }
+                                if (dx > 0 && lane < 31) { kr = 0; continue; }
+                            }
+                            a = min(a, sL[(y + dy) * P + c + dx]);
+                        }
+                    }
+                    int v = minplus_scan_lr(a, kl, lane);
+                    int u = minplus_scan_rl(v, kr, lane);
+                    __syncwarp();
+                    if (u < lp) {
+                        sL[y * P + c] = u;
+                        ch = true;
+                    }
+                    __syncwarp();
+                }
+            }
+            ++nrounds;
+            if (!__any_sync(FULL, ch)) break;
+            changed_any = true;
+        }
+        if (lane == 0 && rounds) atomicAdd(rounds, (unsigned long long)nrounds);
+        if (changed_any)
+            for (int r = 1; r <= kTile; ++r)
+                if (g.inimg(r, c) && sP[r * P + c]) stcg(L + g.gidx(r, c), sL[r * P + c]);
+        return border_scan(lane, [&](int pr, int pc, int qr, int qc) {
+            int pmq = sP[qr * P + qc];
+            if (!pmq) return false;
+            int j = nb_index(pc - qc, pr - qr);  // direction q -> p
+            return ((pmq >> j) & 1) && sL[pr * P + pc] < sL[qr * P + qc];
+        });
+    }
+};
+
+// ------------------------------------------------------------------ the persistent kernel
+template <class Rule, class T>
+__global__ void __launch_bounds__(kWarps * 32) k_wl_run(Rule rule, Worklist wl) {
+    extern __shared__ __align__(16) int smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T* sm = reinterpret_cast<T*>(smem_raw) + warp * Rule::kWords;
+    while (true) {
+        int32_t t = -1;
+        if (lane == 0) t = wl_pop(wl);
+        t = __shfl_sync(FULL, t, 0);
+        if (t < 0) {
+            int done = 0;
+            if (lane == 0) done = vload(&wl.ctr[2]) == 0ull;
+            if (__shfl_sync(FULL, done, 0)) break;
+            __nanosleep(200);
+            continue;
+        }
+        if (lane == 0) atomicExch(&wl.state[t], ST_BUSY);
+        __threadfence();
+        __syncwarp();
+        const int tx = t % wl.ntx, ty = t / wl.ntx;
+        while (true) {
+            uint32_t bits = rule.process(tx * kTile, ty * kTile, sm, lane, &wl.ctr[4]);
+            __threadfence();
+            __syncwarp();
+            if (lane < 8 && ((bits >> lane) & 1)) {
+                int nx = tx + dx8(lane), ny = ty + dy8(lane);
+                if (nx >= 0 && ny >= 0 && nx < wl.ntx && ny < wl.nty) wl_activate(wl, ny * wl.ntx + nx);
+            }
+            __syncwarp();
+            int again = 0;
+            if (lane == 0) {
+                uint32_t o = atomicCAS(&wl.state[t], ST_BUSY, ST_IDLE);
+                if (o == ST_BUSY) {
+                    atomicAdd(&wl.ctr[2], ~0ull);  // pending -= 1
+                } else {
+                    atomicExch(&wl.state[t], ST_BUSY);
+                    again = 1;
+                }
+                atomicAdd(&wl.ctr[3], 1ull);
+            }
+            again = __shfl_sync(FULL, again, 0);
+            if (!again) break;
+            __threadfence();
+        }
+    }
+}
+
+__global__ void k_wl_reset(Worklist wl, int seed_all) {
+    const int n = wl.ntx * wl.nty;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < wl.cap; i += gridDim.x * blockDim.x) {
+        if (i < n) wl.state[i] = seed_all ? ST_QUEUED : ST_IDLE;
+        wl.queue[i] = (seed_all && i < n) ? i : EMPTY;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 8)
+        wl.ctr[threadIdx.x] = (seed_all && (threadIdx.x == 1 || threadIdx.x == 2)) ? (unsigned long long)n : 0ull;
+}
+
+// seed the tiles that contain any nonzero mask pixel (one warp per tile)
+__global__ void k_wl_seed_mask(Worklist wl, const uint8_t* __restrict__ mask, int w, int h) {
+    const int n = wl.ntx * wl.nty;
+    const int lane = threadIdx.x & 31;
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += (gridDim.x * blockDim.x) >> 5) {
+        int tx = t % wl.ntx, ty = t / wl.ntx;
+        int gx = tx * kTile + lane;
+        bool any = false;
+        if (gx < w)
+            for (int r = 0; r < kTile; ++r) {
+                int gy = ty * kTile + r;
+                if (gy >= h) break;
+                any |= mask[(int64_t)gy * w + gx] != 0;
+            }
+        if (__any_sync(FULL, any) && lane == 0) {
+            wl.state[t] = ST_QUEUED;
+            unsigned long long pos = atomicAdd(&wl.ctr[1], 1ull);
+            atomicAdd(&wl.ctr[2], 1ull);
+            wl.queue[pos] = t;
+        }
+    }
+}
+
+template <class Rule, class T>
+void run_rule(const Rule& rule, const Worklist& wl, cudaStream_t s) {
+    const size_t smem = sizeof(T) * Rule::kWords * kWarps;
+    static int blocks = 0;
+    if (blocks == 0) {
+        cudaFuncSetAttribute(k_wl_run<Rule, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0, dev = 0, nsm = 148;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wl_run<Rule, T>, kWarps * 32, smem);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        blocks = nsm * (per_sm > 0 ? per_sm : 1);
+    }
+    int ntiles = wl.ntx * wl.nty;
+    int b = std::min(blocks, (ntiles + kWarps - 1) / kWarps);
+    if (b < 1) b = 1;
+    k_wl_run<Rule, T><<<b, kWarps * 32, smem, s>>>(rule, wl);
+}
+
+// ------------------------------------------------------------------ init kernels
+__global__ void k_copy_min_u8(const uint8_t* __restrict__ a, const uint8_t* __restrict__ b, int64_t n,
+                              uint8_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = min(a[i], b[i]);
+}
+
+// S4 top-hat: cand = (g - recon > g1) & !rbc
+__global__ void k_tophat(const uint8_t* __restrict__ g, const uint8_t* __restrict__ R,
+                         const uint8_t* __restrict__ rbc, int g1, int64_t n, uint8_t* __restrict__ cand) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        cand[i] = (((int)g[i] - (int)R[i]) > g1 && !rbc[i]) ? 1 : 0;
+}
+
+__global__ void k_recon_init_f32(const float* __restrict__ marker, const float* __restrict__ mask,
+                                 const uint8_t* __restrict__ dom, int64_t n, float* __restrict__ R) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        R[i] = (dom == nullptr || dom[i]) ? fminf(marker[i], mask[i]) : NAN;
+}
+
+inline int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 16); }
+
+}  // namespace
+
+void launch_recon_init_f32(const float* marker, const float* mask, const uint8_t* dom, int64_t n, float* R,
+                           cudaStream_t s) {
+    if (n) k_recon_init_f32<<<grid_for(n), 256, 0, s>>>(marker, mask, dom, n, R);
+}
+
+void wl_init_all(const Worklist& wl, cudaStream_t s) {
+    k_wl_reset<<<grid_for(wl.cap), 256, 0, s>>>(wl, 1);
+}
+
+void wl_init_from_mask(const Worklist& wl, const uint8_t* mask, int w, int h, cudaStream_t s) {
+    k_wl_reset<<<grid_for(wl.cap), 256, 0, s>>>(wl, 0);
+    int n = wl.ntx * wl.nty;
+    k_wl_seed_mask<<<(int)std::min<int64_t>((n + 7) / 8, 148 * 16), 256, 0, s>>>(wl, mask, w, h);
+}
+
+void launch_recon_init_u8(const uint8_t* marker, const uint8_t* mask, uint8_t* R, int w, int h,
+                          cudaStream_t s) {
+    int64_t n = (int64_t)w * h;
+    if (n) k_copy_min_u8<<<grid_for(n), 256, 0, s>>>(marker, mask, n, R);
+}
+
+void launch_recon_u8(const uint8_t* mask, uint8_t* R, int w, int h, const Worklist& wl,
+                     cudaStream_t s) {
+    if ((int64_t)w * h == 0) return;
+    wl_init_all(wl, s);
+    RuleMR<int, uint8_t> rule{mask, R, nullptr, w, h};
+    run_rule<RuleMR<int, uint8_t>, int>(rule, wl, s);
+}
+
+void launch_recon_f32(const float* mask, const uint8_t* dom, float* R, int w, int h,
+                      const Worklist& wl, bool init_from_mask_tiles, cudaStream_t s) {
+    if ((int64_t)w * h == 0) return;
+    if (init_from_mask_tiles && dom)
+        wl_init_from_mask(wl, dom, w, h, s);
+    else
+        wl_init_all(wl, s);
+    RuleMR<float, float> rule{mask, R, dom, w, h};
+    run_rule<RuleMR<float, float>, float>(rule, wl, s);
+}
+
+void launch_plateau_dist(const float* c, int32_t* d, int w, int h, const Worklist& wl,
+                         const uint8_t* F, cudaStream_t s) {
+    if ((int64_t)w * h == 0) return;
+    wl_init_from_mask(wl, F, w, h, s);
+    RuleW2 rule{c, d, w, h};
+    run_rule<RuleW2, int>(rule, wl, s);
+}
+
+void launch_parent_min(const uint8_t* pm, int32_t* L, int w, int h, const Worklist& wl,
+                       const uint8_t* F, cudaStream_t s) {
+    if ((int64_t)w * h == 0) return;
+    wl_init_from_mask(wl, F, w, h, s);
+    RuleW3 rule{pm, L, w, h};
+    run_rule<RuleW3, int>(rule, wl, s);
+}
+
+void launch_tophat(const uint8_t* g, const uint8_t* R, const uint8_t* rbc, int g1, int w, int h,
+                   uint8_t* cand, cudaStream_t s) {
+    int64_t n = (int64_t)w * h;
+    if (n) k_tophat<<<grid_for(n), 256, 0, s>>>(g, R, rbc, g1, n, cand);
+}
+
+}  // namespace hp

@@ -1,0 +1,283 @@
+"""Thin ctypes binding of libhp (include/hp.h).  Argument marshalling only: every step of
+the pipeline runs in the library's sm_100a kernels.  torch is used for device memory and
+streams.  There is no fallback: if libhp.so is missing or the device is not a B200, the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+SO_PATH = os.path.join(_HERE, "libhp.so")
+
+NFEAT = 34
+FLAG_RBC_HI, FLAG_RBC_LO, FLAG_R_GT_B, FLAG_BG = 1, 2, 4, 8
+OBJ_TOUCHES_BORDER = 1
+FEATURE_NAMES = [
+    "area", "perimeter", "centroid_x", "centroid_y", "bbox_w", "bbox_h", "major", "minor",
+    "eccentricity", "orientation", "eqdiam", "compactness", "extent",
+    "int_mean", "int_std", "int_min", "int_max", "int_median", "int_skew", "int_kurt",
+    "int_entropy", "int_energy",
+    "grad_mean", "grad_std", "grad_skew", "grad_kurt",
+    "glcm_asm", "glcm_contrast", "glcm_correlation", "glcm_homogeneity", "glcm_entropy",
+    "glcm_shade", "glcm_prominence", "glcm_maxprob",
+]
+
+STAGES = ["CD", "RBC", "OPEN", "RECON", "AREA", "FILL", "EDT", "MARKERS", "WATERSHED",
+          "BWLABEL", "FEATURES", "IWPP_RAW", "CCL8", "CCL4", "RECON_F32"]
+STAGE = {n: i for i, n in enumerate(STAGES)}
+STATUS = {0: "ok", 1: "invalid argument", 2: "CUDA error", 3: "out of memory",
+          4: "object capacity exceeded", 5: "unsupported device (need sm_100)"}
+
+# symbols include/hp.h declares (checked by tests/test_abi.py)
+EXPORTS = ["hp_default_params", "hp_ctx_create", "hp_ctx_destroy", "hp_status_str",
+           "hp_last_error", "hp_version", "hp_segment_tile", "hp_features_tile",
+           "hp_process_tile", "hp_run_tiles", "hp_stage_run", "hp_set_stage_timing",
+           "hp_get_stage_times"]
+
+
+class HPError(RuntimeError):
+    def __init__(self, status, msg=""):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Params(C.Structure):
+    _fields_ = [("q", (C.c_float * 3) * 3), ("g_scale", C.c_float), ("bg_rgb_min", C.c_int32),
+                ("bg_skip_frac", C.c_float), ("rbc_t1", C.c_int32), ("rbc_t2", C.c_int32),
+                ("open_diam", C.c_int32), ("g1", C.c_int32), ("cand_min_area", C.c_int32),
+                ("cand_max_area", C.c_int32), ("h", C.c_float), ("obj_min_area", C.c_int32),
+                ("obj_max_area", C.c_int32), ("glcm_levels", C.c_int32)]
+
+    def to_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "q"}
+        d["q"] = [[self.q[k][j] for j in range(3)] for k in range(3)]
+        return d
+
+    @classmethod
+    def from_dict(cls, d):
+        p = cls()
+        for f, _ in cls._fields_:
+            if f == "q":
+                for k in range(3):
+                    for j in range(3):
+                        p.q[k][j] = d["q"][k][j]
+            else:
+                setattr(p, f, d[f])
+        return p
+
+
+class Config(C.Structure):
+    _fields_ = [("device", C.c_int32), ("max_width", C.c_int32), ("max_height", C.c_int32),
+                ("n_slots", C.c_int32), ("max_objects", C.c_int32), ("params", Params)]
+
+
+class Image(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("width", C.c_int32), ("height", C.c_int32),
+                ("pitch_bytes", C.c_int64)]
+
+
+class Labels(C.Structure):
+    _fields_ = [("labels", C.c_void_p), ("labels_pitch_elems", C.c_int64),
+                ("n_objects_dev", C.c_void_p)]
+
+
+class FeatureTable(C.Structure):
+    _fields_ = [("label", C.c_void_p), ("flags", C.c_void_p), ("feat", C.c_void_p),
+                ("capacity", C.c_int32), ("n_rows_dev", C.c_void_p)]
+
+
+class StageIO(C.Structure):
+    _fields_ = [("in_", C.c_void_p * 4), ("out", C.c_void_p * 4), ("width", C.c_int32),
+                ("height", C.c_int32)]
+
+
+NEXT_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
+                      C.POINTER(C.c_int64))
+DONE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_int32),
+                      C.POINTER(C.c_int32), C.POINTER(C.c_float), C.c_int)
+
+
+class TileSource(C.Structure):
+    _fields_ = [("next", NEXT_FN), ("user", C.c_void_p), ("width", C.c_int32),
+                ("height", C.c_int32)]
+
+
+class ResultSink(C.Structure):
+    _fields_ = [("done", DONE_FN), ("user", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libhp.so (built in-tree by paper_1209_3332_b200/build.py).  Raises if missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(SO_PATH):
+            raise ImportError(f"libhp.so not built ({SO_PATH}); run python -m "
+                              "paper_1209_3332_b200.build or __graft_entry__.build()")
+        L = C.CDLL(SO_PATH)
+        P, i32 = C.c_void_p, C.c_int32
+        sig = {
+            "hp_default_params": (None, [C.POINTER(Params)]),
+            "hp_ctx_create": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_void_p)]),
+            "hp_ctx_destroy": (C.c_int, [P]),
+            "hp_status_str": (C.c_char_p, [C.c_int]),
+            "hp_last_error": (C.c_char_p, [P]),
+            "hp_version": (i32, []),
+            "hp_segment_tile": (C.c_int, [P, i32, C.POINTER(Image), C.POINTER(Labels), P]),
+            "hp_features_tile": (C.c_int, [P, i32, C.POINTER(Image), C.POINTER(Labels),
+                                           C.POINTER(FeatureTable), P]),
+            "hp_process_tile": (C.c_int, [P, i32, C.POINTER(Image), C.POINTER(Labels),
+                                          C.POINTER(FeatureTable), P]),
+            "hp_run_tiles": (C.c_int, [P, C.POINTER(TileSource), C.POINTER(ResultSink)]),
+            "hp_stage_run": (C.c_int, [P, i32, C.c_int, C.POINTER(StageIO), P]),
+            "hp_set_stage_timing": (C.c_int, [P, i32]),
+            "hp_get_stage_times": (C.c_int, [P, i32, C.POINTER(C.c_float)]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def default_params() -> Params:
+    p = Params()
+    lib().hp_default_params(C.byref(p))
+    return p
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Context:
+    """One hp_ctx: scratch for n_slots tiles of up to max_width x max_height on `device`."""
+
+    def __init__(self, device=0, max_width=4096, max_height=4096, n_slots=1, max_objects=65536,
+                 params: Params | None = None):
+        cfg = Config(device, max_width, max_height, n_slots, max_objects,
+                     params if params is not None else default_params())
+        h = C.c_void_p()
+        st = lib().hp_ctx_create(C.byref(cfg), C.byref(h))
+        if st != 0:
+            raise HPError(st, "hp_ctx_create")
+        self._h = h
+        self.cfg = cfg
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hp_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _chk(self, st, what):
+        if st != 0:
+            msg = lib().hp_last_error(self._h)
+            raise HPError(st, f"{what}: {msg.decode() if msg else ''}")
+
+    @staticmethod
+    def image(rgb):
+        """rgb: uint8 tensor [H, W, 3] (device for tile calls)."""
+        h, w = rgb.shape[0], rgb.shape[1]
+        return Image(rgb.data_ptr(), w, h, rgb.stride(0) * rgb.element_size())
+
+    def segment_tile(self, slot, rgb, labels, n_objects, stream=None):
+        im = self.image(rgb)
+        lab = Labels(labels.data_ptr(), labels.stride(0), n_objects.data_ptr())
+        self._chk(lib().hp_segment_tile(self._h, slot, C.byref(im), C.byref(lab), _stream(stream)),
+                  "hp_segment_tile")
+
+    def features_tile(self, slot, rgb, labels, n_objects, t_label, t_flags, t_feat, n_rows,
+                      stream=None):
+        im = self.image(rgb)
+        lab = Labels(labels.data_ptr(), labels.stride(0), n_objects.data_ptr())
+        tab = FeatureTable(t_label.data_ptr(), t_flags.data_ptr(), t_feat.data_ptr(),
+                           t_label.shape[0], n_rows.data_ptr())
+        self._chk(lib().hp_features_tile(self._h, slot, C.byref(im), C.byref(lab), C.byref(tab),
+                                         _stream(stream)), "hp_features_tile")
+
+    def process_tile(self, slot, rgb, labels, n_objects, t_label, t_flags, t_feat, n_rows,
+                     stream=None):
+        im = self.image(rgb)
+        lab = Labels(labels.data_ptr(), labels.stride(0), n_objects.data_ptr())
+        tab = FeatureTable(t_label.data_ptr(), t_flags.data_ptr(), t_feat.data_ptr(),
+                           t_label.shape[0], n_rows.data_ptr())
+        self._chk(lib().hp_process_tile(self._h, slot, C.byref(im), C.byref(lab), C.byref(tab),
+                                        _stream(stream)), "hp_process_tile")
+
+    def stage_run(self, slot, stage, ins, outs, width, height, stream=None):
+        io = StageIO()
+        for k, t in enumerate(ins):
+            io.in_[k] = None if t is None else t.data_ptr()
+        for k, t in enumerate(outs):
+            io.out[k] = None if t is None else t.data_ptr()
+        io.width, io.height = width, height
+        st = STAGE[stage] if isinstance(stage, str) else stage
+        self._chk(lib().hp_stage_run(self._h, slot, st, C.byref(io), _stream(stream)),
+                  f"hp_stage_run({stage})")
+
+    def set_stage_timing(self, on=True):
+        self._chk(lib().hp_set_stage_timing(self._h, 1 if on else 0), "hp_set_stage_timing")
+
+    def stage_times(self, slot=0):
+        ms = (C.c_float * 11)()
+        self._chk(lib().hp_get_stage_times(self._h, slot, ms), "hp_get_stage_times")
+        return list(ms)
+
+    def run_tiles(self, next_tile, on_done, width, height):
+        """Demand-driven driver.  next_tile() -> (host_ptr:int, pitch:int, tile_id:int) or
+        None when drained; host memory must be pinned and stay valid until on_done for that
+        tile.  on_done(tile_id, label[n], flags[n], feat[n, 34], status) gets numpy COPIES."""
+        keep = []
+
+        def _next(user, pp, ppitch, ptid):
+            try:
+                r = next_tile()
+            except Exception:  # noqa: BLE001 -- never raise through C
+                return 1
+            if r is None:
+                return 1
+            ptr, pitch, tid = r
+            pp[0] = ptr
+            ppitch[0] = pitch
+            ptid[0] = tid
+            return 0
+
+        def _done(user, tid, n, plab, pflags, pfeat, st):
+            lab = np.ctypeslib.as_array(plab, shape=(max(n, 1),))[:n].copy()
+            fl = np.ctypeslib.as_array(pflags, shape=(max(n, 1),))[:n].copy()
+            ft = np.ctypeslib.as_array(pfeat, shape=(max(n, 1) * NFEAT,))[:n * NFEAT].copy()
+            on_done(int(tid), lab, fl, ft.reshape(n, NFEAT), int(st))
+
+        nf, df = NEXT_FN(_next), DONE_FN(_done)
+        keep += [nf, df]
+        src = TileSource(nf, None, width, height)
+        sink = ResultSink(df, None)
+        self._chk(lib().hp_run_tiles(self._h, C.byref(src), C.byref(sink)), "hp_run_tiles")

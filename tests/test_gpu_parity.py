@@ -1,0 +1,275 @@
+"""GPU parity: every libhp stage (called through the C ABI) against the oracle, fed the
+oracle's own inputs, bit-exact on integer outputs and within reading C18's tolerance on
+float features; then the whole pipeline end to end, the IWPP stress inputs and the
+multi-tile driver.  Needs a B200 (-m gpu)."""
+import numpy as np
+import pytest
+
+import oracle
+from synth import make_stress
+from synth.hne import TileSpec, make_config_tile, make_tile
+from tests.gpu_util import assert_features_equal, features_close, stage
+
+pytestmark = pytest.mark.gpu
+
+U8, I32, F32, U32, I64 = np.uint8, np.int32, np.float32, np.uint32, np.int64
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1209_3332_b200 import Context
+    c = Context(0, 4096, 4096, n_slots=2, max_objects=65536)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def chain():
+    """Oracle intermediates of the config-1 tile."""
+    rgb = make_config_tile(1)
+    p = oracle.default_params()
+    d = {"rgb": rgb}
+    d["g"], d["flags"], d["nbg"] = oracle.cd(rgb, p)
+    d["rbc"] = oracle.rbc(d["flags"])
+    d["open"] = oracle.open_(d["g"], 19)
+    d["cand"], d["recon"] = oracle.recon_to_nuclei(d["g"], d["open"], d["rbc"], 50, with_recon=True)
+    d["big0"] = oracle.area_threshold(d["cand"], 11, 1000)
+    d["F"] = oracle.fill_holes(d["big0"])
+    d["d2"], d["dist"] = oracle.edt(d["F"])
+    d["ML"], d["J"], _ = oracle.markers(d["dist"], d["F"], 1.0)
+    d["split"], d["c"], d["d"], d["L"] = oracle.watershed(d["dist"], d["ML"], d["F"])
+    d["labels"], d["nobj"] = oracle.bwlabel(d["split"], 21, 1000)
+    d["rows"] = oracle.features(d["labels"], d["g"])
+    return d
+
+
+def test_cd(ctx, chain):
+    h, w = chain["g"].shape
+    g, fl, nbg = stage(ctx, "CD", [chain["rgb"]], [((h, w), U8), ((h, w), U8), ((1,), I64)], w, h)
+    assert np.array_equal(g, chain["g"]) and np.array_equal(fl, chain["flags"])
+    assert int(nbg[0]) == chain["nbg"]
+
+
+def test_rbc(ctx, chain):
+    h, w = chain["g"].shape
+    (r,) = stage(ctx, "RBC", [chain["flags"]], [((h, w), U8)], w, h)
+    assert np.array_equal(r, chain["rbc"]) and r.sum() > 0
+
+
+def test_open(ctx, chain):
+    h, w = chain["g"].shape
+    (o,) = stage(ctx, "OPEN", [chain["g"]], [((h, w), U8)], w, h)
+    assert np.array_equal(o, chain["open"])
+
+
+def test_recon(ctx, chain):
+    h, w = chain["g"].shape
+    cand, rec = stage(ctx, "RECON", [chain["g"], chain["open"], chain["rbc"]],
+                      [((h, w), U8), ((h, w), U8)], w, h)
+    assert np.array_equal(rec, chain["recon"])
+    assert np.array_equal(cand, chain["cand"])
+
+
+def test_area_fill(ctx, chain):
+    h, w = chain["g"].shape
+    (b,) = stage(ctx, "AREA", [chain["cand"]], [((h, w), U8)], w, h)
+    assert np.array_equal(b, chain["big0"])
+    (F,) = stage(ctx, "FILL", [chain["big0"]], [((h, w), U8)], w, h)
+    assert np.array_equal(F, chain["F"])
+
+
+def test_edt(ctx, chain):
+    h, w = chain["g"].shape
+    d2, dist = stage(ctx, "EDT", [chain["F"]], [((h, w), U32), ((h, w), F32)], w, h)
+    assert np.array_equal(d2, chain["d2"])
+    assert np.array_equal(dist, chain["dist"])
+
+
+def test_markers_watershed(ctx, chain):
+    h, w = chain["g"].shape
+    ML, J = stage(ctx, "MARKERS", [chain["dist"], chain["F"]], [((h, w), I32), ((h, w), F32)], w, h)
+    assert np.array_equal(J, chain["J"])
+    assert np.array_equal(ML, chain["ML"])
+    split, c, d, L = stage(ctx, "WATERSHED", [chain["dist"], chain["ML"], chain["F"]],
+                           [((h, w), U8), ((h, w), F32), ((h, w), I32), ((h, w), I32)], w, h)
+    assert np.array_equal(c, chain["c"])
+    assert np.array_equal(d, chain["d"])
+    assert np.array_equal(L, chain["L"])
+    assert np.array_equal(split, chain["split"])
+
+
+def test_bwlabel_features(ctx, chain):
+    h, w = chain["g"].shape
+    lab, n = stage(ctx, "BWLABEL", [chain["split"]], [((h, w), I32), ((1,), I32)], w, h)
+    assert np.array_equal(lab, chain["labels"]) and int(n[0]) == chain["nobj"]
+    cap = 65536
+    rl, rf, ft, nr = stage(ctx, "FEATURES", [chain["labels"], chain["g"]],
+                           [((cap,), I32), ((cap,), I32), ((cap, 34), F32), ((1,), I32)], w, h)
+    k = int(nr[0])
+    ol, of, ot = chain["rows"]
+    assert k == len(ol)
+    assert_features_equal(rl[:k], rf[:k], ft[:k], ol, of, ot)
+
+
+SHAPES = [(1, 1), (1, 77), (77, 1), (33, 65), (100, 257), (257, 100), (64, 64)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("dens", [0.0, 0.3, 0.6, 1.0])
+def test_ccl_random(ctx, shape, dens):
+    h, w = shape
+    fg = (np.random.default_rng(h * 1000 + w + int(dens * 10)).random(shape) < dens).astype(U8)
+    for conn, name in [(8, "CCL8"), (4, "CCL4")]:
+        (lab,) = stage(ctx, name, [fg], [((h, w), I32)], w, h)
+        exp, _ = oracle.ccl(fg, conn)
+        assert np.array_equal(lab, exp), (name, shape, dens)
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_open_ragged(ctx, shape):
+    h, w = shape
+    g = np.random.default_rng(w * 7 + h).integers(0, 256, size=shape).astype(U8)
+    (o,) = stage(ctx, "OPEN", [g], [((h, w), U8)], w, h)
+    assert np.array_equal(o, oracle.open_(g, 19))
+
+
+@pytest.mark.parametrize("shape", SHAPES + [(300, 333)])
+@pytest.mark.parametrize("levels", [2, 256])
+def test_iwpp_random(ctx, shape, levels):
+    h, w = shape
+    rng = np.random.default_rng(h * 31 + w + levels)
+    mask = (rng.integers(0, levels, size=shape) * (255 // (levels - 1))).astype(U8)
+    marker = rng.integers(0, 256, size=shape).astype(U8)
+    marker[rng.random(shape) < 0.8] = 0
+    rec, _ = stage(ctx, "IWPP_RAW", [marker, mask], [((h, w), U8), ((4,), I64)], w, h)
+    assert np.array_equal(rec, oracle.recon_u8(marker, mask))
+
+
+@pytest.mark.parametrize("shape", [(37, 53), (130, 70), (256, 256)])
+def test_recon_f32_domain(ctx, shape):
+    h, w = shape
+    rng = np.random.default_rng(h + w)
+    dom = (rng.random(shape) < 0.75).astype(U8)
+    mask = (rng.integers(0, 20, size=shape) * 0.25).astype(F32)
+    marker = np.where(rng.random(shape) < 0.05, mask, -np.inf).astype(F32)
+    (rec,) = stage(ctx, "RECON_F32", [marker, mask, dom], [((h, w), F32)], w, h)
+    exp = oracle.recon_f32(marker, mask, dom)
+    assert np.array_equal(rec[dom == 1], exp[dom == 1])
+
+
+@pytest.mark.parametrize("shape", SHAPES + [(512, 300)])
+@pytest.mark.parametrize("dens", [0.5, 0.9, 1.0])
+def test_edt_random(ctx, shape, dens):
+    h, w = shape
+    F = (np.random.default_rng(h + 3 * w).random(shape) < dens).astype(U8)
+    d2, dist = stage(ctx, "EDT", [F], [((h, w), U32), ((h, w), F32)], w, h)
+    e2, ed = oracle.edt(F)
+    assert np.array_equal(dist, ed)
+    if (F == 0).any():
+        assert np.array_equal(d2, e2)
+
+
+def test_edt_far_background(ctx):
+    # one background column far from most pixels: exercises the Meijster fallback rows
+    h, w = 64, 1500
+    F = np.ones((h, w), U8)
+    F[:, 3] = 0
+    d2, dist = stage(ctx, "EDT", [F], [((h, w), U32), ((h, w), F32)], w, h)
+    e2, ed = oracle.edt(F)
+    assert np.array_equal(d2, e2) and np.array_equal(dist, ed)
+
+
+def _gpu_process(ctx, rgb, slot=0, cap=65536):
+    import torch
+    h, w = rgb.shape[:2]
+    t = torch.from_numpy(np.ascontiguousarray(rgb)).cuda()
+    lab = torch.zeros((h, w), dtype=torch.int32, device="cuda")
+    nobj = torch.zeros(1, dtype=torch.int32, device="cuda")
+    tl = torch.zeros(cap, dtype=torch.int32, device="cuda")
+    tf = torch.zeros(cap, dtype=torch.int32, device="cuda")
+    tt = torch.zeros((cap, 34), dtype=torch.float32, device="cuda")
+    nr = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.process_tile(slot, t, lab, nobj, tl, tf, tt, nr)
+    torch.cuda.synchronize()
+    k = int(nr.item())
+    return (lab.cpu().numpy(), int(nobj.item()), tl[:k].cpu().numpy(), tf[:k].cpu().numpy(),
+            tt[:k].cpu().numpy())
+
+
+def _check_pipeline(ctx, rgb):
+    lab, nobj, gl, gf, gt = _gpu_process(ctx, rgb)
+    olab, ol, of, ot = oracle.process_tile(rgb)
+    agree = (lab == olab).mean()
+    assert np.array_equal(lab, olab), f"pixel agreement {agree:.6f}"
+    assert nobj == len(ol)
+    assert_features_equal(gl, gf, gt, ol, of, ot)
+    return nobj
+
+
+def test_pipeline_config1(ctx):
+    assert _check_pipeline(ctx, make_config_tile(1)) > 10
+
+
+@pytest.mark.parametrize("seed,t", [(7, 0.4), (8, 0.7)])
+def test_pipeline_partial_tissue(ctx, seed, t):
+    rgb = make_tile(seed, TileSpec(1024, 768, tissue_frac=t))["rgb"]
+    _check_pipeline(ctx, rgb)
+
+
+def test_pipeline_edge_cases(ctx):
+    _check_pipeline(ctx, np.full((64, 80, 3), 255, U8))          # glass only
+    _check_pipeline(ctx, np.zeros((50, 70, 3), U8))               # black
+    _check_pipeline(ctx, make_tile(3, TileSpec(96, 136))["rgb"])  # small ragged tile
+
+
+@pytest.mark.slow
+def test_pipeline_config2_4k(ctx):
+    assert _check_pipeline(ctx, make_config_tile(2)) > 1000
+
+
+def test_determinism(ctx):
+    rgb = make_config_tile(1)
+    a = _gpu_process(ctx, rgb, slot=0)
+    b = _gpu_process(ctx, rgb, slot=1)
+    for x, y in zip(a, b):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
+
+
+@pytest.mark.parametrize("kind", ["serpentine", "spiral"])
+@pytest.mark.parametrize("ramp", [False, True])
+def test_iwpp_stress(ctx, kind, ramp):
+    size = 1024
+    marker, mask, _ = make_stress(kind, size, ramp)
+    rec, st = stage(ctx, "IWPP_RAW", [marker, mask], [((size, size), U8), ((4,), I64)], size, size)
+    assert np.array_equal(rec, mask)
+
+
+def test_run_tiles(ctx):
+    import torch
+    tiles = [make_tile(100 + i, TileSpec(512, 512))["rgb"] for i in range(5)]
+    pinned = [torch.from_numpy(t).pin_memory() for t in tiles]
+    order = list(range(len(tiles))) * 2
+    it = iter(order)
+    got = {}
+
+    def nxt():
+        try:
+            i = next(it)
+        except StopIteration:
+            return None
+        return pinned[i].data_ptr(), 3 * 512, i
+
+    def done(tid, lab, fl, ft, st):
+        assert st == 0
+        if tid in got:
+            assert np.array_equal(got[tid][2], ft)  # repeats are byte-identical
+        got[tid] = (lab, fl, ft)
+
+    ctx.run_tiles(nxt, done, 512, 512)
+    assert sorted(got) == list(range(len(tiles)))
+    for i, rgb in enumerate(tiles):
+        _, ol, of, ot = oracle.process_tile(rgb)
+        assert_features_equal(got[i][0], got[i][1], got[i][2], ol, of, ot)
