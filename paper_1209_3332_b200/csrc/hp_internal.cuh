@@ -120,7 +120,7 @@ void launch_rbc(const uint8_t* flags, int w, int h, int32_t* lab, int32_t* aux, 
 void launch_fill_holes(const uint8_t* big0, int w, int h, int32_t* lab, int32_t* aux,
                        uint8_t* F, cudaStream_t s);
 // IWPP / worklist engine
-void wl_init_all(const Worklist& wl, cudaStream_t s);
+void wl_init_all(const Worklist& wl, int w, int h, cudaStream_t s);
 void wl_init_from_mask(const Worklist& wl, const uint8_t* mask, int w, int h, cudaStream_t s);
 void launch_recon_u8(const uint8_t* mask, uint8_t* R, int w, int h, const Worklist& wl,
                      cudaStream_t s);

@@ -521,6 +521,14 @@ __global__ void k_recon_init_f32(const float* __restrict__ marker, const float* 
 
 inline int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 16); }
 
+// the tile grid follows the current image, not the context's maximum size
+Worklist sized(const Worklist& wl, int w, int h) {
+    Worklist r = wl;
+    r.ntx = (w + kTile - 1) / kTile;
+    r.nty = (h + kTile - 1) / kTile;
+    return r;
+}
+
 }  // namespace
 
 void launch_recon_init_f32(const float* marker, const float* mask, const uint8_t* dom, int64_t n, float* R,
@@ -528,11 +536,13 @@ void launch_recon_init_f32(const float* marker, const float* mask, const uint8_t
     if (n) k_recon_init_f32<<<grid_for(n), 256, 0, s>>>(marker, mask, dom, n, R);
 }
 
-void wl_init_all(const Worklist& wl, cudaStream_t s) {
+void wl_init_all(const Worklist& wl0, int w, int h, cudaStream_t s) {
+    Worklist wl = sized(wl0, w, h);
     k_wl_reset<<<grid_for(wl.cap), 256, 0, s>>>(wl, 1);
 }
 
-void wl_init_from_mask(const Worklist& wl, const uint8_t* mask, int w, int h, cudaStream_t s) {
+void wl_init_from_mask(const Worklist& wl0, const uint8_t* mask, int w, int h, cudaStream_t s) {
+    Worklist wl = sized(wl0, w, h);
     k_wl_reset<<<grid_for(wl.cap), 256, 0, s>>>(wl, 0);
     int n = wl.ntx * wl.nty;
     k_wl_seed_mask<<<(int)std::min<int64_t>((n + 7) / 8, 148 * 16), 256, 0, s>>>(wl, mask, w, h);
@@ -547,9 +557,9 @@ void launch_recon_init_u8(const uint8_t* marker, const uint8_t* mask, uint8_t* R
 void launch_recon_u8(const uint8_t* mask, uint8_t* R, int w, int h, const Worklist& wl,
                      cudaStream_t s) {
     if ((int64_t)w * h == 0) return;
-    wl_init_all(wl, s);
+    wl_init_all(wl, w, h, s);
     RuleMR<int, uint8_t> rule{mask, R, nullptr, w, h};
-    run_rule<RuleMR<int, uint8_t>, int>(rule, wl, s);
+    run_rule<RuleMR<int, uint8_t>, int>(rule, sized(wl, w, h), s);
 }
 
 void launch_recon_f32(const float* mask, const uint8_t* dom, float* R, int w, int h,
@@ -558,9 +568,9 @@ void launch_recon_f32(const float* mask, const uint8_t* dom, float* R, int w, in
     if (init_from_mask_tiles && dom)
         wl_init_from_mask(wl, dom, w, h, s);
     else
-        wl_init_all(wl, s);
+        wl_init_all(wl, w, h, s);
     RuleMR<float, float> rule{mask, R, dom, w, h};
-    run_rule<RuleMR<float, float>, float>(rule, wl, s);
+    run_rule<RuleMR<float, float>, float>(rule, sized(wl, w, h), s);
 }
 
 void launch_plateau_dist(const float* c, int32_t* d, int w, int h, const Worklist& wl,
@@ -568,7 +578,7 @@ void launch_plateau_dist(const float* c, int32_t* d, int w, int h, const Worklis
     if ((int64_t)w * h == 0) return;
     wl_init_from_mask(wl, F, w, h, s);
     RuleW2 rule{c, d, w, h};
-    run_rule<RuleW2, int>(rule, wl, s);
+    run_rule<RuleW2, int>(rule, sized(wl, w, h), s);
 }
 
 void launch_parent_min(const uint8_t* pm, int32_t* L, int w, int h, const Worklist& wl,
@@ -576,7 +586,7 @@ void launch_parent_min(const uint8_t* pm, int32_t* L, int w, int h, const Workli
     if ((int64_t)w * h == 0) return;
     wl_init_from_mask(wl, F, w, h, s);
     RuleW3 rule{pm, L, w, h};
-    run_rule<RuleW3, int>(rule, wl, s);
+    run_rule<RuleW3, int>(rule, sized(wl, w, h), s);
 }
 
 void launch_tophat(const uint8_t* g, const uint8_t* R, const uint8_t* rbc, int g1, int w, int h,
