@@ -1,0 +1,384 @@
+#!/usr/bin/env python
+"""bench.py -- 4K x 4K tiles/s (segmentation + features) on N B200s, one process per GPU.
+
+A step = one pass of the whole hot path (S1..S11) over a batch of B
+distinct synthetic 4096x4096 H&E tiles per GPU (BASELINE.json configs[1] tile shape).
+  value  device-resident tiles/s: inputs already in HBM, CUDA events on the launching
+         stream with every slot stream joined, max over ranks, all ranks' tiles counted.
+  e2e    the same metric through the public multi-tile driver hp_run_tiles: pinned host
+         tiles, H2D of every tile and D2H of its feature rows inside the timed region.
+Tiles shard across ranks with no data-path collective ("scaling": "weak").
+--impl reference times the CPU oracle (oracle/, the deliberately plain checker) on the
+box's host cores on bounded samples of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "4K×4K tiles/s (seg+features) at 1/2/4/8 B200; per-stage HBM GB/s"
+UNIT = "tiles/s"
+STAGES = ["S1 colour deconvolution", "S2 RBC detection", "S3 morph open 19x19",
+          "S4 ReconToNuclei (IWPP)", "S5 AreaThreshold", "S6 FillHoles", "S7 EDT",
+          "S8 markers (IWPP f32 + RMAX)", "S9 watershed (W1-W3)", "S10 BWLabel",
+          "S11 features"]
+# algorithmic floor bytes per pixel of each stage (read each input once,
+# write each output once, in the §8(a) layouts); DESIGN.md "Roofline" restates them.
+FLOOR_BPP = [5, 2, 2, 4, 2, 2, 5, 9, 10, 5, 5]
+DTYPE = "u8/i32/f32"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+# ----------------------------------------------------------------- inputs
+def _gen(args):
+    seed, size = args
+    from synth.hne import TileSpec, make_tile
+    cache = os.path.join(tempfile.gettempdir(), "hp_bench_tiles")
+    os.makedirs(cache, exist_ok=True)
+    fn = os.path.join(cache, f"t{seed}_{size}.npy")
+    if os.path.exists(fn):
+        try:
+            return np.load(fn)
+        except Exception:  # noqa: BLE001
+            pass
+    rgb = make_tile(seed, TileSpec(size, size))["rgb"]
+    np.save(fn + ".tmp.npy", rgb)
+    os.replace(fn + ".tmp.npy", fn)
+    return rgb
+
+
+def make_tiles(rank, batch, size):
+    seeds = [1000 + rank * batch + i for i in range(batch)]   # configs[2] pool seeds
+    nproc = max(1, min(len(seeds), (os.cpu_count() or 2) // max(1, env_int("LOCAL_WORLD_SIZE", 1))))
+    ctx = mp.get_context("fork")
+    with ctx.Pool(nproc) as pool:
+        return pool.map(_gen, [(s, size) for s in seeds])
+
+
+# ----------------------------------------------------------------- clocks
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.fn = None
+
+    def start(self):
+        try:
+            fd, self.fn = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "-i", str(self.index),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.fn, "w"), stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:  # noqa: BLE001
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.fn):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.fn)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    fn = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(fn))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback"
+
+
+def traffic_for(stage_idx):
+    """dram bytes per launch of the dominant stage's kernels from a committed ncu capture."""
+    fn = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(fn))
+        return d.get("per_stage_bytes", {}).get(str(stage_idx))
+    except Exception:  # noqa: BLE001
+        return None
+
+
+# ----------------------------------------------------------------- CPU oracle leg
+def _oracle_tile(i):
+    import oracle
+    t0 = time.perf_counter()
+    oracle.process_tile(_POOL_TILES[i % len(_POOL_TILES)], cap=65536)
+    return time.perf_counter() - t0
+
+
+_POOL_TILES = []
+
+
+def oracle_rate(tiles, n_tiles, workers):
+    """Oracle tiles/s on `workers` host processes over n_tiles tiles (one tile per task)."""
+    global _POOL_TILES
+    _POOL_TILES = tiles
+    import oracle
+    oracle.build()
+    ctx = mp.get_context("fork")
+    with ctx.Pool(workers) as pool:
+        t0 = time.perf_counter()
+        pool.map(_oracle_tile, range(n_tiles), chunksize=1)
+        wall = time.perf_counter() - t0
+    return n_tiles / wall, wall
+
+
+def cpu_workers():
+    return max(1, min(os.cpu_count() or 1, 32))
+
+
+# ----------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="hp", choices=["hp", "reference"])
+    ap.add_argument("--batch", type=int, default=8, help="distinct 4K tiles per GPU per step")
+    ap.add_argument("--slots", type=int, default=4, help="tiles in flight per GPU (n_slots)")
+    ap.add_argument("--size", type=int, default=4096)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    workload = (f"configs[1] tile shape: {args.size}x{args.size} synthetic H&E RGB tiles, "
+                f"segmentation+features; {args.batch} distinct tiles per GPU per step")
+    config = {"workload": workload, "tile": f"{args.size}x{args.size}x3 u8",
+              "batch_per_gpu": args.batch, "slots": args.slots,
+              "l2": "inputs larger than L2 (each step reads %d distinct tiles = %.0f MB)"
+                    % (args.batch, args.batch * 3 * args.size * args.size / 1e6),
+              "parallelism": f"tiles sharded over {world} GPU(s), no data-path collective"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        tiles = make_tiles(0, args.batch, args.size)
+        P = cpu_workers()
+        for _ in range(args.warmup):
+            oracle_rate(tiles, P, P)
+        vals, walls = [], []
+        for _ in range(args.steps):
+            v, w = oracle_rate(tiles, P, P)
+            vals.append(v)
+            walls.append(w)
+        total_t = sum(walls)
+        value = P * args.steps / total_t
+        sample = f"{P} tiles per step (one per host process), cycling {len(tiles)} distinct tiles"
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1000 * total_t / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": DTYPE,
+                "data": "synthetic (seeded H&E painter, synth/hne.py)", "config": config,
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "oracle",
+                                 "sample": sample},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1209_3332_b200 import Context, hp
+
+    B, S, size = args.batch, args.slots, args.size
+    t_gen = time.time()
+    tiles = make_tiles(rank, B, size)
+    log(f"[rank {rank}] generated {B} tiles in {time.time() - t_gen:.1f}s")
+    cap = 8192
+    ctx = Context(local, size, size, n_slots=S, max_objects=cap)
+    dev = [torch.from_numpy(t).cuda() for t in tiles]
+    lab = [torch.empty((size, size), dtype=torch.int32, device="cuda") for _ in range(S)]
+    nob = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(S)]
+    tl = [torch.empty(cap, dtype=torch.int32, device="cuda") for _ in range(S)]
+    tf = [torch.empty(cap, dtype=torch.int32, device="cuda") for _ in range(S)]
+    tt = [torch.empty((cap, 34), dtype=torch.float32, device="cuda") for _ in range(S)]
+    nr = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(S)]
+    streams = [torch.cuda.Stream() for _ in range(S)]
+    main_s = torch.cuda.current_stream()
+
+    def step():
+        ev0 = torch.cuda.Event()
+        ev0.record(main_s)
+        for s in streams:
+            s.wait_event(ev0)
+        for i in range(B):
+            k = i % S
+            ctx.process_tile(k, dev[i], lab[k], nob[k], tl[k], tf[k], tt[k], nr[k], stream=streams[k])
+        for s in streams:
+            e = torch.cuda.Event()
+            e.record(s)
+            main_s.wait_event(e)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    objs = sum(int(n.item()) for n in nr)
+
+    ctx.set_stage_timing(True)
+    clocks = Clocks(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    l0 = hp.launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(main_s)
+    for _ in range(args.steps):
+        step()
+    end.record(main_s)
+    torch.cuda.synchronize()
+    barrier()
+    launches = hp.launch_count() - l0
+    clk = clocks.stop()
+    ms = start.elapsed_time(end)
+    stage_sum, ntiles_timed = ctx.stage_times_accum()
+    ctx.set_stage_timing(False)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * B * args.steps / (ms_max / 1000.0)
+
+    # per-stage achieved algorithmic GB/s (stage events on the tile's own stream; slots run
+    # concurrently, so these are in-situ durations)
+    npx = size * size
+    peak, peak_kind = peaks()
+    per_stage = []
+    for k in range(11):
+        sms = stage_sum[k] / max(1, ntiles_timed)
+        gbs = FLOOR_BPP[k] * npx / (sms / 1e3) / 1e9 if sms > 0 else None
+        per_stage.append({"stage": STAGES[k], "ms": round(sms, 4), "alg_bytes_per_tile": FLOOR_BPP[k] * npx,
+                          "alg_GBps": None if gbs is None else round(gbs, 1),
+                          "frac": None if gbs is None else round(gbs / peak, 4)})
+    dom = max(range(11), key=lambda k: per_stage[k]["ms"])
+    dstage = per_stage[dom]
+    roofline = {"bound": "hbm", "kernel": dstage["stage"], "achieved": dstage["alg_GBps"],
+                "peak": peak, "unit": "GB/s",
+                "frac": dstage["frac"], "traffic": traffic_for(dom),
+                "peak_kind": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+                "share_of_step": round(dstage["ms"] / max(1e-9, sum(p["ms"] for p in per_stage)), 4)}
+
+    # e2e through hp_run_tiles: pinned host tiles, H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        pinned = [torch.from_numpy(x).pin_memory() for x in tiles]
+        rows_copied = min(cap, 4096)
+        d2h_per_tile = 4 + rows_copied * (4 + 4 + 34 * 4)
+
+        def run(ntiles):
+            it = iter(range(ntiles))
+
+            def nxt():
+                try:
+                    i = next(it)
+                except StopIteration:
+                    return None
+                return pinned[i % B].data_ptr(), 3 * size, i
+
+            def done(tid, l, f, ft, st):
+                if st != 0:
+                    raise RuntimeError(f"tile {tid} status {st}")
+
+            ctx.run_tiles(nxt, done, size, size)
+
+        run(B * max(1, args.warmup))
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        run(B * args.steps)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        barrier()
+        tw = torch.tensor([wall], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * B * args.steps / float(tw.item()), "unit": UNIT,
+               "h2d_bytes_per_step": B * 3 * size * size, "d2h_bytes_per_step": B * d2h_per_tile,
+               "api": "hp_run_tiles (pinned host tiles, per-slot H2D/compute/D2H streams)",
+               "timer": "host wall clock bracketed by device synchronize"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        P = cpu_workers()
+        n = 2 * P
+        v, w = oracle_rate(tiles, n, P)
+        cpu = {"value": v, "unit": UNIT, "cores": P, "kind": "oracle",
+               "sample": f"{n} tiles of the same workload ({len(tiles)} distinct 4K tiles cycled), "
+                         f"one tile per host process, {w:.1f}s wall"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": DTYPE,
+                "data": "synthetic (seeded H&E painter, synth/hne.py)", "config": config,
+                "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline,
+                "per_stage": per_stage, "cpu_baseline": cpu, "clocks": clk,
+                "objects_per_tile": objs / max(1, S), "impl": "hp"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    ctx.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -195,10 +195,16 @@ typedef struct hp_stage_io {
 hp_status hp_stage_run(hp_ctx* ctx, int32_t slot, hp_stage st, const hp_stage_io* io,
                        hp_stream s);
 
-/* Per-stage timing of the last hp_segment_tile / hp_process_tile on a slot, recorded with
- * CUDA events when enabled (adds events to the stream; off by default).  ms[11] = S1..S11. */
+/* Per-stage timing, recorded with CUDA events on the tile's stream when enabled (off by
+ * default).  Each segment/process call on a slot uses the next of 256 event sets per slot.
+ * hp_get_stage_times: S1..S11 milliseconds of the slot's last tile (synchronises on it).
+ * hp_stage_times_accum: sums over every tile recorded since the last accumulation or
+ * enable (up to 256 per slot), writes the number of tiles to *count, and resets. */
 hp_status hp_set_stage_timing(hp_ctx* ctx, int32_t enable);
 hp_status hp_get_stage_times(hp_ctx* ctx, int32_t slot, float* ms11);
+hp_status hp_stage_times_accum(hp_ctx* ctx, float* ms11, int32_t* count);
+/* Number of libhp kernel launches issued by this process so far (diagnostics). */
+int64_t   hp_launch_count(void);
 
 #ifdef __cplusplus
 }

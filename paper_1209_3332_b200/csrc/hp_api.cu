@@ -6,6 +6,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <array>
+#include <atomic>
 #include <mutex>
 #include <new>
 #include <string>
@@ -18,6 +20,11 @@ void launch_zero_outside_f32(const float* src, const uint8_t* F, int64_t n, floa
 void launch_recon_init_f32(const float* marker, const float* mask, const uint8_t* dom, int64_t n, float* R,
                            cudaStream_t s);
 }
+
+namespace hp {
+static std::atomic<long long> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace hp
 
 using namespace hp;
 
@@ -32,12 +39,16 @@ struct hp_ctx {
     std::vector<void*> dev_blocks;
     std::vector<void*> host_blocks;
     int rows_copied = 0;  // rows copied back per tile in hp_run_tiles
+    // stage-timing ring: per slot, kRing sets of 12 events (one set per tile)
+    std::vector<std::vector<std::array<cudaEvent_t, 12>>> ring;
+    std::vector<int> ring_pos, ring_n;
 };
 
 namespace {
 
 constexpr int kAbiVersion = 1;
 constexpr int kRowsAsync = 4096;
+constexpr int kRing = 256;
 
 void set_err(hp_ctx* ctx, const char* fmt, ...) {
     char buf[512];
@@ -100,8 +111,16 @@ hp_status check_image(hp_ctx* ctx, const hp_image* im) {
     return HP_OK;
 }
 
+int slot_index(hp_ctx* ctx, Slot& sl) { return (int)(&sl - ctx->slots.data()); }
+
 void ev(hp_ctx* ctx, Slot& sl, int k, cudaStream_t s) {
-    if (ctx->timing) cudaEventRecord(sl.ev[k], s);
+    if (!ctx->timing) return;
+    int i = slot_index(ctx, sl);
+    if (k == 0) {
+        ctx->ring_pos[i] = (ctx->ring_pos[i] + 1) % kRing;
+        ctx->ring_n[i] = std::min(ctx->ring_n[i] + 1, kRing);
+    }
+    cudaEventRecord(ctx->ring[i][ctx->ring_pos[i]][k], s);
 }
 
 // S1..S10 on device buffers (the segmentation stage instance)
@@ -179,6 +198,8 @@ hp_status check_labels(hp_ctx* ctx, const hp_labels* l, int w) {
 extern "C" {
 
 int32_t hp_version(void) { return kAbiVersion; }
+
+int64_t hp_launch_count(void) { return hp::g_launches.load(); }
 
 void hp_default_params(hp_params* p) {
     if (!p) return;
@@ -305,8 +326,6 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
             hp_ctx_destroy(ctx);
             return HP_ERR_CUDA;
         }
-        for (int k = 0; k < 12; ++k)
-            if (cudaEventCreate(&s.ev[k]) != cudaSuccess) { hp_ctx_destroy(ctx); return HP_ERR_CUDA; }
         cudaMemset(s.counters, 0, 32);
         cudaMemset(s.cnt32, 0, 32);
         cudaMemset(s.wl.ctr, 0, 64);
@@ -323,9 +342,11 @@ hp_status hp_ctx_destroy(hp_ctx* ctx) {
     for (Slot& s : ctx->slots) {
         if (s.stream) cudaStreamDestroy(s.stream);
         if (s.done_ev) cudaEventDestroy(s.done_ev);
-        for (int k = 0; k < 12; ++k)
-            if (s.ev[k]) cudaEventDestroy(s.ev[k]);
     }
+    for (auto& r : ctx->ring)
+        for (auto& set : r)
+            for (auto& e : set)
+                if (e) cudaEventDestroy(e);
     for (void* p : ctx->dev_blocks) cudaFree(p);
     for (void* p : ctx->host_blocks) cudaFreeHost(p);
     delete ctx;
@@ -367,24 +388,60 @@ hp_status hp_process_tile(hp_ctx* ctx, int32_t slot, const hp_image* rgb, hp_lab
 }
 
 hp_status hp_set_stage_timing(hp_ctx* ctx, int32_t enable) {
-    if (!ctx) return HP_ERR_INVALID;
+    hp_status st = enter(ctx, 0);
+    if (st) return st;
+    if (enable && ctx->ring.empty()) {
+        ctx->ring.resize(ctx->slots.size());
+        ctx->ring_pos.assign(ctx->slots.size(), -1);
+        ctx->ring_n.assign(ctx->slots.size(), 0);
+        for (auto& r : ctx->ring) {
+            r.resize(kRing);
+            for (auto& set : r)
+                for (auto& e : set)
+                    if (cudaEventCreate(&e) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "event create");
+        }
+    }
+    if (enable)
+        for (size_t i = 0; i < ctx->slots.size(); ++i) ctx->ring_n[i] = 0;
     ctx->timing = enable != 0;
+    return HP_OK;
+}
+
+static hp_status sum_set(hp_ctx* ctx, std::array<cudaEvent_t, 12>& set, float* ms11) {
+    cudaError_t e = cudaEventSynchronize(set[11]);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "stage times");
+    for (int k = 0; k < 11; ++k) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, set[k], set[k + 1]) != cudaSuccess) ms = 0.f;
+        ms11[k] += ms;
+    }
+    cudaGetLastError();
     return HP_OK;
 }
 
 hp_status hp_get_stage_times(hp_ctx* ctx, int32_t slot, float* ms11) {
     hp_status st = enter(ctx, slot);
     if (st) return st;
-    if (!ms11) return HP_ERR_INVALID;
-    Slot& sl = ctx->slots[slot];
-    cudaError_t e = cudaEventSynchronize(sl.ev[11]);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "stage times");
-    for (int k = 0; k < 11; ++k) {
-        float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, sl.ev[k], sl.ev[k + 1]) != cudaSuccess) ms = -1.f;
-        ms11[k] = ms;
+    if (!ms11 || ctx->ring.empty() || ctx->ring_n[slot] == 0) return HP_ERR_INVALID;
+    for (int k = 0; k < 11; ++k) ms11[k] = 0.f;
+    return sum_set(ctx, ctx->ring[slot][ctx->ring_pos[slot]], ms11);
+}
+
+hp_status hp_stage_times_accum(hp_ctx* ctx, float* ms11, int32_t* count) {
+    hp_status st = enter(ctx, 0);
+    if (st) return st;
+    if (!ms11 || !count || ctx->ring.empty()) return HP_ERR_INVALID;
+    for (int k = 0; k < 11; ++k) ms11[k] = 0.f;
+    int32_t n = 0;
+    for (size_t i = 0; i < ctx->slots.size(); ++i) {
+        for (int j = 0; j < ctx->ring_n[i]; ++j) {
+            int pos = (ctx->ring_pos[i] - j + kRing) % kRing;
+            if ((st = sum_set(ctx, ctx->ring[i][pos], ms11))) return st;
+            ++n;
+        }
+        ctx->ring_n[i] = 0;
     }
-    cudaGetLastError();
+    *count = n;
     return HP_OK;
 }
 

@@ -73,8 +73,6 @@ struct Slot {
     // small device counters: [0] bg count (u64), [1] any-bg flag, [2] n objects, ...
     unsigned long long* counters;
     int32_t* cnt32;  // [0] n_obj raw, [1] edt pathological rows, [2..] misc
-    // per-stage timing events
-    cudaEvent_t ev[12];
     // run_tiles staging
     uint8_t* rgb_dev;
     int32_t* lab_dev;
@@ -88,6 +86,9 @@ struct Slot {
 };
 
 // ---------------------------------------------------------------- launchers (host)
+// every kernel launch of libhp goes through (note_launch(), kernel<<<...>>>(...)) so the
+// bench can report how many of OUR kernels ran (hp_launch_count)
+void note_launch();
 // S1
 void launch_cd(const uint8_t* rgb, int w, int h, int64_t pitch, const float* lut,
                const hp_params& p, uint8_t* g, uint8_t* flags, unsigned long long* bg_count,

@@ -51,13 +51,21 @@ __device__ __forceinline__ int nplus(int conn, int k, int& dx, int& dy) {
     return 2;
 }
 
-__device__ __forceinline__ int find_s(const int* s, int x) {
-    int p = s[x];
-    while (p != x) {
-        x = p;
-        p = s[x];
+__device__ __forceinline__ int find_s(int* s, int x) {
+    volatile int* vs = s;
+    int r = x, p = vs[r];
+    while (p != r) {
+        r = p;
+        p = vs[r];
     }
-    return x;
+    // path compression (monotone: atomicMin never undoes a concurrent hook)
+    while (x != r) {
+        int nx = vs[x];
+        if (nx <= r) break;
+        atomicMin(&s[x], r);
+        x = nx;
+    }
+    return r;
 }
 
 __device__ __forceinline__ void union_s(int* s, int a, int b) {
@@ -85,10 +93,23 @@ __device__ __forceinline__ int32_t find_g(const int32_t* lab, int32_t x) {
     return x;
 }
 
+// find with path compression: every node on the walked path is re-hooked straight to the
+// root found (atomicMin keeps hooks monotone, so concurrent unions are never undone)
+__device__ __forceinline__ int32_t find_gc(int32_t* lab, int32_t x) {
+    int32_t r = find_g(lab, x);
+    while (x != r) {
+        int32_t nx = __ldcg(lab + x);
+        if (nx <= r) break;
+        atomicMin(&lab[x], r);
+        x = nx;
+    }
+    return r;
+}
+
 __device__ __forceinline__ void union_g(int32_t* lab, int32_t a, int32_t b) {
     while (true) {
-        a = find_g(lab, a);
-        b = find_g(lab, b);
+        a = find_gc(lab, a);
+        b = find_gc(lab, b);
         if (a == b) return;
         if (a < b) {
             int32_t t = a;
@@ -107,13 +128,21 @@ __global__ void __launch_bounds__(256) k_ccl_local(Src src, int conn, int32_t* _
     const int lx = threadIdx.x & 31;
     const int w = src.w, h = src.h;
     bool fgv[4];
+    // one warp per tile row: horizontal runs are linked at once from the row's ballot --
+    // each pixel points at the first pixel of its run (a run start has no left link), so
+    // dense foreground never builds long hook chains
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         int ly = (threadIdx.x >> 5) + 8 * k;
         int gx = tx0 + lx, gy = ty0 + ly;
-        bool f = gx < w && gy < h && src.fg((int64_t)gy * w + gx);
+        int64_t p = (int64_t)gy * w + gx;
+        bool f = gx < w && gy < h && src.fg(p);
         fgv[k] = f;
-        s[ly * kTile + lx] = f ? ly * kTile + lx : -1;
+        unsigned fm = __ballot_sync(0xffffffffu, f);
+        bool lk = f && lx > 0 && ((fm >> (lx - 1)) & 1) && src.conn(p, p - 1);
+        unsigned nl = ~__ballot_sync(0xffffffffu, lk) & (0xffffffffu >> (31 - lx));
+        int start = 31 - __clz(nl);
+        s[ly * kTile + lx] = f ? ly * kTile + start : -1;
     }
     __syncthreads();
 #pragma unroll
@@ -126,6 +155,7 @@ __global__ void __launch_bounds__(256) k_ccl_local(Src src, int conn, int32_t* _
         for (int j = 0; j < nn; ++j) {
             int dx, dy;
             nplus(conn, j, dx, dy);
+            if (dy == 0) continue;  // horizontal links are the runs above
             int nx = lx + dx, ny = ly + dy;
             if (nx < 0 || nx >= kTile || ny < 0) continue;
             int ni = ny * kTile + nx;
@@ -291,16 +321,16 @@ void launch_ccl(const CclSrc& cs, int w, int h, int conn, int32_t* lab, int32_t*
     if (n == 0) return;
     Src src = mk(cs, w, h);
     dim3 grid((w + kTile - 1) / kTile, (h + kTile - 1) / kTile);
-    k_ccl_local<<<grid, 256, 0, s>>>(src, conn, lab);
-    k_ccl_merge<<<grid, 96, 0, s>>>(src, conn, lab);
-    k_ccl_flatten<<<grid_for(n), 256, 0, s>>>(lab, n, aux_zero);
+    (note_launch(), k_ccl_local<<<grid, 256, 0, s>>>(src, conn, lab));
+    (note_launch(), k_ccl_merge<<<grid, 96, 0, s>>>(src, conn, lab));
+    (note_launch(), k_ccl_flatten<<<grid_for(n), 256, 0, s>>>(lab, n, aux_zero));
 }
 
 void launch_ccl_count(const CclSrc&, int w, int h, const int32_t* lab, int32_t* aux,
                       cudaStream_t s) {
     const int64_t n = (int64_t)w * h;
     if (n == 0) return;
-    k_ccl_count<<<grid_for(n), 256, 0, s>>>(lab, n, aux);
+    (note_launch(), k_ccl_count<<<grid_for(n), 256, 0, s>>>(lab, n, aux));
 }
 
 void launch_ccl_area_filter(const CclSrc& cs, int w, int h, const int32_t* lab,
@@ -308,14 +338,14 @@ void launch_ccl_area_filter(const CclSrc& cs, int w, int h, const int32_t* lab,
                             cudaStream_t s) {
     const int64_t n = (int64_t)w * h;
     if (n == 0) return;
-    k_ccl_area_filter<<<grid_for(n), 256, 0, s>>>(mk(cs, w, h), lab, area, amin, amax, out);
+    (note_launch(), k_ccl_area_filter<<<grid_for(n), 256, 0, s>>>(mk(cs, w, h), lab, area, amin, amax, out));
 }
 
 void launch_ccl_to_labels(const CclSrc&, int w, int h, const int32_t* lab, int32_t* out,
                           cudaStream_t s) {
     const int64_t n = (int64_t)w * h;
     if (n == 0) return;
-    k_ccl_to_labels<<<grid_for(n), 256, 0, s>>>(lab, n, out);
+    (note_launch(), k_ccl_to_labels<<<grid_for(n), 256, 0, s>>>(lab, n, out));
 }
 
 // S2 -- RBC detection: rbc = BinRecon8(RBC_HI, RBC_LO) & R_GT_B, as CCL-select: the
@@ -326,8 +356,8 @@ void launch_rbc(const uint8_t* flags, int w, int h, int32_t* lab, int32_t* aux, 
     if (n == 0) return;
     CclSrc cs{flags, (uint8_t)HP_FLAG_RBC_LO, false, nullptr};
     launch_ccl(cs, w, h, 8, lab, aux, s);
-    k_rbc_hit<<<grid_for(n), 256, 0, s>>>(flags, lab, n, aux);
-    k_rbc_out<<<grid_for(n), 256, 0, s>>>(flags, lab, n, aux, rbc);
+    (note_launch(), k_rbc_hit<<<grid_for(n), 256, 0, s>>>(flags, lab, n, aux));
+    (note_launch(), k_rbc_out<<<grid_for(n), 256, 0, s>>>(flags, lab, n, aux, rbc));
 }
 
 // S6 -- FillHolles: 4-connected background components that contain no
@@ -338,8 +368,8 @@ void launch_fill_holes(const uint8_t* big0, int w, int h, int32_t* lab, int32_t*
     if (n == 0) return;
     CclSrc cs{big0, 0, true, nullptr};
     launch_ccl(cs, w, h, 4, lab, aux, s);
-    k_fill_border<<<grid_for(2LL * (w + h)), 256, 0, s>>>(lab, w, h, aux);
-    k_fill_out<<<grid_for(n), 256, 0, s>>>(big0, lab, n, aux, F);
+    (note_launch(), k_fill_border<<<grid_for(2LL * (w + h)), 256, 0, s>>>(lab, w, h, aux));
+    (note_launch(), k_fill_out<<<grid_for(n), 256, 0, s>>>(big0, lab, n, aux, F));
 }
 
 }  // namespace hp

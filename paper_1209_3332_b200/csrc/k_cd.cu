@@ -126,10 +126,10 @@ void launch_cd(const uint8_t* rgb, int w, int h, int64_t pitch, const float* lut
     if (vec) {
         int64_t nchunks = n / 16;
         int blocks = (int)std::min<int64_t>((nchunks + 255) / 256, grid);
-        k_cd_vec16<<<blocks, 256, 0, s>>>(rgb, w, h, pitch, lut, k, g, flags, bg_count);
+        (note_launch(), k_cd_vec16<<<blocks, 256, 0, s>>>(rgb, w, h, pitch, lut, k, g, flags, bg_count));
     } else {
         int blocks = (int)std::min<int64_t>((n + 255) / 256, grid);
-        k_cd_scalar<<<blocks, 256, 0, s>>>(rgb, w, h, pitch, lut, k, g, flags, bg_count);
+        (note_launch(), k_cd_scalar<<<blocks, 256, 0, s>>>(rgb, w, h, pitch, lut, k, g, flags, bg_count));
     }
 }
 

@@ -180,15 +180,15 @@ void launch_edt(const uint8_t* F, int w, int h, Slot& sl, uint32_t* d2_out, floa
     int32_t* any_bg = sl.cnt32 + 1;
     cudaMemsetAsync(any_bg, 0, sizeof(int32_t), s);
     int64_t nthreads = (int64_t)w * nseg;
-    k_edt_seg<<<grid_for(nthreads), 256, 0, s>>>(F, w, h, nseg, sl.seg_top, sl.seg_bot, any_bg);
-    k_edt_col<<<grid_for(nthreads), 256, 0, s>>>(F, w, h, nseg, sl.seg_top, sl.seg_bot, sl.gcol);
+    (note_launch(), k_edt_seg<<<grid_for(nthreads), 256, 0, s>>>(F, w, h, nseg, sl.seg_top, sl.seg_bot, any_bg));
+    (note_launch(), k_edt_col<<<grid_for(nthreads), 256, 0, s>>>(F, w, h, nseg, sl.seg_top, sl.seg_bot, sl.gcol));
     size_t smem = sizeof(uint32_t) * (size_t)w;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_edt_row, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    k_edt_row<<<h, 256, smem, s>>>(F, w, h, sl.gcol, any_bg, sl.aux, sl.d, d2_out, dist);
+    (note_launch(), k_edt_row<<<h, 256, smem, s>>>(F, w, h, sl.gcol, any_bg, sl.aux, sl.d, d2_out, dist));
 }
 
 }  // namespace hp

@@ -129,7 +129,7 @@ __device__ __forceinline__ int refl(int i, int n) {
     return i;
 }
 
-__global__ void __launch_bounds__(kFT) k_obj_feat(const int32_t* __restrict__ labels, int64_t lpitch,
+__global__ void __launch_bounds__(kFT, 3) k_obj_feat(const int32_t* __restrict__ labels, int64_t lpitch,
                                                   const uint8_t* __restrict__ g, int w, int h,
                                                   const int32_t* __restrict__ cnt, int32_t cap,
                                                   const int32_t* __restrict__ rank_root,
@@ -359,15 +359,15 @@ void launch_features(const int32_t* labels, int64_t lpitch, const uint8_t* g, in
     int32_t* cnt = sl.cnt32 + 2;
     cudaMemsetAsync(cnt, 0, sizeof(int32_t), s);
     if (n > 0) {
-        k_obj_find<<<grid_for(n), 256, 0, s>>>(labels, lpitch, w, h, cnt, sl.obj_root, max_objects);
-        k_obj_rank<<<std::max(1, std::min(148 * 4, (max_objects + 255) / 256)), 256, 0, s>>>(
-            cnt, max_objects, sl.obj_root, sl.obj_rank, sl.aux);
-        k_bbox_init<<<std::max(1, std::min(148 * 4, (max_objects + 255) / 256)), 256, 0, s>>>(cnt, max_objects, sl.obj_bbox);
-        k_obj_bbox<<<grid_for(n), 256, 0, s>>>(labels, lpitch, w, h, cnt, max_objects, sl.aux, sl.obj_bbox);
-        k_obj_feat<<<148 * 8, kFT, 0, s>>>(labels, lpitch, g, w, h, cnt, max_objects, sl.obj_rank,
-                                           sl.obj_bbox, row_label, row_flags, feat, capacity);
+        (note_launch(), k_obj_find<<<grid_for(n), 256, 0, s>>>(labels, lpitch, w, h, cnt, sl.obj_root, max_objects));
+        (note_launch(), k_obj_rank<<<std::max(1, std::min(148 * 4, (max_objects + 255) / 256)), 256, 0, s>>>(
+            cnt, max_objects, sl.obj_root, sl.obj_rank, sl.aux));
+        (note_launch(), k_bbox_init<<<std::max(1, std::min(148 * 4, (max_objects + 255) / 256)), 256, 0, s>>>(cnt, max_objects, sl.obj_bbox));
+        (note_launch(), k_obj_bbox<<<grid_for(n), 256, 0, s>>>(labels, lpitch, w, h, cnt, max_objects, sl.aux, sl.obj_bbox));
+        (note_launch(), k_obj_feat<<<148 * 8, kFT, 0, s>>>(labels, lpitch, g, w, h, cnt, max_objects, sl.obj_rank,
+                                           sl.obj_bbox, row_label, row_flags, feat, capacity));
     }
-    k_copy_count<<<1, 1, 0, s>>>(cnt, n_rows);
+    (note_launch(), k_copy_count<<<1, 1, 0, s>>>(cnt, n_rows));
 }
 
 }  // namespace hp

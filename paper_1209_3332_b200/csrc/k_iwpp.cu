@@ -18,6 +18,7 @@
 // Every update is a valid monotone propagation, hence any schedule reaches the same unique
 // fixed point as the oracle's sequential Vincent / BFS algorithms.
 #include <cfloat>
+#include <cstdlib>
 #include <cmath>
 
 #include "hp_internal.cuh"
@@ -42,17 +43,20 @@ __device__ __forceinline__ void wl_push(const Worklist& wl, int32_t t) {
     while (atomicCAS(&wl.queue[slot], EMPTY, t) != EMPTY) __nanosleep(64);
 }
 
-__device__ __forceinline__ int32_t wl_pop(const Worklist& wl) {
+// Ticket pop: one atomicAdd per pop, no CAS races on the head.  The ticket h names queue
+// position h; if that item has not been pushed yet, the holder waits on its own slot until
+// it arrives or until nothing is pending (then no push can ever come: -1 = terminate).
+__device__ __forceinline__ int32_t wl_pop_ticket(const Worklist& wl, unsigned long long h) {
+    const int slot = (int)(h % (unsigned long long)wl.cap);
+    int ns = 32;
     while (true) {
-        unsigned long long h = vload(&wl.ctr[0]);
-        unsigned long long t = vload(&wl.ctr[1]);
-        if (h >= t) return -1;
-        if (atomicCAS(&wl.ctr[0], h, h + 1) == h) {
-            int slot = (int)(h % (unsigned long long)wl.cap);
-            int32_t v;
-            while ((v = atomicExch(&wl.queue[slot], EMPTY)) == EMPTY) __nanosleep(32);
-            return v;
+        if (*reinterpret_cast<volatile int32_t*>(&wl.queue[slot]) != EMPTY) {
+            int32_t v = atomicExch(&wl.queue[slot], EMPTY);
+            if (v != EMPTY) return v;
         }
+        if (vload(&wl.ctr[2]) == 0ull) return -1;
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
     }
 }
 
@@ -190,19 +194,40 @@ struct RuleMR {
         T* sR = sm;
         T* sM = sm + kHalo * P;
         TileGeo g{x0, y0, w, h};
-        for (int r = 0; r < kHalo; ++r)
-            for (int c = lane; c < kHalo; c += 32) {
-                T rv = neg(), mv = neg();
-                if (g.inimg(r, c)) {
-                    int64_t i = g.gidx(r, c);
-                    if (dom == nullptr || ldcg(dom + i)) {
-                        rv = (T)ldcg(R + i);
-                        mv = (T)ldcg(mask + i);
-                    }
+        // all loads of the 34x34 window issued back to back (17 rows per batch) so their
+        // L2 latencies overlap; lanes 0/1 also fetch the two right-most halo columns
+        auto load = [&](int r, int cc, T& rv, T& mv) {
+            rv = neg();
+            mv = neg();
+            if (cc < kHalo && g.inimg(r, cc)) {
+                int64_t i = g.gidx(r, cc);
+                if (dom == nullptr || ldcg(dom + i)) {
+                    rv = (T)ldcg(R + i);
+                    mv = (T)ldcg(mask + i);
                 }
-                sR[r * P + c] = rv;
-                sM[r * P + c] = mv;
             }
+        };
+#pragma unroll
+        for (int r0 = 0; r0 < kHalo; r0 += 17) {
+            T rv[17], mv[17];
+#pragma unroll
+            for (int k = 0; k < 17; ++k) load(r0 + k, lane, rv[k], mv[k]);
+#pragma unroll
+            for (int k = 0; k < 17; ++k) {
+                sR[(r0 + k) * P + lane] = rv[k];
+                sM[(r0 + k) * P + lane] = mv[k];
+            }
+        }
+        if (lane < 2) {
+            T rv[kHalo], mv[kHalo];
+#pragma unroll
+            for (int r = 0; r < kHalo; ++r) load(r, 32 + lane, rv[r], mv[r]);
+#pragma unroll
+            for (int r = 0; r < kHalo; ++r) {
+                sR[r * P + 32 + lane] = rv[r];
+                sM[r * P + 32 + lane] = mv[r];
+            }
+        }
         __syncwarp();
         const int c = lane + 1;
         bool changed_any = false;
@@ -213,11 +238,14 @@ struct RuleMR {
                 for (int k = 0; k < kTile; ++k) {
                     int y = pass == 0 ? 1 + k : kTile - k;
                     T m = sM[y * P + c], rr = sR[y * P + c];
-                    T b = rr;
-                    b = tmax(b, tmax(sR[(y - 1) * P + c - 1], tmax(sR[(y - 1) * P + c], sR[(y - 1) * P + c + 1])));
-                    b = tmax(b, tmax(sR[(y + 1) * P + c - 1], tmax(sR[(y + 1) * P + c], sR[(y + 1) * P + c + 1])));
-                    if (lane == 0) b = tmax(b, sR[y * P]);
-                    if (lane == 31) b = tmax(b, sR[y * P + kHalo - 1]);
+                    T vmax = tmax(tmax(sR[(y - 1) * P + c - 1], tmax(sR[(y - 1) * P + c], sR[(y - 1) * P + c + 1])),
+                                  tmax(sR[(y + 1) * P + c - 1], tmax(sR[(y + 1) * P + c], sR[(y + 1) * P + c + 1])));
+                    T lft = sR[y * P + c - 1], rgt = sR[y * P + c + 1];
+                    // a row whose every pixel is already >= min(mask, max of its N8) is stable
+                    if (!__any_sync(FULL, tmin(tmax(vmax, tmax(lft, rgt)), m) > rr)) continue;
+                    T b = tmax(rr, vmax);
+                    if (lane == 0) b = tmax(b, lft);
+                    if (lane == 31) b = tmax(b, rgt);
                     T lo = tmin(b, m);
                     T v = clamp_scan_lr<T>(lo, m, lane);
                     T u = clamp_scan_rl<T>(v, m, lane);
@@ -266,18 +294,23 @@ struct RuleW2 {
         int* sD = sm;
         float* sC = reinterpret_cast<float*>(sm + kHalo * P);
         TileGeo g{x0, y0, w, h};
-        for (int r = 0; r < kHalo; ++r)
-            for (int c = lane; c < kHalo; c += 32) {
-                int dv = kInfI;
-                float cv = NAN;
-                if (g.inimg(r, c)) {
-                    int64_t i = g.gidx(r, c);
-                    dv = ldcg(d + i);
-                    cv = ldcg(cpl + i);
-                }
-                sD[r * P + c] = dv;
-                sC[r * P + c] = cv;
+        auto ld = [&](int r, int cc) {
+            int dv = kInfI;
+            float cv = NAN;
+            if (g.inimg(r, cc)) {
+                int64_t i = g.gidx(r, cc);
+                dv = ldcg(d + i);
+                cv = ldcg(cpl + i);
             }
+            sD[r * P + cc] = dv;
+            sC[r * P + cc] = cv;
+        };
+#pragma unroll
+        for (int r = 0; r < kHalo; ++r) ld(r, lane);
+        if (lane < 2) {
+#pragma unroll
+            for (int r = 0; r < kHalo; ++r) ld(r, 32 + lane);
+        }
         __syncwarp();
         const int c = lane + 1;
         bool changed_any = false;
@@ -302,6 +335,9 @@ struct RuleW2 {
                         if (lane > 0 && sC[y * P + c - 1] == cp) kl = 1;
                         if (lane < 31 && sC[y * P + c + 1] == cp) kr = 1;
                     }
+                    int aall = min(a, min(kl == 1 ? sat_add(sD[y * P + c - 1], 1) : kInfI,
+                                          kr == 1 ? sat_add(sD[y * P + c + 1], 1) : kInfI));
+                    if (!__any_sync(FULL, aall < dp)) continue;  // stable row
                     int v = minplus_scan_lr(a, kl, lane);
                     int u = minplus_scan_rl(v, kr, lane);
                     __syncwarp();
@@ -338,17 +374,22 @@ struct RuleW3 {
         int* sL = sm;
         int* sP = sm + kHalo * P;
         TileGeo g{x0, y0, w, h};
-        for (int r = 0; r < kHalo; ++r)
-            for (int c = lane; c < kHalo; c += 32) {
-                int lv = kInfI, pv = 0;
-                if (g.inimg(r, c)) {
-                    int64_t i = g.gidx(r, c);
-                    lv = ldcg(L + i);
-                    pv = ldcg(pm + i);
-                }
-                sL[r * P + c] = lv;
-                sP[r * P + c] = pv;
+        auto ld = [&](int r, int cc) {
+            int lv = kInfI, pv = 0;
+            if (g.inimg(r, cc)) {
+                int64_t i = g.gidx(r, cc);
+                lv = ldcg(L + i);
+                pv = ldcg(pm + i);
             }
+            sL[r * P + cc] = lv;
+            sP[r * P + cc] = pv;
+        };
+#pragma unroll
+        for (int r = 0; r < kHalo; ++r) ld(r, lane);
+        if (lane < 2) {
+#pragma unroll
+            for (int r = 0; r < kHalo; ++r) ld(r, 32 + lane);
+        }
         __syncwarp();
         const int c = lane + 1;
         bool changed_any = false;
@@ -373,6 +414,8 @@ struct RuleW3 {
                             a = min(a, sL[(y + dy) * P + c + dx]);
                         }
                     }
+                    int aall = min(a, min(kl == 0 ? sL[y * P + c - 1] : kInfI, kr == 0 ? sL[y * P + c + 1] : kInfI));
+                    if (!__any_sync(FULL, aall < lp)) continue;  // stable row
                     int v = minplus_scan_lr(a, kl, lane);
                     int u = minplus_scan_rl(v, kr, lane);
                     __syncwarp();
@@ -402,21 +445,17 @@ struct RuleW3 {
 
 // ------------------------------------------------------------------ the persistent kernel
 template <class Rule, class T>
-__global__ void __launch_bounds__(kWarps * 32) k_wl_run(Rule rule, Worklist wl) {
+// 5 CTAs x 4 warps per SM: the 38 KB of shared memory per CTA allows 5, and the register
+// cap (<= 102 per thread) keeps registers from being the tighter limit
+__global__ void __launch_bounds__(kWarps * 32, 5) k_wl_run(Rule rule, Worklist wl) {
     extern __shared__ __align__(16) int smem_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     T* sm = reinterpret_cast<T*>(smem_raw) + warp * Rule::kWords;
     while (true) {
         int32_t t = -1;
-        if (lane == 0) t = wl_pop(wl);
+        if (lane == 0) t = wl_pop_ticket(wl, atomicAdd(&wl.ctr[0], 1ull));
         t = __shfl_sync(FULL, t, 0);
-        if (t < 0) {
-            int done = 0;
-            if (lane == 0) done = vload(&wl.ctr[2]) == 0ull;
-            if (__shfl_sync(FULL, done, 0)) break;
-            __nanosleep(200);
-            continue;
-        }
+        if (t < 0) break;
         if (lane == 0) atomicExch(&wl.state[t], ST_BUSY);
         __threadfence();
         __syncwarp();
@@ -491,12 +530,18 @@ void run_rule(const Rule& rule, const Worklist& wl, cudaStream_t s) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wl_run<Rule, T>, kWarps * 32, smem);
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        blocks = nsm * (per_sm > 0 ? per_sm : 1);
+        // Measured on B200 (tools/diag_iwpp.py): the recon is throughput-bound on tile jobs
+        // (time ~ 1 / resident warps), so the persistent grid fills every SM to occupancy.
+        // HP_WL_CTAS_PER_SM caps it (experiments with co-running slots).
+        int want = 64;
+        if (const char* e = getenv("HP_WL_CTAS_PER_SM")) want = atoi(e);
+        if (want < 1) want = 1;
+        blocks = nsm * std::min(want, per_sm > 0 ? per_sm : 1);
     }
     int ntiles = wl.ntx * wl.nty;
     int b = std::min(blocks, (ntiles + kWarps - 1) / kWarps);
     if (b < 1) b = 1;
-    k_wl_run<Rule, T><<<b, kWarps * 32, smem, s>>>(rule, wl);
+    (note_launch(), k_wl_run<Rule, T><<<b, kWarps * 32, smem, s>>>(rule, wl));
 }
 
 // ------------------------------------------------------------------ init kernels
@@ -533,25 +578,25 @@ Worklist sized(const Worklist& wl, int w, int h) {
 
 void launch_recon_init_f32(const float* marker, const float* mask, const uint8_t* dom, int64_t n, float* R,
                            cudaStream_t s) {
-    if (n) k_recon_init_f32<<<grid_for(n), 256, 0, s>>>(marker, mask, dom, n, R);
+    if (n) (note_launch(), k_recon_init_f32<<<grid_for(n), 256, 0, s>>>(marker, mask, dom, n, R));
 }
 
 void wl_init_all(const Worklist& wl0, int w, int h, cudaStream_t s) {
     Worklist wl = sized(wl0, w, h);
-    k_wl_reset<<<grid_for(wl.cap), 256, 0, s>>>(wl, 1);
+    (note_launch(), k_wl_reset<<<grid_for(wl.cap), 256, 0, s>>>(wl, 1));
 }
 
 void wl_init_from_mask(const Worklist& wl0, const uint8_t* mask, int w, int h, cudaStream_t s) {
     Worklist wl = sized(wl0, w, h);
-    k_wl_reset<<<grid_for(wl.cap), 256, 0, s>>>(wl, 0);
+    (note_launch(), k_wl_reset<<<grid_for(wl.cap), 256, 0, s>>>(wl, 0));
     int n = wl.ntx * wl.nty;
-    k_wl_seed_mask<<<(int)std::min<int64_t>((n + 7) / 8, 148 * 16), 256, 0, s>>>(wl, mask, w, h);
+    (note_launch(), k_wl_seed_mask<<<(int)std::min<int64_t>((n + 7) / 8, 148 * 16), 256, 0, s>>>(wl, mask, w, h));
 }
 
 void launch_recon_init_u8(const uint8_t* marker, const uint8_t* mask, uint8_t* R, int w, int h,
                           cudaStream_t s) {
     int64_t n = (int64_t)w * h;
-    if (n) k_copy_min_u8<<<grid_for(n), 256, 0, s>>>(marker, mask, n, R);
+    if (n) (note_launch(), k_copy_min_u8<<<grid_for(n), 256, 0, s>>>(marker, mask, n, R));
 }
 
 void launch_recon_u8(const uint8_t* mask, uint8_t* R, int w, int h, const Worklist& wl,
@@ -592,7 +637,7 @@ void launch_parent_min(const uint8_t* pm, int32_t* L, int w, int h, const Workli
 void launch_tophat(const uint8_t* g, const uint8_t* R, const uint8_t* rbc, int g1, int w, int h,
                    uint8_t* cand, cudaStream_t s) {
     int64_t n = (int64_t)w * h;
-    if (n) k_tophat<<<grid_for(n), 256, 0, s>>>(g, R, rbc, g1, n, cand);
+    if (n) (note_launch(), k_tophat<<<grid_for(n), 256, 0, s>>>(g, R, rbc, g1, n, cand));
 }
 
 }  // namespace hp

@@ -144,8 +144,8 @@ void launch_open(const uint8_t* g, int w, int h, int diam, uint8_t* tmp, uint8_t
         attr_set = true;
     }
     dim3 grid((w + TW - 1) / TW, (h + md.th - 1) / md.th);
-    k_morph<true><<<grid, 256, smem, s>>>(g, w, h, md, tmp);
-    k_morph<false><<<grid, 256, smem, s>>>(tmp, w, h, md, out);
+    (note_launch(), k_morph<true><<<grid, 256, smem, s>>>(g, w, h, md, tmp));
+    (note_launch(), k_morph<false><<<grid, 256, smem, s>>>(tmp, w, h, md, out));
 }
 
 }  // namespace hp

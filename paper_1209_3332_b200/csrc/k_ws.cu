@@ -191,12 +191,12 @@ void launch_markers(const float* dist, const uint8_t* F, float hh, int w, int h,
                     int32_t* ML, float* J, cudaStream_t s) {
     const int64_t n = (int64_t)w * h;
     if (n == 0) return;
-    k_j_init<<<grid_for(n), 256, 0, s>>>(dist, F, hh, n, J);
+    (note_launch(), k_j_init<<<grid_for(n), 256, 0, s>>>(dist, F, hh, n, J));
     launch_recon_f32(dist, F, J, w, h, sl.wl, true, s);
     CclSrc zones{F, 0, false, J};
     launch_ccl(zones, w, h, 8, sl.lab, sl.aux, s);
-    k_notmax<<<grid_for(n), 256, 0, s>>>(J, F, sl.lab, w, h, sl.aux);
-    k_ml<<<grid_for(n), 256, 0, s>>>(F, sl.lab, sl.aux, n, ML);
+    (note_launch(), k_notmax<<<grid_for(n), 256, 0, s>>>(J, F, sl.lab, w, h, sl.aux));
+    (note_launch(), k_ml<<<grid_for(n), 256, 0, s>>>(F, sl.lab, sl.aux, n, ML));
 }
 
 void launch_watershed(const float* dist, const int32_t* ML, const uint8_t* F, int w, int h,
@@ -204,16 +204,16 @@ void launch_watershed(const float* dist, const int32_t* ML, const uint8_t* F, in
                       cudaStream_t s) {
     const int64_t n = (int64_t)w * h;
     if (n == 0) return;
-    k_c_init<<<grid_for(n), 256, 0, s>>>(dist, ML, F, n, sl.c);
+    (note_launch(), k_c_init<<<grid_for(n), 256, 0, s>>>(dist, ML, F, n, sl.c));
     launch_recon_f32(dist, F, sl.c, w, h, sl.wl, true, s);                // W1
-    k_d_init<<<grid_for(n), 256, 0, s>>>(sl.c, ML, F, w, h, sl.d);
+    (note_launch(), k_d_init<<<grid_for(n), 256, 0, s>>>(sl.c, ML, F, w, h, sl.d));
     launch_plateau_dist(sl.c, sl.d, w, h, sl.wl, F, s);                    // W2
-    k_parents<<<grid_for(n), 256, 0, s>>>(sl.c, sl.d, ML, F, w, h, sl.pmask, sl.L);
+    (note_launch(), k_parents<<<grid_for(n), 256, 0, s>>>(sl.c, sl.d, ML, F, w, h, sl.pmask, sl.L));
     launch_parent_min(sl.pmask, sl.L, w, h, sl.wl, F, s);                  // W3
-    k_lines<<<grid_for(n), 256, 0, s>>>(sl.L, F, w, h, split);
-    if (c_out) k_zero_outside<float><<<grid_for(n), 256, 0, s>>>(sl.c, F, n, c_out);
-    if (d_out) k_zero_outside<int32_t><<<grid_for(n), 256, 0, s>>>(sl.d, F, n, d_out);
-    if (L_out) k_zero_outside<int32_t><<<grid_for(n), 256, 0, s>>>(sl.L, F, n, L_out);
+    (note_launch(), k_lines<<<grid_for(n), 256, 0, s>>>(sl.L, F, w, h, split));
+    if (c_out) (note_launch(), k_zero_outside<float><<<grid_for(n), 256, 0, s>>>(sl.c, F, n, c_out));
+    if (d_out) (note_launch(), k_zero_outside<int32_t><<<grid_for(n), 256, 0, s>>>(sl.d, F, n, d_out));
+    if (L_out) (note_launch(), k_zero_outside<int32_t><<<grid_for(n), 256, 0, s>>>(sl.L, F, n, L_out));
 }
 
 void launch_bwlabel(const uint8_t* split, int w, int h, int amin, int amax, Slot& sl,
@@ -224,12 +224,12 @@ void launch_bwlabel(const uint8_t* split, int w, int h, int amin, int amax, Slot
     CclSrc cs{split, 0, false, nullptr};
     launch_ccl(cs, w, h, 8, sl.lab, sl.aux, s);
     launch_ccl_count(cs, w, h, sl.lab, sl.aux, s);
-    k_bw_label<<<grid_for(n), 256, 0, s>>>(sl.lab, sl.aux, w, h, amin, amax, labels, lpitch, n_objects);
+    (note_launch(), k_bw_label<<<grid_for(n), 256, 0, s>>>(sl.lab, sl.aux, w, h, amin, amax, labels, lpitch, n_objects));
 }
 
 // exposed for the verification ABI (J outside F -> 0)
 void launch_zero_outside_f32(const float* src, const uint8_t* F, int64_t n, float* dst, cudaStream_t s) {
-    if (n) k_zero_outside<float><<<grid_for(n), 256, 0, s>>>(src, F, n, dst);
+    if (n) (note_launch(), k_zero_outside<float><<<grid_for(n), 256, 0, s>>>(src, F, n, dst));
 }
 
 }  // namespace hp

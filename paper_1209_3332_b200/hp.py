@@ -36,7 +36,7 @@ STATUS = {0: "ok", 1: "invalid argument", 2: "CUDA error", 3: "out of memory",
 EXPORTS = ["hp_default_params", "hp_ctx_create", "hp_ctx_destroy", "hp_status_str",
            "hp_last_error", "hp_version", "hp_segment_tile", "hp_features_tile",
            "hp_process_tile", "hp_run_tiles", "hp_stage_run", "hp_set_stage_timing",
-           "hp_get_stage_times"]
+           "hp_get_stage_times", "hp_stage_times_accum", "hp_launch_count"]
 
 
 class HPError(RuntimeError):
@@ -138,6 +138,8 @@ def lib():
             "hp_stage_run": (C.c_int, [P, i32, C.c_int, C.POINTER(StageIO), P]),
             "hp_set_stage_timing": (C.c_int, [P, i32]),
             "hp_get_stage_times": (C.c_int, [P, i32, C.POINTER(C.c_float)]),
+            "hp_stage_times_accum": (C.c_int, [P, C.POINTER(C.c_float), C.POINTER(C.c_int32)]),
+            "hp_launch_count": (C.c_int64, []),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -145,6 +147,11 @@ def lib():
             fn.argtypes = args
         _lib = L
     return _lib
+
+
+def launch_count() -> int:
+    """libhp kernel launches issued by this process so far."""
+    return int(lib().hp_launch_count())
 
 
 def default_params() -> Params:
@@ -250,6 +257,13 @@ class Context:
         ms = (C.c_float * 11)()
         self._chk(lib().hp_get_stage_times(self._h, slot, ms), "hp_get_stage_times")
         return list(ms)
+
+    def stage_times_accum(self):
+        """(sum of S1..S11 ms over the recorded tiles, number of tiles)."""
+        ms = (C.c_float * 11)()
+        n = C.c_int32()
+        self._chk(lib().hp_stage_times_accum(self._h, ms, C.byref(n)), "hp_stage_times_accum")
+        return list(ms), int(n.value)
 
     def run_tiles(self, next_tile, on_done, width, height):
         """Demand-driven driver.  next_tile() -> (host_ptr:int, pitch:int, tile_id:int) or

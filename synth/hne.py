@@ -45,21 +45,12 @@ def make_pool_seed(slide: int, idx: int) -> int:
 
 def _smooth_field(rng, h, w, scale):
     """Uniform noise at 1/scale resolution, bilinearly upsampled and normalised to [0,1]."""
+    import cv2
     lh, lw = max(2, h // scale + 2), max(2, w // scale + 2)
-    low = rng.random((lh, lw))
-    ys = np.linspace(0.0, lh - 1.001, h)
-    xs = np.linspace(0.0, lw - 1.001, w)
-    y0 = ys.astype(np.int64)
-    x0 = xs.astype(np.int64)
-    fy = (ys - y0)[:, None]
-    fx = (xs - x0)[None, :]
-    a = low[y0][:, x0]
-    b = low[y0][:, x0 + 1]
-    c = low[y0 + 1][:, x0]
-    d = low[y0 + 1][:, x0 + 1]
-    f = (a * (1 - fx) + b * fx) * (1 - fy) + (c * (1 - fx) + d * fx) * fy
-    lo, hi = f.min(), f.max()
-    return (f - lo) / max(hi - lo, 1e-12)
+    low = rng.random((lh, lw), dtype=np.float32)
+    f = cv2.resize(low, (w, h), interpolation=cv2.INTER_LINEAR)
+    lo, hi = float(f.min()), float(f.max())
+    return (f - lo) * np.float32(1.0 / max(hi - lo, 1e-12))
 
 
 def _paint_ellipse(ch, cx, cy, a, b, theta, value, noise_rng, noise_sigma, mode="max"):
@@ -103,8 +94,8 @@ def make_tile(seed: int, spec: TileSpec = TileSpec()) -> dict:
     # 2. stroma
     s1 = _smooth_field(rng, h, w, 8)
     s2 = _smooth_field(rng, h, w, 8)
-    c_e = np.where(tissue, 0.25 + 0.25 * s1, 0.0)
-    c_h = np.where(tissue, 0.04 + 0.04 * s2, 0.0)
+    c_e = np.where(tissue, np.float32(0.25) + np.float32(0.25) * s1, np.float32(0.0))
+    c_h = np.where(tissue, np.float32(0.04) + np.float32(0.04) * s2, np.float32(0.0))
 
     # 3. nuclei
     n_tissue = int(tissue.sum())
@@ -137,10 +128,10 @@ def make_tile(seed: int, spec: TileSpec = TileSpec()) -> dict:
                 nuclei.append((ex, ey, ea, eb, et))
 
     # 5. compose (Beer-Lambert) + sensor noise
-    od = c_h[..., None] * _PAINT_H + c_e[..., None] * _PAINT_E
-    img = 255.0 * np.power(10.0, -od)
+    od = c_h[..., None] * _PAINT_H.astype(np.float32) + c_e[..., None] * _PAINT_E.astype(np.float32)
+    img = np.float32(255.0) * np.exp(od * np.float32(-np.log(10.0)))
     del od
-    img += rng.normal(0.0, spec.noise_sigma, size=img.shape)
+    img += np.float32(spec.noise_sigma) * rng.standard_normal(size=img.shape, dtype=np.float32)
 
     # 4. red blood cells (painted over, saturated red)
     n_rbc = int(rng.poisson(spec.rbc_rel_density * spec.density * n_tissue)) if n_tissue else 0
