@@ -31,7 +31,9 @@ def timed(fn, reps=3):
 def main():
     size = 4096
     ctx = Context(0, size, size, n_slots=1, max_objects=8192)
-    rgb = torch.from_numpy(make_config_tile(2)).cuda()
+    pool = [a for a in sys.argv if a.startswith("--pool=")]
+    src = make_config_tile(3, int(pool[0].split("=")[1])) if pool else make_config_tile(2)
+    rgb = torch.from_numpy(src).cuda()
     g = torch.empty((size, size), dtype=torch.uint8, device="cuda")
     fl = torch.empty_like(g)
     nbg = torch.zeros(1, dtype=torch.int64, device="cuda")
