@@ -148,7 +148,7 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
     launch_open(sl.g, w, h, p.open_diam, sl.u8b, sl.u8a, s);                                          // S3
     ev(ctx, sl, 3, s);
     launch_recon_init_u8(sl.u8a, sl.g, sl.u8b, w, h, s);                                              // S4
-    launch_recon_u8(sl.g, sl.u8b, w, h, sl.wl, s);
+    launch_recon_u8_auto(sl.g, sl.u8b, w, h, sl.wl, s);
     launch_tophat(sl.g, sl.u8b, sl.rbc, p.g1, w, h, sl.cand, s);
     ev(ctx, sl, 4, s);
     CclSrc cs{sl.cand, 0, false, nullptr};                                                            // S5
@@ -297,6 +297,9 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.seg_top = (int16_t*)A(2 * (size_t)nseg * cfg->max_width);
         s.seg_bot = (int16_t*)A(2 * (size_t)nseg * cfg->max_width);
         s.wl.state = (uint32_t*)A(4 * (size_t)ntiles);
+        // per tile (tile engine) or per region sub-tile (region engine, 128 px regions)
+        const size_t nsub = (size_t)((cfg->max_width + 127) / 128) * ((cfg->max_height + 127) / 128) * 16;
+        s.wl.inrows = (uint32_t*)A(4 * std::max((size_t)ntiles, nsub));
         s.wl.queue = (int32_t*)A(4 * (size_t)cap);
         s.wl.ctr = (unsigned long long*)A(8 * 8);
         s.wl.cap = cap;
@@ -316,7 +319,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.h_feat = (float*)halloc(4 * (size_t)mo * HP_NFEAT);
         s.h_nrows = (int32_t*)halloc(16);
         void* all[] = {s.g, s.flags, s.rbc, s.u8a, s.u8b, s.cand, s.big0, s.F, s.split, s.pmask, s.lab, s.aux,
-                       s.ML, s.d, s.L, s.dist, s.J, s.c, s.gcol, s.seg_top, s.seg_bot, s.wl.state, s.wl.queue,
+                       s.ML, s.d, s.L, s.dist, s.J, s.c, s.gcol, s.seg_top, s.seg_bot, s.wl.state, s.wl.inrows, s.wl.queue,
                        s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
                        s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows};
         for (void* p : all)
@@ -480,7 +483,7 @@ hp_status hp_stage_run(hp_ctx* ctx, int32_t slot, hp_stage stage, const hp_stage
         case HP_STAGE_RECON: {
             if (!need({io->in[0], io->in[1], io->in[2], io->out[0]})) break;
             launch_recon_init_u8(in8(1), in8(0), sl.u8b, w, h, s);
-            launch_recon_u8(in8(0), sl.u8b, w, h, sl.wl, s);
+            launch_recon_u8_auto(in8(0), sl.u8b, w, h, sl.wl, s);
             launch_tophat(in8(0), sl.u8b, in8(2), p.g1, w, h, (uint8_t*)io->out[0], s);
             if (io->out[1]) cudaMemcpyAsync(io->out[1], sl.u8b, n, cudaMemcpyDeviceToDevice, s);
             return check_launch(ctx, "stage recon");
@@ -527,7 +530,7 @@ hp_status hp_stage_run(hp_ctx* ctx, int32_t slot, hp_stage stage, const hp_stage
         case HP_STAGE_IWPP_RAW: {
             if (!need({io->in[0], io->in[1], io->out[0]})) break;
             launch_recon_init_u8(in8(0), in8(1), (uint8_t*)io->out[0], w, h, s);
-            launch_recon_u8(in8(1), (uint8_t*)io->out[0], w, h, sl.wl, s);
+            launch_recon_u8_auto(in8(1), (uint8_t*)io->out[0], w, h, sl.wl, s);
             if (io->out[1]) cudaMemcpyAsync(io->out[1], sl.wl.ctr + 3, 2 * sizeof(unsigned long long),
                                             cudaMemcpyDeviceToDevice, s);
             return check_launch(ctx, "stage iwpp");

@@ -49,6 +49,7 @@ __host__ __device__ __forceinline__ int nb_index(int dx, int dy) {
 // ctr[3] tiles processed, ctr[4] local rounds.
 struct Worklist {
     uint32_t* state;
+    uint32_t* inrows;   // per tile: rows (bit y-1) whose halo neighbours improved since last job
     int32_t* queue;
     unsigned long long* ctr;
     int32_t cap;      // ring capacity (>= ntiles + max warps)
@@ -125,6 +126,12 @@ void wl_init_all(const Worklist& wl, int w, int h, cudaStream_t s);
 void wl_init_from_mask(const Worklist& wl, const uint8_t* mask, int w, int h, cudaStream_t s);
 void launch_recon_u8(const uint8_t* mask, uint8_t* R, int w, int h, const Worklist& wl,
                      cudaStream_t s);
+// region-granular variant (k_region.cu); the default for S4 unless HP_IWPP_TILES=1
+void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, const Worklist& wl,
+                             cudaStream_t s);
+// dispatch between the two (same result; env HP_IWPP_TILES=1 selects the tile engine)
+void launch_recon_u8_auto(const uint8_t* mask, uint8_t* R, int w, int h, const Worklist& wl,
+                          cudaStream_t s);
 void launch_recon_f32(const float* mask, const uint8_t* dom, float* R, int w, int h,
                       const Worklist& wl, bool init_from_mask_tiles, cudaStream_t s);
 void launch_plateau_dist(const float* c, int32_t* d, int w, int h, const Worklist& wl,

@@ -200,16 +200,31 @@ __global__ void __launch_bounds__(kWarps * 32, 5) k_wl_run(Rule rule, Worklist w
         t = __shfl_sync(FULL, t, 0);
         if (t < 0) break;
         if (lane == 0) atomicExch(&wl.state[t], ST_BUSY);
-        __threadfence();
-        __syncwarp();
         const int tx = t % wl.ntx, ty = t / wl.ntx;
         while (true) {
-            uint32_t bits = rule.process(tx * kTile, ty * kTile, sm, lane, &wl.ctr[4]);
+            // rows whose halo improved since this tile's last job (all rows on the first)
+            uint32_t rows = 0;
+            if (lane == 0) rows = atomicExch(&wl.inrows[t], 0u);
+            rows = __shfl_sync(FULL, rows, 0);
             __threadfence();
             __syncwarp();
-            if (lane < 8 && ((bits >> lane) & 1)) {
-                int nx = tx + dx8(lane), ny = ty + dy8(lane);
-                if (nx >= 0 && ny >= 0 && nx < wl.ntx && ny < wl.nty) wl_activate(wl, ny * wl.ntx + nx);
+            uint32_t nbm[8];
+            bool changed = false;
+            if (rows) changed = rule.process(tx * kTile, ty * kTile, sm, lane, rows, &wl.ctr[4], nbm);
+            if (changed) {
+                __threadfence();  // tile data visible before the neighbours are told
+                uint32_t mine = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (lane == j) mine = nbm[j];
+                if (lane < 8 && mine) {
+                    int nx = tx + dx8(lane), ny = ty + dy8(lane);
+                    if (nx >= 0 && ny >= 0 && nx < wl.ntx && ny < wl.nty) {
+                        int nt = ny * wl.ntx + nx;
+                        atomicOr(&wl.inrows[nt], mine);
+                        wl_activate(wl, nt);
+                    }
+                }
             }
             __syncwarp();
             int again = 0;
@@ -233,7 +248,10 @@ __global__ void __launch_bounds__(kWarps * 32, 5) k_wl_run(Rule rule, Worklist w
 __global__ void k_wl_reset(Worklist wl, int seed_all) {
     const int n = wl.ntx * wl.nty;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < wl.cap; i += gridDim.x * blockDim.x) {
-        if (i < n) wl.state[i] = seed_all ? ST_QUEUED : ST_IDLE;
+        if (i < n) {
+            wl.state[i] = seed_all ? ST_QUEUED : ST_IDLE;
+            wl.inrows[i] = seed_all ? 0xffffffffu : 0u;
+        }
         wl.queue[i] = (seed_all && i < n) ? i : EMPTY;
     }
     if (blockIdx.x == 0 && threadIdx.x < 8)
@@ -256,6 +274,7 @@ __global__ void k_wl_seed_mask(Worklist wl, const uint8_t* __restrict__ mask, in
             }
         if (__any_sync(FULL, any) && lane == 0) {
             wl.state[t] = ST_QUEUED;
+            wl.inrows[t] = 0xffffffffu;
             unsigned long long pos = atomicAdd(&wl.ctr[1], 1ull);
             atomicAdd(&wl.ctr[2], 1ull);
             wl.queue[pos] = t;
@@ -346,8 +365,8 @@ void launch_recon_u8(const uint8_t* mask, uint8_t* R, int w, int h, const Workli
                      cudaStream_t s) {
     if ((int64_t)w * h == 0) return;
     wl_init_all(wl, w, h, s);
-    RuleMR<int, uint8_t> rule{mask, R, nullptr, w, h};
-    run_rule<RuleMR<int, uint8_t>, int>(rule, sized(wl, w, h), s);
+    RuleMR8 rule{mask, R, w, h};
+    run_rule<RuleMR8, int>(rule, sized(wl, w, h), s);
 }
 
 void launch_recon_f32(const float* mask, const uint8_t* dom, float* R, int w, int h,
@@ -357,8 +376,8 @@ void launch_recon_f32(const float* mask, const uint8_t* dom, float* R, int w, in
         wl_init_from_mask(wl, dom, w, h, s);
     else
         wl_init_all(wl, w, h, s);
-    RuleMR<float, float> rule{mask, R, dom, w, h};
-    run_rule<RuleMR<float, float>, float>(rule, sized(wl, w, h), s);
+    RuleMRf rule{mask, R, dom, w, h};
+    run_rule<RuleMRf, int>(rule, sized(wl, w, h), s);
 }
 
 void launch_plateau_dist(const float* c, int32_t* d, int w, int h, const Worklist& wl,

@@ -1,0 +1,365 @@
+// k_region.cu -- IWPP morphological reconstruction on u8 planes at REGION granularity
+// (S4 ReconToNuclei; HP_STAGE_IWPP_RAW).
+//
+// Measured (tools/diag_iwpp.py, r1): with one warp per 32x32 tile job, the reconstruction of
+// some tiles is dominated by long sequential chains of tile jobs (same job count, 2.5 ms vs
+// 19 ms), i.e. by the cost of one hop through the global queue.  Here one CTA of RX*RY warps
+// owns a region of RX x RY tiles (128 x 128 px): the region window (plus halo) lives in
+// shared memory as bytes; each warp closes its own 32x32 sub-tile with the row-scan sweeps
+// of iwpp_rules.cuh (reading its neighbours' pixels live), then the CTA barriers, each warp
+// derives the rows its neighbour sub-tiles can still improve, and the CTA iterates until the
+// region is stable.  A chain hop inside a region costs a barrier instead of a queue round
+// trip, and regions are 16x fewer than tiles.  Between regions: the asynchronous worklist of
+// k_iwpp.cu (ticket queue, IDLE/QUEUED/BUSY/BUSY_DIRTY states, per-sub-tile incoming rows).
+// Every update is a valid monotone propagation: the fixed point equals the oracle's.
+#include <cstdlib>
+
+#include "hp_internal.cuh"
+
+namespace hp {
+namespace {
+
+constexpr uint32_t ST_IDLE = 0, ST_QUEUED = 1, ST_BUSY = 2, ST_DIRTY = 3;
+constexpr int32_t EMPTY = -1;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int RX = 4, RY = 4, NW = RX * RY;
+constexpr int RWW = RX * 8 + 2;      // window words per row: bytes [X0-4, X0+128+4)
+constexpr int RWB = RWW * 4;         // window bytes per row
+constexpr int ROWS = RY * kTile + 2; // window rows
+
+__device__ __forceinline__ unsigned long long vload(const unsigned long long* p) {
+    return *reinterpret_cast<const volatile unsigned long long*>(p);
+}
+
+__device__ __forceinline__ void q_push(const Worklist& wl, int32_t t) {
+    unsigned long long pos = atomicAdd(&wl.ctr[1], 1ull);
+    int slot = (int)(pos % (unsigned long long)wl.cap);
+    while (atomicCAS(&wl.queue[slot], EMPTY, t) != EMPTY) __nanosleep(64);
+}
+
+__device__ __forceinline__ int32_t q_pop(const Worklist& wl) {
+    const unsigned long long h = atomicAdd(&wl.ctr[0], 1ull);
+    const int slot = (int)(h % (unsigned long long)wl.cap);
+    int ns = 32;
+    while (true) {
+        if (*reinterpret_cast<volatile int32_t*>(&wl.queue[slot]) != EMPTY) {
+            int32_t v = atomicExch(&wl.queue[slot], EMPTY);
+            if (v != EMPTY) return v;
+        }
+        if (vload(&wl.ctr[2]) == 0ull) return -1;
+        __nanosleep(ns);
+        if (ns < 1024) ns <<= 1;
+    }
+}
+
+__device__ __forceinline__ void q_activate(const Worklist& wl, int32_t t) {
+    uint32_t s = *reinterpret_cast<volatile uint32_t*>(&wl.state[t]);
+    while (true) {
+        if (s == ST_IDLE) {
+            uint32_t o = atomicCAS(&wl.state[t], ST_IDLE, ST_QUEUED);
+            if (o == ST_IDLE) {
+                atomicAdd(&wl.ctr[2], 1ull);
+                q_push(wl, t);
+                return;
+            }
+            s = o;
+        } else if (s == ST_BUSY) {
+            uint32_t o = atomicCAS(&wl.state[t], ST_BUSY, ST_DIRTY);
+            if (o == ST_BUSY) return;
+            s = o;
+        } else {
+            return;
+        }
+    }
+}
+
+template <bool LR>
+__device__ __forceinline__ int clamp_scan(int lo, int hi, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        int lo_o = LR ? __shfl_up_sync(FULL, lo, off) : __shfl_down_sync(FULL, lo, off);
+        int hi_o = LR ? __shfl_up_sync(FULL, hi, off) : __shfl_down_sync(FULL, hi, off);
+        bool take = LR ? lane >= off : lane + off < 32;
+        int nlo = min(hi, max(lo, lo_o)), nhi = min(hi, max(lo, hi_o));
+        lo = take ? nlo : lo;
+        hi = take ? nhi : hi;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint32_t load_word(const uint8_t* plane, int w, int h, int gx, int gy) {
+    if (gy < 0 || gy >= h) return 0u;
+    const uint8_t* rowp = plane + (int64_t)gy * w;
+    if (gx >= 0 && gx + 3 < w && (((uintptr_t)(rowp + gx)) & 3) == 0)
+        return __ldcg(reinterpret_cast<const unsigned int*>(rowp + gx));
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        int x = gx + b;
+        if (x >= 0 && x < w) v |= (uint32_t)__ldcg(reinterpret_cast<const unsigned char*>(rowp + x)) << (8 * b);
+    }
+    return v;
+}
+
+struct Smem {
+    uint32_t R[ROWS * RWW];
+    uint32_t M[ROWS * RWW];
+    uint32_t dirty[NW];
+    uint32_t chg[NW];
+    int job;
+    int again;
+};
+
+// byte of window pixel (wr, wc): window column wc (0 .. RX*32+1) is byte wc + 3
+__device__ __forceinline__ int bidx(int wr, int wc) { return wr * RWB + wc + 3; }
+
+__global__ void __launch_bounds__(NW * 32, 1) k_region_mr8(const uint8_t* __restrict__ mask,
+                                                           uint8_t* __restrict__ R, int w, int h,
+                                                           Worklist wl) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& S = *reinterpret_cast<Smem*>(smem_raw);
+    const uint8_t* sR = reinterpret_cast<const uint8_t*>(S.R);
+    uint8_t* sRw = reinterpret_cast<uint8_t*>(S.R);
+    const uint8_t* sM = reinterpret_cast<const uint8_t*>(S.M);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sx = warp % RX, sy = warp / RX;
+    const int wr0 = sy * kTile, wc0 = sx * kTile;  // window origin of this sub-tile (minus halo)
+
+    // close row y (1..32) of this warp's sub-tile; true iff it changed
+    auto row = [&](int y) -> bool {
+        const int wr = wr0 + y, wc = wc0 + lane + 1;
+        int m = sM[bidx(wr, wc)], rr = sR[bidx(wr, wc)];
+        int up = max(max(sR[bidx(wr - 1, wc - 1)], sR[bidx(wr - 1, wc)]), sR[bidx(wr - 1, wc + 1)]);
+        int dn = max(max(sR[bidx(wr + 1, wc - 1)], sR[bidx(wr + 1, wc)]), sR[bidx(wr + 1, wc + 1)]);
+        int vmax = max(up, dn);
+        int lft = sR[bidx(wr, wc - 1)], rgt = sR[bidx(wr, wc + 1)];
+        if (!__any_sync(FULL, min(max(vmax, max(lft, rgt)), m) > rr)) return false;
+        int b = max(rr, vmax);
+        if (lane == 0) b = max(b, lft);
+        if (lane == 31) b = max(b, rgt);
+        int lo = min(b, m);
+        int u = max(clamp_scan<true>(lo, m, lane), clamp_scan<false>(lo, m, lane));
+        __syncwarp();
+        if (u != rr) sRw[bidx(wr, wc)] = (uint8_t)u;
+        __syncwarp();
+        return true;
+    };
+    // can window pixel p (pr, pc) improve window pixel q (qr, qc)?
+    auto improves = [&](int pr, int pc, int qr, int qc) {
+        return min((int)sR[bidx(pr, pc)], (int)sM[bidx(qr, qc)]) > (int)sR[bidx(qr, qc)];
+    };
+
+    while (true) {
+        if (threadIdx.x == 0) {
+            int t = q_pop(wl);
+            if (t >= 0) atomicExch(&wl.state[t], ST_BUSY);
+            S.job = t;
+        }
+        __syncthreads();
+        const int t = S.job;
+        if (t < 0) break;
+        const int rx = t % wl.ntx, ry = t / wl.ntx;
+        const int X0 = rx * RX * kTile, Y0 = ry * RY * kTile;
+        while (true) {
+            if (lane == 0) S.dirty[warp] = atomicExch(&wl.inrows[t * NW + warp], 0u);
+            __threadfence();
+            __syncthreads();
+            int any_in = 0;
+#pragma unroll
+            for (int k = 0; k < NW; ++k) any_in |= S.dirty[k] != 0;
+            uint32_t mychg = 0;
+            if (any_in) {
+                for (int k = threadIdx.x; k < ROWS * RWW; k += blockDim.x) {
+                    int r = k / RWW, wi = k - r * RWW;
+                    int gx = X0 - 4 + 4 * wi, gy = Y0 - 1 + r;
+                    S.R[k] = load_word(R, w, h, gx, gy);
+                    S.M[k] = load_word(mask, w, h, gx, gy);
+                }
+                __syncthreads();
+                uint32_t dirty = S.dirty[warp];
+                int iters = 0;
+                while (true) {
+                    // Gauss-Seidel sweeps of this sub-tile (see iwpp_rules.cuh sweep_rows)
+                    uint32_t chg = 0;
+                    while (dirty) {
+                        for (int y = 1; y <= kTile; ++y) {
+                            const uint32_t bit = 1u << (y - 1);
+                            if (!(dirty & bit)) continue;
+                            dirty &= ~bit;
+                            if (row(y)) { chg |= bit; dirty |= (bit << 1) | (bit >> 1); }
+                        }
+                        if (!dirty) break;
+                        for (int y = kTile; y >= 1; --y) {
+                            const uint32_t bit = 1u << (y - 1);
+                            if (!(dirty & bit)) continue;
+                            dirty &= ~bit;
+                            if (row(y)) { chg |= bit; dirty |= (bit << 1) | (bit >> 1); }
+                        }
+                    }
+                    mychg |= chg;
+                    if (lane == 0) S.chg[warp] = chg;
+                    ++iters;
+                    __syncthreads();
+                    // rows of this sub-tile that a changed in-region neighbour can improve
+                    uint32_t nd = 0;
+                    const int c = wc0 + lane + 1, r = wr0 + lane + 1;
+                    if (sy > 0 && (S.chg[warp - RX] | S.chg[warp - RX - (sx > 0)] | S.chg[warp - RX + (sx < RX - 1)])) {
+                        bool f = improves(wr0, c - 1, wr0 + 1, c) || improves(wr0, c, wr0 + 1, c) ||
+                                 improves(wr0, c + 1, wr0 + 1, c);
+                        if (__any_sync(FULL, f)) nd |= 1u;
+                    }
+                    if (sy < RY - 1 && (S.chg[warp + RX] | S.chg[warp + RX - (sx > 0)] | S.chg[warp + RX + (sx < RX - 1)])) {
+                        const int br = wr0 + kTile;
+                        bool f = improves(br + 1, c - 1, br, c) || improves(br + 1, c, br, c) ||
+                                 improves(br + 1, c + 1, br, c);
+                        if (__any_sync(FULL, f)) nd |= 1u << 31;
+                    }
+                    if (sx > 0 && (S.chg[warp - 1] | (sy > 0 ? S.chg[warp - 1 - RX] : 0u) | (sy < RY - 1 ? S.chg[warp - 1 + RX] : 0u))) {
+                        bool f = improves(r - 1, wc0, r, wc0 + 1) || improves(r, wc0, r, wc0 + 1) ||
+                                 improves(r + 1, wc0, r, wc0 + 1);
+                        nd |= __ballot_sync(FULL, f);
+                    }
+                    if (sx < RX - 1 && (S.chg[warp + 1] | (sy > 0 ? S.chg[warp + 1 - RX] : 0u) | (sy < RY - 1 ? S.chg[warp + 1 + RX] : 0u))) {
+                        const int bc = wc0 + kTile;
+                        bool f = improves(r - 1, bc + 1, r, bc) || improves(r, bc + 1, r, bc) ||
+                                 improves(r + 1, bc + 1, r, bc);
+                        nd |= __ballot_sync(FULL, f);
+                    }
+                    dirty = nd;
+                    const int more = __syncthreads_or(nd != 0);
+                    if (!more) break;
+                }
+                if (threadIdx.x == 0) atomicAdd(&wl.ctr[4], (unsigned long long)iters);
+                // write back the changed rows of this sub-tile (interior words)
+                if (mychg) {
+                    for (int k = lane; k < kTile * 8; k += 32) {
+                        int y = 1 + (k >> 3), wi = k & 7;
+                        if (!((mychg >> (y - 1)) & 1)) continue;
+                        int gx = X0 + wc0 + 4 * wi, gy = Y0 + wr0 + y - 1;
+                        if (gy >= h || gx >= w) continue;
+                        uint8_t* dst = R + (int64_t)gy * w + gx;
+                        uint32_t v = S.R[(wr0 + y) * RWW + sx * 8 + 1 + wi];
+                        if (gx + 3 < w && (((uintptr_t)dst) & 3) == 0) {
+                            __stcg(reinterpret_cast<unsigned int*>(dst), v);
+                        } else {
+                            for (int b = 0; b < 4 && gx + b < w; ++b)
+                                __stcg(reinterpret_cast<unsigned char*>(dst + b), (unsigned char)(v >> (8 * b)));
+                        }
+                    }
+                    __threadfence();
+                    // activations of sub-tiles in neighbouring regions (edges of the region)
+                    uint32_t m8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    const int c = wc0 + lane + 1, r = wr0 + lane + 1;
+                    constexpr uint32_t TOP = 1u << 31, BOT = 1u;
+#pragma unroll
+                    for (int d = -1; d <= 1; ++d) {
+                        if (sy == 0 && improves(wr0 + 1, c, wr0, c + d)) {
+                            if (c + d == wc0) m8[0] |= TOP;
+                            else if (c + d == wc0 + kTile + 1) m8[2] |= TOP;
+                            else m8[1] |= TOP;
+                        }
+                        if (sy == RY - 1 && improves(wr0 + kTile, c, wr0 + kTile + 1, c + d)) {
+                            if (c + d == wc0) m8[5] |= BOT;
+                            else if (c + d == wc0 + kTile + 1) m8[7] |= BOT;
+                            else m8[6] |= BOT;
+                        }
+                        if (sx == 0 && improves(r, wc0 + 1, r + d, wc0)) {
+                            if (r + d == wr0) m8[0] |= TOP;
+                            else if (r + d == wr0 + kTile + 1) m8[5] |= BOT;
+                            else m8[3] |= 1u << (lane + d);
+                        }
+                        if (sx == RX - 1 && improves(r, wc0 + kTile, r + d, wc0 + kTile + 1)) {
+                            if (r + d == wr0) m8[2] |= TOP;
+                            else if (r + d == wr0 + kTile + 1) m8[7] |= BOT;
+                            else m8[4] |= 1u << (lane + d);
+                        }
+                    }
+                    // (diagonal reach across the region edge from an inner sub-tile's corner is
+                    // covered by the top/bottom row checks: c + d == wc0 / wc0 + 33)
+                    uint32_t mine = 0;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        uint32_t v = __reduce_or_sync(FULL, m8[j]);
+                        if (lane == j) mine = v;
+                    }
+                    if (lane < 8 && mine) {
+                        int gsx = rx * RX + sx + dx8(lane), gsy = ry * RY + sy + dy8(lane);
+                        int nrx = gsx >= 0 ? gsx / RX : -1, nry = gsy >= 0 ? gsy / RY : -1;
+                        if (gsx >= 0 && gsy >= 0 && nrx < wl.ntx && nry < wl.nty && (nrx != rx || nry != ry)) {
+                            int nt = nry * wl.ntx + nrx;
+                            int sub = (gsy % RY) * RX + (gsx % RX);
+                            atomicOr(&wl.inrows[nt * NW + sub], mine);
+                            q_activate(wl, nt);
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int again = 0;
+                uint32_t o = atomicCAS(&wl.state[t], ST_BUSY, ST_IDLE);
+                if (o == ST_BUSY) {
+                    atomicAdd(&wl.ctr[2], ~0ull);
+                } else {
+                    atomicExch(&wl.state[t], ST_BUSY);
+                    again = 1;
+                }
+                atomicAdd(&wl.ctr[3], 1ull);
+                S.again = again;
+            }
+            __syncthreads();
+            if (!S.again) break;
+        }
+    }
+}
+
+__global__ void k_rg_reset(Worklist wl) {
+    const int n = wl.ntx * wl.nty;
+    const int lim = max(wl.cap, n * NW);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < lim; i += gridDim.x * blockDim.x) {
+        if (i < n) wl.state[i] = ST_QUEUED;
+        if (i < n * NW) wl.inrows[i] = 0xffffffffu;
+        if (i < wl.cap) wl.queue[i] = i < n ? i : EMPTY;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 8)
+        wl.ctr[threadIdx.x] = (threadIdx.x == 1 || threadIdx.x == 2) ? (unsigned long long)n : 0ull;
+}
+
+}  // namespace
+
+void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, const Worklist& wl0,
+                             cudaStream_t s) {
+    if ((int64_t)w * h == 0) return;
+    Worklist wl = wl0;
+    wl.ntx = (w + RX * kTile - 1) / (RX * kTile);
+    wl.nty = (h + RY * kTile - 1) / (RY * kTile);
+    const int n = wl.ntx * wl.nty;
+    (note_launch(), k_rg_reset<<<(int)std::min<int64_t>((std::max<int64_t>(wl.cap, (int64_t)n * NW) + 255) / 256, 148 * 16), 256, 0, s>>>(wl));
+    static int blocks = 0;
+    const size_t smem = sizeof(Smem);
+    if (blocks == 0) {
+        cudaFuncSetAttribute(k_region_mr8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0, dev = 0, nsm = 148;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_region_mr8, NW * 32, smem);
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        blocks = nsm * (per_sm > 0 ? per_sm : 1);
+    }
+    int b = std::max(1, std::min(blocks, n));
+    (note_launch(), k_region_mr8<<<b, NW * 32, smem, s>>>(mask, R, w, h, wl));
+}
+
+void launch_recon_u8_auto(const uint8_t* mask, uint8_t* R, int w, int h, const Worklist& wl,
+                          cudaStream_t s) {
+    static int use_tiles = -1;
+    if (use_tiles < 0) {
+        const char* e = getenv("HP_IWPP_TILES");
+        use_tiles = (e && atoi(e) == 1) ? 1 : 0;
+    }
+    if (use_tiles)
+        launch_recon_u8(mask, R, w, h, wl, s);
+    else
+        launch_recon_u8_regions(mask, R, w, h, wl, s);
+}
+
+}  // namespace hp
