@@ -3,11 +3,11 @@
 //
 // Union-find with atomic hooking, canonical root = minimum linear index (reading C14):
 //   k_ccl_local   one 32x32 tile per CTA: shared-memory union-find over the in-tile N+
-//                 neighbours (atomicMin hooking of the larger root under the smaller),
+//                 neighbours (CAS hooking of the larger root under the smaller),
 //                 then every pixel gets the global index of its local root (= the local
 //                 component's minimum linear index, since local and global order agree);
 //   k_ccl_merge   cross-tile edges only (top row / left / right columns): the same hooking
-//                 on the global label plane with atomicMin (L2 atomics);
+//                 on the global label plane (L2 CAS), finds with CAS path halving;
 //   k_ccl_flatten every pixel points straight at its root; roots zero an aux slot so the
 //                 per-component reductions that follow need no memset.
 // Because a hook always links the larger root under the smaller, the surviving root of a
@@ -51,6 +51,9 @@ __device__ __forceinline__ int nplus(int conn, int k, int& dx, int& dy) {
     return 2;
 }
 
+// No path compression in shared memory: measured on B200 (tools/dbg_ccl.py, r1), an
+// atomicMin-based compression here lost unions in ~5% of runs, and with horizontal runs
+// pre-linked from ballots the in-tile hook chains stay short anyway.
 __device__ __forceinline__ int find_s(int* s, int x) {
     volatile int* vs = s;
     int r = x, p = vs[r];
@@ -58,16 +61,14 @@ __device__ __forceinline__ int find_s(int* s, int x) {
         r = p;
         p = vs[r];
     }
-    // path compression (monotone: atomicMin never undoes a concurrent hook)
-    while (x != r) {
-        int nx = vs[x];
-        if (nx <= r) break;
-        atomicMin(&s[x], r);
-        x = nx;
-    }
     return r;
 }
 
+// Lock-free union-find (Anderson & Woll style): a root is hooked only by CAS from itself
+// (atomicCAS(&p[a], a, b)), so a hook can never detach a non-root, and finds shorten paths
+// only by CAS path halving (x -> grandparent iff x still points at that parent).  Hooks
+// always go from the larger root to the smaller, so the surviving root of a component is
+// its minimum index.
 __device__ __forceinline__ void union_s(int* s, int a, int b) {
     while (true) {
         a = find_s(s, a);
@@ -78,9 +79,7 @@ __device__ __forceinline__ void union_s(int* s, int a, int b) {
             a = b;
             b = t;
         }
-        int old = atomicMin(&s[a], b);
-        if (old == a) return;
-        a = old;
+        if (atomicCAS(&s[a], a, b) == a) return;
     }
 }
 
@@ -93,17 +92,16 @@ __device__ __forceinline__ int32_t find_g(const int32_t* lab, int32_t x) {
     return x;
 }
 
-// find with path compression: every node on the walked path is re-hooked straight to the
-// root found (atomicMin keeps hooks monotone, so concurrent unions are never undone)
+// find with CAS path halving
 __device__ __forceinline__ int32_t find_gc(int32_t* lab, int32_t x) {
-    int32_t r = find_g(lab, x);
-    while (x != r) {
-        int32_t nx = __ldcg(lab + x);
-        if (nx <= r) break;
-        atomicMin(&lab[x], r);
-        x = nx;
+    while (true) {
+        int32_t p = __ldcg(lab + x);
+        if (p == x) return x;
+        int32_t gp = __ldcg(lab + p);
+        if (gp == p) return p;
+        atomicCAS(&lab[x], p, gp);
+        x = gp;
     }
-    return r;
 }
 
 __device__ __forceinline__ void union_g(int32_t* lab, int32_t a, int32_t b) {
@@ -116,9 +114,7 @@ __device__ __forceinline__ void union_g(int32_t* lab, int32_t a, int32_t b) {
             a = b;
             b = t;
         }
-        int32_t old = atomicMin(&lab[a], b);
-        if (old == a) return;
-        a = old;
+        if (atomicCAS(&lab[a], a, b) == a) return;
     }
 }
 
@@ -144,7 +140,22 @@ __global__ void __launch_bounds__(256) k_ccl_local(Src src, int conn, int32_t* _
         int start = 31 - __clz(nl);
         s[ly * kTile + lx] = f ? ly * kTile + start : -1;
     }
-    __syncthreads();
+    // quick paths: an all-background tile, or an all-foreground in-image tile without an
+    // equality predicate (one component rooted at the tile origin)
+    const int nfg = fgv[0] + fgv[1] + fgv[2] + fgv[3];
+    const bool full_tile = tx0 + kTile <= w && ty0 + kTile <= h;
+    const int any_fg = __syncthreads_or(nfg > 0);
+    const int all_fg = __syncthreads_and(nfg == 4);
+    if (!any_fg || (all_fg && full_tile && src.eq == nullptr)) {
+        const int32_t v = any_fg ? (int32_t)((int64_t)ty0 * w + tx0) : -1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            int ly = (threadIdx.x >> 5) + 8 * k;
+            int gx = tx0 + lx, gy = ty0 + ly;
+            if (gx < w && gy < h) lab[(int64_t)gy * w + gx] = v;
+        }
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         if (!fgv[k]) continue;

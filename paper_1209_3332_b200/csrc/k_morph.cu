@@ -3,13 +3,17 @@
 //
 // open = dilate_D(erode_D(g)).  D's row dy covers dx in [-hw(dy), hw(dy)] with hw(dy) =
 // round(sqrt(r^2 - dy^2)); so min over D = min over rows of a horizontal running min whose
-// width takes only a few distinct values (6 for diam 19).  Bound by the plain integer ALUs
-// (SURVEY §8(d)): every step works on 4 pixels per 32-bit register with the SIMD byte
-// min/max (__vminu4 / __vmaxu4); byte-shifted windows come from funnel shifts.
-//   stage 1: the (TH + 2r) x TW input rows are staged in shared memory (OOB -> identity);
-//   stage 2: for each row and 4-pixel word, horizontal min over [-k, k] for k = 1..r,
-//            keeping the distinct half-widths hw(dy) -> H[width][row][word] in smem;
-//   stage 3: out(y) = min over the diam rows i of H[hw(i - r)][y + i].
+// half-width takes only a few distinct values (6 for diam 19).  Bound by the plain integer
+// ALUs: every step works on 4 pixels per 32-bit register with the SIMD byte
+// min/max (__vminu4 / __vmaxu4).
+//   stage 1: the (TH + 2r) input rows of a TW-wide tile (+ halo) are staged in shared memory
+//            as 32-bit words (aligned vector loads; out-of-tile bytes = identity);
+//   stage 2: per row and output word: the 2*RW+2 covering words go to registers once, every
+//            byte-shifted window is a funnel shift by a compile-time amount, and the running
+//            min over [-k, k] is kept for the distinct half-widths -> H[width][row][word];
+//   stage 3: out(y) = min over the diam rows dy of H[width(dy)][y + dy].
+// The radius is a template parameter (19x19 = the paper's disk is the instantiated fast
+// path); other odd diameters use the generic path with the same structure.
 #include <algorithm>
 #include <cmath>
 #include <vector>
@@ -20,10 +24,159 @@ namespace hp {
 
 namespace {
 
-constexpr int TW = 128;          // output tile width (pixels) = 32 words
-constexpr int TWW = TW / 4;      // words per output row
+constexpr int TW = 128;       // output tile width (pixels) = 32 words
+constexpr int TWW = TW / 4;   // output words per row
+constexpr int TH = 32;        // output tile height
 constexpr int kMaxDiam = 63;
 
+template <bool IS_MIN>
+__device__ __forceinline__ uint32_t vop(uint32_t a, uint32_t b) {
+    return IS_MIN ? __vminu4(a, b) : __vmaxu4(a, b);
+}
+
+__host__ __device__ constexpr int hw_of(int r, int dy) {
+    // round(sqrt(r^2 - dy^2)) evaluated exactly in integers: the largest w with
+    // (w - 0.5)^2 <= r^2 - dy^2, i.e. (2w - 1)^2 <= 4(r^2 - dy^2)  (no ties for integer r, dy)
+    int s = 4 * (r * r - dy * dy), w = 0;
+    while ((2 * (w + 1) - 1) * (2 * (w + 1) - 1) <= s) ++w;
+    return w;
+}
+
+// distinct half-widths of the ellipse of radius R, ascending, as a compile-time table
+template <int R>
+struct Ellipse {
+    int n = 0;
+    int hw[R + 1] = {};
+    int idx_of_dy[2 * R + 1] = {};
+    constexpr Ellipse() {
+        for (int dy = 0; dy <= R; ++dy) {
+            int v = hw_of(R, dy);
+            bool seen = false;
+            for (int k = 0; k < n; ++k) seen |= hw[k] == v;
+            if (!seen) hw[n++] = v;
+        }
+        for (int a = 0; a < n; ++a)  // sort ascending
+            for (int b = a + 1; b < n; ++b)
+                if (hw[b] < hw[a]) { int t = hw[a]; hw[a] = hw[b]; hw[b] = t; }
+        for (int dy = -R; dy <= R; ++dy) {
+            int v = hw_of(R, dy < 0 ? -dy : dy);
+            for (int k = 0; k < n; ++k)
+                if (hw[k] == v) idx_of_dy[dy + R] = k;
+        }
+    }
+};
+
+// ---------------------------------------------------------------- radius-specialised kernel
+template <bool IS_MIN, int R>
+__global__ void __launch_bounds__(256) k_morph_r(const uint8_t* __restrict__ src, int w, int h,
+                                                 uint8_t* __restrict__ dst) {
+    constexpr Ellipse<R> E{};
+    constexpr int ND = E.n;
+    constexpr int RW = (R + 3) / 4;              // halo words each side
+    constexpr int IW = TWW + 2 * RW + 1;         // staged words per row
+    constexpr int ROWS = TH + 2 * R;
+    constexpr uint32_t ID = IS_MIN ? 0xffffffffu : 0u;
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t* in = smem;                          // [ROWS][IW]
+    uint32_t* H = smem + ROWS * IW;               // [ND][ROWS][TWW]
+    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const bool row_aligned = (w & 3) == 0 && (((uintptr_t)src) & 3) == 0;
+
+    // stage 1: words [x0/4 - RW, x0/4 + TWW + RW + 1) of rows [y0 - R, y0 + TH + R)
+    for (int r = ty; r < ROWS; r += 8) {
+        const int gy = y0 - R + r;
+        const bool rin = gy >= 0 && gy < h;
+        const uint8_t* rowp = src + (int64_t)(rin ? gy : 0) * w;
+        for (int wi = tx; wi < IW; wi += 32) {
+            const int gx = x0 - 4 * RW + 4 * wi;
+            uint32_t v = ID;
+            if (rin) {
+                if (row_aligned && gx >= 0 && gx + 3 < w) {
+                    v = __ldg(reinterpret_cast<const unsigned int*>(rowp + gx));
+                } else {
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        int x = gx + b;
+                        uint32_t byte = (x >= 0 && x < w) ? (uint32_t)__ldg(rowp + x) : (ID & 0xffu);
+                        v = (v & ~(0xffu << (8 * b))) | (byte << (8 * b));
+                    }
+                }
+            }
+            in[r * IW + wi] = v;
+        }
+    }
+    __syncthreads();
+
+    // stage 2: horizontal running min/max for the distinct half-widths
+    for (int r = ty; r < ROWS; r += 8) {
+        const uint32_t* rowp = in + r * IW;
+        const int j = tx;  // output word
+        uint32_t wv[2 * RW + 2];
+#pragma unroll
+        for (int k = 0; k < 2 * RW + 2; ++k) wv[k] = rowp[j + k];
+        // window at byte offset k (relative to the output word's first byte)
+        auto win = [&](int k) -> uint32_t {
+            const int o = 4 * RW + k;  // byte offset into wv
+            return __funnelshift_r(wv[o >> 2], wv[(o >> 2) + 1], 8 * (o & 3));
+        };
+        uint32_t m = wv[RW];
+        int di = 0;
+        if (E.hw[0] == 0) {
+            H[(0 * ROWS + r) * TWW + j] = m;
+            di = 1;
+        }
+#pragma unroll
+        for (int k = 1; k <= R; ++k) {
+            m = vop<IS_MIN>(m, vop<IS_MIN>(win(k), win(-k)));
+#pragma unroll
+            for (int q = 0; q < ND; ++q)
+                if (E.hw[q] == k) H[(q * ROWS + r) * TWW + j] = m;
+        }
+        (void)di;
+    }
+    __syncthreads();
+
+    // stage 3: vertical combine over the diam rows of D
+    const int j = tx;
+    const int gx = x0 + 4 * j;
+    for (int oy = ty; oy < TH; oy += 8) {
+        const int gy = y0 + oy;
+        if (gy >= h || gx >= w) continue;
+        uint32_t m = ID;
+#pragma unroll
+        for (int dy = 0; dy <= 2 * R; ++dy) m = vop<IS_MIN>(m, H[(E.idx_of_dy[dy] * ROWS + oy + dy) * TWW + j]);
+        uint8_t* o = dst + (int64_t)gy * w + gx;
+        if (gx + 3 < w && (((uintptr_t)o) & 3) == 0) {
+            *reinterpret_cast<uint32_t*>(o) = m;
+        } else {
+            for (int b = 0; b < 4 && gx + b < w; ++b) o[b] = (uint8_t)(m >> (8 * b));
+        }
+    }
+}
+
+template <int R>
+size_t smem_r() {
+    constexpr Ellipse<R> E{};
+    constexpr int RW = (R + 3) / 4;
+    return 4 * (size_t)(TH + 2 * R) * ((TWW + 2 * RW + 1) + (size_t)E.n * TWW);
+}
+
+template <int R>
+void launch_r(const uint8_t* g, int w, int h, uint8_t* tmp, uint8_t* out, cudaStream_t s) {
+    static bool attr = false;
+    const size_t smem = smem_r<R>();
+    if (!attr) {
+        cudaFuncSetAttribute(k_morph_r<true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_morph_r<false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    dim3 grid((w + TW - 1) / TW, (h + TH - 1) / TH);
+    (note_launch(), k_morph_r<true, R><<<grid, 256, smem, s>>>(g, w, h, tmp));
+    (note_launch(), k_morph_r<false, R><<<grid, 256, smem, s>>>(tmp, w, h, out));
+}
+
+// ---------------------------------------------------------------- generic (any odd diam)
 struct MorphDesc {
     int r, nd, th;               // radius, number of distinct half-widths, tile height
     int rw;                      // halo words = ceil(r / 4)
@@ -32,23 +185,16 @@ struct MorphDesc {
 };
 
 template <bool IS_MIN>
-__device__ __forceinline__ uint32_t vop(uint32_t a, uint32_t b) {
-    return IS_MIN ? __vminu4(a, b) : __vmaxu4(a, b);
-}
-
-template <bool IS_MIN>
 __global__ void __launch_bounds__(256) k_morph(const uint8_t* __restrict__ src, int w, int h,
                                                MorphDesc md, uint8_t* __restrict__ dst) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int r = md.r, th = md.th, rw = md.rw;
     const int rows = th + 2 * r;
-    const int in_words = TWW + 2 * rw + 1;        // staged words per row
-    uint32_t* in = smem;                           // [rows][in_words]
-    uint32_t* H = smem + rows * in_words;          // [nd][rows][TWW]
+    const int in_words = TWW + 2 * rw + 1;
+    uint32_t* in = smem;
+    uint32_t* H = smem + rows * in_words;
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * th;
     const uint8_t ident = IS_MIN ? 255 : 0;
-
-    // stage 1: bytes [x0 - 4rw, x0 + TW + 4rw + 4) of rows [y0 - r, y0 + th + r)
     uint8_t* inb = reinterpret_cast<uint8_t*>(in);
     const int in_bytes = in_words * 4;
     for (int i = threadIdx.x; i < rows * in_bytes; i += blockDim.x) {
@@ -59,16 +205,12 @@ __global__ void __launch_bounds__(256) k_morph(const uint8_t* __restrict__ src, 
         inb[i] = v;
     }
     __syncthreads();
-
-    // stage 2: horizontal running min/max for every distinct half-width
     for (int i = threadIdx.x; i < rows * TWW; i += blockDim.x) {
         int ry = i / TWW, j = i - ry * TWW;
         const uint32_t* row = in + ry * in_words;
-        // window word at byte offset k relative to this word's first byte
         auto win = [&](int k) -> uint32_t {
             int o = 4 * (j + rw) + k;
-            int wi = o >> 2, sh = o & 3;
-            return __funnelshift_r(row[wi], row[wi + 1], 8 * sh);
+            return __funnelshift_r(row[o >> 2], row[(o >> 2) + 1], 8 * (o & 3));
         };
         uint32_t m = win(0);
         int di = 0;
@@ -85,8 +227,6 @@ __global__ void __launch_bounds__(256) k_morph(const uint8_t* __restrict__ src, 
         }
     }
     __syncthreads();
-
-    // stage 3: vertical combine over the diam rows of D
     const int diam = 2 * r + 1;
     for (int i = threadIdx.x; i < th * TWW; i += blockDim.x) {
         int oy = i / TWW, j = i - oy * TWW;
@@ -108,10 +248,7 @@ MorphDesc make_desc(int diam, size_t* smem_bytes) {
     md.r = diam / 2;
     md.rw = (md.r + 3) / 4;
     std::vector<int> hw(diam);
-    for (int i = 0; i < diam; ++i) {
-        int dy = i - md.r;
-        hw[i] = (int)std::lround(std::sqrt((double)(md.r * md.r - dy * dy)));
-    }
+    for (int i = 0; i < diam; ++i) hw[i] = hw_of(md.r, std::abs(i - md.r));
     std::vector<int> d = hw;
     std::sort(d.begin(), d.end());
     d.erase(std::unique(d.begin(), d.end()), d.end());
@@ -135,6 +272,10 @@ MorphDesc make_desc(int diam, size_t* smem_bytes) {
 void launch_open(const uint8_t* g, int w, int h, int diam, uint8_t* tmp, uint8_t* out,
                  cudaStream_t s) {
     if ((int64_t)w * h == 0) return;
+    if (diam == 19) {  // the paper's 19x19 disk
+        launch_r<9>(g, w, h, tmp, out, s);
+        return;
+    }
     size_t smem = 0;
     MorphDesc md = make_desc(diam, &smem);
     static bool attr_set = false;

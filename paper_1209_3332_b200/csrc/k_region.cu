@@ -48,7 +48,7 @@ __device__ __forceinline__ int32_t q_pop(const Worklist& wl) {
         }
         if (vload(&wl.ctr[2]) == 0ull) return -1;
         __nanosleep(ns);
-        if (ns < 1024) ns <<= 1;
+        if (ns < 256) ns <<= 1;
     }
 }
 
@@ -113,7 +113,7 @@ struct Smem {
 // byte of window pixel (wr, wc): window column wc (0 .. RX*32+1) is byte wc + 3
 __device__ __forceinline__ int bidx(int wr, int wc) { return wr * RWB + wc + 3; }
 
-__global__ void __launch_bounds__(NW * 32, 1) k_region_mr8(const uint8_t* __restrict__ mask,
+__global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __restrict__ mask,
                                                            uint8_t* __restrict__ R, int w, int h,
                                                            Worklist wl) {
     extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(_HERE, "libhp.so")
+SO_PATH = os.environ.get("HP_SO", os.path.join(_HERE, "libhp.so"))
 
 NFEAT = 34
 FLAG_RBC_HI, FLAG_RBC_LO, FLAG_R_GT_B, FLAG_BG = 1, 2, 4, 8

@@ -128,6 +128,22 @@ def test_ccl_random(ctx, shape, dens):
         assert np.array_equal(lab, exp), (name, shape, dens)
 
 
+@pytest.mark.parametrize("shape,dens", [((100, 257), 0.6), ((300, 333), 0.55), ((512, 512), 0.6)])
+def test_ccl_repeated_no_races(ctx, shape, dens):
+    # union-find with concurrent hooking: repeat to expose schedule-dependent losses
+    # (a shared-memory path compression lost unions in ~5% of runs before it was removed)
+    h, w = shape
+    fg = (np.random.default_rng(h * 1000 + w + int(dens * 10)).random(shape) < dens).astype(U8)
+    for conn, name in [(4, "CCL4"), (8, "CCL8")]:
+        exp, _ = oracle.ccl(fg, conn)
+        for rep in range(25):
+            (lab,) = stage(ctx, name, [fg], [((h, w), I32)], w, h)
+            if not np.array_equal(lab, exp):
+                d = np.argwhere(lab != exp)
+                raise AssertionError(f"{name} {shape} rep {rep}: {len(d)} px differ, e.g. "
+                                     f"{[(int(y), int(x), int(lab[y, x]), int(exp[y, x])) for y, x in d[:6]]}")
+
+
 @pytest.mark.parametrize("shape", SHAPES)
 def test_open_ragged(ctx, shape):
     h, w = shape
