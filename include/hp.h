@@ -177,7 +177,8 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
  *                                                  out2 feat f32[cap][34], out3 n_rows i32[1]
  *                                                  (cap = max_objects)
  *  IWPP_RAW  in0 marker u8, in1 mask u8         -> out0 recon u8, out1 stats i64[4]
- *                                                  (tiles processed, rounds, -, -)
+ *                                                  (jobs, sweep iterations, ns regions were
+ *                                                  owned, row closures attempted)
  *  CCL8/CCL4 in0 fg u8                          -> out0 labels i32 (1 + min index, 0 = bg)
  *  RECON_F32 in0 marker f32, in1 mask f32, in2 domain u8 (may be NULL) -> out0 recon f32
  */

@@ -531,7 +531,7 @@ hp_status hp_stage_run(hp_ctx* ctx, int32_t slot, hp_stage stage, const hp_stage
             if (!need({io->in[0], io->in[1], io->out[0]})) break;
             launch_recon_init_u8(in8(0), in8(1), (uint8_t*)io->out[0], w, h, s);
             launch_recon_u8_auto(in8(1), (uint8_t*)io->out[0], w, h, sl.wl, s);
-            if (io->out[1]) cudaMemcpyAsync(io->out[1], sl.wl.ctr + 3, 2 * sizeof(unsigned long long),
+            if (io->out[1]) cudaMemcpyAsync(io->out[1], sl.wl.ctr + 3, 4 * sizeof(unsigned long long),
                                             cudaMemcpyDeviceToDevice, s);
             return check_launch(ctx, "stage iwpp");
         }

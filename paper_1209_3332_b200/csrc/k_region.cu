@@ -108,7 +108,14 @@ struct Smem {
     uint32_t chg[NW];
     int job;
     int again;
+    unsigned long long t0;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // byte of window pixel (wr, wc): window column wc (0 .. RX*32+1) is byte wc + 3
 __device__ __forceinline__ int bidx(int wr, int wc) { return wr * RWB + wc + 3; }
@@ -153,6 +160,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __rest
         if (threadIdx.x == 0) {
             int t = q_pop(wl);
             if (t >= 0) atomicExch(&wl.state[t], ST_BUSY);
+            S.t0 = gtimer();
             S.job = t;
         }
         __syncthreads();
@@ -160,6 +168,11 @@ __global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __rest
         if (t < 0) break;
         const int rx = t % wl.ntx, ry = t / wl.ntx;
         const int X0 = rx * RX * kTile, Y0 = ry * RY * kTile;
+        // interior regions (window fully inside the image, rows 4-byte aligned) take the
+        // unconditional vector path
+        const bool inner = X0 >= 4 && X0 + RX * kTile + 4 <= w && Y0 >= 1 && Y0 + RY * kTile + 1 <= h &&
+                           (w & 3) == 0 && (((uintptr_t)R | (uintptr_t)mask) & 3) == 0;
+        bool have_window = false;
         while (true) {
             if (lane == 0) S.dirty[warp] = atomicExch(&wl.inrows[t * NW + warp], 0u);
             __threadfence();
@@ -169,15 +182,65 @@ __global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __rest
             for (int k = 0; k < NW; ++k) any_in |= S.dirty[k] != 0;
             uint32_t mychg = 0;
             if (any_in) {
-                for (int k = threadIdx.x; k < ROWS * RWW; k += blockDim.x) {
-                    int r = k / RWW, wi = k - r * RWW;
-                    int gx = X0 - 4 + 4 * wi, gy = Y0 - 1 + r;
-                    S.R[k] = load_word(R, w, h, gx, gy);
-                    S.M[k] = load_word(mask, w, h, gx, gy);
+                if (!have_window) {
+                    // the whole window: all of a thread's loads are issued before any store
+                    constexpr int NIT = (ROWS * RWW + NW * 32 - 1) / (NW * 32);
+                    uint32_t vr[NIT], vm[NIT];
+                    if (inner) {
+                        const uint8_t* rb = R + (int64_t)(Y0 - 1) * w + (X0 - 4);
+                        const uint8_t* mb = mask + (int64_t)(Y0 - 1) * w + (X0 - 4);
+#pragma unroll
+                        for (int i = 0; i < NIT; ++i) {
+                            int k = threadIdx.x + i * NW * 32;
+                            if (k < ROWS * RWW) {
+                                int r = k / RWW, wi = k - r * RWW;
+                                int64_t o = (int64_t)r * w + 4 * wi;
+                                vr[i] = __ldcg(reinterpret_cast<const unsigned int*>(rb + o));
+                                vm[i] = __ldcg(reinterpret_cast<const unsigned int*>(mb + o));
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < NIT; ++i) {
+                            int k = threadIdx.x + i * NW * 32;
+                            if (k < ROWS * RWW) {
+                                int r = k / RWW, wi = k - r * RWW;
+                                int gx = X0 - 4 + 4 * wi, gy = Y0 - 1 + r;
+                                vr[i] = load_word(R, w, h, gx, gy);
+                                vm[i] = load_word(mask, w, h, gx, gy);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < NIT; ++i) {
+                        int k = threadIdx.x + i * NW * 32;
+                        if (k < ROWS * RWW) {
+                            S.R[k] = vr[i];
+                            S.M[k] = vm[i];
+                        }
+                    }
+                    have_window = true;
+                } else {
+                    // re-processing the same region: only the halo ring of R can have changed
+                    // (the interior is owned by this CTA; the mask never changes)
+                    constexpr int NH = 2 * RWW + 2 * (ROWS - 2);
+                    for (int k = threadIdx.x; k < NH; k += blockDim.x) {
+                        int r, wi;
+                        if (k < 2 * RWW) {
+                            r = k < RWW ? 0 : ROWS - 1;
+                            wi = k % RWW;
+                        } else {
+                            int j = k - 2 * RWW;
+                            r = 1 + (j >> 1);
+                            wi = (j & 1) ? RWW - 1 : 0;
+                        }
+                        S.R[r * RWW + wi] = load_word(R, w, h, X0 - 4 + 4 * wi, Y0 - 1 + r);
+                    }
                 }
                 __syncthreads();
                 uint32_t dirty = S.dirty[warp];
                 int iters = 0;
+                int nrows = 0;
                 while (true) {
                     // Gauss-Seidel sweeps of this sub-tile (see iwpp_rules.cuh sweep_rows)
                     uint32_t chg = 0;
@@ -186,6 +249,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __rest
                             const uint32_t bit = 1u << (y - 1);
                             if (!(dirty & bit)) continue;
                             dirty &= ~bit;
+                            ++nrows;
                             if (row(y)) { chg |= bit; dirty |= (bit << 1) | (bit >> 1); }
                         }
                         if (!dirty) break;
@@ -193,6 +257,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __rest
                             const uint32_t bit = 1u << (y - 1);
                             if (!(dirty & bit)) continue;
                             dirty &= ~bit;
+                            ++nrows;
                             if (row(y)) { chg |= bit; dirty |= (bit << 1) | (bit >> 1); }
                         }
                     }
@@ -230,6 +295,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __rest
                     if (!more) break;
                 }
                 if (threadIdx.x == 0) atomicAdd(&wl.ctr[4], (unsigned long long)iters);
+                if (lane == 0) atomicAdd(&wl.ctr[6], (unsigned long long)nrows);
                 // write back the changed rows of this sub-tile (interior words)
                 if (mychg) {
                     for (int k = lane; k < kTile * 8; k += 32) {
@@ -305,6 +371,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __rest
                     again = 1;
                 }
                 atomicAdd(&wl.ctr[3], 1ull);
+                if (!again) atomicAdd(&wl.ctr[5], gtimer() - S.t0);  // ns a region was owned
                 S.again = again;
             }
             __syncthreads();

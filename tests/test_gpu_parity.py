@@ -73,6 +73,31 @@ def test_recon(ctx, chain):
     assert np.array_equal(cand, chain["cand"])
 
 
+@pytest.mark.parametrize("kind", ["uniform", "blobs", "ramp"])
+def test_recon_cand_clipped(ctx, kind):
+    # the pipeline's S4 computes cand through recon(max(open,K), max(g,K)); check it against
+    # the oracle's plain recon + threshold on inputs with very different K
+    rng = np.random.default_rng({"uniform": 1, "blobs": 2, "ramp": 3}[kind])
+    h, w = 300, 400
+    if kind == "uniform":
+        g = rng.integers(0, 256, size=(h, w)).astype(U8)
+    elif kind == "blobs":
+        g = (10 + rng.integers(0, 6, size=(h, w))).astype(np.int32)
+        yy, xx = np.mgrid[:h, :w]
+        for _ in range(40):
+            cy, cx, r, v = rng.uniform(0, h), rng.uniform(0, w), rng.uniform(3, 9), rng.integers(60, 250)
+            g = np.where((yy - cy) ** 2 + (xx - cx) ** 2 <= r * r, v, g)
+        g = g.astype(U8)
+    else:
+        g = ((np.add.outer(np.arange(h), np.arange(w)) % 256) ^ rng.integers(0, 64, size=(h, w))).astype(U8)
+    op = oracle.open_(g, 19)
+    rbc = (rng.random((h, w)) < 0.01).astype(U8)
+    cand, rec = stage(ctx, "RECON", [g, op, rbc], [((h, w), U8), ((h, w), U8)], w, h)
+    ecand, erec = oracle.recon_to_nuclei(g, op, rbc, 50, with_recon=True)
+    assert np.array_equal(rec, erec)
+    assert np.array_equal(cand, ecand)
+
+
 def test_area_fill(ctx, chain):
     h, w = chain["g"].shape
     (b,) = stage(ctx, "AREA", [chain["cand"]], [((h, w), U8)], w, h)

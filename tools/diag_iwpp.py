@@ -44,9 +44,11 @@ def main():
     st = torch.zeros(4, dtype=torch.int64, device="cuda")
     ms = timed(lambda: ctx.stage_run(0, "IWPP_RAW", [op, g], [rec, st], size, size))
     ntiles = (size // 32) ** 2
-    print(json.dumps({"case": "recon(open, g) config2", "ms": ms, "tiles": ntiles,
-                      "tile_jobs": int(st[0]), "rounds": int(st[1]),
-                      "jobs_per_tile": int(st[0]) / ntiles}), flush=True)
+    print(json.dumps({"case": "recon(open, g) " + (pool[0] if pool else "config2"), "ms": ms,
+                      "jobs": int(st[0]), "iterations": int(st[1]),
+                      "owned_ms_total": int(st[2]) / 1e6, "avg_parallel_regions": int(st[2]) / 1e6 / ms,
+                      "us_per_job": int(st[2]) / 1e3 / max(1, int(st[0])), "row_closures": int(st[3])}),
+          flush=True)
     for kind in ([] if "--quick" in sys.argv else ["serpentine", "spiral"]):
         for ramp in [False, True]:
             mk, mask, L = make_stress(kind, size, ramp)
