@@ -320,31 +320,33 @@ def main():
     # e2e through hp_run_tiles: pinned host tiles, H2D + D2H inside the timed region
     e2e = None
     if not args.no_e2e:
+        # the production path: a demand-driven tile queue shared by all ranks (PAPER.md:
+        # 370-389), hp_run_tiles with per-slot H2D/compute/D2H streams, and the end-of-run
+        # NCCL gather of every rank's feature rows to rank 0 -- all inside the timed region
+        from paper_1209_3332_b200.dist import DistTileSource, TileQueue, gather_rows, table_digest
         pinned = [torch.from_numpy(x).pin_memory() for x in tiles]
         rows_copied = min(cap, 4096)
         d2h_per_tile = 4 + rows_copied * (4 + 4 + 34 * 4)
 
-        def run(ntiles):
-            it = iter(range(ntiles))
-
-            def nxt():
-                try:
-                    i = next(it)
-                except StopIteration:
-                    return None
-                return pinned[i % B].data_ptr(), 3 * size, i
+        def run(ntiles, key):
+            q = TileQueue(ntiles, block=S, key=key)
+            src = DistTileSource(q, lambda tid: pinned[tid % B])
+            results = {}
 
             def done(tid, l, f, ft, st):
                 if st != 0:
                     raise RuntimeError(f"tile {tid} status {st}")
+                results[tid] = (l, f, ft)
 
-            ctx.run_tiles(nxt, done, size, size)
+            ctx.run_tiles(src, done, size, size)
+            torch.cuda.synchronize()
+            return gather_rows(results, device=torch.device("cuda", local)), len(src.taken)
 
-        run(B * max(1, args.warmup))
+        run(world * B * max(1, args.warmup), "hp/warm")
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        run(B * args.steps)
+        table, mine = run(world * B * args.steps, "hp/timed")
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         barrier()
@@ -352,9 +354,13 @@ def main():
         if world > 1:
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)
         e2e = {"value": world * B * args.steps / float(tw.item()), "unit": UNIT,
-               "h2d_bytes_per_step": B * 3 * size * size, "d2h_bytes_per_step": B * d2h_per_tile,
-               "api": "hp_run_tiles (pinned host tiles, per-slot H2D/compute/D2H streams)",
-               "timer": "host wall clock bracketed by device synchronize"}
+               "h2d_bytes_per_step": world * B * 3 * size * size,
+               "d2h_bytes_per_step": world * B * d2h_per_tile,
+               "api": "hp_run_tiles fed by the shared demand-driven tile queue; NCCL gather of "
+                      "all feature rows to rank 0 inside the timed region",
+               "timer": "host wall clock bracketed by device synchronize and barriers, max over ranks",
+               "rows_gathered": None if table is None else int(len(table)),
+               "table_digest": None if table is None else table_digest(table)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -381,4 +387,11 @@ def main():
 
 
 if __name__ == "__main__":
-    sys.exit(main())
+    try:
+        rc = main()
+    except BaseException:  # report loudly: a rank that dies silently is undiagnosable
+        import traceback
+        traceback.print_exc()
+        sys.stderr.flush()
+        raise
+    sys.exit(rc)

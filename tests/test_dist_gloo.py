@@ -1,0 +1,107 @@
+"""Multi-process host logic of the tile sharding on CPU with gloo,
+world_size 2: the demand-driven queue hands every tile out exactly once, the in-flight
+window never exceeds n_slots (SPEC.md:398's window invariant, via a null pipeline that
+mimics hp_run_tiles' slot discipline), and the gathered table is the sorted union --
+identical to a single-process run."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1209_3332_b200.dist import (DistTileSource, TileQueue, gather_rows, pack_rows,
+                                       table_digest, unpack_rows)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _fake_rows(tid):
+    rng = np.random.default_rng(tid)
+    n = int(rng.integers(0, 5))
+    lab = np.sort(rng.choice(10_000, size=n, replace=False)).astype(np.int32) + 1
+    fl = (lab % 2).astype(np.int32)
+    ft = rng.random((n, 34)).astype(np.float32)
+    return lab, fl, ft
+
+
+def _null_run(source, n_slots, inflight_log):
+    """Stand-in for hp_run_tiles: round-robin slots, at most n_slots tiles in flight."""
+    results, slots = {}, [None] * n_slots
+    i = 0
+    while True:
+        if slots[i] is not None:
+            tid = slots[i]
+            results[tid] = _fake_rows(tid)
+            slots[i] = None
+        r = source()
+        if r is None:
+            for k in range(n_slots):
+                if slots[k] is not None:
+                    results[slots[k]] = _fake_rows(slots[k])
+                    slots[k] = None
+            return results
+        slots[i] = r[2]
+        inflight_log.append(sum(s is not None for s in slots))
+        i = (i + 1) % n_slots
+
+
+def _worker(rank, world, port, n_tiles, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    q = TileQueue(n_tiles, block=3)
+    pool = [torch.zeros((4, 4, 3), dtype=torch.uint8) for _ in range(5)]
+    src = DistTileSource(q, lambda tid: pool[tid % len(pool)])
+    log = []
+    res = _null_run(src, n_slots=2, inflight_log=log)
+    table = gather_rows(res)
+    if rank == 0:
+        out_q.put((sorted(src.taken), table_digest(table), len(table), max(log) if log else 0))
+    else:
+        out_q.put((sorted(src.taken), None, None, max(log) if log else 0))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_tiles", [0, 1, 37])
+def test_queue_and_gather_world2(n_tiles):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n_tiles, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    taken = sorted(t for o in outs for t in o[0])
+    assert taken == list(range(n_tiles))                      # every tile exactly once
+    assert all(o[3] <= 2 for o in outs)                        # window bound (n_slots = 2)
+    digest = next(o[1] for o in outs if o[1] is not None)
+    ref = {t: _fake_rows(t) for t in range(n_tiles)}
+    rec = np.sort(unpack_rows(pack_rows(ref)), order=["tile", "label"])
+    assert digest == table_digest(rec)                         # sorted union = 1-process table
+
+
+def test_pack_roundtrip():
+    res = {7: _fake_rows(7), 3: _fake_rows(3)}
+    rec = unpack_rows(pack_rows(res))
+    assert list(rec["tile"]) == [3] * len(res[3][0]) + [7] * len(res[7][0])
+    assert np.array_equal(rec["label"][:len(res[3][0])], res[3][0])
+
+
+def test_single_process_queue():
+    q = TileQueue(10, block=4, store=None)
+    blocks = []
+    while (b := q.grab()) is not None:
+        blocks.append(list(b))
+    assert blocks == [[0, 1, 2, 3], [4, 5, 6, 7], [8, 9]]
