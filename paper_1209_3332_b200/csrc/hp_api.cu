@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <array>
 #include <atomic>
@@ -39,6 +40,7 @@ struct hp_ctx {
     std::vector<void*> dev_blocks;
     std::vector<void*> host_blocks;
     int rows_copied = 0;  // rows copied back per tile in hp_run_tiles
+    bool global_s8s10 = false;  // env HP_GLOBAL_S8S10=1: the per-stage global path in the pipeline
     // stage-timing ring: per slot, kRing sets of 12 events (one set per tile)
     std::vector<std::vector<std::array<cudaEvent_t, 12>>> ring;
     std::vector<int> ring_pos, ring_n;
@@ -160,12 +162,21 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
     ev(ctx, sl, 6, s);
     launch_edt(sl.F, w, h, sl, nullptr, sl.dist, s);                                                 // S7
     ev(ctx, sl, 7, s);
-    launch_markers(sl.dist, sl.F, p.h, w, h, sl, sl.ML, sl.J, s);                                   // S8
-    ev(ctx, sl, 8, s);
-    launch_watershed(sl.dist, sl.ML, sl.F, w, h, sl, sl.split, nullptr, nullptr, nullptr, s);       // S9
-    ev(ctx, sl, 9, s);
-    launch_bwlabel(sl.split, w, h, p.obj_min_area, p.obj_max_area, sl, labels, lpitch, n_objects, s); // S10
-    ev(ctx, sl, 10, s);
+    if (ctx->global_s8s10) {
+        launch_markers(sl.dist, sl.F, p.h, w, h, sl, sl.ML, sl.J, s);                               // S8
+        ev(ctx, sl, 8, s);
+        launch_watershed(sl.dist, sl.ML, sl.F, w, h, sl, sl.split, nullptr, nullptr, nullptr, s);   // S9
+        ev(ctx, sl, 9, s);
+        launch_bwlabel(sl.split, w, h, p.obj_min_area, p.obj_max_area, sl, labels, lpitch, n_objects, s); // S10
+        ev(ctx, sl, 10, s);
+    } else {
+        // S8-S10 fused: one CTA per 8-component of F (timed under S8; S9/S10 read 0)
+        launch_components(sl.F, sl.dist, p.h, p.obj_min_area, p.obj_max_area, w, h, sl, labels, lpitch,
+                          n_objects, s);
+        ev(ctx, sl, 8, s);
+        ev(ctx, sl, 9, s);
+        ev(ctx, sl, 10, s);
+    }
     return check_launch(ctx, "segment");
 }
 
@@ -260,6 +271,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
     ctx->cfg = *cfg;
     ctx->device = cfg->device;
     ctx->rows_copied = std::min(cfg->max_objects, kRowsAsync);
+    if (const char* e = getenv("HP_GLOBAL_S8S10")) ctx->global_s8s10 = atoi(e) == 1;
     auto dalloc = [&](size_t bytes) -> void* {
         void* p = nullptr;
         if (cudaMalloc(&p, bytes ? bytes : 16) != cudaSuccess) return nullptr;
@@ -306,6 +318,10 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.obj_root = (int32_t*)A(4 * (size_t)mo);
         s.obj_rank = (int32_t*)A(4 * (size_t)mo);
         s.obj_bbox = (int32_t*)A(16 * (size_t)mo);
+        s.comp_cap = (int32_t)(N / 4 + 16);  // at most N/4 8-components in N pixels
+        s.comp_root = (int32_t*)A(4 * (size_t)s.comp_cap);
+        s.comp_bbox = (int4*)A(16 * (size_t)s.comp_cap);
+        s.cid = (int32_t*)A(4 * N);
         s.counters = (unsigned long long*)A(8 * 4);
         s.cnt32 = (int32_t*)A(4 * 8);
         s.rgb_dev = (uint8_t*)A(3 * N);
@@ -320,7 +336,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.h_nrows = (int32_t*)halloc(16);
         void* all[] = {s.g, s.flags, s.rbc, s.u8a, s.u8b, s.cand, s.big0, s.F, s.split, s.pmask, s.lab, s.aux,
                        s.ML, s.d, s.L, s.dist, s.J, s.c, s.gcol, s.seg_top, s.seg_bot, s.wl.state, s.wl.inrows, s.wl.queue,
-                       s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
+                       s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.comp_root, s.comp_bbox, s.cid, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
                        s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows};
         for (void* p : all)
             if (!p) { hp_ctx_destroy(ctx); return HP_ERR_NOMEM; }

@@ -71,6 +71,11 @@ struct Slot {
     Worklist wl;
     // objects
     int32_t *obj_root, *obj_bbox, *obj_rank;
+    // F components (k_comp.cu): root list, bounding boxes, root -> component id plane
+    int32_t* comp_root;
+    int4* comp_bbox;
+    int32_t* cid;
+    int32_t comp_cap;
     // small device counters: [0] bg count (u64), [1] any-bg flag, [2] n objects, ...
     unsigned long long* counters;
     int32_t* cnt32;  // [0] n_obj raw, [1] edt pathological rows, [2..] misc
@@ -155,6 +160,9 @@ void launch_watershed(const float* dist, const int32_t* ML, const uint8_t* F, in
 // S10
 void launch_bwlabel(const uint8_t* split, int w, int h, int amin, int amax, Slot& sl,
                     int32_t* labels, int64_t lpitch, int32_t* n_objects, cudaStream_t s);
+// S8-S10 fused per F component (k_comp.cu)
+void launch_components(const uint8_t* F, const float* dist, float hh, int amin, int amax, int w, int h,
+                       Slot& sl, int32_t* labels, int64_t lpitch, int32_t* n_objects, cudaStream_t s);
 // S11
 void launch_features(const int32_t* labels, int64_t lpitch, const uint8_t* g, int w, int h,
                      Slot& sl, int32_t max_objects, int32_t* row_label, int32_t* row_flags,

@@ -410,7 +410,13 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_region_mr8, NW * 32, smem);
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        blocks = nsm * (per_sm > 0 ? per_sm : 1);
+        // One CTA per SM (measured, bench.py r1: 229 vs 193 tiles/s at 2 CTAs/SM): on hard tiles
+        // the reconstruction is latency-bound on chains of region jobs, so leaving half the
+        // SM resources free lets another slot's tile run beside it.
+        int want = 1;
+        if (const char* e = getenv("HP_RG_CTAS_PER_SM")) want = atoi(e);
+        want = std::max(1, std::min(want, per_sm > 0 ? per_sm : 1));
+        blocks = nsm * want;
     }
     int b = std::max(1, std::min(blocks, n));
     (note_launch(), k_region_mr8<<<b, NW * 32, smem, s>>>(mask, R, w, h, wl));
