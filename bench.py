@@ -37,6 +37,7 @@ STAGES = ["S1 colour deconvolution", "S2 RBC detection", "S3 morph open 19x19",
 # algorithmic floor bytes per pixel of each stage (read each input once,
 # write each output once, in the §8(a) layouts); DESIGN.md "Roofline" restates them.
 FLOOR_BPP = [5, 2, 2, 4, 2, 2, 5, 9, 10, 5, 5]
+FUSED_BPP = 13
 DTYPE = "u8/i32/f32"
 
 
@@ -303,13 +304,22 @@ def main():
     npx = size * size
     peak, peak_kind = peaks()
     per_stage = []
-    for k in range(11):
-        sms = stage_sum[k] / max(1, ntiles_timed)
-        gbs = FLOOR_BPP[k] * npx / (sms / 1e3) / 1e9 if sms > 0 else None
-        per_stage.append({"stage": STAGES[k], "ms": round(sms, 4), "alg_bytes_per_tile": FLOOR_BPP[k] * npx,
+    # default pipeline: S8-S11 run fused per F-component (k_comp.cu), timed as one stage;
+    # its floor = read F labels + dist + g, write labels (4 + 4 + 1 + 4 B/px)
+    fused = os.environ.get("HP_GLOBAL_S8S10", "0") != "1"
+    rows = [(STAGES[k], stage_sum[k], FLOOR_BPP[k]) for k in range(7)]
+    if fused:
+        rows.append(("S8-S11 fused per component (markers, watershed, BWLabel, features)",
+                     sum(stage_sum[7:11]), FUSED_BPP))
+    else:
+        rows += [(STAGES[k], stage_sum[k], FLOOR_BPP[k]) for k in range(7, 11)]
+    for name, tot, bpp in rows:
+        sms = tot / max(1, ntiles_timed)
+        gbs = bpp * npx / (sms / 1e3) / 1e9 if sms > 0 else None
+        per_stage.append({"stage": name, "ms": round(sms, 4), "alg_bytes_per_tile": bpp * npx,
                           "alg_GBps": None if gbs is None else round(gbs, 1),
                           "frac": None if gbs is None else round(gbs / peak, 4)})
-    dom = max(range(11), key=lambda k: per_stage[k]["ms"])
+    dom = max(range(len(per_stage)), key=lambda k: per_stage[k]["ms"])
     dstage = per_stage[dom]
     roofline = {"bound": "hbm", "kernel": dstage["stage"], "achieved": dstage["alg_GBps"],
                 "peak": peak, "unit": "GB/s",

@@ -20,7 +20,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-Xptxas", "-v"] + ARCH
-PER_FILE = {"k_feat.cu": ["-fmad=false"]}
+PER_FILE = {"k_feat.cu": ["-fmad=false"], "k_comp.cu": ["-fmad=false"]}
 
 
 def sources():

@@ -126,8 +126,12 @@ void ev(hp_ctx* ctx, Slot& sl, int k, cudaStream_t s) {
 }
 
 // S1..S10 on device buffers (the segmentation stage instance)
+// S1..S10; with `table` the fused per-component path also computes S11 into it and *fused
+// is set (the caller then skips the separate feature stage)
 hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, int64_t lpitch,
-                  int32_t* n_objects, cudaStream_t s) {
+                  int32_t* n_objects, cudaStream_t s, hp_feature_table* table = nullptr,
+                  bool* fused = nullptr) {
+    if (fused) *fused = false;
     const hp_params& p = ctx->cfg.params;
     const int w = rgb->width, h = rgb->height;
     ev(ctx, sl, 0, s);
@@ -171,11 +175,15 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
         ev(ctx, sl, 10, s);
     } else {
         // S8-S10 fused: one CTA per 8-component of F (timed under S8; S9/S10 read 0)
-        launch_components(sl.F, sl.dist, p.h, p.obj_min_area, p.obj_max_area, w, h, sl, labels, lpitch,
-                          n_objects, s);
+        launch_components(sl.F, sl.dist, sl.g, p.h, p.obj_min_area, p.obj_max_area, w, h, sl, labels, lpitch,
+                          n_objects, table, ctx->cfg.max_objects, s);
         ev(ctx, sl, 8, s);
         ev(ctx, sl, 9, s);
         ev(ctx, sl, 10, s);
+        if (table && fused) {
+            *fused = true;
+            ev(ctx, sl, 11, s);
+        }
     }
     return check_launch(ctx, "segment");
 }
@@ -323,7 +331,10 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.comp_bbox = (int4*)A(16 * (size_t)s.comp_cap);
         s.cid = (int32_t*)A(4 * N);
         s.counters = (unsigned long long*)A(8 * 4);
-        s.cnt32 = (int32_t*)A(4 * 8);
+        s.cnt32 = (int32_t*)A(4 * 16);
+        s.stg_label = (int32_t*)A(4 * (size_t)mo);
+        s.stg_flags = (int32_t*)A(4 * (size_t)mo);
+        s.stg_feat = (float*)A(4 * (size_t)mo * HP_NFEAT);
         s.rgb_dev = (uint8_t*)A(3 * N);
         s.lab_dev = (int32_t*)A(4 * N);
         s.tab_label = (int32_t*)A(4 * (size_t)mo);
@@ -336,7 +347,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.h_nrows = (int32_t*)halloc(16);
         void* all[] = {s.g, s.flags, s.rbc, s.u8a, s.u8b, s.cand, s.big0, s.F, s.split, s.pmask, s.lab, s.aux,
                        s.ML, s.d, s.L, s.dist, s.J, s.c, s.gcol, s.seg_top, s.seg_bot, s.wl.state, s.wl.inrows, s.wl.queue,
-                       s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.comp_root, s.comp_bbox, s.cid, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
+                       s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.comp_root, s.comp_bbox, s.cid, s.stg_label, s.stg_flags, s.stg_feat, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
                        s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows};
         for (void* p : all)
             if (!p) { hp_ctx_destroy(ctx); return HP_ERR_NOMEM; }
@@ -346,7 +357,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
             return HP_ERR_CUDA;
         }
         cudaMemset(s.counters, 0, 32);
-        cudaMemset(s.cnt32, 0, 32);
+        cudaMemset(s.cnt32, 0, 64);
         cudaMemset(s.wl.ctr, 0, 64);
     }
     if (cudaDeviceSynchronize() != cudaSuccess) { hp_ctx_destroy(ctx); return HP_ERR_CUDA; }
@@ -401,8 +412,9 @@ hp_status hp_process_tile(hp_ctx* ctx, int32_t slot, const hp_image* rgb, hp_lab
         return st;
     Slot& sl = ctx->slots[slot];
     cudaStream_t cs = (cudaStream_t)s;
-    st = segment(ctx, sl, rgb, lab->labels, lab->labels_pitch_elems, lab->n_objects_dev, cs);
-    if (st) return st;
+    bool fused = false;
+    st = segment(ctx, sl, rgb, lab->labels, lab->labels_pitch_elems, lab->n_objects_dev, cs, out, &fused);
+    if (st || fused) return st;
     return features(ctx, sl, rgb->width, rgb->height, lab->labels, lab->labels_pitch_elems, out, cs);
 }
 
@@ -631,8 +643,9 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
         cudaMemcpy2DAsync(sl.rgb_dev, 3 * (size_t)w, host, (size_t)pitch, 3 * (size_t)w, h, cudaMemcpyHostToDevice, s);
         hp_image im{sl.rgb_dev, w, h, 3LL * w};
         hp_feature_table tab{sl.tab_label, sl.tab_flags, sl.tab_feat, mo, sl.tab_nrows};
-        st = segment(ctx, sl, &im, sl.lab_dev, w, sl.cnt32 + 4, s);
-        if (!st) st = features(ctx, sl, w, h, sl.lab_dev, w, &tab, s);
+        bool fused = false;
+        st = segment(ctx, sl, &im, sl.lab_dev, w, sl.cnt32 + 4, s, &tab, &fused);
+        if (!st && !fused) st = features(ctx, sl, w, h, sl.lab_dev, w, &tab, s);
         if (st) return st;
         cudaMemcpyAsync(sl.h_nrows, sl.tab_nrows, 4, cudaMemcpyDeviceToHost, s);
         cudaMemcpyAsync(sl.h_label, sl.tab_label, 4 * (size_t)ctx->rows_copied, cudaMemcpyDeviceToHost, s);

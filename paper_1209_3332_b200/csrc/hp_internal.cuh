@@ -76,9 +76,12 @@ struct Slot {
     int4* comp_bbox;
     int32_t* cid;
     int32_t comp_cap;
+    // staging table of the fused S8-S11 path (rows in discovery order)
+    int32_t *stg_label, *stg_flags;
+    float* stg_feat;
     // small device counters: [0] bg count (u64), [1] any-bg flag, [2] n objects, ...
     unsigned long long* counters;
-    int32_t* cnt32;  // [0] n_obj raw, [1] edt pathological rows, [2..] misc
+    int32_t* cnt32;  // [1] edt any-bg, [2] features count, [4] run_tiles n_objects, [8..11] k_comp
     // run_tiles staging
     uint8_t* rgb_dev;
     int32_t* lab_dev;
@@ -161,8 +164,9 @@ void launch_watershed(const float* dist, const int32_t* ML, const uint8_t* F, in
 void launch_bwlabel(const uint8_t* split, int w, int h, int amin, int amax, Slot& sl,
                     int32_t* labels, int64_t lpitch, int32_t* n_objects, cudaStream_t s);
 // S8-S10 fused per F component (k_comp.cu)
-void launch_components(const uint8_t* F, const float* dist, float hh, int amin, int amax, int w, int h,
-                       Slot& sl, int32_t* labels, int64_t lpitch, int32_t* n_objects, cudaStream_t s);
+void launch_components(const uint8_t* F, const float* dist, const uint8_t* g, float hh, int amin, int amax,
+                       int w, int h, Slot& sl, int32_t* labels, int64_t lpitch, int32_t* n_objects,
+                       const hp_feature_table* table, int32_t max_objects, cudaStream_t s);
 // S11
 void launch_features(const int32_t* labels, int64_t lpitch, const uint8_t* g, int w, int h,
                      Slot& sl, int32_t max_objects, int32_t* row_label, int32_t* row_flags,

@@ -1,32 +1,30 @@
-// k_comp.cu -- S8 markers + S9 watershed + S10 BWLabel of the pipeline, one CTA per
-// 8-connected component of F (objects are a bag of independent tasks).
+// k_comp.cu -- S8 markers + S9 watershed + S10 BWLabel (+ S11 features) of the pipeline,
+// one CTA per 8-connected component of F (objects are a bag of tasks).
 //
-// Every step of S8-S10 (reading C12/C13) is a fixed point over the graph of
+// Every step of S8-S10 (readings C12/C13) is a fixed point over the graph of
 // N8 neighbours INSIDE F, so the 8-connected components of F are independent problems.  The
 // global path (k_ws.cu + the tile worklists of k_iwpp.cu, kept for hp_stage_run) pays ~25
 // launches and three device-wide worklists per tile for objects of ~100-1000 pixels; here one
-// CTA per component iterates each fixed point to convergence inside the component's
-// bounding box (the working set stays in L1/L2), using the same monotone update rules:
-//   J  = recon(dist - h, dist)           max-clamp relaxation           (h-maxima)
-//   zl = flat-zone label = min index      min propagation over equal-J   (RMAX zones)
-//   M  = zones with no higher neighbour;  ML = 1 + zone label
-//   c  = recon(dist on M else -inf, dist) max-clamp relaxation           (W1)
-//   d  = plateau distance                 min-plus relaxation            (W2)
-//   L  = min label over the parents       min relaxation                 (W3)
-//   split = F minus lines; objects = 8-components of split (min-index labels), area-filtered
-// Each relaxation is monotone and converges to the unique fixed point the oracle computes, in
-// any order; convergence is detected with __syncthreads_or.  Components of any size work
-// (large ones just iterate longer).
-#include <cfloat>
+// CTA owns one component:
+//   shared-memory paths -- one WARP per component for windows (bbox + 1-px ring) <= 640 px
+//     (~99% of nuclei; warp-synchronous, 16 components in flight per SM), one CTA for
+//     <= 3072 px: the window is staged in smem
+//     (membership, dist); the max-clamp / min-plus / min relaxations (J, W1, W2, W3) iterate
+//     to their fixed points with __syncthreads_or convergence; flat zones and the final
+//     objects are labelled by union-find in smem (CAS hooking, min-index roots); then the
+//     S11 features of each kept object are computed in the same CTA (feat_common.cuh);
+//   global fallback (bigger components): the same relaxations on the slot's global planes
+//     (any size), objects listed for k_obj_feat_list.
+// Rows from both paths land in a staging table and k_rows_scatter orders them by label.
+// Every relaxation is monotone toward a unique fixed point, so the result equals the oracle's.
 #include <climits>
-#include <cmath>
 
-#include "hp_internal.cuh"
+#include "feat_common.cuh"
 
 namespace hp {
 namespace {
 
-constexpr int kCT = 256;  // threads per component CTA (8 warps: warp = row, lane = column)
+constexpr int kCT = kFT;          // threads per component CTA (8 warps)
 
 #define GRID_LOOP(i, n) \
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
@@ -80,43 +78,391 @@ __global__ void k_comp_bbox(const int32_t* __restrict__ lab, const int32_t* __re
     }
 }
 
-// ---------------------------------------------------------------- per-component solver
 struct CompArgs {
     const uint8_t* F;
     const int32_t* labF;   // root (min index) of each F pixel's 8-component, -1 outside F
     const float* dist;
+    const uint8_t* g;      // for features
     float hh;
     int w, h;
-    float* J;
-    float* c;
-    int32_t* zl;           // flat-zone label, then split-object label
-    int32_t* d;
-    int32_t* L;
-    int32_t* aux;          // per-root flags / counters (roots are pixels of the component)
-    uint8_t* pm;           // parent bitmask
-    uint8_t* split;
+    int amin, amax;
     int32_t* labels;       // output (pitch lpitch), zeroed beforehand
     int64_t lpitch;
     int32_t* n_objects;
-    int amin, amax;
+    // staging table of rows (any order) and its counter
+    int32_t* rows_cnt;
+    int32_t rows_cap;
+    int32_t* row_label;
+    int32_t* row_flags;
+    float* row_feat;
+    int do_features;
+    // overflow: components too big for shared memory -> global path
+    int32_t* ovf_cnt;
+    int32_t* ovf_list;
+    // global-path planes
+    float *J, *c;
+    int32_t *zl, *d, *L, *aux;
+    uint8_t *pm, *split;
+    // objects of the global path that need features: (root, component id)
+    int32_t* gobj_cnt;
+    int2* gobj;
+    int32_t gobj_cap;
 };
 
-__global__ void __launch_bounds__(kCT) k_components(CompArgs a, const int32_t* __restrict__ cnt, int32_t cap,
-                                                    const int32_t* __restrict__ roots,
-                                                    const int4* __restrict__ bbox) {
+__device__ __forceinline__ int cfind(int* P, int x) {
+    volatile int* vp = P;
+    int p = vp[x];
+    while (p != x) {
+        x = p;
+        p = vp[x];
+    }
+    return x;
+}
+__device__ __forceinline__ void cunion(int* P, int a, int b) {
+    while (true) {
+        a = cfind(P, a);
+        b = cfind(P, b);
+        if (a == b) return;
+        if (a < b) {
+            int t = a;
+            a = b;
+            b = t;
+        }
+        if (atomicCAS(&P[a], a, b) == a) return;
+    }
+}
+
+__device__ __forceinline__ void write_row(const CompArgs& a, int32_t label, int border, const double* f) {
+    int slot = atomicAdd(a.rows_cnt, 1);
+    if (slot < a.rows_cap) {
+        a.row_label[slot] = label;
+        a.row_flags[slot] = border ? HP_OBJ_TOUCHES_BORDER : 0;
+        for (int k = 0; k < HP_NFEAT; ++k) a.row_feat[(int64_t)slot * HP_NFEAT + k] = (float)f[k];
+    }
+}
+
+// ---------------------------------------------------------------- shared-memory path
+// Per-team window storage (4-byte planes first for alignment); 19 B per window pixel.
+template <int CAP, int KO>
+struct CompSm {
+    float dist[CAP];
+    float A[CAP];      // J, then c
+    int32_t B[CAP];    // zone union-find, then L, then object union-find
+    int32_t C[CAP];    // zone flags, then d, then object areas
+    uint8_t mem[CAP];
+    uint8_t pm[CAP];
+    uint8_t sp[CAP];
+    int nobj;
+    int objroot[KO];
+    FeatSmem fs;
+};
+
+// Solve S8-S11 of one component in a team's shared memory.  Returns false (nothing written)
+// if the component must go to the global path instead.
+template <class Team, int CAP, int KO>
+__device__ bool comp_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, const CompArgs& a,
+                           int32_t root, int4 bb) {
+    const int w = a.w, h = a.h;
+    const int tr = team.rank();
+    constexpr int TS = Team::size;
+    const int wx0 = bb.x - 1, wy0 = bb.y - 1;
+    const int WX = bb.z - bb.x + 3, WY = bb.w - bb.y + 3;
+    const int NWIN = WX * WY;
+    const int nbo[8] = {-WX - 1, -WX, -WX + 1, -1, 1, WX - 1, WX, WX + 1};
+    auto gidx = [&](int li) -> int32_t {
+        int ly = li / WX, lx = li - ly * WX;
+        return (int32_t)((int64_t)(wy0 + ly) * w + (wx0 + lx));
+    };
+    // ---- stage the window (ring pixels are never members: no bounds checks later)
+    for (int li = tr; li < NWIN; li += TS) {
+        int ly = li / WX, lx = li - ly * WX;
+        int gx = wx0 + lx, gy = wy0 + ly;
+        uint8_t m = 0;
+        float dv = 0.f;
+        if (gx >= 0 && gy >= 0 && gx < w && gy < h) {
+            int64_t p = (int64_t)gy * w + gx;
+            if (a.labF[p] == root) {
+                m = 1;
+                dv = a.dist[p];
+            }
+        }
+        S.mem[li] = m;
+        S.dist[li] = dv;
+    }
+    if (tr == 0) S.nobj = 0;
+    team.sync();
+    auto each = [&](auto fn) {
+        for (int li = tr; li < NWIN; li += TS)
+            if (S.mem[li]) fn(li);
+    };
+    auto converge = [&](auto step) {
+        while (true) {
+            int ch = 0;
+            each([&](int li) { ch |= step(li) ? 1 : 0; });
+            if (!team.any(ch)) break;
+        }
+    };
+    // ---- S8: J = recon(dist - h, dist)
+    each([&](int li) { S.A[li] = fminf(__fsub_rn(S.dist[li], a.hh), S.dist[li]); });
+    team.sync();
+    converge([&](int li) -> bool {
+        float jp = S.A[li], b = jp;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (S.mem[li + nbo[j]]) b = fmaxf(b, S.A[li + nbo[j]]);
+        float nv = fminf(b, S.dist[li]);
+        if (nv > jp) { S.A[li] = nv; return true; }
+        return false;
+    });
+    // flat zones of J: union-find over N+ neighbours with equal J (min-index roots)
+    each([&](int li) { S.B[li] = li; });
+    team.sync();
+    each([&](int li) {
+        float jp = S.A[li];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // (-1,-1) (0,-1) (1,-1) (-1,0)
+            int q = li + nbo[j];
+            if (S.mem[q] && S.A[q] == jp) cunion(S.B, li, q);
+        }
+    });
+    team.sync();
+    each([&](int li) { S.C[li] = cfind(S.B, li); });
+    team.sync();
+    each([&](int li) { S.B[li] = S.C[li]; });
+    team.sync();
+    // RMAX: zone flag = some pixel of the zone has a higher neighbour
+    each([&](int li) { if (S.B[li] == li) S.C[li] = 0; });
+    team.sync();
+    each([&](int li) {
+        float jp = S.A[li];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            int q = li + nbo[j];
+            if (S.mem[q] && S.A[q] > jp) { S.C[S.B[li]] = 1; break; }
+        }
+    });
+    team.sync();
+    // ---- markers -> L initial (ML = 1 + global min index of the zone, else inf) and W1 init
+    each([&](int li) { S.pm[li] = S.C[S.B[li]] == 0; });  // staged: zone flags live at roots
+    team.sync();
+    each([&](int li) {
+        const int32_t ml = S.pm[li] ? gidx(S.B[li]) + 1 : kInfI;
+        S.B[li] = ml;
+        S.A[li] = ml != kInfI ? S.dist[li] : -INFINITY;
+    });
+    team.sync();
+    // ---- S9 W1: c = recon(dist on markers else -inf, dist)
+    converge([&](int li) -> bool {
+        float cp = S.A[li], b = cp;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if (S.mem[li + nbo[j]]) b = fmaxf(b, S.A[li + nbo[j]]);
+        float nv = fminf(b, S.dist[li]);
+        if (nv > cp) { S.A[li] = nv; return true; }
+        return false;
+    });
+    // ---- W2: plateau distance (markers: B != inf)
+    each([&](int li) {
+        int32_t v = kInfI;
+        if (S.B[li] != kInfI) {
+            v = 0;
+        } else {
+            float cp = S.A[li];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                int q = li + nbo[j];
+                if (S.mem[q] && S.A[q] > cp) { v = 1; break; }
+            }
+        }
+        S.C[li] = v;
+    });
+    team.sync();
+    converge([&](int li) -> bool {
+        int32_t dp = S.C[li];
+        if (dp <= 1) return false;
+        float cp = S.A[li];
+        int32_t b = dp;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            int q = li + nbo[j];
+            if (S.mem[q] && S.A[q] == cp) b = min(b, sat_add(S.C[q], 1));
+        }
+        if (b < dp) { S.C[li] = b; return true; }
+        return false;
+    });
+    // ---- parents: argmin over neighbours with c(q) >= c(p) of (-c(q), d(q))
+    each([&](int li) {
+        uint8_t bits = 0;
+        if (S.B[li] == kInfI) {
+            float cp = S.A[li];
+            bool have = false;
+            float bc = 0.f;
+            int32_t bd = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                int q = li + nbo[j];
+                if (!S.mem[q]) continue;
+                float cq = S.A[q];
+                if (!(cq >= cp)) continue;
+                int32_t dq = S.C[q];
+                if (!have || cq > bc || (cq == bc && dq < bd)) {
+                    have = true;
+                    bc = cq;
+                    bd = dq;
+                    bits = (uint8_t)(1u << j);
+                } else if (cq == bc && dq == bd) {
+                    bits |= (uint8_t)(1u << j);
+                }
+            }
+        }
+        S.pm[li] = bits;
+    });
+    team.sync();
+    // ---- W3: L = min over parents
+    converge([&](int li) -> bool {
+        int pmk = S.pm[li];
+        if (!pmk) return false;
+        int32_t lp = S.B[li], b = lp;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            if ((pmk >> j) & 1) b = min(b, S.B[li + nbo[j]]);
+        if (b < lp) { S.B[li] = b; return true; }
+        return false;
+    });
+    // ---- lines, split
+    each([&](int li) {
+        int32_t lp = S.B[li];
+        uint8_t v = 1;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            int q = li + nbo[j];
+            if (S.mem[q] && S.B[q] < lp) { v = 0; break; }
+        }
+        S.sp[li] = v;
+    });
+    team.sync();
+    // ---- S10: objects = 8-components of split (union-find), area filter
+    each([&](int li) { S.B[li] = li; });
+    team.sync();
+    each([&](int li) {
+        if (!S.sp[li]) return;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            int q = li + nbo[j];
+            if (S.mem[q] && S.sp[q]) cunion(S.B, li, q);
+        }
+    });
+    team.sync();
+    each([&](int li) { S.C[li] = S.sp[li] ? cfind(S.B, li) : -1; });
+    team.sync();
+    each([&](int li) { S.B[li] = S.C[li]; });  // object root (local) or -1
+    team.sync();
+    each([&](int li) { if (S.B[li] == li) S.C[li] = 0; });
+    team.sync();
+    each([&](int li) { if (S.B[li] >= 0) atomicAdd(&S.C[S.B[li]], 1); });
+    team.sync();
+    each([&](int li) {
+        if (S.B[li] == li && S.C[li] >= a.amin && S.C[li] <= a.amax) {
+            int k = atomicAdd(&S.nobj, 1);
+            if (k < KO) S.objroot[k] = li;
+        }
+    });
+    team.sync();
+    const int nobj = S.nobj;
+    if (nobj > KO) return false;  // too many objects for the list: global path instead
+    each([&](int li) {
+        int r = S.B[li];
+        int32_t v = 0;
+        if (r >= 0 && S.C[r] >= a.amin && S.C[r] <= a.amax) v = gidx(r) + 1;
+        int ly = li / WX, lx = li - ly * WX;
+        a.labels[(int64_t)(wy0 + ly) * a.lpitch + (wx0 + lx)] = v;
+    });
+    if (tr == 0 && nobj) atomicAdd(a.n_objects, nobj);
+    team.sync();
+    // ---- S11: features of each kept object
+    if (a.do_features) {
+        for (int k = 0; k < nobj; ++k) {
+            const int r = S.objroot[k];
+            auto inP = [&](int x, int y) -> bool {
+                int lx = x - wx0, ly = y - wy0;
+                if (lx < 0 || ly < 0 || lx >= WX || ly >= WY) return false;
+                const int li = ly * WX + lx;  // non-members hold stale values: test mem first
+                return S.mem[li] && S.B[li] == r;
+            };
+            double f[HP_NFEAT];
+            int border = 0;
+            object_features(team, inP, a.g, w, h, bb.x, bb.y, bb.z, bb.w, S.fs, red, f, &border);
+            if (tr == 0) write_row(a, gidx(r) + 1, border, f);
+            team.sync();
+        }
+    }
+    return true;
+}
+
+constexpr int kCapW = 640, kKoW = 48;    // warp path: windows up to 640 px (~99% of nuclei)
+constexpr int kCapC = 3072, kKoC = 192;  // CTA path
+constexpr int kWarpsPB = 4;
+
+__device__ __forceinline__ int win_px(int4 bb) { return (bb.z - bb.x + 3) * (bb.w - bb.y + 3); }
+
+__device__ __forceinline__ void to_global(const CompArgs& a, int ci) {
+    int k = atomicAdd(a.ovf_cnt, 1);
+    a.ovf_list[k] = ci;
+}
+
+__global__ void __launch_bounds__(kWarpsPB * 32, 4) k_comp_warp(CompArgs a, const int32_t* __restrict__ cnt,
+                                                               int32_t cap, const int32_t* __restrict__ roots,
+                                                               const int4* __restrict__ bbox) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto& S = reinterpret_cast<CompSm<kCapW, kKoW>*>(smem_raw)[warp];
+    TeamRed* unused = nullptr;  // warp reductions need no shared scratch
+    const TeamWarp team{lane};
     const int ncomp = min(*cnt, cap);
+    for (int ci = blockIdx.x * kWarpsPB + warp; ci < ncomp; ci += gridDim.x * kWarpsPB) {
+        const int4 bb = bbox[ci];
+        if (win_px(bb) > kCapW) continue;  // CTA or global path
+        if (!comp_solve(team, S, *unused, a, roots[ci], bb) && lane == 0) to_global(a, ci);
+        __syncwarp();
+    }
+}
+
+__global__ void __launch_bounds__(kCT, 2) k_comp_cta(CompArgs a, const int32_t* __restrict__ cnt, int32_t cap,
+                                                     const int32_t* __restrict__ roots,
+                                                     const int4* __restrict__ bbox) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto& S = *reinterpret_cast<CompSm<kCapC, kKoC>*>(smem_raw);
+    __shared__ TeamRed red;
+    const TeamCTA team;
+    const int ncomp = min(*cnt, cap);
+    for (int ci = blockIdx.x; ci < ncomp; ci += gridDim.x) {
+        const int4 bb = bbox[ci];
+        const int wp = win_px(bb);
+        if (wp <= kCapW) continue;  // warp path
+        if (wp > kCapC) {
+            if (threadIdx.x == 0) to_global(a, ci);
+            continue;
+        }
+        if (!comp_solve(team, S, red, a, roots[ci], bb) && threadIdx.x == 0) to_global(a, ci);
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- global fallback
+__global__ void __launch_bounds__(kCT) k_comp_global(CompArgs a, const int32_t* __restrict__ roots,
+                                                     const int4* __restrict__ bbox) {
+    const int ncomp = *a.ovf_cnt;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int w = a.w, h = a.h;
-    for (int ci = blockIdx.x; ci < ncomp; ci += gridDim.x) {
+    for (int oi = blockIdx.x; oi < ncomp; oi += gridDim.x) {
+        const int ci = a.ovf_list[oi];
         const int32_t root = roots[ci];
         const int4 bb = bbox[ci];
         const int bx0 = bb.x, by0 = bb.y, bx1 = bb.z, by1 = bb.w;
         auto mem = [&](int x, int y) -> bool {
             if (x < 0 || y < 0 || x >= w || y >= h) return false;
-            int64_t q = (int64_t)y * w + x;
-            return a.labF[q] == root;
+            return a.labF[(int64_t)y * w + x] == root;
         };
-        // iterate the component's pixels: warps over rows, lanes over columns
         auto each = [&](auto fn) {
             for (int y = by0 + warp; y <= by1; y += kCT / 32)
                 for (int x = bx0 + lane; x <= bx1; x += 32) {
@@ -124,7 +470,6 @@ __global__ void __launch_bounds__(kCT) k_components(CompArgs a, const int32_t* _
                     if (a.labF[p] == root) fn(x, y, p);
                 }
         };
-        // run `step` over all pixels until no pixel changes (CTA-wide)
         auto converge = [&](auto step) {
             while (true) {
                 int ch = 0;
@@ -132,30 +477,24 @@ __global__ void __launch_bounds__(kCT) k_components(CompArgs a, const int32_t* _
                 if (!__syncthreads_or(ch)) break;
             }
         };
-        // ---- S8: J = recon(dist - h, dist) restricted to the component
-        each([&](int x, int y, int64_t p) {
-            float dv = a.dist[p];
-            a.J[p] = fminf(__fsub_rn(dv, a.hh), dv);
-        });
+        each([&](int x, int y, int64_t p) { a.J[p] = fminf(__fsub_rn(a.dist[p], a.hh), a.dist[p]); });
         __syncthreads();
         converge([&](int x, int y, int64_t p) -> bool {
-            float jp = a.J[p], m = a.dist[p], b = jp;
+            float jp = a.J[p], b = jp;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 int qx = x + dx8(j), qy = y + dy8(j);
                 if (mem(qx, qy)) b = fmaxf(b, a.J[(int64_t)qy * w + qx]);
             }
-            float nv = fminf(b, m);
+            float nv = fminf(b, a.dist[p]);
             if (nv > jp) { a.J[p] = nv; return true; }
             return false;
         });
-        // flat zones of J (8-connected, equal J): min-index label propagation
         each([&](int x, int y, int64_t p) { a.zl[p] = (int32_t)p; });
         __syncthreads();
         converge([&](int x, int y, int64_t p) -> bool {
-            int32_t z = a.zl[p];
+            int32_t z = a.zl[p], b = z;
             float jp = a.J[p];
-            int32_t b = z;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 int qx = x + dx8(j), qy = y + dy8(j);
@@ -166,7 +505,6 @@ __global__ void __launch_bounds__(kCT) k_components(CompArgs a, const int32_t* _
             if (b < z) { a.zl[p] = b; return true; }
             return false;
         });
-        // RMAX: a zone is a regional maximum iff none of its pixels has a higher neighbour
         each([&](int x, int y, int64_t p) { if (a.zl[p] == (int32_t)p) a.aux[p] = 0; });
         __syncthreads();
         each([&](int x, int y, int64_t p) {
@@ -178,8 +516,6 @@ __global__ void __launch_bounds__(kCT) k_components(CompArgs a, const int32_t* _
             }
         });
         __syncthreads();
-        // ---- S9 W1: c = recon(dist on markers else -inf, dist); markers: ML = 1 + zone label
-        // (d holds ML temporarily)
         each([&](int x, int y, int64_t p) {
             int32_t z = a.zl[p];
             int32_t ml = a.aux[z] == 0 ? z + 1 : 0;
@@ -188,20 +524,18 @@ __global__ void __launch_bounds__(kCT) k_components(CompArgs a, const int32_t* _
         });
         __syncthreads();
         converge([&](int x, int y, int64_t p) -> bool {
-            float cp = a.c[p], m = a.dist[p], b = cp;
+            float cp = a.c[p], b = cp;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 int qx = x + dx8(j), qy = y + dy8(j);
                 if (mem(qx, qy)) b = fmaxf(b, a.c[(int64_t)qy * w + qx]);
             }
-            float nv = fminf(b, m);
+            float nv = fminf(b, a.dist[p]);
             if (nv > cp) { a.c[p] = nv; return true; }
             return false;
         });
-        // L initial (markers) before d overwrites ML
         each([&](int x, int y, int64_t p) { a.L[p] = a.d[p] ? a.d[p] : kInfI; });
         __syncthreads();
-        // ---- W2: d = 0 markers, 1 with a higher neighbour, else 1 + min equal-c neighbour
         each([&](int x, int y, int64_t p) {
             int32_t v = kInfI;
             if (a.L[p] != kInfI) {
@@ -232,7 +566,6 @@ __global__ void __launch_bounds__(kCT) k_components(CompArgs a, const int32_t* _
             if (b < dp) { a.d[p] = b; return true; }
             return false;
         });
-        // ---- parents: argmin over neighbours with c(q) >= c(p) of (-c(q), d(q))
         each([&](int x, int y, int64_t p) {
             uint8_t bits = 0;
             if (a.L[p] == kInfI) {
@@ -261,7 +594,6 @@ __global__ void __launch_bounds__(kCT) k_components(CompArgs a, const int32_t* _
             a.pm[p] = bits;
         });
         __syncthreads();
-        // ---- W3: L = min over parents, from +inf
         converge([&](int x, int y, int64_t p) -> bool {
             int pmk = a.pm[p];
             if (!pmk) return false;
@@ -272,7 +604,6 @@ __global__ void __launch_bounds__(kCT) k_components(CompArgs a, const int32_t* _
             if (b < lp) { a.L[p] = b; return true; }
             return false;
         });
-        // ---- lines, split
         each([&](int x, int y, int64_t p) {
             int32_t lp = a.L[p];
             uint8_t v = 1;
@@ -284,7 +615,6 @@ __global__ void __launch_bounds__(kCT) k_components(CompArgs a, const int32_t* _
             a.split[p] = v;
         });
         __syncthreads();
-        // ---- S10: 8-components of split inside this component, min-index labels
         each([&](int x, int y, int64_t p) { a.zl[p] = a.split[p] ? (int32_t)p : -1; });
         __syncthreads();
         converge([&](int x, int y, int64_t p) -> bool {
@@ -314,7 +644,11 @@ __global__ void __launch_bounds__(kCT) k_components(CompArgs a, const int32_t* _
                 int area = a.aux[z];
                 if (area >= a.amin && area <= a.amax) {
                     v = z + 1;
-                    if (z == (int32_t)p) atomicAdd(a.n_objects, 1);
+                    if (z == (int32_t)p) {
+                        atomicAdd(a.n_objects, 1);
+                        int k = atomicAdd(a.gobj_cnt, 1);
+                        if (k < a.gobj_cap) a.gobj[k] = make_int2(z, ci);
+                    }
                 }
             }
             a.labels[(int64_t)y * a.lpitch + x] = v;
@@ -323,26 +657,129 @@ __global__ void __launch_bounds__(kCT) k_components(CompArgs a, const int32_t* _
     }
 }
 
+// features of the objects produced by the global fallback (component bbox bounds the object)
+__global__ void __launch_bounds__(kFT, 2) k_obj_feat_list(CompArgs a, const int4* __restrict__ bbox) {
+    __shared__ FeatSmem fs;
+    __shared__ TeamRed red;
+    const TeamCTA team;
+    const int n = min(*a.gobj_cnt, a.gobj_cap);
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const int2 e = a.gobj[i];
+        const int32_t lab = e.x + 1;
+        const int4 bb = bbox[e.y];
+        auto inP = [&](int x, int y) {
+            return x >= 0 && y >= 0 && x < a.w && y < a.h && a.labels[(int64_t)y * a.lpitch + x] == lab;
+        };
+        double f[HP_NFEAT];
+        int border = 0;
+        object_features(team, inP, a.g, a.w, a.h, bb.x, bb.y, bb.z, bb.w, fs, red, f, &border);
+        if (threadIdx.x == 0) write_row(a, lab, border, f);
+        __syncthreads();
+    }
+}
+
+// order the staged rows by label (rank = number of smaller labels) into the output table
+__global__ void k_rows_scatter(const int32_t* __restrict__ cnt, int32_t cap, const int32_t* __restrict__ sl,
+                               const int32_t* __restrict__ sf, const float* __restrict__ sfeat,
+                               int32_t* __restrict__ ol, int32_t* __restrict__ of, float* __restrict__ ofeat,
+                               int32_t capacity) {
+    const int n = min(*cnt, cap);
+    __shared__ int32_t chunk[1024];
+    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
+        int i = base + threadIdx.x;
+        int32_t me = i < n ? sl[i] : 0;
+        int rk = 0;
+        for (int c0 = 0; c0 < n; c0 += 1024) {
+            __syncthreads();
+            for (int k = threadIdx.x; k < 1024 && c0 + k < n; k += blockDim.x) chunk[k] = sl[c0 + k];
+            __syncthreads();
+            int lim = min(1024, n - c0);
+            for (int k = 0; k < lim; ++k) rk += chunk[k] < me;
+        }
+        if (i < n && rk < capacity) {
+            ol[rk] = me;
+            of[rk] = sf[i];
+            for (int k = 0; k < HP_NFEAT; ++k) ofeat[(int64_t)rk * HP_NFEAT + k] = sfeat[(int64_t)i * HP_NFEAT + k];
+        }
+    }
+}
+
+__global__ void k_copy_i32(const int32_t* __restrict__ src, int32_t* __restrict__ dst) { *dst = *src; }
+
 }  // namespace
 
-// S8-S10 of the pipeline on F (u8) and dist (f32): labels (zeroed here) + n_objects.
-void launch_components(const uint8_t* F, const float* dist, float hh, int amin, int amax, int w, int h,
-                       Slot& sl, int32_t* labels, int64_t lpitch, int32_t* n_objects, cudaStream_t s) {
+// S8-S10 (+ S11 when table != nullptr) of the pipeline on F and dist: labels (zeroed here),
+// n_objects, and the feature rows in label order.
+void launch_components(const uint8_t* F, const float* dist, const uint8_t* g, float hh, int amin, int amax,
+                       int w, int h, Slot& sl, int32_t* labels, int64_t lpitch, int32_t* n_objects,
+                       const hp_feature_table* table, int32_t max_objects, cudaStream_t s) {
     const int64_t n = (int64_t)w * h;
     cudaMemsetAsync(n_objects, 0, sizeof(int32_t), s);
     cudaMemset2DAsync(labels, lpitch * sizeof(int32_t), 0, w * sizeof(int32_t), h, s);
-    if (n == 0) return;
+    int32_t* cnt = sl.cnt32 + 8;     // components
+    int32_t* ovf = sl.cnt32 + 9;     // overflow components
+    int32_t* rows = sl.cnt32 + 10;   // staged rows
+    int32_t* gobj = sl.cnt32 + 11;   // objects of the global path
+    cudaMemsetAsync(sl.cnt32 + 8, 0, 4 * sizeof(int32_t), s);
+    if (n == 0) {
+        if (table) cudaMemsetAsync(table->n_rows_dev, 0, sizeof(int32_t), s);
+        return;
+    }
     CclSrc cs{F, 0, false, nullptr};
     launch_ccl(cs, w, h, 8, sl.lab, nullptr, s);
-    int32_t* cnt = sl.cnt32 + 6;
-    cudaMemsetAsync(cnt, 0, sizeof(int32_t), s);
     const int32_t cap = sl.comp_cap;
     (note_launch(), k_comp_roots<<<grid_for(n), 256, 0, s>>>(sl.lab, n, cnt, sl.comp_root, cap, sl.cid));
     (note_launch(), k_comp_bbox_init<<<grid_for(cap), 256, 0, s>>>(cnt, cap, sl.comp_bbox));
     (note_launch(), k_comp_bbox<<<grid_for(n), 256, 0, s>>>(sl.lab, sl.cid, w, h, cap, sl.comp_bbox));
-    CompArgs a{F, sl.lab, dist, hh, w, h, sl.J, sl.c, sl.ML, sl.d, sl.L, sl.aux, sl.pmask, sl.split,
-               labels, lpitch, n_objects, amin, amax};
-    (note_launch(), k_components<<<148 * 8, kCT, 0, s>>>(a, cnt, cap, sl.comp_root, sl.comp_bbox));
+    CompArgs a{};
+    a.F = F;
+    a.labF = sl.lab;
+    a.dist = dist;
+    a.g = g;
+    a.hh = hh;
+    a.w = w;
+    a.h = h;
+    a.amin = amin;
+    a.amax = amax;
+    a.labels = labels;
+    a.lpitch = lpitch;
+    a.n_objects = n_objects;
+    a.rows_cnt = rows;
+    a.rows_cap = max_objects;
+    a.row_label = sl.stg_label;
+    a.row_flags = sl.stg_flags;
+    a.row_feat = sl.stg_feat;
+    a.do_features = table != nullptr;
+    a.ovf_cnt = ovf;
+    a.ovf_list = sl.cid;  // the root -> component map is no longer needed after k_comp_bbox
+    a.J = sl.J;
+    a.c = sl.c;
+    a.zl = sl.ML;
+    a.d = sl.d;
+    a.L = sl.L;
+    a.aux = sl.aux;
+    a.pm = sl.pmask;
+    a.split = sl.split;
+    a.gobj_cnt = gobj;
+    a.gobj = reinterpret_cast<int2*>(sl.obj_bbox);
+    a.gobj_cap = max_objects;
+    const size_t smw = kWarpsPB * sizeof(CompSm<kCapW, kKoW>), smc = sizeof(CompSm<kCapC, kKoC>);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_comp_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
+        cudaFuncSetAttribute(k_comp_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+        attr = true;
+    }
+    (note_launch(), k_comp_warp<<<148 * 4, kWarpsPB * 32, smw, s>>>(a, cnt, cap, sl.comp_root, sl.comp_bbox));
+    (note_launch(), k_comp_cta<<<148 * 2, kCT, smc, s>>>(a, cnt, cap, sl.comp_root, sl.comp_bbox));
+    (note_launch(), k_comp_global<<<148, kCT, 0, s>>>(a, sl.comp_root, sl.comp_bbox));
+    if (table) {
+        (note_launch(), k_obj_feat_list<<<148 * 2, kFT, 0, s>>>(a, sl.comp_bbox));
+        (note_launch(), k_rows_scatter<<<std::max(1, std::min(148 * 4, (max_objects + 255) / 256)), 256, 0, s>>>(
+            rows, max_objects, sl.stg_label, sl.stg_flags, sl.stg_feat, table->label, table->flags, table->feat,
+            table->capacity));
+        (note_launch(), k_copy_i32<<<1, 1, 0, s>>>(rows, table->n_rows_dev));
+    }
 }
 
 }  // namespace hp
