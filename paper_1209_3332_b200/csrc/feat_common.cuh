@@ -41,6 +41,23 @@ struct TeamCTA {
         __syncthreads();
         return r;
     }
+    // exclusive prefix sum over ranks (rank order)
+    __device__ __forceinline__ long long scan_excl(long long v, long long* red) const {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        long long inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            long long u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        __syncthreads();
+        if (lane == 31) red[warp] = inc;
+        __syncthreads();
+        long long off = 0;
+        for (int k = 0; k < warp; ++k) off += red[k];
+        __syncthreads();
+        return off + inc - v;
+    }
 };
 
 struct TeamWarp {
@@ -55,6 +72,15 @@ struct TeamWarp {
         for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_down_sync(0xffffffffu, v, o));
         return __shfl_sync(0xffffffffu, v, 0);
     }
+    __device__ __forceinline__ long long scan_excl(long long v, long long*) const {
+        long long inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            long long u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        return inc - v;
+    }
 };
 
 struct OpAdd {
@@ -62,10 +88,12 @@ struct OpAdd {
     __device__ __forceinline__ T operator()(T a, T b) const { return a + b; }
 };
 struct OpMin {
-    __device__ __forceinline__ int operator()(int a, int b) const { return a < b ? a : b; }
+    template <class T>
+    __device__ __forceinline__ T operator()(T a, T b) const { return a < b ? a : b; }
 };
 struct OpMax {
-    __device__ __forceinline__ int operator()(int a, int b) const { return a > b ? a : b; }
+    template <class T>
+    __device__ __forceinline__ T operator()(T a, T b) const { return a > b ? a : b; }
 };
 
 __device__ __forceinline__ int refl(int i, int n) {
@@ -95,18 +123,37 @@ __device__ void object_features(const Team& team, InP inP, const uint8_t* __rest
     const int tr = team.rank();
     constexpr int TS = Team::size;
     const int sw = bx1 - bx0 + 1, sh = by1 - by0 + 1;  // search box
-    const int64_t nb = (int64_t)sw * sh;
+    const int nb = sw * sh;
     int oxmin = INT_MAX, oymin = INT_MAX, oxmax = -1, oymax = -1;
         for (int i = tr; i < 256; i += TS) hist[i] = 0;
         for (int i = tr; i < 64; i += TS) glcm[i] = 0;
         team.sync();
-        auto G = [&](int x, int y) { return (int)g[(int64_t)refl(y, h) * w + refl(x, w)]; };
+        // Sobel magnitude at (x, y); REFLECT_101 only needed on the tile's outer ring
+        auto sobel = [&](int x, int y) -> float {
+            int t[9];
+            if (x > 0 && y > 0 && x < w - 1 && y < h - 1) {
+                const uint8_t* r0 = g + (int64_t)(y - 1) * w + (x - 1);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    t[3 * k] = r0[(int64_t)k * w];
+                    t[3 * k + 1] = r0[(int64_t)k * w + 1];
+                    t[3 * k + 2] = r0[(int64_t)k * w + 2];
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 9; ++k)
+                    t[k] = g[(int64_t)refl(y + k / 3 - 1, h) * w + refl(x + k % 3 - 1, w)];
+            }
+            int gx = (t[2] + 2 * t[5] + t[8]) - (t[0] + 2 * t[3] + t[6]);
+            int gy = (t[6] + 2 * t[7] + t[8]) - (t[0] + 2 * t[1] + t[2]);
+            return __fsqrt_rn((float)(gx * gx + gy * gy));
+        };
         long long A = 0, sx = 0, sy = 0, sxx = 0, syy = 0, sxy = 0, per = 0;
         int border = 0;
         double gs = 0.0;
         float gmin = INFINITY, gmax = -INFINITY;
-        for (int64_t k = tr; k < nb; k += TS) {
-            int y = by0 + (int)(k / sw), x = bx0 + (int)(k % sw);
+        for (int k = tr; k < nb; k += TS) {
+            int y = by0 + k / sw, x = bx0 + k % sw;
             if (!inP(x, y)) continue;
             ++A;
             oxmin = min(oxmin, x);
@@ -131,9 +178,7 @@ __device__ void object_features(const Team& team, InP inP, const uint8_t* __rest
                 atomicAdd(&glcm[i * 8 + j], 1u);
                 atomicAdd(&glcm[j * 8 + i], 1u);
             }
-            int gx = (G(x + 1, y - 1) + 2 * G(x + 1, y) + G(x + 1, y + 1)) - (G(x - 1, y - 1) + 2 * G(x - 1, y) + G(x - 1, y + 1));
-            int gy = (G(x - 1, y + 1) + 2 * G(x, y + 1) + G(x + 1, y + 1)) - (G(x - 1, y - 1) + 2 * G(x, y - 1) + G(x + 1, y - 1));
-            float m = __fsqrt_rn((float)(gx * gx + gy * gy));
+            const float m = sobel(x, y);
             gs += (double)m;
             gmin = fminf(gmin, m);
             gmax = fmaxf(gmax, m);
@@ -166,12 +211,10 @@ __device__ void object_features(const Team& team, InP inP, const uint8_t* __rest
         const double Ad = (double)A;
         const double gmean = gs / Ad;
         double g2 = 0.0, g3 = 0.0, g4 = 0.0;
-        for (int64_t k = tr; k < nb; k += TS) {
-            int y = by0 + (int)(k / sw), x = bx0 + (int)(k % sw);
+        for (int k = tr; k < nb; k += TS) {
+            int y = by0 + k / sw, x = bx0 + k % sw;
             if (!inP(x, y)) continue;
-            int gx = (G(x + 1, y - 1) + 2 * G(x + 1, y) + G(x + 1, y + 1)) - (G(x - 1, y - 1) + 2 * G(x - 1, y) + G(x - 1, y + 1));
-            int gy = (G(x - 1, y + 1) + 2 * G(x, y + 1) + G(x + 1, y + 1)) - (G(x - 1, y - 1) + 2 * G(x, y - 1) + G(x + 1, y - 1));
-            double dv = (double)__fsqrt_rn((float)(gx * gx + gy * gy)) - gmean;
+            double dv = (double)sobel(x, y) - gmean;
             double d2 = dv * dv;
             g2 += d2;
             g3 += d2 * dv;
@@ -180,6 +223,94 @@ __device__ void object_features(const Team& team, InP inP, const uint8_t* __rest
         g2 = team.reduce(g2, red.d, OpAdd());
         g3 = team.reduce(g3, red.d, OpAdd());
         g4 = team.reduce(g4, red.d, OpAdd());
+        // ---- intensity histogram: rank r owns bins [r*NB, r*NB + NB), NB = 256 / team size
+        constexpr int NB = 256 / TS;
+        long long s1 = 0, cnt = 0;
+        int vmin = 255, vmax = 0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+            const int v = tr * NB + q;
+            const unsigned int hv = hist[v];
+            if (hv) {
+                s1 += (long long)hv * v;
+                cnt += hv;
+                vmin = min(vmin, v);
+                vmax = max(vmax, v);
+            }
+        }
+        s1 = team.reduce(s1, red.l, OpAdd());
+        vmin = team.reduce(vmin, red.i, OpMin());
+        vmax = team.reduce(vmax, red.i, OpMax());
+        const double mean = (double)s1 / Ad;
+        double m2 = 0, m3 = 0, m4 = 0, ent = 0, en = 0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+            const int v = tr * NB + q;
+            if (!hist[v]) continue;
+            double dv = v - mean, hv = (double)hist[v];
+            m2 += hv * dv * dv;
+            m3 += hv * dv * dv * dv;
+            m4 += hv * dv * dv * dv * dv;
+            double pv = hv / Ad;
+            ent -= pv * log2(pv);
+            en += pv * pv;
+        }
+        m2 = team.reduce(m2, red.d, OpAdd()) / Ad;
+        m3 = team.reduce(m3, red.d, OpAdd()) / Ad;
+        m4 = team.reduce(m4, red.d, OpAdd()) / Ad;
+        ent = team.reduce(ent, red.d, OpAdd());
+        en = team.reduce(en, red.d, OpAdd());
+        // median: the lowest bin whose cumulative count reaches ceil(A / 2)
+        const long long half = (A + 1) / 2;
+        long long cum = team.scan_excl(cnt, red.l);
+        int med = 256;
+        if (cum < half && cum + cnt >= half) {
+#pragma unroll
+            for (int q = 0; q < NB; ++q) {
+                cum += hist[tr * NB + q];
+                if (cum >= half) { med = tr * NB + q; break; }
+            }
+        }
+        med = team.reduce(med, red.i, OpMin());
+        // ---- Haralick on the symmetric 8x8 GLCM: rank r owns entries r, r + TS, ... (< 64)
+        long long S = 0;
+        for (int k = tr; k < 64; k += TS) S += glcm[k];
+        S = team.reduce(S, red.l, OpAdd());
+        const double Sd = (double)S;
+        double mui = 0, muj = 0;
+        for (int k = tr; k < 64; k += TS) {
+            const double pij = (double)glcm[k] / Sd;
+            mui += (k >> 3) * pij;
+            muj += (k & 7) * pij;
+        }
+        mui = team.reduce(mui, red.d, OpAdd());
+        muj = team.reduce(muj, red.d, OpAdd());
+        double si = 0, sj = 0, asm_ = 0, con = 0, cor = 0, hom = 0, gent = 0, shade = 0, prom = 0, pmax = 0;
+        for (int k = tr; k < 64; k += TS) {
+            const int i = k >> 3, j = k & 7;
+            const double pij = (double)glcm[k] / Sd;
+            si += (i - mui) * (i - mui) * pij;
+            sj += (j - muj) * (j - muj) * pij;
+            asm_ += pij * pij;
+            con += (double)((i - j) * (i - j)) * pij;
+            cor += (i - mui) * (j - muj) * pij;
+            hom += pij / (1.0 + (double)((i - j) * (i - j)));
+            if (pij > 0) gent -= pij * log2(pij);
+            double t = i + j - mui - muj;
+            shade += t * t * t * pij;
+            prom += t * t * t * t * pij;
+            pmax = fmax(pmax, pij);
+        }
+        si = sqrt(team.reduce(si, red.d, OpAdd()));
+        sj = sqrt(team.reduce(sj, red.d, OpAdd()));
+        asm_ = team.reduce(asm_, red.d, OpAdd());
+        con = team.reduce(con, red.d, OpAdd());
+        cor = team.reduce(cor, red.d, OpAdd());
+        hom = team.reduce(hom, red.d, OpAdd());
+        gent = team.reduce(gent, red.d, OpAdd());
+        shade = team.reduce(shade, red.d, OpAdd());
+        prom = team.reduce(prom, red.d, OpAdd());
+        pmax = team.reduce(pmax, red.d, OpMax());
         if (tr == 0) {
             const double PI = 3.14159265358979323846;
             // shape
@@ -205,35 +336,7 @@ __device__ void object_features(const Team& team, InP inP, const uint8_t* __rest
             f[HP_F_EQDIAM] = sqrt(4.0 * Ad / PI);
             f[HP_F_COMPACTNESS] = 4.0 * PI * Ad / ((double)per * (double)per);
             f[HP_F_EXTENT] = Ad / (bwd * bhd);
-            // intensity (histogram, ascending bins)
-            long long s1 = 0;
-            int vmin = 255, vmax = 0;
-            for (int v = 0; v < 256; ++v)
-                if (hist[v]) {
-                    s1 += (long long)hist[v] * v;
-                    vmin = min(vmin, v);
-                    vmax = max(vmax, v);
-                }
-            double mean = (double)s1 / Ad, m2 = 0, m3 = 0, m4 = 0, ent = 0, en = 0;
-            for (int v = 0; v < 256; ++v) {
-                if (!hist[v]) continue;
-                double dv = v - mean, hv = (double)hist[v];
-                m2 += hv * dv * dv;
-                m3 += hv * dv * dv * dv;
-                m4 += hv * dv * dv * dv * dv;
-                double pv = hv / Ad;
-                ent -= pv * log2(pv);
-                en += pv * pv;
-            }
-            m2 /= Ad;
-            m3 /= Ad;
-            m4 /= Ad;
-            long long half = (A + 1) / 2, cum = 0;
-            int med = 0;
-            for (int v = 0; v < 256; ++v) {
-                cum += hist[v];
-                if (cum >= half) { med = v; break; }
-            }
+            // intensity
             bool flat = vmin == vmax;
             f[HP_F_INT_MEAN] = mean;
             f[HP_F_INT_STD] = flat ? 0.0 : sqrt(m2);
@@ -251,41 +354,10 @@ __device__ void object_features(const Team& team, InP inP, const uint8_t* __rest
             f[HP_F_GRAD_STD] = gflat ? 0.0 : sqrt(gg2);
             f[HP_F_GRAD_SKEW] = gflat ? 0.0 : gg3 / (gg2 * sqrt(gg2));
             f[HP_F_GRAD_KURT] = gflat ? 0.0 : gg4 / (gg2 * gg2);
-            // Haralick on the symmetric 8x8 GLCM
-            long long S = 0;
-            for (int i = 0; i < 64; ++i) S += glcm[i];
+            // Haralick
             if (S == 0) {
                 for (int k = HP_F_GLCM_ASM; k <= HP_F_GLCM_MAXPROB; ++k) f[k] = 0.0;
             } else {
-                double Pm[64], mui = 0, muj = 0;
-                for (int i = 0; i < 8; ++i)
-                    for (int j = 0; j < 8; ++j) {
-                        Pm[i * 8 + j] = (double)glcm[i * 8 + j] / (double)S;
-                        mui += i * Pm[i * 8 + j];
-                        muj += j * Pm[i * 8 + j];
-                    }
-                double si = 0, sj = 0;
-                for (int i = 0; i < 8; ++i)
-                    for (int j = 0; j < 8; ++j) {
-                        si += (i - mui) * (i - mui) * Pm[i * 8 + j];
-                        sj += (j - muj) * (j - muj) * Pm[i * 8 + j];
-                    }
-                si = sqrt(si);
-                sj = sqrt(sj);
-                double asm_ = 0, con = 0, cor = 0, hom = 0, gent = 0, shade = 0, prom = 0, pmax = 0;
-                for (int i = 0; i < 8; ++i)
-                    for (int j = 0; j < 8; ++j) {
-                        double pij = Pm[i * 8 + j];
-                        asm_ += pij * pij;
-                        con += (double)((i - j) * (i - j)) * pij;
-                        cor += (i - mui) * (j - muj) * pij;
-                        hom += pij / (1.0 + (double)((i - j) * (i - j)));
-                        if (pij > 0) gent -= pij * log2(pij);
-                        double t = i + j - mui - muj;
-                        shade += t * t * t * pij;
-                        prom += t * t * t * t * pij;
-                        pmax = fmax(pmax, pij);
-                    }
                 f[HP_F_GLCM_ASM] = asm_;
                 f[HP_F_GLCM_CONTRAST] = con;
                 f[HP_F_GLCM_CORRELATION] = (si * sj == 0.0) ? 1.0 : cor / (si * sj);
