@@ -104,8 +104,8 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t* plane, int w, int h
 struct Smem {
     uint32_t R[ROWS * RWW];
     uint32_t M[ROWS * RWW];
-    uint32_t dirty[NW];
-    uint32_t chg[NW];
+    uint32_t dirty[NW];  // rows of each sub-tile that may still improve (pushed by neighbours)
+    int pend;            // sub-tiles with dirty != 0 plus sub-tiles being processed
     int job;
     int again;
     unsigned long long t0;
@@ -237,11 +237,30 @@ __global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __rest
                         S.R[r * RWW + wi] = load_word(R, w, h, X0 - 4 + 4 * wi, Y0 - 1 + r);
                     }
                 }
+                if (threadIdx.x == 0) {
+                    int np = 0;
+                    for (int k = 0; k < NW; ++k) np += S.dirty[k] != 0;
+                    S.pend = np;
+                }
                 __syncthreads();
-                uint32_t dirty = S.dirty[warp];
+                // Asynchronous sub-tile warps: a warp takes its own dirty rows, sweeps them to a
+                // fixed point, then pushes the rows of in-region neighbour sub-tiles its changed
+                // border pixels can improve.  Token count: a 0 -> nonzero transition of a dirty
+                // mask adds one to pend, a warp releases the token it took after its pushes, so
+                // pend == 0 iff no sub-tile of the region has work left.
                 int iters = 0;
                 int nrows = 0;
+                const int c = wc0 + lane + 1, r = wr0 + lane + 1;
                 while (true) {
+                    uint32_t dirty = 0;
+                    if (lane == 0 && *reinterpret_cast<volatile uint32_t*>(&S.dirty[warp]))
+                        dirty = atomicExch(&S.dirty[warp], 0u);
+                    dirty = __shfl_sync(FULL, dirty, 0);
+                    if (!dirty) {
+                        if (*reinterpret_cast<volatile int*>(&S.pend) == 0) break;
+                        __nanosleep(20);
+                        continue;
+                    }
                     // Gauss-Seidel sweeps of this sub-tile (see iwpp_rules.cuh sweep_rows)
                     uint32_t chg = 0;
                     while (dirty) {
@@ -261,40 +280,56 @@ __global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __rest
                             if (row(y)) { chg |= bit; dirty |= (bit << 1) | (bit >> 1); }
                         }
                     }
-                    mychg |= chg;
-                    if (lane == 0) S.chg[warp] = chg;
                     ++iters;
-                    __syncthreads();
-                    // rows of this sub-tile that a changed in-region neighbour can improve
-                    uint32_t nd = 0;
-                    const int c = wc0 + lane + 1, r = wr0 + lane + 1;
-                    if (sy > 0 && (S.chg[warp - RX] | S.chg[warp - RX - (sx > 0)] | S.chg[warp - RX + (sx < RX - 1)])) {
-                        bool f = improves(wr0, c - 1, wr0 + 1, c) || improves(wr0, c, wr0 + 1, c) ||
-                                 improves(wr0, c + 1, wr0 + 1, c);
-                        if (__any_sync(FULL, f)) nd |= 1u;
+                    mychg |= chg;
+                    if (chg) {
+                        // rows of in-region neighbours that changed border pixels can improve
+                        // (m8 index = N8 direction of the neighbour, bit = its row)
+                        uint32_t m8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                        constexpr uint32_t TOP = 1u << 31, BOT = 1u;
+                        const bool mine_row = (chg >> lane) & 1;
+#pragma unroll
+                        for (int d = -1; d <= 1; ++d) {
+                            if (sy > 0 && (chg & 1) && improves(wr0 + 1, c, wr0, c + d)) {
+                                if (c + d == wc0) { if (sx > 0) m8[0] |= TOP; }
+                                else if (c + d == wc0 + kTile + 1) { if (sx < RX - 1) m8[2] |= TOP; }
+                                else m8[1] |= TOP;
+                            }
+                            if (sy < RY - 1 && (chg >> 31) && improves(wr0 + kTile, c, wr0 + kTile + 1, c + d)) {
+                                if (c + d == wc0) { if (sx > 0) m8[5] |= BOT; }
+                                else if (c + d == wc0 + kTile + 1) { if (sx < RX - 1) m8[7] |= BOT; }
+                                else m8[6] |= BOT;
+                            }
+                            if (sx > 0 && mine_row && improves(r, wc0 + 1, r + d, wc0)) {
+                                if (r + d == wr0) { if (sy > 0) m8[0] |= TOP; }
+                                else if (r + d == wr0 + kTile + 1) { if (sy < RY - 1) m8[5] |= BOT; }
+                                else m8[3] |= 1u << (lane + d);
+                            }
+                            if (sx < RX - 1 && mine_row && improves(r, wc0 + kTile, r + d, wc0 + kTile + 1)) {
+                                if (r + d == wr0) { if (sy > 0) m8[2] |= TOP; }
+                                else if (r + d == wr0 + kTile + 1) { if (sy < RY - 1) m8[7] |= BOT; }
+                                else m8[4] |= 1u << (lane + d);
+                            }
+                        }
+                        uint32_t mine = 0;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            uint32_t v = __reduce_or_sync(FULL, m8[j]);
+                            if (lane == j) mine = v;
+                        }
+                        if (lane < 8 && mine) {
+                            const int nw = (sy + dy8(lane)) * RX + (sx + dx8(lane));
+                            if (atomicOr(&S.dirty[nw], mine) == 0u) atomicAdd(&S.pend, 1);
+                        }
                     }
-                    if (sy < RY - 1 && (S.chg[warp + RX] | S.chg[warp + RX - (sx > 0)] | S.chg[warp + RX + (sx < RX - 1)])) {
-                        const int br = wr0 + kTile;
-                        bool f = improves(br + 1, c - 1, br, c) || improves(br + 1, c, br, c) ||
-                                 improves(br + 1, c + 1, br, c);
-                        if (__any_sync(FULL, f)) nd |= 1u << 31;
+                    __syncwarp();
+                    if (lane == 0) {
+                        __threadfence_block();
+                        atomicSub(&S.pend, 1);
                     }
-                    if (sx > 0 && (S.chg[warp - 1] | (sy > 0 ? S.chg[warp - 1 - RX] : 0u) | (sy < RY - 1 ? S.chg[warp - 1 + RX] : 0u))) {
-                        bool f = improves(r - 1, wc0, r, wc0 + 1) || improves(r, wc0, r, wc0 + 1) ||
-                                 improves(r + 1, wc0, r, wc0 + 1);
-                        nd |= __ballot_sync(FULL, f);
-                    }
-                    if (sx < RX - 1 && (S.chg[warp + 1] | (sy > 0 ? S.chg[warp + 1 - RX] : 0u) | (sy < RY - 1 ? S.chg[warp + 1 + RX] : 0u))) {
-                        const int bc = wc0 + kTile;
-                        bool f = improves(r - 1, bc + 1, r, bc) || improves(r, bc + 1, r, bc) ||
-                                 improves(r + 1, bc + 1, r, bc);
-                        nd |= __ballot_sync(FULL, f);
-                    }
-                    dirty = nd;
-                    const int more = __syncthreads_or(nd != 0);
-                    if (!more) break;
                 }
-                if (threadIdx.x == 0) atomicAdd(&wl.ctr[4], (unsigned long long)iters);
+                __syncthreads();
+                if (lane == 0) atomicAdd(&wl.ctr[4], (unsigned long long)iters);  // sub-tile sweep sets
                 if (lane == 0) atomicAdd(&wl.ctr[6], (unsigned long long)nrows);
                 // write back the changed rows of this sub-tile (interior words)
                 if (mychg) {
