@@ -184,8 +184,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hp", choices=["hp", "reference"])
-    ap.add_argument("--batch", type=int, default=8, help="distinct 4K tiles per GPU per step")
-    ap.add_argument("--slots", type=int, default=2, help="tiles in flight per GPU (n_slots)")
+    ap.add_argument("--batch", type=int, default=12, help="distinct 4K tiles per GPU per step")
+    ap.add_argument("--slots", type=int, default=6, help="tiles in flight per GPU (n_slots)")
     ap.add_argument("--size", type=int, default=4096)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -34,7 +34,11 @@ def _stale(obj, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Build libhp.so; a named variant (extra -D defines, for experiments) builds into
+    _build_<variant>/ and libhp_<variant>.so (select it at run time with HP_SO=...)."""
+    BUILD = globals()["BUILD"] + (f"_{variant}" if variant else "")
+    SO = os.path.join(HERE, f"libhp_{variant}.so") if variant else globals()["SO"]
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(HERE, "..", "include", "hp.h"))
@@ -43,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         src = os.path.join(CSRC, f)
         obj = os.path.join(BUILD, f.replace(".cu", ".o"))
         if force or _stale(obj, [src] + headers):
-            cmd = [NVCC, "-c", src, "-o", obj] + COMMON + PER_FILE.get(f, [])
+            cmd = [NVCC, "-c", src, "-o", obj] + COMMON + PER_FILE.get(f, []) + list(defines)
             jobs.append((f, cmd))
     logs = {}
 
@@ -73,4 +77,6 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    var = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")]
+    defs = [a for a in sys.argv if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose=True, variant=var[0] if var else "", defines=defs))

@@ -2,16 +2,16 @@
 // (S4 ReconToNuclei; HP_STAGE_IWPP_RAW).
 //
 // Measured (tools/diag_iwpp.py, r1): with one warp per 32x32 tile job, the reconstruction of
-// some tiles is dominated by long sequential chains of tile jobs (same job count, 2.5 ms vs
-// 19 ms), i.e. by the cost of one hop through the global queue.  Here one CTA of RX*RY warps
-// owns a region of RX x RY tiles (128 x 128 px): the region window (plus halo) lives in
-// shared memory as bytes; each warp closes its own 32x32 sub-tile with the row-scan sweeps
-// of iwpp_rules.cuh (reading its neighbours' pixels live), then the CTA barriers, each warp
-// derives the rows its neighbour sub-tiles can still improve, and the CTA iterates until the
-// region is stable.  A chain hop inside a region costs a barrier instead of a queue round
-// trip, and regions are 16x fewer than tiles.  Between regions: the asynchronous worklist of
-// k_iwpp.cu (ticket queue, IDLE/QUEUED/BUSY/BUSY_DIRTY states, per-sub-tile incoming rows).
-// Every update is a valid monotone propagation: the fixed point equals the oracle's.
+// some tiles is dominated by long sequential chains of tile jobs, i.e. by the cost of one hop
+// through the global queue.  Here one CTA of RX*RY warps owns a region of RX x RY sub-tiles
+// (128 x 128 px): the region window (plus halo) lives in shared memory as bytes; each warp
+// closes its own 32x32 sub-tile with row-scan sweeps (reading its neighbours' pixels live),
+// then pushes the rows of neighbouring sub-tiles its changed border pixels can improve into
+// their shared-memory dirty masks.  The warps run asynchronously (no CTA barrier per
+// iteration); a token count of dirty masks plus in-flight sweeps detects the region's fixed
+// point.  Between regions: the asynchronous worklist (ticket queue, IDLE/QUEUED/BUSY/
+// BUSY_DIRTY states, per-sub-tile incoming rows).  Every update is a valid monotone
+// propagation: the fixed point equals the oracle's.
 #include <cstdlib>
 
 #include "hp_internal.cuh"
@@ -22,7 +22,17 @@ namespace {
 constexpr uint32_t ST_IDLE = 0, ST_QUEUED = 1, ST_BUSY = 2, ST_DIRTY = 3;
 constexpr int32_t EMPTY = -1;
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int RX = 4, RY = 4, NW = RX * RY;
+#ifndef HP_RX
+// 128 x 128 px regions.  Measured (r1, config-2 tiles): 8x4 sub-tiles close one tile faster
+// alone (0.91 vs 1.04 ms) but a 1024-thread CTA fills the SM's register file, so tiles of the
+// other slots cannot co-run: 301 vs 395 tiles/s in bench.py at 4 slots.
+#define HP_RX 4
+#define HP_RY 4
+#endif
+#ifndef HP_POLL_NS
+#define HP_POLL_NS 400  // idle sub-tile warps back off (frees issue slots for co-running work)
+#endif
+constexpr int RX = HP_RX, RY = HP_RY, NW = RX * RY;
 constexpr int RWW = RX * 8 + 2;      // window words per row: bytes [X0-4, X0+128+4)
 constexpr int RWB = RWW * 4;         // window bytes per row
 constexpr int ROWS = RY * kTile + 2; // window rows
@@ -120,7 +130,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // byte of window pixel (wr, wc): window column wc (0 .. RX*32+1) is byte wc + 3
 __device__ __forceinline__ int bidx(int wr, int wc) { return wr * RWB + wc + 3; }
 
-__global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __restrict__ mask,
+__global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : 2) k_region_mr8(const uint8_t* __restrict__ mask,
                                                            uint8_t* __restrict__ R, int w, int h,
                                                            Worklist wl) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -145,7 +155,13 @@ __global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __rest
         if (lane == 0) b = max(b, lft);
         if (lane == 31) b = max(b, rgt);
         int lo = min(b, m);
-        int u = max(clamp_scan<true>(lo, m, lane), clamp_scan<false>(lo, m, lane));
+        // the clamp scans are only needed if some pixel can take a horizontal neighbour's value
+        int nl = __shfl_up_sync(FULL, lo, 1), nr = __shfl_down_sync(FULL, lo, 1);
+        if (lane == 0) nl = 0;
+        if (lane == 31) nr = 0;
+        int u = lo;
+        if (__any_sync(FULL, min(max(nl, nr), m) > lo))
+            u = max(clamp_scan<true>(lo, m, lane), clamp_scan<false>(lo, m, lane));
         __syncwarp();
         if (u != rr) sRw[bidx(wr, wc)] = (uint8_t)u;
         __syncwarp();
@@ -258,7 +274,7 @@ __global__ void __launch_bounds__(NW * 32, 2) k_region_mr8(const uint8_t* __rest
                     dirty = __shfl_sync(FULL, dirty, 0);
                     if (!dirty) {
                         if (*reinterpret_cast<volatile int*>(&S.pend) == 0) break;
-                        __nanosleep(20);
+                        __nanosleep(HP_POLL_NS);
                         continue;
                     }
                     // Gauss-Seidel sweeps of this sub-tile (see iwpp_rules.cuh sweep_rows)
