@@ -23,8 +23,10 @@ struct TeamRed {
     int i[kFT / 32];
 };
 
+template <int NT = kFT>
 struct TeamCTA {
-    static constexpr int size = kFT;
+    static_assert(NT % 32 == 0 && NT <= kFT, "TeamRed holds one slot per warp of kFT threads");
+    static constexpr int size = NT;
     __device__ __forceinline__ int rank() const { return threadIdx.x; }
     __device__ __forceinline__ void sync() const { __syncthreads(); }
     __device__ __forceinline__ int any(int b) const { return __syncthreads_or(b); }
@@ -37,7 +39,7 @@ struct TeamCTA {
         if (lane == 0) red[warp] = v;
         __syncthreads();
         T r = red[0];
-        for (int k = 1; k < kFT / 32; ++k) r = op(r, red[k]);
+        for (int k = 1; k < NT / 32; ++k) r = op(r, red[k]);
         __syncthreads();
         return r;
     }

@@ -74,6 +74,7 @@ struct Slot {
     // F components (k_comp.cu): root list, bounding boxes, root -> component id plane
     int32_t* comp_root;
     int4* comp_bbox;
+    int32_t* comp_big;  // components whose window needs a whole block (k_comp.cu)
     int32_t* cid;
     int32_t comp_cap;
     // staging table of the fused S8-S11 path (rows in discovery order)

@@ -6,9 +6,9 @@
 // global path (k_ws.cu + the tile worklists of k_iwpp.cu, kept for hp_stage_run) pays ~25
 // launches and three device-wide worklists per tile for objects of ~100-1000 pixels; here one
 // CTA owns one component:
-//   shared-memory paths -- one WARP per component for windows (bbox + 1-px ring) <= 640 px
-//     (~99% of nuclei; warp-synchronous, 16 components in flight per SM), one CTA for
-//     <= 3072 px: the window is staged in smem
+//   shared-memory path (k_comp_fused) -- one WARP per component for windows (bbox + 1-px
+//     ring) <= 640 px (~99% of nuclei; warp-synchronous, 16 components in flight per SM), one
+//     4-warp block for <= 2560 px: the window is staged in smem
 //     (membership, dist); the max-clamp / min-plus / min relaxations (J, W1, W2, W3) iterate
 //     to their fixed points with __syncthreads_or convergence; flat zones and the final
 //     objects are labelled by union-find in smem (CAS hooking, min-index roots); then the
@@ -399,9 +399,10 @@ __device__ bool comp_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, c
     return true;
 }
 
-constexpr int kCapW = 640, kKoW = 48;    // warp path: windows up to 640 px (~99% of nuclei)
-constexpr int kCapC = 3072, kKoC = 192;  // CTA path
+constexpr int kCapW = 640, kKoW = 48;    // warp team: windows up to 640 px (~99% of nuclei)
 constexpr int kWarpsPB = 4;
+constexpr int kCapB = 2560, kKoB = 160;  // block team (4 warps): the same shared memory, one window
+static_assert(sizeof(CompSm<kCapB, kKoB>) <= kWarpsPB * sizeof(CompSm<kCapW, kKoW>), "block window too big");
 
 __device__ __forceinline__ int win_px(int4 bb) { return (bb.z - bb.x + 3) * (bb.w - bb.y + 3); }
 
@@ -410,41 +411,60 @@ __device__ __forceinline__ void to_global(const CompArgs& a, int ci) {
     a.ovf_list[k] = ci;
 }
 
-__global__ void __launch_bounds__(kWarpsPB * 32, 4) k_comp_warp(CompArgs a, const int32_t* __restrict__ cnt,
-                                                               int32_t cap, const int32_t* __restrict__ roots,
-                                                               const int4* __restrict__ bbox) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    auto& S = reinterpret_cast<CompSm<kCapW, kKoW>*>(smem_raw)[warp];
-    TeamRed* unused = nullptr;  // warp reductions need no shared scratch
-    const TeamWarp team{lane};
-    const int ncomp = min(*cnt, cap);
-    for (int ci = blockIdx.x * kWarpsPB + warp; ci < ncomp; ci += gridDim.x * kWarpsPB) {
-        const int4 bb = bbox[ci];
-        if (win_px(bb) > kCapW) continue;  // CTA or global path
-        if (!comp_solve(team, S, *unused, a, roots[ci], bb) && lane == 0) to_global(a, ci);
-        __syncwarp();
+// windows > kCapW go to the block list, windows > kCapB straight to the global path
+__global__ void k_comp_classify(CompArgs a, const int32_t* __restrict__ cnt, int32_t cap,
+                                const int4* __restrict__ bbox, int32_t* __restrict__ big, int32_t* __restrict__ nbig) {
+    const int n = min(*cnt, cap);
+    GRID_LOOP(ci, (int64_t)n) {
+        const int wp = win_px(bbox[ci]);
+        if (wp > kCapB) to_global(a, (int)ci);
+        else if (wp > kCapW) big[atomicAdd(nbig, 1)] = (int)ci;
     }
 }
 
-__global__ void __launch_bounds__(kCT, 2) k_comp_cta(CompArgs a, const int32_t* __restrict__ cnt, int32_t cap,
-                                                     const int32_t* __restrict__ roots,
-                                                     const int4* __restrict__ bbox) {
+// One launch for every shared-memory component: each block first takes big components off
+// the block list (whole-block team), then its warps take small components one at a time off
+// the component list (warp teams) -- dynamic queues, so the few big windows run beside the
+// many small ones instead of as a serial tail.
+__global__ void __launch_bounds__(kWarpsPB * 32, 4) k_comp_fused(CompArgs a, const int32_t* __restrict__ cnt,
+                                                                int32_t cap, const int32_t* __restrict__ roots,
+                                                                const int4* __restrict__ bbox,
+                                                                const int32_t* __restrict__ big,
+                                                                const int32_t* __restrict__ nbig_p,
+                                                                int32_t* __restrict__ heads) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    auto& S = *reinterpret_cast<CompSm<kCapC, kKoC>*>(smem_raw);
     __shared__ TeamRed red;
-    const TeamCTA team;
-    const int ncomp = min(*cnt, cap);
-    for (int ci = blockIdx.x; ci < ncomp; ci += gridDim.x) {
-        const int4 bb = bbox[ci];
-        const int wp = win_px(bb);
-        if (wp <= kCapW) continue;  // warp path
-        if (wp > kCapC) {
-            if (threadIdx.x == 0) to_global(a, ci);
-            continue;
+    __shared__ int s_job;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {
+        auto& S = *reinterpret_cast<CompSm<kCapB, kKoB>*>(smem_raw);
+        const TeamCTA<kWarpsPB * 32> team;
+        const int nbig = *nbig_p;
+        while (true) {
+            if (threadIdx.x == 0) s_job = atomicAdd(&heads[0], 1);
+            __syncthreads();
+            const int bi = s_job;
+            __syncthreads();
+            if (bi >= nbig) break;
+            const int ci = big[bi];
+            if (!comp_solve(team, S, red, a, roots[ci], bbox[ci]) && threadIdx.x == 0) to_global(a, ci);
+            __syncthreads();
         }
-        if (!comp_solve(team, S, red, a, roots[ci], bb) && threadIdx.x == 0) to_global(a, ci);
-        __syncthreads();
+    }
+    {
+        auto& S = reinterpret_cast<CompSm<kCapW, kKoW>*>(smem_raw)[warp];
+        const TeamWarp team{lane};
+        const int ncomp = min(*cnt, cap);
+        while (true) {
+            int ci = 0;
+            if (lane == 0) ci = atomicAdd(&heads[1], 1);
+            ci = __shfl_sync(0xffffffffu, ci, 0);
+            if (ci >= ncomp) break;
+            const int4 bb = bbox[ci];
+            if (win_px(bb) > kCapW) continue;  // block list or global path
+            if (!comp_solve(team, S, red, a, roots[ci], bb) && lane == 0) to_global(a, ci);
+            __syncwarp();
+        }
     }
 }
 
@@ -661,7 +681,7 @@ __global__ void __launch_bounds__(kCT) k_comp_global(CompArgs a, const int32_t* 
 __global__ void __launch_bounds__(kFT, 2) k_obj_feat_list(CompArgs a, const int4* __restrict__ bbox) {
     __shared__ FeatSmem fs;
     __shared__ TeamRed red;
-    const TeamCTA team;
+    const TeamCTA<> team;
     const int n = min(*a.gobj_cnt, a.gobj_cap);
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
         const int2 e = a.gobj[i];
@@ -720,7 +740,9 @@ void launch_components(const uint8_t* F, const float* dist, const uint8_t* g, fl
     int32_t* ovf = sl.cnt32 + 9;     // overflow components
     int32_t* rows = sl.cnt32 + 10;   // staged rows
     int32_t* gobj = sl.cnt32 + 11;   // objects of the global path
-    cudaMemsetAsync(sl.cnt32 + 8, 0, 4 * sizeof(int32_t), s);
+    int32_t* nbig = sl.cnt32 + 12;   // block-list components
+    int32_t* heads = sl.cnt32 + 13;  // [0] block-list head, [1] component-list head
+    cudaMemsetAsync(sl.cnt32 + 8, 0, 8 * sizeof(int32_t), s);
     if (n == 0) {
         if (table) cudaMemsetAsync(table->n_rows_dev, 0, sizeof(int32_t), s);
         return;
@@ -763,15 +785,15 @@ void launch_components(const uint8_t* F, const float* dist, const uint8_t* g, fl
     a.gobj_cnt = gobj;
     a.gobj = reinterpret_cast<int2*>(sl.obj_bbox);
     a.gobj_cap = max_objects;
-    const size_t smw = kWarpsPB * sizeof(CompSm<kCapW, kKoW>), smc = sizeof(CompSm<kCapC, kKoC>);
+    const size_t smw = kWarpsPB * sizeof(CompSm<kCapW, kKoW>);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_comp_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
-        cudaFuncSetAttribute(k_comp_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+        cudaFuncSetAttribute(k_comp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
         attr = true;
     }
-    (note_launch(), k_comp_warp<<<148 * 4, kWarpsPB * 32, smw, s>>>(a, cnt, cap, sl.comp_root, sl.comp_bbox));
-    (note_launch(), k_comp_cta<<<148 * 2, kCT, smc, s>>>(a, cnt, cap, sl.comp_root, sl.comp_bbox));
+    (note_launch(), k_comp_classify<<<grid_for(cap), 256, 0, s>>>(a, cnt, cap, sl.comp_bbox, sl.comp_big, nbig));
+    (note_launch(), k_comp_fused<<<148 * 4, kWarpsPB * 32, smw, s>>>(a, cnt, cap, sl.comp_root, sl.comp_bbox,
+                                                                     sl.comp_big, nbig, heads));
     (note_launch(), k_comp_global<<<148, kCT, 0, s>>>(a, sl.comp_root, sl.comp_bbox));
     if (table) {
         (note_launch(), k_obj_feat_list<<<148 * 2, kFT, 0, s>>>(a, sl.comp_bbox));

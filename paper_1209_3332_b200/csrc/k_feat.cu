@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kFT, 3) k_obj_feat(const int32_t* __restrict__
                                                   float* __restrict__ out_feat, int32_t capacity) {
     __shared__ FeatSmem fs;
     __shared__ TeamRed red;
-    const TeamCTA team;
+    const TeamCTA<> team;
     const int n = min(*cnt, min(cap, capacity));
     for (int obj = blockIdx.x; obj < n; obj += gridDim.x) {
         const int32_t root = rank_root[obj];
