@@ -149,7 +149,7 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
             return check_launch(ctx, "bg skip");
         }
     }
-    launch_rbc(sl.flags, w, h, sl.lab, sl.aux, sl.rbc, s);                                           // S2
+    launch_rbc(sl.flags, w, h, sl, sl.rbc, s);                                                      // S2
     ev(ctx, sl, 2, s);
     launch_open(sl.g, w, h, p.open_diam, sl.u8b, sl.u8a, s);                                          // S3
     ev(ctx, sl, 3, s);
@@ -157,12 +157,9 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
     launch_recon_u8_auto(sl.g, sl.u8b, w, h, sl.wl, s);
     launch_tophat(sl.g, sl.u8b, sl.rbc, p.g1, w, h, sl.cand, s);
     ev(ctx, sl, 4, s);
-    CclSrc cs{sl.cand, 0, false, nullptr};                                                            // S5
-    launch_ccl(cs, w, h, 8, sl.lab, sl.aux, s);
-    launch_ccl_count(cs, w, h, sl.lab, sl.aux, s);
-    launch_ccl_area_filter(cs, w, h, sl.lab, sl.aux, p.cand_min_area, p.cand_max_area, sl.big0, s);
+    launch_area_select(sl.cand, w, h, p.cand_min_area, p.cand_max_area, sl, sl.big0, s);           // S5
     ev(ctx, sl, 5, s);
-    launch_fill_holes(sl.big0, w, h, sl.lab, sl.aux, sl.F, s);                                       // S6
+    launch_fill_holes(sl.big0, w, h, sl, sl.F, s);                                                  // S6
     ev(ctx, sl, 6, s);
     launch_edt(sl.F, w, h, sl, nullptr, sl.dist, s);                                                 // S7
     ev(ctx, sl, 7, s);
@@ -331,6 +328,9 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.comp_bbox = (int4*)A(16 * (size_t)s.comp_cap);
         s.cid = (int32_t*)A(4 * N);
         s.comp_big = (int32_t*)A(4 * (size_t)s.comp_cap);
+        s.cs_edge = (int32_t*)A(4 * 4 * kTile * (size_t)ntiles);
+        s.cs_roots = (int32_t*)A(4 * (size_t)kTile * kTile * ntiles);
+        s.cs_nroots = (int32_t*)A(4 * (size_t)ntiles);
         s.counters = (unsigned long long*)A(8 * 4);
         s.cnt32 = (int32_t*)A(4 * 16);
         s.stg_label = (int32_t*)A(4 * (size_t)mo);
@@ -348,7 +348,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.h_nrows = (int32_t*)halloc(16);
         void* all[] = {s.g, s.flags, s.rbc, s.u8a, s.u8b, s.cand, s.big0, s.F, s.split, s.pmask, s.lab, s.aux,
                        s.ML, s.d, s.L, s.dist, s.J, s.c, s.gcol, s.seg_top, s.seg_bot, s.wl.state, s.wl.inrows, s.wl.queue,
-                       s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.comp_root, s.comp_bbox, s.comp_big, s.cid, s.stg_label, s.stg_flags, s.stg_feat, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
+                       s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.comp_root, s.comp_bbox, s.comp_big, s.cs_edge, s.cs_roots, s.cs_nroots, s.cid, s.stg_label, s.stg_flags, s.stg_feat, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
                        s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows};
         for (void* p : all)
             if (!p) { hp_ctx_destroy(ctx); return HP_ERR_NOMEM; }
@@ -503,7 +503,7 @@ hp_status hp_stage_run(hp_ctx* ctx, int32_t slot, hp_stage stage, const hp_stage
             return check_launch(ctx, "stage cd");
         case HP_STAGE_RBC:
             if (!need({io->in[0], io->out[0]})) break;
-            launch_rbc(in8(0), w, h, sl.lab, sl.aux, (uint8_t*)io->out[0], s);
+            launch_rbc(in8(0), w, h, sl, (uint8_t*)io->out[0], s);
             return check_launch(ctx, "stage rbc");
         case HP_STAGE_OPEN:
             if (!need({io->in[0], io->out[0]})) break;
@@ -519,16 +519,12 @@ hp_status hp_stage_run(hp_ctx* ctx, int32_t slot, hp_stage stage, const hp_stage
         }
         case HP_STAGE_AREA: {
             if (!need({io->in[0], io->out[0]})) break;
-            CclSrc cs{in8(0), 0, false, nullptr};
-            launch_ccl(cs, w, h, 8, sl.lab, sl.aux, s);
-            launch_ccl_count(cs, w, h, sl.lab, sl.aux, s);
-            launch_ccl_area_filter(cs, w, h, sl.lab, sl.aux, p.cand_min_area, p.cand_max_area,
-                                   (uint8_t*)io->out[0], s);
+            launch_area_select(in8(0), w, h, p.cand_min_area, p.cand_max_area, sl, (uint8_t*)io->out[0], s);
             return check_launch(ctx, "stage area");
         }
         case HP_STAGE_FILL:
             if (!need({io->in[0], io->out[0]})) break;
-            launch_fill_holes(in8(0), w, h, sl.lab, sl.aux, (uint8_t*)io->out[0], s);
+            launch_fill_holes(in8(0), w, h, sl, (uint8_t*)io->out[0], s);
             return check_launch(ctx, "stage fill");
         case HP_STAGE_EDT:
             if (!need({io->in[0], io->out[1]})) break;

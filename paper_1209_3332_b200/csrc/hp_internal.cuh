@@ -75,6 +75,9 @@ struct Slot {
     int32_t* comp_root;
     int4* comp_bbox;
     int32_t* comp_big;  // components whose window needs a whole block (k_comp.cu)
+    int32_t* cs_edge;    // k_ccls.cu: per 32x32 tile, the roots of its 4 x 32 edge pixels
+    int32_t* cs_roots;   // k_ccls.cu: per tile, its local roots (up to 1024)
+    int32_t* cs_nroots;  // k_ccls.cu: per tile, number of local roots
     int32_t* cid;
     int32_t comp_cap;
     // staging table of the fused S8-S11 path (rows in discovery order)
@@ -125,11 +128,12 @@ void launch_ccl_area_filter(const CclSrc& src, int w, int h, const int32_t* lab,
 void launch_ccl_to_labels(const CclSrc& src, int w, int h, const int32_t* lab, int32_t* out,
                           cudaStream_t s);
 // S2
-void launch_rbc(const uint8_t* flags, int w, int h, int32_t* lab, int32_t* aux, uint8_t* rbc,
-                cudaStream_t s);
+// k_ccls.cu (CCL-select: u8 output from a per-component property, no label plane)
+void launch_rbc(const uint8_t* flags, int w, int h, Slot& sl, uint8_t* rbc, cudaStream_t s);
 // S6
-void launch_fill_holes(const uint8_t* big0, int w, int h, int32_t* lab, int32_t* aux,
-                       uint8_t* F, cudaStream_t s);
+void launch_fill_holes(const uint8_t* big0, int w, int h, Slot& sl, uint8_t* F, cudaStream_t s);
+void launch_area_select(const uint8_t* cand, int w, int h, int amin, int amax, Slot& sl, uint8_t* out,
+                        cudaStream_t s);
 // IWPP / worklist engine
 void wl_init_all(const Worklist& wl, int w, int h, cudaStream_t s);
 void wl_init_from_mask(const Worklist& wl, const uint8_t* mask, int w, int h, cudaStream_t s);

@@ -1,5 +1,6 @@
-// k_ccl.cu -- connected-component labelling engine (BWLabel PAPER.md:602; used by RBC
-// detection S2, AreaThreshold S5, FillHoles S6, markers S8 and S10).
+// k_ccl.cu -- connected-component labelling engine (BWLabel PAPER.md:602): the per-pixel
+// label plane of the pipeline's F components (S8-S11, k_comp.cu), the global S10 path and the
+// CCL8/CCL4 stages.  S2/S5/S6 need only a per-component property and use k_ccls.cu.
 //
 // Union-find with atomic hooking, canonical root = minimum linear index (reading C14):
 //   k_ccl_local   one 32x32 tile per CTA: shared-memory union-find over the in-tile N+
@@ -274,51 +275,6 @@ __global__ void k_ccl_to_labels(const int32_t* __restrict__ lab, int64_t n, int3
     }
 }
 
-// S2 helpers: roots hit by an RBC_HI pixel; output = hit & R_GT_B
-__global__ void k_rbc_hit(const uint8_t* __restrict__ flags, const int32_t* __restrict__ lab,
-                          int64_t n, int32_t* __restrict__ aux) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        if ((flags[p] & (HP_FLAG_RBC_HI | HP_FLAG_RBC_LO)) == (HP_FLAG_RBC_HI | HP_FLAG_RBC_LO))
-            aux[lab[p]] = 1;
-    }
-}
-__global__ void k_rbc_out(const uint8_t* __restrict__ flags, const int32_t* __restrict__ lab,
-                          int64_t n, const int32_t* __restrict__ aux, uint8_t* __restrict__ rbc) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        int32_t r = lab[p];
-        rbc[p] = (r >= 0 && aux[r] && (flags[p] & HP_FLAG_R_GT_B)) ? 1 : 0;
-    }
-}
-
-// S6 helpers: background components touching the tile border; F = big0 | enclosed bg
-__global__ void k_fill_border(const int32_t* __restrict__ lab, int w, int h, int32_t* __restrict__ aux) {
-    int64_t nb = 2LL * w + 2LL * h;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int x, y;
-        if (i < w) { x = (int)i; y = 0; }
-        else if (i < 2LL * w) { x = (int)(i - w); y = h - 1; }
-        else if (i < 2LL * w + h) { x = 0; y = (int)(i - 2LL * w); }
-        else { x = w - 1; y = (int)(i - 2LL * w - h); }
-        int32_t r = lab[(int64_t)y * w + x];
-        if (r >= 0) aux[r] = 1;
-    }
-}
-__global__ void k_fill_out(const uint8_t* __restrict__ big0, const int32_t* __restrict__ lab,
-                           int64_t n, const int32_t* __restrict__ aux, uint8_t* __restrict__ F) {
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        uint8_t v = big0[p] ? 1 : 0;
-        if (!v) {
-            int32_t r = lab[p];
-            v = (r >= 0 && aux[r] == 0) ? 1 : 0;
-        }
-        F[p] = v;
-    }
-}
-
 inline int grid_for(int64_t n) {
     int64_t b = (n + 255) / 256;
     return (int)std::min<int64_t>(b, 148 * 16);
@@ -357,30 +313,6 @@ void launch_ccl_to_labels(const CclSrc&, int w, int h, const int32_t* lab, int32
     const int64_t n = (int64_t)w * h;
     if (n == 0) return;
     (note_launch(), k_ccl_to_labels<<<grid_for(n), 256, 0, s>>>(lab, n, out));
-}
-
-// S2 -- RBC detection: rbc = BinRecon8(RBC_HI, RBC_LO) & R_GT_B, as CCL-select: the
-// RBC_LO components that contain an RBC_HI pixel.
-void launch_rbc(const uint8_t* flags, int w, int h, int32_t* lab, int32_t* aux, uint8_t* rbc,
-                cudaStream_t s) {
-    const int64_t n = (int64_t)w * h;
-    if (n == 0) return;
-    CclSrc cs{flags, (uint8_t)HP_FLAG_RBC_LO, false, nullptr};
-    launch_ccl(cs, w, h, 8, lab, aux, s);
-    (note_launch(), k_rbc_hit<<<grid_for(n), 256, 0, s>>>(flags, lab, n, aux));
-    (note_launch(), k_rbc_out<<<grid_for(n), 256, 0, s>>>(flags, lab, n, aux, rbc));
-}
-
-// S6 -- FillHolles: 4-connected background components that contain no
-// tile-border pixel are holes (reading C8).
-void launch_fill_holes(const uint8_t* big0, int w, int h, int32_t* lab, int32_t* aux,
-                       uint8_t* F, cudaStream_t s) {
-    const int64_t n = (int64_t)w * h;
-    if (n == 0) return;
-    CclSrc cs{big0, 0, true, nullptr};
-    launch_ccl(cs, w, h, 4, lab, aux, s);
-    (note_launch(), k_fill_border<<<grid_for(2LL * (w + h)), 256, 0, s>>>(lab, w, h, aux));
-    (note_launch(), k_fill_out<<<grid_for(n), 256, 0, s>>>(big0, lab, n, aux, F));
 }
 
 }  // namespace hp

@@ -1,0 +1,389 @@
+// k_ccls.cu -- "CCL-select": per-pixel u8 outputs that depend on a property of the pixel's
+// connected component, without a per-pixel label plane in HBM.  Used by S2 RBC detection
+// (components of RBC_LO that contain an RBC_HI pixel), S5 AreaThreshold
+// (components of the candidate mask with min <= area <= max) and S6 FillHoles
+// (4-connected background components that touch no tile-border pixel, PAPER.md:598,
+// reading C8).
+//
+// k_ccl.cu's engine writes an int32 root for every pixel (64 MB per 4K tile) and every
+// consumer re-reads it; here (32x32 tiles as there):
+//   k_cs_local   shared-memory union-find of the tile (runs from ballots + CAS hooking, the
+//                same scheme as k_ccl_local); per local component: area and property bits,
+//                reduced in shared memory and written ONLY at the component's root entry
+//                (global index of its minimum pixel); tile-edge pixels' roots to a compact
+//                edge array; the tile's local roots to a list;
+//   k_cs_merge   cross-tile unions from the edge arrays (CAS hooking of the larger root under
+//                the smaller on the sparse parent array, finds with CAS path halving);
+//   k_cs_accum   every non-root local root adds its area / ORs its bits into its global root
+//                and points straight at it (no unions run any more, so this is safe);
+//   k_cs_out     recomputes the tile's local union-find and writes the u8 output from the
+//                global root's property word.
+// HBM traffic per pixel: the input plane twice and the u8 output once (plus small arrays).
+// The property word packs the area (bits 0-28: images up to 2^29 - 1 px) with the OR-bits
+// HIT (bit 29) and TOUCH (bit 30); atomicAdd of areas never carries into the flag bits.
+#include "hp_internal.cuh"
+
+namespace hp {
+namespace {
+
+constexpr int32_t kAreaMask = (1 << 29) - 1;
+constexpr int32_t kHit = 1 << 29, kTouch = 1 << 30;
+constexpr int kT = kTile;  // 32
+
+enum SelMode { SEL_AREA = 0, SEL_RBC = 1, SEL_FILL = 2 };
+
+struct Sel {
+    const uint8_t* plane;  // SEL_AREA: candidate mask; SEL_RBC: flags; SEL_FILL: big0
+    int w, h;
+    int amin, amax;
+    template <int MODE>
+    __device__ __forceinline__ bool fg(uint8_t v) const {
+        if (MODE == SEL_AREA) return v != 0;
+        if (MODE == SEL_RBC) return (v & HP_FLAG_RBC_LO) != 0;
+        return v == 0;  // SEL_FILL: background of big0
+    }
+    // the pixel's property bit (OR-reduced per component)
+    template <int MODE>
+    __device__ __forceinline__ bool bit(uint8_t v, int x, int y) const {
+        if (MODE == SEL_RBC) return (v & (HP_FLAG_RBC_HI | HP_FLAG_RBC_LO)) == (HP_FLAG_RBC_HI | HP_FLAG_RBC_LO);
+        if (MODE == SEL_FILL) return x == 0 || y == 0 || x == w - 1 || y == h - 1;
+        return false;
+    }
+    template <int MODE>
+    __device__ __forceinline__ uint8_t out(uint8_t v, bool f, int32_t prop) const {
+        if (MODE == SEL_AREA) {
+            const int a = prop & kAreaMask;
+            return f && a >= amin && a <= amax;
+        }
+        if (MODE == SEL_RBC) return f && (prop & kHit) && (v & HP_FLAG_R_GT_B);
+        return f ? !(prop & kTouch) : 1;  // SEL_FILL: big0 | enclosed background
+    }
+};
+
+template <int MODE>
+__device__ __forceinline__ int32_t mode_bit() { return MODE == SEL_RBC ? kHit : (MODE == SEL_FILL ? kTouch : 0); }
+
+__device__ __forceinline__ int find_l(const int* s, int x) {
+    const volatile int* vs = s;
+    int p = vs[x];
+    while (p != x) {
+        x = p;
+        p = vs[x];
+    }
+    return x;
+}
+__device__ __forceinline__ void union_l(int* s, int a, int b) {
+    while (true) {
+        a = find_l(s, a);
+        b = find_l(s, b);
+        if (a == b) return;
+        if (a < b) {
+            int t = a;
+            a = b;
+            b = t;
+        }
+        if (atomicCAS(&s[a], a, b) == a) return;
+    }
+}
+__device__ __forceinline__ int32_t find_c(int32_t* P, int32_t x) {
+    while (true) {
+        int32_t p = __ldcg(P + x);
+        if (p == x) return x;
+        int32_t gp = __ldcg(P + p);
+        if (gp == p) return p;
+        atomicCAS(&P[x], p, gp);
+        x = gp;
+    }
+}
+__device__ __forceinline__ void union_c(int32_t* P, int32_t a, int32_t b) {
+    while (true) {
+        a = find_c(P, a);
+        b = find_c(P, b);
+        if (a == b) return;
+        if (a < b) {
+            int32_t t = a;
+            a = b;
+            b = t;
+        }
+        if (atomicCAS(&P[a], a, b) == a) return;
+    }
+}
+
+// One 256-thread CTA per 32x32 tile; thread (lane = column, warp) owns rows warp + 8k, so a
+// row is one warp: its ballot is the row's foreground mask, every pixel points at the start of
+// its horizontal run, and only RUN STARTS union, once with each run of the row above that
+// touches the run (8-conn: columns xs-1 .. xe+1, 4-conn: xs .. xe) -- one union per adjacent
+// pair of runs.  Roots, areas, property bits and outputs are then handled once per run (the
+// run start), shared with the run's pixels by a shuffle.  (Measured r1: a warp-per-tile
+// variant with lane = column and 32 serial rows was 2x slower.)
+struct TileSm {
+    int s[kT * kT];
+    int acc[kT * kT];
+    unsigned rowm[kT];  // foreground mask of each row
+    unsigned bitm[kT];  // property-bit mask of each row
+    int nr;
+};
+
+__device__ __forceinline__ int run_start(unsigned fm, int lane) {
+    const unsigned nl = ~(fm & (fm << 1)) & (0xffffffffu >> (31 - lane));
+    return 31 - __clz(nl);
+}
+__device__ __forceinline__ int run_end(unsigned fm, int xs) {
+    const unsigned tail = ~(fm >> xs);
+    return tail == 0 ? 31 : xs + __ffs(tail) - 2;
+}
+__device__ __forceinline__ unsigned span(int lo, int hi) {  // bits lo..hi
+    return (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+}
+
+// loads + runs + unions; returns 0 (no foreground), 1 (general), 2 (all foreground)
+template <int MODE>
+__device__ __forceinline__ int tile_uf(const Sel& sel, int conn, int tx0, int ty0, TileSm& T, uint8_t (&v)[4],
+                                       unsigned (&fms)[4], bool clear_acc) {
+    const int lane = threadIdx.x & 31;
+    const int w = sel.w, h = sel.h;
+    const int gx = tx0 + lane;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int gy = ty0 + (threadIdx.x >> 5) + 8 * k;
+        v[k] = (gx < w && gy < h) ? __ldg(sel.plane + (int64_t)gy * w + gx) : (uint8_t)0;
+    }
+    int nfg = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int ly = (threadIdx.x >> 5) + 8 * k;
+        const int gy = ty0 + ly;
+        const bool f = gx < w && gy < h && sel.fg<MODE>(v[k]);
+        const unsigned fm = __ballot_sync(0xffffffffu, f);
+        const unsigned bm = __ballot_sync(0xffffffffu, f && sel.bit<MODE>(v[k], gx, gy));
+        fms[k] = fm;
+        if (lane == 0) {
+            T.rowm[ly] = fm;
+            T.bitm[ly] = bm;
+        }
+        nfg += f;
+        T.s[ly * kT + lane] = f ? ly * kT + run_start(fm, lane) : -1;
+        if (clear_acc) T.acc[ly * kT + lane] = 0;
+    }
+    if (threadIdx.x == 0) T.nr = 0;
+    const int any_fg = __syncthreads_or(nfg > 0);
+    const int all_fg = __syncthreads_and(nfg == 4);
+    if (!any_fg) return 0;
+    if (all_fg) return 2;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int ly = (threadIdx.x >> 5) + 8 * k;
+        const unsigned fm = fms[k];
+        if (ly == 0 || !((fm >> lane) & 1) || (lane > 0 && ((fm >> (lane - 1)) & 1))) continue;  // run starts
+        const unsigned above = T.rowm[ly - 1];
+        if (!above) continue;
+        const int re = run_end(fm, lane);
+        const int lo = conn == 8 ? max(lane - 1, 0) : lane, hi = conn == 8 ? min(re + 1, 31) : re;
+        const unsigned ov = above & span(lo, hi);
+        unsigned segs = ov & ~(ov << 1);  // first column of each touching run (within the range)
+        const int li = ly * kT + lane;
+        while (segs) {
+            const int b = __ffs(segs) - 1;
+            segs &= segs - 1;
+            union_l(T.s, li, (ly - 1) * kT + b);
+        }
+    }
+    __syncthreads();
+    return 1;
+}
+
+__device__ __forceinline__ bool is_run_start(unsigned fm, int lane) {
+    return ((fm >> lane) & 1) && !(lane > 0 && ((fm >> (lane - 1)) & 1));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __restrict__ P, int32_t* __restrict__ X,
+                                                  int32_t* __restrict__ E, int32_t* __restrict__ roots,
+                                                  int32_t* __restrict__ nroots) {
+    __shared__ TileSm T;
+    const int tx0 = blockIdx.x * kT, ty0 = blockIdx.y * kT;
+    const int t = blockIdx.y * gridDim.x + blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int w = sel.w, h = sel.h;
+    uint8_t v[4];
+    unsigned fms[4];
+    const int kind = tile_uf<MODE>(sel, conn, tx0, ty0, T, v, fms, true);
+    int32_t* Et = E + (int64_t)t * 4 * kT;
+    auto gidx = [&](int li) -> int32_t { return (int32_t)((int64_t)(ty0 + li / kT) * w + tx0 + li % kT); };
+    if (kind == 0) {
+        if (threadIdx.x < 4 * kT) Et[threadIdx.x] = -1;
+        if (threadIdx.x == 0) nroots[t] = 0;
+        return;
+    }
+    if (kind == 2) {  // one component rooted at the tile origin
+        const int32_t G = gidx(0);
+        if (threadIdx.x < 4 * kT) Et[threadIdx.x] = G;
+        if (threadIdx.x < 32) {
+            const unsigned anyb = __any_sync(0xffffffffu, T.bitm[threadIdx.x] != 0);
+            if (threadIdx.x == 0) {
+                P[G] = G;
+                X[G] = kT * kT | (anyb ? mode_bit<MODE>() : 0);
+                roots[(int64_t)t * kT * kT] = G;
+                nroots[t] = 1;
+            }
+        }
+        return;
+    }
+    // per run: area and property bit at the run's root
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int ly = (threadIdx.x >> 5) + 8 * k;
+        const unsigned fm = fms[k];
+        if (!is_run_start(fm, lane)) continue;
+        const int re = run_end(fm, lane);
+        const int r = find_l(T.s, ly * kT + lane);
+        atomicAdd(&T.acc[r], re - lane + 1);
+        if (T.bitm[ly] & span(lane, re)) atomicOr(&T.acc[r], mode_bit<MODE>());
+    }
+    __syncthreads();
+    // roots: run starts that are their own parent
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int ly = (threadIdx.x >> 5) + 8 * k;
+        const int li = ly * kT + lane;
+        if (T.s[li] == li) {
+            const int32_t G = gidx(li);
+            P[G] = G;
+            X[G] = T.acc[li];
+            roots[(int64_t)t * kT * kT + atomicAdd(&T.nr, 1)] = G;
+        }
+    }
+    // tile-edge roots: side 0 top row, 1 bottom row, 2 left column, 3 right column
+    if (threadIdx.x < 4 * kT) {
+        const int side = threadIdx.x >> 5;
+        const int lxx = side < 2 ? lane : (side == 2 ? 0 : kT - 1);
+        const int lyy = side < 2 ? (side == 0 ? 0 : kT - 1) : lane;
+        const int li = lyy * kT + lxx;
+        int32_t e = -1;
+        if (tx0 + lxx < w && ty0 + lyy < h && T.s[li] >= 0) e = gidx(find_l(T.s, li));
+        Et[threadIdx.x] = e;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) nroots[t] = T.nr;
+}
+
+// cross-tile unions: top row, left and right columns of each tile against the edge arrays of
+// the tiles above / left / right (N+ neighbours outside the tile)
+__global__ void __launch_bounds__(96) k_cs_merge(int conn, int ntx, int nty, const int32_t* __restrict__ E,
+                                                 int32_t* __restrict__ P) {
+    const int bx = blockIdx.x, by = blockIdx.y;
+    const int side = threadIdx.x >> 5, i = threadIdx.x & 31;
+    auto e = [&](int tx, int ty, int sd, int k) -> int32_t {
+        if (tx < 0 || ty < 0 || tx >= ntx || ty >= nty) return -1;
+        return E[((int64_t)(ty * ntx + tx)) * 4 * kT + sd * kT + k];
+    };
+    if (side == 0) {  // top row pixel (i, 0)
+        const int32_t me = e(bx, by, 0, i);
+        if (me < 0 || by == 0) return;
+        int32_t q = e(bx, by - 1, 1, i);
+        if (q >= 0) union_c(P, me, q);
+        if (conn == 8) {
+            q = i > 0 ? e(bx, by - 1, 1, i - 1) : e(bx - 1, by - 1, 1, kT - 1);
+            if (q >= 0) union_c(P, me, q);
+            q = i < kT - 1 ? e(bx, by - 1, 1, i + 1) : e(bx + 1, by - 1, 1, 0);
+            if (q >= 0) union_c(P, me, q);
+        }
+    } else if (side == 1) {  // left column pixel (0, i)
+        const int32_t me = e(bx, by, 2, i);
+        if (me < 0 || bx == 0) return;
+        int32_t q = e(bx - 1, by, 3, i);
+        if (q >= 0) union_c(P, me, q);
+        if (conn == 8 && i > 0) {  // (i == 0: the top-row thread covers the diagonal)
+            q = e(bx - 1, by, 3, i - 1);
+            if (q >= 0) union_c(P, me, q);
+        }
+    } else {  // right column pixel (31, i): up-right neighbour in the right tile (8-conn)
+        if (conn != 8 || i == 0) return;
+        const int32_t me = e(bx, by, 3, i);
+        if (me < 0) return;
+        const int32_t q = e(bx + 1, by, 2, i - 1);
+        if (q >= 0) union_c(P, me, q);
+    }
+}
+
+__global__ void k_cs_accum(int ntiles, const int32_t* __restrict__ roots, const int32_t* __restrict__ nroots,
+                           int32_t* __restrict__ P, int32_t* __restrict__ X) {
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int n = nroots[t];
+        for (int k = threadIdx.x; k < n; k += blockDim.x) {
+            const int32_t G = roots[(int64_t)t * kT * kT + k];
+            const int32_t R = find_c(P, G);
+            if (R == G) continue;
+            const int32_t x = X[G];
+            atomicAdd(&X[R], x & kAreaMask);
+            if (x & ~kAreaMask) atomicOr(&X[R], x & ~kAreaMask);
+            P[G] = R;
+        }
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_cs_out(Sel sel, int conn, const int32_t* __restrict__ P,
+                                                const int32_t* __restrict__ X, uint8_t* __restrict__ out) {
+    __shared__ TileSm T;
+    const int tx0 = blockIdx.x * kT, ty0 = blockIdx.y * kT;
+    const int lane = threadIdx.x & 31;
+    const int w = sel.w, h = sel.h;
+    uint8_t v[4];
+    unsigned fms[4];
+    const int kind = tile_uf<MODE>(sel, conn, tx0, ty0, T, v, fms, false);
+    const int gx = tx0 + lane;
+    int32_t prop0 = 0;
+    if (kind == 2) prop0 = __ldg(X + __ldg(P + (int32_t)((int64_t)ty0 * w + tx0)));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int ly = (threadIdx.x >> 5) + 8 * k;
+        const int gy = ty0 + ly;
+        const unsigned fm = fms[k];
+        const bool f = (fm >> lane) & 1;
+        int32_t prop = prop0;
+        if (kind == 1) {
+            const int st = f ? run_start(fm, lane) : lane;
+            int32_t pr = 0;
+            if (f && st == lane) {
+                const int r = find_l(T.s, ly * kT + lane);
+                pr = __ldg(X + __ldg(P + (int32_t)((int64_t)(ty0 + r / kT) * w + tx0 + r % kT)));
+            }
+            prop = __shfl_sync(0xffffffffu, pr, st);
+        }
+        if (gx < w && gy < h) out[(int64_t)gy * w + gx] = sel.out<MODE>(v[k], f, prop);
+    }
+}
+
+template <int MODE>
+void run_select(Sel sel, int conn, Slot& sl, uint8_t* out, cudaStream_t s) {
+    const int w = sel.w, h = sel.h;
+    if ((int64_t)w * h == 0) return;
+    const int ntx = (w + kT - 1) / kT, nty = (h + kT - 1) / kT;
+    const int ntiles = ntx * nty;
+    dim3 grid(ntx, nty);
+    int32_t* P = sl.lab;
+    int32_t* X = sl.aux;
+    (note_launch(), k_cs_local<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, sl.cs_edge, sl.cs_roots, sl.cs_nroots));
+    (note_launch(), k_cs_merge<<<grid, 96, 0, s>>>(conn, ntx, nty, sl.cs_edge, P));
+    const int gb = std::min(ntiles, 148 * 8);
+    (note_launch(), k_cs_accum<<<gb, 128, 0, s>>>(ntiles, sl.cs_roots, sl.cs_nroots, P, X));
+    (note_launch(), k_cs_out<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, out));
+}
+
+}  // namespace
+
+void launch_rbc(const uint8_t* flags, int w, int h, Slot& sl, uint8_t* rbc, cudaStream_t s) {
+    run_select<SEL_RBC>(Sel{flags, w, h, 0, 0}, 8, sl, rbc, s);
+}
+
+void launch_area_select(const uint8_t* cand, int w, int h, int amin, int amax, Slot& sl, uint8_t* out,
+                        cudaStream_t s) {
+    run_select<SEL_AREA>(Sel{cand, w, h, amin, amax}, 8, sl, out, s);
+}
+
+void launch_fill_holes(const uint8_t* big0, int w, int h, Slot& sl, uint8_t* F, cudaStream_t s) {
+    run_select<SEL_FILL>(Sel{big0, w, h, 0, 0}, 4, sl, F, s);
+}
+
+}  // namespace hp
