@@ -121,10 +121,12 @@ __device__ __forceinline__ void union_g(int32_t* lab, int32_t a, int32_t b) {
 
 __global__ void __launch_bounds__(256) k_ccl_local(Src src, int conn, int32_t* __restrict__ lab) {
     __shared__ int s[kTile * kTile];
+    __shared__ unsigned rowm[kTile];
     const int tx0 = blockIdx.x * kTile, ty0 = blockIdx.y * kTile;
     const int lx = threadIdx.x & 31;
     const int w = src.w, h = src.h;
     bool fgv[4];
+    unsigned fmv[4], lkm[4];
     // one warp per tile row: horizontal runs are linked at once from the row's ballot --
     // each pixel points at the first pixel of its run (a run start has no left link), so
     // dense foreground never builds long hook chains
@@ -136,8 +138,11 @@ __global__ void __launch_bounds__(256) k_ccl_local(Src src, int conn, int32_t* _
         bool f = gx < w && gy < h && src.fg(p);
         fgv[k] = f;
         unsigned fm = __ballot_sync(0xffffffffu, f);
+        fmv[k] = fm;
+        if (lx == 0) rowm[ly] = fm;
         bool lk = f && lx > 0 && ((fm >> (lx - 1)) & 1) && src.conn(p, p - 1);
-        unsigned nl = ~__ballot_sync(0xffffffffu, lk) & (0xffffffffu >> (31 - lx));
+        lkm[k] = __ballot_sync(0xffffffffu, lk);
+        unsigned nl = ~lkm[k] & (0xffffffffu >> (31 - lx));
         int start = 31 - __clz(nl);
         s[ly * kTile + lx] = f ? ly * kTile + start : -1;
     }
@@ -157,38 +162,66 @@ __global__ void __launch_bounds__(256) k_ccl_local(Src src, int conn, int32_t* _
         }
         return;
     }
+    if (src.eq == nullptr) {
+        // plain binary image: only run starts union, once with each run of the row above that
+        // touches the run (8-conn: columns xs-1 .. xe+1, 4-conn: xs .. xe)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        if (!fgv[k]) continue;
-        int ly = (threadIdx.x >> 5) + 8 * k;
-        int li = ly * kTile + lx;
-        int64_t p = (int64_t)(ty0 + ly) * w + tx0 + lx;
-        int nn = conn == 8 ? 4 : 2;
-        for (int j = 0; j < nn; ++j) {
-            int dx, dy;
-            nplus(conn, j, dx, dy);
-            if (dy == 0) continue;  // horizontal links are the runs above
-            int nx = lx + dx, ny = ly + dy;
-            if (nx < 0 || nx >= kTile || ny < 0) continue;
-            int ni = ny * kTile + nx;
-            if (s[ni] < 0) continue;  // background never changes
-            int64_t q = (int64_t)(ty0 + ny) * w + tx0 + nx;
-            if (!src.conn(p, q)) continue;
-            union_s(s, li, ni);
+        for (int k = 0; k < 4; ++k) {
+            const int ly = (threadIdx.x >> 5) + 8 * k;
+            const unsigned fm = fmv[k];
+            if (ly == 0 || !((fm >> lx) & 1) || (lx > 0 && ((fm >> (lx - 1)) & 1))) continue;
+            const unsigned above = rowm[ly - 1];
+            if (!above) continue;
+            const unsigned tail = ~(fm >> lx);
+            const int re = tail == 0 ? 31 : lx + __ffs(tail) - 2;
+            const int lo = conn == 8 ? max(lx - 1, 0) : lx, hi = conn == 8 ? min(re + 1, 31) : re;
+            const unsigned rm = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+            const unsigned ov = above & rm;
+            unsigned segs = ov & ~(ov << 1);
+            while (segs) {
+                const int b = __ffs(segs) - 1;
+                segs &= segs - 1;
+                union_s(s, ly * kTile + lx, (ly - 1) * kTile + b);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!fgv[k]) continue;
+            int ly = (threadIdx.x >> 5) + 8 * k;
+            int li = ly * kTile + lx;
+            int64_t p = (int64_t)(ty0 + ly) * w + tx0 + lx;
+            int nn = conn == 8 ? 4 : 2;
+            for (int j = 0; j < nn; ++j) {
+                int dx, dy;
+                nplus(conn, j, dx, dy);
+                if (dy == 0) continue;  // horizontal links are the runs above
+                int nx = lx + dx, ny = ly + dy;
+                if (nx < 0 || nx >= kTile || ny < 0) continue;
+                int ni = ny * kTile + nx;
+                if (s[ni] < 0) continue;  // background never changes
+                int64_t q = (int64_t)(ty0 + ny) * w + tx0 + nx;
+                if (!src.conn(p, q)) continue;
+                union_s(s, li, ni);
+            }
         }
     }
     __syncthreads();
+    // one find per run (at its start), shared with the run by a shuffle
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         int ly = (threadIdx.x >> 5) + 8 * k;
         int gx = tx0 + lx, gy = ty0 + ly;
+        int r = 0;
+        if (fgv[k] && !((lkm[k] >> lx) & 1)) r = find_s(s, ly * kTile + lx);  // run starts
+        const unsigned nl = ~lkm[k] & (0xffffffffu >> (31 - lx));
+        r = __shfl_sync(0xffffffffu, r, 31 - __clz(nl));
         if (gx >= w || gy >= h) continue;
         int64_t p = (int64_t)gy * w + gx;
         if (!fgv[k]) {
             lab[p] = -1;
             continue;
         }
-        int r = find_s(s, ly * kTile + lx);
         lab[p] = (int32_t)((int64_t)(ty0 + r / kTile) * w + tx0 + r % kTile);
     }
 }

@@ -267,50 +267,56 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
     if (threadIdx.x == 0) nroots[t] = T.nr;
 }
 
-// cross-tile unions: top row, left and right columns of each tile against the edge arrays of
-// the tiles above / left / right (N+ neighbours outside the tile)
-__global__ void __launch_bounds__(96) k_cs_merge(int conn, int ntx, int nty, const int32_t* __restrict__ E,
-                                                 int32_t* __restrict__ P) {
-    const int bx = blockIdx.x, by = blockIdx.y;
-    const int side = threadIdx.x >> 5, i = threadIdx.x & 31;
+// cross-tile unions, one warp per (tile, side): the tile's top row against the bottom row of
+// the tile above, its left column against the right column of the tile on the left.  Edge
+// pixels of one run (consecutive foreground along the edge) share a local root, so only run
+// starts union, once with each touching run across the edge (8-conn: positions i0-1 .. i1+1,
+// which also covers every right-column diagonal; 4-conn: i0 .. i1); the 8-conn corner
+// diagonals (up-left of (0,0), up-right of (31,0)) are taken by the top row's end lanes.
+__global__ void __launch_bounds__(256) k_cs_merge(int conn, int ntx, int nty, const int32_t* __restrict__ E,
+                                                  int32_t* __restrict__ P) {
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gt >= (int64_t)ntx * nty * 2 * kT) return;  // (whole warps: 2 * kT per tile)
+    const int t = (int)(gt / (2 * kT)), j = (int)(gt % (2 * kT));
+    const int bx = t % ntx, by = t / ntx;
+    const int side = j >> 5, i = j & 31;
     auto e = [&](int tx, int ty, int sd, int k) -> int32_t {
         if (tx < 0 || ty < 0 || tx >= ntx || ty >= nty) return -1;
-        return E[((int64_t)(ty * ntx + tx)) * 4 * kT + sd * kT + k];
+        return __ldg(E + ((int64_t)(ty * ntx + tx)) * 4 * kT + sd * kT + k);
     };
-    if (side == 0) {  // top row pixel (i, 0)
-        const int32_t me = e(bx, by, 0, i);
-        if (me < 0 || by == 0) return;
-        int32_t q = e(bx, by - 1, 1, i);
-        if (q >= 0) union_c(P, me, q);
-        if (conn == 8) {
-            q = i > 0 ? e(bx, by - 1, 1, i - 1) : e(bx - 1, by - 1, 1, kT - 1);
-            if (q >= 0) union_c(P, me, q);
-            q = i < kT - 1 ? e(bx, by - 1, 1, i + 1) : e(bx + 1, by - 1, 1, 0);
-            if (q >= 0) union_c(P, me, q);
+    const int ntxb = side == 0 ? bx : bx - 1, ntyb = side == 0 ? by - 1 : by;  // tile across the edge
+    const int nside = side == 0 ? 1 : 3;                                       // its bottom row / right column
+    const int32_t me = e(bx, by, side == 0 ? 0 : 2, i);
+    const int32_t q = e(ntxb, ntyb, nside, i);
+    const unsigned mine = __ballot_sync(0xffffffffu, me >= 0);
+    const unsigned other = __ballot_sync(0xffffffffu, q >= 0);
+    if (me < 0) return;
+    if (other && ((mine >> i) & 1) && !(i > 0 && ((mine >> (i - 1)) & 1))) {  // run start
+        const unsigned tail = ~(mine >> i);
+        const int re = tail == 0 ? 31 : i + __ffs(tail) - 2;
+        const int lo = conn == 8 ? max(i - 1, 0) : i, hi = conn == 8 ? min(re + 1, 31) : re;
+        const unsigned ov = other & span(lo, hi);
+        unsigned segs = ov & ~(ov << 1);
+        while (segs) {
+            const int b = __ffs(segs) - 1;
+            segs &= segs - 1;
+            union_c(P, me, e(ntxb, ntyb, nside, b));
         }
-    } else if (side == 1) {  // left column pixel (0, i)
-        const int32_t me = e(bx, by, 2, i);
-        if (me < 0 || bx == 0) return;
-        int32_t q = e(bx - 1, by, 3, i);
-        if (q >= 0) union_c(P, me, q);
-        if (conn == 8 && i > 0) {  // (i == 0: the top-row thread covers the diagonal)
-            q = e(bx - 1, by, 3, i - 1);
-            if (q >= 0) union_c(P, me, q);
-        }
-    } else {  // right column pixel (31, i): up-right neighbour in the right tile (8-conn)
-        if (conn != 8 || i == 0) return;
-        const int32_t me = e(bx, by, 3, i);
-        if (me < 0) return;
-        const int32_t q = e(bx + 1, by, 2, i - 1);
-        if (q >= 0) union_c(P, me, q);
+    }
+    if (conn == 8 && side == 0 && (i == 0 || i == kT - 1)) {
+        const int32_t d = i == 0 ? e(bx - 1, by - 1, 1, kT - 1) : e(bx + 1, by - 1, 1, 0);
+        if (d >= 0) union_c(P, me, d);
     }
 }
 
-__global__ void k_cs_accum(int ntiles, const int32_t* __restrict__ roots, const int32_t* __restrict__ nroots,
-                           int32_t* __restrict__ P, int32_t* __restrict__ X) {
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+// one warp per tile
+__global__ void __launch_bounds__(256) k_cs_accum(int ntiles, const int32_t* __restrict__ roots,
+                                                  const int32_t* __restrict__ nroots, int32_t* __restrict__ P,
+                                                  int32_t* __restrict__ X) {
+    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (t < ntiles) {
         const int n = nroots[t];
-        for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        for (int k = threadIdx.x & 31; k < n; k += 32) {
             const int32_t G = roots[(int64_t)t * kT * kT + k];
             const int32_t R = find_c(P, G);
             if (R == G) continue;
@@ -365,9 +371,9 @@ void run_select(Sel sel, int conn, Slot& sl, uint8_t* out, cudaStream_t s) {
     int32_t* P = sl.lab;
     int32_t* X = sl.aux;
     (note_launch(), k_cs_local<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, sl.cs_edge, sl.cs_roots, sl.cs_nroots));
-    (note_launch(), k_cs_merge<<<grid, 96, 0, s>>>(conn, ntx, nty, sl.cs_edge, P));
-    const int gb = std::min(ntiles, 148 * 8);
-    (note_launch(), k_cs_accum<<<gb, 128, 0, s>>>(ntiles, sl.cs_roots, sl.cs_nroots, P, X));
+    (note_launch(), k_cs_merge<<<(int)(((int64_t)ntiles * 2 * kT + 255) / 256), 256, 0, s>>>(conn, ntx, nty,
+                                                                                           sl.cs_edge, P));
+    (note_launch(), k_cs_accum<<<(ntiles + 7) / 8, 256, 0, s>>>(ntiles, sl.cs_roots, sl.cs_nroots, P, X));
     (note_launch(), k_cs_out<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, out));
 }
 
