@@ -4,7 +4,7 @@
 // Measured (tools/diag_iwpp.py, r1): with one warp per 32x32 tile job, the reconstruction of
 // some tiles is dominated by long sequential chains of tile jobs, i.e. by the cost of one hop
 // through the global queue.  Here one CTA of RX*RY warps owns a region of RX x RY sub-tiles
-// (128 x 128 px): the region window (plus halo) lives in shared memory as bytes; each warp
+// of 64 x 32 px (256 x 128 px): the region window (plus halo) lives in shared memory as bytes; each warp
 // closes its own 32x32 sub-tile with row-scan sweeps (reading its neighbours' pixels live),
 // then pushes the rows of neighbouring sub-tiles its changed border pixels can improve into
 // their shared-memory dirty masks.  The warps run asynchronously (no CTA barrier per
@@ -23,17 +23,23 @@ constexpr uint32_t ST_IDLE = 0, ST_QUEUED = 1, ST_BUSY = 2, ST_DIRTY = 3;
 constexpr int32_t EMPTY = -1;
 constexpr unsigned FULL = 0xffffffffu;
 #ifndef HP_RX
-// 128 x 128 px regions.  Measured (r1, config-2 tiles): 8x4 sub-tiles close one tile faster
-// alone (0.91 vs 1.04 ms) but a 1024-thread CTA fills the SM's register file, so tiles of the
-// other slots cannot co-run: 301 vs 395 tiles/s in bench.py at 4 slots.
+// 4 x 4 sub-tiles.  Measured (r1, config-2 tiles, 32 px sub-tiles): 8x4 sub-tiles close one
+// tile faster alone (0.91 vs 1.04 ms) but a 1024-thread CTA fills the SM's register file, so
+// tiles of the other slots cannot co-run: 301 vs 395 tiles/s in bench.py at 4 slots -- hence
+// wider sub-tiles (HP_PPL pixels per lane) rather than more warps.
 #define HP_RX 4
 #define HP_RY 4
 #endif
 #ifndef HP_POLL_NS
 #define HP_POLL_NS 400  // idle sub-tile warps back off (frees issue slots for co-running work)
 #endif
+#ifndef HP_PPL
+#define HP_PPL 2  // pixels per lane: sub-tiles of 64 x 32 px, regions of 256 x 128 px
+#endif
 constexpr int RX = HP_RX, RY = HP_RY, NW = RX * RY;
-constexpr int RWW = RX * 8 + 2;      // window words per row: bytes [X0-4, X0+128+4)
+constexpr int PPL = HP_PPL;            // pixels per lane in a sub-tile row
+constexpr int SW = 32 * PPL;           // sub-tile width (px); sub-tile height is kTile = 32
+constexpr int RWW = RX * SW / 4 + 2;   // window words per row: bytes [X0-4, X0+RX*SW+4)
 constexpr int RWB = RWW * 4;         // window bytes per row
 constexpr int ROWS = RY * kTile + 2; // window rows
 
@@ -140,30 +146,88 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : 2) k_region_mr8(const 
     const uint8_t* sM = reinterpret_cast<const uint8_t*>(S.M);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sx = warp % RX, sy = warp / RX;
-    const int wr0 = sy * kTile, wc0 = sx * kTile;  // window origin of this sub-tile (minus halo)
+    const int wr0 = sy * kTile, wc0 = sx * SW;  // window origin of this sub-tile (minus halo)
 
-    // close row y (1..32) of this warp's sub-tile; true iff it changed
+    // close row y (1..32) of this warp's sub-tile (lane owns PPL adjacent pixels); true iff it
+    // may have changed.  A pixel's update is the clamp f(v) = min(m, max(lo, v)) of the value v
+    // arriving along the row; clamps compose, so a lane's PPL pixels are one clamp and the row
+    // closure is a warp scan of clamps in each direction.
     auto row = [&](int y) -> bool {
-        const int wr = wr0 + y, wc = wc0 + lane + 1;
-        int m = sM[bidx(wr, wc)], rr = sR[bidx(wr, wc)];
-        int up = max(max(sR[bidx(wr - 1, wc - 1)], sR[bidx(wr - 1, wc)]), sR[bidx(wr - 1, wc + 1)]);
-        int dn = max(max(sR[bidx(wr + 1, wc - 1)], sR[bidx(wr + 1, wc)]), sR[bidx(wr + 1, wc + 1)]);
-        int vmax = max(up, dn);
-        int lft = sR[bidx(wr, wc - 1)], rgt = sR[bidx(wr, wc + 1)];
-        if (!__any_sync(FULL, min(max(vmax, max(lft, rgt)), m) > rr)) return false;
-        int b = max(rr, vmax);
-        if (lane == 0) b = max(b, lft);
-        if (lane == 31) b = max(b, rgt);
-        int lo = min(b, m);
+        const int wr = wr0 + y, c0 = wc0 + PPL * lane + 1;
+        int m[PPL], rr[PPL], vm[PPL];
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+            const int c = c0 + j;
+            m[j] = sM[bidx(wr, c)];
+            rr[j] = sR[bidx(wr, c)];
+            const int up = max(max(sR[bidx(wr - 1, c - 1)], sR[bidx(wr - 1, c)]), sR[bidx(wr - 1, c + 1)]);
+            const int dn = max(max(sR[bidx(wr + 1, c - 1)], sR[bidx(wr + 1, c)]), sR[bidx(wr + 1, c + 1)]);
+            vm[j] = max(up, dn);
+        }
+        const int lft = sR[bidx(wr, c0 - 1)], rgt = sR[bidx(wr, c0 + PPL)];
+        bool can = false;
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+            const int hn = max(j == 0 ? lft : rr[j - 1], j == PPL - 1 ? rgt : rr[j + 1]);
+            can |= min(max(vm[j], hn), m[j]) > rr[j];
+        }
+        if (!__any_sync(FULL, can)) return false;
+        int lo[PPL];
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+            int b = max(rr[j], vm[j]);
+            if (j == 0 && lane == 0) b = max(b, lft);
+            if (j == PPL - 1 && lane == 31) b = max(b, rgt);
+            lo[j] = min(b, m[j]);
+        }
         // the clamp scans are only needed if some pixel can take a horizontal neighbour's value
-        int nl = __shfl_up_sync(FULL, lo, 1), nr = __shfl_down_sync(FULL, lo, 1);
+        int nl = __shfl_up_sync(FULL, lo[PPL - 1], 1), nr = __shfl_down_sync(FULL, lo[0], 1);
         if (lane == 0) nl = 0;
         if (lane == 31) nr = 0;
-        int u = lo;
-        if (__any_sync(FULL, min(max(nl, nr), m) > lo))
-            u = max(clamp_scan<true>(lo, m, lane), clamp_scan<false>(lo, m, lane));
+        bool need = false;
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) {
+            const int a = j == 0 ? nl : lo[j - 1], bb = j == PPL - 1 ? nr : lo[j + 1];
+            need |= min(max(a, bb), m[j]) > lo[j];
+        }
+        int u[PPL];
+#pragma unroll
+        for (int j = 0; j < PPL; ++j) u[j] = lo[j];
+        if (__any_sync(FULL, need)) {
+            // left -> right: the lane's clamp is pixel PPL-1 o ... o pixel 0
+            int FL = lo[0], FH = m[0];
+#pragma unroll
+            for (int j = 1; j < PPL; ++j) {
+                FL = min(m[j], max(lo[j], FL));
+                FH = min(m[j], max(lo[j], FH));
+            }
+            int in = __shfl_up_sync(FULL, clamp_scan<true>(FL, FH, lane), 1);
+            if (lane == 0) in = 0;
+            int fw[PPL];
+#pragma unroll
+            for (int j = 0; j < PPL; ++j) {
+                in = min(m[j], max(lo[j], in));
+                fw[j] = in;
+            }
+            // right -> left
+            int BL = lo[PPL - 1], BH = m[PPL - 1];
+#pragma unroll
+            for (int j = PPL - 2; j >= 0; --j) {
+                BL = min(m[j], max(lo[j], BL));
+                BH = min(m[j], max(lo[j], BH));
+            }
+            int ib = __shfl_down_sync(FULL, clamp_scan<false>(BL, BH, lane), 1);
+            if (lane == 31) ib = 0;
+#pragma unroll
+            for (int j = PPL - 1; j >= 0; --j) {
+                ib = min(m[j], max(lo[j], ib));
+                u[j] = max(fw[j], ib);
+            }
+        }
         __syncwarp();
-        if (u != rr) sRw[bidx(wr, wc)] = (uint8_t)u;
+#pragma unroll
+        for (int j = 0; j < PPL; ++j)
+            if (u[j] != rr[j]) sRw[bidx(wr, c0 + j)] = (uint8_t)u[j];
         __syncwarp();
         return true;
     };
@@ -183,10 +247,10 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : 2) k_region_mr8(const 
         const int t = S.job;
         if (t < 0) break;
         const int rx = t % wl.ntx, ry = t / wl.ntx;
-        const int X0 = rx * RX * kTile, Y0 = ry * RY * kTile;
+        const int X0 = rx * RX * SW, Y0 = ry * RY * kTile;
         // interior regions (window fully inside the image, rows 4-byte aligned) take the
         // unconditional vector path
-        const bool inner = X0 >= 4 && X0 + RX * kTile + 4 <= w && Y0 >= 1 && Y0 + RY * kTile + 1 <= h &&
+        const bool inner = X0 >= 4 && X0 + RX * SW + 4 <= w && Y0 >= 1 && Y0 + RY * kTile + 1 <= h &&
                            (w & 3) == 0 && (((uintptr_t)R | (uintptr_t)mask) & 3) == 0;
         bool have_window = false;
         while (true) {
@@ -266,7 +330,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : 2) k_region_mr8(const 
                 // pend == 0 iff no sub-tile of the region has work left.
                 int iters = 0;
                 int nrows = 0;
-                const int c = wc0 + lane + 1, r = wr0 + lane + 1;
+                const int r = wr0 + lane + 1;
                 while (true) {
                     uint32_t dirty = 0;
                     if (lane == 0 && *reinterpret_cast<volatile uint32_t*>(&S.dirty[warp]))
@@ -306,22 +370,26 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : 2) k_region_mr8(const 
                         const bool mine_row = (chg >> lane) & 1;
 #pragma unroll
                         for (int d = -1; d <= 1; ++d) {
-                            if (sy > 0 && (chg & 1) && improves(wr0 + 1, c, wr0, c + d)) {
-                                if (c + d == wc0) { if (sx > 0) m8[0] |= TOP; }
-                                else if (c + d == wc0 + kTile + 1) { if (sx < RX - 1) m8[2] |= TOP; }
-                                else m8[1] |= TOP;
-                            }
-                            if (sy < RY - 1 && (chg >> 31) && improves(wr0 + kTile, c, wr0 + kTile + 1, c + d)) {
-                                if (c + d == wc0) { if (sx > 0) m8[5] |= BOT; }
-                                else if (c + d == wc0 + kTile + 1) { if (sx < RX - 1) m8[7] |= BOT; }
-                                else m8[6] |= BOT;
+#pragma unroll
+                            for (int j = 0; j < PPL; ++j) {
+                                const int c = wc0 + PPL * lane + 1 + j;
+                                if (sy > 0 && (chg & 1) && improves(wr0 + 1, c, wr0, c + d)) {
+                                    if (c + d == wc0) { if (sx > 0) m8[0] |= TOP; }
+                                    else if (c + d == wc0 + SW + 1) { if (sx < RX - 1) m8[2] |= TOP; }
+                                    else m8[1] |= TOP;
+                                }
+                                if (sy < RY - 1 && (chg >> 31) && improves(wr0 + kTile, c, wr0 + kTile + 1, c + d)) {
+                                    if (c + d == wc0) { if (sx > 0) m8[5] |= BOT; }
+                                    else if (c + d == wc0 + SW + 1) { if (sx < RX - 1) m8[7] |= BOT; }
+                                    else m8[6] |= BOT;
+                                }
                             }
                             if (sx > 0 && mine_row && improves(r, wc0 + 1, r + d, wc0)) {
                                 if (r + d == wr0) { if (sy > 0) m8[0] |= TOP; }
                                 else if (r + d == wr0 + kTile + 1) { if (sy < RY - 1) m8[5] |= BOT; }
                                 else m8[3] |= 1u << (lane + d);
                             }
-                            if (sx < RX - 1 && mine_row && improves(r, wc0 + kTile, r + d, wc0 + kTile + 1)) {
+                            if (sx < RX - 1 && mine_row && improves(r, wc0 + SW, r + d, wc0 + SW + 1)) {
                                 if (r + d == wr0) { if (sy > 0) m8[2] |= TOP; }
                                 else if (r + d == wr0 + kTile + 1) { if (sy < RY - 1) m8[7] |= BOT; }
                                 else m8[4] |= 1u << (lane + d);
@@ -349,13 +417,14 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : 2) k_region_mr8(const 
                 if (lane == 0) atomicAdd(&wl.ctr[6], (unsigned long long)nrows);
                 // write back the changed rows of this sub-tile (interior words)
                 if (mychg) {
-                    for (int k = lane; k < kTile * 8; k += 32) {
-                        int y = 1 + (k >> 3), wi = k & 7;
+                    constexpr int WPR = SW / 4;  // words per sub-tile row
+                    for (int k = lane; k < kTile * WPR; k += 32) {
+                        int y = 1 + k / WPR, wi = k % WPR;
                         if (!((mychg >> (y - 1)) & 1)) continue;
                         int gx = X0 + wc0 + 4 * wi, gy = Y0 + wr0 + y - 1;
                         if (gy >= h || gx >= w) continue;
                         uint8_t* dst = R + (int64_t)gy * w + gx;
-                        uint32_t v = S.R[(wr0 + y) * RWW + sx * 8 + 1 + wi];
+                        uint32_t v = S.R[(wr0 + y) * RWW + sx * WPR + 1 + wi];
                         if (gx + 3 < w && (((uintptr_t)dst) & 3) == 0) {
                             __stcg(reinterpret_cast<unsigned int*>(dst), v);
                         } else {
@@ -366,33 +435,37 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : 2) k_region_mr8(const 
                     __threadfence();
                     // activations of sub-tiles in neighbouring regions (edges of the region)
                     uint32_t m8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                    const int c = wc0 + lane + 1, r = wr0 + lane + 1;
+                    const int r = wr0 + lane + 1;
                     constexpr uint32_t TOP = 1u << 31, BOT = 1u;
 #pragma unroll
                     for (int d = -1; d <= 1; ++d) {
-                        if (sy == 0 && improves(wr0 + 1, c, wr0, c + d)) {
-                            if (c + d == wc0) m8[0] |= TOP;
-                            else if (c + d == wc0 + kTile + 1) m8[2] |= TOP;
-                            else m8[1] |= TOP;
-                        }
-                        if (sy == RY - 1 && improves(wr0 + kTile, c, wr0 + kTile + 1, c + d)) {
-                            if (c + d == wc0) m8[5] |= BOT;
-                            else if (c + d == wc0 + kTile + 1) m8[7] |= BOT;
-                            else m8[6] |= BOT;
+#pragma unroll
+                        for (int j = 0; j < PPL; ++j) {
+                            const int c = wc0 + PPL * lane + 1 + j;
+                            if (sy == 0 && improves(wr0 + 1, c, wr0, c + d)) {
+                                if (c + d == wc0) m8[0] |= TOP;
+                                else if (c + d == wc0 + SW + 1) m8[2] |= TOP;
+                                else m8[1] |= TOP;
+                            }
+                            if (sy == RY - 1 && improves(wr0 + kTile, c, wr0 + kTile + 1, c + d)) {
+                                if (c + d == wc0) m8[5] |= BOT;
+                                else if (c + d == wc0 + SW + 1) m8[7] |= BOT;
+                                else m8[6] |= BOT;
+                            }
                         }
                         if (sx == 0 && improves(r, wc0 + 1, r + d, wc0)) {
                             if (r + d == wr0) m8[0] |= TOP;
                             else if (r + d == wr0 + kTile + 1) m8[5] |= BOT;
                             else m8[3] |= 1u << (lane + d);
                         }
-                        if (sx == RX - 1 && improves(r, wc0 + kTile, r + d, wc0 + kTile + 1)) {
+                        if (sx == RX - 1 && improves(r, wc0 + SW, r + d, wc0 + SW + 1)) {
                             if (r + d == wr0) m8[2] |= TOP;
                             else if (r + d == wr0 + kTile + 1) m8[7] |= BOT;
                             else m8[4] |= 1u << (lane + d);
                         }
                     }
                     // (diagonal reach across the region edge from an inner sub-tile's corner is
-                    // covered by the top/bottom row checks: c + d == wc0 / wc0 + 33)
+                    // covered by the top/bottom row checks: c + d == wc0 / wc0 + SW + 1)
                     uint32_t mine = 0;
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
@@ -449,7 +522,7 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
                              cudaStream_t s) {
     if ((int64_t)w * h == 0) return;
     Worklist wl = wl0;
-    wl.ntx = (w + RX * kTile - 1) / (RX * kTile);
+    wl.ntx = (w + RX * SW - 1) / (RX * SW);
     wl.nty = (h + RY * kTile - 1) / (RY * kTile);
     const int n = wl.ntx * wl.nty;
     (note_launch(), k_rg_reset<<<(int)std::min<int64_t>((std::max<int64_t>(wl.cap, (int64_t)n * NW) + 255) / 256, 148 * 16), 256, 0, s>>>(wl));
