@@ -4,8 +4,8 @@
 // open = dilate_D(erode_D(g)).  D's row dy covers dx in [-hw(dy), hw(dy)] with hw(dy) =
 // round(sqrt(r^2 - dy^2)); so min over D = min over rows of a horizontal running min whose
 // half-width takes only a few distinct values (6 for diam 19).  Bound by the plain integer
-// ALUs: every step works on 4 pixels per 32-bit register with the SIMD byte
-// min/max (__vminu4 / __vmaxu4).
+// ALUs: the 19x19 fast path works on 2 pixels per register with the native
+// 3-input u16x2 min/max; the generic path on 4 pixels with the byte SIMD __vminu4/__vmaxu4.
 //   stage 1: the (TH + 2r) input rows of a TW-wide tile (+ halo) are staged in shared memory
 //            as 32-bit words (aligned vector loads; out-of-tile bytes = identity);
 //   stage 2: per row and output word: the 2*RW+2 covering words go to registers once, every
@@ -67,99 +67,113 @@ struct Ellipse {
 };
 
 // ---------------------------------------------------------------- radius-specialised kernel
+// sm_100a has native 16-bit-lane min/max with three inputs (VIMNMX3.U16x2) but emulates the
+// byte-lane __vminu4 with ~7 LOP3/PRMT/IADD instructions (SASS, r1), so the fast path keeps
+// 2 pixels per 32-bit word in u16 lanes: a running min over [-k, k] costs one 3-input op per
+// step, the vertical combine one per two rows.
+template <bool IS_MIN>
+__device__ __forceinline__ uint32_t vop3(uint32_t a, uint32_t b, uint32_t c) {
+    return IS_MIN ? __vimin3_u16x2(a, b, c) : __vimax3_u16x2(a, b, c);
+}
+
+constexpr int TW2 = 64;        // output tile width (pixels) = 32 u16x2 words
+constexpr int TH2 = 32;        // output tile height
+
 template <bool IS_MIN, int R>
 __global__ void __launch_bounds__(256) k_morph_r(const uint8_t* __restrict__ src, int w, int h,
                                                  uint8_t* __restrict__ dst) {
     constexpr Ellipse<R> E{};
     constexpr int ND = E.n;
-    constexpr int RW = (R + 3) / 4;              // halo words each side
-    constexpr int IW = TWW + 2 * RW + 1;         // staged words per row
-    constexpr int ROWS = TH + 2 * R;
-    constexpr uint32_t ID = IS_MIN ? 0xffffffffu : 0u;
+    constexpr int RW = 2 * ((R + 3) / 4);        // halo words (2 px each) per side: 4-px aligned
+    constexpr int IW = 32 + 2 * RW + 2;          // staged words per row (even: loads in pairs)
+    constexpr int ROWS = TH2 + 2 * R;
+    constexpr uint32_t ID = IS_MIN ? 0x00ff00ffu : 0u;
     extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t* in = smem;                          // [ROWS][IW]
-    uint32_t* H = smem + ROWS * IW;               // [ND][ROWS][TWW]
-    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
+    uint32_t* in = smem;                          // [ROWS][IW] u16x2
+    uint32_t* H = smem + ROWS * IW;               // [ND][ROWS][32]
+    const int x0 = blockIdx.x * TW2, y0 = blockIdx.y * TH2;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const bool row_aligned = (w & 3) == 0 && (((uintptr_t)src) & 3) == 0;
 
-    // stage 1: words [x0/4 - RW, x0/4 + TWW + RW + 1) of rows [y0 - R, y0 + TH + R)
-    for (int r = ty; r < ROWS; r += 8) {
+    // stage 1: pixels [x0 - 2RW, x0 + 64 + 2RW + 2) of rows [y0 - R, y0 + TH2 + R), 4 px per load
+    constexpr int NQ = IW / 2;  // 4-pixel groups per row
+    for (int i = threadIdx.x; i < ROWS * NQ; i += blockDim.x) {
+        const int r = i / NQ, q = i - r * NQ;
         const int gy = y0 - R + r;
-        const bool rin = gy >= 0 && gy < h;
-        const uint8_t* rowp = src + (int64_t)(rin ? gy : 0) * w;
-        for (int wi = tx; wi < IW; wi += 32) {
-            const int gx = x0 - 4 * RW + 4 * wi;
-            uint32_t v = ID;
-            if (rin) {
-                if (row_aligned && gx >= 0 && gx + 3 < w) {
-                    v = __ldg(reinterpret_cast<const unsigned int*>(rowp + gx));
-                } else {
+        const int gx = x0 - 2 * RW + 4 * q;
+        uint32_t v = IS_MIN ? 0xffffffffu : 0u;
+        if (gy >= 0 && gy < h) {
+            const uint8_t* rowp = src + (int64_t)gy * w;
+            if (row_aligned && gx >= 0 && gx + 3 < w) {
+                v = __ldg(reinterpret_cast<const unsigned int*>(rowp + gx));
+            } else {
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        int x = gx + b;
-                        uint32_t byte = (x >= 0 && x < w) ? (uint32_t)__ldg(rowp + x) : (ID & 0xffu);
-                        v = (v & ~(0xffu << (8 * b))) | (byte << (8 * b));
-                    }
+                for (int b = 0; b < 4; ++b) {
+                    const int x = gx + b;
+                    const uint32_t byte = (x >= 0 && x < w) ? (uint32_t)__ldg(rowp + x) : (IS_MIN ? 0xffu : 0u);
+                    v = (v & ~(0xffu << (8 * b))) | (byte << (8 * b));
                 }
             }
-            in[r * IW + wi] = v;
         }
+        in[r * IW + 2 * q] = __byte_perm(v, 0, 0x4140);      // px 0, 1 -> u16 lanes
+        in[r * IW + 2 * q + 1] = __byte_perm(v, 0, 0x4342);  // px 2, 3
     }
     __syncthreads();
 
-    // stage 2: horizontal running min/max for the distinct half-widths
+    // stage 2: horizontal running min/max for the distinct half-widths; one warp per row,
+    // lane = output word (pixels 2j, 2j+1)
     for (int r = ty; r < ROWS; r += 8) {
         const uint32_t* rowp = in + r * IW;
-        const int j = tx;  // output word
+        const int j = tx;
         uint32_t wv[2 * RW + 2];
 #pragma unroll
         for (int k = 0; k < 2 * RW + 2; ++k) wv[k] = rowp[j + k];
-        // window at byte offset k (relative to the output word's first byte)
-        auto win = [&](int k) -> uint32_t {
-            const int o = 4 * RW + k;  // byte offset into wv
-            return __funnelshift_r(wv[o >> 2], wv[(o >> 2) + 1], 8 * (o & 3));
+        auto win = [&](int k) -> uint32_t {  // pixels (2j + k, 2j + 1 + k)
+            const int o = 2 * RW + k;
+            return (o & 1) ? __funnelshift_r(wv[o >> 1], wv[(o >> 1) + 1], 16) : wv[o >> 1];
         };
         uint32_t m = wv[RW];
-        int di = 0;
-        if (E.hw[0] == 0) {
-            H[(0 * ROWS + r) * TWW + j] = m;
-            di = 1;
-        }
+#pragma unroll
+        for (int q = 0; q < ND; ++q)
+            if (E.hw[q] == 0) H[(q * ROWS + r) * 32 + j] = m;
 #pragma unroll
         for (int k = 1; k <= R; ++k) {
-            m = vop<IS_MIN>(m, vop<IS_MIN>(win(k), win(-k)));
+            m = vop3<IS_MIN>(m, win(k), win(-k));
 #pragma unroll
             for (int q = 0; q < ND; ++q)
-                if (E.hw[q] == k) H[(q * ROWS + r) * TWW + j] = m;
+                if (E.hw[q] == k) H[(q * ROWS + r) * 32 + j] = m;
         }
-        (void)di;
     }
     __syncthreads();
 
-    // stage 3: vertical combine over the diam rows of D
+    // stage 3: vertical combine over the 2R+1 rows of D (two rows per 3-input op)
     const int j = tx;
-    const int gx = x0 + 4 * j;
-    for (int oy = ty; oy < TH; oy += 8) {
+    const int gx = x0 + 2 * j;
+    for (int oy = ty; oy < TH2; oy += 8) {
         const int gy = y0 + oy;
         if (gy >= h || gx >= w) continue;
-        uint32_t m = ID;
+        uint32_t m = H[(E.idx_of_dy[0] * ROWS + oy) * 32 + j];
 #pragma unroll
-        for (int dy = 0; dy <= 2 * R; ++dy) m = vop<IS_MIN>(m, H[(E.idx_of_dy[dy] * ROWS + oy + dy) * TWW + j]);
+        for (int dy = 1; dy + 1 <= 2 * R; dy += 2)
+            m = vop3<IS_MIN>(m, H[(E.idx_of_dy[dy] * ROWS + oy + dy) * 32 + j],
+                             H[(E.idx_of_dy[dy + 1] * ROWS + oy + dy + 1) * 32 + j]);
+        const uint32_t pk = __byte_perm(m, 0, 0x0020);  // u16 lanes -> 2 bytes
         uint8_t* o = dst + (int64_t)gy * w + gx;
-        if (gx + 3 < w && (((uintptr_t)o) & 3) == 0) {
-            *reinterpret_cast<uint32_t*>(o) = m;
+        if (gx + 1 < w && (((uintptr_t)o) & 1) == 0) {
+            *reinterpret_cast<uint16_t*>(o) = (uint16_t)pk;
         } else {
-            for (int b = 0; b < 4 && gx + b < w; ++b) o[b] = (uint8_t)(m >> (8 * b));
+            o[0] = (uint8_t)pk;
+            if (gx + 1 < w) o[1] = (uint8_t)(pk >> 8);
         }
     }
+    (void)ID;
 }
 
 template <int R>
 size_t smem_r() {
     constexpr Ellipse<R> E{};
-    constexpr int RW = (R + 3) / 4;
-    return 4 * (size_t)(TH + 2 * R) * ((TWW + 2 * RW + 1) + (size_t)E.n * TWW);
+    constexpr int RW = 2 * ((R + 3) / 4);
+    return 4 * (size_t)(TH2 + 2 * R) * ((32 + 2 * RW + 2) + (size_t)E.n * 32);
 }
 
 template <int R>
@@ -171,7 +185,7 @@ void launch_r(const uint8_t* g, int w, int h, uint8_t* tmp, uint8_t* out, cudaSt
         cudaFuncSetAttribute(k_morph_r<false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    dim3 grid((w + TW - 1) / TW, (h + TH - 1) / TH);
+    dim3 grid((w + TW2 - 1) / TW2, (h + TH2 - 1) / TH2);
     (note_launch(), k_morph_r<true, R><<<grid, 256, smem, s>>>(g, w, h, tmp));
     (note_launch(), k_morph_r<false, R><<<grid, 256, smem, s>>>(tmp, w, h, out));
 }
