@@ -7,8 +7,8 @@
 // launches and three device-wide worklists per tile for objects of ~100-1000 pixels; here one
 // CTA owns one component:
 //   shared-memory path (k_comp_fused) -- one WARP per component for windows (bbox + 1-px
-//     ring) <= 640 px (~99% of nuclei; warp-synchronous, 16 components in flight per SM), one
-//     4-warp block for <= 2560 px: the window is staged in smem
+//     ring) <= 576 px (~99% of nuclei; warp-synchronous, 16 components in flight per SM), one
+//     4-warp block for <= 2432 px: the window is staged in smem
 //     (membership, dist); the max-clamp / min-plus / min relaxations (J, W1, W2, W3) iterate
 //     to their fixed points with __syncthreads_or convergence; flat zones and the final
 //     objects are labelled by union-find in smem (CAS hooking, min-index roots); then the
@@ -109,14 +109,18 @@ struct CompArgs {
     int32_t gobj_cap;
 };
 
+// find with CAS path halving (x -> grandparent iff x still points at that parent; safe beside
+// concurrent CAS hooks, which only ever re-point roots)
 __device__ __forceinline__ int cfind(int* P, int x) {
     volatile int* vp = P;
-    int p = vp[x];
-    while (p != x) {
-        x = p;
-        p = vp[x];
+    while (true) {
+        const int p = vp[x];
+        if (p == x) return x;
+        const int gp = vp[p];
+        if (gp == p) return p;
+        atomicCAS(&P[x], p, gp);
+        x = gp;
     }
-    return x;
 }
 __device__ __forceinline__ void cunion(int* P, int a, int b) {
     while (true) {
@@ -149,9 +153,11 @@ struct CompSm {
     float A[CAP];      // J, then c
     int32_t B[CAP];    // zone union-find, then L, then object union-find
     int32_t C[CAP];    // zone flags, then d, then object areas
+    int16_t list[CAP];  // member pixels (window indices), compacted once
     uint8_t mem[CAP];
     uint8_t pm[CAP];
     uint8_t sp[CAP];
+    int nmem;
     int nobj;
     int objroot[KO];
     FeatSmem fs;
@@ -173,27 +179,43 @@ __device__ bool comp_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, c
         int ly = li / WX, lx = li - ly * WX;
         return (int32_t)((int64_t)(wy0 + ly) * w + (wx0 + lx));
     };
-    // ---- stage the window (ring pixels are never members: no bounds checks later)
-    for (int li = tr; li < NWIN; li += TS) {
-        int ly = li / WX, lx = li - ly * WX;
-        int gx = wx0 + lx, gy = wy0 + ly;
-        uint8_t m = 0;
-        float dv = 0.f;
-        if (gx >= 0 && gy >= 0 && gx < w && gy < h) {
-            int64_t p = (int64_t)gy * w + gx;
-            if (a.labF[p] == root) {
-                m = 1;
-                dv = a.dist[p];
-            }
-        }
-        S.mem[li] = m;
-        S.dist[li] = dv;
+    // ---- stage the window (ring pixels are never members: no bounds checks later) and list
+    // the members, so every later pass touches members only
+    if (tr == 0) {
+        S.nobj = 0;
+        S.nmem = 0;
     }
-    if (tr == 0) S.nobj = 0;
     team.sync();
+    int nmem = 0;
+    for (int base = 0; base < NWIN; base += TS) {
+        const int li = base + tr;
+        bool m = false;
+        if (li < NWIN) {
+            const int ly = li / WX, lx = li - ly * WX;
+            const int gx = wx0 + lx, gy = wy0 + ly;
+            float dv = 0.f;
+            if (gx >= 0 && gy >= 0 && gx < w && gy < h) {
+                const int64_t p = (int64_t)gy * w + gx;
+                if (a.labF[p] == root) {
+                    m = true;
+                    dv = a.dist[p];
+                }
+            }
+            S.mem[li] = m;
+            S.dist[li] = dv;
+        }
+        if constexpr (TS == 32) {  // warp team: ballot compaction (window order)
+            const unsigned bal = __ballot_sync(0xffffffffu, m);
+            if (m) S.list[nmem + __popc(bal & ((1u << tr) - 1u))] = (int16_t)li;
+            nmem += __popc(bal);
+        } else {
+            if (m) S.list[atomicAdd(&S.nmem, 1)] = (int16_t)li;
+        }
+    }
+    team.sync();
+    if constexpr (TS != 32) nmem = S.nmem;
     auto each = [&](auto fn) {
-        for (int li = tr; li < NWIN; li += TS)
-            if (S.mem[li]) fn(li);
+        for (int k = tr; k < nmem; k += TS) fn((int)S.list[k]);
     };
     auto converge = [&](auto step) {
         while (true) {
@@ -399,9 +421,13 @@ __device__ bool comp_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, c
     return true;
 }
 
-constexpr int kCapW = 640, kKoW = 48;    // warp team: windows up to 640 px (~99% of nuclei)
+#ifndef HP_CAPW
+#define HP_CAPW 576  // 4 blocks of 4 warps per SM (measured r1: 0.54 ms vs 0.57 at 640)
+#define HP_CAPB 2432
+#endif
+constexpr int kCapW = HP_CAPW, kKoW = 48;  // warp team: windows up to kCapW px (~99% of nuclei)
 constexpr int kWarpsPB = 4;
-constexpr int kCapB = 2560, kKoB = 160;  // block team (4 warps): the same shared memory, one window
+constexpr int kCapB = HP_CAPB, kKoB = 160; // block team (4 warps): the same shared memory, one window
 static_assert(sizeof(CompSm<kCapB, kKoB>) <= kWarpsPB * sizeof(CompSm<kCapW, kKoW>), "block window too big");
 
 __device__ __forceinline__ int win_px(int4 bb) { return (bb.z - bb.x + 3) * (bb.w - bb.y + 3); }
