@@ -155,6 +155,10 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
     ev(ctx, sl, 3, s);
     launch_recon_init_u8(sl.u8a, sl.g, sl.u8b, w, h, s);                                              // S4
     launch_recon_u8_auto(sl.g, sl.u8b, w, h, sl.wl, s);
+#ifdef HP_WHATIF_S4X2  // experiment only: a second, independent S4 into scratch (marginal cost)
+    launch_recon_init_u8(sl.u8a, sl.g, sl.pmask, w, h, s);
+    launch_recon_u8_auto(sl.g, sl.pmask, w, h, sl.wl, s);
+#endif
     launch_tophat(sl.g, sl.u8b, sl.rbc, p.g1, w, h, sl.cand, s);
     ev(ctx, sl, 4, s);
     launch_area_select(sl.cand, w, h, p.cand_min_area, p.cand_max_area, sl, sl.big0, s);           // S5

@@ -30,6 +30,12 @@ constexpr unsigned FULL = 0xffffffffu;
 #define HP_RX 4
 #define HP_RY 4
 #endif
+#ifndef HP_RG_WAITERS
+#define HP_RG_WAITERS 4
+#endif
+#ifndef HP_RG_MIN_ALIVE
+#define HP_RG_MIN_ALIVE 16
+#endif
 #ifndef HP_POLL_NS
 #define HP_POLL_NS 400  // idle sub-tile warps back off (frees issue slots for co-running work)
 #endif
@@ -238,8 +244,23 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : 2) k_region_mr8(const 
 
     while (true) {
         if (threadIdx.x == 0) {
-            int t = q_pop(wl);
-            if (t >= 0) atomicExch(&wl.state[t], ST_BUSY);
+            // Retire instead of queueing for work when HP_RG_WAITERS CTAs already wait on an
+            // empty queue (at least HP_RG_MIN_ALIVE stay): on chain-bound tiles only a few
+            // dozen regions are active at a time, and idle CTAs would hold a quarter of every
+            // SM's threads and half its registers from the other slots' kernels for
+            // milliseconds.  Only a CTA without a ticket retires, so no pushed job is lost.
+            int t = -1;
+            const unsigned long long hd = vload(&wl.ctr[0]), tl = vload(&wl.ctr[1]);
+            bool retire = false;
+            if (hd >= tl + HP_RG_WAITERS) {
+                const unsigned long long r = atomicAdd(&wl.ctr[7], 1ull);
+                if (r + HP_RG_MIN_ALIVE < gridDim.x) retire = true;
+                else atomicAdd(&wl.ctr[7], ~0ull);
+            }
+            if (!retire) {
+                t = q_pop(wl);
+                if (t >= 0) atomicExch(&wl.state[t], ST_BUSY);
+            }
             S.t0 = gtimer();
             S.job = t;
         }
