@@ -30,6 +30,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #define HP_RX 4
 #define HP_RY 4
 #endif
+#ifndef HP_RG_ORDER
+#define HP_RG_ORDER 1  // initial job order: 0 raster, 1 four-colour (r1: 3018 -> 2165 jobs, 689 -> 725 tiles/s)
+#endif
 #ifndef HP_RG_WAITERS
 #define HP_RG_WAITERS 4
 #endif
@@ -531,7 +534,27 @@ __global__ void k_rg_reset(Worklist wl) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < lim; i += gridDim.x * blockDim.x) {
         if (i < n) wl.state[i] = ST_QUEUED;
         if (i < n * NW) wl.inrows[i] = 0xffffffffu;
-        if (i < wl.cap) wl.queue[i] = i < n ? i : EMPTY;
+        if (i < wl.cap) {
+            int32_t v = EMPTY;
+            if (i < n) {
+#if HP_RG_ORDER == 1
+                // 4-colour order (x parity, y parity): no two regions of one colour are
+                // 8-adjacent, so a wave of one colour never reads a neighbour mid-update
+                int k = i, c = 0;
+                for (; c < 4; ++c) {
+                    const int nx = (wl.ntx - (c & 1) + 1) / 2, ny = (wl.nty - (c >> 1) + 1) / 2;
+                    if (k < nx * ny) {
+                        v = (2 * (k / nx) + (c >> 1)) * wl.ntx + 2 * (k % nx) + (c & 1);
+                        break;
+                    }
+                    k -= nx * ny;
+                }
+#else
+                v = i;
+#endif
+            }
+            wl.queue[i] = v;
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x < 8)
         wl.ctr[threadIdx.x] = (threadIdx.x == 1 || threadIdx.x == 2) ? (unsigned long long)n : 0ull;
