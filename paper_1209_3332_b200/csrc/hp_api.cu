@@ -13,6 +13,8 @@
 #include <new>
 #include <string>
 #include <vector>
+#include <thread>
+#include <chrono>
 
 #include "hp_internal.cuh"
 
@@ -620,23 +622,15 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
         --inflight;
         return HP_OK;
     };
-    int next_slot = 0;
-    while (true) {
-        int i = next_slot;
-        next_slot = (next_slot + 1) % ns;
-        if (tile_of[i] >= 0) {
-            if ((st = deliver(i))) return st;
-        }
-        if (drained) {
-            if (inflight == 0) break;
-            continue;
-        }
+    // Fill every free slot, then deliver whichever in-flight slot finishes first: tiles take
+    // very different times (chain-bound reconstructions), so waiting on slots in a fixed
+    // order would leave finished slots idle behind a slow one.
+    auto submit = [&](int i) -> hp_status {
         const uint8_t* host = nullptr;
         int64_t pitch = 0, tid = -1;
         if (src->next(src->user, &host, &pitch, &tid) != 0) {
             drained = true;
-            if (inflight == 0) break;
-            continue;
+            return HP_OK;
         }
         if (!host || pitch < 3LL * w) return HP_ERR_INVALID;
         Slot& sl = ctx->slots[i];
@@ -645,18 +639,39 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
         hp_image im{sl.rgb_dev, w, h, 3LL * w};
         hp_feature_table tab{sl.tab_label, sl.tab_flags, sl.tab_feat, mo, sl.tab_nrows};
         bool fused = false;
-        st = segment(ctx, sl, &im, sl.lab_dev, w, sl.cnt32 + 4, s, &tab, &fused);
-        if (!st && !fused) st = features(ctx, sl, w, h, sl.lab_dev, w, &tab, s);
-        if (st) return st;
+        hp_status r = segment(ctx, sl, &im, sl.lab_dev, w, sl.cnt32 + 4, s, &tab, &fused);
+        if (!r && !fused) r = features(ctx, sl, w, h, sl.lab_dev, w, &tab, s);
+        if (r) return r;
         cudaMemcpyAsync(sl.h_nrows, sl.tab_nrows, 4, cudaMemcpyDeviceToHost, s);
         cudaMemcpyAsync(sl.h_label, sl.tab_label, 4 * (size_t)ctx->rows_copied, cudaMemcpyDeviceToHost, s);
         cudaMemcpyAsync(sl.h_flags, sl.tab_flags, 4 * (size_t)ctx->rows_copied, cudaMemcpyDeviceToHost, s);
         cudaMemcpyAsync(sl.h_feat, sl.tab_feat, 4 * (size_t)ctx->rows_copied * HP_NFEAT, cudaMemcpyDeviceToHost, s);
         cudaEventRecord(sl.done_ev, s);
-        if ((st = check_launch(ctx, "run_tiles"))) return st;
+        if ((r = check_launch(ctx, "run_tiles"))) return r;
         tile_of[i] = tid;
         st_of[i] = HP_OK;
         ++inflight;
+        return HP_OK;
+    };
+    int scan = 0;
+    while (true) {
+        for (int i = 0; i < ns && !drained; ++i)
+            if (tile_of[i] < 0 && (st = submit(i))) return st;
+        if (inflight == 0) break;
+        int done = -1;
+        for (int k = 0; k < ns && done < 0; ++k) {
+            const int i = (scan + k) % ns;
+            if (tile_of[i] < 0) continue;
+            const cudaError_t q = cudaEventQuery(ctx->slots[i].done_ev);
+            if (q == cudaSuccess) done = i;
+            else if (q != cudaErrorNotReady) return cuda_fail(ctx, q, "run_tiles query");
+        }
+        if (done < 0) {
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+            continue;
+        }
+        scan = (done + 1) % ns;
+        if ((st = deliver(done))) return st;
     }
     return HP_OK;
 }
