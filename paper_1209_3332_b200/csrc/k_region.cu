@@ -30,6 +30,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #define HP_RX 4
 #define HP_RY 4
 #endif
+#ifndef HP_RG_MINB
+#define HP_RG_MINB 2  // launch-bounds min blocks: 2 -> <= 64 registers per thread
+#endif
 #ifndef HP_RG_ORDER
 #define HP_RG_ORDER 1  // initial job order: 0 raster, 1 four-colour (r1: 3018 -> 2165 jobs, 689 -> 725 tiles/s)
 #endif
@@ -40,7 +43,10 @@ constexpr unsigned FULL = 0xffffffffu;
 #define HP_RG_MIN_ALIVE 16
 #endif
 #ifndef HP_POLL_NS
-#define HP_POLL_NS 400  // idle sub-tile warps back off (frees issue slots for co-running work)
+#define HP_POLL_NS 400       // idle sub-tile warps back off (frees issue slots for co-running work)
+#endif
+#ifndef HP_POLL_MAX_NS
+#define HP_POLL_MAX_NS 1600  // back-off cap (r1: 400-6400 within noise in bench.py)
 #endif
 #ifndef HP_PPL
 #define HP_PPL 2  // pixels per lane: sub-tiles of 64 x 32 px, regions of 256 x 128 px
@@ -145,7 +151,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // byte of window pixel (wr, wc): window column wc (0 .. RX*32+1) is byte wc + 3
 __device__ __forceinline__ int bidx(int wr, int wc) { return wr * RWB + wc + 3; }
 
-__global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : 2) k_region_mr8(const uint8_t* __restrict__ mask,
+__global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_t* __restrict__ mask,
                                                            uint8_t* __restrict__ R, int w, int h,
                                                            Worklist wl) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -355,6 +361,7 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : 2) k_region_mr8(const 
                 int iters = 0;
                 int nrows = 0;
                 const int r = wr0 + lane + 1;
+                unsigned backoff = HP_POLL_NS;
                 while (true) {
                     uint32_t dirty = 0;
                     if (lane == 0 && *reinterpret_cast<volatile uint32_t*>(&S.dirty[warp]))
@@ -362,9 +369,13 @@ __global__ void __launch_bounds__(NW * 32, NW >= 32 ? 1 : 2) k_region_mr8(const 
                     dirty = __shfl_sync(FULL, dirty, 0);
                     if (!dirty) {
                         if (*reinterpret_cast<volatile int*>(&S.pend) == 0) break;
-                        __nanosleep(HP_POLL_NS);
+                        // idle: exponential back-off so waiting warps leave the issue slots to
+                        // the working ones and to co-running kernels
+                        __nanosleep(backoff);
+                        backoff = min(2u * backoff, (unsigned)HP_POLL_MAX_NS);
                         continue;
                     }
+                    backoff = HP_POLL_NS;
                     // Gauss-Seidel sweeps of this sub-tile (see iwpp_rules.cuh sweep_rows)
                     uint32_t chg = 0;
                     while (dirty) {
