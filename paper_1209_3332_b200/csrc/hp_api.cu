@@ -153,17 +153,14 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
     }
     launch_rbc(sl.flags, w, h, sl, sl.rbc, s);                                                      // S2
     ev(ctx, sl, 2, s);
-    launch_open(sl.g, w, h, p.open_diam, sl.u8b, sl.u8a, s);                                          // S3
+    // the opening is anti-extensive (symmetric SE containing the origin, out-of-tile pixels
+    // ignored: open(g) <= g), so S4's marker min(open, g) is the opening itself
+    launch_open(sl.g, w, h, p.open_diam, sl.u8a, sl.u8b, s);                                          // S3
     ev(ctx, sl, 3, s);
-    launch_recon_init_u8(sl.u8a, sl.g, sl.u8b, w, h, s);                                              // S4
-    launch_recon_u8_auto(sl.g, sl.u8b, w, h, sl.wl, s);
-#ifdef HP_WHATIF_S4X2  // experiment only: a second, independent S4 into scratch (marginal cost)
-    launch_recon_init_u8(sl.u8a, sl.g, sl.pmask, w, h, s);
-    launch_recon_u8_auto(sl.g, sl.pmask, w, h, sl.wl, s);
-#endif
-    launch_tophat(sl.g, sl.u8b, sl.rbc, p.g1, w, h, sl.cand, s);
+    launch_recon_u8_auto(sl.g, sl.u8b, w, h, sl.wl, s);                                               // S4
     ev(ctx, sl, 4, s);
-    launch_area_select(sl.cand, w, h, p.cand_min_area, p.cand_max_area, sl, sl.big0, s);           // S5
+    // S5 on the top-hat candidates (g - recon > g1) & !rbc, evaluated inside the CCL passes
+    launch_area_select_tophat(sl.g, sl.u8b, sl.rbc, p.g1, w, h, p.cand_min_area, p.cand_max_area, sl, sl.big0, s);
     ev(ctx, sl, 5, s);
     launch_fill_holes(sl.big0, w, h, sl, sl.F, s);                                                  // S6
     ev(ctx, sl, 6, s);

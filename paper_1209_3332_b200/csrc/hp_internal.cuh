@@ -134,6 +134,8 @@ void launch_rbc(const uint8_t* flags, int w, int h, Slot& sl, uint8_t* rbc, cuda
 void launch_fill_holes(const uint8_t* big0, int w, int h, Slot& sl, uint8_t* F, cudaStream_t s);
 void launch_area_select(const uint8_t* cand, int w, int h, int amin, int amax, Slot& sl, uint8_t* out,
                         cudaStream_t s);
+void launch_area_select_tophat(const uint8_t* g, const uint8_t* R, const uint8_t* rbc, int g1, int w, int h,
+                               int amin, int amax, Slot& sl, uint8_t* out, cudaStream_t s);
 // IWPP / worklist engine
 void wl_init_all(const Worklist& wl, int w, int h, cudaStream_t s);
 void wl_init_from_mask(const Worklist& wl, const uint8_t* mask, int w, int h, cudaStream_t s);

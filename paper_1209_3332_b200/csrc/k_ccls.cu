@@ -30,15 +30,25 @@ constexpr int32_t kAreaMask = (1 << 29) - 1;
 constexpr int32_t kHit = 1 << 29, kTouch = 1 << 30;
 constexpr int kT = kTile;  // 32
 
-enum SelMode { SEL_AREA = 0, SEL_RBC = 1, SEL_FILL = 2 };
+enum SelMode { SEL_AREA = 0, SEL_RBC = 1, SEL_FILL = 2, SEL_AREA_TH = 3 };
 
 struct Sel {
-    const uint8_t* plane;  // SEL_AREA: candidate mask; SEL_RBC: flags; SEL_FILL: big0
+    const uint8_t* plane;  // SEL_AREA: candidate mask; SEL_RBC: flags; SEL_FILL: big0; SEL_AREA_TH: g
     int w, h;
     int amin, amax;
+    const uint8_t* R = nullptr;    // SEL_AREA_TH: the reconstruction
+    const uint8_t* rbc = nullptr;  // SEL_AREA_TH: the RBC mask
+    int g1 = 0;                    // SEL_AREA_TH: top-hat threshold
+    // the pixel's byte: the plane, or for SEL_AREA_TH the top-hat candidate of S4 (PAPER.md:596,
+    // reading C9): (g - recon > g1) & !rbc
+    template <int MODE>
+    __device__ __forceinline__ uint8_t load(int64_t p) const {
+        if (MODE == SEL_AREA_TH) return ((int)__ldg(plane + p) - (int)__ldg(R + p)) > g1 && !__ldg(rbc + p);
+        return __ldg(plane + p);
+    }
     template <int MODE>
     __device__ __forceinline__ bool fg(uint8_t v) const {
-        if (MODE == SEL_AREA) return v != 0;
+        if (MODE == SEL_AREA || MODE == SEL_AREA_TH) return v != 0;
         if (MODE == SEL_RBC) return (v & HP_FLAG_RBC_LO) != 0;
         return v == 0;  // SEL_FILL: background of big0
     }
@@ -51,7 +61,7 @@ struct Sel {
     }
     template <int MODE>
     __device__ __forceinline__ uint8_t out(uint8_t v, bool f, int32_t prop) const {
-        if (MODE == SEL_AREA) {
+        if (MODE == SEL_AREA || MODE == SEL_AREA_TH) {
             const int a = prop & kAreaMask;
             return f && a >= amin && a <= amax;
         }
@@ -146,7 +156,7 @@ __device__ __forceinline__ int tile_uf(const Sel& sel, int conn, int tx0, int ty
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int gy = ty0 + (threadIdx.x >> 5) + 8 * k;
-        v[k] = (gx < w && gy < h) ? __ldg(sel.plane + (int64_t)gy * w + gx) : (uint8_t)0;
+        v[k] = (gx < w && gy < h) ? sel.load<MODE>((int64_t)gy * w + gx) : (uint8_t)0;
     }
     int nfg = 0;
 #pragma unroll
@@ -386,6 +396,15 @@ void launch_rbc(const uint8_t* flags, int w, int h, Slot& sl, uint8_t* rbc, cuda
 void launch_area_select(const uint8_t* cand, int w, int h, int amin, int amax, Slot& sl, uint8_t* out,
                         cudaStream_t s) {
     run_select<SEL_AREA>(Sel{cand, w, h, amin, amax}, 8, sl, out, s);
+}
+
+void launch_area_select_tophat(const uint8_t* g, const uint8_t* R, const uint8_t* rbc, int g1, int w, int h,
+                               int amin, int amax, Slot& sl, uint8_t* out, cudaStream_t s) {
+    Sel sel{g, w, h, amin, amax};
+    sel.R = R;
+    sel.rbc = rbc;
+    sel.g1 = g1;
+    run_select<SEL_AREA_TH>(sel, 8, sl, out, s);
 }
 
 void launch_fill_holes(const uint8_t* big0, int w, int h, Slot& sl, uint8_t* F, cudaStream_t s) {
