@@ -10,8 +10,8 @@ worker, so the data path has no exchange step:
   D2H streams, at most n_slots tiles in flight = the paper's window).
 * ``gather_rows`` -- the one collective: at the end, every rank's feature rows go to rank 0
   (all_gather of counts, then a padded all_gather_into_tensor of packed rows -- NCCL over
-  NVLink on GPUs, gloo on CPU), sorted by (tile_id, label) so the table is identical for
-  any number of GPUs.
+  NVLink on GPUs, gloo on CPU), merged into (tile_id, label) order so the table is identical
+  for any number of GPUs.
 
 torch.distributed is plumbing here; the pixels never leave the GPU that processes them.
 """
@@ -81,54 +81,114 @@ class DistTileSource:
         return t.data_ptr(), t.stride(0) * t.element_size(), tid
 
 
-ROW_DTYPE = np.dtype([("tile", "<i8"), ("label", "<i4"), ("flags", "<i4"), ("feat", "<f4", (NFEAT,))])
+class Rows:
+    """A feature table in columns: tile id, label, flags, 34 features per object row."""
+
+    __slots__ = ("tile", "label", "flags", "feat")
+
+    def __init__(self, tile, label, flags, feat):
+        self.tile = np.ascontiguousarray(tile, dtype=np.int64)
+        self.label = np.ascontiguousarray(label, dtype=np.int32)
+        self.flags = np.ascontiguousarray(flags, dtype=np.int32)
+        self.feat = np.ascontiguousarray(feat, dtype=np.float32).reshape(-1, NFEAT)
+
+    def __len__(self):
+        return int(self.tile.shape[0])
+
+    def take(self, a, b):
+        return Rows(self.tile[a:b], self.label[a:b], self.flags[a:b], self.feat[a:b])
+
+    @staticmethod
+    def concat(parts):
+        if not parts:
+            return Rows(np.empty(0, np.int64), np.empty(0, np.int32), np.empty(0, np.int32),
+                        np.empty((0, NFEAT), np.float32))
+        return Rows(np.concatenate([p.tile for p in parts]), np.concatenate([p.label for p in parts]),
+                    np.concatenate([p.flags for p in parts]), np.concatenate([p.feat for p in parts]))
+
+    def sorted(self):
+        """(tile, label) order -- the canonical table order (reading C14)."""
+        o = np.lexsort((self.label, self.tile))
+        return Rows(self.tile[o], self.label[o], self.flags[o], self.feat[o])
 
 
-def pack_rows(results: dict) -> np.ndarray:
-    """{tile_id: (label[n], flags[n], feat[n, 34])} -> uint8 [N, ROW_BYTES] (tile order)."""
+def to_rows(results: dict) -> Rows:
+    """{tile_id: (label[n], flags[n], feat[n, 34])} -> Rows in tile order (rows of a tile in
+    the order given: hp_run_tiles delivers them by ascending label)."""
     tids = sorted(results)
     counts = [len(results[t][0]) for t in tids]
-    total = int(sum(counts))
-    rec = np.empty(total, dtype=ROW_DTYPE)
-    if total:
-        rec["tile"] = np.repeat(np.asarray(tids, np.int64), counts)
-        rec["label"] = np.concatenate([results[t][0] for t in tids])
-        rec["flags"] = np.concatenate([results[t][1] for t in tids])
-        rec["feat"] = np.concatenate([np.asarray(results[t][2], np.float32).reshape(-1, NFEAT) for t in tids])
-    return rec.view(np.uint8).reshape(total, ROW_BYTES)
+    if not tids or sum(counts) == 0:
+        return Rows.concat([])
+    return Rows(np.repeat(np.asarray(tids, np.int64), counts),
+                np.concatenate([results[t][0] for t in tids]),
+                np.concatenate([results[t][1] for t in tids]),
+                np.concatenate([np.asarray(results[t][2], np.float32).reshape(-1, NFEAT) for t in tids]))
 
 
-def unpack_rows(buf: np.ndarray) -> np.ndarray:
-    return np.ascontiguousarray(buf).view(ROW_DTYPE).reshape(-1)
+_FIELDS = (("tile", np.int64, 8), ("label", np.int32, 4), ("flags", np.int32, 4), ("feat", np.float32, 4 * NFEAT))
 
 
 def gather_rows(results: dict, device=None):
-    """Gather every rank's packed rows on rank 0 (sorted by tile, label); None elsewhere."""
+    """Gather every rank's rows on rank 0 in (tile, label) order; None elsewhere.
+
+    One all_gather of the counts, then one all_gather_into_tensor of a flat per-rank buffer
+    holding each column in its own region (padded to the largest count); rank 0 merges the
+    per-tile runs."""
     import torch
     import torch.distributed as dist
-    local = pack_rows(results)
+    local = to_rows(results)
     if not dist.is_initialized() or dist.get_world_size() == 1:
-        return unpack_rows(local)  # pack_rows emits tile order; rows within a tile are label order
+        return local  # to_rows emits tile order; rows within a tile are label order
     world = dist.get_world_size()
     dev = device if device is not None else torch.device("cpu")
-    cnt = torch.tensor([local.shape[0]], dtype=torch.int64, device=dev)
+    n = len(local)
+    cnt = torch.tensor([n], dtype=torch.int64, device=dev)
     counts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
     dist.all_gather(counts, cnt)
     counts = [int(c.item()) for c in counts]
     mx = max(counts) if counts else 0
-    pad = torch.zeros((mx, ROW_BYTES), dtype=torch.uint8, device=dev)
-    if local.shape[0]:
-        pad[:local.shape[0]] = torch.from_numpy(local).to(dev)
-    out = torch.zeros((world * mx, ROW_BYTES), dtype=torch.uint8, device=dev)
-    dist.all_gather_into_tensor(out, pad)
+    per = mx * ROW_BYTES
+    buf = torch.zeros(max(per, 1), dtype=torch.uint8, device=dev)
+    off = 0
+    for name, dt, nb in _FIELDS:
+        col = getattr(local, name)
+        if n:
+            buf[off:off + n * nb] = torch.from_numpy(col.reshape(-1).view(np.uint8)).to(dev)
+        off += mx * nb
+    out = torch.empty(world * max(per, 1), dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(out, buf)
     if dist.get_rank() != 0:
         return None
-    allb = out.cpu().numpy().reshape(world, mx, ROW_BYTES)
-    rows = np.concatenate([allb[r, :counts[r]] for r in range(world)], axis=0)
-    rec = unpack_rows(rows)
-    return rec[np.lexsort((rec["label"], rec["tile"]))]
+    host = out.cpu().numpy()
+    parts = []
+    for r in range(world):
+        base, off, cols = r * max(per, 1), 0, {}
+        for name, dt, nb in _FIELDS:
+            cols[name] = host[base + off:base + off + counts[r] * nb].view(dt)
+            off += mx * nb
+        parts.append(Rows(cols["tile"], cols["label"], cols["flags"], cols["feat"]))
+    return merge_tile_runs(parts)
 
 
-def table_digest(rec: np.ndarray) -> str:
-    """Order-independent content digest of a gathered (sorted) table."""
-    return hashlib.sha256(np.ascontiguousarray(rec).view(np.uint8).tobytes()).hexdigest()[:16]
+def merge_tile_runs(parts) -> Rows:
+    """Merge per-rank tables into (tile, label) order.  Each rank's table is already in that
+    order and a tile belongs to one rank, so sorting the per-tile runs and concatenating them
+    is enough -- O(rows) copying instead of sorting every row."""
+    runs = []
+    for r, rec in enumerate(parts):
+        if len(rec) == 0:
+            continue
+        t = rec.tile
+        starts = np.flatnonzero(np.r_[True, t[1:] != t[:-1]])
+        ends = np.r_[starts[1:], len(t)]
+        runs.extend((int(t[a]), r, int(a), int(b)) for a, b in zip(starts, ends))
+    runs.sort()
+    return Rows.concat([parts[r].take(a, b) for _, r, a, b in runs])
+
+
+def table_digest(rows: Rows) -> str:
+    """Content digest of a table (column by column)."""
+    h = hashlib.sha256()
+    for name, _, _ in _FIELDS:
+        h.update(np.ascontiguousarray(getattr(rows, name)).view(np.uint8).tobytes())
+    return h.hexdigest()[:16]

@@ -12,8 +12,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1209_3332_b200.dist import (DistTileSource, TileQueue, gather_rows, pack_rows,
-                                       table_digest, unpack_rows)
+from paper_1209_3332_b200.dist import DistTileSource, TileQueue, gather_rows, table_digest, to_rows
 
 
 def _free_port():
@@ -88,15 +87,21 @@ def test_queue_and_gather_world2(n_tiles):
     assert all(o[3] <= 2 for o in outs)                        # window bound (n_slots = 2)
     digest = next(o[1] for o in outs if o[1] is not None)
     ref = {t: _fake_rows(t) for t in range(n_tiles)}
-    rec = np.sort(unpack_rows(pack_rows(ref)), order=["tile", "label"])
-    assert digest == table_digest(rec)                         # sorted union = 1-process table
+    assert digest == table_digest(to_rows(ref).sorted())       # sorted union = 1-process table
 
 
-def test_pack_roundtrip():
-    res = {7: _fake_rows(7), 3: _fake_rows(3)}
-    rec = unpack_rows(pack_rows(res))
-    assert list(rec["tile"]) == [3] * len(res[3][0]) + [7] * len(res[7][0])
-    assert np.array_equal(rec["label"][:len(res[3][0])], res[3][0])
+def test_rows_columns_and_merge():
+    from paper_1209_3332_b200.dist import merge_tile_runs
+    res = {7: _fake_rows(7), 3: _fake_rows(3), 11: _fake_rows(11)}
+    rec = to_rows(res)
+    assert list(rec.tile) == [3] * len(res[3][0]) + [7] * len(res[7][0]) + [11] * len(res[11][0])
+    assert np.array_equal(rec.label[:len(res[3][0])], res[3][0])
+    assert rec.feat.shape == (len(rec), 34)
+    # two "ranks" holding interleaved tiles merge into the 1-process order
+    a = to_rows({3: res[3], 11: res[11]})
+    b = to_rows({7: res[7]})
+    assert table_digest(merge_tile_runs([a, b])) == table_digest(rec)
+    assert table_digest(merge_tile_runs([b, a])) == table_digest(rec.sorted())
 
 
 def test_single_process_queue():
