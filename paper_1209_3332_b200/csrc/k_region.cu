@@ -36,6 +36,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HP_RG_ORDER
 #define HP_RG_ORDER 1  // initial job order: 0 raster, 1 four-colour (r1: 3018 -> 2165 jobs, 689 -> 725 tiles/s)
 #endif
+#ifndef HP_RG_EAGER
+#define HP_RG_EAGER 0  // eager in-region pushes of border changes (r1: 88.9 -> 106.6 ms owned, 727 -> 688 tiles/s: off)
+#endif
 #ifndef HP_RG_WAITERS
 #define HP_RG_WAITERS 4
 #endif
@@ -167,7 +170,7 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
     // may have changed.  A pixel's update is the clamp f(v) = min(m, max(lo, v)) of the value v
     // arriving along the row; clamps compose, so a lane's PPL pixels are one clamp and the row
     // closure is a warp scan of clamps in each direction.
-    auto row = [&](int y) -> bool {
+    auto row = [&](int y) -> int {
         const int wr = wr0 + y, c0 = wc0 + PPL * lane + 1;
         int m[PPL], rr[PPL], vm[PPL];
 #pragma unroll
@@ -186,7 +189,7 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
             const int hn = max(j == 0 ? lft : rr[j - 1], j == PPL - 1 ? rgt : rr[j + 1]);
             can |= min(max(vm[j], hn), m[j]) > rr[j];
         }
-        if (!__any_sync(FULL, can)) return false;
+        if (!__any_sync(FULL, can)) return 0;
         int lo[PPL];
 #pragma unroll
         for (int j = 0; j < PPL; ++j) {
@@ -244,7 +247,14 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
         for (int j = 0; j < PPL; ++j)
             if (u[j] != rr[j]) sRw[bidx(wr, c0 + j)] = (uint8_t)u[j];
         __syncwarp();
-        return true;
+#if HP_RG_EAGER
+        // which of the sub-tile's left / right column pixels changed (for eager pushes)
+        const int lc = __shfl_sync(FULL, (int)(u[0] != rr[0]), 0);
+        const int rc = __shfl_sync(FULL, (int)(u[PPL - 1] != rr[PPL - 1]), 31);
+        return 1 | (lc << 1) | (rc << 2);
+#else
+        return 1;
+#endif
     };
     // can window pixel p (pr, pc) improve window pixel q (qr, qc)?
     auto improves = [&](int pr, int pc, int qr, int qc) {
@@ -376,15 +386,39 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                         continue;
                     }
                     backoff = HP_POLL_NS;
-                    // Gauss-Seidel sweeps of this sub-tile (see iwpp_rules.cuh sweep_rows)
+                    // Gauss-Seidel sweeps of this sub-tile (see iwpp_rules.cuh sweep_rows).  With
+                    // HP_RG_EAGER, a changed top/bottom row or left/right column pixel marks the
+                    // orthogonal in-region neighbour's adjacent rows dirty at once, so the
+                    // neighbour starts while this sweep continues (the precise 8-neighbour pushes
+                    // after the sweep set still follow).
                     uint32_t chg = 0;
+                    auto eager = [&](int y, int code) {
+#if HP_RG_EAGER
+                        if (lane != 0) return;
+                        auto push = [&](int nw, uint32_t m) {
+                            if (atomicOr(&S.dirty[nw], m) == 0u) atomicAdd(&S.pend, 1);
+                        };
+                        if (y == kTile && sy < RY - 1) push(warp + RX, 1u);
+                        if (y == 1 && sy > 0) push(warp - RX, 1u << 31);
+                        const uint32_t near = (uint32_t)((7ull << (y - 1)) >> 1);  // rows y-1, y, y+1
+                        if ((code & 2) && sx > 0) push(warp - 1, near);
+                        if ((code & 4) && sx < RX - 1) push(warp + 1, near);
+#else
+                        (void)y;
+                        (void)code;
+#endif
+                    };
                     while (dirty) {
                         for (int y = 1; y <= kTile; ++y) {
                             const uint32_t bit = 1u << (y - 1);
                             if (!(dirty & bit)) continue;
                             dirty &= ~bit;
                             ++nrows;
-                            if (row(y)) { chg |= bit; dirty |= (bit << 1) | (bit >> 1); }
+                            if (const int rc = row(y)) {
+                                chg |= bit;
+                                dirty |= (bit << 1) | (bit >> 1);
+                                eager(y, rc);
+                            }
                         }
                         if (!dirty) break;
                         for (int y = kTile; y >= 1; --y) {
@@ -392,7 +426,11 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                             if (!(dirty & bit)) continue;
                             dirty &= ~bit;
                             ++nrows;
-                            if (row(y)) { chg |= bit; dirty |= (bit << 1) | (bit >> 1); }
+                            if (const int rc = row(y)) {
+                                chg |= bit;
+                                dirty |= (bit << 1) | (bit >> 1);
+                                eager(y, rc);
+                            }
                         }
                     }
                     ++iters;
