@@ -37,7 +37,7 @@ STAGES = ["S1 colour deconvolution", "S2 RBC detection", "S3 morph open 19x19",
 # algorithmic floor bytes per pixel of each stage (read each input once,
 # write each output once, in the §8(a) layouts); DESIGN.md "Roofline" restates them.
 FLOOR_BPP = [5, 2, 2, 4, 2, 2, 5, 9, 10, 5, 5]
-FUSED_BPP = 13
+FUSED_BPP = 6
 DTYPE = "u8/i32/f32"
 
 
@@ -304,15 +304,15 @@ def main():
     npx = size * size
     peak, peak_kind = peaks()
     per_stage = []
-    # default pipeline: S8-S11 run fused per F-component (k_comp.cu), timed as one stage;
-    # its floor = read F labels + dist + g, write labels (4 + 4 + 1 + 4 B/px)
+    # default pipeline: S7-S11 run fused per F-component (k_comp.cu), timed as one stage;
+    # its floor = read F + g, write labels (1 + 1 + 4 B/px)
     fused = os.environ.get("HP_GLOBAL_S8S10", "0") != "1"
-    rows = [(STAGES[k], stage_sum[k], FLOOR_BPP[k]) for k in range(7)]
+    rows = [(STAGES[k], stage_sum[k], FLOOR_BPP[k]) for k in range(6)]
     if fused:
-        rows.append(("S8-S11 fused per component (markers, watershed, BWLabel, features)",
-                     sum(stage_sum[7:11]), FUSED_BPP))
+        rows.append(("S7-S11 fused per component (EDT, markers, watershed, BWLabel, features)",
+                     sum(stage_sum[6:11]), FUSED_BPP))
     else:
-        rows += [(STAGES[k], stage_sum[k], FLOOR_BPP[k]) for k in range(7, 11)]
+        rows += [(STAGES[k], stage_sum[k], FLOOR_BPP[k]) for k in range(6, 11)]
     for name, tot, bpp in rows:
         sms = tot / max(1, ntiles_timed)
         gbs = bpp * npx / (sms / 1e3) / 1e9 if sms > 0 else None

@@ -164,9 +164,9 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
     ev(ctx, sl, 5, s);
     launch_fill_holes(sl.big0, w, h, sl, sl.F, s);                                                  // S6
     ev(ctx, sl, 6, s);
-    launch_edt(sl.F, w, h, sl, nullptr, sl.dist, s);                                                 // S7
-    ev(ctx, sl, 7, s);
     if (ctx->global_s8s10) {
+        launch_edt(sl.F, w, h, sl, nullptr, sl.dist, s);                                             // S7
+        ev(ctx, sl, 7, s);
         launch_markers(sl.dist, sl.F, p.h, w, h, sl, sl.ML, sl.J, s);                               // S8
         ev(ctx, sl, 8, s);
         launch_watershed(sl.dist, sl.ML, sl.F, w, h, sl, sl.split, nullptr, nullptr, nullptr, s);   // S9
@@ -174,7 +174,8 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
         launch_bwlabel(sl.split, w, h, p.obj_min_area, p.obj_max_area, sl, labels, lpitch, n_objects, s); // S10
         ev(ctx, sl, 10, s);
     } else {
-        // S8-S10 fused: one CTA per 8-component of F (timed under S8; S9/S10 read 0)
+        // S7-S11 fused per 8-component of F (k_comp.cu; timed under S8, S7/S9/S10 read 0)
+        ev(ctx, sl, 7, s);
         launch_components(sl.F, sl.dist, sl.g, p.h, p.obj_min_area, p.obj_max_area, w, h, sl, labels, lpitch,
                           n_objects, table, ctx->cfg.max_objects, s);
         ev(ctx, sl, 8, s);

@@ -159,8 +159,8 @@ void launch_recon_init_u8(const uint8_t* marker, const uint8_t* mask, uint8_t* R
 void launch_tophat(const uint8_t* g, const uint8_t* R, const uint8_t* rbc, int g1, int w, int h,
                    uint8_t* cand, cudaStream_t s);
 // S7
-void launch_edt(const uint8_t* F, int w, int h, Slot& sl, uint32_t* d2_out, float* dist,
-                cudaStream_t s);
+void launch_edt(const uint8_t* F, int w, int h, Slot& sl, uint32_t* d2_out, float* dist, cudaStream_t s,
+                const int32_t* cond = nullptr);
 // S8, S9
 void launch_markers(const float* dist, const uint8_t* F, float hh, int w, int h, Slot& sl,
                     int32_t* ML, float* J, cudaStream_t s);
@@ -171,7 +171,7 @@ void launch_watershed(const float* dist, const int32_t* ML, const uint8_t* F, in
 void launch_bwlabel(const uint8_t* split, int w, int h, int amin, int amax, Slot& sl,
                     int32_t* labels, int64_t lpitch, int32_t* n_objects, cudaStream_t s);
 // S8-S10 fused per F component (k_comp.cu)
-void launch_components(const uint8_t* F, const float* dist, const uint8_t* g, float hh, int amin, int amax,
+void launch_components(const uint8_t* F, float* dist_scratch, const uint8_t* g, float hh, int amin, int amax,
                        int w, int h, Slot& sl, int32_t* labels, int64_t lpitch, int32_t* n_objects,
                        const hp_feature_table* table, int32_t max_objects, cudaStream_t s);
 // S11

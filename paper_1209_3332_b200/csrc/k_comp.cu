@@ -158,6 +158,7 @@ struct CompSm {
     uint8_t pm[CAP];
     uint8_t sp[CAP];
     int nmem;
+    int nbnd;
     int nobj;
     int objroot[KO];
     FeatSmem fs;
@@ -184,6 +185,7 @@ __device__ bool comp_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, c
     if (tr == 0) {
         S.nobj = 0;
         S.nmem = 0;
+        S.nbnd = 0;
     }
     team.sync();
     int nmem = 0;
@@ -193,16 +195,10 @@ __device__ bool comp_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, c
         if (li < NWIN) {
             const int ly = li / WX, lx = li - ly * WX;
             const int gx = wx0 + lx, gy = wy0 + ly;
-            float dv = 0.f;
-            if (gx >= 0 && gy >= 0 && gx < w && gy < h) {
-                const int64_t p = (int64_t)gy * w + gx;
-                if (a.labF[p] == root) {
-                    m = true;
-                    dv = a.dist[p];
-                }
-            }
+            const bool in = gx >= 0 && gy >= 0 && gx < w && gy < h;
+            if (in) m = a.labF[(int64_t)gy * w + gx] == root;
             S.mem[li] = m;
-            S.dist[li] = dv;
+            S.pm[li] = in;  // (scratch until the parent pass)
         }
         if constexpr (TS == 32) {  // warp team: ballot compaction (window order)
             const unsigned bal = __ballot_sync(0xffffffffu, m);
@@ -217,6 +213,49 @@ __device__ bool comp_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, c
     auto each = [&](auto fn) {
         for (int k = tr; k < nmem; k += TS) fn((int)S.list[k]);
     };
+    // ---- S7 EDT of the members, exactly, inside the window (reading C11).
+    // For a member p at distance d from the nearest background pixel q, the open disk of
+    // radius d around p is foreground and 8-connected, so it lies in p's component; one
+    // step from q toward p lands in that disk, so q is 8-adjacent to the component: every
+    // nearest background pixel is an in-tile non-member of the window touching a member.  No
+    // such pixel = the component is the whole tile = no background: +inf.
+    {
+        int nb = 0;
+        int32_t* bl = S.C;  // boundary pixels, (ly << 16) | lx
+        for (int base = 0; base < NWIN; base += TS) {
+            const int li = base + tr;
+            bool bnd = false;
+            if (li < NWIN && !S.mem[li] && S.pm[li]) {
+                const int ly = li / WX, lx = li - ly * WX;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int qx = lx + dx8(j), qy = ly + dy8(j);
+                    if (qx >= 0 && qy >= 0 && qx < WX && qy < WY && S.mem[qy * WX + qx]) bnd = true;
+                }
+            }
+            const int code = bnd ? (((li / WX) << 16) | (li % WX)) : 0;
+            if constexpr (TS == 32) {
+                const unsigned bal = __ballot_sync(0xffffffffu, bnd);
+                if (bnd) bl[nb + __popc(bal & ((1u << tr) - 1u))] = code;
+                nb += __popc(bal);
+            } else {
+                if (bnd) bl[atomicAdd(&S.nbnd, 1)] = code;
+            }
+        }
+        team.sync();
+        if constexpr (TS != 32) nb = S.nbnd;
+        each([&](int li) {
+            const int ly = li / WX, lx = li - ly * WX;
+            uint32_t best = 0xffffffffu;
+            for (int k = 0; k < nb; ++k) {
+                const int c = bl[k];
+                const int dx = (c & 0xffff) - lx, dy = (c >> 16) - ly;
+                best = min(best, (uint32_t)(dx * dx + dy * dy));
+            }
+            S.dist[li] = nb == 0 ? INFINITY : __fsqrt_rn(__uint2float_rn(best));
+        });
+        team.sync();
+    }
     auto converge = [&](auto step) {
         while (true) {
             int ch = 0;
@@ -756,7 +795,9 @@ __global__ void k_copy_i32(const int32_t* __restrict__ src, int32_t* __restrict_
 
 // S8-S10 (+ S11 when table != nullptr) of the pipeline on F and dist: labels (zeroed here),
 // n_objects, and the feature rows in label order.
-void launch_components(const uint8_t* F, const float* dist, const uint8_t* g, float hh, int amin, int amax,
+// S7-S11 per component.  dist_scratch: a slot plane that receives the global EDT, computed
+// only if some component takes the global path (the shared-memory path computes its own).
+void launch_components(const uint8_t* F, float* dist_scratch, const uint8_t* g, float hh, int amin, int amax,
                        int w, int h, Slot& sl, int32_t* labels, int64_t lpitch, int32_t* n_objects,
                        const hp_feature_table* table, int32_t max_objects, cudaStream_t s) {
     const int64_t n = (int64_t)w * h;
@@ -782,7 +823,7 @@ void launch_components(const uint8_t* F, const float* dist, const uint8_t* g, fl
     CompArgs a{};
     a.F = F;
     a.labF = sl.lab;
-    a.dist = dist;
+    a.dist = dist_scratch;
     a.g = g;
     a.hh = hh;
     a.w = w;
@@ -820,6 +861,7 @@ void launch_components(const uint8_t* F, const float* dist, const uint8_t* g, fl
     (note_launch(), k_comp_classify<<<grid_for(cap), 256, 0, s>>>(a, cnt, cap, sl.comp_bbox, sl.comp_big, nbig));
     (note_launch(), k_comp_fused<<<148 * 4, kWarpsPB * 32, smw, s>>>(a, cnt, cap, sl.comp_root, sl.comp_bbox,
                                                                      sl.comp_big, nbig, heads));
+    launch_edt(F, w, h, sl, nullptr, dist_scratch, s, ovf);  // no-op unless a component overflowed
     (note_launch(), k_comp_global<<<148, kCT, 0, s>>>(a, sl.comp_root, sl.comp_bbox));
     if (table) {
         (note_launch(), k_obj_feat_list<<<148 * 2, kFT, 0, s>>>(a, sl.comp_bbox));

@@ -30,7 +30,8 @@ constexpr uint32_t kInfSq = 0x7fffffffu;
 
 __global__ void k_edt_seg(const uint8_t* __restrict__ F, int w, int h, int nseg,
                           int16_t* __restrict__ top, int16_t* __restrict__ bot,
-                          int32_t* __restrict__ any_bg) {
+                          int32_t* __restrict__ any_bg, const int32_t* __restrict__ cond) {
+    if (cond && *cond == 0) return;
     int64_t n = (int64_t)w * nseg;
     bool found = false;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -51,7 +52,8 @@ __global__ void k_edt_seg(const uint8_t* __restrict__ F, int w, int h, int nseg,
 
 __global__ void k_edt_col(const uint8_t* __restrict__ F, int w, int h, int nseg,
                           const int16_t* __restrict__ top, const int16_t* __restrict__ bot,
-                          uint16_t* __restrict__ gcol) {
+                          uint16_t* __restrict__ gcol, const int32_t* __restrict__ cond) {
+    if (cond && *cond == 0) return;
     int64_t n = (int64_t)w * nseg;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int seg = (int)(i / w), x = (int)(i - (int64_t)seg * w);
@@ -92,7 +94,9 @@ __global__ void __launch_bounds__(256) k_edt_row(const uint8_t* __restrict__ F, 
                                                  const uint16_t* __restrict__ gcol,
                                                  const int32_t* __restrict__ any_bg,
                                                  int32_t* __restrict__ scr_s, int32_t* __restrict__ scr_t,
-                                                 uint32_t* __restrict__ d2out, float* __restrict__ dist) {
+                                                 uint32_t* __restrict__ d2out, float* __restrict__ dist,
+                                                 const int32_t* __restrict__ cond) {
+    if (cond && *cond == 0) return;
     extern __shared__ uint32_t sq[];
     __shared__ int need_full;
     const int y = blockIdx.x;
@@ -173,22 +177,24 @@ inline int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 
 
 }  // namespace
 
+// cond (device int, may be null): skip the whole transform when *cond == 0 at run time (the
+// pipeline needs the global plane only for components that fall back to the global path)
 void launch_edt(const uint8_t* F, int w, int h, Slot& sl, uint32_t* d2_out, float* dist,
-                cudaStream_t s) {
+                cudaStream_t s, const int32_t* cond) {
     if ((int64_t)w * h == 0) return;
     const int nseg = (h + kSeg - 1) / kSeg;
     int32_t* any_bg = sl.cnt32 + 1;
     cudaMemsetAsync(any_bg, 0, sizeof(int32_t), s);
     int64_t nthreads = (int64_t)w * nseg;
-    (note_launch(), k_edt_seg<<<grid_for(nthreads), 256, 0, s>>>(F, w, h, nseg, sl.seg_top, sl.seg_bot, any_bg));
-    (note_launch(), k_edt_col<<<grid_for(nthreads), 256, 0, s>>>(F, w, h, nseg, sl.seg_top, sl.seg_bot, sl.gcol));
+    (note_launch(), k_edt_seg<<<grid_for(nthreads), 256, 0, s>>>(F, w, h, nseg, sl.seg_top, sl.seg_bot, any_bg, cond));
+    (note_launch(), k_edt_col<<<grid_for(nthreads), 256, 0, s>>>(F, w, h, nseg, sl.seg_top, sl.seg_bot, sl.gcol, cond));
     size_t smem = sizeof(uint32_t) * (size_t)w;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_edt_row, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    (note_launch(), k_edt_row<<<h, 256, smem, s>>>(F, w, h, sl.gcol, any_bg, sl.aux, sl.d, d2_out, dist));
+    (note_launch(), k_edt_row<<<h, 256, smem, s>>>(F, w, h, sl.gcol, any_bg, sl.aux, sl.d, d2_out, dist, cond));
 }
 
 }  // namespace hp
