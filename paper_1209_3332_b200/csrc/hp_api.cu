@@ -42,7 +42,8 @@ struct hp_ctx {
     std::vector<void*> dev_blocks;
     std::vector<void*> host_blocks;
     int rows_copied = 0;  // rows copied back per tile in hp_run_tiles
-    bool global_s8s10 = false;  // env HP_GLOBAL_S8S10=1: the per-stage global path in the pipeline
+    bool global_s8s10 = false;
+    int prio = 0;  // env HP_PRIO: 1 = S4 on a high-priority stream, 2 = S4 and S7-S11  // env HP_GLOBAL_S8S10=1: the per-stage global path in the pipeline
     // stage-timing ring: per slot, kRing sets of 12 events (one set per tile)
     std::vector<std::vector<std::array<cudaEvent_t, 12>>> ring;
     std::vector<int> ring_pos, ring_n;
@@ -157,7 +158,21 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
     // ignored: open(g) <= g), so S4's marker min(open, g) is the opening itself
     launch_open(sl.g, w, h, p.open_diam, sl.u8a, sl.u8b, s);                                          // S3
     ev(ctx, sl, 3, s);
-    launch_recon_u8_auto(sl.g, sl.u8b, w, h, sl.wl, s);                                               // S4
+    {                                                                                                 // S4
+        // optionally on the slot's high-priority stream: its CTAs then take SM resources
+        // first as the other slots' blocks retire
+        cudaStream_t rs = s;
+        if (ctx->prio >= 1) {
+            cudaEventRecord(sl.fork_ev, s);
+            cudaStreamWaitEvent(sl.hstream, sl.fork_ev, 0);
+            rs = sl.hstream;
+        }
+        launch_recon_u8_auto(sl.g, sl.u8b, w, h, sl.wl, rs);
+        if (ctx->prio >= 1) {
+            cudaEventRecord(sl.join_ev, sl.hstream);
+            cudaStreamWaitEvent(s, sl.join_ev, 0);
+        }
+    }
     ev(ctx, sl, 4, s);
     // S5 on the top-hat candidates (g - recon > g1) & !rbc, evaluated inside the CCL passes
     launch_area_select_tophat(sl.g, sl.u8b, sl.rbc, p.g1, w, h, p.cand_min_area, p.cand_max_area, sl, sl.big0, s);
@@ -176,8 +191,18 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
     } else {
         // S7-S11 fused per 8-component of F (k_comp.cu; timed under S8, S7/S9/S10 read 0)
         ev(ctx, sl, 7, s);
+        cudaStream_t cs = s;
+        if (ctx->prio >= 2) {
+            cudaEventRecord(sl.fork_ev, s);
+            cudaStreamWaitEvent(sl.hstream, sl.fork_ev, 0);
+            cs = sl.hstream;
+        }
         launch_components(sl.F, sl.dist, sl.g, p.h, p.obj_min_area, p.obj_max_area, w, h, sl, labels, lpitch,
-                          n_objects, table, ctx->cfg.max_objects, s);
+                          n_objects, table, ctx->cfg.max_objects, cs);
+        if (ctx->prio >= 2) {
+            cudaEventRecord(sl.join_ev, sl.hstream);
+            cudaStreamWaitEvent(s, sl.join_ev, 0);
+        }
         ev(ctx, sl, 8, s);
         ev(ctx, sl, 9, s);
         ev(ctx, sl, 10, s);
@@ -281,6 +306,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
     ctx->device = cfg->device;
     ctx->rows_copied = std::min(cfg->max_objects, kRowsAsync);
     if (const char* e = getenv("HP_GLOBAL_S8S10")) ctx->global_s8s10 = atoi(e) == 1;
+    if (const char* e = getenv("HP_PRIO")) ctx->prio = atoi(e);
     auto dalloc = [&](size_t bytes) -> void* {
         void* p = nullptr;
         if (cudaMalloc(&p, bytes ? bytes : 16) != cudaSuccess) return nullptr;
@@ -356,8 +382,13 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
                        s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows};
         for (void* p : all)
             if (!p) { hp_ctx_destroy(ctx); return HP_ERR_NOMEM; }
+        int prio_lo = 0, prio_hi = 0;
+        cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
         if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&s.done_ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaStreamCreateWithPriority(&s.hstream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.done_ev, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.fork_ev, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.join_ev, cudaEventDisableTiming) != cudaSuccess) {
             hp_ctx_destroy(ctx);
             return HP_ERR_CUDA;
         }
@@ -376,7 +407,10 @@ hp_status hp_ctx_destroy(hp_ctx* ctx) {
     cudaDeviceSynchronize();
     for (Slot& s : ctx->slots) {
         if (s.stream) cudaStreamDestroy(s.stream);
+        if (s.hstream) cudaStreamDestroy(s.hstream);
         if (s.done_ev) cudaEventDestroy(s.done_ev);
+        if (s.fork_ev) cudaEventDestroy(s.fork_ev);
+        if (s.join_ev) cudaEventDestroy(s.join_ev);
     }
     for (auto& r : ctx->ring)
         for (auto& set : r)

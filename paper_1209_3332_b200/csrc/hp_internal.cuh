@@ -96,6 +96,9 @@ struct Slot {
     int32_t *h_label, *h_flags, *h_nrows;
     float* h_feat;
     cudaEvent_t done_ev;
+    // high-priority side stream for the latency-bound stages (hp_ctx::prio)
+    cudaStream_t hstream;
+    cudaEvent_t fork_ev, join_ev;
 };
 
 // ---------------------------------------------------------------- launchers (host)
