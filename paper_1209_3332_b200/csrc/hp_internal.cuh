@@ -78,6 +78,11 @@ struct Slot {
     int32_t* cs_edge;    // k_ccls.cu: per 32x32 tile, the roots of its 4 x 32 edge pixels
     int32_t* cs_roots;   // k_ccls.cu: per tile, its local roots (up to 1024)
     int32_t* cs_nroots;  // k_ccls.cu: per tile, number of local roots
+    // S5 component list (k_ccls.cu listing; consumed by the per-component S6 / S7-S11 kernels)
+    int32_t* sc_root;
+    int4* sc_bbox;
+    int32_t* sc_area;
+    int32_t* sc_big;
     int32_t* cid;
     int32_t comp_cap;
     // staging table of the fused S8-S11 path (rows in discovery order)
@@ -134,11 +139,17 @@ void launch_ccl_to_labels(const CclSrc& src, int w, int h, const int32_t* lab, i
 // k_ccls.cu (CCL-select: u8 output from a per-component property, no label plane)
 void launch_rbc(const uint8_t* flags, int w, int h, Slot& sl, uint8_t* rbc, cudaStream_t s);
 // S6
-void launch_fill_holes(const uint8_t* big0, int w, int h, Slot& sl, uint8_t* F, cudaStream_t s);
+void launch_fill_holes(const uint8_t* big0, int w, int h, Slot& sl, uint8_t* F, cudaStream_t s,
+                       const int32_t* gate = nullptr);
 void launch_area_select(const uint8_t* cand, int w, int h, int amin, int amax, Slot& sl, uint8_t* out,
                         cudaStream_t s);
 void launch_area_select_tophat(const uint8_t* g, const uint8_t* R, const uint8_t* rbc, int g1, int w, int h,
-                               int amin, int amax, Slot& sl, uint8_t* out, cudaStream_t s);
+                               int amin, int amax, Slot& sl, uint8_t* out, int32_t* count, cudaStream_t s);
+// S6 per S5 component (k_comp.cu): F = component | its holes, enc = other candidates inside a
+// hole; *gate set to 1 if a component's window is too large (then the caller's gated whole-tile
+// FillHoles must run)
+void launch_fill_components(const uint8_t* big0, int w, int h, Slot& sl, const int32_t* count, uint8_t* F,
+                            uint8_t* enc, int32_t* gate, cudaStream_t s);
 // IWPP / worklist engine
 void wl_init_all(const Worklist& wl, int w, int h, cudaStream_t s);
 void wl_init_from_mask(const Worklist& wl, const uint8_t* mask, int w, int h, cudaStream_t s);

@@ -21,6 +21,8 @@
 // HBM traffic per pixel: the input plane twice and the u8 output once (plus small arrays).
 // The property word packs the area (bits 0-28: images up to 2^29 - 1 px) with the OR-bits
 // HIT (bit 29) and TOUCH (bit 30); atomicAdd of areas never carries into the flag bits.
+#include <climits>
+
 #include "hp_internal.cuh"
 
 namespace hp {
@@ -39,6 +41,9 @@ struct Sel {
     const uint8_t* R = nullptr;    // SEL_AREA_TH: the reconstruction
     const uint8_t* rbc = nullptr;  // SEL_AREA_TH: the RBC mask
     int g1 = 0;                    // SEL_AREA_TH: top-hat threshold
+    // SEL_AREA_TH: per-root bounding boxes, written at root entries only (sparse planes)
+    int32_t *bx0 = nullptr, *by0 = nullptr, *bx1 = nullptr, *by1 = nullptr;
+    const int32_t* gate = nullptr;  // if set: every pass is a no-op unless *gate != 0
     // the pixel's byte: the plane, or for SEL_AREA_TH the top-hat candidate of S4 (PAPER.md:596,
     // reading C9): (g - recon > g1) & !rbc
     template <int MODE>
@@ -211,13 +216,24 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
                                                   int32_t* __restrict__ E, int32_t* __restrict__ roots,
                                                   int32_t* __restrict__ nroots) {
     __shared__ TileSm T;
+    constexpr bool BB = MODE == SEL_AREA_TH;  // bounding boxes per component
+    __shared__ int bbs[BB ? 4 : 1][BB ? kT * kT : 1];
+    if (sel.gate && *sel.gate == 0) return;
     const int tx0 = blockIdx.x * kT, ty0 = blockIdx.y * kT;
     const int t = blockIdx.y * gridDim.x + blockIdx.x;
     const int lane = threadIdx.x & 31;
     const int w = sel.w, h = sel.h;
+    if constexpr (BB) {
+        for (int i = threadIdx.x; i < kT * kT; i += blockDim.x) {
+            bbs[0][i] = INT_MAX;
+            bbs[1][i] = INT_MAX;
+            bbs[2][i] = -1;
+            bbs[3][i] = -1;
+        }
+    }
     uint8_t v[4];
     unsigned fms[4];
-    const int kind = tile_uf<MODE>(sel, conn, tx0, ty0, T, v, fms, true);
+    const int kind = tile_uf<MODE>(sel, conn, tx0, ty0, T, v, fms, true);  // (its barriers order bbs)
     int32_t* Et = E + (int64_t)t * 4 * kT;
     auto gidx = [&](int li) -> int32_t { return (int32_t)((int64_t)(ty0 + li / kT) * w + tx0 + li % kT); };
     if (kind == 0) {
@@ -233,6 +249,12 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
             if (threadIdx.x == 0) {
                 P[G] = G;
                 X[G] = kT * kT | (anyb ? mode_bit<MODE>() : 0);
+                if constexpr (BB) {
+                    sel.bx0[G] = tx0;
+                    sel.by0[G] = ty0;
+                    sel.bx1[G] = tx0 + kT - 1;
+                    sel.by1[G] = ty0 + kT - 1;
+                }
                 roots[(int64_t)t * kT * kT] = G;
                 nroots[t] = 1;
             }
@@ -249,6 +271,12 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
         const int r = find_l(T.s, ly * kT + lane);
         atomicAdd(&T.acc[r], re - lane + 1);
         if (T.bitm[ly] & span(lane, re)) atomicOr(&T.acc[r], mode_bit<MODE>());
+        if constexpr (BB) {
+            atomicMin(&bbs[0][r], tx0 + lane);
+            atomicMin(&bbs[1][r], ty0 + ly);
+            atomicMax(&bbs[2][r], tx0 + re);
+            atomicMax(&bbs[3][r], ty0 + ly);
+        }
     }
     __syncthreads();
     // roots: run starts that are their own parent
@@ -260,6 +288,12 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
             const int32_t G = gidx(li);
             P[G] = G;
             X[G] = T.acc[li];
+            if constexpr (BB) {
+                sel.bx0[G] = bbs[0][li];
+                sel.by0[G] = bbs[1][li];
+                sel.bx1[G] = bbs[2][li];
+                sel.by1[G] = bbs[3][li];
+            }
             roots[(int64_t)t * kT * kT + atomicAdd(&T.nr, 1)] = G;
         }
     }
@@ -284,7 +318,8 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
 // which also covers every right-column diagonal; 4-conn: i0 .. i1); the 8-conn corner
 // diagonals (up-left of (0,0), up-right of (31,0)) are taken by the top row's end lanes.
 __global__ void __launch_bounds__(256) k_cs_merge(int conn, int ntx, int nty, const int32_t* __restrict__ E,
-                                                  int32_t* __restrict__ P) {
+                                                  int32_t* __restrict__ P, const int32_t* __restrict__ gate) {
+    if (gate && *gate == 0) return;
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gt >= (int64_t)ntx * nty * 2 * kT) return;  // (whole warps: 2 * kT per tile)
     const int t = (int)(gt / (2 * kT)), j = (int)(gt % (2 * kT));
@@ -322,7 +357,8 @@ __global__ void __launch_bounds__(256) k_cs_merge(int conn, int ntx, int nty, co
 // one warp per tile
 __global__ void __launch_bounds__(256) k_cs_accum(int ntiles, const int32_t* __restrict__ roots,
                                                   const int32_t* __restrict__ nroots, int32_t* __restrict__ P,
-                                                  int32_t* __restrict__ X) {
+                                                  int32_t* __restrict__ X, Sel sel) {
+    if (sel.gate && *sel.gate == 0) return;
     const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
     if (t < ntiles) {
         const int n = nroots[t];
@@ -333,6 +369,12 @@ __global__ void __launch_bounds__(256) k_cs_accum(int ntiles, const int32_t* __r
             const int32_t x = X[G];
             atomicAdd(&X[R], x & kAreaMask);
             if (x & ~kAreaMask) atomicOr(&X[R], x & ~kAreaMask);
+            if (sel.bx0) {
+                atomicMin(&sel.bx0[R], sel.bx0[G]);
+                atomicMin(&sel.by0[R], sel.by0[G]);
+                atomicMax(&sel.bx1[R], sel.bx1[G]);
+                atomicMax(&sel.by1[R], sel.by1[G]);
+            }
             P[G] = R;
         }
     }
@@ -342,6 +384,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k_cs_out(Sel sel, int conn, const int32_t* __restrict__ P,
                                                 const int32_t* __restrict__ X, uint8_t* __restrict__ out) {
     __shared__ TileSm T;
+    if (sel.gate && *sel.gate == 0) return;
     const int tx0 = blockIdx.x * kT, ty0 = blockIdx.y * kT;
     const int lane = threadIdx.x & 31;
     const int w = sel.w, h = sel.h;
@@ -371,8 +414,40 @@ __global__ void __launch_bounds__(256) k_cs_out(Sel sel, int conn, const int32_t
     }
 }
 
+// the global roots of the components that pass the area filter, with their bounding boxes
+// (one warp per tile, over the tile's local roots: a local root is a global root iff P[G] == G)
+__global__ void __launch_bounds__(256) k_cs_list(int ntiles, const int32_t* __restrict__ roots,
+                                                 const int32_t* __restrict__ nroots, const int32_t* __restrict__ P,
+                                                 const int32_t* __restrict__ X, Sel sel, int32_t* __restrict__ out_root,
+                                                 int4* __restrict__ out_bbox, int32_t* __restrict__ out_area,
+                                                 int32_t* __restrict__ count, int32_t cap) {
+    const int t = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (t >= ntiles) return;
+    const int n = nroots[t];
+    for (int k = threadIdx.x & 31; k < n; k += 32) {
+        const int32_t G = roots[(int64_t)t * kT * kT + k];
+        if (P[G] != G) continue;
+        const int a = X[G] & kAreaMask;
+        if (a < sel.amin || a > sel.amax) continue;
+        const int i = atomicAdd(count, 1);
+        if (i < cap) {
+            out_root[i] = G;
+            out_bbox[i] = make_int4(sel.bx0[G], sel.by0[G], sel.bx1[G], sel.by1[G]);
+            out_area[i] = a;
+        }
+    }
+}
+
+struct ListOut {
+    int32_t* root = nullptr;
+    int4* bbox = nullptr;
+    int32_t* area = nullptr;
+    int32_t* count = nullptr;  // zeroed by the caller
+    int32_t cap = 0;
+};
+
 template <int MODE>
-void run_select(Sel sel, int conn, Slot& sl, uint8_t* out, cudaStream_t s) {
+void run_select(Sel sel, int conn, Slot& sl, uint8_t* out, cudaStream_t s, const ListOut* lo = nullptr) {
     const int w = sel.w, h = sel.h;
     if ((int64_t)w * h == 0) return;
     const int ntx = (w + kT - 1) / kT, nty = (h + kT - 1) / kT;
@@ -382,9 +457,12 @@ void run_select(Sel sel, int conn, Slot& sl, uint8_t* out, cudaStream_t s) {
     int32_t* X = sl.aux;
     (note_launch(), k_cs_local<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, sl.cs_edge, sl.cs_roots, sl.cs_nroots));
     (note_launch(), k_cs_merge<<<(int)(((int64_t)ntiles * 2 * kT + 255) / 256), 256, 0, s>>>(conn, ntx, nty,
-                                                                                           sl.cs_edge, P));
-    (note_launch(), k_cs_accum<<<(ntiles + 7) / 8, 256, 0, s>>>(ntiles, sl.cs_roots, sl.cs_nroots, P, X));
-    (note_launch(), k_cs_out<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, out));
+                                                                                           sl.cs_edge, P, sel.gate));
+    (note_launch(), k_cs_accum<<<(ntiles + 7) / 8, 256, 0, s>>>(ntiles, sl.cs_roots, sl.cs_nroots, P, X, sel));
+    if (out) (note_launch(), k_cs_out<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, out));
+    if (lo)
+        (note_launch(), k_cs_list<<<(ntiles + 7) / 8, 256, 0, s>>>(ntiles, sl.cs_roots, sl.cs_nroots, P, X, sel,
+                                                                   lo->root, lo->bbox, lo->area, lo->count, lo->cap));
 }
 
 }  // namespace
@@ -398,17 +476,34 @@ void launch_area_select(const uint8_t* cand, int w, int h, int amin, int amax, S
     run_select<SEL_AREA>(Sel{cand, w, h, amin, amax}, 8, sl, out, s);
 }
 
+// S5 on the top-hat candidates, also listing the kept components (root, bounding box) into
+// sl.sc_root / sl.sc_bbox with their count at *count (zeroed here); the sparse bounding-box
+// planes borrow the slot's global-path planes ML, d, L, J.
 void launch_area_select_tophat(const uint8_t* g, const uint8_t* R, const uint8_t* rbc, int g1, int w, int h,
-                               int amin, int amax, Slot& sl, uint8_t* out, cudaStream_t s) {
+                               int amin, int amax, Slot& sl, uint8_t* out, int32_t* count, cudaStream_t s) {
     Sel sel{g, w, h, amin, amax};
     sel.R = R;
     sel.rbc = rbc;
     sel.g1 = g1;
-    run_select<SEL_AREA_TH>(sel, 8, sl, out, s);
+    sel.bx0 = sl.ML;
+    sel.by0 = sl.d;
+    sel.bx1 = sl.L;
+    sel.by1 = reinterpret_cast<int32_t*>(sl.J);
+    cudaMemsetAsync(count, 0, sizeof(int32_t), s);
+    ListOut lo;
+    lo.root = sl.sc_root;
+    lo.bbox = sl.sc_bbox;
+    lo.area = sl.sc_area;
+    lo.count = count;
+    lo.cap = sl.comp_cap;
+    run_select<SEL_AREA_TH>(sel, 8, sl, out, s, &lo);
 }
 
-void launch_fill_holes(const uint8_t* big0, int w, int h, Slot& sl, uint8_t* F, cudaStream_t s) {
-    run_select<SEL_FILL>(Sel{big0, w, h, 0, 0}, 4, sl, F, s);
+void launch_fill_holes(const uint8_t* big0, int w, int h, Slot& sl, uint8_t* F, cudaStream_t s,
+                       const int32_t* gate) {
+    Sel sel{big0, w, h, 0, 0};
+    sel.gate = gate;
+    run_select<SEL_FILL>(sel, 4, sl, F, s);
 }
 
 }  // namespace hp

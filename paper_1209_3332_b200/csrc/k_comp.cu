@@ -533,6 +533,202 @@ __global__ void __launch_bounds__(kWarpsPB * 32, 4) k_comp_fused(CompArgs a, con
     }
 }
 
+// ---------------------------------------------------------------- S6 per S5 component
+// FillHoles (reading C8: 4-connected background components touching no tile-
+// border pixel) per kept candidate component A.  A hole is a bounded 4-connected background
+// region; its boundary is an 8-connected set of foreground pixels, so it is enclosed by ONE
+// 8-component and lies inside that component's bounding box.  In A's window (bbox + 1-px
+// ring): A = the 8-component of A's root among the window's candidate pixels; every other
+// window pixel counts as background; seeds = the ring, out-of-tile and tile-border pixels;
+// the non-A pixels not 4-connected to a seed are A's holes (candidate pixels of other
+// components enclosed there -- islands -- are filled with them and marked in enc).  F =
+// union over components of A | holes(A) equals FillHoles(big0) exactly.
+struct FillArgs {
+    const uint8_t* big0;
+    int w, h;
+    uint8_t* F;
+    uint8_t* enc;
+    int32_t* gate;
+};
+
+// A = the 8-component of the root among the window's candidate pixels (union-find) -> sp
+template <class Team, int CAP, int KO>
+__device__ void fill_isolate(const Team& team, CompSm<CAP, KO>& S, const FillArgs& a, int WX, int NWIN, int li_root) {
+    const int tr = team.rank();
+    constexpr int TS = Team::size;
+    auto win = [&](auto fn) {
+        for (int li = tr; li < NWIN; li += TS) fn(li);
+    };
+    win([&](int li) {
+        if (!S.mem[li]) return;
+        const int ly = li / WX, lx = li - ly * WX;
+        if (lx > 0 && S.mem[li - 1]) cunion(S.B, li, li - 1);
+        if (ly > 0) {
+            if (S.mem[li - WX]) cunion(S.B, li, li - WX);
+            if (lx > 0 && S.mem[li - WX - 1]) cunion(S.B, li, li - WX - 1);
+            if (lx < WX - 1 && S.mem[li - WX + 1]) cunion(S.B, li, li - WX + 1);
+        }
+    });
+    team.sync();
+    const int rA = cfind(S.B, li_root);
+    win([&](int li) { S.sp[li] = S.mem[li] && cfind(S.B, li) == rA; });
+    team.sync();
+}
+
+// the holes of A (sp): 4-connected union-find over the non-A pixels, seeds = ring, out-of-tile
+// and tile-border pixels; F |= A | holes, enc |= candidates inside the holes
+template <class Team, int CAP, int KO>
+__device__ void fill_holes_window(const Team& team, CompSm<CAP, KO>& S, const FillArgs& a, int WX, int WY,
+                                  int NWIN, int wx0, int wy0) {
+    const int w = a.w, h = a.h;
+    const int tr = team.rank();
+    constexpr int TS = Team::size;
+    auto win = [&](auto fn) {
+        for (int li = tr; li < NWIN; li += TS) fn(li);
+    };
+    win([&](int li) { S.C[li] = S.sp[li] ? -1 : li; });
+    team.sync();
+    win([&](int li) {
+        if (S.sp[li]) return;
+        const int ly = li / WX, lx = li - ly * WX;
+        if (lx > 0 && !S.sp[li - 1]) cunion(S.C, li, li - 1);
+        if (ly > 0 && !S.sp[li - WX]) cunion(S.C, li, li - WX);
+    });
+    team.sync();
+    win([&](int li) { S.B[li] = 0; });  // seed flags at the 4-roots
+    team.sync();
+    win([&](int li) {
+        if (S.sp[li]) return;
+        const int ly = li / WX, lx = li - ly * WX;
+        const int gx = wx0 + lx, gy = wy0 + ly;
+        const bool seed = lx == 0 || ly == 0 || lx == WX - 1 || ly == WY - 1 || !S.pm[li] || gx == 0 || gy == 0 ||
+                          gx == w - 1 || gy == h - 1;
+        if (seed) S.B[cfind(S.C, li)] = 1;
+    });
+    team.sync();
+    win([&](int li) {
+        if (!S.pm[li]) return;
+        const int ly = li / WX, lx = li - ly * WX;
+        const int64_t p = (int64_t)(wy0 + ly) * w + (wx0 + lx);
+        if (S.sp[li]) {
+            a.F[p] = 1;
+        } else if (S.B[cfind(S.C, li)] == 0) {  // a hole of A
+            a.F[p] = 1;
+            if (S.mem[li]) a.enc[p] = 1;         // another candidate, enclosed by A
+        }
+    });
+    team.sync();
+}
+
+template <class Team, int CAP, int KO>
+__device__ void fill_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, const FillArgs& a, int32_t root,
+                           int4 bb, int area) {
+    const int w = a.w, h = a.h;
+    const int tr = team.rank();
+    constexpr int TS = Team::size;
+    const int wx0 = bb.x - 1, wy0 = bb.y - 1;
+    const int WX = bb.z - bb.x + 3, WY = bb.w - bb.y + 3;
+    const int NWIN = WX * WY;
+    const int li_root = (root / w - wy0) * WX + (root % w - wx0);
+    auto win = [&](auto fn) {
+        for (int li = tr; li < NWIN; li += TS) fn(li);
+    };
+    // stage: candidate pixels (mem), in-tile flags (pm)
+    int ncand = 0;
+    win([&](int li) {
+        const int ly = li / WX, lx = li - ly * WX;
+        const int gx = wx0 + lx, gy = wy0 + ly;
+        const bool in = gx >= 0 && gy >= 0 && gx < w && gy < h;
+        const bool c = in && a.big0[(int64_t)gy * w + gx];
+        S.mem[li] = c;
+        S.pm[li] = in;
+        S.B[li] = li;
+        ncand += c;
+    });
+    ncand = team.reduce(ncand, red.i, OpAdd());
+    team.sync();
+    // fast path 1: the window holds no other candidate, so A = every candidate pixel
+    if (ncand == area) {
+        win([&](int li) { S.sp[li] = S.mem[li]; });
+        team.sync();
+    } else {
+        fill_isolate(team, S, a, WX, NWIN, li_root);
+    }
+    // fast path 2: holes of the one 8-component A from its Euler number (bit-quads, Gray 1971:
+    // E8 = (n1 - n3 - 2 nD) / 4, holes = 1 - E8 for 4-connected background)
+    int q = 0;
+    for (int k = tr; k < (WX - 1) * (WY - 1); k += TS) {
+        const int qy = k / (WX - 1), qx = k - qy * (WX - 1);
+        const int li = qy * WX + qx;
+        const int b0 = S.sp[li], b1 = S.sp[li + 1], b2 = S.sp[li + WX], b3 = S.sp[li + WX + 1];
+        const int nq = b0 + b1 + b2 + b3;
+        if (nq == 1) q += 1;
+        else if (nq == 3) q -= 1;
+        else if (nq == 2 && b0 == b3) q -= 2;  // diagonal pair
+    }
+    q = team.reduce(q, red.i, OpAdd());
+    const bool holes = (4 - q) / 4 > 0;  // holes = 1 - q / 4
+    if (!holes) {
+        win([&](int li) {
+            if (S.sp[li]) a.F[(int64_t)(wy0 + li / WX) * w + (wx0 + li % WX)] = 1;
+        });
+        team.sync();
+        return;
+    }
+    fill_holes_window(team, S, a, WX, WY, NWIN, wx0, wy0);
+}
+
+__global__ void k_fill_classify(const int32_t* __restrict__ cnt, int32_t cap, const int4* __restrict__ bbox,
+                                int32_t* __restrict__ big, int32_t* __restrict__ nbig, int32_t* __restrict__ gate) {
+    const int n = min(*cnt, cap);
+    GRID_LOOP(ci, (int64_t)n) {
+        const int wp = win_px(bbox[ci]);
+        if (wp > kCapB) atomicExch(gate, 1);
+        else if (wp > kCapW) big[atomicAdd(nbig, 1)] = (int)ci;
+    }
+}
+
+__global__ void __launch_bounds__(kWarpsPB * 32, 4) k_fill_fused(FillArgs a, const int32_t* __restrict__ cnt,
+                                                                int32_t cap, const int32_t* __restrict__ roots,
+                                                                const int4* __restrict__ bbox,
+                                                                const int32_t* __restrict__ areas,
+                                                                const int32_t* __restrict__ big,
+                                                                const int32_t* __restrict__ nbig_p,
+                                                                int32_t* __restrict__ heads) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ int s_job;
+    __shared__ TeamRed red;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {
+        auto& S = *reinterpret_cast<CompSm<kCapB, kKoB>*>(smem_raw);
+        const TeamCTA<kWarpsPB * 32> team;
+        const int nbig = *nbig_p;
+        while (true) {
+            if (threadIdx.x == 0) s_job = atomicAdd(&heads[0], 1);
+            __syncthreads();
+            const int bi = s_job;
+            __syncthreads();
+            if (bi >= nbig) break;
+            const int ci = big[bi];
+            fill_solve(team, S, red, a, roots[ci], bbox[ci], areas[ci]);
+        }
+    }
+    {
+        auto& S = reinterpret_cast<CompSm<kCapW, kKoW>*>(smem_raw)[warp];
+        const TeamWarp team{lane};
+        const int ncomp = min(*cnt, cap);
+        while (true) {
+            int ci = 0;
+            if (lane == 0) ci = atomicAdd(&heads[1], 1);
+            ci = __shfl_sync(0xffffffffu, ci, 0);
+            if (ci >= ncomp) break;
+            const int4 bb = bbox[ci];
+            if (win_px(bb) > kCapW) continue;  // block list, or the gated whole-tile path
+            fill_solve(team, S, red, a, roots[ci], bb, areas[ci]);
+        }
+    }
+}
+
 // ---------------------------------------------------------------- global fallback
 __global__ void __launch_bounds__(kCT) k_comp_global(CompArgs a, const int32_t* __restrict__ roots,
                                                      const int4* __restrict__ bbox) {
@@ -870,6 +1066,29 @@ void launch_components(const uint8_t* F, float* dist_scratch, const uint8_t* g, 
             table->capacity));
         (note_launch(), k_copy_i32<<<1, 1, 0, s>>>(rows, table->n_rows_dev));
     }
+}
+
+void launch_fill_components(const uint8_t* big0, int w, int h, Slot& sl, const int32_t* count, uint8_t* F,
+                            uint8_t* enc, int32_t* gate, cudaStream_t s) {
+    const int64_t n = (int64_t)w * h;
+    int32_t* nbig = sl.cnt32 + 18;
+    int32_t* heads = sl.cnt32 + 19;  // [0] block-list head, [1] component-list head
+    cudaMemsetAsync(gate, 0, sizeof(int32_t), s);
+    cudaMemsetAsync(sl.cnt32 + 18, 0, 3 * sizeof(int32_t), s);
+    if (n == 0) return;
+    cudaMemsetAsync(F, 0, n, s);
+    cudaMemsetAsync(enc, 0, n, s);
+    FillArgs a{big0, w, h, F, enc, gate};
+    const size_t smw = kWarpsPB * sizeof(CompSm<kCapW, kKoW>);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_fill_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
+        attr = true;
+    }
+    const int32_t cap = sl.comp_cap;
+    (note_launch(), k_fill_classify<<<grid_for(cap), 256, 0, s>>>(count, cap, sl.sc_bbox, sl.sc_big, nbig, gate));
+    (note_launch(), k_fill_fused<<<148 * 4, kWarpsPB * 32, smw, s>>>(a, count, cap, sl.sc_root, sl.sc_bbox,
+                                                                     sl.sc_area, sl.sc_big, nbig, heads));
 }
 
 }  // namespace hp
