@@ -176,14 +176,10 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
     ev(ctx, sl, 4, s);
     // S5 on the top-hat candidates (g - recon > g1) & !rbc, evaluated inside the CCL passes
     int32_t* ncomp5 = sl.cnt32 + 16;  // S5 components kept (listed with root and bbox)
-    int32_t* fill_gate = sl.cnt32 + 17;
     launch_area_select_tophat(sl.g, sl.u8b, sl.rbc, p.g1, w, h, p.cand_min_area, p.cand_max_area, sl, sl.big0,
                               ncomp5, s);
     ev(ctx, sl, 5, s);
-    // S6 per S5 component in shared-memory windows; the whole-tile FillHoles runs only if a
-    // component's window is too big for shared memory (gate set on the device)
-    launch_fill_components(sl.big0, w, h, sl, ncomp5, sl.F, sl.split, fill_gate, s);              // S6
-    launch_fill_holes(sl.big0, w, h, sl, sl.F, s, fill_gate);
+    launch_fill_components(sl.big0, w, h, sl, ncomp5, sl.F, sl.split, s);                           // S6
     ev(ctx, sl, 6, s);
     if (ctx->global_s8s10) {
         launch_edt(sl.F, w, h, sl, nullptr, sl.dist, s);                                             // S7
@@ -371,6 +367,9 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.sc_bbox = (int4*)A(16 * (size_t)s.comp_cap);
         s.sc_area = (int32_t*)A(4 * (size_t)s.comp_cap);
         s.sc_big = (int32_t*)A(4 * (size_t)s.comp_cap);
+        s.sc_huge = (int32_t*)A(4 * (size_t)s.comp_cap);
+        s.big_px = (int64_t)(cfg->max_width + 2) * (cfg->max_height + 2);
+        s.big_scratch = (uint8_t*)A(28 * (size_t)s.big_px);
         s.counters = (unsigned long long*)A(8 * 4);
         s.cnt32 = (int32_t*)A(4 * 32);
         s.stg_label = (int32_t*)A(4 * (size_t)mo);
@@ -388,7 +387,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.h_nrows = (int32_t*)halloc(16);
         void* all[] = {s.g, s.flags, s.rbc, s.u8a, s.u8b, s.cand, s.big0, s.F, s.split, s.pmask, s.lab, s.aux,
                        s.ML, s.d, s.L, s.dist, s.J, s.c, s.gcol, s.seg_top, s.seg_bot, s.wl.state, s.wl.inrows, s.wl.queue,
-                       s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.comp_root, s.comp_bbox, s.comp_big, s.cs_edge, s.cs_roots, s.cs_nroots, s.sc_root, s.sc_bbox, s.sc_area, s.sc_big, s.cid, s.stg_label, s.stg_flags, s.stg_feat, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
+                       s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.comp_root, s.comp_bbox, s.comp_big, s.cs_edge, s.cs_roots, s.cs_nroots, s.sc_root, s.sc_bbox, s.sc_area, s.sc_big, s.sc_huge, s.big_scratch, s.cid, s.stg_label, s.stg_flags, s.stg_feat, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
                        s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows};
         for (void* p : all)
             if (!p) { hp_ctx_destroy(ctx); return HP_ERR_NOMEM; }

@@ -83,6 +83,10 @@ struct Slot {
     int4* sc_bbox;
     int32_t* sc_area;
     int32_t* sc_big;
+    int32_t* sc_huge;      // components whose window exceeds shared memory
+    // global-memory window storage for those (k_comp.cu CompGm), big_px pixels per plane
+    uint8_t* big_scratch;
+    int64_t big_px;
     int32_t* cid;
     int32_t comp_cap;
     // staging table of the fused S8-S11 path (rows in discovery order)
@@ -146,10 +150,10 @@ void launch_area_select(const uint8_t* cand, int w, int h, int amin, int amax, S
 void launch_area_select_tophat(const uint8_t* g, const uint8_t* R, const uint8_t* rbc, int g1, int w, int h,
                                int amin, int amax, Slot& sl, uint8_t* out, int32_t* count, cudaStream_t s);
 // S6 per S5 component (k_comp.cu): F = component | its holes, enc = other candidates inside a
-// hole; *gate set to 1 if a component's window is too large (then the caller's gated whole-tile
-// FillHoles must run)
+// hole (shared-memory windows; the rare windows too big for shared memory in one block over
+// global-memory storage)
 void launch_fill_components(const uint8_t* big0, int w, int h, Slot& sl, const int32_t* count, uint8_t* F,
-                            uint8_t* enc, int32_t* gate, cudaStream_t s);
+                            uint8_t* enc, cudaStream_t s);
 // IWPP / worklist engine
 void wl_init_all(const Worklist& wl, int w, int h, cudaStream_t s);
 void wl_init_from_mask(const Worklist& wl, const uint8_t* mask, int w, int h, cudaStream_t s);

@@ -149,6 +149,8 @@ __device__ __forceinline__ void write_row(const CompArgs& a, int32_t label, int 
 // Per-team window storage (4-byte planes first for alignment); 19 B per window pixel.
 template <int CAP, int KO>
 struct CompSm {
+    using list_t = int16_t;
+    static constexpr int kKO = KO;
     float dist[CAP];
     float A[CAP];      // J, then c
     int32_t B[CAP];    // zone union-find, then L, then object union-find
@@ -164,10 +166,58 @@ struct CompSm {
     FeatSmem fs;
 };
 
+// The same per-window storage in global memory, for windows too large for shared memory (one
+// block processes them one after another; the planes are slot scratch of (W+2)(H+2) pixels).
+struct CompGm {
+    using list_t = int32_t;
+    static constexpr int kKO = 1 << 30;  // objroot holds up to one entry per window pixel
+    float* dist;
+    float* A;
+    int32_t* B;
+    int32_t* C;
+    int32_t* list;
+    uint8_t* mem;
+    uint8_t* pm;
+    uint8_t* sp;
+    int& nmem;
+    int& nbnd;
+    int& nobj;
+    int32_t* objroot;
+    FeatSmem& fs;
+};
+
+struct BigScratch {
+    float* dist;
+    float* A;
+    int32_t* B;
+    int32_t* C;
+    int32_t* list;
+    int32_t* objroot;
+    uint8_t* mem;
+    uint8_t* pm;
+    uint8_t* sp;
+};
+
+inline BigScratch carve_big(const Slot& sl) {
+    const int64_t n = sl.big_px;
+    uint8_t* p = sl.big_scratch;
+    BigScratch b;
+    b.dist = reinterpret_cast<float*>(p);
+    b.A = reinterpret_cast<float*>(p + 4 * n);
+    b.B = reinterpret_cast<int32_t*>(p + 8 * n);
+    b.C = reinterpret_cast<int32_t*>(p + 12 * n);
+    b.list = reinterpret_cast<int32_t*>(p + 16 * n);
+    b.objroot = reinterpret_cast<int32_t*>(p + 20 * n);
+    b.mem = p + 24 * n;
+    b.pm = p + 25 * n;
+    b.sp = p + 26 * n;
+    return b;
+}
+
 // Solve S8-S11 of one component in a team's shared memory.  Returns false (nothing written)
 // if the component must go to the global path instead.
-template <class Team, int CAP, int KO>
-__device__ bool comp_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, const CompArgs& a,
+template <class Team, class St>
+__device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs& a,
                            int32_t root, int4 bb) {
     const int w = a.w, h = a.h;
     const int tr = team.rank();
@@ -202,10 +252,10 @@ __device__ bool comp_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, c
         }
         if constexpr (TS == 32) {  // warp team: ballot compaction (window order)
             const unsigned bal = __ballot_sync(0xffffffffu, m);
-            if (m) S.list[nmem + __popc(bal & ((1u << tr) - 1u))] = (int16_t)li;
+            if (m) S.list[nmem + __popc(bal & ((1u << tr) - 1u))] = (typename St::list_t)li;
             nmem += __popc(bal);
         } else {
-            if (m) S.list[atomicAdd(&S.nmem, 1)] = (int16_t)li;
+            if (m) S.list[atomicAdd(&S.nmem, 1)] = (typename St::list_t)li;
         }
     }
     team.sync();
@@ -425,12 +475,12 @@ __device__ bool comp_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, c
     each([&](int li) {
         if (S.B[li] == li && S.C[li] >= a.amin && S.C[li] <= a.amax) {
             int k = atomicAdd(&S.nobj, 1);
-            if (k < KO) S.objroot[k] = li;
+            if (k < St::kKO) S.objroot[k] = li;
         }
     });
     team.sync();
     const int nobj = S.nobj;
-    if (nobj > KO) return false;  // too many objects for the list: global path instead
+    if (nobj > St::kKO) return false;  // too many objects for the list: global path instead
     each([&](int li) {
         int r = S.B[li];
         int32_t v = 0;
@@ -548,12 +598,11 @@ struct FillArgs {
     int w, h;
     uint8_t* F;
     uint8_t* enc;
-    int32_t* gate;
 };
 
 // A = the 8-component of the root among the window's candidate pixels (union-find) -> sp
-template <class Team, int CAP, int KO>
-__device__ void fill_isolate(const Team& team, CompSm<CAP, KO>& S, const FillArgs& a, int WX, int NWIN, int li_root) {
+template <class Team, class St>
+__device__ void fill_isolate(const Team& team, St& S, const FillArgs& a, int WX, int NWIN, int li_root) {
     const int tr = team.rank();
     constexpr int TS = Team::size;
     auto win = [&](auto fn) {
@@ -577,8 +626,8 @@ __device__ void fill_isolate(const Team& team, CompSm<CAP, KO>& S, const FillArg
 
 // the holes of A (sp): 4-connected union-find over the non-A pixels, seeds = ring, out-of-tile
 // and tile-border pixels; F |= A | holes, enc |= candidates inside the holes
-template <class Team, int CAP, int KO>
-__device__ void fill_holes_window(const Team& team, CompSm<CAP, KO>& S, const FillArgs& a, int WX, int WY,
+template <class Team, class St>
+__device__ void fill_holes_window(const Team& team, St& S, const FillArgs& a, int WX, int WY,
                                   int NWIN, int wx0, int wy0) {
     const int w = a.w, h = a.h;
     const int tr = team.rank();
@@ -620,8 +669,8 @@ __device__ void fill_holes_window(const Team& team, CompSm<CAP, KO>& S, const Fi
     team.sync();
 }
 
-template <class Team, int CAP, int KO>
-__device__ void fill_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, const FillArgs& a, int32_t root,
+template <class Team, class St>
+__device__ void fill_solve(const Team& team, St& S, TeamRed& red, const FillArgs& a, int32_t root,
                            int4 bb, int area) {
     const int w = a.w, h = a.h;
     const int tr = team.rank();
@@ -678,13 +727,33 @@ __device__ void fill_solve(const Team& team, CompSm<CAP, KO>& S, TeamRed& red, c
     fill_holes_window(team, S, a, WX, WY, NWIN, wx0, wy0);
 }
 
-__global__ void k_fill_classify(const int32_t* __restrict__ cnt, int32_t cap, const int4* __restrict__ bbox,
-                                int32_t* __restrict__ big, int32_t* __restrict__ nbig, int32_t* __restrict__ gate) {
+// windows > kCapW: block list; > kCapB: huge list (global-memory storage)
+__global__ void k_win_classify(const int32_t* __restrict__ cnt, int32_t cap, const int4* __restrict__ bbox,
+                               int32_t* __restrict__ big, int32_t* __restrict__ nbig, int32_t* __restrict__ huge,
+                               int32_t* __restrict__ nhuge) {
     const int n = min(*cnt, cap);
     GRID_LOOP(ci, (int64_t)n) {
         const int wp = win_px(bbox[ci]);
-        if (wp > kCapB) atomicExch(gate, 1);
+        if (wp > kCapB) huge[atomicAdd(nhuge, 1)] = (int)ci;
         else if (wp > kCapW) big[atomicAdd(nbig, 1)] = (int)ci;
+    }
+}
+
+// the huge windows, one after another in one block over global-memory storage
+constexpr int kHugeT = 256;
+__global__ void __launch_bounds__(kHugeT) k_fill_huge(FillArgs a, const int32_t* __restrict__ roots,
+                                                      const int4* __restrict__ bbox, const int32_t* __restrict__ areas,
+                                                      const int32_t* __restrict__ huge,
+                                                      const int32_t* __restrict__ nhuge, BigScratch bs) {
+    __shared__ int nmem, nbnd, nobj;
+    __shared__ FeatSmem fs;
+    __shared__ TeamRed red;
+    CompGm S{bs.dist, bs.A, bs.B, bs.C, bs.list, bs.mem, bs.pm, bs.sp, nmem, nbnd, nobj, bs.objroot, fs};
+    const TeamCTA<kHugeT> team;
+    const int n = *nhuge;
+    for (int k = 0; k < n; ++k) {
+        const int ci = huge[k];
+        fill_solve(team, S, red, a, roots[ci], bbox[ci], areas[ci]);
     }
 }
 
@@ -723,7 +792,7 @@ __global__ void __launch_bounds__(kWarpsPB * 32, 4) k_fill_fused(FillArgs a, con
             ci = __shfl_sync(0xffffffffu, ci, 0);
             if (ci >= ncomp) break;
             const int4 bb = bbox[ci];
-            if (win_px(bb) > kCapW) continue;  // block list, or the gated whole-tile path
+            if (win_px(bb) > kCapW) continue;  // block or huge list
             fill_solve(team, S, red, a, roots[ci], bb, areas[ci]);
         }
     }
@@ -1069,16 +1138,16 @@ void launch_components(const uint8_t* F, float* dist_scratch, const uint8_t* g, 
 }
 
 void launch_fill_components(const uint8_t* big0, int w, int h, Slot& sl, const int32_t* count, uint8_t* F,
-                            uint8_t* enc, int32_t* gate, cudaStream_t s) {
+                            uint8_t* enc, cudaStream_t s) {
     const int64_t n = (int64_t)w * h;
     int32_t* nbig = sl.cnt32 + 18;
     int32_t* heads = sl.cnt32 + 19;  // [0] block-list head, [1] component-list head
-    cudaMemsetAsync(gate, 0, sizeof(int32_t), s);
-    cudaMemsetAsync(sl.cnt32 + 18, 0, 3 * sizeof(int32_t), s);
+    int32_t* nhuge = sl.cnt32 + 21;
+    cudaMemsetAsync(sl.cnt32 + 18, 0, 4 * sizeof(int32_t), s);
     if (n == 0) return;
     cudaMemsetAsync(F, 0, n, s);
     cudaMemsetAsync(enc, 0, n, s);
-    FillArgs a{big0, w, h, F, enc, gate};
+    FillArgs a{big0, w, h, F, enc};
     const size_t smw = kWarpsPB * sizeof(CompSm<kCapW, kKoW>);
     static bool attr = false;
     if (!attr) {
@@ -1086,9 +1155,12 @@ void launch_fill_components(const uint8_t* big0, int w, int h, Slot& sl, const i
         attr = true;
     }
     const int32_t cap = sl.comp_cap;
-    (note_launch(), k_fill_classify<<<grid_for(cap), 256, 0, s>>>(count, cap, sl.sc_bbox, sl.sc_big, nbig, gate));
+    (note_launch(), k_win_classify<<<grid_for(cap), 256, 0, s>>>(count, cap, sl.sc_bbox, sl.sc_big, nbig, sl.sc_huge,
+                                                                  nhuge));
     (note_launch(), k_fill_fused<<<148 * 4, kWarpsPB * 32, smw, s>>>(a, count, cap, sl.sc_root, sl.sc_bbox,
                                                                      sl.sc_area, sl.sc_big, nbig, heads));
+    (note_launch(), k_fill_huge<<<1, kHugeT, 0, s>>>(a, sl.sc_root, sl.sc_bbox, sl.sc_area, sl.sc_huge, nhuge,
+                                                    carve_big(sl)));
 }
 
 }  // namespace hp

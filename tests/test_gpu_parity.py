@@ -260,6 +260,30 @@ def test_pipeline_partial_tissue(ctx, seed, t):
     _check_pipeline(ctx, rgb)
 
 
+def _painted_tile():
+    """A sparse synthetic tile with a thin dark ring (a candidate whose bounding box is far
+    larger than any shared-memory window, with a large hole: the huge-window S6 path and the
+    global S7-S11 fallback) and a 1-px diagonal line (area < 1000 px, window ~160K px)."""
+    rgb = make_tile(11, TileSpec(1024, 1024, density=2e-5))["rgb"].copy()
+    yy, xx = np.mgrid[0:1024, 0:1024]
+    ring = np.abs(np.hypot(xx - 400, yy - 400) - 70) < 1.0
+    line = (np.abs((xx - 600) - (yy - 500)) < 1) & (xx > 600) & (xx < 1000)
+    for m in (ring, line):
+        rgb[m] = (70, 30, 110)
+    return rgb
+
+
+def test_pipeline_huge_windows(ctx):
+    rgb = _painted_tile()
+    # the painted structures do reach S6 as candidates (else the test would test nothing)
+    g, fl, _ = oracle.cd(rgb)
+    cand = oracle.recon_to_nuclei(g, oracle.open_(g), oracle.rbc(fl))
+    big0 = oracle.area_threshold(cand)
+    assert big0[328:472, 328:472].sum() > 300        # the ring (bbox 142 x 142)
+    assert big0[500:900, 600:1000].sum() > 200       # the line (bbox ~400 x 400)
+    _check_pipeline(ctx, rgb)
+
+
 def test_pipeline_edge_cases(ctx):
     _check_pipeline(ctx, np.full((64, 80, 3), 255, U8))          # glass only
     _check_pipeline(ctx, np.zeros((50, 70, 3), U8))               # black
