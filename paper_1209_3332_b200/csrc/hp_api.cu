@@ -199,7 +199,7 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
             cudaStreamWaitEvent(sl.hstream, sl.fork_ev, 0);
             cs = sl.hstream;
         }
-        launch_components(sl.F, sl.dist, sl.g, p.h, p.obj_min_area, p.obj_max_area, w, h, sl, labels, lpitch,
+        launch_components(ncomp5, sl.split, sl.g, p.h, p.obj_min_area, p.obj_max_area, w, h, sl, labels, lpitch,
                           n_objects, table, ctx->cfg.max_objects, cs);
         if (ctx->prio >= 2) {
             cudaEventRecord(sl.join_ev, sl.hstream);

@@ -31,57 +31,9 @@ constexpr int kCT = kFT;          // threads per component CTA (8 warps)
 
 inline int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 16); }
 
-// ---------------------------------------------------------------- component discovery
-__global__ void k_comp_roots(const int32_t* __restrict__ lab, int64_t n, int32_t* __restrict__ cnt,
-                             int32_t* __restrict__ roots, int32_t cap, int32_t* __restrict__ cid) {
-    GRID_LOOP(p, n) {
-        if (lab[p] == (int32_t)p) {
-            int i = atomicAdd(cnt, 1);
-            if (i < cap) {
-                roots[i] = (int32_t)p;
-                cid[p] = i;
-            }
-        }
-    }
-}
-
-__global__ void k_comp_bbox_init(const int32_t* __restrict__ cnt, int32_t cap, int4* __restrict__ bbox) {
-    const int n = min(*cnt, cap);
-    GRID_LOOP(i, (int64_t)n) bbox[i] = make_int4(INT_MAX, INT_MAX, -1, -1);
-}
-
-__global__ void k_comp_bbox(const int32_t* __restrict__ lab, const int32_t* __restrict__ cid, int w, int h,
-                            int32_t cap, int4* __restrict__ bbox) {
-    const int64_t n = (int64_t)w * h;
-    for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
-        int64_t p = base + threadIdx.x;
-        int id = -1, x = 0, y = 0;
-        if (p < n) {
-            int32_t r = lab[p];
-            if (r >= 0) {
-                id = cid[r];
-                y = (int)(p / w);
-                x = (int)(p - (int64_t)y * w);
-            }
-        }
-        unsigned peers = __match_any_sync(0xffffffffu, id);
-        if (id < 0 || id >= cap) continue;
-        int x0 = __reduce_min_sync(peers, x), y0 = __reduce_min_sync(peers, y);
-        int x1 = __reduce_max_sync(peers, x), y1 = __reduce_max_sync(peers, y);
-        if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) {
-            int* b = reinterpret_cast<int*>(&bbox[id]);
-            atomicMin(&b[0], x0);
-            atomicMin(&b[1], y0);
-            atomicMax(&b[2], x1);
-            atomicMax(&b[3], y1);
-        }
-    }
-}
-
 struct CompArgs {
-    const uint8_t* F;
-    const int32_t* labF;   // root (min index) of each F pixel's 8-component, -1 outside F
-    const float* dist;
+    const int32_t* labF;   // per F pixel: the root of its F component (written by S6), else ~0
+    const uint8_t* enc;    // S6: candidate pixels enclosed in another component's hole
     const uint8_t* g;      // for features
     float hh;
     int w, h;
@@ -96,17 +48,9 @@ struct CompArgs {
     int32_t* row_flags;
     float* row_feat;
     int do_features;
-    // overflow: components too big for shared memory -> global path
+    // components for the global-memory (one block) path: huge windows, object-list overflow
     int32_t* ovf_cnt;
     int32_t* ovf_list;
-    // global-path planes
-    float *J, *c;
-    int32_t *zl, *d, *L, *aux;
-    uint8_t *pm, *split;
-    // objects of the global path that need features: (root, component id)
-    int32_t* gobj_cnt;
-    int2* gobj;
-    int32_t gobj_cap;
 };
 
 // find with CAS path halving (x -> grandparent iff x still points at that parent; safe beside
@@ -527,10 +471,14 @@ __device__ __forceinline__ void to_global(const CompArgs& a, int ci) {
 }
 
 // windows > kCapW go to the block list, windows > kCapB straight to the global path
+// S5 components -> block list (windows > kCapW) / global-memory list (> kCapB); islands enclosed
+// in another component's hole (enc at their root) are solved with their encloser
 __global__ void k_comp_classify(CompArgs a, const int32_t* __restrict__ cnt, int32_t cap,
-                                const int4* __restrict__ bbox, int32_t* __restrict__ big, int32_t* __restrict__ nbig) {
+                                const int32_t* __restrict__ roots, const int4* __restrict__ bbox,
+                                int32_t* __restrict__ big, int32_t* __restrict__ nbig) {
     const int n = min(*cnt, cap);
     GRID_LOOP(ci, (int64_t)n) {
+        if (a.enc[roots[ci]]) continue;
         const int wp = win_px(bbox[ci]);
         if (wp > kCapB) to_global(a, (int)ci);
         else if (wp > kCapW) big[atomicAdd(nbig, 1)] = (int)ci;
@@ -576,7 +524,7 @@ __global__ void __launch_bounds__(kWarpsPB * 32, 4) k_comp_fused(CompArgs a, con
             ci = __shfl_sync(0xffffffffu, ci, 0);
             if (ci >= ncomp) break;
             const int4 bb = bbox[ci];
-            if (win_px(bb) > kCapW) continue;  // block list or global path
+            if (win_px(bb) > kCapW || a.enc[roots[ci]]) continue;  // block / global list, or an island
             if (!comp_solve(team, S, red, a, roots[ci], bb) && lane == 0) to_global(a, ci);
             __syncwarp();
         }
@@ -598,7 +546,15 @@ struct FillArgs {
     int w, h;
     uint8_t* F;
     uint8_t* enc;
+    unsigned* labF;  // per F pixel: min root over the components whose F contains it (~0 else)
 };
+
+// F pixel p belongs to the F component of root: an island enclosed by A is written by A and by
+// itself; A's root (its minimum linear index, above the island) wins, as in a CCL of F
+__device__ __forceinline__ void mark_f(const FillArgs& a, int64_t p, int32_t root) {
+    a.F[p] = 1;
+    atomicMin(&a.labF[p], (unsigned)root);
+}
 
 // A = the 8-component of the root among the window's candidate pixels (union-find) -> sp
 template <class Team, class St>
@@ -628,7 +584,7 @@ __device__ void fill_isolate(const Team& team, St& S, const FillArgs& a, int WX,
 // and tile-border pixels; F |= A | holes, enc |= candidates inside the holes
 template <class Team, class St>
 __device__ void fill_holes_window(const Team& team, St& S, const FillArgs& a, int WX, int WY,
-                                  int NWIN, int wx0, int wy0) {
+                                  int NWIN, int wx0, int wy0, int32_t root) {
     const int w = a.w, h = a.h;
     const int tr = team.rank();
     constexpr int TS = Team::size;
@@ -660,9 +616,9 @@ __device__ void fill_holes_window(const Team& team, St& S, const FillArgs& a, in
         const int ly = li / WX, lx = li - ly * WX;
         const int64_t p = (int64_t)(wy0 + ly) * w + (wx0 + lx);
         if (S.sp[li]) {
-            a.F[p] = 1;
+            mark_f(a, p, root);
         } else if (S.B[cfind(S.C, li)] == 0) {  // a hole of A
-            a.F[p] = 1;
+            mark_f(a, p, root);
             if (S.mem[li]) a.enc[p] = 1;         // another candidate, enclosed by A
         }
     });
@@ -719,12 +675,12 @@ __device__ void fill_solve(const Team& team, St& S, TeamRed& red, const FillArgs
     const bool holes = (4 - q) / 4 > 0;  // holes = 1 - q / 4
     if (!holes) {
         win([&](int li) {
-            if (S.sp[li]) a.F[(int64_t)(wy0 + li / WX) * w + (wx0 + li % WX)] = 1;
+            if (S.sp[li]) mark_f(a, (int64_t)(wy0 + li / WX) * w + (wx0 + li % WX), root);
         });
         team.sync();
         return;
     }
-    fill_holes_window(team, S, a, WX, WY, NWIN, wx0, wy0);
+    fill_holes_window(team, S, a, WX, WY, NWIN, wx0, wy0, root);
 }
 
 // windows > kCapW: block list; > kCapB: huge list (global-memory storage)
@@ -754,6 +710,21 @@ __global__ void __launch_bounds__(kHugeT) k_fill_huge(FillArgs a, const int32_t*
     for (int k = 0; k < n; ++k) {
         const int ci = huge[k];
         fill_solve(team, S, red, a, roots[ci], bbox[ci], areas[ci]);
+    }
+}
+
+// S7-S11 of the components left to the global-memory storage, one after another in one block
+__global__ void __launch_bounds__(kHugeT) k_comp_huge(CompArgs a, const int32_t* __restrict__ roots,
+                                                      const int4* __restrict__ bbox, BigScratch bs) {
+    __shared__ int nmem, nbnd, nobj;
+    __shared__ FeatSmem fs;
+    __shared__ TeamRed red;
+    CompGm S{bs.dist, bs.A, bs.B, bs.C, bs.list, bs.mem, bs.pm, bs.sp, nmem, nbnd, nobj, bs.objroot, fs};
+    const TeamCTA<kHugeT> team;
+    const int n = *a.ovf_cnt;
+    for (int k = 0; k < n; ++k) {
+        const int ci = a.ovf_list[k];
+        comp_solve(team, S, red, a, roots[ci], bbox[ci]);
     }
 }
 
@@ -798,237 +769,6 @@ __global__ void __launch_bounds__(kWarpsPB * 32, 4) k_fill_fused(FillArgs a, con
     }
 }
 
-// ---------------------------------------------------------------- global fallback
-__global__ void __launch_bounds__(kCT) k_comp_global(CompArgs a, const int32_t* __restrict__ roots,
-                                                     const int4* __restrict__ bbox) {
-    const int ncomp = *a.ovf_cnt;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int w = a.w, h = a.h;
-    for (int oi = blockIdx.x; oi < ncomp; oi += gridDim.x) {
-        const int ci = a.ovf_list[oi];
-        const int32_t root = roots[ci];
-        const int4 bb = bbox[ci];
-        const int bx0 = bb.x, by0 = bb.y, bx1 = bb.z, by1 = bb.w;
-        auto mem = [&](int x, int y) -> bool {
-            if (x < 0 || y < 0 || x >= w || y >= h) return false;
-            return a.labF[(int64_t)y * w + x] == root;
-        };
-        auto each = [&](auto fn) {
-            for (int y = by0 + warp; y <= by1; y += kCT / 32)
-                for (int x = bx0 + lane; x <= bx1; x += 32) {
-                    int64_t p = (int64_t)y * w + x;
-                    if (a.labF[p] == root) fn(x, y, p);
-                }
-        };
-        auto converge = [&](auto step) {
-            while (true) {
-                int ch = 0;
-                each([&](int x, int y, int64_t p) { ch |= step(x, y, p) ? 1 : 0; });
-                if (!__syncthreads_or(ch)) break;
-            }
-        };
-        each([&](int x, int y, int64_t p) { a.J[p] = fminf(__fsub_rn(a.dist[p], a.hh), a.dist[p]); });
-        __syncthreads();
-        converge([&](int x, int y, int64_t p) -> bool {
-            float jp = a.J[p], b = jp;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                int qx = x + dx8(j), qy = y + dy8(j);
-                if (mem(qx, qy)) b = fmaxf(b, a.J[(int64_t)qy * w + qx]);
-            }
-            float nv = fminf(b, a.dist[p]);
-            if (nv > jp) { a.J[p] = nv; return true; }
-            return false;
-        });
-        each([&](int x, int y, int64_t p) { a.zl[p] = (int32_t)p; });
-        __syncthreads();
-        converge([&](int x, int y, int64_t p) -> bool {
-            int32_t z = a.zl[p], b = z;
-            float jp = a.J[p];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                int qx = x + dx8(j), qy = y + dy8(j);
-                if (!mem(qx, qy)) continue;
-                int64_t q = (int64_t)qy * w + qx;
-                if (a.J[q] == jp) b = min(b, a.zl[q]);
-            }
-            if (b < z) { a.zl[p] = b; return true; }
-            return false;
-        });
-        each([&](int x, int y, int64_t p) { if (a.zl[p] == (int32_t)p) a.aux[p] = 0; });
-        __syncthreads();
-        each([&](int x, int y, int64_t p) {
-            float jp = a.J[p];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                int qx = x + dx8(j), qy = y + dy8(j);
-                if (mem(qx, qy) && a.J[(int64_t)qy * w + qx] > jp) { a.aux[a.zl[p]] = 1; break; }
-            }
-        });
-        __syncthreads();
-        each([&](int x, int y, int64_t p) {
-            int32_t z = a.zl[p];
-            int32_t ml = a.aux[z] == 0 ? z + 1 : 0;
-            a.d[p] = ml;
-            a.c[p] = ml ? a.dist[p] : -INFINITY;
-        });
-        __syncthreads();
-        converge([&](int x, int y, int64_t p) -> bool {
-            float cp = a.c[p], b = cp;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                int qx = x + dx8(j), qy = y + dy8(j);
-                if (mem(qx, qy)) b = fmaxf(b, a.c[(int64_t)qy * w + qx]);
-            }
-            float nv = fminf(b, a.dist[p]);
-            if (nv > cp) { a.c[p] = nv; return true; }
-            return false;
-        });
-        each([&](int x, int y, int64_t p) { a.L[p] = a.d[p] ? a.d[p] : kInfI; });
-        __syncthreads();
-        each([&](int x, int y, int64_t p) {
-            int32_t v = kInfI;
-            if (a.L[p] != kInfI) {
-                v = 0;
-            } else {
-                float cp = a.c[p];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    int qx = x + dx8(j), qy = y + dy8(j);
-                    if (mem(qx, qy) && a.c[(int64_t)qy * w + qx] > cp) { v = 1; break; }
-                }
-            }
-            a.d[p] = v;
-        });
-        __syncthreads();
-        converge([&](int x, int y, int64_t p) -> bool {
-            int32_t dp = a.d[p];
-            if (dp <= 1) return false;
-            float cp = a.c[p];
-            int32_t b = dp;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                int qx = x + dx8(j), qy = y + dy8(j);
-                if (!mem(qx, qy)) continue;
-                int64_t q = (int64_t)qy * w + qx;
-                if (a.c[q] == cp) b = min(b, sat_add(a.d[q], 1));
-            }
-            if (b < dp) { a.d[p] = b; return true; }
-            return false;
-        });
-        each([&](int x, int y, int64_t p) {
-            uint8_t bits = 0;
-            if (a.L[p] == kInfI) {
-                float cp = a.c[p];
-                bool have = false;
-                float bc = 0.f;
-                int32_t bd = 0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    int qx = x + dx8(j), qy = y + dy8(j);
-                    if (!mem(qx, qy)) continue;
-                    int64_t q = (int64_t)qy * w + qx;
-                    float cq = a.c[q];
-                    if (!(cq >= cp)) continue;
-                    int32_t dq = a.d[q];
-                    if (!have || cq > bc || (cq == bc && dq < bd)) {
-                        have = true;
-                        bc = cq;
-                        bd = dq;
-                        bits = (uint8_t)(1u << j);
-                    } else if (cq == bc && dq == bd) {
-                        bits |= (uint8_t)(1u << j);
-                    }
-                }
-            }
-            a.pm[p] = bits;
-        });
-        __syncthreads();
-        converge([&](int x, int y, int64_t p) -> bool {
-            int pmk = a.pm[p];
-            if (!pmk) return false;
-            int32_t lp = a.L[p], b = lp;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                if ((pmk >> j) & 1) b = min(b, a.L[(int64_t)(y + dy8(j)) * w + x + dx8(j)]);
-            if (b < lp) { a.L[p] = b; return true; }
-            return false;
-        });
-        each([&](int x, int y, int64_t p) {
-            int32_t lp = a.L[p];
-            uint8_t v = 1;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                int qx = x + dx8(j), qy = y + dy8(j);
-                if (mem(qx, qy) && a.L[(int64_t)qy * w + qx] < lp) { v = 0; break; }
-            }
-            a.split[p] = v;
-        });
-        __syncthreads();
-        each([&](int x, int y, int64_t p) { a.zl[p] = a.split[p] ? (int32_t)p : -1; });
-        __syncthreads();
-        converge([&](int x, int y, int64_t p) -> bool {
-            int32_t z = a.zl[p];
-            if (z < 0) return false;
-            int32_t b = z;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                int qx = x + dx8(j), qy = y + dy8(j);
-                if (!mem(qx, qy)) continue;
-                int32_t zq = a.zl[(int64_t)qy * w + qx];
-                if (zq >= 0) b = min(b, zq);
-            }
-            if (b < z) { a.zl[p] = b; return true; }
-            return false;
-        });
-        each([&](int x, int y, int64_t p) { if (a.zl[p] == (int32_t)p) a.aux[p] = 0; });
-        __syncthreads();
-        each([&](int x, int y, int64_t p) {
-            int32_t z = a.zl[p];
-            if (z >= 0) atomicAdd(&a.aux[z], 1);
-        });
-        __syncthreads();
-        each([&](int x, int y, int64_t p) {
-            int32_t z = a.zl[p], v = 0;
-            if (z >= 0) {
-                int area = a.aux[z];
-                if (area >= a.amin && area <= a.amax) {
-                    v = z + 1;
-                    if (z == (int32_t)p) {
-                        atomicAdd(a.n_objects, 1);
-                        int k = atomicAdd(a.gobj_cnt, 1);
-                        if (k < a.gobj_cap) a.gobj[k] = make_int2(z, ci);
-                    }
-                }
-            }
-            a.labels[(int64_t)y * a.lpitch + x] = v;
-        });
-        __syncthreads();
-    }
-}
-
-// features of the objects produced by the global fallback (component bbox bounds the object)
-__global__ void __launch_bounds__(kFT, 2) k_obj_feat_list(CompArgs a, const int4* __restrict__ bbox) {
-    __shared__ FeatSmem fs;
-    __shared__ TeamRed red;
-    const TeamCTA<> team;
-    const int n = min(*a.gobj_cnt, a.gobj_cap);
-    for (int i = blockIdx.x; i < n; i += gridDim.x) {
-        const int2 e = a.gobj[i];
-        const int32_t lab = e.x + 1;
-        const int4 bb = bbox[e.y];
-        auto inP = [&](int x, int y) {
-            return x >= 0 && y >= 0 && x < a.w && y < a.h && a.labels[(int64_t)y * a.lpitch + x] == lab;
-        };
-        double f[HP_NFEAT];
-        int border = 0;
-        object_features(team, inP, a.g, a.w, a.h, bb.x, bb.y, bb.z, bb.w, fs, red, f, &border);
-        if (threadIdx.x == 0) write_row(a, lab, border, f);
-        __syncthreads();
-    }
-}
-
-// order the staged rows by label (rank = number of smaller labels) into the output table
 __global__ void k_rows_scatter(const int32_t* __restrict__ cnt, int32_t cap, const int32_t* __restrict__ sl,
                                const int32_t* __restrict__ sf, const float* __restrict__ sfeat,
                                int32_t* __restrict__ ol, int32_t* __restrict__ of, float* __restrict__ ofeat,
@@ -1060,18 +800,19 @@ __global__ void k_copy_i32(const int32_t* __restrict__ src, int32_t* __restrict_
 
 // S8-S10 (+ S11 when table != nullptr) of the pipeline on F and dist: labels (zeroed here),
 // n_objects, and the feature rows in label order.
-// S7-S11 per component.  dist_scratch: a slot plane that receives the global EDT, computed
-// only if some component takes the global path (the shared-memory path computes its own).
-void launch_components(const uint8_t* F, float* dist_scratch, const uint8_t* g, float hh, int amin, int amax,
+// S7-S11 per F component, from the S5 component list: the F component of a kept candidate
+// component A is A with its holes and any islands inside them -- the pixels whose root word
+// (written by S6) is A's root.  Islands enclosed by another component (enc at their root) are
+// solved with their encloser.  Shared-memory windows (warp / block teams); windows too big for
+// shared memory and object-list overflows in one block over global-memory storage.
+void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t* g, float hh, int amin, int amax,
                        int w, int h, Slot& sl, int32_t* labels, int64_t lpitch, int32_t* n_objects,
                        const hp_feature_table* table, int32_t max_objects, cudaStream_t s) {
     const int64_t n = (int64_t)w * h;
     cudaMemsetAsync(n_objects, 0, sizeof(int32_t), s);
     cudaMemset2DAsync(labels, lpitch * sizeof(int32_t), 0, w * sizeof(int32_t), h, s);
-    int32_t* cnt = sl.cnt32 + 8;     // components
-    int32_t* ovf = sl.cnt32 + 9;     // overflow components
+    int32_t* ovf = sl.cnt32 + 9;     // components for the global-memory path
     int32_t* rows = sl.cnt32 + 10;   // staged rows
-    int32_t* gobj = sl.cnt32 + 11;   // objects of the global path
     int32_t* nbig = sl.cnt32 + 12;   // block-list components
     int32_t* heads = sl.cnt32 + 13;  // [0] block-list head, [1] component-list head
     cudaMemsetAsync(sl.cnt32 + 8, 0, 8 * sizeof(int32_t), s);
@@ -1079,16 +820,10 @@ void launch_components(const uint8_t* F, float* dist_scratch, const uint8_t* g, 
         if (table) cudaMemsetAsync(table->n_rows_dev, 0, sizeof(int32_t), s);
         return;
     }
-    CclSrc cs{F, 0, false, nullptr};
-    launch_ccl(cs, w, h, 8, sl.lab, nullptr, s);
     const int32_t cap = sl.comp_cap;
-    (note_launch(), k_comp_roots<<<grid_for(n), 256, 0, s>>>(sl.lab, n, cnt, sl.comp_root, cap, sl.cid));
-    (note_launch(), k_comp_bbox_init<<<grid_for(cap), 256, 0, s>>>(cnt, cap, sl.comp_bbox));
-    (note_launch(), k_comp_bbox<<<grid_for(n), 256, 0, s>>>(sl.lab, sl.cid, w, h, cap, sl.comp_bbox));
     CompArgs a{};
-    a.F = F;
     a.labF = sl.lab;
-    a.dist = dist_scratch;
+    a.enc = enc;
     a.g = g;
     a.hh = hh;
     a.w = w;
@@ -1105,31 +840,19 @@ void launch_components(const uint8_t* F, float* dist_scratch, const uint8_t* g, 
     a.row_feat = sl.stg_feat;
     a.do_features = table != nullptr;
     a.ovf_cnt = ovf;
-    a.ovf_list = sl.cid;  // the root -> component map is no longer needed after k_comp_bbox
-    a.J = sl.J;
-    a.c = sl.c;
-    a.zl = sl.ML;
-    a.d = sl.d;
-    a.L = sl.L;
-    a.aux = sl.aux;
-    a.pm = sl.pmask;
-    a.split = sl.split;
-    a.gobj_cnt = gobj;
-    a.gobj = reinterpret_cast<int2*>(sl.obj_bbox);
-    a.gobj_cap = max_objects;
+    a.ovf_list = sl.sc_huge;  // (S6's huge list is consumed by then: same stream)
     const size_t smw = kWarpsPB * sizeof(CompSm<kCapW, kKoW>);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_comp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
         attr = true;
     }
-    (note_launch(), k_comp_classify<<<grid_for(cap), 256, 0, s>>>(a, cnt, cap, sl.comp_bbox, sl.comp_big, nbig));
-    (note_launch(), k_comp_fused<<<148 * 4, kWarpsPB * 32, smw, s>>>(a, cnt, cap, sl.comp_root, sl.comp_bbox,
-                                                                     sl.comp_big, nbig, heads));
-    launch_edt(F, w, h, sl, nullptr, dist_scratch, s, ovf);  // no-op unless a component overflowed
-    (note_launch(), k_comp_global<<<148, kCT, 0, s>>>(a, sl.comp_root, sl.comp_bbox));
+    (note_launch(), k_comp_classify<<<grid_for(cap), 256, 0, s>>>(a, count5, cap, sl.sc_root, sl.sc_bbox,
+                                                                   sl.sc_big, nbig));
+    (note_launch(), k_comp_fused<<<148 * 4, kWarpsPB * 32, smw, s>>>(a, count5, cap, sl.sc_root, sl.sc_bbox,
+                                                                     sl.sc_big, nbig, heads));
+    (note_launch(), k_comp_huge<<<1, kHugeT, 0, s>>>(a, sl.sc_root, sl.sc_bbox, carve_big(sl)));
     if (table) {
-        (note_launch(), k_obj_feat_list<<<148 * 2, kFT, 0, s>>>(a, sl.comp_bbox));
         (note_launch(), k_rows_scatter<<<std::max(1, std::min(148 * 4, (max_objects + 255) / 256)), 256, 0, s>>>(
             rows, max_objects, sl.stg_label, sl.stg_flags, sl.stg_feat, table->label, table->flags, table->feat,
             table->capacity));
@@ -1147,7 +870,8 @@ void launch_fill_components(const uint8_t* big0, int w, int h, Slot& sl, const i
     if (n == 0) return;
     cudaMemsetAsync(F, 0, n, s);
     cudaMemsetAsync(enc, 0, n, s);
-    FillArgs a{big0, w, h, F, enc};
+    cudaMemsetAsync(sl.lab, 0xff, 4 * n, s);
+    FillArgs a{big0, w, h, F, enc, reinterpret_cast<unsigned*>(sl.lab)};
     const size_t smw = kWarpsPB * sizeof(CompSm<kCapW, kKoW>);
     static bool attr = false;
     if (!attr) {
