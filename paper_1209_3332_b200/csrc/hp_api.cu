@@ -168,6 +168,11 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
             rs = sl.hstream;
         }
         launch_recon_u8_auto(sl.g, sl.u8b, w, h, sl.wl, rs);
+#ifdef HP_WHATIF_S4X2  // experiment only: a second, independent S4 into scratch (marginal cost)
+        cudaMemcpyAsync(sl.pmask, sl.u8a, (size_t)w * h, cudaMemcpyDeviceToDevice, rs);
+        launch_open(sl.g, w, h, p.open_diam, sl.cand, sl.pmask, rs);
+        launch_recon_u8_auto(sl.g, sl.pmask, w, h, sl.wl, rs);
+#endif
         if (ctx->prio >= 1) {
             cudaEventRecord(sl.join_ev, sl.hstream);
             cudaStreamWaitEvent(s, sl.join_ev, 0);

@@ -36,6 +36,12 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HP_RG_ORDER
 #define HP_RG_ORDER 1  // initial job order: 0 raster, 1 four-colour (r1: 3018 -> 2165 jobs, 689 -> 725 tiles/s)
 #endif
+#ifndef HP_RG_PROFILE
+#define HP_RG_PROFILE 0  // timing breakdown in the stats (experiments)
+#endif
+#ifndef HP_RG_JACOBI
+#define HP_RG_JACOBI 0  // neighbour-exchange steps tried before the row scans
+#endif
 #ifndef HP_RG_EAGER
 #define HP_RG_EAGER 0  // eager in-region pushes of border changes (r1: 88.9 -> 106.6 ms owned, 727 -> 688 tiles/s: off)
 #endif
@@ -142,7 +148,7 @@ struct Smem {
     int pend;            // sub-tiles with dirty != 0 plus sub-tiles being processed
     int job;
     int again;
-    unsigned long long t0;
+    unsigned long long t0, tA, tB;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -211,7 +217,37 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
         int u[PPL];
 #pragma unroll
         for (int j = 0; j < PPL; ++j) u[j] = lo[j];
-        if (__any_sync(FULL, need)) {
+        bool scan = __any_sync(FULL, need);
+#if HP_RG_JACOBI > 0
+        // short propagation first: up to HP_RG_JACOBI neighbour-exchange steps (each lane
+        // relaxes its pixels from both row neighbours); stop at the fixed point, else close the
+        // row with the scans from the partially propagated values (same closure)
+        for (int it = 0; scan && it < HP_RG_JACOBI; ++it) {
+            int left = __shfl_up_sync(FULL, u[PPL - 1], 1), right = __shfl_down_sync(FULL, u[0], 1);
+            if (lane == 0) left = 0;
+            if (lane == 31) right = 0;
+            bool ch = false;
+#pragma unroll
+            for (int j = 0; j < PPL; ++j) {
+                const int nb = max(j == 0 ? left : u[j - 1], j == PPL - 1 ? right : u[j + 1]);
+                const int nv = min(m[j], max(u[j], nb));
+                ch |= nv != u[j];
+                u[j] = nv;
+            }
+#pragma unroll
+            for (int j = PPL - 2; j >= 0; --j) {
+                const int nv = min(m[j], max(u[j], u[j + 1]));
+                ch |= nv != u[j];
+                u[j] = nv;
+            }
+            scan = __any_sync(FULL, ch);
+        }
+        if (scan) {
+#pragma unroll
+            for (int j = 0; j < PPL; ++j) lo[j] = u[j];
+        }
+#endif
+        if (scan) {
             // left -> right: the lane's clamp is pixel PPL-1 o ... o pixel 0
             int FL = lo[0], FH = m[0];
 #pragma unroll
@@ -361,6 +397,9 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                     int np = 0;
                     for (int k = 0; k < NW; ++k) np += S.dirty[k] != 0;
                     S.pend = np;
+#if HP_RG_PROFILE
+                    S.tA = gtimer();
+#endif
                 }
                 __syncthreads();
                 // Asynchronous sub-tile warps: a warp takes its own dirty rows, sweeps them to a
@@ -486,8 +525,15 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                     }
                 }
                 __syncthreads();
+#if HP_RG_PROFILE  // ctr[4] = ns in the sub-tile loop, ctr[6] = ns in write-back + activation
+                if (threadIdx.x == 0) {
+                    S.tB = gtimer();
+                    atomicAdd(&wl.ctr[4], S.tB - S.tA);
+                }
+#else
                 if (lane == 0) atomicAdd(&wl.ctr[4], (unsigned long long)iters);  // sub-tile sweep sets
                 if (lane == 0) atomicAdd(&wl.ctr[6], (unsigned long long)nrows);
+#endif
                 // write back the changed rows of this sub-tile (interior words)
                 if (mychg) {
                     constexpr int WPR = SW / 4;  // words per sub-tile row
@@ -559,6 +605,9 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
             }
             __syncthreads();
             if (threadIdx.x == 0) {
+#if HP_RG_PROFILE
+                if (any_in) atomicAdd(&wl.ctr[6], gtimer() - S.tB);
+#endif
                 int again = 0;
                 uint32_t o = atomicCAS(&wl.state[t], ST_BUSY, ST_IDLE);
                 if (o == ST_BUSY) {
