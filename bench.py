@@ -186,6 +186,7 @@ def main():
     ap.add_argument("--impl", default="hp", choices=["hp", "reference"])
     ap.add_argument("--batch", type=int, default=12, help="distinct 4K tiles per GPU per step")
     ap.add_argument("--slots", type=int, default=6, help="tiles in flight per GPU (n_slots)")
+    ap.add_argument("--e2e-slots", type=int, default=14, help="context slots used by hp_run_tiles (e2e)")
     ap.add_argument("--size", type=int, default=4096)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -197,7 +198,7 @@ def main():
     workload = (f"configs[1] tile shape: {args.size}x{args.size} synthetic H&E RGB tiles, "
                 f"segmentation+features; {args.batch} distinct tiles per GPU per step")
     config = {"workload": workload, "tile": f"{args.size}x{args.size}x3 u8",
-              "batch_per_gpu": args.batch, "slots": args.slots,
+              "batch_per_gpu": args.batch, "slots": args.slots, "e2e_slots": max(args.slots, args.e2e_slots),
               "l2": "inputs larger than L2 (each step reads %d distinct tiles = %.0f MB)"
                     % (args.batch, args.batch * 3 * args.size * args.size / 1e6),
               "parallelism": f"tiles sharded over {world} GPU(s), no data-path collective"}
@@ -242,7 +243,9 @@ def main():
     tiles = make_tiles(rank, B, size)
     log(f"[rank {rank}] generated {B} tiles in {time.time() - t_gen:.1f}s")
     cap = 8192
-    ctx = Context(local, size, size, n_slots=S, max_objects=cap)
+    # the device-resident step uses S slots; hp_run_tiles (e2e) uses every slot of the context:
+    # more tiles in flight hide each slot's own H2D behind the others' compute
+    ctx = Context(local, size, size, n_slots=max(S, args.e2e_slots), max_objects=cap)
     dev = [torch.from_numpy(t).cuda() for t in tiles]
     lab = [torch.empty((size, size), dtype=torch.int32, device="cuda") for _ in range(S)]
     nob = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(S)]

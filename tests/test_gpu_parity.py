@@ -284,6 +284,31 @@ def test_pipeline_huge_windows(ctx):
     _check_pipeline(ctx, rgb)
 
 
+def _island_tile():
+    """Candidates inside other candidates' holes: a ring with a separate dot inside, and two
+    nested rings around a dot (islands must be solved with their enclosing component)."""
+    rgb = make_tile(12, TileSpec(512, 512, density=2e-5))["rgb"].copy()
+    yy, xx = np.mgrid[0:512, 0:512]
+    paint = np.zeros((512, 512), bool)
+    r1 = np.hypot(xx - 120, yy - 140)
+    paint |= (np.abs(r1 - 13) < 1.0) | (r1 < 3.2)                       # ring + dot
+    r2 = np.hypot(xx - 330, yy - 300)
+    paint |= (np.abs(r2 - 22) < 1.0) | (np.abs(r2 - 11) < 1.0) | (r2 < 3.2)  # nested rings + dot
+    rgb[paint] = (70, 30, 110)
+    return rgb
+
+
+def test_pipeline_islands(ctx):
+    rgb = _island_tile()
+    g, fl, _ = oracle.cd(rgb)
+    big0 = oracle.area_threshold(oracle.recon_to_nuclei(g, oracle.open_(g), oracle.rbc(fl)))
+    _, n_in = oracle.ccl(big0[100:180, 80:160])
+    assert n_in >= 2                                   # ring and dot are separate candidates
+    F = oracle.fill_holes(big0)
+    assert F[135:145, 115:125].all()                   # ... merged into one F component
+    _check_pipeline(ctx, rgb)
+
+
 def test_pipeline_edge_cases(ctx):
     _check_pipeline(ctx, np.full((64, 80, 3), 255, U8))          # glass only
     _check_pipeline(ctx, np.zeros((50, 70, 3), U8))               # black
