@@ -309,6 +309,16 @@ def test_pipeline_islands(ctx):
     _check_pipeline(ctx, rgb)
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_pipeline_random_small(ctx, seed):
+    """Small tiles of varied size, nucleus density and tissue fraction (ragged tile grids,
+    components touching tile borders, touching / overlapping nuclei, vesicular nuclei)."""
+    rng = np.random.default_rng(500 + seed)
+    h, w = int(rng.integers(96, 400)), int(rng.integers(96, 400))
+    spec = TileSpec(w, h, tissue_frac=float(rng.uniform(0.3, 1.0)), density=float(rng.uniform(0.5e-4, 4e-4)))
+    _check_pipeline(ctx, make_tile(600 + seed, spec)["rgb"])
+
+
 def test_pipeline_edge_cases(ctx):
     _check_pipeline(ctx, np.full((64, 80, 3), 255, U8))          # glass only
     _check_pipeline(ctx, np.zeros((50, 70, 3), U8))               # black
