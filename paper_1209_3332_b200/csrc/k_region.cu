@@ -145,6 +145,7 @@ struct Smem {
     uint32_t R[ROWS * RWW];
     uint32_t M[ROWS * RWW];
     uint32_t dirty[NW];  // rows of each sub-tile that may still improve (pushed by neighbours)
+    uint32_t first_mask[NW];  // (HP_RG_PROFILE == 2) the incoming masks of the job
     int pend;            // sub-tiles with dirty != 0 plus sub-tiles being processed
     int job;
     int again;
@@ -400,6 +401,9 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
 #if HP_RG_PROFILE
                     S.tA = gtimer();
 #endif
+#if HP_RG_PROFILE == 2
+                    for (int k = 0; k < NW; ++k) S.first_mask[k] = S.dirty[k];
+#endif
                 }
                 __syncthreads();
                 // Asynchronous sub-tile warps: a warp takes its own dirty rows, sweeps them to a
@@ -525,7 +529,14 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                     }
                 }
                 __syncthreads();
-#if HP_RG_PROFILE  // ctr[4] = ns in the sub-tile loop, ctr[6] = ns in write-back + activation
+#if HP_RG_PROFILE == 2  // ctr[4] = loop ns of first jobs (all rows dirty), ctr[6] = of the rest
+                if (threadIdx.x == 0) {
+                    S.tB = gtimer();
+                    bool first = true;
+                    for (int k = 0; k < NW; ++k) first &= S.first_mask[k] == 0xffffffffu;
+                    atomicAdd(&wl.ctr[first ? 4 : 6], S.tB - S.tA);
+                }
+#elif HP_RG_PROFILE  // ctr[4] = ns in the sub-tile loop, ctr[6] = ns in write-back + activation
                 if (threadIdx.x == 0) {
                     S.tB = gtimer();
                     atomicAdd(&wl.ctr[4], S.tB - S.tA);
@@ -605,7 +616,7 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
             }
             __syncthreads();
             if (threadIdx.x == 0) {
-#if HP_RG_PROFILE
+#if HP_RG_PROFILE == 1
                 if (any_in) atomicAdd(&wl.ctr[6], gtimer() - S.tB);
 #endif
                 int again = 0;
