@@ -43,7 +43,8 @@ struct hp_ctx {
     std::vector<void*> host_blocks;
     int rows_copied = 0;  // rows copied back per tile in hp_run_tiles
     bool global_s8s10 = false;
-    int prio = 0;  // env HP_PRIO: 1 = S4 on a high-priority stream, 2 = S4 and S7-S11  // env HP_GLOBAL_S8S10=1: the per-stage global path in the pipeline
+    int prio = 0;  // env HP_PRIO: 1 = S4 on a high-priority stream, 2 = S4 and S7-S11
+    bool graphs = true;  // env HP_GRAPHS=0: hp_run_tiles launches every op instead of a graph  // env HP_GLOBAL_S8S10=1: the per-stage global path in the pipeline
     // stage-timing ring: per slot, kRing sets of 12 events (one set per tile)
     std::vector<std::vector<std::array<cudaEvent_t, 12>>> ring;
     std::vector<int> ring_pos, ring_n;
@@ -314,6 +315,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
     ctx->rows_copied = std::min(cfg->max_objects, kRowsAsync);
     if (const char* e = getenv("HP_GLOBAL_S8S10")) ctx->global_s8s10 = atoi(e) == 1;
     if (const char* e = getenv("HP_PRIO")) ctx->prio = atoi(e);
+    if (const char* e = getenv("HP_GRAPHS")) ctx->graphs = atoi(e) != 0;
     auto dalloc = [&](size_t bytes) -> void* {
         void* p = nullptr;
         if (cudaMalloc(&p, bytes ? bytes : 16) != cudaSuccess) return nullptr;
@@ -424,6 +426,7 @@ hp_status hp_ctx_destroy(hp_ctx* ctx) {
         if (s.hstream) cudaStreamDestroy(s.hstream);
         if (s.done_ev) cudaEventDestroy(s.done_ev);
         if (s.fork_ev) cudaEventDestroy(s.fork_ev);
+        if (s.gexec) cudaGraphExecDestroy(s.gexec);
         if (s.join_ev) cudaEventDestroy(s.join_ev);
     }
     for (auto& r : ctx->ring)
@@ -684,14 +687,47 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
         cudaMemcpy2DAsync(sl.rgb_dev, 3 * (size_t)w, host, (size_t)pitch, 3 * (size_t)w, h, cudaMemcpyHostToDevice, s);
         hp_image im{sl.rgb_dev, w, h, 3LL * w};
         hp_feature_table tab{sl.tab_label, sl.tab_flags, sl.tab_feat, mo, sl.tab_nrows};
-        bool fused = false;
-        hp_status r = segment(ctx, sl, &im, sl.lab_dev, w, sl.cnt32 + 4, s, &tab, &fused);
-        if (!r && !fused) r = features(ctx, sl, w, h, sl.lab_dev, w, &tab, s);
-        if (r) return r;
-        cudaMemcpyAsync(sl.h_nrows, sl.tab_nrows, 4, cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(sl.h_label, sl.tab_label, 4 * (size_t)ctx->rows_copied, cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(sl.h_flags, sl.tab_flags, 4 * (size_t)ctx->rows_copied, cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(sl.h_feat, sl.tab_feat, 4 * (size_t)ctx->rows_copied * HP_NFEAT, cudaMemcpyDeviceToHost, s);
+        // the tile's chain: segmentation + features on the slot's own buffers, rows D2H
+        auto chain = [&]() -> hp_status {
+            bool fused = false;
+            hp_status r = segment(ctx, sl, &im, sl.lab_dev, w, sl.cnt32 + 4, s, &tab, &fused);
+            if (!r && !fused) r = features(ctx, sl, w, h, sl.lab_dev, w, &tab, s);
+            if (r) return r;
+            cudaMemcpyAsync(sl.h_nrows, sl.tab_nrows, 4, cudaMemcpyDeviceToHost, s);
+            cudaMemcpyAsync(sl.h_label, sl.tab_label, 4 * (size_t)ctx->rows_copied, cudaMemcpyDeviceToHost, s);
+            cudaMemcpyAsync(sl.h_flags, sl.tab_flags, 4 * (size_t)ctx->rows_copied, cudaMemcpyDeviceToHost, s);
+            cudaMemcpyAsync(sl.h_feat, sl.tab_feat, 4 * (size_t)ctx->rows_copied * HP_NFEAT, cudaMemcpyDeviceToHost, s);
+            return HP_OK;
+        };
+        // CUDA graph: the slot's first tile of a size runs op by op (one-time
+        // setup), the second is captured, every later tile replays the graph -- one launch
+        // instead of ~30 API calls.  Not with stage timing or the host-synchronising
+        // background skip, whose host decisions a graph cannot replay.
+        const bool graphable = ctx->graphs && !ctx->timing && ctx->cfg.params.bg_skip_frac > 1.0f &&
+                               ctx->prio == 0;
+        hp_status r = HP_OK;
+        if (graphable && sl.gexec && sl.graph_w == w && sl.graph_h == h) {
+            if (cudaGraphLaunch(sl.gexec, s) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "graph launch");
+        } else if (graphable && sl.graph_w == w && sl.graph_h == h) {
+            cudaGraph_t g = nullptr;
+            if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+                return cuda_fail(ctx, cudaGetLastError(), "begin capture");
+            r = chain();
+            const cudaError_t ce = cudaStreamEndCapture(s, &g);
+            if (r) return r;
+            if (ce != cudaSuccess || cudaGraphInstantiate(&sl.gexec, g, 0) != cudaSuccess)
+                return cuda_fail(ctx, cudaGetLastError(), "graph capture");
+            cudaGraphDestroy(g);
+            if (cudaGraphLaunch(sl.gexec, s) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "graph launch");
+        } else {
+            if ((r = chain())) return r;
+            if (sl.gexec) {
+                cudaGraphExecDestroy(sl.gexec);
+                sl.gexec = nullptr;
+            }
+            sl.graph_w = w;
+            sl.graph_h = h;
+        }
         cudaEventRecord(sl.done_ev, s);
         if ((r = check_launch(ctx, "run_tiles"))) return r;
         tile_of[i] = tid;

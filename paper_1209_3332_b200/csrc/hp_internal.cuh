@@ -105,6 +105,9 @@ struct Slot {
     int32_t *h_label, *h_flags, *h_nrows;
     float* h_feat;
     cudaEvent_t done_ev;
+    // hp_run_tiles: the per-tile chain (compute + D2H) captured once as a CUDA graph
+    cudaGraphExec_t gexec;
+    int graph_w, graph_h;
     // high-priority side stream for the latency-bound stages (hp_ctx::prio)
     cudaStream_t hstream;
     cudaEvent_t fork_ev, join_ev;

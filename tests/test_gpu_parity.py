@@ -347,6 +347,33 @@ def test_iwpp_stress(ctx, kind, ramp):
     assert np.array_equal(rec, mask)
 
 
+def test_run_tiles_size_change(ctx):
+    """hp_run_tiles replays a per-slot CUDA graph; a new tile size must rebuild it."""
+    import torch
+    for (h, w, base) in [(256, 384, 700), (320, 200, 710), (256, 384, 720)]:
+        tiles = [make_tile(base + i, TileSpec(h, w))["rgb"] for i in range(7)]
+        pinned = [torch.from_numpy(t).pin_memory() for t in tiles]
+        it = iter(range(len(tiles)))
+        got = {}
+
+        def nxt():
+            try:
+                i = next(it)
+            except StopIteration:
+                return None
+            return pinned[i].data_ptr(), 3 * w, i
+
+        def done(tid, lab, fl, ft, st):
+            assert st == 0
+            got[tid] = (lab, fl, ft)
+
+        ctx.run_tiles(nxt, done, w, h)
+        assert sorted(got) == list(range(len(tiles)))
+        for i, rgb in enumerate(tiles):
+            _, ol, of, ot = oracle.process_tile(rgb)
+            assert_features_equal(got[i][0], got[i][1], got[i][2], ol, of, ot)
+
+
 def test_run_tiles(ctx):
     import torch
     tiles = [make_tile(100 + i, TileSpec(512, 512))["rgb"] for i in range(5)]
