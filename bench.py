@@ -251,7 +251,7 @@ def main():
     nob = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(S)]
     tl = [torch.empty(cap, dtype=torch.int32, device="cuda") for _ in range(S)]
     tf = [torch.empty(cap, dtype=torch.int32, device="cuda") for _ in range(S)]
-    tt = [torch.empty((cap, 34), dtype=torch.float32, device="cuda") for _ in range(S)]
+    tt = [torch.empty((cap, 36), dtype=torch.float32, device="cuda") for _ in range(S)]
     nr = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(S)]
     streams = [torch.cuda.Stream() for _ in range(S)]
     main_s = torch.cuda.current_stream()
@@ -339,7 +339,7 @@ def main():
         from paper_1209_3332_b200.dist import DistTileSource, TileQueue, gather_rows, table_digest
         pinned = [torch.from_numpy(x).pin_memory() for x in tiles]
         rows_copied = min(cap, 4096)
-        d2h_per_tile = 4 + rows_copied * (4 + 4 + 34 * 4)
+        d2h_per_tile = 4 + rows_copied * (4 + 4 + 36 * 4)
 
         def run(ntiles, key):
             q = TileQueue(ntiles, block=S, key=key)

@@ -65,7 +65,8 @@ enum {
     HP_F_GRAD_MEAN, HP_F_GRAD_STD, HP_F_GRAD_SKEW, HP_F_GRAD_KURT,          /* gradient: 4 */
     HP_F_GLCM_ASM, HP_F_GLCM_CONTRAST, HP_F_GLCM_CORRELATION, HP_F_GLCM_HOMOGENEITY,
     HP_F_GLCM_ENTROPY, HP_F_GLCM_SHADE, HP_F_GLCM_PROMINENCE, HP_F_GLCM_MAXPROB, /* Haralick: 8 */
-    HP_NFEAT = 34
+    HP_F_EDGE_COUNT, HP_F_EDGE_FRAC,                                       /* edge (Canny): 2 */
+    HP_NFEAT = 36
 };
 
 /* Every constant of the method (readings C3-C12 of DESIGN.md; defaults from
@@ -85,6 +86,9 @@ typedef struct hp_params {
     float   h;              /* h-maxima height on the distance map, > 0 (default 1.0) */
     int32_t obj_min_area, obj_max_area;    /* S10 inclusive area bounds (21, 1000) */
     int32_t glcm_levels;    /* must be 8 (q = g >> 5) */
+    int32_t canny_low, canny_high;  /* Canny hysteresis thresholds on the L1 3x3-Sobel magnitude
+                                       of g, 0 <= low <= high (defaults 100, 200; PAPER.md:604,
+                                       639 "OpenCV(Canny)"; reading C22) */
 } hp_params;
 
 typedef struct hp_config {
@@ -174,19 +178,20 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
  *                                                  out3 L i32 (c, d, L: 0 outside F)
  *  BWLABEL   in0 split u8                       -> out0 labels i32, out1 n_objects i32[1]
  *  FEATURES  in0 labels i32, in1 g u8           -> out0 label i32[cap], out1 flags i32[cap],
- *                                                  out2 feat f32[cap][34], out3 n_rows i32[1]
+ *                                                  out2 feat f32[cap][36], out3 n_rows i32[1]
  *                                                  (cap = max_objects)
  *  IWPP_RAW  in0 marker u8, in1 mask u8         -> out0 recon u8, out1 stats i64[4]
  *                                                  (jobs, sweep iterations, ns regions were
  *                                                  owned, row closures attempted)
  *  CCL8/CCL4 in0 fg u8                          -> out0 labels i32 (1 + min index, 0 = bg)
  *  RECON_F32 in0 marker f32, in1 mask f32, in2 domain u8 (may be NULL) -> out0 recon f32
+ *  CANNY     in0 g u8                           -> out0 edges u8 (0/1): cv2.Canny(g, low, high)
  */
 typedef enum {
     HP_STAGE_CD = 0, HP_STAGE_RBC, HP_STAGE_OPEN, HP_STAGE_RECON, HP_STAGE_AREA,
     HP_STAGE_FILL, HP_STAGE_EDT, HP_STAGE_MARKERS, HP_STAGE_WATERSHED, HP_STAGE_BWLABEL,
     HP_STAGE_FEATURES, HP_STAGE_IWPP_RAW, HP_STAGE_CCL8, HP_STAGE_CCL4, HP_STAGE_RECON_F32,
-    HP_STAGE_COUNT
+    HP_STAGE_CANNY, HP_STAGE_COUNT
 } hp_stage;
 typedef struct hp_stage_io {
     const void* in[4];

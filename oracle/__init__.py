@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.cpp")
 
-NFEAT = 34
+NFEAT = 36
 FLAG_RBC_HI, FLAG_RBC_LO, FLAG_R_GT_B, FLAG_BG = 1, 2, 4, 8
 OBJ_TOUCHES_BORDER = 1
 
@@ -39,7 +39,8 @@ class Params(C.Structure):
                 ("bg_skip_frac", C.c_float), ("rbc_t1", C.c_int32), ("rbc_t2", C.c_int32),
                 ("open_diam", C.c_int32), ("g1", C.c_int32), ("cand_min_area", C.c_int32),
                 ("cand_max_area", C.c_int32), ("h", C.c_float), ("obj_min_area", C.c_int32),
-                ("obj_max_area", C.c_int32), ("glcm_levels", C.c_int32)]
+                ("obj_max_area", C.c_int32), ("glcm_levels", C.c_int32), ("canny_low", C.c_int32),
+                ("canny_high", C.c_int32)]
 
     def to_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "q"}
@@ -252,7 +253,16 @@ def bwlabel(split, amin=21, amax=1000):
     return lab, int(n[0])
 
 
-def features(labels, g, cap=None):
+def canny(g, low=100, high=200):
+    """Feature-stage Canny edges (0/1) of g: cv2.Canny(g, low, high) written out (C22)."""
+    g = _u8(g)
+    h, w = g.shape
+    out = np.empty((h, w), np.uint8)
+    _chk(lib().or_canny(_p(g), w, h, int(low), int(high), _p(out)), "or_canny")
+    return out
+
+
+def features(labels, g, cap=None, canny_low=100, canny_high=200):
     labels = np.ascontiguousarray(labels, np.int32)
     g = _u8(g)
     h, w = g.shape
@@ -262,8 +272,8 @@ def features(labels, g, cap=None):
     rf = np.zeros(cap, np.int32)
     ft = np.zeros((cap, NFEAT), np.float32)
     n = np.zeros(1, np.int32)
-    _chk(lib().or_features(_p(labels), _p(g), w, h, 8, cap, _p(rl), _p(rf), _p(ft), _p(n)),
-         "or_features")
+    _chk(lib().or_features(_p(labels), _p(g), w, h, 8, int(canny_low), int(canny_high), cap, _p(rl), _p(rf),
+                           _p(ft), _p(n)), "or_features")
     k = int(n[0])
     return rl[:k], rf[:k], ft[:k]
 

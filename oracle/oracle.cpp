@@ -208,6 +208,8 @@ void or_default_params(or_params* p) {
     p->obj_min_area = 21;
     p->obj_max_area = 1000;
     p->glcm_levels = 8;
+    p->canny_low = 100;   // reading C22
+    p->canny_high = 200;
 }
 
 // S1 -- colour deconvolution + pixel thresholds used by RBC detection
@@ -623,13 +625,88 @@ int or_bwlabel(const uint8_t* split, int w, int h, int amin, int amax, int32_t* 
     return 0;
 }
 
-// S11 -- Features comp. (reading C16, C17).
+// Feature-stage Canny ("OpenCV(Canny)"; reading C22): cv2.Canny(g, low,
+// high) with aperture 3 and the L1 gradient norm, written out step by step:
+//   dx, dy = 3x3 Sobel of g with replicated borders; m = |dx| + |dy|;
+//   non-maximum suppression along the gradient direction, the sector chosen with
+//   tan(22.5 deg) in 15-bit fixed point (TG22 = 13573), out-of-tile magnitudes 0:
+//     horizontal  m > m(x-1, y) and m >= m(x+1, y)
+//     vertical    m > m(x, y-1) and m >= m(x, y+1)
+//     diagonal    s = sign(dx * dy): m > m(x-s, y-1) and m > m(x+s, y+1);
+//   candidates = local maxima with m > low; edges = the 8-connected components of the
+//   candidates that contain a candidate with m > high (hysteresis, BFS).
+int or_canny(const uint8_t* g, int w, int h, int low, int high, uint8_t* edges) {
+    if (!g || !edges || w < 0 || h < 0) return 1;
+    const int64_t n = (int64_t)w * h;
+    std::vector<int32_t> dx(n), dy(n), mag(n);
+    auto G = [&](int x, int y) {
+        x = std::min(std::max(x, 0), w - 1);
+        y = std::min(std::max(y, 0), h - 1);
+        return (int32_t)g[(int64_t)y * w + x];
+    };
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            const int64_t p = (int64_t)y * w + x;
+            dx[p] = (G(x + 1, y - 1) + 2 * G(x + 1, y) + G(x + 1, y + 1)) -
+                    (G(x - 1, y - 1) + 2 * G(x - 1, y) + G(x - 1, y + 1));
+            dy[p] = (G(x - 1, y + 1) + 2 * G(x, y + 1) + G(x + 1, y + 1)) -
+                    (G(x - 1, y - 1) + 2 * G(x, y - 1) + G(x + 1, y - 1));
+            mag[p] = std::abs(dx[p]) + std::abs(dy[p]);
+        }
+    auto M = [&](int x, int y) -> int32_t { return inb(x, y, w, h) ? mag[(int64_t)y * w + x] : 0; };
+    const int64_t TG22 = 13573;  // (int)(tan(22.5 deg) * 2^15 + 0.5)
+    std::vector<uint8_t> cand(n, 0);
+    std::deque<int64_t> fifo;
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x) {
+            const int64_t p = (int64_t)y * w + x;
+            const int32_t m = mag[p];
+            if (m <= low) continue;
+            const int64_t ax = std::abs(dx[p]), ay = (int64_t)std::abs(dy[p]) << 15;
+            const int64_t tg22x = ax * TG22, tg67x = tg22x + (ax << 16);
+            bool lm;
+            if (ay < tg22x) {
+                lm = m > M(x - 1, y) && m >= M(x + 1, y);
+            } else if (ay > tg67x) {
+                lm = m > M(x, y - 1) && m >= M(x, y + 1);
+            } else {
+                const int s = ((dx[p] ^ dy[p]) < 0) ? -1 : 1;
+                lm = m > M(x - s, y - 1) && m > M(x + s, y + 1);
+            }
+            if (!lm) continue;
+            cand[p] = 1;
+            if (m > high) fifo.push_back(p);
+        }
+    std::memset(edges, 0, (size_t)n);
+    for (int64_t p : fifo) edges[p] = 1;
+    while (!fifo.empty()) {
+        const int64_t p = fifo.front();
+        fifo.pop_front();
+        const int x = (int)(p % w), y = (int)(p / w);
+        for (int j = 0; j < 8; ++j) {
+            const int qx = x + DX8[j], qy = y + DY8[j];
+            if (!inb(qx, qy, w, h)) continue;
+            const int64_t q = (int64_t)qy * w + qx;
+            if (cand[q] && !edges[q]) {
+                edges[q] = 1;
+                fifo.push_back(q);
+            }
+        }
+    }
+    return 0;
+}
+
+// S11 -- Features comp. (reading C16, C17, C22).
 // Feature order: see DESIGN.md "Feature table".
 int or_features(const int32_t* labels, const uint8_t* g, int w, int h, int glcm_levels,
-                int32_t cap, int32_t* row_label, int32_t* row_flags, float* feat,
-                int32_t* n_rows) {
-    if (!labels || !g || w < 0 || h < 0 || glcm_levels != 8 || cap < 0) return 1;
+                int canny_low, int canny_high, int32_t cap, int32_t* row_label,
+                int32_t* row_flags, float* feat, int32_t* n_rows) {
+    if (!labels || !g || w < 0 || h < 0 || glcm_levels != 8 || cap < 0 || canny_low < 0 ||
+        canny_high < canny_low)
+        return 1;
     const int64_t n = (int64_t)w * h;
+    std::vector<uint8_t> edges(n);
+    or_canny(g, w, h, canny_low, canny_high, edges.data());
     std::map<int32_t, std::vector<int64_t>> objs;  // ascending label order
     for (int64_t p = 0; p < n; ++p)
         if (labels[p] > 0) objs[labels[p]].push_back(p);
@@ -824,6 +901,11 @@ int or_features(const int32_t* labels, const uint8_t* g, int w, int h, int glcm_
             out[32] = prom;
             out[33] = pmax;
         }
+        // ---- edge (2): Canny edge pixels of the object, and their fraction of its area
+        int64_t ne = 0;
+        for (int64_t p : P) ne += edges[p];
+        out[34] = (double)ne;
+        out[35] = (double)ne / Ad;
         if (row_label) row_label[row] = lab;
         if (row_flags) row_flags[row] = border ? OR_OBJ_TOUCHES_BORDER : 0;
         if (feat)
@@ -899,7 +981,8 @@ int or_process_tile(const uint8_t* rgb, int w, int h, int64_t pitch, const or_pa
     std::vector<uint8_t> g(n), flags(n);
     auto a = clk::now();
     or_cd(rgb, w, h, pitch, p, g.data(), flags.data(), nullptr);
-    rc = or_features(labels, g.data(), w, h, p->glcm_levels, cap, row_label, row_flags, feat, n_rows);
+    rc = or_features(labels, g.data(), w, h, p->glcm_levels, p->canny_low, p->canny_high, cap, row_label,
+                     row_flags, feat, n_rows);
     auto b = clk::now();
     if (t) t[10] = secs(a, b);
     return rc;

@@ -32,11 +32,12 @@ typedef struct or_params {
     float   h;              /* h-maxima height on the distance map */
     int32_t obj_min_area, obj_max_area;
     int32_t glcm_levels;    /* 8 */
+    int32_t canny_low, canny_high;  /* Canny hysteresis thresholds on the L1 Sobel magnitude */
 } or_params;
 
 enum { OR_FLAG_RBC_HI = 1, OR_FLAG_RBC_LO = 2, OR_FLAG_R_GT_B = 4, OR_FLAG_BG = 8 };
 enum { OR_OBJ_TOUCHES_BORDER = 1 };
-enum { OR_NFEAT = 34 };
+enum { OR_NFEAT = 36 };
 
 /* Defaults; q is computed here in double from the Ruifrok-Johnston H&E vectors. */
 void or_default_params(or_params* p);
@@ -82,11 +83,13 @@ int or_watershed(const float* dist, const int32_t* ML, const uint8_t* F, int w, 
 /* S10: CCL8 of split, area filter, labels = 1 + min index, else 0. */
 int or_bwlabel(const uint8_t* split, int w, int h, int amin, int amax,
                int32_t* labels, int32_t* n_objects);
+/* Feature-stage Canny: cv2.Canny(g, low, high) (aperture 3, L1 norm); edges 0/1. */
+int or_canny(const uint8_t* g, int w, int h, int low, int high, uint8_t* edges);
 /* S11: one row per object in ascending label order: label, flags, feat[OR_NFEAT].
  * Returns 4 if more than cap objects (n_rows still written). */
 int or_features(const int32_t* labels, const uint8_t* g, int w, int h, int glcm_levels,
-                int32_t cap, int32_t* row_label, int32_t* row_flags, float* feat,
-                int32_t* n_rows);
+                int canny_low, int canny_high, int32_t cap, int32_t* row_label,
+                int32_t* row_flags, float* feat, int32_t* n_rows);
 /* S1..S10 composed; optional per-stage seconds (11 doubles, S1..S11 order) in t_stage. */
 int or_segment_tile(const uint8_t* rgb, int w, int h, int64_t pitch, const or_params* p,
                     int32_t* labels, int32_t* n_objects, double* t_stage);

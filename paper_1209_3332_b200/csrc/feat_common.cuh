@@ -115,11 +115,12 @@ struct FeatSmem {
 
 // Every thread of the team calls this for one object P = {(x, y) : inP(x, y)} inside the
 // search box [bx0, bx1] x [by0, by1]; g is the tile's u8 plane (w x h, REFLECT_101 Sobel).
-// Team rank 0 receives the 34 features in f and the border flag.
+// Team rank 0 receives the 36 features in f and the border flag.  edge: the tile's Canny
+// edge plane (0/1, reading C22).
 template <class Team, class InP>
-__device__ void object_features(const Team& team, InP inP, const uint8_t* __restrict__ g, int w, int h,
-                                int bx0, int by0, int bx1, int by1, FeatSmem& fs, TeamRed& red, double* f,
-                                int* border_out) {
+__device__ void object_features(const Team& team, InP inP, const uint8_t* __restrict__ g,
+                                const uint8_t* __restrict__ edge, int w, int h, int bx0, int by0, int bx1,
+                                int by1, FeatSmem& fs, TeamRed& red, double* f, int* border_out) {
     unsigned int* hist = fs.hist;
     unsigned int* glcm = fs.glcm;
     const int tr = team.rank();
@@ -150,7 +151,7 @@ __device__ void object_features(const Team& team, InP inP, const uint8_t* __rest
             int gy = (t[6] + 2 * t[7] + t[8]) - (t[0] + 2 * t[1] + t[2]);
             return __fsqrt_rn((float)(gx * gx + gy * gy));
         };
-        long long A = 0, sx = 0, sy = 0, sxx = 0, syy = 0, sxy = 0, per = 0;
+        long long A = 0, sx = 0, sy = 0, sxx = 0, syy = 0, sxy = 0, per = 0, ne = 0;
         int border = 0;
         double gs = 0.0;
         float gmin = INFINITY, gmax = -INFINITY;
@@ -170,6 +171,7 @@ __device__ void object_features(const Team& team, InP inP, const uint8_t* __rest
             if (x == 0 || y == 0 || x == w - 1 || y == h - 1) border = 1;
             if (!inP(x - 1, y) || !inP(x + 1, y) || !inP(x, y - 1) || !inP(x, y + 1)) ++per;
             int gv = g[(int64_t)y * w + x];
+            ne += edge[(int64_t)y * w + x];
             atomicAdd(&hist[gv], 1u);
             const int OX[4] = {1, 1, 0, -1}, OY[4] = {0, 1, 1, 1};
 #pragma unroll
@@ -192,6 +194,7 @@ __device__ void object_features(const Team& team, InP inP, const uint8_t* __rest
         syy = team.reduce(syy, red.l, OpAdd());
         sxy = team.reduce(sxy, red.l, OpAdd());
         per = team.reduce(per, red.l, OpAdd());
+        ne = team.reduce(ne, red.l, OpAdd());
         border = team.reduce(border, red.i, OpAdd());
         oxmin = team.reduce(oxmin, red.i, OpMin());
         oymin = team.reduce(oymin, red.i, OpMin());
@@ -369,6 +372,9 @@ __device__ void object_features(const Team& team, InP inP, const uint8_t* __rest
                 f[HP_F_GLCM_PROMINENCE] = prom;
                 f[HP_F_GLCM_MAXPROB] = pmax;
             }
+            // edge (Canny): edge pixels of the object and their fraction of its area
+            f[HP_F_EDGE_COUNT] = (double)ne;
+            f[HP_F_EDGE_FRAC] = (double)ne / Ad;
             *border_out = border;
         }
         team.sync();

@@ -92,6 +92,7 @@ bool params_ok(const hp_params& p, std::string* why) {
     if (p.obj_min_area < 0 || p.obj_min_area > p.obj_max_area) return bad("obj area bounds");
     if (!(p.h > 0.0f) || !std::isfinite(p.h)) return bad("h must be finite and > 0");
     if (p.glcm_levels != 8) return bad("glcm_levels must be 8");
+    if (p.canny_low < 0 || p.canny_high < p.canny_low) return bad("need 0 <= canny_low <= canny_high");
     return true;
 }
 
@@ -205,8 +206,10 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
             cudaStreamWaitEvent(sl.hstream, sl.fork_ev, 0);
             cs = sl.hstream;
         }
-        launch_components(ncomp5, sl.split, sl.g, p.h, p.obj_min_area, p.obj_max_area, w, h, sl, labels, lpitch,
-                          n_objects, table, ctx->cfg.max_objects, cs);
+        // the feature stage's Canny, only when features are produced
+        if (table) launch_canny(sl.g, w, h, p.canny_low, p.canny_high, sl, sl.cand, cs);
+        launch_components(ncomp5, sl.split, sl.g, sl.cand, p.h, p.obj_min_area, p.obj_max_area, w, h, sl, labels,
+                          lpitch, n_objects, table, ctx->cfg.max_objects, cs);
         if (ctx->prio >= 2) {
             cudaEventRecord(sl.join_ev, sl.hstream);
             cudaStreamWaitEvent(s, sl.join_ev, 0);
@@ -224,8 +227,10 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
 
 hp_status features(hp_ctx* ctx, Slot& sl, int w, int h, const int32_t* labels, int64_t lpitch,
                    hp_feature_table* out, cudaStream_t s) {
-    launch_features(labels, lpitch, sl.g, w, h, sl, ctx->cfg.max_objects, out->label, out->flags,
-                    out->feat, out->capacity, out->n_rows_dev, s);                                   // S11
+    const hp_params& p = ctx->cfg.params;
+    launch_canny(sl.g, w, h, p.canny_low, p.canny_high, sl, sl.cand, s);                             // S11
+    launch_features(labels, lpitch, sl.g, sl.cand, w, h, sl, ctx->cfg.max_objects, out->label, out->flags,
+                    out->feat, out->capacity, out->n_rows_dev, s);
     ev(ctx, sl, 11, s);
     return check_launch(ctx, "features");
 }
@@ -277,6 +282,8 @@ void hp_default_params(hp_params* p) {
     p->obj_min_area = 21;
     p->obj_max_area = 1000;
     p->glcm_levels = 8;
+    p->canny_low = 100;  // reading C22
+    p->canny_high = 200;
 }
 
 const char* hp_status_str(hp_status st) {
@@ -603,10 +610,15 @@ hp_status hp_stage_run(hp_ctx* ctx, int32_t slot, hp_stage stage, const hp_stage
             return check_launch(ctx, "stage bwlabel");
         case HP_STAGE_FEATURES:
             if (!need({io->in[0], io->in[1], io->out[0], io->out[1], io->out[2], io->out[3]})) break;
-            launch_features((const int32_t*)io->in[0], w, in8(1), w, h, sl, ctx->cfg.max_objects,
+            launch_canny(in8(1), w, h, p.canny_low, p.canny_high, sl, sl.cand, s);
+            launch_features((const int32_t*)io->in[0], w, in8(1), sl.cand, w, h, sl, ctx->cfg.max_objects,
                             (int32_t*)io->out[0], (int32_t*)io->out[1], (float*)io->out[2], ctx->cfg.max_objects,
                             (int32_t*)io->out[3], s);
             return check_launch(ctx, "stage features");
+        case HP_STAGE_CANNY:
+            if (!need({io->in[0], io->out[0]})) break;
+            launch_canny(in8(0), w, h, p.canny_low, p.canny_high, sl, (uint8_t*)io->out[0], s);
+            return check_launch(ctx, "stage canny");
         case HP_STAGE_IWPP_RAW: {
             if (!need({io->in[0], io->in[1], io->out[0]})) break;
             launch_recon_init_u8(in8(0), in8(1), (uint8_t*)io->out[0], w, h, s);

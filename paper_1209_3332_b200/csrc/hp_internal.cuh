@@ -192,11 +192,13 @@ void launch_watershed(const float* dist, const int32_t* ML, const uint8_t* F, in
 void launch_bwlabel(const uint8_t* split, int w, int h, int amin, int amax, Slot& sl,
                     int32_t* labels, int64_t lpitch, int32_t* n_objects, cudaStream_t s);
 // S8-S10 fused per F component (k_comp.cu)
-void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t* g, float hh, int amin, int amax,
-                       int w, int h, Slot& sl, int32_t* labels, int64_t lpitch, int32_t* n_objects,
-                       const hp_feature_table* table, int32_t max_objects, cudaStream_t s);
+void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t* g, const uint8_t* edge, float hh,
+                       int amin, int amax, int w, int h, Slot& sl, int32_t* labels, int64_t lpitch,
+                       int32_t* n_objects, const hp_feature_table* table, int32_t max_objects, cudaStream_t s);
 // S11
-void launch_features(const int32_t* labels, int64_t lpitch, const uint8_t* g, int w, int h,
+// Feature-stage Canny (k_ccls.cu): edges 0/1 = cv2.Canny(g, low, high), reading C22
+void launch_canny(const uint8_t* g, int w, int h, int low, int high, Slot& sl, uint8_t* edges, cudaStream_t s);
+void launch_features(const int32_t* labels, int64_t lpitch, const uint8_t* g, const uint8_t* edge, int w, int h,
                      Slot& sl, int32_t max_objects, int32_t* row_label, int32_t* row_flags,
                      float* feat, int32_t capacity, int32_t* n_rows, cudaStream_t s);
 

@@ -32,7 +32,7 @@ constexpr int32_t kAreaMask = (1 << 29) - 1;
 constexpr int32_t kHit = 1 << 29, kTouch = 1 << 30;
 constexpr int kT = kTile;  // 32
 
-enum SelMode { SEL_AREA = 0, SEL_RBC = 1, SEL_FILL = 2, SEL_AREA_TH = 3 };
+enum SelMode { SEL_AREA = 0, SEL_RBC = 1, SEL_FILL = 2, SEL_AREA_TH = 3, SEL_EDGE = 4 };
 
 struct Sel {
     const uint8_t* plane;  // SEL_AREA: candidate mask; SEL_RBC: flags; SEL_FILL: big0; SEL_AREA_TH: g
@@ -44,6 +44,7 @@ struct Sel {
     // SEL_AREA_TH: per-root bounding boxes, written at root entries only (sparse planes)
     int32_t *bx0 = nullptr, *by0 = nullptr, *bx1 = nullptr, *by1 = nullptr;
     const int32_t* gate = nullptr;  // if set: every pass is a no-op unless *gate != 0
+    int32_t *P = nullptr, *X = nullptr;  // sparse root planes (default: the slot's lab / aux)
     // the pixel's byte: the plane, or for SEL_AREA_TH the top-hat candidate of S4 (PAPER.md:596,
     // reading C9): (g - recon > g1) & !rbc
     template <int MODE>
@@ -53,7 +54,7 @@ struct Sel {
     }
     template <int MODE>
     __device__ __forceinline__ bool fg(uint8_t v) const {
-        if (MODE == SEL_AREA || MODE == SEL_AREA_TH) return v != 0;
+        if (MODE == SEL_AREA || MODE == SEL_AREA_TH || MODE == SEL_EDGE) return v != 0;
         if (MODE == SEL_RBC) return (v & HP_FLAG_RBC_LO) != 0;
         return v == 0;  // SEL_FILL: background of big0
     }
@@ -61,6 +62,7 @@ struct Sel {
     template <int MODE>
     __device__ __forceinline__ bool bit(uint8_t v, int x, int y) const {
         if (MODE == SEL_RBC) return (v & (HP_FLAG_RBC_HI | HP_FLAG_RBC_LO)) == (HP_FLAG_RBC_HI | HP_FLAG_RBC_LO);
+        if (MODE == SEL_EDGE) return v == 2;  // a strong Canny candidate
         if (MODE == SEL_FILL) return x == 0 || y == 0 || x == w - 1 || y == h - 1;
         return false;
     }
@@ -71,12 +73,15 @@ struct Sel {
             return f && a >= amin && a <= amax;
         }
         if (MODE == SEL_RBC) return f && (prop & kHit) && (v & HP_FLAG_R_GT_B);
+        if (MODE == SEL_EDGE) return f && (prop & kHit);  // hysteresis
         return f ? !(prop & kTouch) : 1;  // SEL_FILL: big0 | enclosed background
     }
 };
 
 template <int MODE>
-__device__ __forceinline__ int32_t mode_bit() { return MODE == SEL_RBC ? kHit : (MODE == SEL_FILL ? kTouch : 0); }
+__device__ __forceinline__ int32_t mode_bit() {
+    return (MODE == SEL_RBC || MODE == SEL_EDGE) ? kHit : (MODE == SEL_FILL ? kTouch : 0);
+}
 
 __device__ __forceinline__ int find_l(const int* s, int x) {
     const volatile int* vs = s;
@@ -453,8 +458,8 @@ void run_select(Sel sel, int conn, Slot& sl, uint8_t* out, cudaStream_t s, const
     const int ntx = (w + kT - 1) / kT, nty = (h + kT - 1) / kT;
     const int ntiles = ntx * nty;
     dim3 grid(ntx, nty);
-    int32_t* P = sl.lab;
-    int32_t* X = sl.aux;
+    int32_t* P = sel.P ? sel.P : sl.lab;
+    int32_t* X = sel.X ? sel.X : sl.aux;
     (note_launch(), k_cs_local<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, sl.cs_edge, sl.cs_roots, sl.cs_nroots));
     (note_launch(), k_cs_merge<<<(int)(((int64_t)ntiles * 2 * kT + 255) / 256), 256, 0, s>>>(conn, ntx, nty,
                                                                                            sl.cs_edge, P, sel.gate));
@@ -465,7 +470,82 @@ void run_select(Sel sel, int conn, Slot& sl, uint8_t* out, cudaStream_t s, const
                                                                    lo->root, lo->bbox, lo->area, lo->count, lo->cap));
 }
 
+// ---------------------------------------------------------------- feature-stage Canny
+// cv2.Canny(g, low, high), aperture 3, L1 norm (reading C22): 3x3 Sobel
+// with replicated borders, m = |dx| + |dy|, non-maximum suppression in the gradient sector
+// (tan(22.5 deg) in 15-bit fixed point; out-of-tile magnitudes 0); map = 2 for local maxima
+// with m > high, 1 for other local maxima with m > low, else 0.  The hysteresis (8-connected
+// components of the candidates that hold a strong one) is the CCL-select SEL_EDGE.
+constexpr int kCW = 32, kCH = 32;  // output tile (256 threads, 4 rows each)
+__global__ void __launch_bounds__(256) k_canny_nms(const uint8_t* __restrict__ g, int w, int h, int low, int high,
+                                                   uint8_t* __restrict__ map) {
+    __shared__ uint8_t sg[kCH + 4][kCW + 4];  // g with a 2-px halo (replicated)
+    __shared__ int16_t sm[kCH + 2][kCW + 2];  // magnitude with a 1-px halo (0 outside the tile)
+    const int x0 = blockIdx.x * kCW, y0 = blockIdx.y * kCH;
+    for (int i = threadIdx.x; i < (kCH + 4) * (kCW + 4); i += blockDim.x) {
+        const int ly = i / (kCW + 4), lx = i - ly * (kCW + 4);
+        const int gx = min(max(x0 + lx - 2, 0), w - 1), gy = min(max(y0 + ly - 2, 0), h - 1);
+        sg[ly][lx] = __ldg(g + (int64_t)gy * w + gx);
+    }
+    __syncthreads();
+    auto sobel = [&](int cy, int cx, int& dx, int& dy) {  // (cy, cx): position in sg
+        dx = (sg[cy - 1][cx + 1] + 2 * sg[cy][cx + 1] + sg[cy + 1][cx + 1]) -
+             (sg[cy - 1][cx - 1] + 2 * sg[cy][cx - 1] + sg[cy + 1][cx - 1]);
+        dy = (sg[cy + 1][cx - 1] + 2 * sg[cy + 1][cx] + sg[cy + 1][cx + 1]) -
+             (sg[cy - 1][cx - 1] + 2 * sg[cy - 1][cx] + sg[cy - 1][cx + 1]);
+    };
+    for (int i = threadIdx.x; i < (kCH + 2) * (kCW + 2); i += blockDim.x) {
+        const int ly = i / (kCW + 2), lx = i - ly * (kCW + 2);  // pixel (x0 + lx - 1, y0 + ly - 1)
+        const int gx = x0 + lx - 1, gy = y0 + ly - 1;
+        int m = 0;
+        if (gx >= 0 && gy >= 0 && gx < w && gy < h) {
+            int dx, dy;
+            sobel(ly + 1, lx + 1, dx, dy);
+            m = abs(dx) + abs(dy);
+        }
+        sm[ly][lx] = (int16_t)m;
+    }
+    __syncthreads();
+    const int lx = threadIdx.x & 31;
+    const int gx = x0 + lx;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int ly = (threadIdx.x >> 5) + 8 * k;
+        const int gy = y0 + ly;
+        if (gx >= w || gy >= h) continue;
+        const int m = sm[ly + 1][lx + 1];
+        uint8_t out = 0;
+        if (m > low) {
+            int dx, dy;
+            sobel(ly + 2, lx + 2, dx, dy);
+            const int ax = abs(dx), ay = abs(dy) << 15;  // |dy| <= 1020: fits in 32 bits
+            const int tg22x = ax * 13573, tg67x = tg22x + (ax << 16);
+            bool lm;
+            if (ay < tg22x) lm = m > sm[ly + 1][lx] && m >= sm[ly + 1][lx + 2];
+            else if (ay > tg67x) lm = m > sm[ly][lx + 1] && m >= sm[ly + 2][lx + 1];
+            else {
+                const int s = ((dx ^ dy) < 0) ? -1 : 1;
+                lm = m > sm[ly][lx + 1 - s] && m > sm[ly + 2][lx + 1 + s];
+            }
+            if (lm) out = m > high ? 2 : 1;
+        }
+        map[(int64_t)gy * w + gx] = out;
+    }
+}
+
 }  // namespace
+
+// Canny edges (0/1) of g.  Scratch: the slot's pmask (candidate map), the sparse planes ML / d
+// and the CCL-select arrays -- free from S6 on, so the pipeline runs it beside S7-S11.
+void launch_canny(const uint8_t* g, int w, int h, int low, int high, Slot& sl, uint8_t* edges, cudaStream_t s) {
+    if ((int64_t)w * h == 0) return;
+    dim3 grid((w + kCW - 1) / kCW, (h + kCH - 1) / kCH);
+    (note_launch(), k_canny_nms<<<grid, 256, 0, s>>>(g, w, h, low, high, sl.pmask));
+    Sel sel{sl.pmask, w, h, 0, 0};
+    sel.P = sl.ML;
+    sel.X = sl.d;
+    run_select<SEL_EDGE>(sel, 8, sl, edges, s);
+}
 
 void launch_rbc(const uint8_t* flags, int w, int h, Slot& sl, uint8_t* rbc, cudaStream_t s) {
     run_select<SEL_RBC>(Sel{flags, w, h, 0, 0}, 8, sl, rbc, s);

@@ -35,6 +35,7 @@ struct CompArgs {
     const int32_t* labF;   // per F pixel: the root of its F component (written by S6), else ~0
     const uint8_t* enc;    // S6: candidate pixels enclosed in another component's hole
     const uint8_t* g;      // for features
+    const uint8_t* edge;   // Canny edges of g (0/1), for features
     float hh;
     int w, h;
     int amin, amax;
@@ -446,7 +447,7 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
             };
             double f[HP_NFEAT];
             int border = 0;
-            object_features(team, inP, a.g, w, h, bb.x, bb.y, bb.z, bb.w, S.fs, red, f, &border);
+            object_features(team, inP, a.g, a.edge, w, h, bb.x, bb.y, bb.z, bb.w, S.fs, red, f, &border);
             if (tr == 0) write_row(a, gidx(r) + 1, border, f);
             team.sync();
         }
@@ -805,7 +806,8 @@ __global__ void k_copy_i32(const int32_t* __restrict__ src, int32_t* __restrict_
 // (written by S6) is A's root.  Islands enclosed by another component (enc at their root) are
 // solved with their encloser.  Shared-memory windows (warp / block teams); windows too big for
 // shared memory and object-list overflows in one block over global-memory storage.
-void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t* g, float hh, int amin, int amax,
+void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t* g, const uint8_t* edge, float hh,
+                       int amin, int amax,
                        int w, int h, Slot& sl, int32_t* labels, int64_t lpitch, int32_t* n_objects,
                        const hp_feature_table* table, int32_t max_objects, cudaStream_t s) {
     const int64_t n = (int64_t)w * h;
@@ -825,6 +827,7 @@ void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t*
     a.labF = sl.lab;
     a.enc = enc;
     a.g = g;
+    a.edge = edge;
     a.hh = hh;
     a.w = w;
     a.h = h;

@@ -98,8 +98,8 @@ __global__ void k_obj_bbox(const int32_t* __restrict__ labels, int64_t lpitch, i
 }
 
 __global__ void __launch_bounds__(kFT, 3) k_obj_feat(const int32_t* __restrict__ labels, int64_t lpitch,
-                                                  const uint8_t* __restrict__ g, int w, int h,
-                                                  const int32_t* __restrict__ cnt, int32_t cap,
+                                                  const uint8_t* __restrict__ g, const uint8_t* __restrict__ edge,
+                                                  int w, int h, const int32_t* __restrict__ cnt, int32_t cap,
                                                   const int32_t* __restrict__ rank_root,
                                                   const int32_t* __restrict__ bbox,
                                                   int32_t* __restrict__ out_label, int32_t* __restrict__ out_flags,
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kFT, 3) k_obj_feat(const int32_t* __restrict__
         };
         double f[HP_NFEAT];
         int border = 0;
-        object_features(team, inP, g, w, h, bbox[4 * obj], bbox[4 * obj + 1], bbox[4 * obj + 2],
+        object_features(team, inP, g, edge, w, h, bbox[4 * obj], bbox[4 * obj + 1], bbox[4 * obj + 2],
                         bbox[4 * obj + 3], fs, red, f, &border);
         if (threadIdx.x == 0) {
             out_label[obj] = lab;
@@ -131,7 +131,7 @@ __global__ void k_copy_count(const int32_t* __restrict__ cnt, int32_t* __restric
 
 }  // namespace
 
-void launch_features(const int32_t* labels, int64_t lpitch, const uint8_t* g, int w, int h,
+void launch_features(const int32_t* labels, int64_t lpitch, const uint8_t* g, const uint8_t* edge, int w, int h,
                      Slot& sl, int32_t max_objects, int32_t* row_label, int32_t* row_flags,
                      float* feat, int32_t capacity, int32_t* n_rows, cudaStream_t s) {
     const int64_t n = (int64_t)w * h;
@@ -143,7 +143,7 @@ void launch_features(const int32_t* labels, int64_t lpitch, const uint8_t* g, in
             cnt, max_objects, sl.obj_root, sl.obj_rank, sl.aux));
         (note_launch(), k_bbox_init<<<std::max(1, std::min(148 * 4, (max_objects + 255) / 256)), 256, 0, s>>>(cnt, max_objects, sl.obj_bbox));
         (note_launch(), k_obj_bbox<<<grid_for(n), 256, 0, s>>>(labels, lpitch, w, h, cnt, max_objects, sl.aux, sl.obj_bbox));
-        (note_launch(), k_obj_feat<<<148 * 8, kFT, 0, s>>>(labels, lpitch, g, w, h, cnt, max_objects, sl.obj_rank,
+        (note_launch(), k_obj_feat<<<148 * 8, kFT, 0, s>>>(labels, lpitch, g, edge, w, h, cnt, max_objects, sl.obj_rank,
                                            sl.obj_bbox, row_label, row_flags, feat, capacity));
     }
     (note_launch(), k_copy_count<<<1, 1, 0, s>>>(cnt, n_rows));

@@ -21,8 +21,8 @@ import hashlib
 
 import numpy as np
 
-NFEAT = 34
-ROW_BYTES = 8 + 4 + 4 + 4 * NFEAT  # tile_id i64, label i32, flags i32, feat f32[34]
+NFEAT = 36
+ROW_BYTES = 8 + 4 + 4 + 4 * NFEAT  # tile_id i64, label i32, flags i32, feat f32[36]
 
 
 def _default_store():
@@ -82,7 +82,7 @@ class DistTileSource:
 
 
 class Rows:
-    """A feature table in columns: tile id, label, flags, 34 features per object row."""
+    """A feature table in columns: tile id, label, flags, 36 features per object row."""
 
     __slots__ = ("tile", "label", "flags", "feat")
 
@@ -113,7 +113,7 @@ class Rows:
 
 
 def to_rows(results: dict) -> Rows:
-    """{tile_id: (label[n], flags[n], feat[n, 34])} -> Rows in tile order (rows of a tile in
+    """{tile_id: (label[n], flags[n], feat[n, 36])} -> Rows in tile order (rows of a tile in
     the order given: hp_run_tiles delivers them by ascending label)."""
     tids = sorted(results)
     counts = [len(results[t][0]) for t in tids]

@@ -13,7 +13,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.environ.get("HP_SO", os.path.join(_HERE, "libhp.so"))
 
-NFEAT = 34
+NFEAT = 36
 FLAG_RBC_HI, FLAG_RBC_LO, FLAG_R_GT_B, FLAG_BG = 1, 2, 4, 8
 OBJ_TOUCHES_BORDER = 1
 FEATURE_NAMES = [
@@ -27,7 +27,7 @@ FEATURE_NAMES = [
 ]
 
 STAGES = ["CD", "RBC", "OPEN", "RECON", "AREA", "FILL", "EDT", "MARKERS", "WATERSHED",
-          "BWLABEL", "FEATURES", "IWPP_RAW", "CCL8", "CCL4", "RECON_F32"]
+          "BWLABEL", "FEATURES", "IWPP_RAW", "CCL8", "CCL4", "RECON_F32", "CANNY"]
 STAGE = {n: i for i, n in enumerate(STAGES)}
 STATUS = {0: "ok", 1: "invalid argument", 2: "CUDA error", 3: "out of memory",
           4: "object capacity exceeded", 5: "unsupported device (need sm_100)"}
@@ -50,7 +50,8 @@ class Params(C.Structure):
                 ("bg_skip_frac", C.c_float), ("rbc_t1", C.c_int32), ("rbc_t2", C.c_int32),
                 ("open_diam", C.c_int32), ("g1", C.c_int32), ("cand_min_area", C.c_int32),
                 ("cand_max_area", C.c_int32), ("h", C.c_float), ("obj_min_area", C.c_int32),
-                ("obj_max_area", C.c_int32), ("glcm_levels", C.c_int32)]
+                ("obj_max_area", C.c_int32), ("glcm_levels", C.c_int32), ("canny_low", C.c_int32),
+                ("canny_high", C.c_int32)]
 
     def to_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_ if f != "q"}
@@ -268,7 +269,7 @@ class Context:
     def run_tiles(self, next_tile, on_done, width, height):
         """Demand-driven driver.  next_tile() -> (host_ptr:int, pitch:int, tile_id:int) or
         None when drained; host memory must be pinned and stay valid until on_done for that
-        tile.  on_done(tile_id, label[n], flags[n], feat[n, 34], status) gets numpy COPIES."""
+        tile.  on_done(tile_id, label[n], flags[n], feat[n, 36], status) gets numpy COPIES."""
         keep = []
 
         def _next(user, pp, ppitch, ptid):

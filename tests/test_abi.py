@@ -37,12 +37,13 @@ def test_default_params_agree_with_oracle():
 
 
 def test_struct_layouts():
-    assert C.sizeof(hp.Params) == 9 * 4 + 13 * 4  # q[3][3] + 13 scalar fields
-    # the C side writes exactly sizeof(hp_params) bytes, glcm_levels last
+    assert C.sizeof(hp.Params) == 9 * 4 + 15 * 4  # q[3][3] + 15 scalar fields
+    # the C side writes exactly sizeof(hp_params) bytes: ..., glcm_levels, canny_low, canny_high
     buf = (C.c_uint8 * 200)(*([0xAB] * 200))
     hp.lib().hp_default_params(C.cast(buf, C.POINTER(hp.Params)))
-    assert all(b == 0xAB for b in buf[88:])
+    assert all(b == 0xAB for b in buf[96:])
     assert int.from_bytes(bytes(buf[84:88]), "little") == 8
+    assert int.from_bytes(bytes(buf[88:92]), "little") == 100 and int.from_bytes(bytes(buf[92:96]), "little") == 200
     assert C.sizeof(hp.Config) == 5 * 4 + C.sizeof(hp.Params)
     assert C.sizeof(hp.Image) == 24 and C.sizeof(hp.Labels) == 24
     assert C.sizeof(hp.StageIO) == 72

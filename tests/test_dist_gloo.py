@@ -28,7 +28,7 @@ def _fake_rows(tid):
     n = int(rng.integers(0, 5))
     lab = np.sort(rng.choice(10_000, size=n, replace=False)).astype(np.int32) + 1
     fl = (lab % 2).astype(np.int32)
-    ft = rng.random((n, 34)).astype(np.float32)
+    ft = rng.random((n, 36)).astype(np.float32)
     return lab, fl, ft
 
 
@@ -96,7 +96,7 @@ def test_rows_columns_and_merge():
     rec = to_rows(res)
     assert list(rec.tile) == [3] * len(res[3][0]) + [7] * len(res[7][0]) + [11] * len(res[11][0])
     assert np.array_equal(rec.label[:len(res[3][0])], res[3][0])
-    assert rec.feat.shape == (len(rec), 34)
+    assert rec.feat.shape == (len(rec), 36)
     # two "ranks" holding interleaved tiles merge into the 1-process order
     a = to_rows({3: res[3], 11: res[11]})
     b = to_rows({7: res[7]})

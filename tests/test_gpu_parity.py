@@ -132,7 +132,7 @@ def test_bwlabel_features(ctx, chain):
     assert np.array_equal(lab, chain["labels"]) and int(n[0]) == chain["nobj"]
     cap = 65536
     rl, rf, ft, nr = stage(ctx, "FEATURES", [chain["labels"], chain["g"]],
-                           [((cap,), I32), ((cap,), I32), ((cap, 34), F32), ((1,), I32)], w, h)
+                           [((cap,), I32), ((cap,), I32), ((cap, 36), F32), ((1,), I32)], w, h)
     k = int(nr[0])
     ol, of, ot = chain["rows"]
     assert k == len(ol)
@@ -213,6 +213,24 @@ def test_edt_random(ctx, shape, dens):
         assert np.array_equal(d2, e2)
 
 
+@pytest.mark.parametrize("shape,blur", [((37, 53), False), ((70, 300), True), ((129, 97), True), ((8, 8), False)])
+def test_canny_random(ctx, shape, blur):
+    import cv2
+    h, w = shape
+    g = np.random.default_rng(h * 7 + w).integers(0, 256, size=shape).astype(U8)
+    if blur:
+        g = cv2.GaussianBlur(g, (5, 5), 1.5)
+    (e,) = stage(ctx, "CANNY", [g], [((h, w), U8)], w, h)
+    assert np.array_equal(e, oracle.canny(g))
+
+
+def test_canny_chain(ctx, chain):
+    h, w = chain["g"].shape
+    (e,) = stage(ctx, "CANNY", [chain["g"]], [((h, w), U8)], w, h)
+    ref = oracle.canny(chain["g"])
+    assert ref.sum() > 100 and np.array_equal(e, ref)
+
+
 def test_edt_far_background(ctx):
     # one background column far from most pixels: exercises the Meijster fallback rows
     h, w = 64, 1500
@@ -231,7 +249,7 @@ def _gpu_process(ctx, rgb, slot=0, cap=65536):
     nobj = torch.zeros(1, dtype=torch.int32, device="cuda")
     tl = torch.zeros(cap, dtype=torch.int32, device="cuda")
     tf = torch.zeros(cap, dtype=torch.int32, device="cuda")
-    tt = torch.zeros((cap, 34), dtype=torch.float32, device="cuda")
+    tt = torch.zeros((cap, 36), dtype=torch.float32, device="cuda")
     nr = torch.zeros(1, dtype=torch.int32, device="cuda")
     ctx.process_tile(slot, t, lab, nobj, tl, tf, tt, nr)
     torch.cuda.synchronize()

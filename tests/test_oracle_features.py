@@ -27,6 +27,7 @@ def _np_features(labels, g):
     rows = []
     cross = ndi.generate_binary_structure(2, 1)
     q = (g >> 5).astype(np.int64)
+    edges = cv2.Canny(g, 100, 200) > 0   # reading C22: OpenCV's Canny itself
     for lab in np.unique(labels[labels > 0]):
         P = labels == lab
         ys, xs = np.nonzero(P)
@@ -80,7 +81,8 @@ def _np_features(labels, g):
                    (Pm / (1 + (i - j) ** 2)).sum(), -(Pm[nz] * np.log2(Pm[nz])).sum(),
                    (t ** 3 * Pm).sum(), (t ** 4 * Pm).sum(), Pm.max()]
         border = xs.min() == 0 or ys.min() == 0 or xs.max() == w - 1 or ys.max() == h - 1
-        rows.append((lab, int(border), shape + inten + grad + tex))
+        ne = int(edges[P].sum())
+        rows.append((lab, int(border), shape + inten + grad + tex + [ne, ne / A]))
     return rows
 
 
@@ -146,6 +148,33 @@ def test_against_numpy_on_pipeline(tile512):
     g, _, _ = oracle.cd(tile512)
     assert n > 10
     _compare(lab, g)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_canny_matches_opencv(seed):
+    """The feature-stage Canny (reading C22) is OpenCV's: cv2.Canny(g, low, high), aperture 3,
+    L1 norm -- on noise, blurred noise and random thresholds, bit for bit."""
+    rng = np.random.default_rng(40 + seed)
+    h, w = (int(v) for v in rng.integers(8, 160, 2))
+    g = rng.integers(0, 256, size=(h, w)).astype(np.uint8)
+    if seed % 2:
+        g = cv2.GaussianBlur(g, (5, 5), 1.5)
+    lo, hi = sorted(int(v) for v in rng.integers(0, 600, 2))
+    assert np.array_equal(oracle.canny(g, lo, hi), (cv2.Canny(g, lo, hi) > 0).astype(np.uint8))
+
+
+def test_canny_on_tile_and_step(tile512):
+    g, _, _ = oracle.cd(tile512)
+    e = oracle.canny(g)
+    assert np.array_equal(e, (cv2.Canny(g, 100, 200) > 0).astype(np.uint8)) and e.sum() > 100
+    # a vertical step of height 60: |dx| = 240 > high on columns 7 and 8; the suppression's
+    # m > left, m >= right keeps the last dark column only
+    step = np.zeros((12, 16), np.uint8)
+    step[:, 8:] = 60
+    e = oracle.canny(step)
+    assert e[:, 7].all() and e.sum() == 12
+    step[:, 8:] = 40                      # |dx| = 160 < high: no strong pixel, no edges
+    assert oracle.canny(step).sum() == 0
 
 
 def test_sobel_reflect101_matches_cv2():

@@ -9,7 +9,7 @@ for i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 8):
     lab = torch.zeros((4096, 4096), dtype=torch.int32, device="cuda")
     nob = torch.zeros(1, dtype=torch.int32, device="cuda")
     tl = torch.zeros(cap, dtype=torch.int32, device="cuda"); tf = torch.zeros(cap, dtype=torch.int32, device="cuda")
-    tt = torch.zeros((cap, 34), dtype=torch.float32, device="cuda"); nr = torch.zeros(1, dtype=torch.int32, device="cuda")
+    tt = torch.zeros((cap, 36), dtype=torch.float32, device="cuda"); nr = torch.zeros(1, dtype=torch.int32, device="cuda")
     ctx.process_tile(0, rgb, lab, nob, tl, tf, tt, nr)
     torch.cuda.synchronize()
     print(i, int(nob.item()), int(nr.item()), flush=True)

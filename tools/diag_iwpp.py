@@ -66,7 +66,7 @@ def main():
     cap = 8192
     tl = torch.empty(cap, dtype=torch.int32, device="cuda")
     tf = torch.empty(cap, dtype=torch.int32, device="cuda")
-    tt = torch.empty((cap, 34), dtype=torch.float32, device="cuda")
+    tt = torch.empty((cap, 36), dtype=torch.float32, device="cuda")
     nr = torch.zeros(1, dtype=torch.int32, device="cuda")
     ctx.process_tile(0, rgb, lab, nob, tl, tf, tt, nr)
     torch.cuda.synchronize()

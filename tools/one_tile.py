@@ -20,7 +20,7 @@ def main():
     nob = torch.zeros(1, dtype=torch.int32, device="cuda")
     tl = torch.empty(cap, dtype=torch.int32, device="cuda")
     tf = torch.empty(cap, dtype=torch.int32, device="cuda")
-    tt = torch.empty((cap, 34), dtype=torch.float32, device="cuda")
+    tt = torch.empty((cap, 36), dtype=torch.float32, device="cuda")
     nr = torch.zeros(1, dtype=torch.int32, device="cuda")
     for _ in range(reps):
         ctx.process_tile(0, rgb, lab, nob, tl, tf, tt, nr)

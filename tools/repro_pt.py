@@ -8,6 +8,6 @@ ctx = Context(0, 4096, 4096, n_slots=1, max_objects=cap)
 d = torch.from_numpy(np.ascontiguousarray(rgb)).cuda()
 lab = torch.empty((h, w), dtype=torch.int32, device="cuda"); nob = torch.zeros(1, dtype=torch.int32, device="cuda")
 tl = torch.empty(cap, dtype=torch.int32, device="cuda"); tf = torch.empty(cap, dtype=torch.int32, device="cuda")
-tt = torch.empty((cap, 34), dtype=torch.float32, device="cuda"); nr = torch.zeros(1, dtype=torch.int32, device="cuda")
+tt = torch.empty((cap, 36), dtype=torch.float32, device="cuda"); nr = torch.zeros(1, dtype=torch.int32, device="cuda")
 ctx.process_tile(0, d, lab, nob, tl, tf, tt, nr)
 torch.cuda.synchronize(); print("ok", int(nob.item()))
