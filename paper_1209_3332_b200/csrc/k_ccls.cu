@@ -385,11 +385,15 @@ __global__ void __launch_bounds__(256) k_cs_accum(int ntiles, const int32_t* __r
     }
 }
 
+// every mode but SEL_FILL outputs 0 on a tile without foreground: the caller zeroes the plane
+// and such tiles (nroots == 0) skip the pass
 template <int MODE>
 __global__ void __launch_bounds__(256) k_cs_out(Sel sel, int conn, const int32_t* __restrict__ P,
-                                                const int32_t* __restrict__ X, uint8_t* __restrict__ out) {
+                                                const int32_t* __restrict__ X, uint8_t* __restrict__ out,
+                                                const int32_t* __restrict__ nroots) {
     __shared__ TileSm T;
     if (sel.gate && *sel.gate == 0) return;
+    if (MODE != SEL_FILL && nroots[blockIdx.y * gridDim.x + blockIdx.x] == 0) return;
     const int tx0 = blockIdx.x * kT, ty0 = blockIdx.y * kT;
     const int lane = threadIdx.x & 31;
     const int w = sel.w, h = sel.h;
@@ -464,7 +468,10 @@ void run_select(Sel sel, int conn, Slot& sl, uint8_t* out, cudaStream_t s, const
     (note_launch(), k_cs_merge<<<(int)(((int64_t)ntiles * 2 * kT + 255) / 256), 256, 0, s>>>(conn, ntx, nty,
                                                                                            sl.cs_edge, P, sel.gate));
     (note_launch(), k_cs_accum<<<(ntiles + 7) / 8, 256, 0, s>>>(ntiles, sl.cs_roots, sl.cs_nroots, P, X, sel));
-    if (out) (note_launch(), k_cs_out<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, out));
+    if (out) {
+        if (MODE != SEL_FILL) cudaMemsetAsync(out, 0, (size_t)w * h, s);
+        (note_launch(), k_cs_out<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, out, sl.cs_nroots));
+    }
     if (lo)
         (note_launch(), k_cs_list<<<(ntiles + 7) / 8, 256, 0, s>>>(ntiles, sl.cs_roots, sl.cs_nroots, P, X, sel,
                                                                    lo->root, lo->bbox, lo->area, lo->count, lo->cap));
