@@ -268,6 +268,35 @@ def _check_pipeline(ctx, rgb):
     return nobj
 
 
+@pytest.mark.parametrize("seed", [21, 22])
+def test_segment_then_features(ctx, seed):
+    """The two-call ABI path: hp_segment_tile (S1-S10, no features), then hp_features_tile
+    on its labels (S1 again, Canny, S11 from the label plane) -- equal to the oracle, and to
+    hp_process_tile's fused rows."""
+    import torch
+    rgb = make_tile(seed, TileSpec(384, 448))["rgb"]
+    h, w = rgb.shape[:2]
+    t = torch.from_numpy(np.ascontiguousarray(rgb)).cuda()
+    lab = torch.zeros((h, w), dtype=torch.int32, device="cuda")
+    nobj = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.segment_tile(1, t, lab, nobj)
+    cap = 4096
+    tl = torch.zeros(cap, dtype=torch.int32, device="cuda")
+    tf = torch.zeros(cap, dtype=torch.int32, device="cuda")
+    tt = torch.zeros((cap, 36), dtype=torch.float32, device="cuda")
+    nr = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.features_tile(1, t, lab, nobj, tl, tf, tt, nr)
+    torch.cuda.synchronize()
+    olab, ol, of, ot = oracle.process_tile(rgb)
+    assert np.array_equal(lab.cpu().numpy(), olab) and int(nobj.item()) == len(ol)
+    k = int(nr.item())
+    gl, gf, gt = tl[:k].cpu().numpy(), tf[:k].cpu().numpy(), tt[:k].cpu().numpy()
+    assert_features_equal(gl, gf, gt, ol, of, ot)
+    _, _, fl, ff, ft = _gpu_process(ctx, rgb)
+    assert np.array_equal(fl, gl) and np.array_equal(ff, gf)
+    assert features_close(ft, gt).all()
+
+
 def test_pipeline_config1(ctx):
     assert _check_pipeline(ctx, make_config_tile(1)) > 10
 
