@@ -212,6 +212,18 @@ hp_status hp_stage_times_accum(hp_ctx* ctx, float* ms11, int32_t* count);
 /* Number of libhp kernel launches issued by this process so far (diagnostics). */
 int64_t   hp_launch_count(void);
 
+/* Per-image feature aggregation (the object features of an
+ * image feed the image-level classification stage).  Segmented reduction of feature rows on
+ * the device: rows [off[g], off[g+1]) of feat (DEVICE, [n_rows][HP_NFEAT] f32, row-major)
+ * form group g (e.g. one slide); out (DEVICE, [n_groups][HP_NFEAT][2] f64) receives per group
+ * and feature the sum and the sum of squares, out_count (DEVICE, i64[n_groups]) the number of
+ * rows.  off: DEVICE i64[n_groups + 1], non-decreasing.  Every thread reduces a fixed set of
+ * rows and the per-group tree has a fixed shape, so the result is bit-identical run to run.
+ * Async on s; HP_ERR_INVALID on null pointers or n_groups < 0.  Across GPUs the callers sum
+ * the outputs with an all-reduce (paper_1209_3332_b200/dist.py aggregate_groups). */
+hp_status hp_reduce_rows(hp_ctx* ctx, const float* feat, const int64_t* off, int32_t n_groups,
+                         double* out, int64_t* out_count, hp_stream s);
+
 #ifdef __cplusplus
 }
 #endif

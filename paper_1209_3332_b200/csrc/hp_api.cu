@@ -521,6 +521,18 @@ hp_status hp_get_stage_times(hp_ctx* ctx, int32_t slot, float* ms11) {
     return sum_set(ctx, ctx->ring[slot][ctx->ring_pos[slot]], ms11);
 }
 
+hp_status hp_reduce_rows(hp_ctx* ctx, const float* feat, const int64_t* off, int32_t n_groups, double* out,
+                         int64_t* out_count, hp_stream s) {
+    hp_status st = enter(ctx, 0);
+    if (st) return st;
+    if (n_groups < 0 || (n_groups > 0 && (!feat || !off || !out || !out_count))) {
+        set_err(ctx, "hp_reduce_rows: null pointer or n_groups < 0");
+        return HP_ERR_INVALID;
+    }
+    launch_reduce_rows(feat, off, n_groups, out, out_count, (cudaStream_t)s);
+    return check_launch(ctx, "reduce_rows");
+}
+
 hp_status hp_stage_times_accum(hp_ctx* ctx, float* ms11, int32_t* count) {
     hp_status st = enter(ctx, 0);
     if (st) return st;

@@ -196,6 +196,9 @@ void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t*
                        int amin, int amax, int w, int h, Slot& sl, int32_t* labels, int64_t lpitch,
                        int32_t* n_objects, const hp_feature_table* table, int32_t max_objects, cudaStream_t s);
 // S11
+// per-image aggregation (k_agg.cu): segmented fp64 sums / sums of squares of feature rows
+void launch_reduce_rows(const float* feat, const int64_t* off, int32_t n_groups, double* out, int64_t* count,
+                        cudaStream_t s);
 // Feature-stage Canny (k_ccls.cu): edges 0/1 = cv2.Canny(g, low, high), reading C22
 void launch_canny(const uint8_t* g, int w, int h, int low, int high, Slot& sl, uint8_t* edges, cudaStream_t s);
 void launch_features(const int32_t* labels, int64_t lpitch, const uint8_t* g, const uint8_t* edge, int w, int h,

@@ -1,0 +1,58 @@
+// k_agg.cu -- per-image feature aggregation: a segmented
+// fp64 reduction of feature rows, one block per group, every thread owning a fixed set of
+// rows and the block combining its partials by a fixed tree -- deterministic.  The rows of a
+// group are contiguous (a rank's table is in tile order and tiles map to slides in order).
+#include "hp_internal.cuh"
+
+namespace hp {
+namespace {
+
+constexpr int kAT = 256;  // threads per group block
+constexpr int kAF = 9;    // features per pass (HP_NFEAT = 36 -> 4 passes; 39 KB of shared memory)
+
+__global__ void __launch_bounds__(kAT) k_reduce_rows(const float* __restrict__ feat, const int64_t* __restrict__ off,
+                                                     double* __restrict__ out, int64_t* __restrict__ count) {
+    __shared__ double red[kAT][2 * kAF + 1];  // (+1: no bank conflicts between threads)
+    const int gi = blockIdx.x;
+    const int64_t r0 = off[gi], r1 = off[gi + 1];
+    if (threadIdx.x == 0) count[gi] = r1 - r0;
+    for (int f0 = 0; f0 < HP_NFEAT; f0 += kAF) {
+        double s[kAF], q[kAF];
+#pragma unroll
+        for (int k = 0; k < kAF; ++k) s[k] = q[k] = 0.0;
+        for (int64_t r = r0 + threadIdx.x; r < r1; r += kAT) {
+            const float* row = feat + r * HP_NFEAT + f0;
+#pragma unroll
+            for (int k = 0; k < kAF; ++k) {
+                const double v = (double)row[k];
+                s[k] += v;
+                q[k] += v * v;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kAF; ++k) {
+            red[threadIdx.x][2 * k] = s[k];
+            red[threadIdx.x][2 * k + 1] = q[k];
+        }
+        __syncthreads();
+        for (int half = kAT / 2; half > 0; half >>= 1) {  // fixed pairwise tree
+            if (threadIdx.x < half)
+                for (int k = 0; k < 2 * kAF; ++k) red[threadIdx.x][k] += red[threadIdx.x + half][k];
+            __syncthreads();
+        }
+        if (threadIdx.x < 2 * kAF) out[((int64_t)gi * HP_NFEAT + f0 + threadIdx.x / 2) * 2 + (threadIdx.x & 1)] =
+            red[0][threadIdx.x];
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+void launch_reduce_rows(const float* feat, const int64_t* off, int32_t n_groups, double* out, int64_t* count,
+                        cudaStream_t s) {
+    static_assert(HP_NFEAT % kAF == 0, "features per pass");
+    if (n_groups == 0) return;
+    (note_launch(), k_reduce_rows<<<n_groups, kAT, 0, s>>>(feat, off, out, count));
+}
+
+}  // namespace hp

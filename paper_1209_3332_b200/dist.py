@@ -192,3 +192,58 @@ def table_digest(rows: Rows) -> str:
     for name, _, _ in _FIELDS:
         h.update(np.ascontiguousarray(getattr(rows, name)).view(np.uint8).tobytes())
     return h.hexdigest()[:16]
+
+
+def group_offsets(rows: Rows, group_of_tile, n_groups: int) -> np.ndarray:
+    """Row offsets of each group (int64[n_groups + 1]) in a tile-ordered table, for a group
+    id that is non-decreasing in the tile id (e.g. slide = tile // tiles_per_slide)."""
+    gid = np.asarray(group_of_tile(rows.tile), np.int64)
+    if len(gid) and (np.any(np.diff(gid) < 0) or gid[0] < 0 or gid[-1] >= n_groups):
+        raise ValueError("group ids must be non-decreasing in the table order and in [0, n_groups)")
+    return np.searchsorted(gid, np.arange(n_groups + 1), side="left").astype(np.int64)
+
+
+def aggregate_groups(rows: Rows, group_of_tile, n_groups: int, reduce=None, device=None):
+    """Per-image (per-group) feature aggregation: every rank reduces its own
+    rows per group -- on the GPU through hp_reduce_rows (``reduce`` = a Context, or any
+    callable (feat, off) -> (sums [G, 36, 2] f64, counts [G] i64)) -- then one all_reduce(SUM)
+    of the partial sums over the process group (NCCL on GPUs, gloo on CPU) gives every rank
+    the totals.  Returns (count [G], mean [G, 36], std [G, 36]) in float64 (population std)."""
+    import torch
+    import torch.distributed as dist
+    off = group_offsets(rows, group_of_tile, n_groups)
+    dev = device if device is not None else torch.device("cpu")
+    if reduce is None or callable(reduce) and not hasattr(reduce, "reduce_rows"):
+        fn = reduce if reduce is not None else _reduce_numpy
+        sums, cnt = fn(rows.feat, off)
+        sums_t = torch.from_numpy(np.ascontiguousarray(sums, np.float64)).to(dev)
+        cnt_t = torch.from_numpy(np.ascontiguousarray(cnt, np.int64)).to(dev)
+    else:  # a Context: the device kernel
+        feat_t = torch.from_numpy(np.ascontiguousarray(rows.feat)).to(dev)
+        off_t = torch.from_numpy(off).to(dev)
+        sums_t = torch.empty((n_groups, NFEAT, 2), dtype=torch.float64, device=dev)
+        cnt_t = torch.empty(n_groups, dtype=torch.int64, device=dev)
+        if n_groups:
+            reduce.reduce_rows(feat_t, off_t, sums_t, cnt_t)
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(sums_t, op=dist.ReduceOp.SUM)
+        dist.all_reduce(cnt_t, op=dist.ReduceOp.SUM)
+    sums = sums_t.cpu().numpy()
+    cnt = cnt_t.cpu().numpy()
+    with np.errstate(invalid="ignore", divide="ignore"):
+        n = cnt[:, None].astype(np.float64)
+        mean = sums[:, :, 0] / n
+        var = np.maximum(sums[:, :, 1] / n - mean * mean, 0.0)
+    return cnt, mean, np.sqrt(var)
+
+
+def _reduce_numpy(feat, off):
+    """Host stand-in for hp_reduce_rows (tests, CPU runs)."""
+    G = len(off) - 1
+    sums = np.zeros((G, NFEAT, 2), np.float64)
+    for g in range(G):
+        f = feat[off[g]:off[g + 1]].astype(np.float64)
+        sums[g, :, 0] = f.sum(axis=0)
+        sums[g, :, 1] = (f * f).sum(axis=0)
+    return sums, np.diff(off).astype(np.int64)
+

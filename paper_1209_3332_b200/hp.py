@@ -36,7 +36,7 @@ STATUS = {0: "ok", 1: "invalid argument", 2: "CUDA error", 3: "out of memory",
 EXPORTS = ["hp_default_params", "hp_ctx_create", "hp_ctx_destroy", "hp_status_str",
            "hp_last_error", "hp_version", "hp_segment_tile", "hp_features_tile",
            "hp_process_tile", "hp_run_tiles", "hp_stage_run", "hp_set_stage_timing",
-           "hp_get_stage_times", "hp_stage_times_accum", "hp_launch_count"]
+           "hp_get_stage_times", "hp_stage_times_accum", "hp_launch_count", "hp_reduce_rows"]
 
 
 class HPError(RuntimeError):
@@ -141,6 +141,7 @@ def lib():
             "hp_get_stage_times": (C.c_int, [P, i32, C.POINTER(C.c_float)]),
             "hp_stage_times_accum": (C.c_int, [P, C.POINTER(C.c_float), C.POINTER(C.c_int32)]),
             "hp_launch_count": (C.c_int64, []),
+            "hp_reduce_rows": (C.c_int, [P, P, P, i32, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -230,6 +231,12 @@ class Context:
                            t_label.shape[0], n_rows.data_ptr())
         self._chk(lib().hp_features_tile(self._h, slot, C.byref(im), C.byref(lab), C.byref(tab),
                                          _stream(stream)), "hp_features_tile")
+
+    def reduce_rows(self, feat, off, out, out_count, stream=None):
+        """hp_reduce_rows: per group g, sums and sums of squares (f64) of the feature rows
+        [off[g], off[g+1]) of feat ([n, 36] f32); all device tensors."""
+        self._chk(lib().hp_reduce_rows(self._h, feat.data_ptr(), off.data_ptr(), off.shape[0] - 1,
+                                       out.data_ptr(), out_count.data_ptr(), _stream(stream)), "hp_reduce_rows")
 
     def process_tile(self, slot, rgb, labels, n_objects, t_label, t_flags, t_feat, n_rows,
                      stream=None):

@@ -12,7 +12,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1209_3332_b200.dist import DistTileSource, TileQueue, gather_rows, table_digest, to_rows
+from paper_1209_3332_b200.dist import (DistTileSource, TileQueue, aggregate_groups, gather_rows, table_digest,
+                                       to_rows)
 
 
 def _free_port():
@@ -110,3 +111,42 @@ def test_single_process_queue():
     while (b := q.grab()) is not None:
         blocks.append(list(b))
     assert blocks == [[0, 1, 2, 3], [4, 5, 6, 7], [8, 9]]
+
+
+def _agg_worker(rank, world, port, n_tiles, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    mine = {t: _fake_rows(t) for t in range(n_tiles) if t % world == rank}   # disjoint tiles
+    cnt, mean, std = aggregate_groups(to_rows(mine), lambda tile: tile // 5, (n_tiles + 4) // 5)
+    out_q.put((rank, cnt, mean, std))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_aggregate_groups_world2():
+    """SURVEY NEXT-4 host logic: per-rank segmented sums + all_reduce == one process's
+    per-group numpy mean / population std over the union of the rows."""
+    n_tiles = 23
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agg_worker, args=(r, 2, port, n_tiles, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted([q.get(timeout=120) for _ in procs], key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = to_rows({t: _fake_rows(t) for t in range(n_tiles)})
+    G = (n_tiles + 4) // 5
+    for _, cnt, mean, std in outs:
+        for g in range(G):
+            sel = (ref.tile // 5) == g
+            assert cnt[g] == sel.sum()
+            if sel.sum():
+                f = ref.feat[sel].astype(np.float64)
+                assert np.allclose(mean[g], f.mean(axis=0), rtol=1e-12, atol=1e-12)
+                assert np.allclose(std[g], f.std(axis=0), rtol=1e-9, atol=1e-9)
+            else:
+                assert np.isnan(mean[g]).all()
+

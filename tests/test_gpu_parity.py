@@ -394,6 +394,49 @@ def test_iwpp_stress(ctx, kind, ramp):
     assert np.array_equal(rec, mask)
 
 
+def test_reduce_rows(ctx):
+    """hp_reduce_rows (segmented fp64 sums) against numpy, with empty groups,
+    and bit-identical run to run."""
+    import torch
+    rng = np.random.default_rng(5)
+    sizes = [0, 1, 7, 300, 0, 2049, 5]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    feat = (rng.standard_normal((int(off[-1]), 36)) * rng.uniform(0.1, 1e3, 36)).astype(np.float32)
+    ft, ot = torch.from_numpy(feat).cuda(), torch.from_numpy(off).cuda()
+    outs = []
+    for _ in range(2):
+        out = torch.full((len(sizes), 36, 2), np.nan, dtype=torch.float64, device="cuda")
+        cnt = torch.full((len(sizes),), -1, dtype=torch.int64, device="cuda")
+        ctx.reduce_rows(ft, ot, out, cnt)
+        torch.cuda.synchronize()
+        outs.append((out.cpu().numpy(), cnt.cpu().numpy()))
+    (o, c), (o2, c2) = outs
+    assert np.array_equal(c, sizes) and np.array_equal(o, o2)      # deterministic
+    for g in range(len(sizes)):
+        f = feat[off[g]:off[g + 1]].astype(np.float64)
+        assert np.allclose(o[g, :, 0], f.sum(axis=0), rtol=1e-12, atol=1e-9)
+        assert np.allclose(o[g, :, 1], (f * f).sum(axis=0), rtol=1e-12, atol=1e-9)
+
+
+def test_aggregate_groups_on_gpu(ctx):
+    """dist.aggregate_groups through the device kernel == numpy on a pipeline table."""
+    import torch
+    from paper_1209_3332_b200.dist import aggregate_groups, to_rows
+    tiles = {i: make_tile(800 + i, TileSpec(256, 256))["rgb"] for i in range(4)}
+    res = {}
+    for i, rgb in tiles.items():
+        _, _, gl, gf, gt = _gpu_process(ctx, rgb)
+        res[i] = (gl, gf, gt)
+    rows = to_rows(res)
+    cnt, mean, std = aggregate_groups(rows, lambda t: t // 2, 2, reduce=ctx, device=torch.device("cuda"))
+    for g in range(2):
+        sel = rows.tile // 2 == g
+        f = rows.feat[sel].astype(np.float64)
+        assert cnt[g] == sel.sum() > 0
+        assert np.allclose(mean[g], f.mean(axis=0), rtol=1e-12, atol=1e-12)
+        assert np.allclose(std[g], f.std(axis=0), rtol=1e-9, atol=1e-9)
+
+
 def test_run_tiles_size_change(ctx):
     """hp_run_tiles replays a per-slot CUDA graph; a new tile size must rebuild it."""
     import torch

@@ -54,7 +54,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1209_3332_b200 import Context
-    from paper_1209_3332_b200.dist import DistTileSource, TileQueue, gather_rows, table_digest
+    from paper_1209_3332_b200.dist import DistTileSource, TileQueue, aggregate_groups, gather_rows, table_digest, to_rows
 
     t0 = time.time()
     pool = [torch.from_numpy(pool_tile(args.config, k)).pin_memory() for k in range(args.pool)]
@@ -78,6 +78,13 @@ def main():
     t_run = time.perf_counter() - t1
     table = gather_rows(results, device=torch.device("cuda", local))
     t_all = time.perf_counter() - t1
+    # per-slide aggregation: device segmented sums per rank, NCCL all-reduce
+    per_slide = 108 if args.config == 4 else n_tiles
+    n_groups = (n_tiles + per_slide - 1) // per_slide
+    ta = time.perf_counter()
+    cnt, mean, std = aggregate_groups(to_rows(results), lambda t: t // per_slide, n_groups, reduce=ctx,
+                                      device=torch.device("cuda", local))
+    agg_ms = 1e3 * (time.perf_counter() - ta)
     tt = torch.tensor([t_all, t_run], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -86,7 +93,9 @@ def main():
                           "slots": args.slots, "tiles_per_s": n_tiles / float(tt[0]),
                           "tiles_per_s_excl_gather": n_tiles / float(tt[1]),
                           "rows": int(len(table)), "digest": table_digest(table),
-                          "my_tiles_rank0": len(src.taken), "pool_gen_s": round(gen_s, 1)}), flush=True)
+                          "my_tiles_rank0": len(src.taken), "pool_gen_s": round(gen_s, 1),
+                          "groups": n_groups, "group_rows": int(cnt.sum()), "agg_ms": round(agg_ms, 1),
+                          "agg_checksum": float(np.nansum(mean) + np.nansum(std))}), flush=True)
     if world > 1:
         dist.destroy_process_group()
     ctx.close()
