@@ -39,6 +39,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HP_RG_PROFILE
 #define HP_RG_PROFILE 0  // timing breakdown in the stats (experiments)
 #endif
+#ifndef HP_RG_FIRSTORDER
+#define HP_RG_FIRSTORDER 0  // first jobs: release sub-tile rows top to bottom
+#endif
 #ifndef HP_RG_JACOBI
 #define HP_RG_JACOBI 0  // neighbour-exchange steps tried before the row scans
 #endif
@@ -150,6 +153,7 @@ struct Smem {
     int job;
     int again;
     unsigned long long t0, tA, tB;
+    int first;  // HP_RG_FIRSTORDER: this job is the region's first
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -395,6 +399,16 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                     }
                 }
                 if (threadIdx.x == 0) {
+#if HP_RG_FIRSTORDER
+                    // a region's first job (every row of every sub-tile dirty): only the top row
+                    // of sub-tiles starts; each releases the one below when its first sweep set
+                    // ends, so lower sub-tiles do not sweep against stale top halos first
+                    bool first = true;
+                    for (int k = 0; k < NW; ++k) first &= S.dirty[k] == 0xffffffffu;
+                    S.first = first;
+                    if (first)
+                        for (int k = RX; k < NW; ++k) S.dirty[k] = 0;
+#endif
                     int np = 0;
                     for (int k = 0; k < NW; ++k) np += S.dirty[k] != 0;
                     S.pend = np;
@@ -478,6 +492,10 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                     }
                     ++iters;
                     mychg |= chg;
+#if HP_RG_FIRSTORDER
+                    if (S.first && sy < RY - 1 && iters == 1 && lane == 0)  // release the sub-tile below
+                        if (atomicOr(&S.dirty[warp + RX], 0xffffffffu) == 0u) atomicAdd(&S.pend, 1);
+#endif
                     if (chg) {
                         // rows of in-region neighbours that changed border pixels can improve
                         // (m8 index = N8 direction of the neighbour, bit = its row)
