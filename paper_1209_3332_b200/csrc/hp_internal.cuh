@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "../../include/hp.h"
 
 namespace hp {
@@ -117,6 +119,25 @@ struct Slot {
 // every kernel launch of libhp goes through (note_launch(), kernel<<<...>>>(...)) so the
 // bench can report how many of OUR kernels ran (hp_launch_count)
 void note_launch();
+// Per-device one-time setup (cudaFuncSetAttribute, occupancy-derived grid sizes apply to the
+// CURRENT device only): run f once for each device a launcher is used on; thread-safe.
+struct PerDevice {
+    std::mutex m;
+    bool done[64] = {};
+    int value[64] = {};
+    template <class F>
+    int get(F f) {  // f() -> int, evaluated once per device; returns the device's value
+        int dev = 0;
+        cudaGetDevice(&dev);
+        dev &= 63;
+        std::lock_guard<std::mutex> g(m);
+        if (!done[dev]) {
+            value[dev] = f();
+            done[dev] = true;
+        }
+        return value[dev];
+    }
+};
 // S1
 void launch_cd(const uint8_t* rgb, int w, int h, int64_t pitch, const float* lut,
                const hp_params& p, uint8_t* g, uint8_t* flags, unsigned long long* bg_count,

@@ -845,11 +845,8 @@ void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t*
     a.ovf_cnt = ovf;
     a.ovf_list = sl.sc_huge;  // (S6's huge list is consumed by then: same stream)
     const size_t smw = kWarpsPB * sizeof(CompSm<kCapW, kKoW>);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_comp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
-        attr = true;
-    }
+    static PerDevice once;
+    once.get([&] { return (int)cudaFuncSetAttribute(k_comp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw); });
     (note_launch(), k_comp_classify<<<grid_for(cap), 256, 0, s>>>(a, count5, cap, sl.sc_root, sl.sc_bbox,
                                                                    sl.sc_big, nbig));
     (note_launch(), k_comp_fused<<<148 * 4, kWarpsPB * 32, smw, s>>>(a, count5, cap, sl.sc_root, sl.sc_bbox,
@@ -876,11 +873,8 @@ void launch_fill_components(const uint8_t* big0, int w, int h, Slot& sl, const i
     cudaMemsetAsync(sl.lab, 0xff, 4 * n, s);
     FillArgs a{big0, w, h, F, enc, reinterpret_cast<unsigned*>(sl.lab)};
     const size_t smw = kWarpsPB * sizeof(CompSm<kCapW, kKoW>);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_fill_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
-        attr = true;
-    }
+    static PerDevice once;
+    once.get([&] { return (int)cudaFuncSetAttribute(k_fill_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw); });
     const int32_t cap = sl.comp_cap;
     (note_launch(), k_win_classify<<<grid_for(cap), 256, 0, s>>>(count, cap, sl.sc_bbox, sl.sc_big, nbig, sl.sc_huge,
                                                                   nhuge));

@@ -189,11 +189,8 @@ void launch_edt(const uint8_t* F, int w, int h, Slot& sl, uint32_t* d2_out, floa
     (note_launch(), k_edt_seg<<<grid_for(nthreads), 256, 0, s>>>(F, w, h, nseg, sl.seg_top, sl.seg_bot, any_bg, cond));
     (note_launch(), k_edt_col<<<grid_for(nthreads), 256, 0, s>>>(F, w, h, nseg, sl.seg_top, sl.seg_bot, sl.gcol, cond));
     size_t smem = sizeof(uint32_t) * (size_t)w;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_edt_row, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    static PerDevice once;
+    once.get([] { return (int)cudaFuncSetAttribute(k_edt_row, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
     (note_launch(), k_edt_row<<<h, 256, smem, s>>>(F, w, h, sl.gcol, any_bg, sl.aux, sl.d, d2_out, dist, cond));
 }
 

@@ -285,8 +285,8 @@ __global__ void k_wl_seed_mask(Worklist wl, const uint8_t* __restrict__ mask, in
 template <class Rule, class T>
 void run_rule(const Rule& rule, const Worklist& wl, cudaStream_t s) {
     const size_t smem = sizeof(T) * Rule::kWords * kWarps;
-    static int blocks = 0;
-    if (blocks == 0) {
+    static PerDevice once;
+    const int blocks = once.get([&] {
         cudaFuncSetAttribute(k_wl_run<Rule, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int per_sm = 0, dev = 0, nsm = 148;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wl_run<Rule, T>, kWarps * 32, smem);
@@ -298,8 +298,8 @@ void run_rule(const Rule& rule, const Worklist& wl, cudaStream_t s) {
         int want = 64;
         if (const char* e = getenv("HP_WL_CTAS_PER_SM")) want = atoi(e);
         if (want < 1) want = 1;
-        blocks = nsm * std::min(want, per_sm > 0 ? per_sm : 1);
-    }
+        return nsm * std::min(want, per_sm > 0 ? per_sm : 1);
+    });
     int ntiles = wl.ntx * wl.nty;
     int b = std::min(blocks, (ntiles + kWarps - 1) / kWarps);
     if (b < 1) b = 1;

@@ -178,13 +178,12 @@ size_t smem_r() {
 
 template <int R>
 void launch_r(const uint8_t* g, int w, int h, uint8_t* tmp, uint8_t* out, cudaStream_t s) {
-    static bool attr = false;
+    static PerDevice once;
     const size_t smem = smem_r<R>();
-    if (!attr) {
+    once.get([&] {
         cudaFuncSetAttribute(k_morph_r<true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_morph_r<false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+        return (int)cudaFuncSetAttribute(k_morph_r<false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
     dim3 grid((w + TW2 - 1) / TW2, (h + TH2 - 1) / TH2);
     (note_launch(), k_morph_r<true, R><<<grid, 256, smem, s>>>(g, w, h, tmp));
     (note_launch(), k_morph_r<false, R><<<grid, 256, smem, s>>>(tmp, w, h, out));
@@ -292,12 +291,11 @@ void launch_open(const uint8_t* g, int w, int h, int diam, uint8_t* tmp, uint8_t
     }
     size_t smem = 0;
     MorphDesc md = make_desc(diam, &smem);
-    static bool attr_set = false;
-    if (!attr_set) {
+    static PerDevice once;
+    once.get([] {
         cudaFuncSetAttribute(k_morph<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(k_morph<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
-    }
+        return (int)cudaFuncSetAttribute(k_morph<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    });
     dim3 grid((w + TW - 1) / TW, (h + md.th - 1) / md.th);
     (note_launch(), k_morph<true><<<grid, 256, smem, s>>>(g, w, h, md, tmp));
     (note_launch(), k_morph<false><<<grid, 256, smem, s>>>(tmp, w, h, md, out));

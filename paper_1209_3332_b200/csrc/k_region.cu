@@ -697,9 +697,9 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
     wl.nty = (h + RY * kTile - 1) / (RY * kTile);
     const int n = wl.ntx * wl.nty;
     (note_launch(), k_rg_reset<<<(int)std::min<int64_t>((std::max<int64_t>(wl.cap, (int64_t)n * NW) + 255) / 256, 148 * 16), 256, 0, s>>>(wl));
-    static int blocks = 0;
+    static PerDevice once;
     const size_t smem = sizeof(Smem);
-    if (blocks == 0) {
+    const int blocks = once.get([&] {
         cudaFuncSetAttribute(k_region_mr8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int per_sm = 0, dev = 0, nsm = 148;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_region_mr8, NW * 32, smem);
@@ -711,8 +711,8 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
         int want = 1;
         if (const char* e = getenv("HP_RG_CTAS_PER_SM")) want = atoi(e);
         want = std::max(1, std::min(want, per_sm > 0 ? per_sm : 1));
-        blocks = nsm * want;
-    }
+        return nsm * want;
+    });
     int b = std::max(1, std::min(blocks, n));
     (note_launch(), k_region_mr8<<<b, NW * 32, smem, s>>>(mask, R, w, h, wl));
 }

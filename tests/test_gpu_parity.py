@@ -297,6 +297,33 @@ def test_segment_then_features(ctx, seed):
     assert features_close(ft, gt).all()
 
 
+def test_two_devices_one_process():
+    """Contexts on two GPUs in one process: per-device kernel attributes and grid sizes."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    from paper_1209_3332_b200 import Context
+    rgb = make_tile(31, TileSpec(320, 384))["rgb"]
+    olab, ol, of, ot = oracle.process_tile(rgb)
+    for dev in (1, 0):
+        with torch.cuda.device(dev):
+            c = Context(dev, 1024, 1024, n_slots=1, max_objects=4096)
+            h, w = rgb.shape[:2]
+            t = torch.from_numpy(np.ascontiguousarray(rgb)).cuda(dev)
+            lab = torch.zeros((h, w), dtype=torch.int32, device=f"cuda:{dev}")
+            nobj = torch.zeros(1, dtype=torch.int32, device=f"cuda:{dev}")
+            tl = torch.zeros(4096, dtype=torch.int32, device=f"cuda:{dev}")
+            tf = torch.zeros(4096, dtype=torch.int32, device=f"cuda:{dev}")
+            tt = torch.zeros((4096, 36), dtype=torch.float32, device=f"cuda:{dev}")
+            nr = torch.zeros(1, dtype=torch.int32, device=f"cuda:{dev}")
+            c.process_tile(0, t, lab, nobj, tl, tf, tt, nr)
+            torch.cuda.synchronize(dev)
+            k = int(nr.item())
+            assert np.array_equal(lab.cpu().numpy(), olab)
+            assert_features_equal(tl[:k].cpu().numpy(), tf[:k].cpu().numpy(), tt[:k].cpu().numpy(), ol, of, ot)
+            c.close()
+
+
 def test_pipeline_config1(ctx):
     assert _check_pipeline(ctx, make_config_tile(1)) > 10
 
