@@ -72,6 +72,11 @@ def test_invalid_config_rejected():
     p.open_diam = 18
     cfg = hp.Config(0, 64, 64, 1, 16, p)
     assert hp.lib().hp_ctx_create(C.byref(cfg), C.byref(h)) == 1
+    for lo, hi in [(-1, 10), (200, 100)]:          # reading C22: 0 <= canny_low <= canny_high
+        p = P.default_params()
+        p.canny_low, p.canny_high = lo, hi
+        cfg = hp.Config(0, 64, 64, 1, 16, p)
+        assert hp.lib().hp_ctx_create(C.byref(cfg), C.byref(h)) == 1
 
 
 def test_product_does_not_touch_oracle():

@@ -324,6 +324,35 @@ def test_two_devices_one_process():
             c.close()
 
 
+def test_table_capacity(ctx):
+    """More objects than table rows: n_rows is still the true count and the rows written are
+    the first ones in label order (hp_run_tiles reports HP_ERR_CAPACITY to its sink)."""
+    import torch
+    rgb = make_tile(41, TileSpec(384, 384))["rgb"]
+    h, w = rgb.shape[:2]
+    _, ol, of, ot = oracle.process_tile(rgb)
+    assert len(ol) > 8
+    t = torch.from_numpy(np.ascontiguousarray(rgb)).cuda()
+    lab = torch.zeros((h, w), dtype=torch.int32, device="cuda")
+    nobj = torch.zeros(1, dtype=torch.int32, device="cuda")
+    cap = 5
+    tl = torch.zeros(cap, dtype=torch.int32, device="cuda")
+    tf = torch.zeros(cap, dtype=torch.int32, device="cuda")
+    tt = torch.zeros((cap, 36), dtype=torch.float32, device="cuda")
+    nr = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.process_tile(0, t, lab, nobj, tl, tf, tt, nr)
+    torch.cuda.synchronize()
+    assert int(nr.item()) == len(ol)
+    assert_features_equal(tl.cpu().numpy(), tf.cpu().numpy(), tt.cpu().numpy(), ol[:cap], of[:cap], ot[:cap])
+
+
+def test_stage_missing_buffer_rejected(ctx):
+    from paper_1209_3332_b200.hp import HPError
+    with pytest.raises(HPError) as e:
+        stage(ctx, "CANNY", [None], [((8, 8), U8)], 8, 8)
+    assert e.value.status == 1
+
+
 def test_pipeline_config1(ctx):
     assert _check_pipeline(ctx, make_config_tile(1)) > 10
 
