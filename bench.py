@@ -65,13 +65,19 @@ def _gen(args):
         except Exception:  # noqa: BLE001
             pass
     rgb = make_tile(seed, TileSpec(size, size))["rgb"]
-    np.save(fn + ".tmp.npy", rgb)
-    os.replace(fn + ".tmp.npy", fn)
+    tmp = f"{fn}.{os.getpid()}.tmp.npy"  # per process: ranks may generate the same tile at once
+    np.save(tmp, rgb)
+    os.replace(tmp, fn)
     return rgb
 
 
 def make_tiles(rank, batch, size):
-    seeds = [1000 + rank * batch + i for i in range(batch)]   # configs[2] pool seeds
+    # configs[2] pool seeds.  Every rank gets the SAME tiles: weak scaling with identical
+    # per-GPU work (tile content varies ~5x in reconstruction cost, and the max-over-ranks
+    # timer would otherwise measure the unluckiest rank's draw); the e2e leg shares one
+    # demand-driven queue across ranks instead.
+    del rank
+    seeds = [1000 + i for i in range(batch)]
     nproc = max(1, min(len(seeds), (os.cpu_count() or 2) // max(1, env_int("LOCAL_WORLD_SIZE", 1))))
     ctx = mp.get_context("fork")
     with ctx.Pool(nproc) as pool:
@@ -201,7 +207,7 @@ def main():
               "batch_per_gpu": args.batch, "slots": args.slots, "e2e_slots": max(args.slots, args.e2e_slots),
               "l2": "inputs larger than L2 (each step reads %d distinct tiles = %.0f MB)"
                     % (args.batch, args.batch * 3 * args.size * args.size / 1e6),
-              "parallelism": f"tiles sharded over {world} GPU(s), no data-path collective"}
+              "parallelism": f"tiles sharded over {world} GPU(s), no data-path collective; every rank times the same {args.batch} tiles"}
 
     if args.impl == "reference":
         if rank != 0:

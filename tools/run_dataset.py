@@ -31,8 +31,9 @@ def pool_tile(config, k):
     if os.path.exists(fn):
         return np.load(fn)
     rgb = make_config_tile(config, k)
-    np.save(fn + ".tmp.npy", rgb)
-    os.replace(fn + ".tmp.npy", fn)
+    tmp = f"{fn}.{os.getpid()}.tmp.npy"  # per process: ranks may generate the same tile at once
+    np.save(tmp, rgb)
+    os.replace(tmp, fn)
     return rgb
 
 
