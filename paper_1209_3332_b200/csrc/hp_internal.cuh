@@ -73,10 +73,6 @@ struct Slot {
     Worklist wl;
     // objects
     int32_t *obj_root, *obj_bbox, *obj_rank;
-    // F components (k_comp.cu): root list, bounding boxes, root -> component id plane
-    int32_t* comp_root;
-    int4* comp_bbox;
-    int32_t* comp_big;  // components whose window needs a whole block (k_comp.cu)
     int32_t* cs_edge;    // k_ccls.cu: per 32x32 tile, the roots of its 4 x 32 edge pixels
     int32_t* cs_roots;   // k_ccls.cu: per tile, its local roots (up to 1024)
     int32_t* cs_nroots;  // k_ccls.cu: per tile, number of local roots
@@ -84,19 +80,19 @@ struct Slot {
     int32_t* sc_root;
     int4* sc_bbox;
     int32_t* sc_area;
-    int32_t* sc_big;
+    int32_t* sc_big;       // components whose window needs a whole block
     int32_t* sc_huge;      // components whose window exceeds shared memory
     // global-memory window storage for those (k_comp.cu CompGm), big_px pixels per plane
     uint8_t* big_scratch;
     int64_t big_px;
-    int32_t* cid;
-    int32_t comp_cap;
-    // staging table of the fused S8-S11 path (rows in discovery order)
+    int32_t comp_cap;      // capacity of the component lists (N / 4 + 16)
+    // staging table of the fused S7-S11 path (rows in discovery order)
     int32_t *stg_label, *stg_flags;
     float* stg_feat;
     // small device counters: [0] bg count (u64), [1] any-bg flag, [2] n objects, ...
     unsigned long long* counters;
-    int32_t* cnt32;  // [1] edt any-bg, [2] features count, [4] run_tiles n_objects, [8..11] k_comp
+    int32_t* cnt32;  // 32 ints: [1] edt any-bg, [2] features count, [4] run_tiles n_objects,
+                     // [8..15] k_comp (S7-S11 queues), [16] S5 component count, [18..21] S6 queues
     // run_tiles staging
     uint8_t* rgb_dev;
     int32_t* lab_dev;

@@ -1,22 +1,27 @@
-// k_comp.cu -- S8 markers + S9 watershed + S10 BWLabel (+ S11 features) of the pipeline,
-// one CTA per 8-connected component of F (objects are a bag of tasks).
+// k_comp.cu -- the pipeline's per-component stages, S6 and S7-S11 (PAPER.md:598-604,
+// 223-224: objects are a bag of tasks).
 //
-// Every step of S8-S10 (readings C12/C13) is a fixed point over the graph of
-// N8 neighbours INSIDE F, so the 8-connected components of F are independent problems.  The
-// global path (k_ws.cu + the tile worklists of k_iwpp.cu, kept for hp_stage_run) pays ~25
-// launches and three device-wide worklists per tile for objects of ~100-1000 pixels; here one
-// CTA owns one component:
-//   shared-memory path (k_comp_fused) -- one WARP per component for windows (bbox + 1-px
-//     ring) <= 576 px (~99% of nuclei; warp-synchronous, 16 components in flight per SM), one
-//     4-warp block for <= 2432 px: the window is staged in smem
-//     (membership, dist); the max-clamp / min-plus / min relaxations (J, W1, W2, W3) iterate
-//     to their fixed points with __syncthreads_or convergence; flat zones and the final
-//     objects are labelled by union-find in smem (CAS hooking, min-index roots); then the
-//     S11 features of each kept object are computed in the same CTA (feat_common.cuh);
-//   global fallback (bigger components): the same relaxations on the slot's global planes
-//     (any size), objects listed for k_obj_feat_list.
-// Rows from both paths land in a staging table and k_rows_scatter orders them by label.
-// Every relaxation is monotone toward a unique fixed point, so the result equals the oracle's.
+// From S6 on every step is local to connected components: a hole of FillHoles is bounded by
+// ONE 8-connected candidate component, so it lies in that component's bounding box; every
+// step of S7-S10 (readings C11-C13) is a fixed point over the N8 neighbours
+// INSIDE F; S11 is per object.  S5 (k_ccls.cu) lists the kept candidate components (root =
+// minimum linear index, bounding box, area); two launches then solve them in windows (bbox +
+// 1-px ring), taken off dynamic queues -- one WARP per window <= 576 px (~99% of nuclei), one
+// 4-warp block per window <= 2432 px, in shared memory; bigger windows (and object-list
+// overflows) in one block over global-memory scratch with the same code (the solvers are
+// templated on the window storage):
+//   k_fill_fused  S6: A = the component (8-connected union-find among the window's candidate
+//                 pixels, skipped when the window holds exactly its area); holes from the
+//                 Euler number (bit-quads) or a 4-connected union-find of the rest seeded at
+//                 the ring / tile border; F |= A | holes, each F pixel's word atomicMin(root)
+//                 (an island enclosed in a hole resolves to its encloser, as a CCL of F
+//                 would), enclosed candidates marked in enc;
+//   k_comp_fused  S7-S11 per component not in enc: members = pixels whose word is the root;
+//                 exact EDT by brute force over the window's boundary pixels; J, flat zones,
+//                 RMAX, markers, W1-W3, lines, BWLabel by monotone relaxations / union-find in
+//                 shared memory; the 36 features of each kept object (feat_common.cuh).
+// Rows land in a staging table and k_rows_scatter orders them by label.  Every relaxation is
+// monotone toward a unique fixed point, so the result equals the oracle's.
 #include <climits>
 
 #include "feat_common.cuh"
