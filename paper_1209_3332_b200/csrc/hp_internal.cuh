@@ -208,7 +208,7 @@ void launch_watershed(const float* dist, const int32_t* ML, const uint8_t* F, in
 // S10
 void launch_bwlabel(const uint8_t* split, int w, int h, int amin, int amax, Slot& sl,
                     int32_t* labels, int64_t lpitch, int32_t* n_objects, cudaStream_t s);
-// S8-S10 fused per F component (k_comp.cu)
+// S7-S11 per F component from the S5 list (k_comp.cu); edge = Canny plane (features only)
 void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t* g, const uint8_t* edge, float hh,
                        int amin, int amax, int w, int h, Slot& sl, int32_t* labels, int64_t lpitch,
                        int32_t* n_objects, const hp_feature_table* table, int32_t max_objects, cudaStream_t s);

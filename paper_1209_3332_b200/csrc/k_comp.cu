@@ -804,8 +804,8 @@ __global__ void k_copy_i32(const int32_t* __restrict__ src, int32_t* __restrict_
 
 }  // namespace
 
-// S8-S10 (+ S11 when table != nullptr) of the pipeline on F and dist: labels (zeroed here),
-// n_objects, and the feature rows in label order.
+// Outputs: labels (zeroed here), n_objects, and (when table != nullptr) the feature rows in
+// label order.
 // S7-S11 per F component, from the S5 component list: the F component of a kept candidate
 // component A is A with its holes and any islands inside them -- the pixels whose root word
 // (written by S6) is A's root.  Islands enclosed by another component (enc at their root) are

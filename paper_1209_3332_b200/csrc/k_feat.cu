@@ -8,8 +8,8 @@
 //   k_obj_feat   one CTA per object (grid-stride over the device-side count): exact
 //                integer sums (area, moments, perimeter, 256-bin histogram and 8x8 GLCM in
 //                shared memory via smem atomics), Sobel magnitude on the fly with fp64
-//                two-pass moments in a fixed reduction order (deterministic), then one
-//                thread finalises the 34 features in fp64 and stores them as f32.
+//                two-pass moments in a fixed reduction order (deterministic), Canny edge
+//                counts, then the team finalises the 36 features in fp64 (stored as f32).
 // Compiled with -fmad=false so the fp64 finaliser rounds like its written formulas.
 #include <cfloat>
 #include <cmath>
