@@ -131,7 +131,7 @@ hp_status   hp_ctx_create(const hp_config* cfg, hp_ctx** out);
 hp_status   hp_ctx_destroy(hp_ctx* ctx);
 const char* hp_status_str(hp_status st);
 const char* hp_last_error(const hp_ctx* ctx);   /* ctx-local message, never NULL */
-int32_t     hp_version(void);                   /* ABI version, currently 1 */
+int32_t     hp_version(void);                   /* ABI version, currently 2 (2: hp_result_sink.arena) */
 
 /* Segmentation stage (S1..S10) of one tile.  rgb: device image.  out: device labels. */
 hp_status hp_segment_tile(hp_ctx* ctx, int32_t slot, const hp_image* rgb, hp_labels* out,
@@ -157,10 +157,30 @@ typedef struct hp_tile_source {
     void*   user;
     int32_t width, height;
 } hp_tile_source;
+/* Device row arena (S12, PAPER.md:566-571 download phase; SURVEY §8(a) S12 "feature rows
+ * are appended to the device arena, or D2H per tile").  All pointers are DEVICE memory
+ * owned by the caller.  Each tile's rows (at most max_objects, in label order) are appended
+ * as one contiguous run at *cursor (reserved with one device atomic), with the tile id in
+ * tile[].  Runs of different tiles land in completion order, so a caller that needs a
+ * fixed order sorts by (tile, label).  cursor: one int64, caller-initialised (normally 0);
+ * it ends at the number of rows offered, which may exceed capacity -- rows past capacity are
+ * dropped and their tile is reported with HP_ERR_CAPACITY. */
+typedef struct hp_row_arena {
+    int64_t* tile;        /* [capacity] tile id of each row */
+    int32_t* label;       /* [capacity] */
+    int32_t* flags;       /* [capacity] HP_OBJ_* bits */
+    float*   feat;        /* [capacity][HP_NFEAT] row-major */
+    int64_t  capacity;
+    int64_t* cursor;      /* one int64 (device): append position */
+} hp_row_arena;
+/* arena == NULL: rows are copied to the host per tile and done() receives them.  arena !=
+ * NULL: rows stay on the device (appended to the arena); done() receives n_rows and NULL row
+ * pointers, and only 12 bytes per tile (row count, arena offset) cross PCIe. */
 typedef struct hp_result_sink {
     void (*done)(void* user, int64_t tile_id, int32_t n_rows, const int32_t* label,
                  const int32_t* flags, const float* feat, hp_status st);
     void* user;
+    const hp_row_arena* arena;  /* ABI version 2 */
 } hp_result_sink;
 hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_sink* sink);
 

@@ -52,7 +52,7 @@ struct hp_ctx {
 
 namespace {
 
-constexpr int kAbiVersion = 1;
+constexpr int kAbiVersion = 2;
 constexpr int kRowsAsync = 4096;
 constexpr int kRing = 256;
 
@@ -380,7 +380,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.sc_huge = (int32_t*)A(4 * (size_t)s.comp_cap);
         s.big_px = (int64_t)(cfg->max_width + 2) * (cfg->max_height + 2);
         s.big_scratch = (uint8_t*)A(28 * (size_t)s.big_px);
-        s.counters = (unsigned long long*)A(8 * 4);
+        s.counters = (unsigned long long*)A(8 * 8);
         s.cnt32 = (int32_t*)A(4 * 32);
         s.stg_label = (int32_t*)A(4 * (size_t)mo);
         s.stg_flags = (int32_t*)A(4 * (size_t)mo);
@@ -395,10 +395,11 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.h_flags = (int32_t*)halloc(4 * (size_t)mo);
         s.h_feat = (float*)halloc(4 * (size_t)mo * HP_NFEAT);
         s.h_nrows = (int32_t*)halloc(16);
+        s.h_arena = (int64_t*)halloc(16);
         void* all[] = {s.g, s.flags, s.rbc, s.u8a, s.u8b, s.cand, s.big0, s.F, s.split, s.pmask, s.lab, s.aux,
                        s.ML, s.d, s.L, s.dist, s.J, s.c, s.gcol, s.seg_top, s.seg_bot, s.wl.state, s.wl.inrows, s.wl.queue,
                        s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.cs_edge, s.cs_roots, s.cs_nroots, s.sc_root, s.sc_bbox, s.sc_area, s.sc_big, s.sc_huge, s.big_scratch, s.stg_label, s.stg_flags, s.stg_feat, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
-                       s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows};
+                       s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows, s.h_arena};
         for (void* p : all)
             if (!p) { hp_ctx_destroy(ctx); return HP_ERR_NOMEM; }
         int prio_lo = 0, prio_hi = 0;
@@ -411,7 +412,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
             hp_ctx_destroy(ctx);
             return HP_ERR_CUDA;
         }
-        cudaMemset(s.counters, 0, 32);
+        cudaMemset(s.counters, 0, 64);
         cudaMemset(s.cnt32, 0, 128);
         cudaMemset(s.wl.ctr, 0, 64);
     }
@@ -667,6 +668,18 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
     if (w < 1 || h < 1 || w > ctx->cfg.max_width || h > ctx->cfg.max_height) return HP_ERR_INVALID;
     const int ns = ctx->cfg.n_slots;
     const int mo = ctx->cfg.max_objects;
+    const hp_row_arena* arena = sink->arena;
+    if (arena && (!arena->tile || !arena->label || !arena->flags || !arena->feat || !arena->cursor ||
+                  arena->capacity < 0)) {
+        set_err(ctx, "run_tiles: arena with a NULL buffer or negative capacity");
+        return HP_ERR_INVALID;
+    }
+    const hp_row_arena no_arena{};
+    const hp_row_arena& akey = arena ? *arena : no_arena;
+    auto same_arena = [&](const hp_row_arena& a) {
+        return a.tile == akey.tile && a.label == akey.label && a.flags == akey.flags && a.feat == akey.feat &&
+               a.capacity == akey.capacity && a.cursor == akey.cursor;
+    };
     std::vector<int64_t> tile_of(ns, -1);
     std::vector<hp_status> st_of(ns, HP_OK);
     bool drained = false;
@@ -679,6 +692,13 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
         hp_status ts = st_of[i];
         if (nrows > mo) ts = HP_ERR_CAPACITY;
         int nr = std::min(nrows, mo);
+        if (arena) {  // rows stay in the device arena; the run [h_arena[1], +nr) may be clipped
+            if (sl.h_arena[1] + nr > arena->capacity) ts = HP_ERR_CAPACITY;
+            sink->done(sink->user, tile_of[i], nr, nullptr, nullptr, nullptr, ts);
+            tile_of[i] = -1;
+            --inflight;
+            return HP_OK;
+        }
         if (nr > ctx->rows_copied) {  // rare: more rows than the async window
             int extra = nr - ctx->rows_copied;
             cudaMemcpy(sl.h_label + ctx->rows_copied, sl.tab_label + ctx->rows_copied, 4 * (size_t)extra, cudaMemcpyDeviceToHost);
@@ -704,6 +724,7 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
         if (!host || pitch < 3LL * w) return HP_ERR_INVALID;
         Slot& sl = ctx->slots[i];
         cudaStream_t s = sl.stream;
+        sl.h_arena[0] = tid;  // read by this tile's H2D (arena mode); the slot's previous tile was delivered
         cudaMemcpy2DAsync(sl.rgb_dev, 3 * (size_t)w, host, (size_t)pitch, 3 * (size_t)w, h, cudaMemcpyHostToDevice, s);
         hp_image im{sl.rgb_dev, w, h, 3LL * w};
         hp_feature_table tab{sl.tab_label, sl.tab_flags, sl.tab_feat, mo, sl.tab_nrows};
@@ -714,6 +735,15 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
             if (!r && !fused) r = features(ctx, sl, w, h, sl.lab_dev, w, &tab, s);
             if (r) return r;
             cudaMemcpyAsync(sl.h_nrows, sl.tab_nrows, 4, cudaMemcpyDeviceToHost, s);
+            if (arena) {  // S12 into the device arena: the tile id goes up, the run offset down
+                int64_t* dev_tid = (int64_t*)&sl.counters[4];
+                int64_t* dev_base = (int64_t*)&sl.counters[5];
+                cudaMemcpyAsync(dev_tid, &sl.h_arena[0], 8, cudaMemcpyHostToDevice, s);
+                launch_arena_append(sl.tab_nrows, mo, sl.tab_label, sl.tab_flags, sl.tab_feat, dev_base, dev_tid,
+                                    *arena, s);
+                cudaMemcpyAsync(&sl.h_arena[1], dev_base, 8, cudaMemcpyDeviceToHost, s);
+                return HP_OK;
+            }
             cudaMemcpyAsync(sl.h_label, sl.tab_label, 4 * (size_t)ctx->rows_copied, cudaMemcpyDeviceToHost, s);
             cudaMemcpyAsync(sl.h_flags, sl.tab_flags, 4 * (size_t)ctx->rows_copied, cudaMemcpyDeviceToHost, s);
             cudaMemcpyAsync(sl.h_feat, sl.tab_feat, 4 * (size_t)ctx->rows_copied * HP_NFEAT, cudaMemcpyDeviceToHost, s);
@@ -726,9 +756,10 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
         const bool graphable = ctx->graphs && !ctx->timing && ctx->cfg.params.bg_skip_frac > 1.0f &&
                                ctx->prio == 0;
         hp_status r = HP_OK;
-        if (graphable && sl.gexec && sl.graph_w == w && sl.graph_h == h) {
+        const bool same = sl.graph_w == w && sl.graph_h == h && same_arena(sl.graph_arena);
+        if (graphable && sl.gexec && same) {
             if (cudaGraphLaunch(sl.gexec, s) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "graph launch");
-        } else if (graphable && sl.graph_w == w && sl.graph_h == h) {
+        } else if (graphable && same) {
             cudaGraph_t g = nullptr;
             if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
                 return cuda_fail(ctx, cudaGetLastError(), "begin capture");
@@ -747,6 +778,7 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
             }
             sl.graph_w = w;
             sl.graph_h = h;
+            sl.graph_arena = akey;
         }
         cudaEventRecord(sl.done_ev, s);
         if ((r = check_launch(ctx, "run_tiles"))) return r;

@@ -89,7 +89,8 @@ struct Slot {
     // staging table of the fused S7-S11 path (rows in discovery order)
     int32_t *stg_label, *stg_flags;
     float* stg_feat;
-    // small device counters: [0] bg count (u64), [1] any-bg flag, [2] n objects, ...
+    // small device counters (8 x u64): [0] bg count, [1] any-bg flag, [2] n objects,
+    // [4] run_tiles arena tile id, [5] run_tiles arena offset
     unsigned long long* counters;
     int32_t* cnt32;  // 32 ints: [1] edt any-bg, [2] features count, [4] run_tiles n_objects,
                      // [8..15] k_comp (S7-S11 queues), [16] S5 component count, [18..21] S6 queues
@@ -102,10 +103,14 @@ struct Slot {
     // pinned host staging for run_tiles results
     int32_t *h_label, *h_flags, *h_nrows;
     float* h_feat;
+    // arena mode: h_arena[0] tile id (H2D into counters[4] each tile), h_arena[1] the run's
+    // arena offset (D2H from counters[5])
+    int64_t* h_arena;
     cudaEvent_t done_ev;
     // hp_run_tiles: the per-tile chain (compute + D2H) captured once as a CUDA graph
     cudaGraphExec_t gexec;
     int graph_w, graph_h;
+    hp_row_arena graph_arena;  // the arena the graph was captured with (all zero: host rows)
     // high-priority side stream for the latency-bound stages (hp_ctx::prio)
     cudaStream_t hstream;
     cudaEvent_t fork_ev, join_ev;
@@ -216,6 +221,11 @@ void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t*
 // per-image aggregation (k_agg.cu): segmented fp64 sums / sums of squares of feature rows
 void launch_reduce_rows(const float* feat, const int64_t* off, int32_t n_groups, double* out, int64_t* count,
                         cudaStream_t s);
+// device row arena of hp_run_tiles (k_agg.cu): reserve min(*nrows, tab_cap) rows at a.cursor
+// (offset -> *base), then copy the tile's rows with tile id *tile_id, clipped to capacity
+void launch_arena_append(const int32_t* nrows, int32_t tab_cap, const int32_t* lab, const int32_t* fl,
+                         const float* feat, int64_t* base, const int64_t* tile_id, const hp_row_arena& a,
+                         cudaStream_t s);
 // Feature-stage Canny (k_ccls.cu): edges 0/1 = cv2.Canny(g, low, high), reading C22
 void launch_canny(const uint8_t* g, int w, int h, int low, int high, Slot& sl, uint8_t* edges, cudaStream_t s);
 void launch_features(const int32_t* labels, int64_t lpitch, const uint8_t* g, const uint8_t* edge, int w, int h,

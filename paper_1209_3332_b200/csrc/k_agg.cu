@@ -2,6 +2,8 @@
 // fp64 reduction of feature rows, one block per group, every thread owning a fixed set of
 // rows and the block combining its partials by a fixed tree -- deterministic.  The rows of a
 // group are contiguous (a rank's table is in tile order and tiles map to slides in order).
+#include <algorithm>
+
 #include "hp_internal.cuh"
 
 namespace hp {
@@ -53,6 +55,50 @@ void launch_reduce_rows(const float* feat, const int64_t* off, int32_t n_groups,
     static_assert(HP_NFEAT % kAF == 0, "features per pass");
     if (n_groups == 0) return;
     (note_launch(), k_reduce_rows<<<n_groups, kAT, 0, s>>>(feat, off, out, count));
+}
+
+}  // namespace hp
+
+// ---------------------------------------------------------------- device row arena (S12)
+// hp_run_tiles with an hp_row_arena: the tile's rows stay on the device and are appended as
+// one run.  Two launches in the slot's chain (both captured in its graph): one thread
+// reserves the run (one atomicAdd on the caller's cursor) and records the offset; then a
+// grid copies the rows, coalesced, clipped to the arena's capacity.
+namespace hp {
+namespace {
+
+__global__ void k_arena_reserve(const int32_t* __restrict__ nrows, int32_t tab_cap, int64_t* cursor,
+                                int64_t* __restrict__ base) {
+    const int64_t n = min(*nrows, tab_cap);
+    *base = (int64_t)atomicAdd((unsigned long long*)cursor, (unsigned long long)n);
+}
+
+__global__ void k_arena_copy(const int32_t* __restrict__ nrows, int32_t tab_cap, const int32_t* __restrict__ lab,
+                             const int32_t* __restrict__ fl, const float* __restrict__ feat,
+                             const int64_t* __restrict__ base_p, const int64_t* __restrict__ tile_id,
+                             hp_row_arena a) {
+    const int64_t n = min(*nrows, tab_cap);
+    const int64_t base = *base_p;
+    const int64_t m = max((int64_t)0, min(n, a.capacity - base));  // rows that fit
+    const int64_t tid = *tile_id;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += stride) {
+        a.tile[base + i] = tid;
+        a.label[base + i] = lab[i];
+        a.flags[base + i] = fl[i];
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m * HP_NFEAT; i += stride)
+        a.feat[base * HP_NFEAT + i] = feat[i];
+}
+
+}  // namespace
+
+void launch_arena_append(const int32_t* nrows, int32_t tab_cap, const int32_t* lab, const int32_t* fl,
+                         const float* feat, int64_t* base, const int64_t* tile_id, const hp_row_arena& a,
+                         cudaStream_t s) {
+    (note_launch(), k_arena_reserve<<<1, 1, 0, s>>>(nrows, tab_cap, a.cursor, base));
+    const int grid = std::max(1, std::min(148, (int)(((int64_t)tab_cap * HP_NFEAT + 1023) / 1024)));
+    (note_launch(), k_arena_copy<<<grid, 256, 0, s>>>(nrows, tab_cap, lab, fl, feat, base, tile_id, a));
 }
 
 }  // namespace hp

@@ -107,8 +107,15 @@ class TileSource(C.Structure):
                 ("height", C.c_int32)]
 
 
+class RowArena(C.Structure):
+    """hp_row_arena: device pointers (tile i64[cap], label i32[cap], flags i32[cap],
+    feat f32[cap][36]), capacity, cursor (one device i64)."""
+    _fields_ = [("tile", C.c_void_p), ("label", C.c_void_p), ("flags", C.c_void_p),
+                ("feat", C.c_void_p), ("capacity", C.c_int64), ("cursor", C.c_void_p)]
+
+
 class ResultSink(C.Structure):
-    _fields_ = [("done", DONE_FN), ("user", C.c_void_p)]
+    _fields_ = [("done", DONE_FN), ("user", C.c_void_p), ("arena", C.POINTER(RowArena))]
 
 
 _lib = None
@@ -273,10 +280,13 @@ class Context:
         self._chk(lib().hp_stage_times_accum(self._h, ms, C.byref(n)), "hp_stage_times_accum")
         return list(ms), int(n.value)
 
-    def run_tiles(self, next_tile, on_done, width, height):
+    def run_tiles(self, next_tile, on_done, width, height, arena=None):
         """Demand-driven driver.  next_tile() -> (host_ptr:int, pitch:int, tile_id:int) or
         None when drained; host memory must be pinned and stay valid until on_done for that
-        tile.  on_done(tile_id, label[n], flags[n], feat[n, 36], status) gets numpy COPIES."""
+        tile.  on_done(tile_id, label[n], flags[n], feat[n, 36], status) gets numpy COPIES.
+        With arena = (tile_ptr, label_ptr, flags_ptr, feat_ptr, capacity, cursor_ptr) (device
+        pointers, hp_row_arena) the rows are appended on the device instead and
+        on_done(tile_id, n_rows, status) is called."""
         keep = []
 
         def _next(user, pp, ppitch, ptid):
@@ -293,6 +303,9 @@ class Context:
             return 0
 
         def _done(user, tid, n, plab, pflags, pfeat, st):
+            if arena is not None:
+                on_done(int(tid), int(n), int(st))
+                return
             lab = np.ctypeslib.as_array(plab, shape=(max(n, 1),))[:n].copy()
             fl = np.ctypeslib.as_array(pflags, shape=(max(n, 1),))[:n].copy()
             ft = np.ctypeslib.as_array(pfeat, shape=(max(n, 1) * NFEAT,))[:n * NFEAT].copy()
@@ -301,5 +314,7 @@ class Context:
         nf, df = NEXT_FN(_next), DONE_FN(_done)
         keep += [nf, df]
         src = TileSource(nf, None, width, height)
-        sink = ResultSink(df, None)
+        ar = None if arena is None else RowArena(*arena)
+        sink = ResultSink(df, None, C.pointer(ar) if ar is not None else None)
+        keep.append(ar)
         self._chk(lib().hp_run_tiles(self._h, C.byref(src), C.byref(sink)), "hp_run_tiles")

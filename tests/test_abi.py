@@ -27,7 +27,7 @@ def test_exports_match_header():
     assert set(decl) == set(hp.EXPORTS), decl
     for name in decl:
         assert hasattr(L, name), name
-    assert L.hp_version() == 1
+    assert L.hp_version() == 2
 
 
 def test_default_params_agree_with_oracle():

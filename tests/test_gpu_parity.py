@@ -546,3 +546,103 @@ def test_run_tiles(ctx):
     for i, rgb in enumerate(tiles):
         _, ol, of, ot = oracle.process_tile(rgb)
         assert_features_equal(got[i][0], got[i][1], got[i][2], ol, of, ot)
+
+
+def _arena(torch, cap):
+    from paper_1209_3332_b200.hp import NFEAT
+    dev = "cuda"
+    a = dict(tile=torch.full((cap,), -1, dtype=torch.int64, device=dev),
+             label=torch.zeros(cap, dtype=torch.int32, device=dev),
+             flags=torch.zeros(cap, dtype=torch.int32, device=dev),
+             feat=torch.zeros(cap, NFEAT, dtype=torch.float32, device=dev),
+             cursor=torch.zeros(1, dtype=torch.int64, device=dev))
+    ptrs = (a["tile"].data_ptr(), a["label"].data_ptr(), a["flags"].data_ptr(),
+            a["feat"].data_ptr(), cap, a["cursor"].data_ptr())
+    return a, ptrs
+
+
+def test_run_tiles_arena(ctx):
+    """S12 into the device arena: every tile's rows land as one contiguous run tagged with
+    its tile id; after sorting by (tile, label) the table is the oracle's.  Tiles repeat
+    (the per-slot graph is captured and replayed with the arena) and a second call with the
+    same arena continues at the cursor."""
+    import torch
+    tiles = [make_tile(300 + i, TileSpec(384, 448))["rgb"] for i in range(5)]
+    pinned = [torch.from_numpy(t).pin_memory() for t in tiles]
+    ref = [oracle.process_tile(rgb)[1:] for rgb in tiles]
+    total = sum(len(r[0]) for r in ref)
+    a, ptrs = _arena(torch, 4 * total + 8)
+    counts = {}
+    for call in range(2):
+        ids = [(call, i) for i in range(len(tiles))] * 2
+        it = iter(ids)
+
+        def nxt():
+            try:
+                c, i = next(it)
+            except StopIteration:
+                return None
+            return pinned[i].data_ptr(), 3 * 448, 10 * c + i
+
+        def done(tid, n, st):
+            assert st == 0
+            counts.setdefault(tid, []).append(n)
+
+        ctx.run_tiles(nxt, done, 448, 384, arena=ptrs)
+    torch.cuda.synchronize()
+    n = int(a["cursor"].item())
+    assert n == 4 * total
+    tile = a["tile"][:n].cpu().numpy()
+    lab = a["label"][:n].cpu().numpy()
+    fl = a["flags"][:n].cpu().numpy()
+    ft = a["feat"][:n].cpu().numpy()
+    assert int(a["tile"][n:].cpu().numpy().max(initial=-1)) == -1  # nothing past the cursor
+    assert sorted(counts) == sorted(10 * c + i for c in range(2) for i in range(len(tiles)))
+    for tid, ns in counts.items():
+        i = tid % 10
+        m = len(ref[i][0])
+        assert ns == [m, m]
+        idx = np.flatnonzero(tile == tid)
+        assert len(idx) == 2 * m
+        # each delivery is one contiguous run in label order, equal to the oracle's table
+        runs = np.split(idx, np.flatnonzero(np.diff(idx) != 1) + 1)
+        runs = [r for run in runs for r in np.split(run, range(m, len(run), m))] if m else []
+        assert len(runs) == (2 if m else 0)
+        for r in runs:
+            assert len(r) == m and np.array_equal(r, np.arange(r[0], r[0] + m))
+            assert_features_equal(lab[r], fl[r], ft[r], *ref[i])
+
+
+def test_run_tiles_arena_overflow(ctx):
+    """An arena smaller than the rows: the cursor still counts every row, rows past the
+    capacity are dropped, and the tiles whose run did not fit report HP_ERR_CAPACITY."""
+    import torch
+    tiles = [make_tile(320 + i, TileSpec(384, 448))["rgb"] for i in range(4)]
+    pinned = [torch.from_numpy(t).pin_memory() for t in tiles]
+    nref = [len(oracle.process_tile(rgb)[1]) for rgb in tiles]
+    cap = sum(nref) // 2
+    a, ptrs = _arena(torch, cap)
+    it = iter(range(len(tiles)))
+    sts = {}
+
+    def nxt():
+        try:
+            i = next(it)
+        except StopIteration:
+            return None
+        return pinned[i].data_ptr(), 3 * 448, i
+
+    def done(tid, n, st):
+        sts[tid] = (n, st)
+
+    ctx.run_tiles(nxt, done, 448, 384, arena=ptrs)
+    torch.cuda.synchronize()
+    assert int(a["cursor"].item()) == sum(nref)
+    assert {t: v[0] for t, v in sts.items()} == dict(enumerate(nref))
+    tile = a["tile"].cpu().numpy()
+    assert (tile >= 0).all()  # the arena is full
+    kept = np.bincount(tile, minlength=len(tiles))
+    for t, (n, st) in sts.items():
+        assert (st == 0) == (kept[t] == n), (t, n, st, kept[t])
+        assert st in (0, 4)
+    assert any(st == 4 for _, st in sts.values())
