@@ -646,3 +646,61 @@ def test_run_tiles_arena_overflow(ctx):
         assert (st == 0) == (kept[t] == n), (t, n, st, kept[t])
         assert st in (0, 4)
     assert any(st == 4 for _, st in sts.values())
+
+
+def _pool_tile(seed):
+    import bench  # the bench's seeded tile cache (same seeds, same painter call)
+    return bench._gen((seed, 4096))
+
+
+def _oracle_digest(rgb):
+    import hashlib
+    olab, ol, of, ot = oracle.process_tile(rgb, cap=65536)
+    return hashlib.sha256(np.ascontiguousarray(olab).tobytes()).hexdigest(), ol, of, ot
+
+
+@pytest.mark.slow
+def test_bench_tiles_in_bench_launch_config():
+    """Parity at BASELINE's full size in the launch configuration bench.py times: the
+    bench's own 4K tiles (configs[2] pool seeds 1000..), six slots with one stream each and
+    all tiles in flight at once, against the oracle -- label planes bit-exact, tables within
+    reading C18.  HP_POOL_PARITY=N checks the first N pool tiles (default 6; 64 = the whole
+    configs[2] pool)."""
+    import hashlib
+    import multiprocessing as mp
+    import os
+
+    import torch
+    from paper_1209_3332_b200 import Context
+    K = int(os.environ.get("HP_POOL_PARITY", "6"))
+    S, size, cap = 6, 4096, 8192
+    c = Context(0, size, size, n_slots=S, max_objects=cap)
+    pctx = mp.get_context("fork")
+    nproc = max(1, min(S, os.cpu_count() or 1))
+    try:
+        lab = [torch.empty((size, size), dtype=torch.int32, device="cuda") for _ in range(S)]
+        nob = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(S)]
+        tl = [torch.empty(cap, dtype=torch.int32, device="cuda") for _ in range(S)]
+        tf = [torch.empty(cap, dtype=torch.int32, device="cuda") for _ in range(S)]
+        tt = [torch.empty((cap, 36), dtype=torch.float32, device="cuda") for _ in range(S)]
+        nr = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(S)]
+        streams = [torch.cuda.Stream() for _ in range(S)]
+        with pctx.Pool(nproc) as pool:
+            for b0 in range(0, K, S):
+                seeds = list(range(1000 + b0, 1000 + min(K, b0 + S)))
+                tiles = pool.map(_pool_tile, seeds)
+                ref = pool.map_async(_oracle_digest, tiles)   # oracle runs while the GPU does
+                dev = [torch.from_numpy(t).cuda() for t in tiles]
+                torch.cuda.synchronize()
+                for k in range(len(tiles)):
+                    c.process_tile(k, dev[k], lab[k], nob[k], tl[k], tf[k], tt[k], nr[k], stream=streams[k])
+                torch.cuda.synchronize()
+                for k, (odig, ol, of, ot) in enumerate(ref.get()):
+                    gl = lab[k].cpu().numpy()
+                    assert hashlib.sha256(gl.tobytes()).hexdigest() == odig, f"labels of seed {seeds[k]}"
+                    n = int(nr[k].item())
+                    assert int(nob[k].item()) == n == len(ol) > 1000
+                    assert_features_equal(tl[k][:n].cpu().numpy(), tf[k][:n].cpu().numpy(),
+                                          tt[k][:n].cpu().numpy(), ol, of, ot)
+    finally:
+        c.close()
