@@ -151,7 +151,10 @@ hp_status hp_process_tile(hp_ctx* ctx, int32_t slot, const hp_image* rgb, hp_lab
  * For each tile, done() is called (on the calling thread) with the tile's rows in HOST
  * memory owned by the context and valid only during the callback (n_rows <= max_objects
  * rows; st = HP_ERR_CAPACITY if the tile had more).  Up to n_slots tiles are in flight;
- * each slot runs H2D -> process -> D2H on its own stream.  Blocks until drained. */
+ * each slot runs H2D -> process -> D2H on its own stream.  Blocks until drained.  Errors: a
+ * NULL source/sink/callback or a size outside the context -> HP_ERR_INVALID before any work;
+ * a tile with a NULL pointer or pitch < 3*width -> HP_ERR_INVALID after the tiles already
+ * in flight have completed (they are not delivered). */
 typedef struct hp_tile_source {
     int   (*next)(void* user, const uint8_t** host_rgb, int64_t* pitch_bytes, int64_t* tile_id);
     void*   user;

@@ -663,9 +663,15 @@ hp_status hp_stage_run(hp_ctx* ctx, int32_t slot, hp_stage stage, const hp_stage
 hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_sink* sink) {
     hp_status st = enter(ctx, 0);
     if (st) return st;
-    if (!src || !src->next || !sink || !sink->done) return HP_ERR_INVALID;
+    if (!src || !src->next || !sink || !sink->done) {
+        set_err(ctx, "run_tiles: NULL source, sink or callback");
+        return HP_ERR_INVALID;
+    }
     const int w = src->width, h = src->height;
-    if (w < 1 || h < 1 || w > ctx->cfg.max_width || h > ctx->cfg.max_height) return HP_ERR_INVALID;
+    if (w < 1 || h < 1 || w > ctx->cfg.max_width || h > ctx->cfg.max_height) {
+        set_err(ctx, "run_tiles: tile size %dx%d outside 1..%dx%d", w, h, ctx->cfg.max_width, ctx->cfg.max_height);
+        return HP_ERR_INVALID;
+    }
     const int ns = ctx->cfg.n_slots;
     const int mo = ctx->cfg.max_objects;
     const hp_row_arena* arena = sink->arena;
@@ -721,7 +727,11 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
             drained = true;
             return HP_OK;
         }
-        if (!host || pitch < 3LL * w) return HP_ERR_INVALID;
+        if (!host || pitch < 3LL * w) {
+            set_err(ctx, "run_tiles: tile %lld has a NULL host pointer or pitch %lld < 3*width", (long long)tid,
+                    (long long)pitch);
+            return HP_ERR_INVALID;
+        }
         Slot& sl = ctx->slots[i];
         cudaStream_t s = sl.stream;
         sl.h_arena[0] = tid;  // read by this tile's H2D (arena mode); the slot's previous tile was delivered
@@ -787,10 +797,16 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
         ++inflight;
         return HP_OK;
     };
+    // on an error, wait for the tiles already in flight (their host buffers are the caller's)
+    auto abandon = [&](hp_status e) {
+        for (int i = 0; i < ns; ++i)
+            if (tile_of[i] >= 0) cudaEventSynchronize(ctx->slots[i].done_ev);
+        return e;
+    };
     int scan = 0;
     while (true) {
         for (int i = 0; i < ns && !drained; ++i)
-            if (tile_of[i] < 0 && (st = submit(i))) return st;
+            if (tile_of[i] < 0 && (st = submit(i))) return abandon(st);
         if (inflight == 0) break;
         int done = -1;
         for (int k = 0; k < ns && done < 0; ++k) {
@@ -798,14 +814,14 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
             if (tile_of[i] < 0) continue;
             const cudaError_t q = cudaEventQuery(ctx->slots[i].done_ev);
             if (q == cudaSuccess) done = i;
-            else if (q != cudaErrorNotReady) return cuda_fail(ctx, q, "run_tiles query");
+            else if (q != cudaErrorNotReady) return abandon(cuda_fail(ctx, q, "run_tiles query"));
         }
         if (done < 0) {
             std::this_thread::sleep_for(std::chrono::microseconds(20));
             continue;
         }
         scan = (done + 1) % ns;
-        if ((st = deliver(done))) return st;
+        if ((st = deliver(done))) return abandon(st);
     }
     return HP_OK;
 }

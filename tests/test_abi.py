@@ -87,3 +87,33 @@ def test_product_does_not_touch_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "oracle.h" not in src and "liboracle" not in src, f
+
+
+def test_struct_layouts_match_header(tmp_path):
+    """Every ctypes structure of the binding has the size and field offsets the C compiler
+    gives the same struct from include/hp.h (compiled here with gcc)."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    pairs = [("hp_params", hp.Params), ("hp_config", hp.Config), ("hp_image", hp.Image),
+             ("hp_labels", hp.Labels), ("hp_feature_table", hp.FeatureTable),
+             ("hp_stage_io", hp.StageIO), ("hp_tile_source", hp.TileSource),
+             ("hp_row_arena", hp.RowArena), ("hp_result_sink", hp.ResultSink)]
+    cname = {"in_": "in"}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "hp.h"', "int main(void) {"]
+    expect = []
+    for cs, py in pairs:
+        lines.append(f'printf("%zu\\n", sizeof({cs}));')
+        expect.append(C.sizeof(py))
+        for f, _ in py._fields_:
+            lines.append(f'printf("%zu\\n", offsetof({cs}, {cname.get(f, f)}));')
+            expect.append(getattr(py, f).offset)
+    lines += ["return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-std=c99", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert got == expect

@@ -704,3 +704,30 @@ def test_bench_tiles_in_bench_launch_config():
                                           tt[k][:n].cpu().numpy(), ol, of, ot)
     finally:
         c.close()
+
+
+def test_run_tiles_errors(ctx):
+    """hp_run_tiles argument errors: a size beyond the context and a bad tile pitch are
+    HP_ERR_INVALID (the bad tile after the good ones in flight finished, undelivered), an
+    arena with a NULL buffer is rejected; the context stays usable afterwards."""
+    import torch
+    from paper_1209_3332_b200.hp import HPError
+    rgb = make_tile(31, TileSpec(128, 160))["rgb"]
+    pinned = torch.from_numpy(rgb).pin_memory()
+    with pytest.raises(HPError) as e:
+        ctx.run_tiles(lambda: None, lambda *a: None, 8192, 64)
+    assert e.value.status == 1
+    seq = iter([(pinned.data_ptr(), 3 * 160, 0), (pinned.data_ptr(), 3 * 160, 1),
+                (pinned.data_ptr(), 3 * 160 - 1, 2)])
+    with pytest.raises(HPError) as e:
+        ctx.run_tiles(lambda: next(seq, None), lambda *a: None, 160, 128)
+    assert e.value.status == 1
+    with pytest.raises(HPError) as e:
+        ctx.run_tiles(lambda: None, lambda *a: None, 160, 128, arena=(0, 0, 0, 0, 10, 0))
+    assert e.value.status == 1
+    got = {}
+    seq = iter([(pinned.data_ptr(), 3 * 160, 7)])
+    ctx.run_tiles(lambda: next(seq, None), lambda t, l, f, x, s: got.setdefault(t, (l, f, x, s)), 160, 128)
+    _, ol, of, ot = oracle.process_tile(rgb)
+    assert got[7][3] == 0
+    assert_features_equal(got[7][0], got[7][1], got[7][2], ol, of, ot)
