@@ -60,6 +60,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HP_POLL_MAX_NS
 #define HP_POLL_MAX_NS 1600  // back-off cap (r1: 400-6400 within noise in bench.py)
 #endif
+#ifndef HP_RG_PACKSCAN
+#define HP_RG_PACKSCAN 0  // both scan directions at once on packed u16x2 clamps (r1: S4 0.78 -> 0.82 ms, bench 843 -> 834: off)
+#endif
 #ifndef HP_PPL
 #define HP_PPL 2  // pixels per lane: sub-tiles of 64 x 32 px, regions of 256 x 128 px
 #endif
@@ -128,6 +131,22 @@ __device__ __forceinline__ int clamp_scan(int lo, int hi, int lane) {
         hi = take ? nhi : hi;
     }
     return lo;
+}
+
+// Both directions at once with each clamp (lo, hi) packed as u16x2: per level one shuffle per
+// direction instead of two, the composition on the native VIMNMX.U16x2, and the two
+// directions' shuffle latencies overlapped.  F scans left -> right, B right -> left.
+__device__ __forceinline__ void clamp_scan_both(uint32_t& F, uint32_t& B, int lane) {
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t fo = __shfl_up_sync(FULL, F, off);
+        const uint32_t bo = __shfl_down_sync(FULL, B, off);
+        // this o other: (min(hi, max(lo, lo_o)), min(hi, max(lo, hi_o)))
+        const uint32_t fn = __vminu2(__vmaxu2(fo, __byte_perm(F, 0, 0x1010)), __byte_perm(F, 0, 0x3232));
+        const uint32_t bn = __vminu2(__vmaxu2(bo, __byte_perm(B, 0, 0x1010)), __byte_perm(B, 0, 0x3232));
+        if (lane >= off) F = fn;
+        if (lane + off < 32) B = bn;
+    }
 }
 
 __device__ __forceinline__ uint32_t load_word(const uint8_t* plane, int w, int h, int gx, int gy) {
@@ -260,14 +279,6 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                 FL = min(m[j], max(lo[j], FL));
                 FH = min(m[j], max(lo[j], FH));
             }
-            int in = __shfl_up_sync(FULL, clamp_scan<true>(FL, FH, lane), 1);
-            if (lane == 0) in = 0;
-            int fw[PPL];
-#pragma unroll
-            for (int j = 0; j < PPL; ++j) {
-                in = min(m[j], max(lo[j], in));
-                fw[j] = in;
-            }
             // right -> left
             int BL = lo[PPL - 1], BH = m[PPL - 1];
 #pragma unroll
@@ -275,8 +286,23 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                 BL = min(m[j], max(lo[j], BL));
                 BH = min(m[j], max(lo[j], BH));
             }
+#if HP_RG_PACKSCAN
+            uint32_t Fp = (uint32_t)FL | ((uint32_t)FH << 16), Bp = (uint32_t)BL | ((uint32_t)BH << 16);
+            clamp_scan_both(Fp, Bp, lane);
+            int in = __shfl_up_sync(FULL, (int)(Fp & 0xffffu), 1);
+            int ib = __shfl_down_sync(FULL, (int)(Bp & 0xffffu), 1);
+#else
+            int in = __shfl_up_sync(FULL, clamp_scan<true>(FL, FH, lane), 1);
             int ib = __shfl_down_sync(FULL, clamp_scan<false>(BL, BH, lane), 1);
+#endif
+            if (lane == 0) in = 0;
             if (lane == 31) ib = 0;
+            int fw[PPL];
+#pragma unroll
+            for (int j = 0; j < PPL; ++j) {
+                in = min(m[j], max(lo[j], in));
+                fw[j] = in;
+            }
 #pragma unroll
             for (int j = PPL - 1; j >= 0; --j) {
                 ib = min(m[j], max(lo[j], ib));
