@@ -148,7 +148,7 @@ def config5():
             ms = min(t)
             res.append({"case": f"{kind} {'ramp' if ramp else 'binary'}", "path_px": int(L), "ms": ms,
                         "ms_all": [round(x, 2) for x in t], "pixels_changed": changed,
-                        "updates_per_s": changed / (ms / 1e3), "jobs": int(st[0]), "sweep_iterations": int(st[1]),
+                        "updates_per_s": changed / (ms / 1e3), "jobs": int(st[0]), "sweep_iterations": int(st[1]), "owned_ns": int(st[2]), "stat3": int(st[3]),
                         "recon_eq_mask": bool(torch.equal(rec, mask))})
     ctx.close()
     return {"config": 5, "size": size, "cases": res,
