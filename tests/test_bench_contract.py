@@ -43,3 +43,27 @@ def test_reference_arm_torchrun_rank0_only():
     assert r.returncode == 0, r.stderr[-2000:]
     lines = _lines(r.stdout)
     assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2
+
+
+@pytest.mark.gpu
+def test_hp_arm_line():
+    """The GPU arm at a small size: the contract keys plus roofline, clocks, gpu_launches and
+    an e2e measured through hp_run_tiles with nonzero H2D/D2H bytes."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    r = subprocess.run([sys.executable, "bench.py", "--steps", "3", "--warmup", "3", "--batch", "4",
+                        "--slots", "2", "--e2e-slots", "2", "--size", "1024", "--no-cpu-baseline"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = _lines(r.stdout)
+    assert len(lines) == 1
+    d = lines[0]
+    assert (KEYS - {"impl", "cpu_baseline"}) <= set(d)
+    assert d["value"] > 0 and d["gpu_launches"] > 0
+    rf = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(rf)
+    assert rf["peak"] > 0 and abs(rf["frac"] - rf["achieved"] / rf["peak"]) < 1e-3
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 4 * 3 * 1024 * 1024
+    assert d["e2e"]["d2h_bytes_per_step"] > 0
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
