@@ -731,3 +731,72 @@ def test_run_tiles_errors(ctx):
     _, ol, of, ot = oracle.process_tile(rgb)
     assert got[7][3] == 0
     assert_features_equal(got[7][0], got[7][1], got[7][2], ol, of, ot)
+
+
+@pytest.mark.parametrize("case", ["small_disk", "strict", "loose"])
+def test_pipeline_nondefault_params(case):
+    """The same hp_params drive both sides: a non-default opening diameter, thresholds, area
+    bounds, h and Canny thresholds give the oracle's labels and rows."""
+    from paper_1209_3332_b200 import Context
+    from paper_1209_3332_b200.hp import Params as HParams
+    p = oracle.default_params()
+    if case == "small_disk":
+        p.open_diam, p.g1, p.h = 11, 40, 2.0
+    elif case == "strict":
+        p.cand_min_area, p.cand_max_area, p.obj_min_area, p.obj_max_area = 30, 400, 40, 300
+        p.canny_low, p.canny_high = 40, 90
+    else:
+        p.rbc_t1, p.rbc_t2, p.g1, p.h = 3, 2, 30, 0.5
+        p.canny_low, p.canny_high = 0, 0
+    rgb = make_tile(41, TileSpec(384, 512))["rgb"]
+    with Context(0, 512, 384, n_slots=1, max_objects=8192, params=HParams.from_dict(p.to_dict())) as c:
+        lab, nobj, gl, gf, gt = _gpu_process(c, rgb, cap=8192)
+    olab, ol, of, ot = oracle.process_tile(rgb, params=p)
+    assert np.array_equal(lab, olab) and nobj == len(ol)
+    assert_features_equal(gl, gf, gt, ol, of, ot)
+
+
+def test_background_skip():
+    """bg_skip_frac <= 1 (reading C19): a tile whose BG fraction reaches it yields no
+    objects on both sides; a tissue tile below it is processed as usual."""
+    from paper_1209_3332_b200 import Context
+    from paper_1209_3332_b200.hp import Params as HParams
+    p = oracle.default_params()
+    p.bg_skip_frac = 0.5
+    glass = make_tile(43, TileSpec(256, 256, tissue_frac=0.2))["rgb"]   # mostly glass
+    tissue = make_tile(44, TileSpec(256, 256))["rgb"]
+    with Context(0, 256, 256, n_slots=1, max_objects=4096, params=HParams.from_dict(p.to_dict())) as c:
+        for rgb in (glass, tissue):
+            lab, nobj, gl, gf, gt = _gpu_process(c, rgb, cap=4096)
+            olab, ol, of, ot = oracle.process_tile(rgb, params=p)
+            assert np.array_equal(lab, olab) and nobj == len(ol)
+            assert_features_equal(gl, gf, gt, ol, of, ot)
+    assert len(oracle.process_tile(glass, params=p)[1]) == 0
+    assert len(oracle.process_tile(tissue, params=p)[1]) > 0
+
+
+def test_strided_input_and_label_pitch(ctx):
+    """A tile that is a window of a wider image (pitch > 3*width) and a label plane with a
+    pitch > width give the same result as the dense call."""
+    import torch
+    big = make_tile(45, TileSpec(320, 600))["rgb"]
+    rgb = np.ascontiguousarray(big[:, 37:37 + 450])
+    ref = _gpu_process(ctx, rgb, cap=8192)
+    olab, ol, of, ot = oracle.process_tile(rgb)
+    assert np.array_equal(ref[0], olab)
+    t = torch.from_numpy(big).cuda()[:, 37:37 + 450]            # stride(0) = 3*600 bytes
+    assert t.stride(0) == 3 * 600
+    lab_wide = torch.full((320, 512), -7, dtype=torch.int32, device="cuda")
+    lab = lab_wide[:, :450]
+    nobj = torch.zeros(1, dtype=torch.int32, device="cuda")
+    cap = 8192
+    tl = torch.zeros(cap, dtype=torch.int32, device="cuda")
+    tf = torch.zeros(cap, dtype=torch.int32, device="cuda")
+    tt = torch.zeros((cap, 36), dtype=torch.float32, device="cuda")
+    nr = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ctx.process_tile(0, t, lab, nobj, tl, tf, tt, nr)
+    torch.cuda.synchronize()
+    k = int(nr.item())
+    assert np.array_equal(lab.cpu().numpy(), olab)
+    assert (lab_wide[:, 450:] == -7).all()                        # the pitch padding is untouched
+    assert_features_equal(tl[:k].cpu().numpy(), tf[:k].cpu().numpy(), tt[:k].cpu().numpy(), ol, of, ot)
