@@ -800,3 +800,17 @@ def test_strided_input_and_label_pitch(ctx):
     assert np.array_equal(lab.cpu().numpy(), olab)
     assert (lab_wide[:, 450:] == -7).all()                        # the pitch padding is untouched
     assert_features_equal(tl[:k].cpu().numpy(), tf[:k].cpu().numpy(), tt[:k].cpu().numpy(), ol, of, ot)
+
+
+@pytest.mark.parametrize("hw", [(1031, 1153), (257, 16384), (4099, 65)])
+def test_pipeline_ragged_and_max_width(hw):
+    """Odd sizes (partial regions, tiles and vector words on both edges; rows not 4-byte
+    aligned) and the maximum width hp_config allows, against the oracle."""
+    from paper_1209_3332_b200 import Context
+    h, w = hw
+    rgb = make_tile(50 + h % 7, TileSpec(h, w))["rgb"]
+    with Context(0, w, h, n_slots=1, max_objects=16384) as c:
+        lab, nobj, gl, gf, gt = _gpu_process(c, rgb, cap=16384)
+    olab, ol, of, ot = oracle.process_tile(rgb)
+    assert np.array_equal(lab, olab) and nobj == len(ol) > 0
+    assert_features_equal(gl, gf, gt, ol, of, ot)
