@@ -133,6 +133,14 @@ void ev(hp_ctx* ctx, Slot& sl, int k, cudaStream_t s) {
 // S1..S10 on device buffers (the segmentation stage instance)
 // S1..S10; with `table` the fused per-component path also computes S11 into it and *fused
 // is set (the caller then skips the separate feature stage)
+// Experiment only (variant builds, -DHP_WHATIF_DUP=k): run step k twice per tile to measure
+// its marginal cost in the concurrent bench (1 S1, 2 S2, 3 S3, 5 S5, 6 S6, 8 Canny, 9 S7-S11).
+// Every duplicated launcher resets its own outputs, so the results are unchanged.
+#ifndef HP_WHATIF_DUP
+#define HP_WHATIF_DUP 0
+#endif
+#define HP_DUP(k) for (int dup_ = 0; dup_ < (HP_WHATIF_DUP == (k) ? 2 : 1); ++dup_)
+
 hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, int64_t lpitch,
                   int32_t* n_objects, cudaStream_t s, hp_feature_table* table = nullptr,
                   bool* fused = nullptr) {
@@ -140,7 +148,7 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
     const hp_params& p = ctx->cfg.params;
     const int w = rgb->width, h = rgb->height;
     ev(ctx, sl, 0, s);
-    launch_cd(rgb->data, w, h, rgb->pitch_bytes, ctx->lut, p, sl.g, sl.flags, &sl.counters[0], s);   // S1
+    HP_DUP(1) launch_cd(rgb->data, w, h, rgb->pitch_bytes, ctx->lut, p, sl.g, sl.flags, &sl.counters[0], s);   // S1
     ev(ctx, sl, 1, s);
     if (p.bg_skip_frac <= 1.0f) {
         unsigned long long nbg = 0;
@@ -154,11 +162,11 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
             return check_launch(ctx, "bg skip");
         }
     }
-    launch_rbc(sl.flags, w, h, sl, sl.rbc, s);                                                      // S2
+    HP_DUP(2) launch_rbc(sl.flags, w, h, sl, sl.rbc, s);                                            // S2
     ev(ctx, sl, 2, s);
     // the opening is anti-extensive (symmetric SE containing the origin, out-of-tile pixels
     // ignored: open(g) <= g), so S4's marker min(open, g) is the opening itself
-    launch_open(sl.g, w, h, p.open_diam, sl.u8a, sl.u8b, s);                                          // S3
+    HP_DUP(3) launch_open(sl.g, w, h, p.open_diam, sl.u8a, sl.u8b, s);                                // S3
     ev(ctx, sl, 3, s);
     {                                                                                                 // S4
         // optionally on the slot's high-priority stream: its CTAs then take SM resources
@@ -183,10 +191,10 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
     ev(ctx, sl, 4, s);
     // S5 on the top-hat candidates (g - recon > g1) & !rbc, evaluated inside the CCL passes
     int32_t* ncomp5 = sl.cnt32 + 16;  // S5 components kept (listed with root and bbox)
-    launch_area_select_tophat(sl.g, sl.u8b, sl.rbc, p.g1, w, h, p.cand_min_area, p.cand_max_area, sl, sl.big0,
+    HP_DUP(5) launch_area_select_tophat(sl.g, sl.u8b, sl.rbc, p.g1, w, h, p.cand_min_area, p.cand_max_area, sl, sl.big0,
                               ncomp5, s);
     ev(ctx, sl, 5, s);
-    launch_fill_components(sl.big0, w, h, sl, ncomp5, sl.F, sl.split, s);                           // S6
+    HP_DUP(6) launch_fill_components(sl.big0, w, h, sl, ncomp5, sl.F, sl.split, s);                 // S6
     ev(ctx, sl, 6, s);
     if (ctx->global_s8s10) {
         launch_edt(sl.F, w, h, sl, nullptr, sl.dist, s);                                             // S7
@@ -207,8 +215,8 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
             cs = sl.hstream;
         }
         // the feature stage's Canny, only when features are produced
-        if (table) launch_canny(sl.g, w, h, p.canny_low, p.canny_high, sl, sl.cand, cs);
-        launch_components(ncomp5, sl.split, sl.g, sl.cand, p.h, p.obj_min_area, p.obj_max_area, w, h, sl, labels,
+        if (table) HP_DUP(8) launch_canny(sl.g, w, h, p.canny_low, p.canny_high, sl, sl.cand, cs);
+        HP_DUP(9) launch_components(ncomp5, sl.split, sl.g, sl.cand, p.h, p.obj_min_area, p.obj_max_area, w, h, sl, labels,
                           lpitch, n_objects, table, ctx->cfg.max_objects, cs);
         if (ctx->prio >= 2) {
             cudaEventRecord(sl.join_ev, sl.hstream);

@@ -483,60 +483,104 @@ void run_select(Sel sel, int conn, Slot& sl, uint8_t* out, cudaStream_t s, const
 // (tan(22.5 deg) in 15-bit fixed point; out-of-tile magnitudes 0); map = 2 for local maxima
 // with m > high, 1 for other local maxima with m > low, else 0.  The hysteresis (8-connected
 // components of the candidates that hold a strong one) is the CCL-select SEL_EDGE.
-constexpr int kCW = 32, kCH = 32;  // output tile (256 threads, 4 rows each)
+// 64 x 32 output tile, 256 threads, 4 horizontally adjacent pixels per thread: g staged as
+// 32-bit words (2-px replicated halo), the Sobel pair of 4 pixels from 3 words of each of 3
+// rows (column sums shared), magnitude (int16) and gradient sector (u8) kept in shared memory
+// so the suppression step reads them instead of recomputing the Sobel.
+constexpr int kNW = 64, kNH = 32;
+constexpr int kGWW = kNW / 4 + 2;  // staged g words per row: pixels [x0 - 4, x0 + kNW + 4)
+constexpr int kGR = kNH + 4;       // staged g rows: [y0 - 2, y0 + kNH + 2)
+constexpr int kMW = kNW + 8;       // magnitude columns [x0 - 4, x0 + kNW + 4) (x0-1 .. x0+kNW used)
+constexpr int kMR = kNH + 2;       // magnitude rows [y0 - 1, y0 + kNH]
+
+__device__ __forceinline__ uint32_t g_word(const uint8_t* __restrict__ g, int w, int h, int gx0, int gy,
+                                           bool aligned) {
+    gy = min(max(gy, 0), h - 1);
+    const uint8_t* row = g + (int64_t)gy * w;
+    if (aligned && gx0 >= 0 && gx0 + 3 < w) return __ldg(reinterpret_cast<const unsigned int*>(row + gx0));
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) v |= (uint32_t)__ldg(row + min(max(gx0 + b, 0), w - 1)) << (8 * b);
+    return v;
+}
+
 __global__ void __launch_bounds__(256) k_canny_nms(const uint8_t* __restrict__ g, int w, int h, int low, int high,
                                                    uint8_t* __restrict__ map) {
-    __shared__ uint8_t sg[kCH + 4][kCW + 4];  // g with a 2-px halo (replicated)
-    __shared__ int16_t sm[kCH + 2][kCW + 2];  // magnitude with a 1-px halo (0 outside the tile)
-    const int x0 = blockIdx.x * kCW, y0 = blockIdx.y * kCH;
-    for (int i = threadIdx.x; i < (kCH + 4) * (kCW + 4); i += blockDim.x) {
-        const int ly = i / (kCW + 4), lx = i - ly * (kCW + 4);
-        const int gx = min(max(x0 + lx - 2, 0), w - 1), gy = min(max(y0 + ly - 2, 0), h - 1);
-        sg[ly][lx] = __ldg(g + (int64_t)gy * w + gx);
+    __shared__ uint32_t sg[kGR][kGWW];
+    __shared__ __align__(8) int16_t sm[kMR][kMW];
+    __shared__ __align__(4) uint8_t sd[kMR][kMW];
+    const int x0 = blockIdx.x * kNW, y0 = blockIdx.y * kNH;
+    const bool aligned = (w & 3) == 0 && (((uintptr_t)g) & 3) == 0;
+    for (int i = threadIdx.x; i < kGR * kGWW; i += blockDim.x) {
+        const int r = i / kGWW, q = i - r * kGWW;
+        sg[r][q] = g_word(g, w, h, x0 - 4 + 4 * q, y0 - 2 + r, aligned);
     }
     __syncthreads();
-    auto sobel = [&](int cy, int cx, int& dx, int& dy) {  // (cy, cx): position in sg
-        dx = (sg[cy - 1][cx + 1] + 2 * sg[cy][cx + 1] + sg[cy + 1][cx + 1]) -
-             (sg[cy - 1][cx - 1] + 2 * sg[cy][cx - 1] + sg[cy + 1][cx - 1]);
-        dy = (sg[cy + 1][cx - 1] + 2 * sg[cy + 1][cx] + sg[cy + 1][cx + 1]) -
-             (sg[cy - 1][cx - 1] + 2 * sg[cy - 1][cx] + sg[cy - 1][cx + 1]);
-    };
-    for (int i = threadIdx.x; i < (kCH + 2) * (kCW + 2); i += blockDim.x) {
-        const int ly = i / (kCW + 2), lx = i - ly * (kCW + 2);  // pixel (x0 + lx - 1, y0 + ly - 1)
-        const int gx = x0 + lx - 1, gy = y0 + ly - 1;
-        int m = 0;
-        if (gx >= 0 && gy >= 0 && gx < w && gy < h) {
-            int dx, dy;
-            sobel(ly + 1, lx + 1, dx, dy);
-            m = abs(dx) + abs(dy);
-        }
-        sm[ly][lx] = (int16_t)m;
-    }
-    __syncthreads();
-    const int lx = threadIdx.x & 31;
-    const int gx = x0 + lx;
+    // Sobel of pixel groups (row gy = y0 - 1 + r, pixels x0 - 4 + 4q + k, k = 0..3)
+    for (int i = threadIdx.x; i < kMR * kGWW; i += blockDim.x) {
+        const int r = i / kGWW, q = i - r * kGWW;
+        const int ql = max(q - 1, 0), qr = min(q + 1, kGWW - 1);  // outermost pixels unused
+        int t[6], c[6], b[6];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int ly = (threadIdx.x >> 5) + 8 * k;
-        const int gy = y0 + ly;
-        if (gx >= w || gy >= h) continue;
-        const int m = sm[ly + 1][lx + 1];
-        uint8_t out = 0;
-        if (m > low) {
-            int dx, dy;
-            sobel(ly + 2, lx + 2, dx, dy);
+        for (int row = 0; row < 3; ++row) {
+            const uint32_t A = sg[r + row][ql], B = sg[r + row][q], C = sg[r + row][qr];
+            int* v = row == 0 ? t : (row == 1 ? c : b);
+            v[0] = A >> 24;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) v[k + 1] = (B >> (8 * k)) & 0xff;
+            v[5] = C & 0xff;
+        }
+        const int gy = y0 - 1 + r;
+        uint32_t mlo = 0, mhi = 0, sec = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // pixel k <-> index k + 1
+            const int gx = x0 - 4 + 4 * q + k;
+            const int dx = (t[k + 2] + 2 * c[k + 2] + b[k + 2]) - (t[k] + 2 * c[k] + b[k]);
+            const int dy = (b[k] + 2 * b[k + 1] + b[k + 2]) - (t[k] + 2 * t[k + 1] + t[k + 2]);
+            int m = abs(dx) + abs(dy);
+            if (gx < 0 || gx >= w || gy < 0 || gy >= h) m = 0;
             const int ax = abs(dx), ay = abs(dy) << 15;  // |dy| <= 1020: fits in 32 bits
             const int tg22x = ax * 13573, tg67x = tg22x + (ax << 16);
-            bool lm;
-            if (ay < tg22x) lm = m > sm[ly + 1][lx] && m >= sm[ly + 1][lx + 2];
-            else if (ay > tg67x) lm = m > sm[ly][lx + 1] && m >= sm[ly + 2][lx + 1];
-            else {
-                const int s = ((dx ^ dy) < 0) ? -1 : 1;
-                lm = m > sm[ly][lx + 1 - s] && m > sm[ly + 2][lx + 1 + s];
-            }
-            if (lm) out = m > high ? 2 : 1;
+            const uint32_t sc = ay < tg22x ? 0u : (ay > tg67x ? 1u : (((dx ^ dy) < 0) ? 2u : 3u));
+            if (k < 2) mlo |= (uint32_t)m << (16 * k);
+            else mhi |= (uint32_t)m << (16 * (k - 2));
+            sec |= sc << (8 * k);
         }
-        map[(int64_t)gy * w + gx] = out;
+        *reinterpret_cast<uint2*>(&sm[r][4 * q]) = make_uint2(mlo, mhi);
+        *reinterpret_cast<uint32_t*>(&sd[r][4 * q]) = sec;
+    }
+    __syncthreads();
+    // suppression: thread -> 4 pixels of 2 rows; sector 0: left/right, 1: up/down, 2: up-right
+    // and down-left, 3: up-left and down-right (">" toward -x / -y, ">=" toward +x / +y)
+    const int cg = threadIdx.x & 15, rg = threadIdx.x >> 4;
+    const int gx0 = x0 + 4 * cg;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const int oy = 2 * rg + rr, gy = y0 + oy;
+        if (gy >= h) continue;
+        const int r = oy + 1;  // sm row of the pixel
+        const int c0 = 4 + 4 * cg;  // sm column of pixel 0
+        uint32_t out = 0;
+        const uint32_t sec = *reinterpret_cast<const uint32_t*>(&sd[r][c0]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int c = c0 + k;
+            const int m = sm[r][c];
+            if (m <= low) continue;
+            const uint32_t sc = (sec >> (8 * k)) & 0xff;
+            bool lm;
+            if (sc == 0) lm = m > sm[r][c - 1] && m >= sm[r][c + 1];
+            else if (sc == 1) lm = m > sm[r - 1][c] && m >= sm[r + 1][c];
+            else if (sc == 2) lm = m > sm[r - 1][c + 1] && m > sm[r + 1][c - 1];
+            else lm = m > sm[r - 1][c - 1] && m > sm[r + 1][c + 1];
+            if (lm) out |= (m > high ? 2u : 1u) << (8 * k);
+        }
+        uint8_t* o = map + (int64_t)gy * w + gx0;
+        if (gx0 + 3 < w && (((uintptr_t)o) & 3) == 0) {
+            *reinterpret_cast<uint32_t*>(o) = out;
+        } else {
+            for (int k = 0; k < 4 && gx0 + k < w; ++k) o[k] = (uint8_t)(out >> (8 * k));
+        }
     }
 }
 
@@ -546,7 +590,7 @@ __global__ void __launch_bounds__(256) k_canny_nms(const uint8_t* __restrict__ g
 // and the CCL-select arrays -- free from S6 on, so the pipeline runs it beside S7-S11.
 void launch_canny(const uint8_t* g, int w, int h, int low, int high, Slot& sl, uint8_t* edges, cudaStream_t s) {
     if ((int64_t)w * h == 0) return;
-    dim3 grid((w + kCW - 1) / kCW, (h + kCH - 1) / kCH);
+    dim3 grid((w + kNW - 1) / kNW, (h + kNH - 1) / kNH);
     (note_launch(), k_canny_nms<<<grid, 256, 0, s>>>(g, w, h, low, high, sl.pmask));
     Sel sel{sl.pmask, w, h, 0, 0};
     sel.P = sl.ML;
