@@ -775,28 +775,27 @@ __global__ void __launch_bounds__(kWarpsPB * 32, 4) k_fill_fused(FillArgs a, con
     }
 }
 
+// Rows to label order: labels are distinct, so a row's rank is the number of smaller labels.
+// One warp per row (grid-stride): the lanes count over the staged labels (L1-resident), then
+// copy the row to its rank -- ~n^2/32 compares spread over the whole GPU, coalesced row copies.
 __global__ void k_rows_scatter(const int32_t* __restrict__ cnt, int32_t cap, const int32_t* __restrict__ sl,
                                const int32_t* __restrict__ sf, const float* __restrict__ sfeat,
                                int32_t* __restrict__ ol, int32_t* __restrict__ of, float* __restrict__ ofeat,
                                int32_t capacity) {
     const int n = min(*cnt, cap);
-    __shared__ int32_t chunk[1024];
-    for (int base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
-        int i = base + threadIdx.x;
-        int32_t me = i < n ? sl[i] : 0;
-        int rk = 0;
-        for (int c0 = 0; c0 < n; c0 += 1024) {
-            __syncthreads();
-            for (int k = threadIdx.x; k < 1024 && c0 + k < n; k += blockDim.x) chunk[k] = sl[c0 + k];
-            __syncthreads();
-            int lim = min(1024, n - c0);
-            for (int k = 0; k < lim; ++k) rk += chunk[k] < me;
-        }
-        if (i < n && rk < capacity) {
+    const int lane = threadIdx.x & 31;
+    const int nw = gridDim.x * (blockDim.x >> 5);
+    for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += nw) {
+        const int32_t me = sl[i];
+        int c = 0;
+        for (int k = lane; k < n; k += 32) c += __ldg(sl + k) < me;
+        const int rk = __reduce_add_sync(0xffffffffu, c);
+        if (rk >= capacity) continue;
+        if (lane == 0) {
             ol[rk] = me;
             of[rk] = sf[i];
-            for (int k = 0; k < HP_NFEAT; ++k) ofeat[(int64_t)rk * HP_NFEAT + k] = sfeat[(int64_t)i * HP_NFEAT + k];
         }
+        for (int k = lane; k < HP_NFEAT; k += 32) ofeat[(int64_t)rk * HP_NFEAT + k] = sfeat[(int64_t)i * HP_NFEAT + k];
     }
 }
 
@@ -858,7 +857,7 @@ void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t*
                                                                      sl.sc_big, nbig, heads));
     (note_launch(), k_comp_huge<<<1, kHugeT, 0, s>>>(a, sl.sc_root, sl.sc_bbox, carve_big(sl)));
     if (table) {
-        (note_launch(), k_rows_scatter<<<std::max(1, std::min(148 * 4, (max_objects + 255) / 256)), 256, 0, s>>>(
+        (note_launch(), k_rows_scatter<<<std::max(1, std::min(148 * 2, (max_objects + 7) / 8)), 256, 0, s>>>(
             rows, max_objects, sl.stg_label, sl.stg_flags, sl.stg_feat, table->label, table->flags, table->feat,
             table->capacity));
         (note_launch(), k_copy_i32<<<1, 1, 0, s>>>(rows, table->n_rows_dev));
