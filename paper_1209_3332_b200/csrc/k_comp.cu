@@ -495,6 +495,15 @@ __global__ void k_comp_classify(CompArgs a, const int32_t* __restrict__ cnt, int
 // the block list (whole-block team), then its warps take small components one at a time off
 // the component list (warp teams) -- dynamic queues, so the few big windows run beside the
 // many small ones instead of as a serial tail.
+// persistent grids: blocks per SM of the fused kernels (each block holds kWarpsPB windows of
+// shared memory while it runs, which the concurrent slots' kernels then cannot use)
+#ifndef HP_COMP_BPS
+#define HP_COMP_BPS 4
+#endif
+#ifndef HP_FILL_BPS
+#define HP_FILL_BPS 4
+#endif
+
 __global__ void __launch_bounds__(kWarpsPB * 32, 4) k_comp_fused(CompArgs a, const int32_t* __restrict__ cnt,
                                                                 int32_t cap, const int32_t* __restrict__ roots,
                                                                 const int4* __restrict__ bbox,
@@ -853,7 +862,7 @@ void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t*
     once.get([&] { return (int)cudaFuncSetAttribute(k_comp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw); });
     (note_launch(), k_comp_classify<<<grid_for(cap), 256, 0, s>>>(a, count5, cap, sl.sc_root, sl.sc_bbox,
                                                                    sl.sc_big, nbig));
-    (note_launch(), k_comp_fused<<<148 * 4, kWarpsPB * 32, smw, s>>>(a, count5, cap, sl.sc_root, sl.sc_bbox,
+    (note_launch(), k_comp_fused<<<148 * HP_COMP_BPS, kWarpsPB * 32, smw, s>>>(a, count5, cap, sl.sc_root, sl.sc_bbox,
                                                                      sl.sc_big, nbig, heads));
     (note_launch(), k_comp_huge<<<1, kHugeT, 0, s>>>(a, sl.sc_root, sl.sc_bbox, carve_big(sl)));
     if (table) {
@@ -882,7 +891,7 @@ void launch_fill_components(const uint8_t* big0, int w, int h, Slot& sl, const i
     const int32_t cap = sl.comp_cap;
     (note_launch(), k_win_classify<<<grid_for(cap), 256, 0, s>>>(count, cap, sl.sc_bbox, sl.sc_big, nbig, sl.sc_huge,
                                                                   nhuge));
-    (note_launch(), k_fill_fused<<<148 * 4, kWarpsPB * 32, smw, s>>>(a, count, cap, sl.sc_root, sl.sc_bbox,
+    (note_launch(), k_fill_fused<<<148 * HP_FILL_BPS, kWarpsPB * 32, smw, s>>>(a, count, cap, sl.sc_root, sl.sc_bbox,
                                                                      sl.sc_area, sl.sc_big, nbig, heads));
     (note_launch(), k_fill_huge<<<1, kHugeT, 0, s>>>(a, sl.sc_root, sl.sc_bbox, sl.sc_area, sl.sc_huge, nhuge,
                                                     carve_big(sl)));
