@@ -36,7 +36,8 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HP_RG_ORDER
 #define HP_RG_ORDER 3  // initial job order: 0 raster, 1 four-colour (r1: 3018 -> 2165 jobs, 689 -> 725 tiles/s),
                        // 2 colour then highest marker, 3 highest marker then colour (2165 -> 1870
-                       // jobs, 858 -> 870 tiles/s), 4 mean marker then colour
+                       // jobs, 858 -> 870 tiles/s), 4 mean marker then colour, 5 region-grid distance
+                       // to the top-marker regions (S4 alone 0.76 -> 0.72 ms but bench 871 -> 826)
 #endif
 #ifndef HP_RG_PROFILE
 #define HP_RG_PROFILE 0  // timing breakdown in the stats (experiments)
@@ -748,15 +749,53 @@ __global__ void __launch_bounds__(256) k_rg_keys(const uint8_t* __restrict__ R, 
     }
 }
 
-// queue[rank] = region, rank by (ORDER 2: colour, then descending max; ORDER 3: descending
-// max, then colour), ties by index
+#if HP_RG_ORDER == 5
+// ORDER 5: key = region-grid distance (8-neighbour steps) to the nearest region holding the
+// tile's highest marker value -- the flood's sources first, then outward wave by wave.  One
+// block: synchronous relaxation over the region grid (a few dozen rounds).
+__global__ void __launch_bounds__(1024) k_rg_dist(Worklist wl, int32_t* __restrict__ keys) {
+    const int n = wl.ntx * wl.nty;
+    __shared__ int top;
+    __shared__ int changed;
+    if (threadIdx.x == 0) top = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) atomicMax(&top, keys[i]);
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) keys[i] = keys[i] == top ? 0 : INT_MAX / 2;
+    __syncthreads();
+    while (true) {
+        if (threadIdx.x == 0) changed = 0;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const int rx = i % wl.ntx, ry = i / wl.ntx;
+            int d = keys[i];
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    const int x = rx + dx, y = ry + dy;
+                    if (x >= 0 && y >= 0 && x < wl.ntx && y < wl.nty) d = min(d, keys[y * wl.ntx + x] + 1);
+                }
+            if (d < keys[i]) {
+                keys[i] = d;  // monotone (Bellman-Ford style): any interleaving converges
+                changed = 1;
+            }
+        }
+        __syncthreads();
+        if (!changed) break;
+        __syncthreads();
+    }
+}
+#endif
+
+// queue[rank] = region, rank by (ORDER 2: colour, then descending max; ORDER 3/4: descending
+// max (mean), then colour; ORDER 5: distance to the top regions, then colour), ties by index
 __global__ void __launch_bounds__(256) k_rg_order(Worklist wl, const int32_t* __restrict__ keys) {
     const int n = wl.ntx * wl.nty;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     auto key = [&](int j) {
         const int c = ((j / wl.ntx) & 1) * 2 + ((j % wl.ntx) & 1);
-        return HP_RG_ORDER == 2 ? c * 256 + (255 - keys[j]) : (255 - keys[j]) * 4 + c;  // 3, 4: key first
+        return HP_RG_ORDER == 2 ? c * 256 + (255 - keys[j])
+                                : (HP_RG_ORDER == 5 ? keys[j] * 4 + c : (255 - keys[j]) * 4 + c);
     };
     const int ki = key(i);
     int rk = 0;
@@ -783,6 +822,9 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
     // tile engine, 32 entries per region)
     int32_t* keys = reinterpret_cast<int32_t*>(wl.state) + n;
     (note_launch(), k_rg_keys<<<n, 256, 0, s>>>(R, w, h, wl, keys));
+#if HP_RG_ORDER == 5
+    (note_launch(), k_rg_dist<<<1, 1024, 0, s>>>(wl, keys));
+#endif
     (note_launch(), k_rg_order<<<(n + 255) / 256, 256, 0, s>>>(wl, keys));
 #endif
     static PerDevice once;
