@@ -146,18 +146,27 @@ __global__ void __launch_bounds__(256) k_morph_r(const uint8_t* __restrict__ src
     }
     __syncthreads();
 
-    // stage 3: vertical combine over the 2R+1 rows of D (two rows per 3-input op)
+    // stage 3: vertical combine over the 2R+1 rows of D (two rows per 3-input op).  A thread
+    // takes 4 consecutive output rows: rows of D with equal half-widths read the same H entry
+    // for neighbouring outputs, so the shared loads are issued once (about a third fewer).
+    constexpr int ORW = TH2 / 8;  // output rows per thread
     const int j = tx;
     const int gx = x0 + 2 * j;
-    for (int oy = ty; oy < TH2; oy += 8) {
-        const int gy = y0 + oy;
-        if (gy >= h || gx >= w) continue;
-        uint32_t m = H[(E.idx_of_dy[0] * ROWS + oy) * 32 + j];
+    const int oy0 = ORW * ty;
+    uint32_t m[ORW];
 #pragma unroll
-        for (int dy = 1; dy + 1 <= 2 * R; dy += 2)
-            m = vop3<IS_MIN>(m, H[(E.idx_of_dy[dy] * ROWS + oy + dy) * 32 + j],
-                             H[(E.idx_of_dy[dy + 1] * ROWS + oy + dy + 1) * 32 + j]);
-        const uint32_t pk = __byte_perm(m, 0, 0x0020);  // u16 lanes -> 2 bytes
+    for (int i = 0; i < ORW; ++i) m[i] = H[(E.idx_of_dy[0] * ROWS + oy0 + i) * 32 + j];
+#pragma unroll
+    for (int dy = 1; dy + 1 <= 2 * R; dy += 2)
+#pragma unroll
+        for (int i = 0; i < ORW; ++i)
+            m[i] = vop3<IS_MIN>(m[i], H[(E.idx_of_dy[dy] * ROWS + oy0 + i + dy) * 32 + j],
+                                H[(E.idx_of_dy[dy + 1] * ROWS + oy0 + i + dy + 1) * 32 + j]);
+#pragma unroll
+    for (int i = 0; i < ORW; ++i) {
+        const int gy = y0 + oy0 + i;
+        if (gy >= h || gx >= w) continue;
+        const uint32_t pk = __byte_perm(m[i], 0, 0x0020);  // u16 lanes -> 2 bytes
         uint8_t* o = dst + (int64_t)gy * w + gx;
         if (gx + 1 < w && (((uintptr_t)o) & 1) == 0) {
             *reinterpret_cast<uint16_t*>(o) = (uint16_t)pk;
