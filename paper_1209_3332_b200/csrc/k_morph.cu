@@ -76,6 +76,9 @@ __device__ __forceinline__ uint32_t vop3(uint32_t a, uint32_t b, uint32_t c) {
     return IS_MIN ? __vimin3_u16x2(a, b, c) : __vimax3_u16x2(a, b, c);
 }
 
+#ifndef HP_MORPH_BPS
+#define HP_MORPH_BPS 4  // persistent blocks per SM of the 19x19 path
+#endif
 constexpr int TW2 = 64;        // output tile width (pixels) = 32 u16x2 words
 constexpr int TH2 = 32;        // output tile height
 
@@ -87,95 +90,120 @@ __global__ void __launch_bounds__(256) k_morph_r(const uint8_t* __restrict__ src
     constexpr int RW = 2 * ((R + 3) / 4);        // halo words (2 px each) per side: 4-px aligned
     constexpr int IW = 32 + 2 * RW + 2;          // staged words per row (even: loads in pairs)
     constexpr int ROWS = TH2 + 2 * R;
-    constexpr uint32_t ID = IS_MIN ? 0x00ff00ffu : 0u;
+    constexpr int NQ = IW / 2;                   // 4-pixel groups per row
+    constexpr int NL = (ROWS * NQ + 255) / 256;  // 4-pixel loads per thread per tile
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t* in = smem;                          // [ROWS][IW] u16x2
     uint32_t* H = smem + ROWS * IW;               // [ND][ROWS][32]
-    const int x0 = blockIdx.x * TW2, y0 = blockIdx.y * TH2;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const bool row_aligned = (w & 3) == 0 && (((uintptr_t)src) & 3) == 0;
+    const int ntx = (w + TW2 - 1) / TW2, ntiles = ntx * ((h + TH2 - 1) / TH2);
 
-    // stage 1: pixels [x0 - 2RW, x0 + 64 + 2RW + 2) of rows [y0 - R, y0 + TH2 + R), 4 px per load
-    constexpr int NQ = IW / 2;  // 4-pixel groups per row
-    for (int i = threadIdx.x; i < ROWS * NQ; i += blockDim.x) {
-        const int r = i / NQ, q = i - r * NQ;
-        const int gy = y0 - R + r;
-        const int gx = x0 - 2 * RW + 4 * q;
-        uint32_t v = IS_MIN ? 0xffffffffu : 0u;
-        if (gy >= 0 && gy < h) {
-            const uint8_t* rowp = src + (int64_t)gy * w;
-            if (row_aligned && gx >= 0 && gx + 3 < w) {
-                v = __ldg(reinterpret_cast<const unsigned int*>(rowp + gx));
-            } else {
+    // Persistent over tiles: the global loads of the NEXT tile's input are issued into
+    // registers before this tile's compute, so their latency hides behind stages 2-3.
+    // stage 1 (per tile): pixels [x0 - 2RW, x0 + 64 + 2RW + 2) of rows [y0 - R, y0 + TH2 + R)
+    uint32_t pre[NL];
+    auto load = [&](int tile) {
+        const int x0 = (tile % ntx) * TW2, y0 = (tile / ntx) * TH2;
 #pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    const int x = gx + b;
-                    const uint32_t byte = (x >= 0 && x < w) ? (uint32_t)__ldg(rowp + x) : (IS_MIN ? 0xffu : 0u);
-                    v = (v & ~(0xffu << (8 * b))) | (byte << (8 * b));
+        for (int l = 0; l < NL; ++l) {
+            const int i = threadIdx.x + 256 * l;
+            uint32_t v = IS_MIN ? 0xffffffffu : 0u;
+            if (i < ROWS * NQ) {
+                const int r = i / NQ, q = i - r * NQ;
+                const int gy = y0 - R + r;
+                const int gx = x0 - 2 * RW + 4 * q;
+                if (gy >= 0 && gy < h) {
+                    const uint8_t* rowp = src + (int64_t)gy * w;
+                    if (row_aligned && gx >= 0 && gx + 3 < w) {
+                        v = __ldg(reinterpret_cast<const unsigned int*>(rowp + gx));
+                    } else {
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) {
+                            const int x = gx + b;
+                            const uint32_t byte =
+                                (x >= 0 && x < w) ? (uint32_t)__ldg(rowp + x) : (IS_MIN ? 0xffu : 0u);
+                            v = (v & ~(0xffu << (8 * b))) | (byte << (8 * b));
+                        }
+                    }
                 }
             }
+            pre[l] = v;
         }
-        in[r * IW + 2 * q] = __byte_perm(v, 0, 0x4140);      // px 0, 1 -> u16 lanes
-        in[r * IW + 2 * q + 1] = __byte_perm(v, 0, 0x4342);  // px 2, 3
-    }
-    __syncthreads();
+    };
+    int tile = blockIdx.x;
+    if (tile < ntiles) load(tile);
+    for (; tile < ntiles; tile += gridDim.x) {
+        const int x0 = (tile % ntx) * TW2, y0 = (tile / ntx) * TH2;
+        __syncthreads();  // the previous tile's stages 2-3 are done with in[] and H[]
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+            const int i = threadIdx.x + 256 * l;
+            if (i < ROWS * NQ) {
+                const int r = i / NQ, q = i - r * NQ;
+                in[r * IW + 2 * q] = __byte_perm(pre[l], 0, 0x4140);      // px 0, 1 -> u16 lanes
+                in[r * IW + 2 * q + 1] = __byte_perm(pre[l], 0, 0x4342);  // px 2, 3
+            }
+        }
+        __syncthreads();
+        if (tile + (int)gridDim.x < ntiles) load(tile + gridDim.x);
 
-    // stage 2: horizontal running min/max for the distinct half-widths; one warp per row,
-    // lane = output word (pixels 2j, 2j+1)
-    for (int r = ty; r < ROWS; r += 8) {
-        const uint32_t* rowp = in + r * IW;
-        const int j = tx;
-        uint32_t wv[2 * RW + 2];
+        // stage 2: horizontal running min/max for the distinct half-widths; one warp per row,
+        // lane = output word (pixels 2j, 2j+1)
+        for (int r = ty; r < ROWS; r += 8) {
+            const uint32_t* rowp = in + r * IW;
+            const int j = tx;
+            uint32_t wv[2 * RW + 2];
 #pragma unroll
-        for (int k = 0; k < 2 * RW + 2; ++k) wv[k] = rowp[j + k];
-        auto win = [&](int k) -> uint32_t {  // pixels (2j + k, 2j + 1 + k)
-            const int o = 2 * RW + k;
-            return (o & 1) ? __funnelshift_r(wv[o >> 1], wv[(o >> 1) + 1], 16) : wv[o >> 1];
-        };
-        uint32_t m = wv[RW];
-#pragma unroll
-        for (int q = 0; q < ND; ++q)
-            if (E.hw[q] == 0) H[(q * ROWS + r) * 32 + j] = m;
-#pragma unroll
-        for (int k = 1; k <= R; ++k) {
-            m = vop3<IS_MIN>(m, win(k), win(-k));
+            for (int k = 0; k < 2 * RW + 2; ++k) wv[k] = rowp[j + k];
+            auto win = [&](int k) -> uint32_t {  // pixels (2j + k, 2j + 1 + k)
+                const int o = 2 * RW + k;
+                return (o & 1) ? __funnelshift_r(wv[o >> 1], wv[(o >> 1) + 1], 16) : wv[o >> 1];
+            };
+            uint32_t m = wv[RW];
 #pragma unroll
             for (int q = 0; q < ND; ++q)
-                if (E.hw[q] == k) H[(q * ROWS + r) * 32 + j] = m;
+                if (E.hw[q] == 0) H[(q * ROWS + r) * 32 + j] = m;
+#pragma unroll
+            for (int k = 1; k <= R; ++k) {
+                m = vop3<IS_MIN>(m, win(k), win(-k));
+#pragma unroll
+                for (int q = 0; q < ND; ++q)
+                    if (E.hw[q] == k) H[(q * ROWS + r) * 32 + j] = m;
+            }
         }
-    }
-    __syncthreads();
+        __syncthreads();
 
-    // stage 3: vertical combine over the 2R+1 rows of D (two rows per 3-input op).  A thread
-    // takes 4 consecutive output rows: rows of D with equal half-widths read the same H entry
-    // for neighbouring outputs, so the shared loads are issued once (about a third fewer).
-    constexpr int ORW = TH2 / 8;  // output rows per thread
-    const int j = tx;
-    const int gx = x0 + 2 * j;
-    const int oy0 = ORW * ty;
-    uint32_t m[ORW];
+        // stage 3: vertical combine over the 2R+1 rows of D (two rows per 3-input op).  A
+        // thread takes 4 consecutive output rows: rows of D with equal half-widths read the
+        // same H entry for neighbouring outputs, so the shared loads are issued once.
+        constexpr int ORW = TH2 / 8;  // output rows per thread
+        const int j = tx;
+        const int gx = x0 + 2 * j;
+        const int oy0 = ORW * ty;
+        uint32_t m[ORW];
 #pragma unroll
-    for (int i = 0; i < ORW; ++i) m[i] = H[(E.idx_of_dy[0] * ROWS + oy0 + i) * 32 + j];
+        for (int i = 0; i < ORW; ++i) m[i] = H[(E.idx_of_dy[0] * ROWS + oy0 + i) * 32 + j];
 #pragma unroll
-    for (int dy = 1; dy + 1 <= 2 * R; dy += 2)
+        for (int dy = 1; dy + 1 <= 2 * R; dy += 2)
 #pragma unroll
-        for (int i = 0; i < ORW; ++i)
-            m[i] = vop3<IS_MIN>(m[i], H[(E.idx_of_dy[dy] * ROWS + oy0 + i + dy) * 32 + j],
-                                H[(E.idx_of_dy[dy + 1] * ROWS + oy0 + i + dy + 1) * 32 + j]);
+            for (int i = 0; i < ORW; ++i)
+                m[i] = vop3<IS_MIN>(m[i], H[(E.idx_of_dy[dy] * ROWS + oy0 + i + dy) * 32 + j],
+                                    H[(E.idx_of_dy[dy + 1] * ROWS + oy0 + i + dy + 1) * 32 + j]);
 #pragma unroll
-    for (int i = 0; i < ORW; ++i) {
-        const int gy = y0 + oy0 + i;
-        if (gy >= h || gx >= w) continue;
-        const uint32_t pk = __byte_perm(m[i], 0, 0x0020);  // u16 lanes -> 2 bytes
-        uint8_t* o = dst + (int64_t)gy * w + gx;
-        if (gx + 1 < w && (((uintptr_t)o) & 1) == 0) {
-            *reinterpret_cast<uint16_t*>(o) = (uint16_t)pk;
-        } else {
-            o[0] = (uint8_t)pk;
-            if (gx + 1 < w) o[1] = (uint8_t)(pk >> 8);
+        for (int i = 0; i < ORW; ++i) {
+            const int gy = y0 + oy0 + i;
+            if (gy >= h || gx >= w) continue;
+            const uint32_t pk = __byte_perm(m[i], 0, 0x0020);  // u16 lanes -> 2 bytes
+            uint8_t* o = dst + (int64_t)gy * w + gx;
+            if (gx + 1 < w && (((uintptr_t)o) & 1) == 0) {
+                *reinterpret_cast<uint16_t*>(o) = (uint16_t)pk;
+            } else {
+                o[0] = (uint8_t)pk;
+                if (gx + 1 < w) o[1] = (uint8_t)(pk >> 8);
+            }
         }
     }
-    (void)ID;
 }
 
 template <int R>
@@ -193,7 +221,9 @@ void launch_r(const uint8_t* g, int w, int h, uint8_t* tmp, uint8_t* out, cudaSt
         cudaFuncSetAttribute(k_morph_r<true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return (int)cudaFuncSetAttribute(k_morph_r<false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     });
-    dim3 grid((w + TW2 - 1) / TW2, (h + TH2 - 1) / TH2);
+    // persistent: as many blocks as fit (shared memory allows 4 per SM), each looping over tiles
+    const int ntiles = ((w + TW2 - 1) / TW2) * ((h + TH2 - 1) / TH2);
+    const int grid = std::max(1, std::min(ntiles, 148 * HP_MORPH_BPS));
     (note_launch(), k_morph_r<true, R><<<grid, 256, smem, s>>>(g, w, h, tmp));
     (note_launch(), k_morph_r<false, R><<<grid, 256, smem, s>>>(tmp, w, h, out));
 }
