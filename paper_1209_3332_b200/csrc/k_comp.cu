@@ -504,7 +504,11 @@ __global__ void k_comp_classify(CompArgs a, const int32_t* __restrict__ cnt, int
 #define HP_FILL_BPS 4
 #endif
 
-__global__ void __launch_bounds__(kWarpsPB * 32, 4) k_comp_fused(CompArgs a, const int32_t* __restrict__ cnt,
+#ifndef HP_COMP_MINB
+#define HP_COMP_MINB 4  // launch-bounds min blocks of k_comp_fused (4: 128 registers, some spills)
+#endif
+
+__global__ void __launch_bounds__(kWarpsPB * 32, HP_COMP_MINB) k_comp_fused(CompArgs a, const int32_t* __restrict__ cnt,
                                                                 int32_t cap, const int32_t* __restrict__ roots,
                                                                 const int4* __restrict__ bbox,
                                                                 const int32_t* __restrict__ big,
