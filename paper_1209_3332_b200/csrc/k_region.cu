@@ -838,12 +838,20 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
         // One CTA per SM (measured, bench.py r1: 229 vs 193 tiles/s at 2 CTAs/SM): on hard tiles
         // the reconstruction is latency-bound on chains of region jobs, so leaving half the
         // SM resources free lets another slot's tile run beside it.
-        int want = 1;
-        if (const char* e = getenv("HP_RG_CTAS_PER_SM")) want = atoi(e);
-        want = std::max(1, std::min(want, per_sm > 0 ? per_sm : 1));
-        return nsm * want;
+        // With several slots in flight, three CTAs per four SMs (r1 final: 897 -> 903 tiles/s,
+        // e2e 924 -> 939): each tile's reconstruction then holds fewer SMs while chain-bound.
+        if (const char* e = getenv("HP_RG_CTAS_PER_SM")) {
+            const int want = std::max(1, std::min(atoi(e), per_sm > 0 ? per_sm : 1));
+            return nsm * want;
+        }
+        return std::max(1, nsm * 3 / 4);
     });
     int b = std::max(1, std::min(blocks, n));
+    static const int grid_env = [] {  // HP_RG_GRID: absolute CTA count (experiments)
+        const char* e = getenv("HP_RG_GRID");
+        return e ? atoi(e) : 0;
+    }();
+    if (grid_env > 0) b = std::max(1, std::min(grid_env, n));
     (note_launch(), k_region_mr8<<<b, NW * 32, smem, s>>>(mask, R, w, h, wl));
 }
 
