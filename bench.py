@@ -86,14 +86,20 @@ def make_tiles(rank, batch, size):
 
 # ----------------------------------------------------------------- clocks
 class Clocks:
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    """nvidia-smi sampler for the clocks line: started before the warm-up (so it is producing
+    samples by the time the timed region starts), every sample timestamped, and only the
+    samples inside [timed-region start, end + one period] count (at least one: stop() waits
+    for the first sample after the region if the region was shorter than a period)."""
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    PERIOD_MS = 50
 
     def __init__(self, index):
         self.index = index
         self.proc = None
         self.fn = None
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
@@ -101,38 +107,66 @@ class Clocks:
             os.close(fd)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "-i", str(self.index),
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.PERIOD_MS)],
                 stdout=open(self.fn, "w"), stderr=subprocess.DEVNULL)
         except Exception:  # noqa: BLE001
             self.proc = None
 
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def _read(self):
+        import datetime
+        rows = []
+        for line in open(self.fn):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(f[1]), float(f[2]), f[4:8]))
+            except ValueError:
+                continue
+        return rows
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        t1 = self.t1 if self.t1 is not None else time.time()
+        t0 = self.t0 if self.t0 is not None else t1
+        hi = t1 + self.PERIOD_MS / 1000.0
+        deadline = time.time() + 5.0
+        rows = []
+        while time.time() < deadline:  # until a sample at or after the region's end exists
+            rows = self._read()
+            if any(r[0] >= t1 for r in rows):
+                break
+            time.sleep(self.PERIOD_MS / 1000.0)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:  # noqa: BLE001
             self.proc.kill()
-        sm, mx, reasons = [], [], set()
+        rows = self._read()
+        os.unlink(self.fn)
+        inside = [r for r in rows if t0 <= r[0] <= hi]
+        if not inside:  # region shorter than a period: the first sample after its start
+            after = [r for r in rows if r[0] >= t0]
+            inside = after[:1]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.fn):
-            f = [x.strip() for x in line.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[3:7]):
+        reasons = set()
+        for r in inside:
+            for n, v in zip(names, r[3]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
-        os.unlink(self.fn)
+        sm = [r[1] for r in inside]
+        mx = [r[2] for r in inside]
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "sample_ms": self.PERIOD_MS}
 
 
 def peaks():
@@ -279,6 +313,8 @@ def main():
         if world > 1:
             dist.barrier()
 
+    clocks = Clocks(local)
+    clocks.start()  # before the warm-up: nvidia-smi takes a while to produce its first sample
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -288,17 +324,17 @@ def main():
     # HP_BENCH_NO_TIMING=1 measures the value without them (experiments)
     stage_timing = os.environ.get("HP_BENCH_NO_TIMING") != "1"
     ctx.set_stage_timing(stage_timing)
-    clocks = Clocks(local)
-    clocks.start()
     barrier()
     torch.cuda.synchronize()
     l0 = hp.launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.mark_start()
     start.record(main_s)
     for _ in range(args.steps):
         step()
     end.record(main_s)
     torch.cuda.synchronize()
+    clocks.mark_end()
     barrier()
     launches = hp.launch_count() - l0
     clk = clocks.stop()
