@@ -29,7 +29,6 @@
 namespace hp {
 namespace {
 
-constexpr int kCT = kFT;          // threads per component CTA (8 warps)
 
 #define GRID_LOOP(i, n) \
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)

@@ -139,6 +139,7 @@ __device__ __forceinline__ int clamp_scan(int lo, int hi, int lane) {
 // Both directions at once with each clamp (lo, hi) packed as u16x2: per level one shuffle per
 // direction instead of two, the composition on the native VIMNMX.U16x2, and the two
 // directions' shuffle latencies overlapped.  F scans left -> right, B right -> left.
+#if HP_RG_PACKSCAN
 __device__ __forceinline__ void clamp_scan_both(uint32_t& F, uint32_t& B, int lane) {
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
@@ -151,6 +152,7 @@ __device__ __forceinline__ void clamp_scan_both(uint32_t& F, uint32_t& B, int la
         if (lane + off < 32) B = bn;
     }
 }
+#endif
 
 __device__ __forceinline__ uint32_t load_word(const uint8_t* plane, int w, int h, int gx, int gy) {
     if (gy < 0 || gy >= h) return 0u;
