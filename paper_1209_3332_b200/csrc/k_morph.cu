@@ -26,7 +26,6 @@ namespace {
 
 constexpr int TW = 128;       // output tile width (pixels) = 32 words
 constexpr int TWW = TW / 4;   // output words per row
-constexpr int TH = 32;        // output tile height
 constexpr int kMaxDiam = 63;
 
 template <bool IS_MIN>
