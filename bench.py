@@ -274,6 +274,10 @@ def main():
     import torch.distributed as dist
 
     torch.cuda.set_device(local)
+    from paper_1209_3332_b200.dist import bind_to_gpu_numa
+    all_cores = sorted(os.sched_getaffinity(0))
+    near = bind_to_gpu_numa(local)  # pinned tiles and the feeder thread on the GPU's NUMA node
+    log(f"[rank {rank}] bound to {len(near) if near else 'all'} cores near GPU {local}")
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1209_3332_b200 import Context, hp
@@ -429,6 +433,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        os.sched_setaffinity(0, all_cores)  # the CPU baseline uses every host core
         P = cpu_workers()
         n = 2 * P
         v, w = oracle_rate(tiles, n, P)

@@ -25,6 +25,38 @@ NFEAT = 36
 ROW_BYTES = 8 + 4 + 4 + 4 * NFEAT  # tile_id i64, label i32, flags i32, feat f32[36]
 
 
+def bind_to_gpu_numa(device: int) -> list | None:
+    """Pin this process to the CPU cores nearest GPU `device` (NVML's CPU affinity), so the
+    pinned host buffers it allocates afterwards (first touch) and its feeder thread sit on the
+    GPU's NUMA node: host->device copies then never cross the socket link.  Returns the cores,
+    or None when NVML is unavailable.  Call before allocating pinned memory."""
+    import os
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            vis = [v.strip() for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+            if device < len(vis) and vis[device].startswith("GPU-"):
+                h = pynvml.nvmlDeviceGetHandleByUUID(vis[device])
+            else:
+                phys = int(vis[device]) if device < len(vis) else device
+                h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        finally:
+            pynvml.nvmlShutdown()
+    except Exception:  # noqa: BLE001 -- no NVML (CPU tests): leave the affinity alone
+        return None
+    cores = [64 * i + b for i, wd in enumerate(words) for b in range(64) if (wd >> b) & 1]
+    cores = [c for c in cores if c < (os.cpu_count() or 0)]
+    if not cores:
+        return None
+    try:
+        os.sched_setaffinity(0, cores)
+    except OSError:
+        return None
+    return cores
+
+
 def _default_store():
     import torch.distributed as dist
     from torch.distributed import distributed_c10d as c10d

@@ -54,6 +54,8 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1209_3332_b200.dist import bind_to_gpu_numa
+    bind_to_gpu_numa(local)  # pinned pool and feeder thread on the GPU's NUMA node
     from paper_1209_3332_b200 import Context
     from paper_1209_3332_b200.dist import DistTileSource, TileQueue, aggregate_groups, gather_rows, table_digest, to_rows
 
