@@ -150,3 +150,16 @@ def test_aggregate_groups_world2():
             else:
                 assert np.isnan(mean[g]).all()
 
+
+
+def test_bind_to_gpu_numa_without_nvml_is_a_no_op():
+    """Without a GPU/NVML the binding helper changes nothing and says so (returns None)."""
+    import os
+
+    import torch
+    from paper_1209_3332_b200.dist import bind_to_gpu_numa
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    before = os.sched_getaffinity(0)
+    assert bind_to_gpu_numa(0) is None
+    assert os.sched_getaffinity(0) == before
