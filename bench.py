@@ -25,6 +25,11 @@ import time
 
 import numpy as np
 
+# Every slot runs its tile chain on its own stream.  The default 8 hardware work queues alias
+# more streams onto shared queues, which serialises kernels of different slots behind each
+# other (r1: 12 slots 878 -> 934 tiles/s, a forked side stream per tile 674 -> 907 with 32).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -225,7 +230,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hp", choices=["hp", "reference"])
     ap.add_argument("--batch", type=int, default=12, help="distinct 4K tiles per GPU per step")
-    ap.add_argument("--slots", type=int, default=6, help="tiles in flight per GPU (n_slots)")
+    ap.add_argument("--slots", type=int, default=12, help="tiles in flight per GPU (n_slots)")
     ap.add_argument("--e2e-slots", type=int, default=14, help="context slots used by hp_run_tiles (e2e)")
     ap.add_argument("--size", type=int, default=4096)
     ap.add_argument("--no-e2e", action="store_true")

@@ -14,6 +14,8 @@ usage: python tools/run_dataset.py --config 3 [--tiles 1000] [--pool 16] [--slot
 import argparse
 import json
 import os
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # one stream per slot (see bench.py)
 import sys
 import time
 
