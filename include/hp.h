@@ -26,7 +26,10 @@
  *    HP_ERR_CUDA and the context is poisoned (every later call returns HP_ERR_CUDA).  More
  *    objects than a table holds -> HP_ERR_CAPACITY is NOT detectable without a host sync:
  *    the count is always written, rows beyond capacity are dropped, and hp_run_tiles
- *    reports HP_ERR_CAPACITY per tile.
+ *    reports HP_ERR_CAPACITY per tile.  On such a tile WHICH rows are kept is unspecified
+ *    (the first objects to finish, not the lowest labels); the kept rows are still complete,
+ *    correct and in ascending label order.  Size max_objects for the workload (a 4K tile of
+ *    the synthetic recipe has ~2,000 objects) and treat HP_ERR_CAPACITY as a failed tile.
  *  - Images are row-major.  Internal planes and the per-stage I/O of hp_stage_run are dense
  *    (pitch = width elements).
  */
@@ -82,9 +85,10 @@ typedef struct hp_params {
     int32_t open_diam;      /* odd in [1, 63]; OpenCV MORPH_ELLIPSE diam x diam (default 19,
                                "a 19x19 disk") */
     int32_t g1;             /* candidate iff g - recon > g1 (default 50) */
-    int32_t cand_min_area, cand_max_area;  /* S5 inclusive area bounds (11, 1000) */
+    int32_t cand_min_area, cand_max_area;  /* S5 inclusive area bounds (11, 1000); max <= 131072 */
     float   h;              /* h-maxima height on the distance map, > 0 (default 1.0) */
-    int32_t obj_min_area, obj_max_area;    /* S10 inclusive area bounds (21, 1000) */
+    int32_t obj_min_area, obj_max_area;    /* S10 inclusive area bounds (21, 1000); max <= 131072
+                                              (keeps S11's exact int64 moment sums in range) */
     int32_t glcm_levels;    /* must be 8 (q = g >> 5) */
     int32_t canny_low, canny_high;  /* Canny hysteresis thresholds on the L1 3x3-Sobel magnitude
                                        of g, 0 <= low <= high (defaults 100, 200; PAPER.md:604,
@@ -242,10 +246,26 @@ int64_t   hp_launch_count(void);
  * and feature the sum and the sum of squares, out_count (DEVICE, i64[n_groups]) the number of
  * rows.  off: DEVICE i64[n_groups + 1], non-decreasing.  Every thread reduces a fixed set of
  * rows and the per-group tree has a fixed shape, so the result is bit-identical run to run.
- * Async on s; HP_ERR_INVALID on null pointers or n_groups < 0.  Across GPUs the callers sum
- * the outputs with an all-reduce (paper_1209_3332_b200/dist.py aggregate_groups). */
+ * Async on s; HP_ERR_INVALID on null pointers or n_groups < 0 (feat may be NULL when every
+ * group is empty: a rank that holds no rows).  Across GPUs the callers sum the outputs with
+ * an all-reduce (paper_1209_3332_b200/dist.py aggregate_groups). */
 hp_status hp_reduce_rows(hp_ctx* ctx, const float* feat, const int64_t* off, int32_t n_groups,
                          double* out, int64_t* out_count, hp_stream s);
+/* Second pass of the per-group mean / standard deviation (two-pass, so the variance is never
+ * formed as E[x^2] - mean^2).  sums (DEVICE, [n_groups][HP_NFEAT][2] f64, the layout of
+ * hp_reduce_rows' out; only the sums [..][0] are read) and count (DEVICE, i64[n_groups]) are
+ * the TOTALS over every rank (after an all-reduce of hp_reduce_rows' outputs).  mean_m2
+ * (DEVICE, [n_groups][HP_NFEAT][2] f64) receives (mean = sum / count, NaN for an empty group;
+ * m2 = sum over THIS caller's rows [off[g], off[g+1]) of (x - mean)^2).  Callers all-reduce
+ * m2 (it is additive over ranks) and finish with hp_group_std.  feat may be NULL when every
+ * group is empty.  Deterministic (fixed row ownership and tree); async on s. */
+hp_status hp_group_center(hp_ctx* ctx, const float* feat, const int64_t* off, int32_t n_groups,
+                          const double* sums, const int64_t* count, double* mean_m2, hp_stream s);
+/* mean[g][f] = mean_m2[g][f][0]; std[g][f] = sqrt(m2 / count) (population), NaN for an
+ * empty group.  All DEVICE: mean_m2 [n_groups][HP_NFEAT][2] f64, count i64[n_groups], mean and
+ * std [n_groups][HP_NFEAT] f64.  Async on s. */
+hp_status hp_group_std(hp_ctx* ctx, const double* mean_m2, const int64_t* count, int32_t n_groups,
+                       double* mean, double* std_out, hp_stream s);
 
 #ifdef __cplusplus
 }

@@ -90,6 +90,7 @@ def lib():
             "or_segment_tile": (C.c_int, [P, C.c_int, C.c_int, i64, C.POINTER(Params), P, P, P]),
             "or_process_tile": (C.c_int, [P, C.c_int, C.c_int, i64, C.POINTER(Params), P, i32,
                                           P, P, P, P, P]),
+            "or_aggregate": (C.c_int, [P, C.c_int, P, C.c_int, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -306,3 +307,19 @@ def process_tile(rgb, params=None, cap=65536, with_times=False):
     k = int(n[0])
     out = (lab, rl[:k], rf[:k], ft[:k])
     return out + (t,) if with_times else out
+
+
+def aggregate(feat, off):
+    """NEXT-4: per group g = rows [off[g], off[g+1]) of feat [n, F] f32 ->
+    (count [G] int64, mean [G, F] f64, population std [G, F] f64), NaN for an empty group."""
+    feat = np.ascontiguousarray(feat, dtype=np.float32)
+    if feat.ndim == 1:
+        feat = feat.reshape(-1, 1)
+    off = np.ascontiguousarray(off, dtype=np.int64)
+    G, F = len(off) - 1, feat.shape[1]
+    cnt = np.empty(G, np.int64)
+    mean = np.empty((G, F), np.float64)
+    std = np.empty((G, F), np.float64)
+    fp = feat if feat.size else np.zeros((1, F), np.float32)
+    _chk(lib().or_aggregate(_p(fp), F, _p(off), G, _p(cnt), _p(mean), _p(std)), "or_aggregate")
+    return cnt, mean, std

@@ -989,3 +989,38 @@ int or_process_tile(const uint8_t* rgb, int w, int h, int64_t pitch, const or_pa
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- NEXT-4 aggregation
+// Per-image feature aggregation ("the features
+// computed for each object ... are aggregated" per image/patient for the classification
+// stage).  For each group g, rows [off[g], off[g+1]) of feat ([n][nfeat] f32): count, the
+// mean of every feature, and the population standard deviation sqrt(sum (x - mean)^2 / n),
+// both in fp64, by the plain two-pass definition.  An empty group gives NaN mean and std.
+int or_aggregate(const float* feat, int nfeat, const int64_t* off, int n_groups, int64_t* count,
+                 double* mean, double* stdv) {
+    if (nfeat < 1 || n_groups < 0 || !off || !count || !mean || !stdv) return 1;
+    const double nan = std::numeric_limits<double>::quiet_NaN();
+    for (int g = 0; g < n_groups; ++g) {
+        const int64_t r0 = off[g], r1 = off[g + 1];
+        if (r1 < r0) return 1;
+        count[g] = r1 - r0;
+        for (int f = 0; f < nfeat; ++f) {
+            if (r1 == r0) {
+                mean[(int64_t)g * nfeat + f] = nan;
+                stdv[(int64_t)g * nfeat + f] = nan;
+                continue;
+            }
+            double s = 0.0;
+            for (int64_t r = r0; r < r1; ++r) s += (double)feat[r * nfeat + f];
+            const double m = s / (double)(r1 - r0);
+            double q = 0.0;
+            for (int64_t r = r0; r < r1; ++r) {
+                const double d = (double)feat[r * nfeat + f] - m;
+                q += d * d;
+            }
+            mean[(int64_t)g * nfeat + f] = m;
+            stdv[(int64_t)g * nfeat + f] = std::sqrt(q / (double)(r1 - r0));
+        }
+    }
+    return 0;
+}

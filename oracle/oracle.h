@@ -97,6 +97,10 @@ int or_segment_tile(const uint8_t* rgb, int w, int h, int64_t pitch, const or_pa
 int or_process_tile(const uint8_t* rgb, int w, int h, int64_t pitch, const or_params* p,
                     int32_t* labels, int32_t cap, int32_t* row_label, int32_t* row_flags,
                     float* feat, int32_t* n_rows, double* t_stage);
+/* NEXT-4 per-image aggregation: per group g (rows [off[g], off[g+1]) of feat [n][nfeat]),
+ * count[g], mean[g][f] and population std[g][f] in fp64 (two-pass); NaN for an empty group. */
+int or_aggregate(const float* feat, int nfeat, const int64_t* off, int n_groups, int64_t* count,
+                 double* mean, double* stdv);
 
 #ifdef __cplusplus
 }

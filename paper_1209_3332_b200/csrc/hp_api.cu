@@ -27,6 +27,15 @@ void launch_recon_init_f32(const float* marker, const float* mask, const uint8_t
 namespace hp {
 static std::atomic<long long> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+static PerDevice g_sms;
+int num_sms() {
+    return g_sms.get([] {
+        int dev = 0, n = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+        return n;
+    });
+}
 }  // namespace hp
 
 using namespace hp;
@@ -90,6 +99,9 @@ bool params_ok(const hp_params& p, std::string* why) {
     if (p.g1 < -256 || p.g1 > 255) return bad("g1 out of range");
     if (p.cand_min_area < 0 || p.cand_min_area > p.cand_max_area) return bad("cand area bounds");
     if (p.obj_min_area < 0 || p.obj_min_area > p.obj_max_area) return bad("obj area bounds");
+    // S11's exact moments A*sum(x^2) - (sum x)^2 stay inside int64 for A <= 2^17 on tiles up to
+    // 16384 px wide (2^17 * 2^17 * 2^28 = 2^62)
+    if (p.cand_max_area > (1 << 17) || p.obj_max_area > (1 << 17)) return bad("area bounds above 131072");
     if (!(p.h > 0.0f) || !std::isfinite(p.h)) return bad("h must be finite and > 0");
     if (p.glcm_levels != 8) return bad("glcm_levels must be 8");
     if (p.canny_low < 0 || p.canny_high < p.canny_low) return bad("need 0 <= canny_low <= canny_high");
@@ -159,6 +171,7 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
             cudaMemset2DAsync(labels, lpitch * sizeof(int32_t), 0, w * sizeof(int32_t), h, s);
             cudaMemsetAsync(n_objects, 0, sizeof(int32_t), s);
             for (int k = 2; k <= 10; ++k) ev(ctx, sl, k, s);
+            if (!table) ev(ctx, sl, 11, s);  // no feature stage follows: close the event set
             return check_launch(ctx, "bg skip");
         }
     }
@@ -230,6 +243,9 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
             ev(ctx, sl, 11, s);
         }
     }
+    // hp_segment_tile (no table): no feature stage follows, so S11's closing event is
+    // recorded here -- hp_get_stage_times synchronises on it
+    if (!table) ev(ctx, sl, 11, s);
     return check_launch(ctx, "segment");
 }
 
@@ -530,12 +546,37 @@ hp_status hp_reduce_rows(hp_ctx* ctx, const float* feat, const int64_t* off, int
                          int64_t* out_count, hp_stream s) {
     hp_status st = enter(ctx, 0);
     if (st) return st;
-    if (n_groups < 0 || (n_groups > 0 && (!feat || !off || !out || !out_count))) {
+    // feat may be NULL when every group is empty (a rank that holds no rows)
+    if (n_groups < 0 || (n_groups > 0 && (!off || !out || !out_count))) {
         set_err(ctx, "hp_reduce_rows: null pointer or n_groups < 0");
         return HP_ERR_INVALID;
     }
     launch_reduce_rows(feat, off, n_groups, out, out_count, (cudaStream_t)s);
     return check_launch(ctx, "reduce_rows");
+}
+
+hp_status hp_group_center(hp_ctx* ctx, const float* feat, const int64_t* off, int32_t n_groups, const double* sums,
+                          const int64_t* count, double* mean_m2, hp_stream s) {
+    hp_status st = enter(ctx, 0);
+    if (st) return st;
+    if (n_groups < 0 || (n_groups > 0 && (!off || !sums || !count || !mean_m2))) {
+        set_err(ctx, "hp_group_center: null pointer or n_groups < 0");
+        return HP_ERR_INVALID;
+    }
+    launch_group_center(feat, off, n_groups, sums, count, mean_m2, (cudaStream_t)s);
+    return check_launch(ctx, "group_center");
+}
+
+hp_status hp_group_std(hp_ctx* ctx, const double* mean_m2, const int64_t* count, int32_t n_groups, double* mean,
+                       double* std_out, hp_stream s) {
+    hp_status st = enter(ctx, 0);
+    if (st) return st;
+    if (n_groups < 0 || (n_groups > 0 && (!mean_m2 || !count || !mean || !std_out))) {
+        set_err(ctx, "hp_group_std: null pointer or n_groups < 0");
+        return HP_ERR_INVALID;
+    }
+    launch_group_std(mean_m2, count, n_groups, mean, std_out, (cudaStream_t)s);
+    return check_launch(ctx, "group_std");
 }
 
 hp_status hp_stage_times_accum(hp_ctx* ctx, float* ms11, int32_t* count) {

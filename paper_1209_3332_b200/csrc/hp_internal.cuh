@@ -139,6 +139,9 @@ struct PerDevice {
         return value[dev];
     }
 };
+// Number of SMs of the current device (148 on a B200), cached per device: every grid that is
+// sized "a multiple of the SM count" takes it from here instead of a literal.
+int num_sms();
 // S1
 void launch_cd(const uint8_t* rgb, int w, int h, int64_t pitch, const float* lut,
                const hp_params& p, uint8_t* g, uint8_t* flags, unsigned long long* bg_count,
@@ -221,6 +224,10 @@ void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t*
 // per-image aggregation (k_agg.cu): segmented fp64 sums / sums of squares of feature rows
 void launch_reduce_rows(const float* feat, const int64_t* off, int32_t n_groups, double* out, int64_t* count,
                         cudaStream_t s);
+void launch_group_center(const float* feat, const int64_t* off, int32_t n_groups, const double* sums,
+                         const int64_t* count, double* mean_m2, cudaStream_t s);
+void launch_group_std(const double* mean_m2, const int64_t* count, int32_t n_groups, double* mean, double* std_out,
+                      cudaStream_t s);
 // device row arena of hp_run_tiles (k_agg.cu): reserve min(*nrows, tab_cap) rows at a.cursor
 // (offset -> *base), then copy the tile's rows with tile id *tile_id, clipped to capacity
 void launch_arena_append(const int32_t* nrows, int32_t tab_cap, const int32_t* lab, const int32_t* fl,

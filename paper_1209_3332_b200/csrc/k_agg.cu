@@ -12,12 +12,25 @@ namespace {
 constexpr int kAT = 256;  // threads per group block
 constexpr int kAF = 9;    // features per pass (HP_NFEAT = 36 -> 4 passes; 39 KB of shared memory)
 
+// kCentered = false: per group and feature the sum and the sum of squares of the rows;
+// kCentered = true (second pass): mean = sum / count from the (all-reduced) first-pass sums,
+// then the sum of squared deviations from that mean, so the variance is never formed as the
+// cancellation-prone E[x^2] - mean^2.  Both write [G][36][2]: (sum, sumsq) or (mean, m2).
+template <bool kCentered>
 __global__ void __launch_bounds__(kAT) k_reduce_rows(const float* __restrict__ feat, const int64_t* __restrict__ off,
+                                                     const double* __restrict__ sums,
+                                                     const int64_t* __restrict__ gcount,
                                                      double* __restrict__ out, int64_t* __restrict__ count) {
     __shared__ double red[kAT][2 * kAF + 1];  // (+1: no bank conflicts between threads)
+    __shared__ double mean_s[HP_NFEAT];
     const int gi = blockIdx.x;
     const int64_t r0 = off[gi], r1 = off[gi + 1];
-    if (threadIdx.x == 0) count[gi] = r1 - r0;
+    if (!kCentered && threadIdx.x == 0) count[gi] = r1 - r0;
+    if (kCentered && threadIdx.x < HP_NFEAT) {
+        const int64_t n = gcount[gi];
+        mean_s[threadIdx.x] = n > 0 ? sums[((int64_t)gi * HP_NFEAT + threadIdx.x) * 2] / (double)n : __longlong_as_double(0x7ff8000000000000LL);
+    }
+    __syncthreads();
     for (int f0 = 0; f0 < HP_NFEAT; f0 += kAF) {
         double s[kAF], q[kAF];
 #pragma unroll
@@ -26,7 +39,7 @@ __global__ void __launch_bounds__(kAT) k_reduce_rows(const float* __restrict__ f
             const float* row = feat + r * HP_NFEAT + f0;
 #pragma unroll
             for (int k = 0; k < kAF; ++k) {
-                const double v = (double)row[k];
+                const double v = kCentered ? (double)row[k] - mean_s[f0 + k] : (double)row[k];
                 s[k] += v;
                 q[k] += v * v;
             }
@@ -42,9 +55,24 @@ __global__ void __launch_bounds__(kAT) k_reduce_rows(const float* __restrict__ f
                 for (int k = 0; k < 2 * kAF; ++k) red[threadIdx.x][k] += red[threadIdx.x + half][k];
             __syncthreads();
         }
-        if (threadIdx.x < 2 * kAF) out[((int64_t)gi * HP_NFEAT + f0 + threadIdx.x / 2) * 2 + (threadIdx.x & 1)] =
-            red[0][threadIdx.x];
+        if (threadIdx.x < 2 * kAF) {
+            const int k = threadIdx.x / 2, which = threadIdx.x & 1;
+            double v = red[0][threadIdx.x];
+            if (kCentered && which == 0) v = mean_s[f0 + k];
+            out[((int64_t)gi * HP_NFEAT + f0 + k) * 2 + which] = v;
+        }
         __syncthreads();
+    }
+}
+
+// std = sqrt(m2 / count) (population), NaN for an empty group; mean passes through.
+__global__ void k_group_std(const double* __restrict__ mm2, const int64_t* __restrict__ gcount, int32_t n_groups,
+                            double* __restrict__ mean_out, double* __restrict__ std_out) {
+    const int64_t n = (int64_t)n_groups * HP_NFEAT;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = gcount[i / HP_NFEAT];
+        mean_out[i] = mm2[2 * i];
+        std_out[i] = c > 0 ? sqrt(mm2[2 * i + 1] / (double)c) : __longlong_as_double(0x7ff8000000000000LL);
     }
 }
 
@@ -54,7 +82,20 @@ void launch_reduce_rows(const float* feat, const int64_t* off, int32_t n_groups,
                         cudaStream_t s) {
     static_assert(HP_NFEAT % kAF == 0, "features per pass");
     if (n_groups == 0) return;
-    (note_launch(), k_reduce_rows<<<n_groups, kAT, 0, s>>>(feat, off, out, count));
+    (note_launch(), k_reduce_rows<false><<<n_groups, kAT, 0, s>>>(feat, off, nullptr, nullptr, out, count));
+}
+
+void launch_group_center(const float* feat, const int64_t* off, int32_t n_groups, const double* sums,
+                         const int64_t* count, double* mean_m2, cudaStream_t s) {
+    if (n_groups == 0) return;
+    (note_launch(), k_reduce_rows<true><<<n_groups, kAT, 0, s>>>(feat, off, sums, count, mean_m2, nullptr));
+}
+
+void launch_group_std(const double* mean_m2, const int64_t* count, int32_t n_groups, double* mean, double* std_out,
+                      cudaStream_t s) {
+    if (n_groups == 0) return;
+    const int grid = std::max(1, std::min(num_sms(), (int)(((int64_t)n_groups * HP_NFEAT + 255) / 256)));
+    (note_launch(), k_group_std<<<grid, 256, 0, s>>>(mean_m2, count, n_groups, mean, std_out));
 }
 
 }  // namespace hp
@@ -97,7 +138,7 @@ void launch_arena_append(const int32_t* nrows, int32_t tab_cap, const int32_t* l
                          const float* feat, int64_t* base, const int64_t* tile_id, const hp_row_arena& a,
                          cudaStream_t s) {
     (note_launch(), k_arena_reserve<<<1, 1, 0, s>>>(nrows, tab_cap, a.cursor, base));
-    const int grid = std::max(1, std::min(148, (int)(((int64_t)tab_cap * HP_NFEAT + 1023) / 1024)));
+    const int grid = std::max(1, std::min(num_sms(), (int)(((int64_t)tab_cap * HP_NFEAT + 1023) / 1024)));
     (note_launch(), k_arena_copy<<<grid, 256, 0, s>>>(nrows, tab_cap, lab, fl, feat, base, tile_id, a));
 }
 

@@ -310,7 +310,7 @@ __global__ void k_ccl_to_labels(const int32_t* __restrict__ lab, int64_t n, int3
 
 inline int grid_for(int64_t n) {
     int64_t b = (n + 255) / 256;
-    return (int)std::min<int64_t>(b, 148 * 16);
+    return (int)std::min<int64_t>(b, num_sms() * 16);
 }
 
 }  // namespace

@@ -122,7 +122,7 @@ void launch_cd(const uint8_t* rgb, int w, int h, int64_t pitch, const float* lut
     if (n == 0) return;
     bool vec = ((uintptr_t)rgb % 16 == 0) && (pitch % 16 == 0) && (w % 16 == 0) &&
                ((uintptr_t)g % 16 == 0) && ((uintptr_t)flags % 16 == 0);
-    const int grid = 148 * 8;
+    const int grid = num_sms() * 8;
     if (vec) {
         int64_t nchunks = n / 16;
         int blocks = (int)std::min<int64_t>((nchunks + 255) / 256, grid);

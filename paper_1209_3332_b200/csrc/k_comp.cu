@@ -33,7 +33,7 @@ namespace {
 #define GRID_LOOP(i, n) \
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
-inline int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 16); }
+inline int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, num_sms() * 16); }
 
 struct CompArgs {
     const int32_t* labF;   // per F pixel: the root of its F component (written by S6), else ~0
@@ -865,11 +865,11 @@ void launch_components(const int32_t* count5, const uint8_t* enc, const uint8_t*
     once.get([&] { return (int)cudaFuncSetAttribute(k_comp_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw); });
     (note_launch(), k_comp_classify<<<grid_for(cap), 256, 0, s>>>(a, count5, cap, sl.sc_root, sl.sc_bbox,
                                                                    sl.sc_big, nbig));
-    (note_launch(), k_comp_fused<<<148 * HP_COMP_BPS, kWarpsPB * 32, smw, s>>>(a, count5, cap, sl.sc_root, sl.sc_bbox,
+    (note_launch(), k_comp_fused<<<num_sms() * HP_COMP_BPS, kWarpsPB * 32, smw, s>>>(a, count5, cap, sl.sc_root, sl.sc_bbox,
                                                                      sl.sc_big, nbig, heads));
     (note_launch(), k_comp_huge<<<1, kHugeT, 0, s>>>(a, sl.sc_root, sl.sc_bbox, carve_big(sl)));
     if (table) {
-        (note_launch(), k_rows_scatter<<<std::max(1, std::min(148 * 2, (max_objects + 7) / 8)), 256, 0, s>>>(
+        (note_launch(), k_rows_scatter<<<std::max(1, std::min(num_sms() * 2, (max_objects + 7) / 8)), 256, 0, s>>>(
             rows, max_objects, sl.stg_label, sl.stg_flags, sl.stg_feat, table->label, table->flags, table->feat,
             table->capacity));
         (note_launch(), k_copy_i32<<<1, 1, 0, s>>>(rows, table->n_rows_dev));
@@ -894,7 +894,7 @@ void launch_fill_components(const uint8_t* big0, int w, int h, Slot& sl, const i
     const int32_t cap = sl.comp_cap;
     (note_launch(), k_win_classify<<<grid_for(cap), 256, 0, s>>>(count, cap, sl.sc_bbox, sl.sc_big, nbig, sl.sc_huge,
                                                                   nhuge));
-    (note_launch(), k_fill_fused<<<148 * HP_FILL_BPS, kWarpsPB * 32, smw, s>>>(a, count, cap, sl.sc_root, sl.sc_bbox,
+    (note_launch(), k_fill_fused<<<num_sms() * HP_FILL_BPS, kWarpsPB * 32, smw, s>>>(a, count, cap, sl.sc_root, sl.sc_bbox,
                                                                      sl.sc_area, sl.sc_big, nbig, heads));
     (note_launch(), k_fill_huge<<<1, kHugeT, 0, s>>>(a, sl.sc_root, sl.sc_bbox, sl.sc_area, sl.sc_huge, nhuge,
                                                     carve_big(sl)));

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(256) k_edt_row(const uint8_t* __restrict__ F, 
     }
 }
 
-inline int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 16); }
+inline int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, num_sms() * 16); }
 
 }  // namespace
 

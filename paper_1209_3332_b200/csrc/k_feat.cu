@@ -24,7 +24,7 @@ namespace {
 #define GRID_LOOP(i, n) \
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
-inline int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 16); }
+inline int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, num_sms() * 16); }
 
 __global__ void k_obj_find(const int32_t* __restrict__ labels, int64_t lpitch, int w, int h,
                            int32_t* __restrict__ cnt, int32_t* __restrict__ roots, int32_t cap) {
@@ -139,11 +139,11 @@ void launch_features(const int32_t* labels, int64_t lpitch, const uint8_t* g, co
     cudaMemsetAsync(cnt, 0, sizeof(int32_t), s);
     if (n > 0) {
         (note_launch(), k_obj_find<<<grid_for(n), 256, 0, s>>>(labels, lpitch, w, h, cnt, sl.obj_root, max_objects));
-        (note_launch(), k_obj_rank<<<std::max(1, std::min(148 * 4, (max_objects + 255) / 256)), 256, 0, s>>>(
+        (note_launch(), k_obj_rank<<<std::max(1, std::min(num_sms() * 4, (max_objects + 255) / 256)), 256, 0, s>>>(
             cnt, max_objects, sl.obj_root, sl.obj_rank, sl.aux));
-        (note_launch(), k_bbox_init<<<std::max(1, std::min(148 * 4, (max_objects + 255) / 256)), 256, 0, s>>>(cnt, max_objects, sl.obj_bbox));
+        (note_launch(), k_bbox_init<<<std::max(1, std::min(num_sms() * 4, (max_objects + 255) / 256)), 256, 0, s>>>(cnt, max_objects, sl.obj_bbox));
         (note_launch(), k_obj_bbox<<<grid_for(n), 256, 0, s>>>(labels, lpitch, w, h, cnt, max_objects, sl.aux, sl.obj_bbox));
-        (note_launch(), k_obj_feat<<<148 * 8, kFT, 0, s>>>(labels, lpitch, g, edge, w, h, cnt, max_objects, sl.obj_rank,
+        (note_launch(), k_obj_feat<<<num_sms() * 8, kFT, 0, s>>>(labels, lpitch, g, edge, w, h, cnt, max_objects, sl.obj_rank,
                                            sl.obj_bbox, row_label, row_flags, feat, capacity));
     }
     (note_launch(), k_copy_count<<<1, 1, 0, s>>>(cnt, n_rows));

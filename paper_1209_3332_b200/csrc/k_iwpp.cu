@@ -326,7 +326,7 @@ __global__ void k_recon_init_f32(const float* __restrict__ marker, const float* 
         R[i] = (dom == nullptr || dom[i]) ? fminf(marker[i], mask[i]) : NAN;
 }
 
-inline int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, 148 * 16); }
+inline int grid_for(int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, num_sms() * 16); }
 
 // the tile grid follows the current image, not the context's maximum size
 Worklist sized(const Worklist& wl, int w, int h) {
@@ -352,7 +352,7 @@ void wl_init_from_mask(const Worklist& wl0, const uint8_t* mask, int w, int h, c
     Worklist wl = sized(wl0, w, h);
     (note_launch(), k_wl_reset<<<grid_for(wl.cap), 256, 0, s>>>(wl, 0));
     int n = wl.ntx * wl.nty;
-    (note_launch(), k_wl_seed_mask<<<(int)std::min<int64_t>((n + 7) / 8, 148 * 16), 256, 0, s>>>(wl, mask, w, h));
+    (note_launch(), k_wl_seed_mask<<<(int)std::min<int64_t>((n + 7) / 8, num_sms() * 16), 256, 0, s>>>(wl, mask, w, h));
 }
 
 void launch_recon_init_u8(const uint8_t* marker, const uint8_t* mask, uint8_t* R, int w, int h,

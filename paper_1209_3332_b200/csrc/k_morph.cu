@@ -222,7 +222,7 @@ void launch_r(const uint8_t* g, int w, int h, uint8_t* tmp, uint8_t* out, cudaSt
     });
     // persistent: as many blocks as fit (shared memory allows 4 per SM), each looping over tiles
     const int ntiles = ((w + TW2 - 1) / TW2) * ((h + TH2 - 1) / TH2);
-    const int grid = std::max(1, std::min(ntiles, 148 * HP_MORPH_BPS));
+    const int grid = std::max(1, std::min(ntiles, num_sms() * HP_MORPH_BPS));
     (note_launch(), k_morph_r<true, R><<<grid, 256, smem, s>>>(g, w, h, tmp));
     (note_launch(), k_morph_r<false, R><<<grid, 256, smem, s>>>(tmp, w, h, out));
 }

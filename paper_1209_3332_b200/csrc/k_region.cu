@@ -818,7 +818,7 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
     wl.ntx = (w + RX * SW - 1) / (RX * SW);
     wl.nty = (h + RY * kTile - 1) / (RY * kTile);
     const int n = wl.ntx * wl.nty;
-    (note_launch(), k_rg_reset<<<(int)std::min<int64_t>((std::max<int64_t>(wl.cap, (int64_t)n * NW) + 255) / 256, 148 * 16), 256, 0, s>>>(wl));
+    (note_launch(), k_rg_reset<<<(int)std::min<int64_t>((std::max<int64_t>(wl.cap, (int64_t)n * NW) + 255) / 256, num_sms() * 16), 256, 0, s>>>(wl));
 #if HP_RG_ORDER >= 2
     // keys in the region-state array past the regions (it is sized for the 32x32 tiles of the
     // tile engine, 32 entries per region)

@@ -235,47 +235,47 @@ def group_offsets(rows: Rows, group_of_tile, n_groups: int) -> np.ndarray:
     return np.searchsorted(gid, np.arange(n_groups + 1), side="left").astype(np.int64)
 
 
-def aggregate_groups(rows: Rows, group_of_tile, n_groups: int, reduce=None, device=None):
-    """Per-image (per-group) feature aggregation: every rank reduces its own
-    rows per group -- on the GPU through hp_reduce_rows (``reduce`` = a Context, or any
-    callable (feat, off) -> (sums [G, 36, 2] f64, counts [G] i64)) -- then one all_reduce(SUM)
-    of the partial sums over the process group (NCCL on GPUs, gloo on CPU) gives every rank
-    the totals.  Returns (count [G], mean [G, 36], std [G, 36]) in float64 (population std)."""
+def aggregate_groups(rows: Rows, group_of_tile, n_groups: int, reduce, device=None):
+    """Per-image (per-group) feature aggregation: the mean
+    and population standard deviation of every feature over each group's object rows, in two
+    device passes with one all-reduce after each (NCCL on GPUs, gloo on CPU):
+
+    1. ``reduce.reduce_rows`` (hp_reduce_rows): per-rank segmented sums and row counts;
+       all_reduce(SUM) gives the totals, hence every group's mean.
+    2. ``reduce.group_center`` (hp_group_center): per-rank sums of squared deviations from
+       that mean; all_reduce(SUM); ``reduce.group_std`` (hp_group_std) finishes std on the
+       device.
+
+    ``reduce`` is a Context (the device kernels); there is no host fallback.  A rank holding
+    no rows still takes part in both all-reduces (its partial sums are zero).  Returns
+    (count [G], mean [G, 36], std [G, 36]) as numpy (int64, float64, float64); NaN for an
+    empty group."""
     import torch
     import torch.distributed as dist
+    if reduce is None or not all(hasattr(reduce, m) for m in ("reduce_rows", "group_center", "group_std")):
+        raise TypeError("aggregate_groups needs a Context (hp_reduce_rows / hp_group_center / hp_group_std)")
     off = group_offsets(rows, group_of_tile, n_groups)
     dev = device if device is not None else torch.device("cpu")
-    if reduce is None or callable(reduce) and not hasattr(reduce, "reduce_rows"):
-        fn = reduce if reduce is not None else _reduce_numpy
-        sums, cnt = fn(rows.feat, off)
-        sums_t = torch.from_numpy(np.ascontiguousarray(sums, np.float64)).to(dev)
-        cnt_t = torch.from_numpy(np.ascontiguousarray(cnt, np.int64)).to(dev)
-    else:  # a Context: the device kernel
-        feat_t = torch.from_numpy(np.ascontiguousarray(rows.feat)).to(dev)
-        off_t = torch.from_numpy(off).to(dev)
-        sums_t = torch.empty((n_groups, NFEAT, 2), dtype=torch.float64, device=dev)
-        cnt_t = torch.empty(n_groups, dtype=torch.int64, device=dev)
-        if n_groups:
-            reduce.reduce_rows(feat_t, off_t, sums_t, cnt_t)
-    if dist.is_initialized() and dist.get_world_size() > 1:
+    multi = dist.is_initialized() and dist.get_world_size() > 1
+    feat_t = torch.from_numpy(np.ascontiguousarray(rows.feat)).to(dev)
+    off_t = torch.from_numpy(off).to(dev)
+    sums_t = torch.zeros((n_groups, NFEAT, 2), dtype=torch.float64, device=dev)
+    cnt_t = torch.zeros(n_groups, dtype=torch.int64, device=dev)
+    mm2_t = torch.zeros((n_groups, NFEAT, 2), dtype=torch.float64, device=dev)
+    mean_t = torch.zeros((n_groups, NFEAT), dtype=torch.float64, device=dev)
+    std_t = torch.zeros((n_groups, NFEAT), dtype=torch.float64, device=dev)
+    if n_groups:
+        reduce.reduce_rows(feat_t, off_t, sums_t, cnt_t)
+    if multi:
         dist.all_reduce(sums_t, op=dist.ReduceOp.SUM)
         dist.all_reduce(cnt_t, op=dist.ReduceOp.SUM)
-    sums = sums_t.cpu().numpy()
-    cnt = cnt_t.cpu().numpy()
-    with np.errstate(invalid="ignore", divide="ignore"):
-        n = cnt[:, None].astype(np.float64)
-        mean = sums[:, :, 0] / n
-        var = np.maximum(sums[:, :, 1] / n - mean * mean, 0.0)
-    return cnt, mean, np.sqrt(var)
-
-
-def _reduce_numpy(feat, off):
-    """Host stand-in for hp_reduce_rows (tests, CPU runs)."""
-    G = len(off) - 1
-    sums = np.zeros((G, NFEAT, 2), np.float64)
-    for g in range(G):
-        f = feat[off[g]:off[g + 1]].astype(np.float64)
-        sums[g, :, 0] = f.sum(axis=0)
-        sums[g, :, 1] = (f * f).sum(axis=0)
-    return sums, np.diff(off).astype(np.int64)
-
+    if n_groups:
+        reduce.group_center(feat_t, off_t, sums_t, cnt_t, mm2_t)
+    if multi:
+        # only the m2 half is additive; the mean half is identical on every rank
+        m2 = mm2_t[:, :, 1].contiguous()
+        dist.all_reduce(m2, op=dist.ReduceOp.SUM)
+        mm2_t[:, :, 1] = m2
+    if n_groups:
+        reduce.group_std(mm2_t, cnt_t, mean_t, std_t)
+    return cnt_t.cpu().numpy(), mean_t.cpu().numpy(), std_t.cpu().numpy()

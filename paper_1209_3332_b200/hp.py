@@ -24,7 +24,9 @@ FEATURE_NAMES = [
     "grad_mean", "grad_std", "grad_skew", "grad_kurt",
     "glcm_asm", "glcm_contrast", "glcm_correlation", "glcm_homogeneity", "glcm_entropy",
     "glcm_shade", "glcm_prominence", "glcm_maxprob",
+    "edge_count", "edge_frac",
 ]
+assert len(FEATURE_NAMES) == NFEAT
 
 STAGES = ["CD", "RBC", "OPEN", "RECON", "AREA", "FILL", "EDT", "MARKERS", "WATERSHED",
           "BWLABEL", "FEATURES", "IWPP_RAW", "CCL8", "CCL4", "RECON_F32", "CANNY"]
@@ -36,7 +38,8 @@ STATUS = {0: "ok", 1: "invalid argument", 2: "CUDA error", 3: "out of memory",
 EXPORTS = ["hp_default_params", "hp_ctx_create", "hp_ctx_destroy", "hp_status_str",
            "hp_last_error", "hp_version", "hp_segment_tile", "hp_features_tile",
            "hp_process_tile", "hp_run_tiles", "hp_stage_run", "hp_set_stage_timing",
-           "hp_get_stage_times", "hp_stage_times_accum", "hp_launch_count", "hp_reduce_rows"]
+           "hp_get_stage_times", "hp_stage_times_accum", "hp_launch_count", "hp_reduce_rows",
+           "hp_group_center", "hp_group_std"]
 
 
 class HPError(RuntimeError):
@@ -149,6 +152,8 @@ def lib():
             "hp_stage_times_accum": (C.c_int, [P, C.POINTER(C.c_float), C.POINTER(C.c_int32)]),
             "hp_launch_count": (C.c_int64, []),
             "hp_reduce_rows": (C.c_int, [P, P, P, i32, P, P, P]),
+            "hp_group_center": (C.c_int, [P, P, P, i32, P, P, P, P]),
+            "hp_group_std": (C.c_int, [P, P, P, i32, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -245,6 +250,18 @@ class Context:
         self._chk(lib().hp_reduce_rows(self._h, feat.data_ptr(), off.data_ptr(), off.shape[0] - 1,
                                        out.data_ptr(), out_count.data_ptr(), _stream(stream)), "hp_reduce_rows")
 
+    def group_center(self, feat, off, sums, count, mean_m2, stream=None):
+        """hp_group_center: per group, mean = sums[..., 0] / count and the sum over these rows
+        of (x - mean)^2 -> mean_m2 [G, 36, 2] f64 (all device tensors; sums/count are totals)."""
+        self._chk(lib().hp_group_center(self._h, feat.data_ptr(), off.data_ptr(), off.shape[0] - 1,
+                                        sums.data_ptr(), count.data_ptr(), mean_m2.data_ptr(), _stream(stream)),
+                  "hp_group_center")
+
+    def group_std(self, mean_m2, count, mean, std, stream=None):
+        """hp_group_std: mean [G, 36] and population std = sqrt(m2 / count) [G, 36] (f64)."""
+        self._chk(lib().hp_group_std(self._h, mean_m2.data_ptr(), count.data_ptr(), count.shape[0],
+                                     mean.data_ptr(), std.data_ptr(), _stream(stream)), "hp_group_std")
+
     def process_tile(self, slot, rgb, labels, n_objects, t_label, t_flags, t_feat, n_rows,
                      stream=None):
         im = self.image(rgb)
@@ -287,12 +304,19 @@ class Context:
         With arena = (tile_ptr, label_ptr, flags_ptr, feat_ptr, capacity, cursor_ptr) (device
         pointers, hp_row_arena) the rows are appended on the device instead and
         on_done(tile_id, n_rows, status) is called."""
+        # ctypes prints and swallows an exception raised inside a C callback, so both
+        # callbacks store the first one; after it no further tile is fed, and it is re-raised
+        # once hp_run_tiles has returned (the tiles already in flight are drained by then).
         keep = []
+        err = []
 
         def _next(user, pp, ppitch, ptid):
+            if err:
+                return 1
             try:
                 r = next_tile()
-            except Exception:  # noqa: BLE001 -- never raise through C
+            except BaseException as e:  # noqa: BLE001 -- never raise through C
+                err.append(e)
                 return 1
             if r is None:
                 return 1
@@ -303,13 +327,18 @@ class Context:
             return 0
 
         def _done(user, tid, n, plab, pflags, pfeat, st):
-            if arena is not None:
-                on_done(int(tid), int(n), int(st))
+            if err:
                 return
-            lab = np.ctypeslib.as_array(plab, shape=(max(n, 1),))[:n].copy()
-            fl = np.ctypeslib.as_array(pflags, shape=(max(n, 1),))[:n].copy()
-            ft = np.ctypeslib.as_array(pfeat, shape=(max(n, 1) * NFEAT,))[:n * NFEAT].copy()
-            on_done(int(tid), lab, fl, ft.reshape(n, NFEAT), int(st))
+            try:
+                if arena is not None:
+                    on_done(int(tid), int(n), int(st))
+                    return
+                lab = np.ctypeslib.as_array(plab, shape=(max(n, 1),))[:n].copy()
+                fl = np.ctypeslib.as_array(pflags, shape=(max(n, 1),))[:n].copy()
+                ft = np.ctypeslib.as_array(pfeat, shape=(max(n, 1) * NFEAT,))[:n * NFEAT].copy()
+                on_done(int(tid), lab, fl, ft.reshape(n, NFEAT), int(st))
+            except BaseException as e:  # noqa: BLE001
+                err.append(e)
 
         nf, df = NEXT_FN(_next), DONE_FN(_done)
         keep += [nf, df]
@@ -317,4 +346,7 @@ class Context:
         ar = None if arena is None else RowArena(*arena)
         sink = ResultSink(df, None, C.pointer(ar) if ar is not None else None)
         keep.append(ar)
-        self._chk(lib().hp_run_tiles(self._h, C.byref(src), C.byref(sink)), "hp_run_tiles")
+        st = lib().hp_run_tiles(self._h, C.byref(src), C.byref(sink))
+        if err:
+            raise err[0]
+        self._chk(st, "hp_run_tiles")

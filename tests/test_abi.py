@@ -117,3 +117,13 @@ def test_struct_layouts_match_header(tmp_path):
     subprocess.run([cc, "-std=c99", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
     assert got == expect
+
+
+def test_feature_names_follow_header_enum():
+    """hp.FEATURE_NAMES has one name per HP_F_* column, in the enum's order."""
+    txt = open(os.path.join(ROOT, "include", "hp.h")).read()
+    body = txt[txt.index("HP_F_AREA = 0"):txt.index("HP_NFEAT = 36")]
+    enum = re.findall(r"\bHP_F_([A-Z_0-9]+)", body)
+    assert len(enum) == hp.NFEAT == len(hp.FEATURE_NAMES)
+    for e, n in zip(enum, hp.FEATURE_NAMES):
+        assert e.lower() == n, (e, n)

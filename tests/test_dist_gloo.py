@@ -113,24 +113,62 @@ def test_single_process_queue():
     assert blocks == [[0, 1, 2, 3], [4, 5, 6, 7], [8, 9]]
 
 
-def _agg_worker(rank, world, port, n_tiles, out_q):
+class HostReducer:
+    """Test stand-in for a Context's three aggregation kernels (hp_reduce_rows,
+    hp_group_center, hp_group_std) on CPU tensors, so the gloo tests exercise the host logic
+    of dist.aggregate_groups (two passes, two all-reduces) without a GPU.  The product has no
+    host reducer."""
+
+    @staticmethod
+    def reduce_rows(feat, off, out, count):
+        f, o = feat.numpy().astype(np.float64), off.numpy()
+        for g in range(len(o) - 1):
+            x = f[o[g]:o[g + 1]]
+            out[g, :, 0] = torch.from_numpy(x.sum(axis=0))
+            out[g, :, 1] = torch.from_numpy((x * x).sum(axis=0))
+            count[g] = int(o[g + 1] - o[g])
+
+    @staticmethod
+    def group_center(feat, off, sums, count, mean_m2):
+        f, o = feat.numpy().astype(np.float64), off.numpy()
+        for g in range(len(o) - 1):
+            n = int(count[g])
+            m = sums[g, :, 0].numpy() / n if n else np.full(36, np.nan)
+            mean_m2[g, :, 0] = torch.from_numpy(m)
+            mean_m2[g, :, 1] = torch.from_numpy(((f[o[g]:o[g + 1]] - m) ** 2).sum(axis=0))
+
+    @staticmethod
+    def group_std(mean_m2, count, mean, std):
+        for g in range(count.shape[0]):
+            n = int(count[g])
+            mean[g] = mean_m2[g, :, 0]
+            std[g] = torch.sqrt(mean_m2[g, :, 1] / n) if n else float("nan")
+
+
+def _agg_worker(rank, world, port, n_tiles, out_q, empty_rank=-1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    mine = {t: _fake_rows(t) for t in range(n_tiles) if t % world == rank}   # disjoint tiles
-    cnt, mean, std = aggregate_groups(to_rows(mine), lambda tile: tile // 5, (n_tiles + 4) // 5)
+    # disjoint tiles; with empty_rank set, that rank holds no rows at all (ADVICE r1: it must
+    # still join both all-reduces instead of failing and hanging the others)
+    mine = {t: _fake_rows(t) for t in range(n_tiles)
+            if (t % world == rank if empty_rank < 0 else rank != empty_rank)}
+    cnt, mean, std = aggregate_groups(to_rows(mine), lambda tile: tile // 5, (n_tiles + 4) // 5, HostReducer())
     out_q.put((rank, cnt, mean, std))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_aggregate_groups_world2():
-    """SURVEY NEXT-4 host logic: per-rank segmented sums + all_reduce == one process's
-    per-group numpy mean / population std over the union of the rows."""
+@pytest.mark.parametrize("empty_rank", [-1, 1])
+def test_aggregate_groups_world2(empty_rank):
+    """SURVEY NEXT-4 host logic: per-rank partial sums, all-reduce, per-rank centred sums,
+    all-reduce == the oracle's per-group mean / population std over the union of the rows
+    (also when one rank holds no rows)."""
+    import oracle
     n_tiles = 23
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_agg_worker, args=(r, 2, port, n_tiles, q)) for r in range(2)]
+    procs = [ctx.Process(target=_agg_worker, args=(r, 2, port, n_tiles, q, empty_rank)) for r in range(2)]
     for p in procs:
         p.start()
     outs = sorted([q.get(timeout=120) for _ in procs], key=lambda o: o[0])
@@ -139,16 +177,12 @@ def test_aggregate_groups_world2():
         assert p.exitcode == 0
     ref = to_rows({t: _fake_rows(t) for t in range(n_tiles)})
     G = (n_tiles + 4) // 5
+    off = np.searchsorted(ref.tile // 5, np.arange(G + 1))
+    rc, rm, rs = oracle.aggregate(ref.feat, off)
     for _, cnt, mean, std in outs:
-        for g in range(G):
-            sel = (ref.tile // 5) == g
-            assert cnt[g] == sel.sum()
-            if sel.sum():
-                f = ref.feat[sel].astype(np.float64)
-                assert np.allclose(mean[g], f.mean(axis=0), rtol=1e-12, atol=1e-12)
-                assert np.allclose(std[g], f.std(axis=0), rtol=1e-9, atol=1e-9)
-            else:
-                assert np.isnan(mean[g]).all()
+        assert np.array_equal(cnt, rc)
+        assert np.allclose(mean, rm, rtol=1e-12, atol=1e-12, equal_nan=True)
+        assert np.allclose(std, rs, rtol=1e-9, atol=1e-12, equal_nan=True)
 
 
 

@@ -484,13 +484,21 @@ def test_aggregate_groups_on_gpu(ctx):
         _, _, gl, gf, gt = _gpu_process(ctx, rgb)
         res[i] = (gl, gf, gt)
     rows = to_rows(res)
-    cnt, mean, std = aggregate_groups(rows, lambda t: t // 2, 2, reduce=ctx, device=torch.device("cuda"))
-    for g in range(2):
-        sel = rows.tile // 2 == g
-        f = rows.feat[sel].astype(np.float64)
-        assert cnt[g] == sel.sum() > 0
-        assert np.allclose(mean[g], f.mean(axis=0), rtol=1e-12, atol=1e-12)
-        assert np.allclose(std[g], f.std(axis=0), rtol=1e-9, atol=1e-9)
+    cnt, mean, std = aggregate_groups(rows, lambda t: t // 2, 3, reduce=ctx, device=torch.device("cuda"))
+    off = np.searchsorted(rows.tile // 2, np.arange(4))
+    rc, rm, rs = oracle.aggregate(rows.feat, off)   # group 2 is empty: NaN on both sides
+    assert np.array_equal(cnt, rc) and cnt[0] > 0 and cnt[1] > 0 and cnt[2] == 0
+    assert np.allclose(mean, rm, rtol=1e-12, atol=1e-12, equal_nan=True)
+    assert np.allclose(std, rs, rtol=1e-10, atol=1e-12, equal_nan=True)
+
+
+def test_aggregate_groups_no_rows(ctx):
+    """A rank with an empty table: the device kernels accept the NULL feature
+    pointer of an empty tensor and report zero counts and NaN statistics."""
+    import torch
+    from paper_1209_3332_b200.dist import Rows, aggregate_groups
+    cnt, mean, std = aggregate_groups(Rows.concat([]), lambda t: t, 2, reduce=ctx, device=torch.device("cuda"))
+    assert list(cnt) == [0, 0] and np.isnan(mean).all() and np.isnan(std).all()
 
 
 def test_run_tiles_size_change(ctx):
