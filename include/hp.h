@@ -213,12 +213,26 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
  *  CCL8/CCL4 in0 fg u8                          -> out0 labels i32 (1 + min index, 0 = bg)
  *  RECON_F32 in0 marker f32, in1 mask f32, in2 domain u8 (may be NULL) -> out0 recon f32
  *  CANNY     in0 g u8                           -> out0 edges u8 (0/1): cv2.Canny(g, low, high)
+ * The whole-plane AREA .. BWLABEL kernels above are verification kernels; the pipeline runs
+ * these three instead, exposed here so each hot-path kernel can be fed the oracle's input:
+ *  AREA_TOPHAT in0 g u8, in1 recon u8, in2 rbc u8 -> out0 big0 u8 (0/1) = S5 of the S4
+ *                                                  candidates ((g - recon) > g1) & !rbc, the
+ *                                                  candidate test evaluated inside S5's CCL;
+ *                                                  out1 (optional) i32[1] components kept
+ *  FILL_COMP   in0 big0 u8                      -> out0 F u8 (0/1): S6 solved per 8-component
+ *                                                  of big0 in its window (k_fill_fused)
+ *  COMPONENTS  in0 F u8 (S6 output), in1 g u8   -> S7-S11 solved per 8-component of F
+ *                                                  (k_comp_fused): out0 labels i32 (S10),
+ *                                                  out1 n_objects i32[1], out2 i32[2][cap]
+ *                                                  (row labels, then row flags), out3 feat
+ *                                                  f32[cap][36]; cap = max_objects, rows in
+ *                                                  ascending label order
  */
 typedef enum {
     HP_STAGE_CD = 0, HP_STAGE_RBC, HP_STAGE_OPEN, HP_STAGE_RECON, HP_STAGE_AREA,
     HP_STAGE_FILL, HP_STAGE_EDT, HP_STAGE_MARKERS, HP_STAGE_WATERSHED, HP_STAGE_BWLABEL,
     HP_STAGE_FEATURES, HP_STAGE_IWPP_RAW, HP_STAGE_CCL8, HP_STAGE_CCL4, HP_STAGE_RECON_F32,
-    HP_STAGE_CANNY, HP_STAGE_COUNT
+    HP_STAGE_CANNY, HP_STAGE_AREA_TOPHAT, HP_STAGE_FILL_COMP, HP_STAGE_COMPONENTS, HP_STAGE_COUNT
 } hp_stage;
 typedef struct hp_stage_io {
     const void* in[4];

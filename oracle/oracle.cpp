@@ -6,9 +6,11 @@
 // follows.  No blocking, fusion or reordering beyond the stated definitions/algorithms:
 // this file is meant to be checked against the text by eye, not to be fast.
 //
-// parity unpinned: the exact Haralick normalisation choices of or_features (GLCM
-// features 26-33) are our definitions (C16); they are pinned only by an independent
-// numpy recomputation in tests/test_oracle_features.py.
+// Pins: every function is checked against what the paper and the mathematics fix
+// (tests/test_oracle_*.py).  The Haralick features 26-33 follow our definitions (reading
+// C16); they are pinned by closed forms on three hand-counted co-occurrence matrices
+// (tests/test_oracle_pins_r2.py) besides an independent numpy recomputation, and the
+// top-hat line of or_recon_to_nuclei by a hand-drawn plane with a known reconstruction.
 #include "oracle.h"
 
 #include <algorithm>

@@ -677,6 +677,41 @@ hp_status hp_stage_run(hp_ctx* ctx, int32_t slot, hp_stage stage, const hp_stage
             if (!need({io->in[0], io->out[0]})) break;
             launch_canny(in8(0), w, h, p.canny_low, p.canny_high, sl, (uint8_t*)io->out[0], s);
             return check_launch(ctx, "stage canny");
+        // The hot path's own S5 / S6 / S7-S11 kernels (the pipeline runs these, not the
+        // whole-plane AREA / FILL / EDT / MARKERS / WATERSHED / BWLABEL kernels above), fed a
+        // caller plane so each can be checked on the oracle's intermediate.
+        case HP_STAGE_AREA_TOPHAT: {
+            if (!need({io->in[0], io->in[1], io->in[2], io->out[0]})) break;
+            int32_t* ncomp5 = sl.cnt32 + 16;
+            launch_area_select_tophat(in8(0), in8(1), in8(2), p.g1, w, h, p.cand_min_area, p.cand_max_area, sl,
+                                      (uint8_t*)io->out[0], ncomp5, s);
+            if (io->out[1]) cudaMemcpyAsync(io->out[1], ncomp5, sizeof(int32_t), cudaMemcpyDeviceToDevice, s);
+            return check_launch(ctx, "stage area tophat");
+        }
+        case HP_STAGE_FILL_COMP:
+        case HP_STAGE_COMPONENTS: {
+            const bool comp = stage == HP_STAGE_COMPONENTS;
+            if (!need({io->in[0], io->out[0]}) ||
+                (comp && !need({io->in[1], io->out[1], io->out[2], io->out[3]})))
+                break;
+            // list the 8-components of the input plane with S5's listing kernel (top-hat of
+            // (plane - 0) > 0 & !0, no area bounds), then S6 per component; for COMPONENTS
+            // the input is S6's output F (no holes left), so this only writes each F pixel's
+            // component root, which S7-S11 consume
+            int32_t* ncomp5 = sl.cnt32 + 16;
+            cudaMemsetAsync(sl.pmask, 0, (size_t)n, s);
+            launch_area_select_tophat(in8(0), sl.pmask, sl.pmask, 0, w, h, 0, INT32_MAX, sl, sl.big0, ncomp5, s);
+            uint8_t* F = comp ? sl.F : (uint8_t*)io->out[0];
+            launch_fill_components(in8(0), w, h, sl, ncomp5, F, sl.split, s);
+            if (!comp) return check_launch(ctx, "stage fill comp");
+            const int32_t cap = ctx->cfg.max_objects;
+            int32_t* lf = (int32_t*)io->out[2];
+            hp_feature_table tab{lf, lf + cap, (float*)io->out[3], cap, sl.tab_nrows};
+            launch_canny(in8(1), w, h, p.canny_low, p.canny_high, sl, sl.cand, s);
+            launch_components(ncomp5, sl.split, in8(1), sl.cand, p.h, p.obj_min_area, p.obj_max_area, w, h, sl,
+                              (int32_t*)io->out[0], w, (int32_t*)io->out[1], &tab, cap, s);
+            return check_launch(ctx, "stage components");
+        }
         case HP_STAGE_IWPP_RAW: {
             if (!need({io->in[0], io->in[1], io->out[0]})) break;
             launch_recon_init_u8(in8(0), in8(1), (uint8_t*)io->out[0], w, h, s);

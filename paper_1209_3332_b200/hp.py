@@ -29,7 +29,8 @@ FEATURE_NAMES = [
 assert len(FEATURE_NAMES) == NFEAT
 
 STAGES = ["CD", "RBC", "OPEN", "RECON", "AREA", "FILL", "EDT", "MARKERS", "WATERSHED",
-          "BWLABEL", "FEATURES", "IWPP_RAW", "CCL8", "CCL4", "RECON_F32", "CANNY"]
+          "BWLABEL", "FEATURES", "IWPP_RAW", "CCL8", "CCL4", "RECON_F32", "CANNY",
+          "AREA_TOPHAT", "FILL_COMP", "COMPONENTS"]
 STAGE = {n: i for i, n in enumerate(STAGES)}
 STATUS = {0: "ok", 1: "invalid argument", 2: "CUDA error", 3: "out of memory",
           4: "object capacity exceeded", 5: "unsupported device (need sm_100)"}

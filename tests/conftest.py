@@ -3,6 +3,10 @@ import sys
 
 import pytest
 
+# the GPU tests run several slot streams at once, like bench.py: give every stream its own
+# hardware work queue (must be set before CUDA is initialised; bench.py sets the same)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -26,10 +26,8 @@ def ctx():
     c.close()
 
 
-@pytest.fixture(scope="module")
-def chain():
-    """Oracle intermediates of the config-1 tile."""
-    rgb = make_config_tile(1)
+def _oracle_chain(rgb):
+    """The oracle's intermediates of every step of one tile."""
     p = oracle.default_params()
     d = {"rgb": rgb}
     d["g"], d["flags"], d["nbg"] = oracle.cd(rgb, p)
@@ -44,6 +42,12 @@ def chain():
     d["labels"], d["nobj"] = oracle.bwlabel(d["split"], 21, 1000)
     d["rows"] = oracle.features(d["labels"], d["g"])
     return d
+
+
+@pytest.fixture(scope="module")
+def chain():
+    """Oracle intermediates of the config-1 tile."""
+    return _oracle_chain(make_config_tile(1))
 
 
 def test_cd(ctx, chain):
@@ -104,6 +108,63 @@ def test_area_fill(ctx, chain):
     assert np.array_equal(b, chain["big0"])
     (F,) = stage(ctx, "FILL", [chain["big0"]], [((h, w), U8)], w, h)
     assert np.array_equal(F, chain["F"])
+
+
+def _check_hot_path_stages(ctx, d, cap=65536):
+    """The pipeline's own S5 (CCL-select on the top-hat), S6 (per-component fill) and S7-S11
+    (per-component EDT .. features) kernels, each fed the oracle's input of that step:
+    integer outputs bit-exact, features within reading C18 (north_star: "bit-exact for every
+    integer/labeling stage when each stage is fed the oracle's own input")."""
+    h, w = d["g"].shape
+    big0, nk = stage(ctx, "AREA_TOPHAT", [d["g"], d["recon"], d["rbc"]], [((h, w), U8), ((1,), I32)], w, h)
+    assert np.array_equal(big0, d["big0"])
+    assert int(nk[0]) == oracle.ccl(d["big0"], 8)[1]
+    (F,) = stage(ctx, "FILL_COMP", [d["big0"]], [((h, w), U8)], w, h)
+    assert np.array_equal(F, d["F"])
+    lab, nob, lf, ft = stage(ctx, "COMPONENTS", [d["F"], d["g"]],
+                             [((h, w), I32), ((1,), I32), ((2, cap), I32), ((cap, 36), F32)], w, h)
+    assert np.array_equal(lab, d["labels"])
+    n = int(nob[0])
+    assert n == d["nobj"]
+    ol, of, ot = d["rows"]
+    assert_features_equal(lf[0, :n], lf[1, :n], ft[:n], ol, of, ot)
+
+
+def test_hot_path_stages_config1(ctx, chain):
+    _check_hot_path_stages(ctx, chain)
+
+
+@pytest.mark.parametrize("seed,shape", [(31, (300, 400)), (32, (257, 129)), (33, (512, 384))])
+def test_hot_path_stages_random(ctx, seed, shape):
+    _check_hot_path_stages(ctx, _oracle_chain(make_tile(seed, TileSpec(*shape))["rgb"]))
+
+
+@pytest.mark.slow
+def test_hot_path_stages_config2(ctx):
+    _check_hot_path_stages(ctx, _oracle_chain(make_config_tile(2)))
+
+
+@pytest.mark.parametrize("shape", [(20, 30), (64, 64), (1, 40)])
+def test_components_all_foreground(ctx, shape):
+    """F covering the whole tile: no background anywhere, so the EDT is +inf on every pixel
+    (reading C11) -- the fused kernel's "component = whole tile" branch.  (20, 30): one object
+    of 600 px; (64, 64): 4096 px, above obj_max_area, so no object (global-memory window)."""
+    h, w = shape
+    rng = np.random.default_rng(h * 1000 + w)
+    F = np.ones((h, w), U8)
+    g = rng.integers(0, 256, size=(h, w)).astype(U8)
+    d2, dist = oracle.edt(F)
+    assert np.isinf(dist).all()
+    ML, _, _ = oracle.markers(dist, F, 1.0)
+    split, _, _, _ = oracle.watershed(dist, ML, F)
+    labels, nobj = oracle.bwlabel(split, 21, 1000)
+    cap = 64
+    lab, nob, lf, ft = stage(ctx, "COMPONENTS", [F, g], [((h, w), I32), ((1,), I32), ((2, cap), I32),
+                                                        ((cap, 36), F32)], w, h)
+    assert np.array_equal(lab, labels) and int(nob[0]) == nobj == (1 if h * w <= 1000 and h * w >= 21 else 0)
+    if nobj:
+        ol, of, ot = oracle.features(labels, g)
+        assert_features_equal(lf[0, :1], lf[1, :1], ft[:1], ol, of, ot)
 
 
 def test_edt(ctx, chain):
@@ -661,30 +722,43 @@ def _pool_tile(seed):
     return bench._gen((seed, 4096))
 
 
-def _oracle_digest(rgb):
+BENCH_SLOTS, BENCH_E2E_SLOTS, BENCH_BATCH = 12, 14, 12   # bench.py's defaults
+
+
+def _oracle_rows(rgb):
     import hashlib
-    olab, ol, of, ot = oracle.process_tile(rgb, cap=65536)
-    return hashlib.sha256(np.ascontiguousarray(olab).tobytes()).hexdigest(), ol, of, ot
+    lab, ol, of, ot = oracle.process_tile(rgb)
+    return hashlib.sha256(lab.tobytes()).hexdigest(), ol, of, ot
+
+
+@pytest.fixture(scope="module")
+def bench_ref():
+    """bench.py's own 4K tiles (configs[2] pool seeds 1000..; HP_POOL_PARITY=N checks the
+    first N, default bench.py's batch of 12, 64 = the whole configs[2] pool) and the oracle's
+    result for each (label digest, rows), computed on all host cores."""
+    import multiprocessing as mp
+    import os
+    K = int(os.environ.get("HP_POOL_PARITY", str(BENCH_BATCH)))
+    pctx = mp.get_context("fork")
+    with pctx.Pool(max(1, min(K, os.cpu_count() or 1))) as pool:
+        tiles = pool.map(_pool_tile, range(1000, 1000 + K))
+        ref = pool.map(_oracle_rows, tiles)
+    return tiles, ref
 
 
 @pytest.mark.slow
-def test_bench_tiles_in_bench_launch_config():
-    """Parity at BASELINE's full size in the launch configuration bench.py times: the
-    bench's own 4K tiles (configs[2] pool seeds 1000..), six slots with one stream each and
-    all tiles in flight at once, against the oracle -- label planes bit-exact, tables within
-    reading C18.  HP_POOL_PARITY=N checks the first N pool tiles (default 6; 64 = the whole
-    configs[2] pool)."""
+def test_bench_tiles_in_bench_launch_config(bench_ref):
+    """Parity at BASELINE's full size in the launch configuration bench.py's device-resident
+    leg times: its 12 tiles through hp_process_tile on 12 slots, one stream each, all in
+    flight at once, 32 hardware work queues (conftest.py, as bench.py) -- label planes
+    bit-exact, tables within reading C18."""
     import hashlib
-    import multiprocessing as mp
-    import os
 
     import torch
     from paper_1209_3332_b200 import Context
-    K = int(os.environ.get("HP_POOL_PARITY", "6"))
-    S, size, cap = 6, 4096, 8192
-    c = Context(0, size, size, n_slots=S, max_objects=cap)
-    pctx = mp.get_context("fork")
-    nproc = max(1, min(S, os.cpu_count() or 1))
+    tiles, ref = bench_ref
+    S, size, cap = BENCH_SLOTS, 4096, 8192
+    c = Context(0, size, size, n_slots=max(S, BENCH_E2E_SLOTS), max_objects=cap)
     try:
         lab = [torch.empty((size, size), dtype=torch.int32, device="cuda") for _ in range(S)]
         nob = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(S)]
@@ -693,23 +767,53 @@ def test_bench_tiles_in_bench_launch_config():
         tt = [torch.empty((cap, 36), dtype=torch.float32, device="cuda") for _ in range(S)]
         nr = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(S)]
         streams = [torch.cuda.Stream() for _ in range(S)]
-        with pctx.Pool(nproc) as pool:
-            for b0 in range(0, K, S):
-                seeds = list(range(1000 + b0, 1000 + min(K, b0 + S)))
-                tiles = pool.map(_pool_tile, seeds)
-                ref = pool.map_async(_oracle_digest, tiles)   # oracle runs while the GPU does
-                dev = [torch.from_numpy(t).cuda() for t in tiles]
-                torch.cuda.synchronize()
-                for k in range(len(tiles)):
-                    c.process_tile(k, dev[k], lab[k], nob[k], tl[k], tf[k], tt[k], nr[k], stream=streams[k])
-                torch.cuda.synchronize()
-                for k, (odig, ol, of, ot) in enumerate(ref.get()):
-                    gl = lab[k].cpu().numpy()
-                    assert hashlib.sha256(gl.tobytes()).hexdigest() == odig, f"labels of seed {seeds[k]}"
-                    n = int(nr[k].item())
-                    assert int(nob[k].item()) == n == len(ol) > 1000
-                    assert_features_equal(tl[k][:n].cpu().numpy(), tf[k][:n].cpu().numpy(),
-                                          tt[k][:n].cpu().numpy(), ol, of, ot)
+        for b0 in range(0, len(tiles), S):
+            idx = list(range(b0, min(len(tiles), b0 + S)))
+            dev = [torch.from_numpy(tiles[i]).cuda() for i in idx]
+            torch.cuda.synchronize()
+            for k in range(len(idx)):
+                c.process_tile(k, dev[k], lab[k], nob[k], tl[k], tf[k], tt[k], nr[k], stream=streams[k])
+            torch.cuda.synchronize()
+            for k, i in enumerate(idx):
+                odig, ol, of, ot = ref[i]
+                gl = lab[k].cpu().numpy()
+                assert hashlib.sha256(gl.tobytes()).hexdigest() == odig, f"labels of pool tile {i}"
+                n = int(nr[k].item())
+                assert int(nob[k].item()) == n == len(ol) > 1000
+                assert_features_equal(tl[k][:n].cpu().numpy(), tf[k][:n].cpu().numpy(),
+                                      tt[k][:n].cpu().numpy(), ol, of, ot)
+    finally:
+        c.close()
+
+
+@pytest.mark.slow
+def test_bench_e2e_launch_config(bench_ref):
+    """Parity of bench.py's e2e leg in its exact configuration: hp_run_tiles on 14 slots with
+    per-slot CUDA graphs (captured on a slot's second tile, replayed after), pinned host tiles,
+    32 hardware work queues, the bench's tiles twice each in a demand-driven order -- every
+    delivered table equals the oracle's (labels and flags exact, features within C18)."""
+    import torch
+    from paper_1209_3332_b200 import Context
+    from paper_1209_3332_b200.dist import DistTileSource, TileQueue
+    tiles, ref = bench_ref
+    K = len(tiles)
+    size, cap = 4096, 8192
+    c = Context(0, size, size, n_slots=max(BENCH_SLOTS, BENCH_E2E_SLOTS), max_objects=cap)
+    try:
+        pinned = [torch.from_numpy(t).pin_memory() for t in tiles]
+        q = TileQueue(2 * K, block=BENCH_SLOTS, store=None)
+        src = DistTileSource(q, lambda tid: pinned[tid % K])
+        got = {}
+
+        def done(tid, l, f, ft, st):
+            assert st == 0, f"tile {tid} status {st}"
+            got[tid] = (l, f, ft)
+
+        c.run_tiles(src, done, size, size)
+        assert sorted(got) == list(range(2 * K))
+        for tid, (l, f, ft) in got.items():
+            _, ol, of, ot = ref[tid % K]
+            assert_features_equal(l, f, ft, ol, of, ot)
     finally:
         c.close()
 
