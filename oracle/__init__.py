@@ -26,10 +26,11 @@ OBJ_TOUCHES_BORDER = 1
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so with g++ (-O2, no FMA contraction, no fast-math)."""
+    srcs = [_SRC, os.path.join(_HERE, "jpeg.cpp")]
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
-            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))):
+            [os.path.getmtime(f) for f in srcs] + [os.path.getmtime(os.path.join(_HERE, "oracle.h"))]):
         cmd = ["g++", "-O2", "-ffp-contract=off", "-fno-fast-math", "-ftree-vectorize", "-std=c++17", "-fPIC",
-               "-shared", "-o", _SO, _SRC]
+               "-shared", "-o", _SO] + srcs
         subprocess.check_call(cmd, cwd=_HERE)
     return _SO
 
@@ -91,6 +92,7 @@ def lib():
             "or_process_tile": (C.c_int, [P, C.c_int, C.c_int, i64, C.POINTER(Params), P, i32,
                                           P, P, P, P, P]),
             "or_aggregate": (C.c_int, [P, C.c_int, P, C.c_int, P, P, P]),
+            "or_jpeg_decode": (C.c_int, [P, i64, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -323,3 +325,16 @@ def aggregate(feat, off):
     fp = feat if feat.size else np.zeros((1, F), np.float32)
     _chk(lib().or_aggregate(_p(fp), F, _p(off), G, _p(cnt), _p(mean), _p(std)), "or_aggregate")
     return cnt, mean, std
+
+
+def jpeg_decode(data):
+    """NEXT-3: baseline JPEG bytes -> RGB u8 [H, W, 3] (T.81 decoding,
+    readings J1-J2: IJG islow IDCT, JFIF colour).  Raises on unsupported / invalid input."""
+    buf = np.frombuffer(bytes(data), dtype=np.uint8) if not isinstance(data, np.ndarray) else \
+        np.ascontiguousarray(data, np.uint8)
+    w = np.zeros(1, np.int32)
+    h = np.zeros(1, np.int32)
+    _chk(lib().or_jpeg_decode(_p(buf), buf.size, _p(w), _p(h), None), "or_jpeg_decode (header)")
+    out = np.empty((int(h[0]), int(w[0]), 3), np.uint8)
+    _chk(lib().or_jpeg_decode(_p(buf), buf.size, _p(w), _p(h), _p(out)), "or_jpeg_decode")
+    return out

@@ -101,6 +101,11 @@ int or_process_tile(const uint8_t* rgb, int w, int h, int64_t pitch, const or_pa
  * count[g], mean[g][f] and population std[g][f] in fp64 (two-pass); NaN for an empty group. */
 int or_aggregate(const float* feat, int nfeat, const int64_t* off, int n_groups, int64_t* count,
                  double* mean, double* stdv);
+/* NEXT-3 compressed ingest (oracle/jpeg.cpp): baseline JPEG (T.81 sequential Huffman,
+ * 8-bit, 3 components at 1x1 sampling, optional restart interval) -> RGB u8 interleaved,
+ * pitch 3*width.  rgb == NULL: only *width / *height are written.  Returns 0, 1 (invalid
+ * stream) or 5 (a JPEG feature outside that scope). */
+int or_jpeg_decode(const uint8_t* data, int64_t n, int32_t* width, int32_t* height, uint8_t* rgb);
 
 #ifdef __cplusplus
 }
