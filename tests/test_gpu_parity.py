@@ -158,7 +158,7 @@ def test_components_all_foreground(ctx, shape):
     ML, _, _ = oracle.markers(dist, F, 1.0)
     split, _, _, _ = oracle.watershed(dist, ML, F)
     labels, nobj = oracle.bwlabel(split, 21, 1000)
-    cap = 64
+    cap = 65536   # hp_stage_run's table capacity is the context's max_objects (hp.h)
     lab, nob, lf, ft = stage(ctx, "COMPONENTS", [F, g], [((h, w), I32), ((1,), I32), ((2, cap), I32),
                                                         ((cap, 36), F32)], w, h)
     assert np.array_equal(lab, labels) and int(nob[0]) == nobj == (1 if h * w <= 1000 and h * w >= 21 else 0)
