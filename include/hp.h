@@ -191,6 +191,43 @@ typedef struct hp_result_sink {
 } hp_result_sink;
 hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_sink* sink);
 
+/* Compressed ingest ("the main limiting factor and bottleneck
+ * is the I/O overhead of reading image tiles", 716-726).  Tiles arrive as baseline JPEG files
+ * (ITU-T T.81 sequential Huffman, 8-bit, 3 components, 4:4:4 sampling, one interleaved scan;
+ * a restart interval (DRI) lets the GPU decode one interval per thread -- without one the
+ * whole scan is a single serial interval).  Only the file crosses PCIe (~4 MB instead of
+ * 50 MB for a quality-90 4K tile).  The host parses the marker segments (a few hundred
+ * bytes); restart-marker search, Huffman decoding, dequantisation, the IDCT (the IJG "islow"
+ * integer method, reading J1 of DESIGN.md) and the JFIF YCbCr->RGB conversion (reading J2)
+ * run on the GPU, fused into S1: the decoded RGB tile is never written to memory.  The
+ * result equals hp_process_tile on the tile cv2.imdecode would return.
+ * Errors: a file outside that scope -> HP_ERR_UNSUPPORTED; a malformed header, a file larger
+ * than 3 * max_width * max_height bytes or a frame larger than the context -> HP_ERR_INVALID
+ * (both before any launch).  A corrupt scan (restart markers not matching the interval, an
+ * invalid Huffman code) is only seen on the device: it sets the decode error word.
+ *
+ * hp_run_tiles_jpeg: hp_run_tiles with next() returning a HOST pointer to a JPEG file and its
+ * size in bytes (pinned memory recommended; valid until the tile is delivered).  Every file
+ * must decode to exactly (width, height).  A file that fails on the host, or whose scan is
+ * corrupt, is delivered through done() with HP_ERR_INVALID / HP_ERR_UNSUPPORTED and no rows;
+ * the run continues with the next tile. */
+typedef struct hp_jpeg_source {
+    int   (*next)(void* user, const uint8_t** host_jpeg, int64_t* nbytes, int64_t* tile_id);
+    void*   user;
+    int32_t width, height;
+} hp_jpeg_source;
+hp_status hp_run_tiles_jpeg(hp_ctx* ctx, const hp_jpeg_source* src, const hp_result_sink* sink);
+/* One JPEG tile through both stages, like hp_process_tile: host_jpeg (HOST, nbytes; keep it
+ * valid until s completes) is uploaded on s.  decode_err_dev (DEVICE int32, may be NULL)
+ * receives 0, or 1 (restart-marker mismatch) | 2 (invalid Huffman code). */
+hp_status hp_process_tile_jpeg(hp_ctx* ctx, int32_t slot, const uint8_t* host_jpeg, int64_t nbytes,
+                               hp_labels* lab, hp_feature_table* out, int32_t* decode_err_dev,
+                               hp_stream s);
+/* Verification entry of the decoder alone: the decoded RGB tile (DEVICE rgb_dev, u8 R,G,B
+ * interleaved, pitch_bytes >= 3*width).  Synchronises s; a corrupt scan -> HP_ERR_INVALID. */
+hp_status hp_decode_jpeg(hp_ctx* ctx, int32_t slot, const uint8_t* host_jpeg, int64_t nbytes,
+                         uint8_t* rgb_dev, int64_t pitch_bytes, hp_stream s);
+
 /* Verification ABI: run ONE operation on caller-provided DEVICE buffers (dense planes of
  * width x height).  Layouts per stage (in -> out):
  *  CD        in0 rgb u8x3 (pitch 3w)            -> out0 g u8, out1 flags u8, out2 bg count i64[1]

@@ -153,14 +153,23 @@ void ev(hp_ctx* ctx, Slot& sl, int k, cudaStream_t s) {
 #endif
 #define HP_DUP(k) for (int dup_ = 0; dup_ < (HP_WHATIF_DUP == (k) ? 2 : 1); ++dup_)
 
+// With jpeg set, S1 reads the slot's JPEG tile (header in sl.jhdr_dev, file in sl.rgb_dev,
+// both uploaded by the caller) and decodes it inside S1 (k_jpeg.cu); rgb gives only the size.
 hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, int64_t lpitch,
                   int32_t* n_objects, cudaStream_t s, hp_feature_table* table = nullptr,
-                  bool* fused = nullptr) {
+                  bool* fused = nullptr, bool jpeg = false) {
     if (fused) *fused = false;
     const hp_params& p = ctx->cfg.params;
     const int w = rgb->width, h = rgb->height;
     ev(ctx, sl, 0, s);
-    HP_DUP(1) launch_cd(rgb->data, w, h, rgb->pitch_bytes, ctx->lut, p, sl.g, sl.flags, &sl.counters[0], s);   // S1
+    if (jpeg) {                                                                                       // S0 + S1
+        cudaMemsetAsync(sl.jerr, 0, sizeof(int32_t), s);
+        const int64_t cap = 3LL * ctx->cfg.max_width * ctx->cfg.max_height;
+        launch_jpeg_decode(sl.jhdr_dev, sl.rgb_dev, cap, w, h, sl.jstarts, sl.jblk, ctx->lut, p, sl.g, sl.flags,
+                           &sl.counters[0], nullptr, 0, sl.jerr, s);
+    } else {
+        HP_DUP(1) launch_cd(rgb->data, w, h, rgb->pitch_bytes, ctx->lut, p, sl.g, sl.flags, &sl.counters[0], s);  // S1
+    }
     ev(ctx, sl, 1, s);
     if (p.bg_skip_frac <= 1.0f) {
         unsigned long long nbg = 0;
@@ -273,6 +282,46 @@ hp_status check_labels(hp_ctx* ctx, const hp_labels* l, int w) {
         return HP_ERR_INVALID;
     }
     return HP_OK;
+}
+
+// NEXT-3: parse a JPEG tile on the host and upload the header and the file into the slot
+// (stream s).  ring: stage the header in the slot's pinned ring (single-tile calls may be
+// issued back to back on one slot) instead of its one run_tiles staging entry.
+hp_status upload_jpeg(hp_ctx* ctx, Slot& sl, const uint8_t* host, int64_t nbytes, cudaStream_t s, bool ring,
+                      int* w, int* h) {
+    const int64_t cap = 3LL * ctx->cfg.max_width * ctx->cfg.max_height;
+    if (!host || nbytes < 4 || nbytes > cap) {
+        set_err(ctx, "jpeg: null buffer or size %lld outside [4, %lld]", (long long)nbytes, (long long)cap);
+        return HP_ERR_INVALID;
+    }
+    JpegHdr* H = sl.jhdr_host;
+    int k = 0;
+    if (ring) {
+        k = sl.jhdr_pos;
+        cudaError_t e = cudaEventSynchronize(sl.jhdr_ev[k]);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "jpeg header staging");
+        H = sl.jhdr_ring + k;
+    }
+    const char* why = "";
+    hp_status st = jpeg_parse(host, nbytes, H, &why);
+    if (st) {
+        set_err(ctx, "jpeg: %s", why);
+        return st;
+    }
+    if (H->width > ctx->cfg.max_width || H->height > ctx->cfg.max_height) {
+        set_err(ctx, "jpeg: %dx%d larger than the context's %dx%d", H->width, H->height, ctx->cfg.max_width,
+                ctx->cfg.max_height);
+        return HP_ERR_INVALID;
+    }
+    cudaMemcpyAsync(sl.jhdr_dev, H, sizeof(JpegHdr), cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(sl.rgb_dev, host, (size_t)nbytes, cudaMemcpyHostToDevice, s);
+    if (ring) {
+        cudaEventRecord(sl.jhdr_ev[k], s);
+        sl.jhdr_pos = (k + 1) % 4;
+    }
+    *w = H->width;
+    *h = H->height;
+    return check_launch(ctx, "jpeg upload");
 }
 
 }  // namespace
@@ -410,6 +459,13 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.stg_flags = (int32_t*)A(4 * (size_t)mo);
         s.stg_feat = (float*)A(4 * (size_t)mo * HP_NFEAT);
         s.rgb_dev = (uint8_t*)A(3 * N);
+        s.jhdr_dev = (JpegHdr*)A(sizeof(JpegHdr));
+        s.jstarts = (int32_t*)A(4 * (size_t)jpeg_max_intervals(N));
+        s.jblk = (int32_t*)A(4 * (size_t)(3 * N / 8192 + 2));
+        s.jerr = (int32_t*)A(16);
+        s.jhdr_host = (JpegHdr*)halloc(sizeof(JpegHdr));
+        s.jhdr_ring = (JpegHdr*)halloc(4 * sizeof(JpegHdr));
+        s.h_jerr = (int32_t*)halloc(16);
         s.lab_dev = (int32_t*)A(4 * N);
         s.tab_label = (int32_t*)A(4 * (size_t)mo);
         s.tab_flags = (int32_t*)A(4 * (size_t)mo);
@@ -423,7 +479,8 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         void* all[] = {s.g, s.flags, s.rbc, s.u8a, s.u8b, s.cand, s.big0, s.F, s.split, s.pmask, s.lab, s.aux,
                        s.ML, s.d, s.L, s.dist, s.J, s.c, s.gcol, s.seg_top, s.seg_bot, s.wl.state, s.wl.inrows, s.wl.queue,
                        s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.cs_edge, s.cs_roots, s.cs_nroots, s.sc_root, s.sc_bbox, s.sc_area, s.sc_big, s.sc_huge, s.big_scratch, s.stg_label, s.stg_flags, s.stg_feat, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
-                       s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows, s.h_arena};
+                       s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows, s.h_arena,
+                       s.jhdr_dev, s.jstarts, s.jblk, s.jerr, s.jhdr_host, s.jhdr_ring, s.h_jerr};
         for (void* p : all)
             if (!p) { hp_ctx_destroy(ctx); return HP_ERR_NOMEM; }
         int prio_lo = 0, prio_hi = 0;
@@ -432,13 +489,19 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
             cudaStreamCreateWithPriority(&s.hstream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
             cudaEventCreateWithFlags(&s.done_ev, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&s.fork_ev, cudaEventDisableTiming) != cudaSuccess ||
-            cudaEventCreateWithFlags(&s.join_ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaEventCreateWithFlags(&s.join_ev, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.jhdr_ev[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.jhdr_ev[1], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.jhdr_ev[2], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s.jhdr_ev[3], cudaEventDisableTiming) != cudaSuccess) {
             hp_ctx_destroy(ctx);
             return HP_ERR_CUDA;
         }
         cudaMemset(s.counters, 0, 64);
         cudaMemset(s.cnt32, 0, 128);
         cudaMemset(s.wl.ctr, 0, 64);
+        cudaMemset(s.jerr, 0, 16);
+        for (cudaEvent_t e : s.jhdr_ev) cudaEventRecord(e, s.stream);
     }
     if (cudaDeviceSynchronize() != cudaSuccess) { hp_ctx_destroy(ctx); return HP_ERR_CUDA; }
     *out = ctx;
@@ -456,6 +519,8 @@ hp_status hp_ctx_destroy(hp_ctx* ctx) {
         if (s.fork_ev) cudaEventDestroy(s.fork_ev);
         if (s.gexec) cudaGraphExecDestroy(s.gexec);
         if (s.join_ev) cudaEventDestroy(s.join_ev);
+        for (cudaEvent_t e : s.jhdr_ev)
+            if (e) cudaEventDestroy(e);
     }
     for (auto& r : ctx->ring)
         for (auto& set : r)
@@ -500,6 +565,57 @@ hp_status hp_process_tile(hp_ctx* ctx, int32_t slot, const hp_image* rgb, hp_lab
     st = segment(ctx, sl, rgb, lab->labels, lab->labels_pitch_elems, lab->n_objects_dev, cs, out, &fused);
     if (st || fused) return st;
     return features(ctx, sl, rgb->width, rgb->height, lab->labels, lab->labels_pitch_elems, out, cs);
+}
+
+hp_status hp_process_tile_jpeg(hp_ctx* ctx, int32_t slot, const uint8_t* host_jpeg, int64_t nbytes, hp_labels* lab,
+                               hp_feature_table* out, int32_t* decode_err_dev, hp_stream s) {
+    hp_status st = enter(ctx, slot);
+    if (st) return st;
+    if ((st = check_labels(ctx, lab, 1)) || (st = check_table(ctx, out))) return st;
+    Slot& sl = ctx->slots[slot];
+    cudaStream_t cs = (cudaStream_t)s;
+    int w = 0, h = 0;
+    if ((st = upload_jpeg(ctx, sl, host_jpeg, nbytes, cs, true, &w, &h))) return st;
+    if (lab->labels_pitch_elems < w) {
+        set_err(ctx, "labels pitch %lld < JPEG width %d", (long long)lab->labels_pitch_elems, w);
+        return HP_ERR_INVALID;
+    }
+    hp_image im{sl.rgb_dev, w, h, 3LL * w};
+    bool fused = false;
+    st = segment(ctx, sl, &im, lab->labels, lab->labels_pitch_elems, lab->n_objects_dev, cs, out, &fused, true);
+    if (!st && !fused) st = features(ctx, sl, w, h, lab->labels, lab->labels_pitch_elems, out, cs);
+    if (!st && decode_err_dev) cudaMemcpyAsync(decode_err_dev, sl.jerr, sizeof(int32_t), cudaMemcpyDeviceToDevice, cs);
+    return st ? st : check_launch(ctx, "process_tile_jpeg");
+}
+
+hp_status hp_decode_jpeg(hp_ctx* ctx, int32_t slot, const uint8_t* host_jpeg, int64_t nbytes, uint8_t* rgb_dev,
+                         int64_t pitch_bytes, hp_stream s) {
+    hp_status st = enter(ctx, slot);
+    if (st) return st;
+    if (!rgb_dev) {
+        set_err(ctx, "hp_decode_jpeg: null output");
+        return HP_ERR_INVALID;
+    }
+    Slot& sl = ctx->slots[slot];
+    cudaStream_t cs = (cudaStream_t)s;
+    int w = 0, h = 0;
+    if ((st = upload_jpeg(ctx, sl, host_jpeg, nbytes, cs, true, &w, &h))) return st;
+    if (pitch_bytes < 3LL * w) {
+        set_err(ctx, "hp_decode_jpeg: pitch < 3*width");
+        return HP_ERR_INVALID;
+    }
+    cudaMemsetAsync(sl.jerr, 0, sizeof(int32_t), cs);
+    launch_jpeg_decode(sl.jhdr_dev, sl.rgb_dev, 3LL * ctx->cfg.max_width * ctx->cfg.max_height, w, h, sl.jstarts,
+                       sl.jblk, ctx->lut, ctx->cfg.params, nullptr, nullptr, nullptr, rgb_dev, pitch_bytes, sl.jerr, cs);
+    cudaMemcpyAsync(sl.h_jerr, sl.jerr, sizeof(int32_t), cudaMemcpyDeviceToHost, cs);
+    cudaError_t e = cudaStreamSynchronize(cs);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "hp_decode_jpeg");
+    if (*sl.h_jerr) {
+        set_err(ctx, "hp_decode_jpeg: corrupt scan (%s)",
+                (*sl.h_jerr & 1) ? "restart markers do not match the restart interval" : "invalid Huffman code");
+        return HP_ERR_INVALID;
+    }
+    return HP_OK;
 }
 
 hp_status hp_set_stage_timing(hp_ctx* ctx, int32_t enable) {
@@ -744,18 +860,14 @@ hp_status hp_stage_run(hp_ctx* ctx, int32_t slot, hp_stage stage, const hp_stage
     return HP_ERR_INVALID;
 }
 
-hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_sink* sink) {
-    hp_status st = enter(ctx, 0);
-    if (st) return st;
-    if (!src || !src->next || !sink || !sink->done) {
-        set_err(ctx, "run_tiles: NULL source, sink or callback");
-        return HP_ERR_INVALID;
-    }
-    const int w = src->width, h = src->height;
-    if (w < 1 || h < 1 || w > ctx->cfg.max_width || h > ctx->cfg.max_height) {
-        set_err(ctx, "run_tiles: tile size %dx%d outside 1..%dx%d", w, h, ctx->cfg.max_width, ctx->cfg.max_height);
-        return HP_ERR_INVALID;
-    }
+}  // extern "C"
+
+namespace {
+
+// The demand-driven multi-tile driver behind hp_run_tiles (raw RGB tiles) and
+// hp_run_tiles_jpeg (JPEG files, NEXT-3).  next(&host, &pitch_or_nbytes, &tile_id) -> 0 / 1.
+template <class Next>
+hp_status run_tiles_impl(hp_ctx* ctx, int w, int h, bool jpeg, Next next, const hp_result_sink* sink) {
     const int ns = ctx->cfg.n_slots;
     const int mo = ctx->cfg.max_objects;
     const hp_row_arena* arena = sink->arena;
@@ -781,6 +893,7 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
         int nrows = *sl.h_nrows;
         hp_status ts = st_of[i];
         if (nrows > mo) ts = HP_ERR_CAPACITY;
+        if (jpeg && *sl.h_jerr) ts = HP_ERR_INVALID;  // corrupt scan: the rows are not trustworthy
         int nr = std::min(nrows, mo);
         if (arena) {  // rows stay in the device arena; the run [h_arena[1], +nr) may be clipped
             if (sl.h_arena[1] + nr > arena->capacity) ts = HP_ERR_CAPACITY;
@@ -805,30 +918,51 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
     // very different times (chain-bound reconstructions), so waiting on slots in a fixed
     // order would leave finished slots idle behind a slow one.
     auto submit = [&](int i) -> hp_status {
-        const uint8_t* host = nullptr;
-        int64_t pitch = 0, tid = -1;
-        if (src->next(src->user, &host, &pitch, &tid) != 0) {
-            drained = true;
-            return HP_OK;
-        }
-        if (!host || pitch < 3LL * w) {
-            set_err(ctx, "run_tiles: tile %lld has a NULL host pointer or pitch %lld < 3*width", (long long)tid,
-                    (long long)pitch);
-            return HP_ERR_INVALID;
-        }
         Slot& sl = ctx->slots[i];
         cudaStream_t s = sl.stream;
+        const uint8_t* host = nullptr;
+        int64_t pitch = 0, tid = -1;
+        while (true) {  // until a tile is in flight on slot i or the source is drained
+            host = nullptr;
+            pitch = 0;
+            tid = -1;
+            if (next(&host, &pitch, &tid) != 0) {
+                drained = true;
+                return HP_OK;
+            }
+            if (!jpeg) {
+                if (!host || pitch < 3LL * w) {
+                    set_err(ctx, "run_tiles: tile %lld has a NULL host pointer or pitch %lld < 3*width", (long long)tid,
+                            (long long)pitch);
+                    return HP_ERR_INVALID;
+                }
+                break;
+            }
+            // a JPEG the decoder cannot take (malformed, out of scope, wrong size) fails alone:
+            // reported through done() with no rows, and the slot takes the next tile
+            int jw = 0, jh = 0;
+            hp_status ps = upload_jpeg(ctx, sl, host, pitch, s, false, &jw, &jh);
+            if (ps == HP_ERR_CUDA) return ps;
+            if (!ps && (jw != w || jh != h)) {
+                set_err(ctx, "run_tiles_jpeg: tile %lld is %dx%d, the source says %dx%d", (long long)tid, jw, jh, w, h);
+                ps = HP_ERR_INVALID;
+            }
+            if (!ps) break;
+            sink->done(sink->user, tid, 0, sl.h_label, sl.h_flags, sl.h_feat, ps);
+        }
         sl.h_arena[0] = tid;  // read by this tile's H2D (arena mode); the slot's previous tile was delivered
-        cudaMemcpy2DAsync(sl.rgb_dev, 3 * (size_t)w, host, (size_t)pitch, 3 * (size_t)w, h, cudaMemcpyHostToDevice, s);
+        if (!jpeg)
+            cudaMemcpy2DAsync(sl.rgb_dev, 3 * (size_t)w, host, (size_t)pitch, 3 * (size_t)w, h, cudaMemcpyHostToDevice, s);
         hp_image im{sl.rgb_dev, w, h, 3LL * w};
         hp_feature_table tab{sl.tab_label, sl.tab_flags, sl.tab_feat, mo, sl.tab_nrows};
         // the tile's chain: segmentation + features on the slot's own buffers, rows D2H
         auto chain = [&]() -> hp_status {
             bool fused = false;
-            hp_status r = segment(ctx, sl, &im, sl.lab_dev, w, sl.cnt32 + 4, s, &tab, &fused);
+            hp_status r = segment(ctx, sl, &im, sl.lab_dev, w, sl.cnt32 + 4, s, &tab, &fused, jpeg);
             if (!r && !fused) r = features(ctx, sl, w, h, sl.lab_dev, w, &tab, s);
             if (r) return r;
             cudaMemcpyAsync(sl.h_nrows, sl.tab_nrows, 4, cudaMemcpyDeviceToHost, s);
+            if (jpeg) cudaMemcpyAsync(sl.h_jerr, sl.jerr, 4, cudaMemcpyDeviceToHost, s);
             if (arena) {  // S12 into the device arena: the tile id goes up, the run offset down
                 int64_t* dev_tid = (int64_t*)&sl.counters[4];
                 int64_t* dev_base = (int64_t*)&sl.counters[5];
@@ -850,7 +984,7 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
         const bool graphable = ctx->graphs && !ctx->timing && ctx->cfg.params.bg_skip_frac > 1.0f &&
                                ctx->prio == 0;
         hp_status r = HP_OK;
-        const bool same = sl.graph_w == w && sl.graph_h == h && same_arena(sl.graph_arena);
+        const bool same = sl.graph_w == w && sl.graph_h == h && sl.graph_jpeg == (int)jpeg && same_arena(sl.graph_arena);
         if (graphable && sl.gexec && same) {
             if (cudaGraphLaunch(sl.gexec, s) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "graph launch");
         } else if (graphable && same) {
@@ -872,6 +1006,7 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
             }
             sl.graph_w = w;
             sl.graph_h = h;
+            sl.graph_jpeg = (int)jpeg;
             sl.graph_arena = akey;
         }
         cudaEventRecord(sl.done_ev, s);
@@ -887,6 +1022,7 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
             if (tile_of[i] >= 0) cudaEventSynchronize(ctx->slots[i].done_ev);
         return e;
     };
+    hp_status st = HP_OK;
     int scan = 0;
     while (true) {
         for (int i = 0; i < ns && !drained; ++i)
@@ -908,6 +1044,46 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
         if ((st = deliver(done))) return abandon(st);
     }
     return HP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_sink* sink) {
+    hp_status st = enter(ctx, 0);
+    if (st) return st;
+    if (!src || !src->next || !sink || !sink->done) {
+        set_err(ctx, "run_tiles: NULL source, sink or callback");
+        return HP_ERR_INVALID;
+    }
+    const int w = src->width, h = src->height;
+    if (w < 1 || h < 1 || w > ctx->cfg.max_width || h > ctx->cfg.max_height) {
+        set_err(ctx, "run_tiles: tile size %dx%d outside 1..%dx%d", w, h, ctx->cfg.max_width, ctx->cfg.max_height);
+        return HP_ERR_INVALID;
+    }
+    return run_tiles_impl(
+        ctx, w, h, false,
+        [&](const uint8_t** host, int64_t* pitch, int64_t* tid) { return src->next(src->user, host, pitch, tid); },
+        sink);
+}
+
+hp_status hp_run_tiles_jpeg(hp_ctx* ctx, const hp_jpeg_source* src, const hp_result_sink* sink) {
+    hp_status st = enter(ctx, 0);
+    if (st) return st;
+    if (!src || !src->next || !sink || !sink->done) {
+        set_err(ctx, "run_tiles_jpeg: NULL source, sink or callback");
+        return HP_ERR_INVALID;
+    }
+    const int w = src->width, h = src->height;
+    if (w < 1 || h < 1 || w > ctx->cfg.max_width || h > ctx->cfg.max_height) {
+        set_err(ctx, "run_tiles_jpeg: tile size %dx%d outside 1..%dx%d", w, h, ctx->cfg.max_width, ctx->cfg.max_height);
+        return HP_ERR_INVALID;
+    }
+    return run_tiles_impl(
+        ctx, w, h, true,
+        [&](const uint8_t** host, int64_t* nbytes, int64_t* tid) { return src->next(src->user, host, nbytes, tid); },
+        sink);
 }
 
 }  // extern "C"

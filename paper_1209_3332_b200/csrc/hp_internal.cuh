@@ -58,6 +58,20 @@ struct Worklist {
     int32_t ntx, nty; // tile grid
 };
 
+// header of a JPEG tile, parsed on the host (k_jpeg.cu jpeg_parse)
+struct JpegHdr {
+    int32_t width, height;
+    int32_t mcux, mcuy;          // 8x8 MCUs per row / column (4:4:4)
+    int32_t ri;                  // MCUs per restart interval (all MCUs when there is no DRI)
+    int32_t n_intervals;
+    int64_t scan_off, scan_len;  // the entropy-coded segment within the file
+    uint16_t q[3][64];           // dequantisation factor per component, natural order
+    uint8_t td[3], ta[3];        // DC table (0..3) and AC table (4..7) of each component
+    uint8_t pad[2];
+    uint8_t bits[8][17];         // BITS[1..16] of tables 0..3 (DC) and 4..7 (AC)
+    uint8_t vals[8][256];        // HUFFVAL
+};
+
 // ---------------------------------------------------------------- scratch of one slot
 struct Slot {
     // u8 planes
@@ -95,7 +109,13 @@ struct Slot {
     int32_t* cnt32;  // 32 ints: [1] edt any-bg, [2] features count, [4] run_tiles n_objects,
                      // [8..15] k_comp (S7-S11 queues), [16] S5 component count, [18..21] S6 queues
     // run_tiles staging
-    uint8_t* rgb_dev;
+    uint8_t* rgb_dev;            // also the JPEG file buffer of the compressed path (3N bytes)
+    JpegHdr* jhdr_dev;           // parsed header of the slot's JPEG tile (device)
+    JpegHdr* jhdr_host;          // pinned staging of that header (hp_run_tiles_jpeg)
+    int32_t* jstarts;            // restart-interval start offsets
+    int32_t* jblk;               // per-chunk restart-marker counts
+    int32_t* jerr;               // decode error word
+    int32_t* h_jerr;             // pinned copy of it, per delivered tile
     int32_t* lab_dev;
     int32_t *tab_label, *tab_flags, *tab_nrows;
     float* tab_feat;
@@ -110,7 +130,13 @@ struct Slot {
     // hp_run_tiles: the per-tile chain (compute + D2H) captured once as a CUDA graph
     cudaGraphExec_t gexec;
     int graph_w, graph_h;
+    int graph_jpeg;            // the graph decodes a JPEG tile (hp_run_tiles_jpeg)
     hp_row_arena graph_arena;  // the arena the graph was captured with (all zero: host rows)
+    // JPEG header staging ring of hp_process_tile_jpeg / hp_decode_jpeg: the host parses
+    // into entry k only after the copy issued from it last time has run (event)
+    JpegHdr* jhdr_ring;        // pinned [kJpegRing]
+    cudaEvent_t jhdr_ev[4];
+    int jhdr_pos;
     // high-priority side stream for the latency-bound stages (hp_ctx::prio)
     cudaStream_t hstream;
     cudaEvent_t fork_ev, join_ev;
@@ -147,6 +173,26 @@ void launch_cd(const uint8_t* rgb, int w, int h, int64_t pitch, const float* lut
                const hp_params& p, uint8_t* g, uint8_t* flags, unsigned long long* bg_count,
                cudaStream_t s);
 void upload_od_lut(float* lut_dev, cudaStream_t s);
+// S0/S1 from a JPEG tile (NEXT-3, k_jpeg.cu).  The host parses the marker segments into a
+// JpegHdr (the tables and the scan's place in the file); the device finds the restart markers,
+// Huffman-decodes one restart interval per thread, dequantises, runs the islow IDCT and
+// the YCbCr->RGB conversion, and feeds every pixel straight into S1 (cd_pixel.cuh): the
+// decoded RGB tile never reaches HBM.
+// Parse a baseline JPEG (T.81 B.2): SOF0/1 8-bit, 3 components with 1x1 sampling, one
+// interleaved sequential scan.  HP_ERR_UNSUPPORTED outside that scope, HP_ERR_INVALID on a
+// malformed stream; *why gets the reason.
+hp_status jpeg_parse(const uint8_t* data, int64_t n, JpegHdr* out, const char** why);
+// Capacity of the per-slot restart-interval offset array for a tile of npx pixels.
+inline int64_t jpeg_max_intervals(int64_t npx) { return npx / 64 + 64; }
+// Decode the file (device copy `file`, header `hdr` on the device) of a w x h tile.
+// rgb == nullptr: S1 fused (g, flags, bg_count as launch_cd); else the decoded RGB tile
+// (pitch rgb_pitch) only -- the verification path.  starts / blkcnt: slot scratch
+// (jpeg_max_intervals entries; file_cap / 8192 + 2 entries).  err: device int, OR-ed with
+// 1 (restart-marker count mismatch) or 2 (invalid Huffman code); the caller zeroes it.
+void launch_jpeg_decode(const JpegHdr* hdr, const uint8_t* file, int64_t file_cap, int w, int h, int32_t* starts,
+                        int32_t* blkcnt, const float* lut, const hp_params& p, uint8_t* g, uint8_t* flags,
+                        unsigned long long* bg_count, uint8_t* rgb, int64_t rgb_pitch, int32_t* err,
+                        cudaStream_t s);
 // S3
 void launch_open(const uint8_t* g, int w, int h, int diam, uint8_t* tmp, uint8_t* out,
                  cudaStream_t s);

@@ -8,39 +8,11 @@
 // one 16-B store each for g and flags (coalesced, 128-bit); scalar path for unaligned input.
 #include <cmath>
 
-#include "hp_internal.cuh"
+#include "cd_pixel.cuh"
 
 namespace hp {
 
 namespace {
-
-struct CdConst {
-    float q00, q10, q20, gs;
-    int t1, t2, bgmin;
-};
-
-__device__ __forceinline__ void cd_pixel(int R, int G, int B, const float* lut, const CdConst& k,
-                                         uint8_t& gout, uint8_t& fout, int& nbg) {
-    float cH = __fmaf_rn(lut[B], k.q20, __fmaf_rn(lut[G], k.q10, __fmul_rn(lut[R], k.q00)));
-    float s = rintf(__fmul_rn(cH, k.gs));
-    s = fminf(fmaxf(s, 0.0f), 255.0f);
-    gout = (uint8_t)s;
-    uint8_t f = 0;
-    if (R > k.t1 * G) f |= HP_FLAG_RBC_HI;
-    if (R > k.t2 * G) f |= HP_FLAG_RBC_LO;
-    if (R > B) f |= HP_FLAG_R_GT_B;
-    if (min(R, min(G, B)) > k.bgmin) {
-        f |= HP_FLAG_BG;
-        ++nbg;
-    }
-    fout = f;
-}
-
-__device__ __forceinline__ void block_count(int nbg, unsigned long long* out) {
-    // warp reduce, one atomic per warp
-    unsigned v = __reduce_add_sync(0xffffffffu, (unsigned)nbg);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, (unsigned long long)v);
-}
 
 __global__ void __launch_bounds__(256) k_cd_vec16(const uint8_t* __restrict__ rgb, int w, int h,
                                                   int64_t pitch, const float* __restrict__ lut_g,

@@ -40,7 +40,8 @@ EXPORTS = ["hp_default_params", "hp_ctx_create", "hp_ctx_destroy", "hp_status_st
            "hp_last_error", "hp_version", "hp_segment_tile", "hp_features_tile",
            "hp_process_tile", "hp_run_tiles", "hp_stage_run", "hp_set_stage_timing",
            "hp_get_stage_times", "hp_stage_times_accum", "hp_launch_count", "hp_reduce_rows",
-           "hp_group_center", "hp_group_std"]
+           "hp_group_center", "hp_group_std", "hp_run_tiles_jpeg", "hp_process_tile_jpeg",
+           "hp_decode_jpeg"]
 
 
 class HPError(RuntimeError):
@@ -111,6 +112,11 @@ class TileSource(C.Structure):
                 ("height", C.c_int32)]
 
 
+class JpegSource(C.Structure):
+    """hp_jpeg_source: next(user, &host_jpeg, &nbytes, &tile_id) -> 0 / 1 (drained)."""
+    _fields_ = [("next", NEXT_FN), ("user", C.c_void_p), ("width", C.c_int32), ("height", C.c_int32)]
+
+
 class RowArena(C.Structure):
     """hp_row_arena: device pointers (tile i64[cap], label i32[cap], flags i32[cap],
     feat f32[cap][36]), capacity, cursor (one device i64)."""
@@ -155,6 +161,10 @@ def lib():
             "hp_reduce_rows": (C.c_int, [P, P, P, i32, P, P, P]),
             "hp_group_center": (C.c_int, [P, P, P, i32, P, P, P, P]),
             "hp_group_std": (C.c_int, [P, P, P, i32, P, P, P]),
+            "hp_run_tiles_jpeg": (C.c_int, [P, C.POINTER(JpegSource), C.POINTER(ResultSink)]),
+            "hp_process_tile_jpeg": (C.c_int, [P, i32, P, C.c_int64, C.POINTER(Labels), C.POINTER(FeatureTable),
+                                               P, P]),
+            "hp_decode_jpeg": (C.c_int, [P, i32, P, C.c_int64, P, C.c_int64, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -305,9 +315,20 @@ class Context:
         With arena = (tile_ptr, label_ptr, flags_ptr, feat_ptr, capacity, cursor_ptr) (device
         pointers, hp_row_arena) the rows are appended on the device instead and
         on_done(tile_id, n_rows, status) is called."""
+        self._run(lib().hp_run_tiles, TileSource, "hp_run_tiles", next_tile, on_done, width, height, arena)
+
+    def run_tiles_jpeg(self, next_tile, on_done, width, height, arena=None):
+        """hp_run_tiles_jpeg (NEXT-3 compressed ingest): as run_tiles, but next_tile() returns
+        (host_ptr, nbytes, tile_id) of a baseline JPEG file of a width x height tile (pinned
+        memory recommended).  A file the decoder rejects is delivered with a nonzero status
+        and no rows."""
+        self._run(lib().hp_run_tiles_jpeg, JpegSource, "hp_run_tiles_jpeg", next_tile, on_done, width, height,
+                  arena)
+
+    def _run(self, fn, src_type, name, next_tile, on_done, width, height, arena):
         # ctypes prints and swallows an exception raised inside a C callback, so both
         # callbacks store the first one; after it no further tile is fed, and it is re-raised
-        # once hp_run_tiles has returned (the tiles already in flight are drained by then).
+        # once the driver has returned (the tiles already in flight are drained by then).
         keep = []
         err = []
 
@@ -343,11 +364,38 @@ class Context:
 
         nf, df = NEXT_FN(_next), DONE_FN(_done)
         keep += [nf, df]
-        src = TileSource(nf, None, width, height)
+        src = src_type(nf, None, width, height)
         ar = None if arena is None else RowArena(*arena)
         sink = ResultSink(df, None, C.pointer(ar) if ar is not None else None)
         keep.append(ar)
-        st = lib().hp_run_tiles(self._h, C.byref(src), C.byref(sink))
+        st = fn(self._h, C.byref(src), C.byref(sink))
         if err:
             raise err[0]
-        self._chk(st, "hp_run_tiles")
+        self._chk(st, name)
+
+    @staticmethod
+    def _host_buf(jpeg):
+        """(pointer, nbytes) of a host JPEG buffer: a numpy u8 array or a (pinned) CPU tensor."""
+        if hasattr(jpeg, "data_ptr"):
+            return jpeg.data_ptr(), jpeg.numel() * jpeg.element_size()
+        a = np.ascontiguousarray(jpeg, dtype=np.uint8)
+        return a.ctypes.data, a.nbytes
+
+    def process_tile_jpeg(self, slot, jpeg, labels, n_objects, t_label, t_flags, t_feat, n_rows,
+                          decode_err=None, stream=None):
+        """hp_process_tile_jpeg: one JPEG tile (host bytes, kept alive until the stream is
+        done) through both stages; decode_err: optional device int32 tensor."""
+        ptr, nb = self._host_buf(jpeg)
+        lab = Labels(labels.data_ptr(), labels.stride(0), n_objects.data_ptr())
+        tab = FeatureTable(t_label.data_ptr(), t_flags.data_ptr(), t_feat.data_ptr(),
+                           t_label.shape[0], n_rows.data_ptr())
+        self._chk(lib().hp_process_tile_jpeg(self._h, slot, C.c_void_p(ptr), nb, C.byref(lab), C.byref(tab),
+                                             None if decode_err is None else C.c_void_p(decode_err.data_ptr()),
+                                             _stream(stream)), "hp_process_tile_jpeg")
+
+    def decode_jpeg(self, slot, jpeg, rgb_out, stream=None):
+        """hp_decode_jpeg: decoded RGB into the device tensor rgb_out [H, W, 3] (synchronises)."""
+        ptr, nb = self._host_buf(jpeg)
+        self._chk(lib().hp_decode_jpeg(self._h, slot, C.c_void_p(ptr), nb, C.c_void_p(rgb_out.data_ptr()),
+                                       rgb_out.stride(0) * rgb_out.element_size(), _stream(stream)),
+                  "hp_decode_jpeg")

@@ -100,7 +100,8 @@ def test_struct_layouts_match_header(tmp_path):
     pairs = [("hp_params", hp.Params), ("hp_config", hp.Config), ("hp_image", hp.Image),
              ("hp_labels", hp.Labels), ("hp_feature_table", hp.FeatureTable),
              ("hp_stage_io", hp.StageIO), ("hp_tile_source", hp.TileSource),
-             ("hp_row_arena", hp.RowArena), ("hp_result_sink", hp.ResultSink)]
+             ("hp_row_arena", hp.RowArena), ("hp_result_sink", hp.ResultSink),
+             ("hp_jpeg_source", hp.JpegSource)]
     cname = {"in_": "in"}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "hp.h"', "int main(void) {"]
     expect = []
