@@ -210,7 +210,8 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
  * size in bytes (pinned memory recommended; valid until the tile is delivered).  Every file
  * must decode to exactly (width, height).  A file that fails on the host, or whose scan is
  * corrupt, is delivered through done() with HP_ERR_INVALID / HP_ERR_UNSUPPORTED and no rows;
- * the run continues with the next tile. */
+ * the run continues with the next tile.  (With a row arena, a corrupt-scan tile's run has
+ * already been appended on the device when its status arrives: drop it by tile id.) */
 typedef struct hp_jpeg_source {
     int   (*next)(void* user, const uint8_t** host_jpeg, int64_t* nbytes, int64_t* tile_id);
     void*   user;

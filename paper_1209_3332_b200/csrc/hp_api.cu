@@ -893,8 +893,11 @@ hp_status run_tiles_impl(hp_ctx* ctx, int w, int h, bool jpeg, Next next, const 
         int nrows = *sl.h_nrows;
         hp_status ts = st_of[i];
         if (nrows > mo) ts = HP_ERR_CAPACITY;
-        if (jpeg && *sl.h_jerr) ts = HP_ERR_INVALID;  // corrupt scan: the rows are not trustworthy
         int nr = std::min(nrows, mo);
+        if (jpeg && *sl.h_jerr) {  // corrupt scan: the rows are not trustworthy
+            ts = HP_ERR_INVALID;
+            if (!arena) nr = 0;    // (arena mode: the run was appended on the device already)
+        }
         if (arena) {  // rows stay in the device arena; the run [h_arena[1], +nr) may be clipped
             if (sl.h_arena[1] + nr > arena->capacity) ts = HP_ERR_CAPACITY;
             sink->done(sink->user, tile_of[i], nr, nullptr, nullptr, nullptr, ts);

@@ -8,10 +8,10 @@ worker, so the data path has no exchange step:
   key-value store), so faster GPUs simply take more tiles.
 * ``DistTileSource`` -- feeds ``Context.run_tiles`` (hp_run_tiles: per-slot H2D / compute /
   D2H streams, at most n_slots tiles in flight = the paper's window).
-* ``gather_rows`` -- the one collective: at the end, every rank's feature rows go to rank 0
-  (all_gather of counts, then a padded all_gather_into_tensor of packed rows -- NCCL over
-  NVLink on GPUs, gloo on CPU), merged into (tile_id, label) order so the table is identical
-  for any number of GPUs.
+* ``RowArena`` / ``gather_rows_device`` -- the one collective: rows stay on the GPU in an
+  hp_row_arena during the run; at the end every rank sends its rows to rank 0 device to
+  device (NCCL point-to-point over NVLink; gloo on CPU), where a stable sort by tile id gives
+  the (tile_id, label) order, so the table is identical for any number of GPUs.
 
 torch.distributed is plumbing here; the pixels never leave the GPU that processes them.
 """
@@ -160,46 +160,111 @@ def to_rows(results: dict) -> Rows:
 _FIELDS = (("tile", np.int64, 8), ("label", np.int32, 4), ("flags", np.int32, 4), ("feat", np.float32, 4 * NFEAT))
 
 
-def gather_rows(results: dict, device=None):
-    """Gather every rank's rows on rank 0 in (tile, label) order; None elsewhere.
+class DeviceRows:
+    """A feature table resident in device memory (torch tensors): tile i64[n], label i32[n],
+    flags i32[n], feat f32[n, 36] -- e.g. the first ``cursor`` rows of an hp_row_arena."""
 
-    One all_gather of the counts, then one all_gather_into_tensor of a flat per-rank buffer
-    holding each column in its own region (padded to the largest count); rank 0 merges the
-    per-tile runs."""
+    __slots__ = ("tile", "label", "flags", "feat")
+
+    def __init__(self, tile, label, flags, feat):
+        self.tile, self.label, self.flags, self.feat = tile, label, flags, feat
+
+    def __len__(self):
+        return int(self.tile.shape[0])
+
+    def to_host(self) -> Rows:
+        return Rows(self.tile.cpu().numpy(), self.label.cpu().numpy(), self.flags.cpu().numpy(),
+                    self.feat.cpu().numpy())
+
+    @staticmethod
+    def from_host(rows: Rows, device):
+        import torch
+        return DeviceRows(*(torch.from_numpy(np.ascontiguousarray(getattr(rows, n))).to(device)
+                            for n in ("tile", "label", "flags", "feat")))
+
+
+class RowArena:
+    """Device buffers of an hp_row_arena (hp.h): hp_run_tiles appends every tile's rows here,
+    so the rows never leave the GPU; ``arena`` is the tuple Context.run_tiles takes."""
+
+    def __init__(self, capacity: int, device):
+        import torch
+        self.capacity = int(capacity)
+        self.tile = torch.empty(self.capacity, dtype=torch.int64, device=device)
+        self.label = torch.empty(self.capacity, dtype=torch.int32, device=device)
+        self.flags = torch.empty(self.capacity, dtype=torch.int32, device=device)
+        self.feat = torch.empty((self.capacity, NFEAT), dtype=torch.float32, device=device)
+        self.cursor = torch.zeros(1, dtype=torch.int64, device=device)
+
+    @property
+    def arena(self):
+        return (self.tile.data_ptr(), self.label.data_ptr(), self.flags.data_ptr(), self.feat.data_ptr(),
+                self.capacity, self.cursor.data_ptr())
+
+    def rows(self) -> DeviceRows:
+        """The rows appended so far (reads the cursor: one device synchronisation)."""
+        n = min(int(self.cursor.item()), self.capacity)
+        return DeviceRows(self.tile[:n], self.label[:n], self.flags[:n], self.feat[:n])
+
+
+def gather_rows_device(rows: DeviceRows, device=None):
+    """The end-of-run gather: every rank's device-resident rows go to rank 0
+    only, device to device (NCCL point-to-point over NVLink on GPUs; gloo on CPU) -- no host
+    round trip and no all-gather to every rank.  Rank 0 returns the merged table in
+    (tile, label) order as DeviceRows, the other ranks None.  Each tile's rows are one
+    contiguous run in label order on one rank (hp_run_tiles delivers a tile's rows at once),
+    so a stable sort by tile id gives the canonical order for any number of GPUs."""
     import torch
     import torch.distributed as dist
-    local = to_rows(results)
+    dev = device if device is not None else rows.tile.device
     if not dist.is_initialized() or dist.get_world_size() == 1:
-        return local  # to_rows emits tile order; rows within a tile are label order
-    world = dist.get_world_size()
+        parts = [rows]
+    else:
+        world, rank = dist.get_world_size(), dist.get_rank()
+        cnt = torch.tensor([len(rows)], dtype=torch.int64, device=dev)
+        counts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+        dist.all_gather(counts, cnt)           # 8 bytes per rank
+        counts = [int(c.item()) for c in counts]
+        cols = ("tile", "label", "flags", "feat")
+        if rank != 0:
+            ops = [dist.P2POp(dist.isend, getattr(rows, c).contiguous(), 0) for c in cols] if counts[rank] else []
+            for w in (dist.batch_isend_irecv(ops) if ops else []):
+                w.wait()
+            return None
+        parts = [rows]
+        ops = []
+        for r in range(1, world):
+            n = counts[r]
+            if n == 0:
+                continue
+            part = DeviceRows(torch.empty(n, dtype=torch.int64, device=dev), torch.empty(n, dtype=torch.int32, device=dev),
+                              torch.empty(n, dtype=torch.int32, device=dev),
+                              torch.empty((n, NFEAT), dtype=torch.float32, device=dev))
+            ops += [dist.P2POp(dist.irecv, getattr(part, c), r) for c in cols]
+            parts.append(part)
+        for w in (dist.batch_isend_irecv(ops) if ops else []):
+            w.wait()
+    tile = torch.cat([p.tile for p in parts])
+    order = torch.argsort(tile, stable=True)
+    return DeviceRows(tile[order], torch.cat([p.label for p in parts])[order],
+                      torch.cat([p.flags for p in parts])[order], torch.cat([p.feat for p in parts])[order])
+
+
+def sort_rows(rows: DeviceRows) -> DeviceRows:
+    """(tile, label) order of one rank's device rows (a stable sort by tile id: each tile's
+    rows are one label-ordered run)."""
+    import torch
+    order = torch.argsort(rows.tile, stable=True)
+    return DeviceRows(rows.tile[order], rows.label[order], rows.flags[order], rows.feat[order])
+
+
+def gather_rows(results: dict, device=None):
+    """Gather host-delivered rows ({tile_id: (label, flags, feat)}, the sink callback's output)
+    on rank 0 in (tile, label) order through gather_rows_device; None on other ranks."""
+    import torch
     dev = device if device is not None else torch.device("cpu")
-    n = len(local)
-    cnt = torch.tensor([n], dtype=torch.int64, device=dev)
-    counts = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
-    dist.all_gather(counts, cnt)
-    counts = [int(c.item()) for c in counts]
-    mx = max(counts) if counts else 0
-    per = mx * ROW_BYTES
-    buf = torch.zeros(max(per, 1), dtype=torch.uint8, device=dev)
-    off = 0
-    for name, dt, nb in _FIELDS:
-        col = getattr(local, name)
-        if n:
-            buf[off:off + n * nb] = torch.from_numpy(col.reshape(-1).view(np.uint8)).to(dev)
-        off += mx * nb
-    out = torch.empty(world * max(per, 1), dtype=torch.uint8, device=dev)
-    dist.all_gather_into_tensor(out, buf)
-    if dist.get_rank() != 0:
-        return None
-    host = out.cpu().numpy()
-    parts = []
-    for r in range(world):
-        base, off, cols = r * max(per, 1), 0, {}
-        for name, dt, nb in _FIELDS:
-            cols[name] = host[base + off:base + off + counts[r] * nb].view(dt)
-            off += mx * nb
-        parts.append(Rows(cols["tile"], cols["label"], cols["flags"], cols["feat"]))
-    return merge_tile_runs(parts)
+    out = gather_rows_device(DeviceRows.from_host(to_rows(results), dev), dev)
+    return None if out is None else out.to_host()
 
 
 def merge_tile_runs(parts) -> Rows:
@@ -254,11 +319,18 @@ def aggregate_groups(rows: Rows, group_of_tile, n_groups: int, reduce, device=No
     import torch.distributed as dist
     if reduce is None or not all(hasattr(reduce, m) for m in ("reduce_rows", "group_center", "group_std")):
         raise TypeError("aggregate_groups needs a Context (hp_reduce_rows / hp_group_center / hp_group_std)")
-    off = group_offsets(rows, group_of_tile, n_groups)
     dev = device if device is not None else torch.device("cpu")
     multi = dist.is_initialized() and dist.get_world_size() > 1
-    feat_t = torch.from_numpy(np.ascontiguousarray(rows.feat)).to(dev)
-    off_t = torch.from_numpy(off).to(dev)
+    if isinstance(rows, DeviceRows):  # rows already on the device (e.g. a RowArena, sorted)
+        gid = group_of_tile(rows.tile)
+        if len(rows) and (bool((gid[1:] < gid[:-1]).any()) or int(gid[0]) < 0 or int(gid[-1]) >= n_groups):
+            raise ValueError("group ids must be non-decreasing in the table order and in [0, n_groups)")
+        feat_t = rows.feat.contiguous()
+        off_t = torch.searchsorted(gid.contiguous(), torch.arange(n_groups + 1, dtype=gid.dtype, device=gid.device))
+    else:
+        off = group_offsets(rows, group_of_tile, n_groups)
+        feat_t = torch.from_numpy(np.ascontiguousarray(rows.feat)).to(dev)
+        off_t = torch.from_numpy(off).to(dev)
     sums_t = torch.zeros((n_groups, NFEAT, 2), dtype=torch.float64, device=dev)
     cnt_t = torch.zeros(n_groups, dtype=torch.int64, device=dev)
     mm2_t = torch.zeros((n_groups, NFEAT, 2), dtype=torch.float64, device=dev)

@@ -682,6 +682,30 @@ def test_run_tiles_arena(ctx):
             assert_features_equal(lab[r], fl[r], ft[r], *ref[i])
 
 
+def test_arena_device_gather(ctx):
+    """dist.RowArena + gather_rows_device (one process): rows appended on the device in
+    completion order come back in (tile, label) order, equal to the oracle's tables."""
+    import torch
+    from paper_1209_3332_b200.dist import RowArena, gather_rows_device
+    tiles = [make_tile(330 + i, TileSpec(256, 320))["rgb"] for i in range(3)]
+    pinned = [torch.from_numpy(t).pin_memory() for t in tiles]
+    ref = [oracle.process_tile(rgb)[1:] for rgb in tiles]
+    ra = RowArena(sum(len(r[0]) for r in ref) * 3 + 16, "cuda")
+    order = iter([5, 1, 7, 3, 2, 0])
+
+    def nxt():
+        t = next(order, None)
+        return None if t is None else (pinned[t % 3].data_ptr(), 3 * 320, t)
+
+    ctx.run_tiles(nxt, lambda tid, n, st: None, 320, 256, arena=ra.arena)
+    tab = gather_rows_device(ra.rows()).to_host()
+    assert list(np.unique(tab.tile)) == [0, 1, 2, 3, 5, 7]
+    assert np.all(np.diff(tab.tile) >= 0)
+    for t in [0, 1, 2, 3, 5, 7]:
+        sel = tab.tile == t
+        assert_features_equal(tab.label[sel], tab.flags[sel], tab.feat[sel], *ref[t % 3])
+
+
 def test_run_tiles_arena_overflow(ctx):
     """An arena smaller than the rows: the cursor still counts every row, rows past the
     capacity are dropped, and the tiles whose run did not fit report HP_ERR_CAPACITY."""
