@@ -142,7 +142,9 @@ __device__ const uint8_t d_zigzag[64] = {0,  1,  8,  16, 9,  2,  3,  10, 17, 24,
                                          58, 59, 52, 45, 38, 31, 39, 46, 53, 60, 61, 54, 47, 55, 62, 63};
 
 constexpr int kChunk = 8192;  // bytes per restart-marker scan chunk (256 threads x 32 B)
-constexpr int kDT = 128;      // decode threads per block (one restart interval each)
+constexpr int kDT = 256;      // decode threads per block (one restart interval each); 2 blocks
+                              // per SM hold 75,776 threads, so a 4K tile's 65,536 intervals
+                              // (restart interval 4) run in one wave
 
 __device__ __forceinline__ bool is_rst(const uint8_t* s, int64_t i, int64_t len) {
     return i + 1 < len && s[i] == 0xFF && s[i + 1] >= 0xD0 && s[i + 1] <= 0xD7;
@@ -269,7 +271,8 @@ struct Bits {
     uint64_t buf;  // left-aligned
     int n;
     bool marker;   // a marker was met: the segment ended, feed zero bits
-    __device__ __forceinline__ void refill() {
+    // slow path: one byte at a time, byte stuffing (0xFF 0x00 -> 0xFF) and markers
+    __device__ __forceinline__ void refill_bytes() {
         while (n <= 56) {
             uint32_t b = 0;
             if (!marker && p < end) {
@@ -285,6 +288,27 @@ struct Bits {
             buf |= (uint64_t)b << (56 - n);
             n += 8;
         }
+    }
+    // fast path: the next 8 bytes in three aligned 32-bit loads; when none of them is 0xFF
+    // (no stuffing, no marker) the whole bytes that fit are appended at once
+    __device__ __forceinline__ void refill() {
+        if (n > 56) return;
+        if (!marker && p + 8 <= end) {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+            const uint32_t* wp = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+            const uint32_t sh = (uint32_t)(a & 3) * 8;
+            const uint32_t w0 = __ldg(wp), w1 = __ldg(wp + 1), w2 = __ldg(wp + 2);
+            const uint32_t lo = __funnelshift_r(w0, w1, sh), hi = __funnelshift_r(w1, w2, sh);  // bytes p..p+7
+            if (!(__vcmpeq4(lo, 0xffffffffu) | __vcmpeq4(hi, 0xffffffffu))) {
+                const uint64_t be = ((uint64_t)__byte_perm(lo, 0, 0x0123) << 32) | __byte_perm(hi, 0, 0x0123);
+                const int k = (64 - n) >> 3;  // whole bytes that fit: 1..8
+                buf |= (k == 8 ? be : (be >> (64 - 8 * k)) << (64 - 8 * k)) >> n;
+                p += k;
+                n += 8 * k;
+                return;
+            }
+        }
+        refill_bytes();
     }
     __device__ __forceinline__ int take(int s) {  // RECEIVE(s), s in 1..16
         const int v = (int)(buf >> (64 - s));
@@ -319,17 +343,20 @@ __device__ __forceinline__ int decode_sym(Bits& br, const HuffSm& T, int t) {
 constexpr int kF0298 = 2446, kF0390 = 3196, kF0541 = 4433, kF0765 = 6270, kF0899 = 7373, kF1175 = 9633,
               kF1501 = 12299, kF1847 = 15137, kF1961 = 16069, kF2053 = 16819, kF2562 = 20995, kF3072 = 25172;
 
-// the 1-D LLM butterfly on x0..x7; results rounded and shifted right by `sh`.  64-bit like
-// the IJG's JLONG: pass-2 products of extreme (but valid) blocks exceed 2^31.
-__device__ __forceinline__ void llm8(long long x0, long long x1, long long x2, long long x3, long long x4,
-                                     long long x5, long long x6, long long x7, int sh, int* o) {
-    const long long z1e = (x2 + x6) * kF0541;
-    const long long t2 = z1e - x6 * kF1847, t3 = z1e + x2 * kF0765;
-    const long long t0 = (x0 + x4) * 8192, t1 = (x0 - x4) * 8192;
-    const long long a10 = t0 + t3, a13 = t0 - t3, a11 = t1 + t2, a12 = t1 - t2;
-    long long z1 = x7 + x1, z2 = x5 + x3, z3 = x7 + x3, z4 = x5 + x1;
-    const long long z5 = (z3 + z4) * kF1175;
-    long long b0 = x7 * kF0298, b1 = x5 * kF2053, b2 = x3 * kF3072, b3 = x1 * kF1501;
+// the 1-D LLM butterfly on x0..x7; results rounded and shifted right by `sh`.  T = long long
+// is the IJG's JLONG; T = int is exact whenever every |input| <= kInt32Safe (the largest sum
+// of products is below 131520 * |input| < 2^31), which holds for every block of a JPEG
+// encoded from 8-bit samples -- the callers check and fall back to 64 bits otherwise.
+constexpr int kInt32Safe = 16000;
+template <class T>
+__device__ __forceinline__ void llm8(T x0, T x1, T x2, T x3, T x4, T x5, T x6, T x7, int sh, int* o) {
+    const T z1e = (x2 + x6) * kF0541;
+    const T t2 = z1e - x6 * kF1847, t3 = z1e + x2 * kF0765;
+    const T t0 = (x0 + x4) * 8192, t1 = (x0 - x4) * 8192;
+    const T a10 = t0 + t3, a13 = t0 - t3, a11 = t1 + t2, a12 = t1 - t2;
+    T z1 = x7 + x1, z2 = x5 + x3, z3 = x7 + x3, z4 = x5 + x1;
+    const T z5 = (z3 + z4) * kF1175;
+    T b0 = x7 * kF0298, b1 = x5 * kF2053, b2 = x3 * kF3072, b3 = x1 * kF1501;
     z1 *= -kF0899;
     z2 *= -kF2562;
     z3 = z3 * -kF1961 + z5;
@@ -338,7 +365,7 @@ __device__ __forceinline__ void llm8(long long x0, long long x1, long long x2, l
     b1 += z2 + z4;
     b2 += z2 + z3;
     b3 += z1 + z4;
-    const long long rnd = 1ll << (sh - 1);
+    const T rnd = (T)1 << (sh - 1);
     o[0] = (int)((a10 + b3 + rnd) >> sh);
     o[7] = (int)((a10 - b3 + rnd) >> sh);
     o[1] = (int)((a11 + b2 + rnd) >> sh);
@@ -373,9 +400,12 @@ __device__ __forceinline__ void idct_block(int* c, uint64_t mask, const uint16_t
             continue;
         }
         long long x[8];
+        long long amax = 0;
 #pragma unroll
-        for (int r = 0; r < 8; ++r)
+        for (int r = 0; r < 8; ++r) {
             x[r] = ((cm >> (8 * r)) & 1) ? (long long)c[(r * 8 + col) * kDT] * q[r * 8 + col] : 0;
+            amax = max(amax, x[r] < 0 ? -x[r] : x[r]);
+        }
         if ((cm & ~1ull) == 0) {  // only the DC of this column
             const int v = (int)(x[0] * 4);
 #pragma unroll
@@ -384,7 +414,10 @@ __device__ __forceinline__ void idct_block(int* c, uint64_t mask, const uint16_t
             continue;
         }
         int o[8];
-        llm8(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7], 13 - 2, o);
+        if (amax <= kInt32Safe)
+            llm8<int>((int)x[0], (int)x[1], (int)x[2], (int)x[3], (int)x[4], (int)x[5], (int)x[6], (int)x[7], 13 - 2, o);
+        else
+            llm8<long long>(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7], 13 - 2, o);
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             c[(r * 8 + col) * kDT] = o[r];
@@ -401,7 +434,16 @@ __device__ __forceinline__ void idct_block(int* c, uint64_t mask, const uint16_t
             for (int k = 0; k < 8; ++k) s[k] = v;
         } else {
             int o[8];
-            llm8(w[0], w[kDT], w[2 * kDT], w[3 * kDT], w[4 * kDT], w[5 * kDT], w[6 * kDT], w[7 * kDT], 13 + 2 + 3, o);
+            int v[8], amax = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                v[k] = w[k * kDT];
+                amax = max(amax, abs(v[k]));
+            }
+            if (amax <= kInt32Safe)
+                llm8<int>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], 13 + 2 + 3, o);
+            else
+                llm8<long long>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], 13 + 2 + 3, o);
 #pragma unroll
             for (int k = 0; k < 8; ++k) s[k] = clamp255(o[k] + 128);
         }
@@ -418,7 +460,7 @@ __device__ __forceinline__ void ycc_rgb(int y, int cb, int cr, int& R, int& G, i
 }
 
 template <bool kRGB>
-__global__ void __launch_bounds__(kDT) k_jpeg_decode(const JpegHdr* __restrict__ H, const uint8_t* __restrict__ file,
+__global__ void __launch_bounds__(kDT, 2) k_jpeg_decode(const JpegHdr* __restrict__ H, const uint8_t* __restrict__ file,
                                                      const int32_t* __restrict__ starts, const float* __restrict__ lut_g,
                                                      CdConst k, uint8_t* __restrict__ g, uint8_t* __restrict__ flags,
                                                      unsigned long long* bg_count, uint8_t* __restrict__ rgb,
@@ -553,7 +595,7 @@ void launch_jpeg_decode(const JpegHdr* hdr, const uint8_t* file, int64_t file_ca
         return 0;
     });
     const int64_t nint_max = ((int64_t)((w + 7) / 8) * ((h + 7) / 8));
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nint_max + kDT - 1) / kDT, nsm * 3));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nint_max + kDT - 1) / kDT, nsm * 2));
     const CdConst k = cd_const(p);
     if (rgb)
         (note_launch(), k_jpeg_decode<true><<<grid, kDT, dyn, s>>>(hdr, file, starts, lut, k, g, flags, nullptr, rgb,

@@ -66,6 +66,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HP_RG_PACKSCAN
 #define HP_RG_PACKSCAN 0  // both scan directions at once on packed u16x2 clamps (r1: S4 0.78 -> 0.82 ms, bench 843 -> 834: off)
 #endif
+#ifndef HP_RG_INIT
+#define HP_RG_INIT 0  // raster + anti-raster initialisation sweep per region before the queue engine
+#endif
 #ifndef HP_PPL
 #define HP_PPL 2  // pixels per lane: sub-tiles of 64 x 32 px, regions of 256 x 128 px
 #endif
@@ -686,12 +689,12 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
     }
 }
 
-__global__ void k_rg_reset(Worklist wl) {
+__global__ void k_rg_reset(Worklist wl, bool seeded) {
     const int n = wl.ntx * wl.nty;
     const int lim = max(wl.cap, n * NW);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < lim; i += gridDim.x * blockDim.x) {
         if (i < n) wl.state[i] = ST_QUEUED;
-        if (i < n * NW) wl.inrows[i] = 0xffffffffu;
+        if (i < n * NW && !seeded) wl.inrows[i] = 0xffffffffu;
         if (i < wl.cap) {
             int32_t v = EMPTY;
             if (i < n) {
@@ -716,6 +719,168 @@ __global__ void k_rg_reset(Worklist wl) {
     }
     if (blockIdx.x == 0 && threadIdx.x < 8)
         wl.ctr[threadIdx.x] = (threadIdx.x == 1 || threadIdx.x == 2) ? (unsigned long long)n : 0ull;
+}
+
+// ---- Vincent's hybrid initialisation ("Vincent MR"), per
+// region: a raster sweep (rows top to bottom, each row closed horizontally in both directions
+// with the row above as input) then an anti-raster sweep (bottom to top, the row below as
+// input), one warp per 256 x 128 px region, values in registers (PXL pixels per lane).  Every
+// update is a monotone step toward the reconstruction, so the queue engine that follows
+// reaches the same fixed point; it is seeded with exactly the sub-tile rows that still hold
+// an improvable pixel (k_rg_seed), instead of every row of every region.
+constexpr int PXL = RX * SW / 32;  // pixels per lane across a region row
+
+__device__ __forceinline__ void row_io_load(const uint8_t* __restrict__ p, int w, int h, int x0, int y, int* v) {
+#pragma unroll
+    for (int j = 0; j < PXL; ++j) v[j] = 0;
+    if (y < 0 || y >= h) return;
+    const uint8_t* rp = p + (int64_t)y * w;
+#pragma unroll
+    for (int j = 0; j < PXL; ++j)
+        if (x0 + j < w) v[j] = __ldcg(reinterpret_cast<const unsigned char*>(rp + x0 + j));
+}
+
+__device__ __forceinline__ int px_load(const uint8_t* __restrict__ p, int w, int h, int x, int y) {
+    return (x < 0 || y < 0 || x >= w || y >= h) ? 0 : (int)__ldcg(reinterpret_cast<const unsigned char*>(p + (int64_t)y * w + x));
+}
+
+// close one region row: lo[j] = min(m, max(r, nb)) then the horizontal clamp scans in both
+// directions (the region's left / right halo pixels as boundary inputs); returns the new row
+__device__ __forceinline__ void close_row(const int* m, const int* r, const int* nb, int lft, int rgt, int lane,
+                                          int* u) {
+    int lo[PXL];
+#pragma unroll
+    for (int j = 0; j < PXL; ++j) {
+        int b = max(r[j], nb[j]);
+        if (j == 0 && lane == 0) b = max(b, lft);
+        if (j == PXL - 1 && lane == 31) b = max(b, rgt);
+        lo[j] = min(b, m[j]);
+    }
+    int FL = lo[0], FH = m[0];
+#pragma unroll
+    for (int j = 1; j < PXL; ++j) {
+        FL = min(m[j], max(lo[j], FL));
+        FH = min(m[j], max(lo[j], FH));
+    }
+    int BL = lo[PXL - 1], BH = m[PXL - 1];
+#pragma unroll
+    for (int j = PXL - 2; j >= 0; --j) {
+        BL = min(m[j], max(lo[j], BL));
+        BH = min(m[j], max(lo[j], BH));
+    }
+    int in = __shfl_up_sync(FULL, clamp_scan<true>(FL, FH, lane), 1);
+    int ib = __shfl_down_sync(FULL, clamp_scan<false>(BL, BH, lane), 1);
+    if (lane == 0) in = 0;
+    if (lane == 31) ib = 0;
+    int fw[PXL];
+#pragma unroll
+    for (int j = 0; j < PXL; ++j) {
+        in = min(m[j], max(lo[j], in));
+        fw[j] = in;
+    }
+#pragma unroll
+    for (int j = PXL - 1; j >= 0; --j) {
+        ib = min(m[j], max(lo[j], ib));
+        u[j] = max(fw[j], ib);
+    }
+}
+
+// 3-wide max of a neighbouring row held in registers (xl / xr: the pixels just outside)
+__device__ __forceinline__ void max3_row(const int* v, int xl, int xr, int lane, int* out) {
+    int left = __shfl_up_sync(FULL, v[PXL - 1], 1), right = __shfl_down_sync(FULL, v[0], 1);
+    if (lane == 0) left = xl;
+    if (lane == 31) right = xr;
+#pragma unroll
+    for (int j = 0; j < PXL; ++j)
+        out[j] = max(v[j], max(j == 0 ? left : v[j - 1], j == PXL - 1 ? right : v[j + 1]));
+}
+
+__global__ void __launch_bounds__(128) k_rg_init(const uint8_t* __restrict__ mask, uint8_t* __restrict__ R, int w,
+                                                 int h, int ntx, int nty) {
+    const int lane = threadIdx.x & 31;
+    const int t = blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (t >= ntx * nty) return;
+    const int X0 = (t % ntx) * RX * SW, Y0 = (t / ntx) * RY * kTile;
+    const int Y1 = min(h, Y0 + RY * kTile);
+    const int x0 = X0 + PXL * lane;
+    int prev[PXL], m[PXL], r[PXL], nb[PXL], u[PXL];
+    // raster: the row above as input (the first from memory)
+    row_io_load(R, w, h, x0, Y0 - 1, prev);
+    int pl = px_load(R, w, h, X0 - 1, Y0 - 1), pr = px_load(R, w, h, X0 + RX * SW, Y0 - 1);
+    for (int y = Y0; y < Y1; ++y) {
+        row_io_load(mask, w, h, x0, y, m);
+        row_io_load(R, w, h, x0, y, r);
+        const int lft = px_load(R, w, h, X0 - 1, y), rgt = px_load(R, w, h, X0 + RX * SW, y);
+        max3_row(prev, pl, pr, lane, nb);
+        close_row(m, r, nb, lft, rgt, lane, u);
+        uint8_t* rp = R + (int64_t)y * w;
+#pragma unroll
+        for (int j = 0; j < PXL; ++j) {
+            if (x0 + j < w && u[j] != r[j]) __stcg(reinterpret_cast<unsigned char*>(rp + x0 + j), (unsigned char)u[j]);
+            prev[j] = u[j];
+        }
+        pl = lft;
+        pr = rgt;
+    }
+    // anti-raster: the row below as input (the first from memory); the row above from memory
+    row_io_load(R, w, h, x0, Y1, prev);
+    pl = px_load(R, w, h, X0 - 1, Y1);
+    pr = px_load(R, w, h, X0 + RX * SW, Y1);
+    for (int y = Y1 - 1; y >= Y0; --y) {
+        int up[PXL], upm[PXL];
+        row_io_load(mask, w, h, x0, y, m);
+        row_io_load(R, w, h, x0, y, r);
+        row_io_load(R, w, h, x0, y - 1, up);
+        const int lft = px_load(R, w, h, X0 - 1, y), rgt = px_load(R, w, h, X0 + RX * SW, y);
+        max3_row(prev, pl, pr, lane, nb);
+        max3_row(up, px_load(R, w, h, X0 - 1, y - 1), px_load(R, w, h, X0 + RX * SW, y - 1), lane, upm);
+#pragma unroll
+        for (int j = 0; j < PXL; ++j) nb[j] = max(nb[j], upm[j]);
+        close_row(m, r, nb, lft, rgt, lane, u);
+        uint8_t* rp = R + (int64_t)y * w;
+#pragma unroll
+        for (int j = 0; j < PXL; ++j) {
+            if (x0 + j < w && u[j] != r[j]) __stcg(reinterpret_cast<unsigned char*>(rp + x0 + j), (unsigned char)u[j]);
+            prev[j] = u[j];
+        }
+        pl = lft;
+        pr = rgt;
+    }
+}
+
+// inrows of every sub-tile = its rows holding a pixel p that some 8-neighbour q can still
+// improve (min(R(q), M(p)) > R(p)); one warp per sub-tile, lane = PPL pixels of a row
+__global__ void __launch_bounds__(256) k_rg_seed(const uint8_t* __restrict__ mask, const uint8_t* __restrict__ R,
+                                                 int w, int h, Worklist wl) {
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int nreg = wl.ntx * wl.nty;
+    if (gw >= nreg * NW) return;
+    const int t = gw / NW, sub = gw % NW;
+    const int X0 = (t % wl.ntx) * RX * SW + (sub % RX) * SW, Y0 = (t / wl.ntx) * RY * kTile + (sub / RX) * kTile;
+    uint32_t rows = 0;
+    for (int yy = 0; yy < kTile; ++yy) {
+        const int y = Y0 + yy;
+        bool imp = false;
+        if (y < h) {
+#pragma unroll
+            for (int j = 0; j < PPL; ++j) {
+                const int x = X0 + PPL * lane + j;
+                if (x >= w) continue;
+                const int rp = px_load(R, w, h, x, y), mp = px_load(mask, w, h, x, y);
+                if (rp >= mp) continue;  // already at its mask: cannot rise
+                int nbv = 0;
+#pragma unroll
+                for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+                    for (int dx = -1; dx <= 1; ++dx)
+                        if (dx || dy) nbv = max(nbv, px_load(R, w, h, x + dx, y + dy));
+                imp |= min(nbv, mp) > rp;
+            }
+        }
+        if (__any_sync(FULL, imp)) rows |= 1u << yy;
+    }
+    if (lane == 0) wl.inrows[t * NW + sub] = rows;
 }
 
 #if HP_RG_ORDER >= 2
@@ -818,7 +983,15 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
     wl.ntx = (w + RX * SW - 1) / (RX * SW);
     wl.nty = (h + RY * kTile - 1) / (RY * kTile);
     const int n = wl.ntx * wl.nty;
-    (note_launch(), k_rg_reset<<<(int)std::min<int64_t>((std::max<int64_t>(wl.cap, (int64_t)n * NW) + 255) / 256, num_sms() * 16), 256, 0, s>>>(wl));
+    static const int init_env = [] {  // HP_RG_INIT=0/1 overrides the compile-time default
+        const char* e = getenv("HP_RG_INIT");
+        return e ? atoi(e) : HP_RG_INIT;
+    }();
+    (note_launch(), k_rg_reset<<<(int)std::min<int64_t>((std::max<int64_t>(wl.cap, (int64_t)n * NW) + 255) / 256, num_sms() * 16), 256, 0, s>>>(wl, init_env != 0));
+    if (init_env) {
+        (note_launch(), k_rg_init<<<(n + 3) / 4, 128, 0, s>>>(mask, R, w, h, wl.ntx, wl.nty));
+        (note_launch(), k_rg_seed<<<(n * NW + 7) / 8, 256, 0, s>>>(mask, R, w, h, wl));
+    }
 #if HP_RG_ORDER >= 2
     // keys in the region-state array past the regions (it is sized for the 32x32 tiles of the
     // tile engine, 32 entries per region)
