@@ -481,7 +481,8 @@ __global__ void __launch_bounds__(kDT, 2) k_jpeg_decode(const JpegHdr* __restric
     const int64_t nmcu = (int64_t)mcux * H->mcuy;
     const uint8_t* scan = file + H->scan_off;
     const uint8_t* scan_end = scan + H->scan_len;
-    const int td[3] = {H->td[0], H->td[1], H->td[2]}, ta[3] = {H->ta[0], H->ta[1], H->ta[2]};
+    // table ids of the three components packed in bytes (no local-memory arrays)
+    const uint32_t tdp = H->td[0] | H->td[1] << 8 | H->td[2] << 16, tap = H->ta[0] | H->ta[1] << 8 | H->ta[2] << 16;
     const bool vec8 = (w & 7) == 0;
     int nbg = 0;
     for (int iv = blockIdx.x * kDT + threadIdx.x; iv < nint; iv += gridDim.x * kDT) {
@@ -495,14 +496,14 @@ __global__ void __launch_bounds__(kDT, 2) k_jpeg_decode(const JpegHdr* __restric
             for (int cpt = 0; cpt < 3; ++cpt) {
                 // --- F.2.2.1 / F.2.2.2: the block's coefficients, zig-zag -> natural order
                 br.refill();
-                int t = decode_sym(br, T, td[cpt]);
+                int t = decode_sym(br, T, (tdp >> (8 * cpt)) & 0xff);
                 if (t < 0 || t > 15) { bad = true; break; }
                 pred[cpt] += t ? extend(br.take(t), t) : 0;
                 coef[0] = pred[cpt];
                 uint64_t mask = 1;
                 for (int kk = 1; kk < 64;) {
                     if (br.n < 32) br.refill();
-                    const int rs = decode_sym(br, T, ta[cpt]);
+                    const int rs = decode_sym(br, T, (tap >> (8 * cpt)) & 0xff);
                     if (rs < 0) { bad = true; break; }
                     const int ss = rs & 15, rr = rs >> 4;
                     if (ss == 0) {

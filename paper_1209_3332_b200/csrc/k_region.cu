@@ -66,6 +66,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HP_RG_PACKSCAN
 #define HP_RG_PACKSCAN 0  // both scan directions at once on packed u16x2 clamps (r1: S4 0.78 -> 0.82 ms, bench 843 -> 834: off)
 #endif
+#ifndef HP_RG_ADI
+#define HP_RG_ADI 0  // alternating-direction (row / column phase) region closure instead of sub-tile sweeps
+#endif
 #ifndef HP_RG_INIT
 #define HP_RG_INIT 0  // raster + anti-raster initialisation sweep per region before the queue engine
 #endif
@@ -883,6 +886,445 @@ __global__ void __launch_bounds__(256) k_rg_seed(const uint8_t* __restrict__ mas
     if (lane == 0) wl.inrows[t * NW + sub] = rows;
 }
 
+// ---- Alternating-direction region closure (HP_RG_ADI): the same queue, states and window as
+// k_region_mr8, but a region job closes its window by alternating two synchronous phases over
+// the whole region instead of asynchronous 64 x 32 sub-tile sweeps:
+//   row phase     every dirty region row closed across the full 256 px (8 px per lane, the
+//                 clamp scans of row()), its rows above / below as inputs;
+//   column phase  every dirty region column closed along its full 128 px (4 px per lane,
+//                 the same clamp scans vertically), its columns left / right as inputs.
+// A pixel a phase raises marks, for the other direction, exactly the lines of the neighbours
+// it can still improve (min(R(p), M(q)) > R(q)), so a horizontal run closes in one row step
+// and a vertical run in one column step -- a 1-px corridor crosses a region in one phase per
+// turn instead of one dependent row closure per row.  Monotone updates: same fixed point.
+constexpr int ACOLS = RX * SW;      // region columns (256)
+constexpr int AROWS = RY * kTile;   // region rows (128)
+constexpr int CPL = AROWS / 32;     // column pixels per lane (4)
+static_assert(PXL == 8 && CPL == 4, "ADI closure assumes 256 x 128 px regions");
+
+struct SmemA {
+    uint32_t R[ROWS * RWW];
+    uint32_t M[ROWS * RWW];
+    uint32_t rowdirty[AROWS / 32];   // bit y-1: window row y needs a row closure
+    uint32_t coldirty[ACOLS / 32];   // bit c-1: window column c needs a column closure
+    uint32_t rowsnap[AROWS / 32];
+    uint32_t colsnap[ACOLS / 32];
+    uint32_t subchg[NW];             // per sub-tile: rows that changed in this job
+    uint32_t dirty_in[NW];
+    int any;
+    int job;
+    int again;
+    unsigned long long t0;
+};
+
+__global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_adi(const uint8_t* __restrict__ mask,
+                                                           uint8_t* __restrict__ R, int w, int h, Worklist wl) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SmemA& S = *reinterpret_cast<SmemA*>(smem_raw);
+    const uint8_t* sR = reinterpret_cast<const uint8_t*>(S.R);
+    uint8_t* sRw = reinterpret_cast<uint8_t*>(S.R);
+    const uint8_t* sM = reinterpret_cast<const uint8_t*>(S.M);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto improves = [&](int pr, int pc, int qr, int qc) {
+        return min((int)sR[bidx(pr, pc)], (int)sM[bidx(qr, qc)]) > (int)sR[bidx(qr, qc)];
+    };
+    auto mark = [&](uint32_t* bits, int i) { atomicOr(&bits[i >> 5], 1u << (i & 31)); };
+
+    // close window row wr (1..AROWS) across the region; returns the lane's changed-pixel mask
+    auto row_close = [&](int wr) -> uint32_t {
+        const int c0 = PXL * lane + 1;
+        int m[PXL], r[PXL], nb[PXL], u[PXL];
+        int upv[PXL + 2], dnv[PXL + 2];
+#pragma unroll
+        for (int j = -1; j <= PXL; ++j) {
+            upv[j + 1] = sR[bidx(wr - 1, c0 + j)];
+            dnv[j + 1] = sR[bidx(wr + 1, c0 + j)];
+        }
+#pragma unroll
+        for (int j = 0; j < PXL; ++j) {
+            m[j] = sM[bidx(wr, c0 + j)];
+            r[j] = sR[bidx(wr, c0 + j)];
+            nb[j] = max(max(max(upv[j], upv[j + 1]), upv[j + 2]), max(max(dnv[j], dnv[j + 1]), dnv[j + 2]));
+        }
+        const int lft = sR[bidx(wr, c0 - 1)], rgt = sR[bidx(wr, c0 + PXL)];
+        bool can = false;
+#pragma unroll
+        for (int j = 0; j < PXL; ++j) {
+            const int hn = max(j == 0 ? lft : r[j - 1], j == PXL - 1 ? rgt : r[j + 1]);
+            can |= min(max(nb[j], hn), m[j]) > r[j];
+        }
+        if (!__any_sync(FULL, can)) return 0;
+        close_row(m, r, nb, lft, rgt, lane, u);
+        uint32_t chg = 0;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < PXL; ++j)
+            if (u[j] != r[j]) {
+                sRw[bidx(wr, c0 + j)] = (uint8_t)u[j];
+                chg |= 1u << j;
+            }
+        __syncwarp();
+        return chg;
+    };
+    // close window column wc (1..ACOLS) along the region; lane owns rows 4*lane+1 .. +4
+    auto col_close = [&](int wc) -> uint32_t {
+        const int r0 = CPL * lane + 1;
+        int m[CPL], r[CPL], nb[CPL], u[CPL];
+        int lv[CPL + 2], rv[CPL + 2];
+#pragma unroll
+        for (int j = -1; j <= CPL; ++j) {
+            lv[j + 1] = sR[bidx(r0 + j, wc - 1)];
+            rv[j + 1] = sR[bidx(r0 + j, wc + 1)];
+        }
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+            m[j] = sM[bidx(r0 + j, wc)];
+            r[j] = sR[bidx(r0 + j, wc)];
+            nb[j] = max(max(max(lv[j], lv[j + 1]), lv[j + 2]), max(max(rv[j], rv[j + 1]), rv[j + 2]));
+        }
+        const int top = sR[bidx(r0 - 1, wc)], bot = sR[bidx(r0 + CPL, wc)];
+        bool can = false;
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+            const int vn = max(j == 0 ? top : r[j - 1], j == CPL - 1 ? bot : r[j + 1]);
+            can |= min(max(nb[j], vn), m[j]) > r[j];
+        }
+        if (!__any_sync(FULL, can)) return 0;
+        int lo[CPL];
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+            int b = max(r[j], nb[j]);
+            if (j == 0 && lane == 0) b = max(b, top);
+            if (j == CPL - 1 && lane == 31) b = max(b, bot);
+            lo[j] = min(b, m[j]);
+        }
+        int FL = lo[0], FH = m[0];
+#pragma unroll
+        for (int j = 1; j < CPL; ++j) {
+            FL = min(m[j], max(lo[j], FL));
+            FH = min(m[j], max(lo[j], FH));
+        }
+        int BL = lo[CPL - 1], BH = m[CPL - 1];
+#pragma unroll
+        for (int j = CPL - 2; j >= 0; --j) {
+            BL = min(m[j], max(lo[j], BL));
+            BH = min(m[j], max(lo[j], BH));
+        }
+        int in = __shfl_up_sync(FULL, clamp_scan<true>(FL, FH, lane), 1);
+        int ib = __shfl_down_sync(FULL, clamp_scan<false>(BL, BH, lane), 1);
+        if (lane == 0) in = 0;
+        if (lane == 31) ib = 0;
+        int fw[CPL];
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) {
+            in = min(m[j], max(lo[j], in));
+            fw[j] = in;
+        }
+#pragma unroll
+        for (int j = CPL - 1; j >= 0; --j) {
+            ib = min(m[j], max(lo[j], ib));
+            u[j] = max(fw[j], ib);
+        }
+        uint32_t chg = 0;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < CPL; ++j)
+            if (u[j] != r[j]) {
+                sRw[bidx(r0 + j, wc)] = (uint8_t)u[j];
+                chg |= 1u << j;
+            }
+        __syncwarp();
+        return chg;
+    };
+
+    while (true) {
+        if (threadIdx.x == 0) {
+            int t = -1;
+            const unsigned long long hd = vload(&wl.ctr[0]), tl = vload(&wl.ctr[1]);
+            bool retire = false;
+            if (hd >= tl + HP_RG_WAITERS) {
+                const unsigned long long rr = atomicAdd(&wl.ctr[7], 1ull);
+                if (rr + HP_RG_MIN_ALIVE < gridDim.x) retire = true;
+                else atomicAdd(&wl.ctr[7], ~0ull);
+            }
+            if (!retire) {
+                t = q_pop(wl);
+                if (t >= 0) atomicExch(&wl.state[t], ST_BUSY);
+            }
+            S.t0 = gtimer();
+            S.job = t;
+        }
+        __syncthreads();
+        const int t = S.job;
+        if (t < 0) break;
+        const int rx = t % wl.ntx, ry = t / wl.ntx;
+        const int X0 = rx * RX * SW, Y0 = ry * RY * kTile;
+        const bool inner = X0 >= 4 && X0 + RX * SW + 4 <= w && Y0 >= 1 && Y0 + RY * kTile + 1 <= h &&
+                           (w & 3) == 0 && (((uintptr_t)R | (uintptr_t)mask) & 3) == 0;
+        bool have_window = false;
+        while (true) {
+            if (lane == 0) {
+                S.dirty_in[warp] = atomicExch(&wl.inrows[t * NW + warp], 0u);
+                S.subchg[warp] = 0;
+            }
+            if (threadIdx.x < AROWS / 32) S.rowdirty[threadIdx.x] = 0;
+            if (threadIdx.x < ACOLS / 32) S.coldirty[threadIdx.x] = 0;
+            __threadfence();
+            __syncthreads();
+            int any_in = 0;
+#pragma unroll
+            for (int k = 0; k < NW; ++k) any_in |= S.dirty_in[k] != 0;
+            if (any_in) {
+                if (!have_window) {
+                    constexpr int NIT = (ROWS * RWW + NW * 32 - 1) / (NW * 32);
+                    uint32_t vr[NIT], vm[NIT];
+                    if (inner) {
+                        const uint8_t* rb = R + (int64_t)(Y0 - 1) * w + (X0 - 4);
+                        const uint8_t* mb = mask + (int64_t)(Y0 - 1) * w + (X0 - 4);
+#pragma unroll
+                        for (int i = 0; i < NIT; ++i) {
+                            int k = threadIdx.x + i * NW * 32;
+                            if (k < ROWS * RWW) {
+                                int rr = k / RWW, wi = k - rr * RWW;
+                                int64_t o = (int64_t)rr * w + 4 * wi;
+                                vr[i] = __ldcg(reinterpret_cast<const unsigned int*>(rb + o));
+                                vm[i] = __ldcg(reinterpret_cast<const unsigned int*>(mb + o));
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < NIT; ++i) {
+                            int k = threadIdx.x + i * NW * 32;
+                            if (k < ROWS * RWW) {
+                                int rr = k / RWW, wi = k - rr * RWW;
+                                int gx = X0 - 4 + 4 * wi, gy = Y0 - 1 + rr;
+                                vr[i] = load_word(R, w, h, gx, gy);
+                                vm[i] = load_word(mask, w, h, gx, gy);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < NIT; ++i) {
+                        int k = threadIdx.x + i * NW * 32;
+                        if (k < ROWS * RWW) {
+                            S.R[k] = vr[i];
+                            S.M[k] = vm[i];
+                        }
+                    }
+                    have_window = true;
+                } else {
+                    constexpr int NH = 2 * RWW + 2 * (ROWS - 2);
+                    for (int k = threadIdx.x; k < NH; k += blockDim.x) {
+                        int rr, wi;
+                        if (k < 2 * RWW) {
+                            rr = k < RWW ? 0 : ROWS - 1;
+                            wi = k % RWW;
+                        } else {
+                            int j = k - 2 * RWW;
+                            rr = 1 + (j >> 1);
+                            wi = (j & 1) ? RWW - 1 : 0;
+                        }
+                        S.R[rr * RWW + wi] = load_word(R, w, h, X0 - 4 + 4 * wi, Y0 - 1 + rr);
+                    }
+                }
+                // the job's dirty sub-tile rows are region rows for the first row phase
+                if (lane == 0) {
+                    const uint32_t d = S.dirty_in[warp];
+                    if (d) atomicOr(&S.rowdirty[(warp / RX) * (kTile / 32)], d);
+                }
+                __syncthreads();
+                int phases = 0, lines = 0;
+                while (true) {
+                    // ---- row phase
+                    if (threadIdx.x < AROWS / 32) {
+                        S.rowsnap[threadIdx.x] = S.rowdirty[threadIdx.x];
+                        S.rowdirty[threadIdx.x] = 0;
+                    }
+                    __syncthreads();
+                    int anyr = 0;
+#pragma unroll
+                    for (int k = 0; k < AROWS / 32; ++k) anyr |= S.rowsnap[k] != 0;
+                    if (anyr) {
+                        ++phases;
+                        for (int y = 1 + warp; y <= AROWS; y += NW) {
+                            if (!((S.rowsnap[(y - 1) >> 5] >> ((y - 1) & 31)) & 1)) continue;
+                            ++lines;
+                            const uint32_t chg = row_close(y);
+                            if (!__any_sync(FULL, chg != 0)) continue;
+                            // neighbours above / below the changed pixels that can still rise
+                            uint32_t cm = 0;  // bits: columns c0-1 .. c0+PXL (10)
+                            const int c0 = PXL * lane + 1;
+#pragma unroll
+                            for (int j = 0; j < PXL; ++j) {
+                                if (!((chg >> j) & 1)) continue;
+#pragma unroll
+                                for (int d = -1; d <= 1; ++d) {
+                                    const int c = c0 + j + d;
+                                    if (c < 1 || c > ACOLS) continue;
+                                    if ((y > 1 && improves(y, c0 + j, y - 1, c)) ||
+                                        (y < AROWS && improves(y, c0 + j, y + 1, c)))
+                                        cm |= 1u << (j + d + 1);
+                                }
+                            }
+                            if (cm) {
+                                for (int b = 0; b < PXL + 2; ++b)
+                                    if ((cm >> b) & 1) mark(S.coldirty, c0 - 1 + b - 1);
+                            }
+                            const unsigned lanes = __ballot_sync(FULL, chg != 0);
+                            if ((lane & 7) == 0 && ((lanes >> lane) & 0xffu)) {
+                                const int sx = lane >> 3, sy = (y - 1) >> 5;
+                                atomicOr(&S.subchg[sy * RX + sx], 1u << ((y - 1) & 31));
+                            }
+                        }
+                    }
+                    __syncthreads();
+                    // ---- column phase
+                    if (threadIdx.x < ACOLS / 32) {
+                        S.colsnap[threadIdx.x] = S.coldirty[threadIdx.x];
+                        S.coldirty[threadIdx.x] = 0;
+                    }
+                    __syncthreads();
+                    int anyc = 0;
+#pragma unroll
+                    for (int k = 0; k < ACOLS / 32; ++k) anyc |= S.colsnap[k] != 0;
+                    if (anyc) {
+                        ++phases;
+                        for (int c = 1 + warp; c <= ACOLS; c += NW) {
+                            if (!((S.colsnap[(c - 1) >> 5] >> ((c - 1) & 31)) & 1)) continue;
+                            ++lines;
+                            const uint32_t chg = col_close(c);
+                            if (!__any_sync(FULL, chg != 0)) continue;
+                            uint32_t rm = 0;  // bits: rows r0-1 .. r0+CPL (6)
+                            const int r0 = CPL * lane + 1;
+#pragma unroll
+                            for (int j = 0; j < CPL; ++j) {
+                                if (!((chg >> j) & 1)) continue;
+#pragma unroll
+                                for (int d = -1; d <= 1; ++d) {
+                                    const int rr = r0 + j + d;
+                                    if (rr < 1 || rr > AROWS) continue;
+                                    if ((c > 1 && improves(r0 + j, c, rr, c - 1)) ||
+                                        (c < ACOLS && improves(r0 + j, c, rr, c + 1)))
+                                        rm |= 1u << (j + d + 1);
+                                }
+                            }
+                            if (rm) {
+                                for (int b = 0; b < CPL + 2; ++b)
+                                    if ((rm >> b) & 1) mark(S.rowdirty, r0 - 1 + b - 1);
+                            }
+                            // sub-tile changed rows: lanes 8k..8k+7 hold rows of sub-tile row k
+                            const int sx = (c - 1) / SW;
+                            uint32_t mine = 0;
+#pragma unroll
+                            for (int j = 0; j < CPL; ++j)
+                                if ((chg >> j) & 1) mine |= 1u << ((r0 - 1 + j) & 31);
+#pragma unroll
+                            for (int k = 0; k < RY; ++k) {
+                                const uint32_t b = __reduce_or_sync(FULL, (lane >> 3) == k ? mine : 0u);
+                                if (lane == 0 && b) atomicOr(&S.subchg[k * RX + sx], b);
+                            }
+                        }
+                    }
+                    __syncthreads();
+                    int more = 0;
+#pragma unroll
+                    for (int k = 0; k < AROWS / 32; ++k) more |= S.rowdirty[k] != 0;
+                    if (!more) break;
+                }
+                if (threadIdx.x == 0) {
+                    atomicAdd(&wl.ctr[4], (unsigned long long)phases);
+                }
+                if (lane == 0) atomicAdd(&wl.ctr[6], (unsigned long long)lines);
+                // write back each sub-tile's changed rows and activate the neighbouring regions
+                // whose halo pixels those rows can improve (as k_region_mr8)
+                const int sx = warp % RX, sy = warp / RX;
+                const int wr0 = sy * kTile, wc0 = sx * SW;
+                const uint32_t mychg = S.subchg[warp];
+                if (mychg) {
+                    constexpr int WPR = SW / 4;
+                    for (int k = lane; k < kTile * WPR; k += 32) {
+                        int y = 1 + k / WPR, wi = k % WPR;
+                        if (!((mychg >> (y - 1)) & 1)) continue;
+                        int gx = X0 + wc0 + 4 * wi, gy = Y0 + wr0 + y - 1;
+                        if (gy >= h || gx >= w) continue;
+                        uint8_t* dst = R + (int64_t)gy * w + gx;
+                        uint32_t v = S.R[(wr0 + y) * RWW + sx * WPR + 1 + wi];
+                        if (gx + 3 < w && (((uintptr_t)dst) & 3) == 0) {
+                            __stcg(reinterpret_cast<unsigned int*>(dst), v);
+                        } else {
+                            for (int b = 0; b < 4 && gx + b < w; ++b)
+                                __stcg(reinterpret_cast<unsigned char*>(dst + b), (unsigned char)(v >> (8 * b)));
+                        }
+                    }
+                    __threadfence();
+                    uint32_t m8[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    const int r = wr0 + lane + 1;
+                    constexpr uint32_t TOP = 1u << 31, BOT = 1u;
+#pragma unroll
+                    for (int d = -1; d <= 1; ++d) {
+#pragma unroll
+                        for (int j = 0; j < PPL; ++j) {
+                            const int c = wc0 + PPL * lane + 1 + j;
+                            if (sy == 0 && improves(wr0 + 1, c, wr0, c + d)) {
+                                if (c + d == wc0) m8[0] |= TOP;
+                                else if (c + d == wc0 + SW + 1) m8[2] |= TOP;
+                                else m8[1] |= TOP;
+                            }
+                            if (sy == RY - 1 && improves(wr0 + kTile, c, wr0 + kTile + 1, c + d)) {
+                                if (c + d == wc0) m8[5] |= BOT;
+                                else if (c + d == wc0 + SW + 1) m8[7] |= BOT;
+                                else m8[6] |= BOT;
+                            }
+                        }
+                        if (sx == 0 && improves(r, wc0 + 1, r + d, wc0)) {
+                            if (r + d == wr0) m8[0] |= TOP;
+                            else if (r + d == wr0 + kTile + 1) m8[5] |= BOT;
+                            else m8[3] |= 1u << (lane + d);
+                        }
+                        if (sx == RX - 1 && improves(r, wc0 + SW, r + d, wc0 + SW + 1)) {
+                            if (r + d == wr0) m8[2] |= TOP;
+                            else if (r + d == wr0 + kTile + 1) m8[7] |= BOT;
+                            else m8[4] |= 1u << (lane + d);
+                        }
+                    }
+                    uint32_t mine = 0;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        uint32_t v = __reduce_or_sync(FULL, m8[j]);
+                        if (lane == j) mine = v;
+                    }
+                    if (lane < 8 && mine) {
+                        int gsx = rx * RX + sx + dx8(lane), gsy = ry * RY + sy + dy8(lane);
+                        int nrx = gsx >= 0 ? gsx / RX : -1, nry = gsy >= 0 ? gsy / RY : -1;
+                        if (gsx >= 0 && gsy >= 0 && nrx < wl.ntx && nry < wl.nty && (nrx != rx || nry != ry)) {
+                            int nt = nry * wl.ntx + nrx;
+                            int sub = (gsy % RY) * RX + (gsx % RX);
+                            atomicOr(&wl.inrows[nt * NW + sub], mine);
+                            q_activate(wl, nt);
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int again = 0;
+                uint32_t o = atomicCAS(&wl.state[t], ST_BUSY, ST_IDLE);
+                if (o == ST_BUSY) {
+                    atomicAdd(&wl.ctr[2], ~0ull);
+                } else {
+                    atomicExch(&wl.state[t], ST_BUSY);
+                    again = 1;
+                }
+                atomicAdd(&wl.ctr[3], 1ull);
+                if (!again) atomicAdd(&wl.ctr[5], gtimer() - S.t0);
+                S.again = again;
+            }
+            __syncthreads();
+            if (!S.again) break;
+        }
+    }
+}
+
 #if HP_RG_ORDER >= 2
 // Initial order by the regions' highest marker value (values flow down from the marker's
 // maxima, so regions holding high peaks go first): key per region = max of the marker.
@@ -1002,7 +1444,25 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
 #endif
     (note_launch(), k_rg_order<<<(n + 255) / 256, 256, 0, s>>>(wl, keys));
 #endif
-    static PerDevice once;
+    static const int adi_env = [] {  // HP_RG_ADI=0/1 overrides the compile-time default
+        const char* e = getenv("HP_RG_ADI");
+        return e ? atoi(e) : HP_RG_ADI;
+    }();
+    static PerDevice once, once_adi;
+    if (adi_env) {
+        const size_t smem_a = sizeof(SmemA);
+        once_adi.get([&] {
+            return (int)cudaFuncSetAttribute(k_region_adi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_a);
+        });
+        const int nsm = num_sms();
+        static const int grid_env_a = [] {
+            const char* e = getenv("HP_RG_GRID");
+            return e ? atoi(e) : 0;
+        }();
+        int b = std::max(1, std::min(grid_env_a > 0 ? grid_env_a : nsm * 3 / 4, n));
+        (note_launch(), k_region_adi<<<b, NW * 32, smem_a, s>>>(mask, R, w, h, wl));
+        return;
+    }
     const size_t smem = sizeof(Smem);
     const int blocks = once.get([&] {
         cudaFuncSetAttribute(k_region_mr8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1,7 +1,8 @@
 """Run-time variants of the S4 engine under the parity tests: the IWPP, reconstruction and
-whole-pipeline parity tests of test_gpu_parity.py re-run in a subprocess with
-HP_RG_INIT=1 (Vincent's raster / anti-raster initialisation per region before the queue
-engine, k_region.cu) and HP_RG_INIT=0, whichever is not the build's default."""
+whole-pipeline parity tests of test_gpu_parity.py re-run in a subprocess with each engine
+setting of k_region.cu: HP_RG_INIT (Vincent's raster / anti-raster initialisation per region
+before the queue engine) and HP_RG_ADI (alternating row / column phase closure of a region
+instead of asynchronous sub-tile sweeps), 0 and 1."""
 import os
 import subprocess
 import sys
@@ -13,12 +14,13 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("init", ["0", "1"])
-def test_s4_init_variant(init):
+@pytest.mark.parametrize("knob,val", [("HP_RG_INIT", "0"), ("HP_RG_INIT", "1"), ("HP_RG_ADI", "0"),
+                                      ("HP_RG_ADI", "1")])
+def test_s4_engine_variant(knob, val):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
-    env = dict(os.environ, HP_RG_INIT=init)
+    env = dict(os.environ, **{knob: val})
     sel = "iwpp or recon or pipeline_config1 or pipeline_random_small or pipeline_islands or hot_path_stages_random"
     r = subprocess.run([sys.executable, "-m", "pytest", "tests/test_gpu_parity.py", "-q", "-x", "-k", sel,
                         "-p", "no:cacheprovider"], cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
