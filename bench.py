@@ -309,22 +309,23 @@ def main():
     def process(tid, k):
         ctx.process_tile(k, dev[tid % B], lab[k], nob[k], tl[k], tf[k], tt[k], nr[k], stream=streams[k])
 
-    def step(key):
-        """One step: B tiles per GPU.  One GPU: all B in flight on the S slot streams.  N GPUs:
-        the N*B tiles of the step are pulled from the shared demand-driven tile queue
-         -- a slot takes the next tile id when its previous tile is done,
-        so a faster GPU takes more tiles; tile id t is pool tile t mod B (every rank holds
-        the pool in HBM)."""
+    def step(key, nsteps=1):
+        """nsteps steps of B tiles per GPU.  One GPU: all B tiles of a step in flight on the S
+        slot streams, steps queued back to back.  N GPUs: the N*B*nsteps tiles are pulled from
+        the shared demand-driven tile queue -- a slot takes the next tile id
+        when its previous tile is done, so a faster GPU takes more tiles, and no GPU idles at
+        a step boundary; tile id t is pool tile t mod B (every rank holds the pool in HBM)."""
         ev0 = torch.cuda.Event()
         ev0.record(main_s)
         for s in streams:
             s.wait_event(ev0)
         if world == 1:
-            for i in range(B):
-                process(i, i % S)
+            for _ in range(nsteps):
+                for i in range(B):
+                    process(i, i % S)
         else:
             from paper_1209_3332_b200.dist import TileQueue
-            q = TileQueue(world * B, block=2, key=key)
+            q = TileQueue(world * B * nsteps, block=2, key=key)
             ids, free, busy = iter(()), list(range(S)), {}
             drained = False
             while True:
@@ -364,8 +365,7 @@ def main():
 
     clocks = Clocks(local)
     clocks.start()  # before the warm-up: nvidia-smi takes a while to produce its first sample
-    for w in range(args.warmup):
-        step(f"hp/dev/w{w}")
+    step("hp/dev/warm", args.warmup)
     torch.cuda.synchronize()
     objs = sum(int(n.item()) for n in nr)
     taken[0] = 0
@@ -380,8 +380,7 @@ def main():
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks.mark_start()
     start.record(main_s)
-    for k in range(args.steps):
-        step(f"hp/dev/t{k}")
+    step("hp/dev/timed", args.steps)
     end.record(main_s)
     torch.cuda.synchronize()
     clocks.mark_end()
