@@ -69,6 +69,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HP_RG_ADI
 #define HP_RG_ADI 0  // alternating-direction (row / column phase) region closure instead of sub-tile sweeps
 #endif
+#ifndef HP_RG_THIN
+#define HP_RG_THIN 0  // jobs with at most this many dirty sub-tile rows use the alternating-phase closure
+#endif
 #ifndef HP_RG_INIT
 #define HP_RG_INIT 0  // raster + anti-raster initialisation sweep per region before the queue engine
 #endif
@@ -174,6 +177,299 @@ __device__ __forceinline__ uint32_t load_word(const uint8_t* plane, int w, int h
     return v;
 }
 
+// byte of window pixel (wr, wc): window column wc (0 .. RX*32+1) is byte wc + 3
+__device__ __forceinline__ int bidx(int wr, int wc) { return wr * RWB + wc + 3; }
+
+constexpr int PXL = RX * SW / 32;  // pixels per lane across a region row
+
+__device__ __forceinline__ void row_io_load(const uint8_t* __restrict__ p, int w, int h, int x0, int y, int* v) {
+#pragma unroll
+    for (int j = 0; j < PXL; ++j) v[j] = 0;
+    if (y < 0 || y >= h) return;
+    const uint8_t* rp = p + (int64_t)y * w;
+#pragma unroll
+    for (int j = 0; j < PXL; ++j)
+        if (x0 + j < w) v[j] = __ldcg(reinterpret_cast<const unsigned char*>(rp + x0 + j));
+}
+
+__device__ __forceinline__ int px_load(const uint8_t* __restrict__ p, int w, int h, int x, int y) {
+    return (x < 0 || y < 0 || x >= w || y >= h) ? 0 : (int)__ldcg(reinterpret_cast<const unsigned char*>(p + (int64_t)y * w + x));
+}
+
+// close one region row: lo[j] = min(m, max(r, nb)) then the horizontal clamp scans in both
+// directions (the region's left / right halo pixels as boundary inputs); returns the new row
+__device__ __forceinline__ void close_row(const int* m, const int* r, const int* nb, int lft, int rgt, int lane,
+                                          int* u) {
+    int lo[PXL];
+#pragma unroll
+    for (int j = 0; j < PXL; ++j) {
+        int b = max(r[j], nb[j]);
+        if (j == 0 && lane == 0) b = max(b, lft);
+        if (j == PXL - 1 && lane == 31) b = max(b, rgt);
+        lo[j] = min(b, m[j]);
+    }
+    int FL = lo[0], FH = m[0];
+#pragma unroll
+    for (int j = 1; j < PXL; ++j) {
+        FL = min(m[j], max(lo[j], FL));
+        FH = min(m[j], max(lo[j], FH));
+    }
+    int BL = lo[PXL - 1], BH = m[PXL - 1];
+#pragma unroll
+    for (int j = PXL - 2; j >= 0; --j) {
+        BL = min(m[j], max(lo[j], BL));
+        BH = min(m[j], max(lo[j], BH));
+    }
+    int in = __shfl_up_sync(FULL, clamp_scan<true>(FL, FH, lane), 1);
+    int ib = __shfl_down_sync(FULL, clamp_scan<false>(BL, BH, lane), 1);
+    if (lane == 0) in = 0;
+    if (lane == 31) ib = 0;
+    int fw[PXL];
+#pragma unroll
+    for (int j = 0; j < PXL; ++j) {
+        in = min(m[j], max(lo[j], in));
+        fw[j] = in;
+    }
+#pragma unroll
+    for (int j = PXL - 1; j >= 0; --j) {
+        ib = min(m[j], max(lo[j], ib));
+        u[j] = max(fw[j], ib);
+    }
+}
+
+// 3-wide max of a neighbouring row held in registers (xl / xr: the pixels just outside)
+__device__ __forceinline__ void max3_row(const int* v, int xl, int xr, int lane, int* out) {
+    int left = __shfl_up_sync(FULL, v[PXL - 1], 1), right = __shfl_down_sync(FULL, v[0], 1);
+    if (lane == 0) left = xl;
+    if (lane == 31) right = xr;
+#pragma unroll
+    for (int j = 0; j < PXL; ++j)
+        out[j] = max(v[j], max(j == 0 ? left : v[j - 1], j == PXL - 1 ? right : v[j + 1]));
+}
+
+constexpr int ACOLS = RX * SW;      // region columns (256)
+constexpr int AROWS = RY * kTile;   // region rows (128)
+constexpr int CPL = AROWS / 32;     // column pixels per lane (4)
+static_assert(PXL == 8 && CPL == 4, "ADI closure assumes 256 x 128 px regions");
+
+// close window row wr (1..AROWS) across the region; returns the lane's changed-pixel mask
+__device__ __forceinline__ uint32_t adi_row_close(const uint8_t* sR, uint8_t* sRw, const uint8_t* sM, int wr, int lane) {
+    const int c0 = PXL * lane + 1;
+    int m[PXL], r[PXL], nb[PXL], u[PXL];
+    int upv[PXL + 2], dnv[PXL + 2];
+#pragma unroll
+    for (int j = -1; j <= PXL; ++j) {
+        upv[j + 1] = sR[bidx(wr - 1, c0 + j)];
+        dnv[j + 1] = sR[bidx(wr + 1, c0 + j)];
+    }
+#pragma unroll
+    for (int j = 0; j < PXL; ++j) {
+        m[j] = sM[bidx(wr, c0 + j)];
+        r[j] = sR[bidx(wr, c0 + j)];
+        nb[j] = max(max(max(upv[j], upv[j + 1]), upv[j + 2]), max(max(dnv[j], dnv[j + 1]), dnv[j + 2]));
+    }
+    const int lft = sR[bidx(wr, c0 - 1)], rgt = sR[bidx(wr, c0 + PXL)];
+    bool can = false;
+#pragma unroll
+    for (int j = 0; j < PXL; ++j) {
+        const int hn = max(j == 0 ? lft : r[j - 1], j == PXL - 1 ? rgt : r[j + 1]);
+        can |= min(max(nb[j], hn), m[j]) > r[j];
+    }
+    if (!__any_sync(FULL, can)) return 0;
+    close_row(m, r, nb, lft, rgt, lane, u);
+    uint32_t chg = 0;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < PXL; ++j)
+        if (u[j] != r[j]) {
+            sRw[bidx(wr, c0 + j)] = (uint8_t)u[j];
+            chg |= 1u << j;
+        }
+    __syncwarp();
+    return chg;
+}
+// close window column wc (1..ACOLS) along the region; lane owns rows 4*lane+1 .. +4
+__device__ __forceinline__ uint32_t adi_col_close(const uint8_t* sR, uint8_t* sRw, const uint8_t* sM, int wc, int lane) {
+    const int r0 = CPL * lane + 1;
+    int m[CPL], r[CPL], nb[CPL], u[CPL];
+    int lv[CPL + 2], rv[CPL + 2];
+#pragma unroll
+    for (int j = -1; j <= CPL; ++j) {
+        lv[j + 1] = sR[bidx(r0 + j, wc - 1)];
+        rv[j + 1] = sR[bidx(r0 + j, wc + 1)];
+    }
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+        m[j] = sM[bidx(r0 + j, wc)];
+        r[j] = sR[bidx(r0 + j, wc)];
+        nb[j] = max(max(max(lv[j], lv[j + 1]), lv[j + 2]), max(max(rv[j], rv[j + 1]), rv[j + 2]));
+    }
+    const int top = sR[bidx(r0 - 1, wc)], bot = sR[bidx(r0 + CPL, wc)];
+    bool can = false;
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+        const int vn = max(j == 0 ? top : r[j - 1], j == CPL - 1 ? bot : r[j + 1]);
+        can |= min(max(nb[j], vn), m[j]) > r[j];
+    }
+    if (!__any_sync(FULL, can)) return 0;
+    int lo[CPL];
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+        int b = max(r[j], nb[j]);
+        if (j == 0 && lane == 0) b = max(b, top);
+        if (j == CPL - 1 && lane == 31) b = max(b, bot);
+        lo[j] = min(b, m[j]);
+    }
+    int FL = lo[0], FH = m[0];
+#pragma unroll
+    for (int j = 1; j < CPL; ++j) {
+        FL = min(m[j], max(lo[j], FL));
+        FH = min(m[j], max(lo[j], FH));
+    }
+    int BL = lo[CPL - 1], BH = m[CPL - 1];
+#pragma unroll
+    for (int j = CPL - 2; j >= 0; --j) {
+        BL = min(m[j], max(lo[j], BL));
+        BH = min(m[j], max(lo[j], BH));
+    }
+    int in = __shfl_up_sync(FULL, clamp_scan<true>(FL, FH, lane), 1);
+    int ib = __shfl_down_sync(FULL, clamp_scan<false>(BL, BH, lane), 1);
+    if (lane == 0) in = 0;
+    if (lane == 31) ib = 0;
+    int fw[CPL];
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+        in = min(m[j], max(lo[j], in));
+        fw[j] = in;
+    }
+#pragma unroll
+    for (int j = CPL - 1; j >= 0; --j) {
+        ib = min(m[j], max(lo[j], ib));
+        u[j] = max(fw[j], ib);
+    }
+    uint32_t chg = 0;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < CPL; ++j)
+        if (u[j] != r[j]) {
+            sRw[bidx(r0 + j, wc)] = (uint8_t)u[j];
+            chg |= 1u << j;
+        }
+    __syncwarp();
+    return chg;
+}
+
+// One region closure by alternating phases (see k_region_adi); S holds the window and the
+// rowdirty / coldirty / rowsnap / colsnap / subchg words (rowdirty seeded by the caller, the
+// rest zero).  On return S.subchg[k] = the rows of sub-tile k that changed.
+template <class SM>
+__device__ void adi_close_region(SM& S, const uint8_t* sR, uint8_t* sRw, const uint8_t* sM, int warp, int lane,
+                                 int& phases, int& lines) {
+    auto improves = [&](int pr, int pc, int qr, int qc) {
+        return min((int)sR[bidx(pr, pc)], (int)sM[bidx(qr, qc)]) > (int)sR[bidx(qr, qc)];
+    };
+    auto mark = [&](uint32_t* bits, int i) { atomicOr(&bits[i >> 5], 1u << (i & 31)); };
+    while (true) {
+        // ---- row phase
+        if (threadIdx.x < AROWS / 32) {
+            S.rowsnap[threadIdx.x] = S.rowdirty[threadIdx.x];
+            S.rowdirty[threadIdx.x] = 0;
+        }
+        __syncthreads();
+        int anyr = 0;
+#pragma unroll
+        for (int k = 0; k < AROWS / 32; ++k) anyr |= S.rowsnap[k] != 0;
+        if (anyr) {
+            ++phases;
+            for (int y = 1 + warp; y <= AROWS; y += NW) {
+                if (!((S.rowsnap[(y - 1) >> 5] >> ((y - 1) & 31)) & 1)) continue;
+                ++lines;
+                const uint32_t chg = adi_row_close(sR, sRw, sM, y, lane);
+                if (!__any_sync(FULL, chg != 0)) continue;
+                // neighbours above / below the changed pixels that can still rise
+                uint32_t cm = 0;  // bits: columns c0-1 .. c0+PXL (10)
+                const int c0 = PXL * lane + 1;
+#pragma unroll
+                for (int j = 0; j < PXL; ++j) {
+                    if (!((chg >> j) & 1)) continue;
+#pragma unroll
+                    for (int d = -1; d <= 1; ++d) {
+                        const int c = c0 + j + d;
+                        if (c < 1 || c > ACOLS) continue;
+                        if ((y > 1 && improves(y, c0 + j, y - 1, c)) ||
+                            (y < AROWS && improves(y, c0 + j, y + 1, c)))
+                            cm |= 1u << (j + d + 1);
+                    }
+                }
+                if (cm) {
+                    for (int b = 0; b < PXL + 2; ++b)
+                        if ((cm >> b) & 1) mark(S.coldirty, c0 - 1 + b - 1);
+                }
+                const unsigned lanes = __ballot_sync(FULL, chg != 0);
+                if ((lane & 7) == 0 && ((lanes >> lane) & 0xffu)) {
+                    const int sx = lane >> 3, sy = (y - 1) >> 5;
+                    atomicOr(&S.subchg[sy * RX + sx], 1u << ((y - 1) & 31));
+                }
+            }
+        }
+        __syncthreads();
+        // ---- column phase
+        if (threadIdx.x < ACOLS / 32) {
+            S.colsnap[threadIdx.x] = S.coldirty[threadIdx.x];
+            S.coldirty[threadIdx.x] = 0;
+        }
+        __syncthreads();
+        int anyc = 0;
+#pragma unroll
+        for (int k = 0; k < ACOLS / 32; ++k) anyc |= S.colsnap[k] != 0;
+        if (anyc) {
+            ++phases;
+            for (int c = 1 + warp; c <= ACOLS; c += NW) {
+                if (!((S.colsnap[(c - 1) >> 5] >> ((c - 1) & 31)) & 1)) continue;
+                ++lines;
+                const uint32_t chg = adi_col_close(sR, sRw, sM, c, lane);
+                if (!__any_sync(FULL, chg != 0)) continue;
+                uint32_t rm = 0;  // bits: rows r0-1 .. r0+CPL (6)
+                const int r0 = CPL * lane + 1;
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                    if (!((chg >> j) & 1)) continue;
+#pragma unroll
+                    for (int d = -1; d <= 1; ++d) {
+                        const int rr = r0 + j + d;
+                        if (rr < 1 || rr > AROWS) continue;
+                        if ((c > 1 && improves(r0 + j, c, rr, c - 1)) ||
+                            (c < ACOLS && improves(r0 + j, c, rr, c + 1)))
+                            rm |= 1u << (j + d + 1);
+                    }
+                }
+                if (rm) {
+                    for (int b = 0; b < CPL + 2; ++b)
+                        if ((rm >> b) & 1) mark(S.rowdirty, r0 - 1 + b - 1);
+                }
+                // sub-tile changed rows: lanes 8k..8k+7 hold rows of sub-tile row k
+                const int sx = (c - 1) / SW;
+                uint32_t mine = 0;
+#pragma unroll
+                for (int j = 0; j < CPL; ++j)
+                    if ((chg >> j) & 1) mine |= 1u << ((r0 - 1 + j) & 31);
+#pragma unroll
+                for (int k = 0; k < RY; ++k) {
+                    const uint32_t b = __reduce_or_sync(FULL, (lane >> 3) == k ? mine : 0u);
+                    if (lane == 0 && b) atomicOr(&S.subchg[k * RX + sx], b);
+                }
+            }
+        }
+        __syncthreads();
+        // every thread reads rowdirty BEFORE the barrier, so the reset at the next row phase
+        // cannot race with a slower warp's read
+        int pend = 0;
+#pragma unroll
+        for (int k = 0; k < AROWS / 32; ++k) pend |= S.rowdirty[k] != 0;
+        if (!__syncthreads_or(pend)) break;
+    }
+}
+
 struct Smem {
     uint32_t R[ROWS * RWW];
     uint32_t M[ROWS * RWW];
@@ -184,6 +480,9 @@ struct Smem {
     int again;
     unsigned long long t0, tA, tB;
     int first;  // HP_RG_FIRSTORDER: this job is the region's first
+    int thin;   // HP_RG_THIN: this job's few dirty rows go to the alternating-phase closure
+    uint32_t rowdirty[AROWS / 32], coldirty[ACOLS / 32], rowsnap[AROWS / 32], colsnap[ACOLS / 32];
+    uint32_t subchg[NW];
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -192,12 +491,10 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-// byte of window pixel (wr, wc): window column wc (0 .. RX*32+1) is byte wc + 3
-__device__ __forceinline__ int bidx(int wr, int wc) { return wr * RWB + wc + 3; }
 
 __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_t* __restrict__ mask,
                                                            uint8_t* __restrict__ R, int w, int h,
-                                                           Worklist wl) {
+                                                           Worklist wl, int thin_rows) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
     const uint8_t* sR = reinterpret_cast<const uint8_t*>(S.R);
@@ -446,9 +743,13 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                     if (first)
                         for (int k = RX; k < NW; ++k) S.dirty[k] = 0;
 #endif
-                    int np = 0;
-                    for (int k = 0; k < NW; ++k) np += S.dirty[k] != 0;
+                    int np = 0, nbits = 0;
+                    for (int k = 0; k < NW; ++k) {
+                        np += S.dirty[k] != 0;
+                        nbits += __popc(S.dirty[k]);
+                    }
                     S.pend = np;
+                    S.thin = nbits <= thin_rows;
 #if HP_RG_PROFILE
                     S.tA = gtimer();
 #endif
@@ -466,7 +767,19 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                 int nrows = 0;
                 const int r = wr0 + lane + 1;
                 unsigned backoff = HP_POLL_NS;
-                while (true) {
+                if (S.thin) {
+                    // a thin job (a few dirty rows, e.g. a wave front crossing the region
+                    // along a corridor): alternating full-width row / full-height column
+                    // closures instead of the sub-tile sweeps
+                    if (threadIdx.x < AROWS / 32) S.rowdirty[threadIdx.x] = 0;
+                    if (threadIdx.x < ACOLS / 32) S.coldirty[threadIdx.x] = 0;
+                    if (lane == 0) S.subchg[warp] = 0;
+                    __syncthreads();
+                    if (lane == 0 && S.dirty[warp]) atomicOr(&S.rowdirty[warp / RX], S.dirty[warp]);
+                    __syncthreads();
+                    adi_close_region(S, sR, sRw, sM, warp, lane, iters, nrows);
+                    mychg = S.subchg[warp];
+                } else while (true) {
                     uint32_t dirty = 0;
                     if (lane == 0 && *reinterpret_cast<volatile uint32_t*>(&S.dirty[warp]))
                         dirty = atomicExch(&S.dirty[warp], 0u);
@@ -731,73 +1044,6 @@ __global__ void k_rg_reset(Worklist wl, bool seeded) {
 // update is a monotone step toward the reconstruction, so the queue engine that follows
 // reaches the same fixed point; it is seeded with exactly the sub-tile rows that still hold
 // an improvable pixel (k_rg_seed), instead of every row of every region.
-constexpr int PXL = RX * SW / 32;  // pixels per lane across a region row
-
-__device__ __forceinline__ void row_io_load(const uint8_t* __restrict__ p, int w, int h, int x0, int y, int* v) {
-#pragma unroll
-    for (int j = 0; j < PXL; ++j) v[j] = 0;
-    if (y < 0 || y >= h) return;
-    const uint8_t* rp = p + (int64_t)y * w;
-#pragma unroll
-    for (int j = 0; j < PXL; ++j)
-        if (x0 + j < w) v[j] = __ldcg(reinterpret_cast<const unsigned char*>(rp + x0 + j));
-}
-
-__device__ __forceinline__ int px_load(const uint8_t* __restrict__ p, int w, int h, int x, int y) {
-    return (x < 0 || y < 0 || x >= w || y >= h) ? 0 : (int)__ldcg(reinterpret_cast<const unsigned char*>(p + (int64_t)y * w + x));
-}
-
-// close one region row: lo[j] = min(m, max(r, nb)) then the horizontal clamp scans in both
-// directions (the region's left / right halo pixels as boundary inputs); returns the new row
-__device__ __forceinline__ void close_row(const int* m, const int* r, const int* nb, int lft, int rgt, int lane,
-                                          int* u) {
-    int lo[PXL];
-#pragma unroll
-    for (int j = 0; j < PXL; ++j) {
-        int b = max(r[j], nb[j]);
-        if (j == 0 && lane == 0) b = max(b, lft);
-        if (j == PXL - 1 && lane == 31) b = max(b, rgt);
-        lo[j] = min(b, m[j]);
-    }
-    int FL = lo[0], FH = m[0];
-#pragma unroll
-    for (int j = 1; j < PXL; ++j) {
-        FL = min(m[j], max(lo[j], FL));
-        FH = min(m[j], max(lo[j], FH));
-    }
-    int BL = lo[PXL - 1], BH = m[PXL - 1];
-#pragma unroll
-    for (int j = PXL - 2; j >= 0; --j) {
-        BL = min(m[j], max(lo[j], BL));
-        BH = min(m[j], max(lo[j], BH));
-    }
-    int in = __shfl_up_sync(FULL, clamp_scan<true>(FL, FH, lane), 1);
-    int ib = __shfl_down_sync(FULL, clamp_scan<false>(BL, BH, lane), 1);
-    if (lane == 0) in = 0;
-    if (lane == 31) ib = 0;
-    int fw[PXL];
-#pragma unroll
-    for (int j = 0; j < PXL; ++j) {
-        in = min(m[j], max(lo[j], in));
-        fw[j] = in;
-    }
-#pragma unroll
-    for (int j = PXL - 1; j >= 0; --j) {
-        ib = min(m[j], max(lo[j], ib));
-        u[j] = max(fw[j], ib);
-    }
-}
-
-// 3-wide max of a neighbouring row held in registers (xl / xr: the pixels just outside)
-__device__ __forceinline__ void max3_row(const int* v, int xl, int xr, int lane, int* out) {
-    int left = __shfl_up_sync(FULL, v[PXL - 1], 1), right = __shfl_down_sync(FULL, v[0], 1);
-    if (lane == 0) left = xl;
-    if (lane == 31) right = xr;
-#pragma unroll
-    for (int j = 0; j < PXL; ++j)
-        out[j] = max(v[j], max(j == 0 ? left : v[j - 1], j == PXL - 1 ? right : v[j + 1]));
-}
-
 __global__ void __launch_bounds__(128) k_rg_init(const uint8_t* __restrict__ mask, uint8_t* __restrict__ R, int w,
                                                  int h, int ntx, int nty) {
     const int lane = threadIdx.x & 31;
@@ -897,11 +1143,6 @@ __global__ void __launch_bounds__(256) k_rg_seed(const uint8_t* __restrict__ mas
 // it can still improve (min(R(p), M(q)) > R(q)), so a horizontal run closes in one row step
 // and a vertical run in one column step -- a 1-px corridor crosses a region in one phase per
 // turn instead of one dependent row closure per row.  Monotone updates: same fixed point.
-constexpr int ACOLS = RX * SW;      // region columns (256)
-constexpr int AROWS = RY * kTile;   // region rows (128)
-constexpr int CPL = AROWS / 32;     // column pixels per lane (4)
-static_assert(PXL == 8 && CPL == 4, "ADI closure assumes 256 x 128 px regions");
-
 struct SmemA {
     uint32_t R[ROWS * RWW];
     uint32_t M[ROWS * RWW];
@@ -928,115 +1169,6 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_adi(const uint8_
     auto improves = [&](int pr, int pc, int qr, int qc) {
         return min((int)sR[bidx(pr, pc)], (int)sM[bidx(qr, qc)]) > (int)sR[bidx(qr, qc)];
     };
-    auto mark = [&](uint32_t* bits, int i) { atomicOr(&bits[i >> 5], 1u << (i & 31)); };
-
-    // close window row wr (1..AROWS) across the region; returns the lane's changed-pixel mask
-    auto row_close = [&](int wr) -> uint32_t {
-        const int c0 = PXL * lane + 1;
-        int m[PXL], r[PXL], nb[PXL], u[PXL];
-        int upv[PXL + 2], dnv[PXL + 2];
-#pragma unroll
-        for (int j = -1; j <= PXL; ++j) {
-            upv[j + 1] = sR[bidx(wr - 1, c0 + j)];
-            dnv[j + 1] = sR[bidx(wr + 1, c0 + j)];
-        }
-#pragma unroll
-        for (int j = 0; j < PXL; ++j) {
-            m[j] = sM[bidx(wr, c0 + j)];
-            r[j] = sR[bidx(wr, c0 + j)];
-            nb[j] = max(max(max(upv[j], upv[j + 1]), upv[j + 2]), max(max(dnv[j], dnv[j + 1]), dnv[j + 2]));
-        }
-        const int lft = sR[bidx(wr, c0 - 1)], rgt = sR[bidx(wr, c0 + PXL)];
-        bool can = false;
-#pragma unroll
-        for (int j = 0; j < PXL; ++j) {
-            const int hn = max(j == 0 ? lft : r[j - 1], j == PXL - 1 ? rgt : r[j + 1]);
-            can |= min(max(nb[j], hn), m[j]) > r[j];
-        }
-        if (!__any_sync(FULL, can)) return 0;
-        close_row(m, r, nb, lft, rgt, lane, u);
-        uint32_t chg = 0;
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < PXL; ++j)
-            if (u[j] != r[j]) {
-                sRw[bidx(wr, c0 + j)] = (uint8_t)u[j];
-                chg |= 1u << j;
-            }
-        __syncwarp();
-        return chg;
-    };
-    // close window column wc (1..ACOLS) along the region; lane owns rows 4*lane+1 .. +4
-    auto col_close = [&](int wc) -> uint32_t {
-        const int r0 = CPL * lane + 1;
-        int m[CPL], r[CPL], nb[CPL], u[CPL];
-        int lv[CPL + 2], rv[CPL + 2];
-#pragma unroll
-        for (int j = -1; j <= CPL; ++j) {
-            lv[j + 1] = sR[bidx(r0 + j, wc - 1)];
-            rv[j + 1] = sR[bidx(r0 + j, wc + 1)];
-        }
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) {
-            m[j] = sM[bidx(r0 + j, wc)];
-            r[j] = sR[bidx(r0 + j, wc)];
-            nb[j] = max(max(max(lv[j], lv[j + 1]), lv[j + 2]), max(max(rv[j], rv[j + 1]), rv[j + 2]));
-        }
-        const int top = sR[bidx(r0 - 1, wc)], bot = sR[bidx(r0 + CPL, wc)];
-        bool can = false;
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) {
-            const int vn = max(j == 0 ? top : r[j - 1], j == CPL - 1 ? bot : r[j + 1]);
-            can |= min(max(nb[j], vn), m[j]) > r[j];
-        }
-        if (!__any_sync(FULL, can)) return 0;
-        int lo[CPL];
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) {
-            int b = max(r[j], nb[j]);
-            if (j == 0 && lane == 0) b = max(b, top);
-            if (j == CPL - 1 && lane == 31) b = max(b, bot);
-            lo[j] = min(b, m[j]);
-        }
-        int FL = lo[0], FH = m[0];
-#pragma unroll
-        for (int j = 1; j < CPL; ++j) {
-            FL = min(m[j], max(lo[j], FL));
-            FH = min(m[j], max(lo[j], FH));
-        }
-        int BL = lo[CPL - 1], BH = m[CPL - 1];
-#pragma unroll
-        for (int j = CPL - 2; j >= 0; --j) {
-            BL = min(m[j], max(lo[j], BL));
-            BH = min(m[j], max(lo[j], BH));
-        }
-        int in = __shfl_up_sync(FULL, clamp_scan<true>(FL, FH, lane), 1);
-        int ib = __shfl_down_sync(FULL, clamp_scan<false>(BL, BH, lane), 1);
-        if (lane == 0) in = 0;
-        if (lane == 31) ib = 0;
-        int fw[CPL];
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) {
-            in = min(m[j], max(lo[j], in));
-            fw[j] = in;
-        }
-#pragma unroll
-        for (int j = CPL - 1; j >= 0; --j) {
-            ib = min(m[j], max(lo[j], ib));
-            u[j] = max(fw[j], ib);
-        }
-        uint32_t chg = 0;
-        __syncwarp();
-#pragma unroll
-        for (int j = 0; j < CPL; ++j)
-            if (u[j] != r[j]) {
-                sRw[bidx(r0 + j, wc)] = (uint8_t)u[j];
-                chg |= 1u << j;
-            }
-        __syncwarp();
-        return chg;
-    };
-
     while (true) {
         if (threadIdx.x == 0) {
             int t = -1;
@@ -1134,103 +1266,7 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_adi(const uint8_
                 }
                 __syncthreads();
                 int phases = 0, lines = 0;
-                while (true) {
-                    // ---- row phase
-                    if (threadIdx.x < AROWS / 32) {
-                        S.rowsnap[threadIdx.x] = S.rowdirty[threadIdx.x];
-                        S.rowdirty[threadIdx.x] = 0;
-                    }
-                    __syncthreads();
-                    int anyr = 0;
-#pragma unroll
-                    for (int k = 0; k < AROWS / 32; ++k) anyr |= S.rowsnap[k] != 0;
-                    if (anyr) {
-                        ++phases;
-                        for (int y = 1 + warp; y <= AROWS; y += NW) {
-                            if (!((S.rowsnap[(y - 1) >> 5] >> ((y - 1) & 31)) & 1)) continue;
-                            ++lines;
-                            const uint32_t chg = row_close(y);
-                            if (!__any_sync(FULL, chg != 0)) continue;
-                            // neighbours above / below the changed pixels that can still rise
-                            uint32_t cm = 0;  // bits: columns c0-1 .. c0+PXL (10)
-                            const int c0 = PXL * lane + 1;
-#pragma unroll
-                            for (int j = 0; j < PXL; ++j) {
-                                if (!((chg >> j) & 1)) continue;
-#pragma unroll
-                                for (int d = -1; d <= 1; ++d) {
-                                    const int c = c0 + j + d;
-                                    if (c < 1 || c > ACOLS) continue;
-                                    if ((y > 1 && improves(y, c0 + j, y - 1, c)) ||
-                                        (y < AROWS && improves(y, c0 + j, y + 1, c)))
-                                        cm |= 1u << (j + d + 1);
-                                }
-                            }
-                            if (cm) {
-                                for (int b = 0; b < PXL + 2; ++b)
-                                    if ((cm >> b) & 1) mark(S.coldirty, c0 - 1 + b - 1);
-                            }
-                            const unsigned lanes = __ballot_sync(FULL, chg != 0);
-                            if ((lane & 7) == 0 && ((lanes >> lane) & 0xffu)) {
-                                const int sx = lane >> 3, sy = (y - 1) >> 5;
-                                atomicOr(&S.subchg[sy * RX + sx], 1u << ((y - 1) & 31));
-                            }
-                        }
-                    }
-                    __syncthreads();
-                    // ---- column phase
-                    if (threadIdx.x < ACOLS / 32) {
-                        S.colsnap[threadIdx.x] = S.coldirty[threadIdx.x];
-                        S.coldirty[threadIdx.x] = 0;
-                    }
-                    __syncthreads();
-                    int anyc = 0;
-#pragma unroll
-                    for (int k = 0; k < ACOLS / 32; ++k) anyc |= S.colsnap[k] != 0;
-                    if (anyc) {
-                        ++phases;
-                        for (int c = 1 + warp; c <= ACOLS; c += NW) {
-                            if (!((S.colsnap[(c - 1) >> 5] >> ((c - 1) & 31)) & 1)) continue;
-                            ++lines;
-                            const uint32_t chg = col_close(c);
-                            if (!__any_sync(FULL, chg != 0)) continue;
-                            uint32_t rm = 0;  // bits: rows r0-1 .. r0+CPL (6)
-                            const int r0 = CPL * lane + 1;
-#pragma unroll
-                            for (int j = 0; j < CPL; ++j) {
-                                if (!((chg >> j) & 1)) continue;
-#pragma unroll
-                                for (int d = -1; d <= 1; ++d) {
-                                    const int rr = r0 + j + d;
-                                    if (rr < 1 || rr > AROWS) continue;
-                                    if ((c > 1 && improves(r0 + j, c, rr, c - 1)) ||
-                                        (c < ACOLS && improves(r0 + j, c, rr, c + 1)))
-                                        rm |= 1u << (j + d + 1);
-                                }
-                            }
-                            if (rm) {
-                                for (int b = 0; b < CPL + 2; ++b)
-                                    if ((rm >> b) & 1) mark(S.rowdirty, r0 - 1 + b - 1);
-                            }
-                            // sub-tile changed rows: lanes 8k..8k+7 hold rows of sub-tile row k
-                            const int sx = (c - 1) / SW;
-                            uint32_t mine = 0;
-#pragma unroll
-                            for (int j = 0; j < CPL; ++j)
-                                if ((chg >> j) & 1) mine |= 1u << ((r0 - 1 + j) & 31);
-#pragma unroll
-                            for (int k = 0; k < RY; ++k) {
-                                const uint32_t b = __reduce_or_sync(FULL, (lane >> 3) == k ? mine : 0u);
-                                if (lane == 0 && b) atomicOr(&S.subchg[k * RX + sx], b);
-                            }
-                        }
-                    }
-                    __syncthreads();
-                    int more = 0;
-#pragma unroll
-                    for (int k = 0; k < AROWS / 32; ++k) more |= S.rowdirty[k] != 0;
-                    if (!more) break;
-                }
+                adi_close_region(S, sR, sRw, sM, warp, lane, phases, lines);
                 if (threadIdx.x == 0) {
                     atomicAdd(&wl.ctr[4], (unsigned long long)phases);
                 }
@@ -1444,6 +1480,10 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
 #endif
     (note_launch(), k_rg_order<<<(n + 255) / 256, 256, 0, s>>>(wl, keys));
 #endif
+    static const int thin_env = [] {  // HP_RG_THIN=k overrides the compile-time default
+        const char* e = getenv("HP_RG_THIN");
+        return e ? atoi(e) : HP_RG_THIN;
+    }();
     static const int adi_env = [] {  // HP_RG_ADI=0/1 overrides the compile-time default
         const char* e = getenv("HP_RG_ADI");
         return e ? atoi(e) : HP_RG_ADI;
@@ -1487,7 +1527,7 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
         return e ? atoi(e) : 0;
     }();
     if (grid_env > 0) b = std::max(1, std::min(grid_env, n));
-    (note_launch(), k_region_mr8<<<b, NW * 32, smem, s>>>(mask, R, w, h, wl));
+    (note_launch(), k_region_mr8<<<b, NW * 32, smem, s>>>(mask, R, w, h, wl, thin_env));
 }
 
 void launch_recon_u8_auto(const uint8_t* mask, uint8_t* R, int w, int h, const Worklist& wl,

@@ -1,8 +1,9 @@
 """Run-time variants of the S4 engine under the parity tests: the IWPP, reconstruction and
 whole-pipeline parity tests of test_gpu_parity.py re-run in a subprocess with each engine
 setting of k_region.cu: HP_RG_INIT (Vincent's raster / anti-raster initialisation per region
-before the queue engine) and HP_RG_ADI (alternating row / column phase closure of a region
-instead of asynchronous sub-tile sweeps), 0 and 1."""
+before the queue engine), HP_RG_ADI (alternating row / column phase closure of a region
+instead of asynchronous sub-tile sweeps) and HP_RG_THIN (that closure only for jobs with at most
+k dirty sub-tile rows; 4096 = every job)."""
 import os
 import subprocess
 import sys
@@ -15,7 +16,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("knob,val", [("HP_RG_INIT", "0"), ("HP_RG_INIT", "1"), ("HP_RG_ADI", "0"),
-                                      ("HP_RG_ADI", "1")])
+                                      ("HP_RG_ADI", "1"), ("HP_RG_THIN", "0"), ("HP_RG_THIN", "8"),
+                                      ("HP_RG_THIN", "4096")])
 def test_s4_engine_variant(knob, val):
     import torch
     if not torch.cuda.is_available():
