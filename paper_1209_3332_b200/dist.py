@@ -207,16 +207,20 @@ class RowArena:
         return DeviceRows(self.tile[:n], self.label[:n], self.flags[:n], self.feat[:n])
 
 
-def gather_rows_device(rows: DeviceRows, device=None):
+def gather_rows_device(rows: DeviceRows, device=None, stats: dict | None = None):
     """The end-of-run gather: every rank's device-resident rows go to rank 0
     only, device to device (NCCL point-to-point over NVLink on GPUs; gloo on CPU) -- no host
     round trip and no all-gather to every rank.  Rank 0 returns the merged table in
     (tile, label) order as DeviceRows, the other ranks None.  Each tile's rows are one
     contiguous run in label order on one rank (hp_run_tiles delivers a tile's rows at once),
-    so a stable sort by tile id gives the canonical order for any number of GPUs."""
+    so a stable sort by tile id gives the canonical order for any number of GPUs.  With
+    ``stats`` (a dict) the transfer and the merge are timed separately (synchronising)."""
+    import time
+
     import torch
     import torch.distributed as dist
     dev = device if device is not None else rows.tile.device
+    t0 = time.perf_counter()
     if not dist.is_initialized() or dist.get_world_size() == 1:
         parts = [rows]
     else:
@@ -244,10 +248,19 @@ def gather_rows_device(rows: DeviceRows, device=None):
             parts.append(part)
         for w in (dist.batch_isend_irecv(ops) if ops else []):
             w.wait()
+    if stats is not None:
+        torch.cuda.synchronize(dev) if torch.device(dev).type == "cuda" else None
+        stats["transfer_s"] = time.perf_counter() - t0
+        stats["received_bytes"] = sum(len(p) for p in parts[1:]) * ROW_BYTES
+    t1 = time.perf_counter()
     tile = torch.cat([p.tile for p in parts])
     order = torch.argsort(tile, stable=True)
-    return DeviceRows(tile[order], torch.cat([p.label for p in parts])[order],
-                      torch.cat([p.flags for p in parts])[order], torch.cat([p.feat for p in parts])[order])
+    out = DeviceRows(tile[order], torch.cat([p.label for p in parts])[order],
+                     torch.cat([p.flags for p in parts])[order], torch.cat([p.feat for p in parts])[order])
+    if stats is not None:
+        torch.cuda.synchronize(dev) if torch.device(dev).type == "cuda" else None
+        stats["merge_s"] = time.perf_counter() - t1
+    return out
 
 
 def sort_rows(rows: DeviceRows) -> DeviceRows:

@@ -163,7 +163,8 @@ def main():
         torch.cuda.synchronize()
         dist.barrier()
     tg = time.perf_counter()
-    table = gather_rows_device(mine_rows)
+    gstats = {}
+    table = gather_rows_device(mine_rows, stats=gstats)
     torch.cuda.synchronize()
     t_gather = time.perf_counter() - tg
     # per-slide aggregation on each rank's own rows, two NCCL all-reduces
@@ -190,6 +191,9 @@ def main():
                 "host_bytes_per_tile": pool_bytes / P,
                 "tiles_per_s": n_tiles / float(tt[0]), "run_s": float(tt[0]), "gather_s": float(tt[1]),
                 "gather_GBps": gathered_bytes / float(tt[1]) / 1e9 if float(tt[1]) > 0 else None,
+                "gather_transfer_s": gstats.get("transfer_s"), "gather_merge_s": gstats.get("merge_s"),
+                "gather_transfer_GBps": (gathered_bytes / gstats["transfer_s"] / 1e9
+                                         if gstats.get("transfer_s") else None),
                 "rows": int(len(table)), "rows_rank0": n_mine, "tiles_taken_total": int(nb[2]),
                 "failed_tiles": int(nb[0]), "digest": h.hexdigest()[:16], "pool_gen_s": round(gen_s, 1),
                 "groups": n_groups, "group_rows": int(cnt.sum()), "agg_ms": round(agg_ms, 1),
