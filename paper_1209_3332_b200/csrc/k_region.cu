@@ -72,6 +72,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef HP_RG_THIN
 #define HP_RG_THIN 0  // jobs with at most this many dirty sub-tile rows use the alternating-phase closure
 #endif
+#ifndef HP_RG_CHAIN
+#define HP_RG_CHAIN 0  // ... and only from a region's HP_RG_CHAIN-th job on (a long chain)
+#endif
 #ifndef HP_RG_INIT
 #define HP_RG_INIT 0  // raster + anti-raster initialisation sweep per region before the queue engine
 #endif
@@ -481,6 +484,7 @@ struct Smem {
     unsigned long long t0, tA, tB;
     int first;  // HP_RG_FIRSTORDER: this job is the region's first
     int thin;   // HP_RG_THIN: this job's few dirty rows go to the alternating-phase closure
+    int visits; // earlier jobs of this region in this launch
     uint32_t rowdirty[AROWS / 32], coldirty[ACOLS / 32], rowsnap[AROWS / 32], colsnap[ACOLS / 32];
     uint32_t subchg[NW];
 };
@@ -494,7 +498,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_t* __restrict__ mask,
                                                            uint8_t* __restrict__ R, int w, int h,
-                                                           Worklist wl, int thin_rows) {
+                                                           Worklist wl, int thin_rows, int chain_visits) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& S = *reinterpret_cast<Smem*>(smem_raw);
     const uint8_t* sR = reinterpret_cast<const uint8_t*>(S.R);
@@ -655,6 +659,9 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                 t = q_pop(wl);
                 if (t >= 0) atomicExch(&wl.state[t], ST_BUSY);
             }
+            // region visit count (state words past the regions and their order keys): a
+            // region popped again and again lies on a long propagation chain
+            S.visits = t >= 0 ? (int)atomicAdd(&wl.state[2 * wl.ntx * wl.nty + t], 1u) : 0;
             S.t0 = gtimer();
             S.job = t;
         }
@@ -749,7 +756,7 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                         nbits += __popc(S.dirty[k]);
                     }
                     S.pend = np;
-                    S.thin = nbits <= thin_rows;
+                    S.thin = nbits <= thin_rows && S.visits >= chain_visits;
 #if HP_RG_PROFILE
                     S.tA = gtimer();
 #endif
@@ -1010,6 +1017,7 @@ __global__ void k_rg_reset(Worklist wl, bool seeded) {
     const int lim = max(wl.cap, n * NW);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < lim; i += gridDim.x * blockDim.x) {
         if (i < n) wl.state[i] = ST_QUEUED;
+        if (i < n) wl.state[2 * n + i] = 0u;  // visit counts (k_region_mr8)
         if (i < n * NW && !seeded) wl.inrows[i] = 0xffffffffu;
         if (i < wl.cap) {
             int32_t v = EMPTY;
@@ -1155,6 +1163,7 @@ struct SmemA {
     int any;
     int job;
     int again;
+    int visits;
     unsigned long long t0;
 };
 
@@ -1183,6 +1192,9 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_adi(const uint8_
                 t = q_pop(wl);
                 if (t >= 0) atomicExch(&wl.state[t], ST_BUSY);
             }
+            // region visit count (state words past the regions and their order keys): a
+            // region popped again and again lies on a long propagation chain
+            S.visits = t >= 0 ? (int)atomicAdd(&wl.state[2 * wl.ntx * wl.nty + t], 1u) : 0;
             S.t0 = gtimer();
             S.job = t;
         }
@@ -1484,6 +1496,10 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
         const char* e = getenv("HP_RG_THIN");
         return e ? atoi(e) : HP_RG_THIN;
     }();
+    static const int chain_env = [] {  // HP_RG_CHAIN=v overrides the compile-time default
+        const char* e = getenv("HP_RG_CHAIN");
+        return e ? atoi(e) : HP_RG_CHAIN;
+    }();
     static const int adi_env = [] {  // HP_RG_ADI=0/1 overrides the compile-time default
         const char* e = getenv("HP_RG_ADI");
         return e ? atoi(e) : HP_RG_ADI;
@@ -1527,7 +1543,7 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
         return e ? atoi(e) : 0;
     }();
     if (grid_env > 0) b = std::max(1, std::min(grid_env, n));
-    (note_launch(), k_region_mr8<<<b, NW * 32, smem, s>>>(mask, R, w, h, wl, thin_env));
+    (note_launch(), k_region_mr8<<<b, NW * 32, smem, s>>>(mask, R, w, h, wl, thin_env, chain_env));
 }
 
 void launch_recon_u8_auto(const uint8_t* mask, uint8_t* R, int w, int h, const Worklist& wl,
