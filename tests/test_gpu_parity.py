@@ -78,9 +78,9 @@ def test_recon(ctx, chain):
 
 
 @pytest.mark.parametrize("kind", ["uniform", "blobs", "ramp"])
-def test_recon_cand_clipped(ctx, kind):
-    # the pipeline's S4 computes cand through recon(max(open,K), max(g,K)); check it against
-    # the oracle's plain recon + threshold on inputs with very different K
+def test_recon_cand_random_planes(ctx, kind):
+    # S4 on planes unlike the tiles (uniform noise, bright blobs, ramps with noise); check it against
+    # the oracle's plain recon + threshold
     rng = np.random.default_rng({"uniform": 1, "blobs": 2, "ramp": 3}[kind])
     h, w = 300, 400
     if kind == "uniform":
