@@ -2,7 +2,7 @@
 # r02f: BASELINE configs[3] (config 4) at full size, 36,848 tiles demand-driven over 1 / 2 / 4
 # GPUs, raw RGB and JPEG ingest, rows in device arenas, device-to-device gather to rank 0;
 # then bench.py at 2 and 4 GPUs.
-O=gpurun_out/r02f; mkdir -p $O
+O=${OUT:-gpurun_out/r02f}; mkdir -p $O
 export CUDA_DEVICE_MAX_CONNECTIONS=32
 nvidia-smi -L > $O/gpus.txt
 port=29600
