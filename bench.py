@@ -320,9 +320,12 @@ def main():
         for s in streams:
             s.wait_event(ev0)
         if world == 1:
-            for _ in range(nsteps):
+            # steps are not joined: each slot stream runs its tiles back to back, and tile i of
+            # step k goes to slot (i + k) mod S, so the chain-bound tiles (3 of the 12 take
+            # 3-6x longer) rotate over the slots instead of piling up on three streams
+            for k in range(nsteps):
                 for i in range(B):
-                    process(i, i % S)
+                    process(i, (i + k) % S)
         else:
             from paper_1209_3332_b200.dist import TileQueue
             q = TileQueue(world * B * nsteps, block=2, key=key)
