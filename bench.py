@@ -233,6 +233,9 @@ def main():
     ap.add_argument("--e2e-slots", type=int, default=14, help="context slots used by hp_run_tiles (e2e)")
     ap.add_argument("--size", type=int, default=4096)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--schedule", default="rotate", choices=["rotate", "join", "fixed"],
+                    help="one GPU: steps unjoined with tiles rotating over slots (default), every step "
+                         "joined (r1), or unjoined with fixed slots")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
@@ -324,8 +327,17 @@ def main():
             # step k goes to slot (i + k) mod S, so the chain-bound tiles (3 of the 12 take
             # 3-6x longer) rotate over the slots instead of piling up on three streams
             for k in range(nsteps):
+                if args.schedule == "join" and k:  # r1 schedule: every step joined, fixed slots
+                    e = torch.cuda.Event()
+                    for st in streams:
+                        e2 = torch.cuda.Event()
+                        e2.record(st)
+                        main_s.wait_event(e2)
+                    e.record(main_s)
+                    for st in streams:
+                        st.wait_event(e)
                 for i in range(B):
-                    process(i, (i + k) % S)
+                    process(i, (i + k) % S if args.schedule == "rotate" else i % S)
         else:
             from paper_1209_3332_b200.dist import TileQueue
             q = TileQueue(world * B * nsteps, block=2, key=key)

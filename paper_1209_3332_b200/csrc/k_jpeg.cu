@@ -226,16 +226,8 @@ __global__ void __launch_bounds__(256) k_rst_write(const JpegHdr* __restrict__ H
 }
 
 // --- Huffman decoding (one bit reader per thread)
-// Fast AC entry (8-bit lookahead), libjpeg-turbo's idea restated: a code of length L <= 8
-// whose magnitude bits also fit (L + s <= 8) decodes in one lookup to (run, value):
-//   bit 31 complete, bits 0-3 L + s, bits 4-7 run, bits 16-23 value (int8);
-//   bit 30 symbol only (s == 0, or L + s > 8): bits 0-3 L, bits 8-15 the symbol RS;
-//   0: the code is longer than 8 bits (MAXCODE walk from length 9).
-constexpr uint32_t kFacFull = 1u << 31, kFacSym = 1u << 30;
-
 struct HuffSm {
-    uint16_t lut[4][512];   // DC tables: 9-bit lookahead, (length << 8) | symbol, 0 = longer code
-    uint32_t fac[4][256];   // AC tables: fast entries (above)
+    uint16_t lut[8][512];   // 9-bit lookahead: (length << 8) | symbol, 0 = longer code
     int32_t maxcode[8][18]; // largest code of each length (left unaligned), -1 = none
     int32_t valoff[8][17];  // HUFFVAL index of a code of length l = code + valoff[l]
     uint8_t vals[8][256];
@@ -259,7 +251,7 @@ __device__ void build_tables(const JpegHdr* __restrict__ H, HuffSm& T) {
     }
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) T.vals[i >> 8][i & 255] = H->vals[i >> 8][i & 255];
     __syncthreads();
-    for (int i = threadIdx.x; i < 4 * 512; i += blockDim.x) {  // DC tables 0..3
+    for (int i = threadIdx.x; i < 8 * 512; i += blockDim.x) {
         const int t = i >> 9, peek = i & 511;
         uint16_t e = 0;
         for (int l = 1; l <= 9; ++l) {
@@ -270,25 +262,6 @@ __device__ void build_tables(const JpegHdr* __restrict__ H, HuffSm& T) {
             }
         }
         T.lut[t][peek] = e;
-    }
-    for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) {  // AC tables 4..7
-        const int t = 4 + (i >> 8), peek = i & 255;
-        uint32_t e = 0;
-        for (int l = 1; l <= 8; ++l) {
-            const int code = peek >> (8 - l);
-            if (T.maxcode[t][l] >= 0 && code >= mincode[t][l] && code <= T.maxcode[t][l]) {
-                const int rs = T.vals[t][code + T.valoff[t][l]], ss = rs & 15;
-                if (ss != 0 && l + ss <= 8) {
-                    int v = (peek >> (8 - l - ss)) & ((1 << ss) - 1);
-                    if (v < (1 << (ss - 1))) v += 1 - (1 << ss);  // EXTEND (F.12)
-                    e = kFacFull | (uint32_t)(l + ss) | (uint32_t)(rs >> 4) << 4 | (uint32_t)(v & 0xff) << 16;
-                } else {
-                    e = kFacSym | (uint32_t)l | (uint32_t)rs << 8;
-                }
-                break;
-            }
-        }
-        T.fac[t - 4][peek] = e;
     }
 }
 
@@ -347,9 +320,15 @@ struct Bits {
 
 __device__ __forceinline__ int extend(int v, int s) { return v < (1 << (s - 1)) ? v - (1 << s) + 1 : v; }
 
-// the MAXCODE walk for codes of length l0..16 (T.81 F.2.2.3); -1 for an invalid code
-__device__ __forceinline__ int decode_long(Bits& br, const HuffSm& T, int t, int l0) {
-    for (int l = l0; l <= 16; ++l) {
+// DECODE (T.81 F.2.2.3) with the lookahead table; -1 for an invalid code
+__device__ __forceinline__ int decode_sym(Bits& br, const HuffSm& T, int t) {
+    const uint16_t e = T.lut[t][br.buf >> 55];
+    if (e) {
+        br.buf <<= (e >> 8);
+        br.n -= (e >> 8);
+        return e & 255;
+    }
+    for (int l = 10; l <= 16; ++l) {
         const int code = (int)(br.buf >> (64 - l));
         if (code <= T.maxcode[t][l]) {
             br.buf <<= l;
@@ -358,17 +337,6 @@ __device__ __forceinline__ int decode_long(Bits& br, const HuffSm& T, int t, int
         }
     }
     return -1;
-}
-
-// DECODE (T.81 F.2.2.3) of a DC symbol with the lookahead table; -1 for an invalid code
-__device__ __forceinline__ int decode_sym(Bits& br, const HuffSm& T, int t) {
-    const uint16_t e = T.lut[t][br.buf >> 55];
-    if (e) {
-        br.buf <<= (e >> 8);
-        br.n -= (e >> 8);
-        return e & 255;
-    }
-    return decode_long(br, T, t, 10);
 }
 
 // --- islow IDCT (reading J1): CONST_BITS 13, PASS1_BITS 2
@@ -533,32 +501,9 @@ __global__ void __launch_bounds__(kDT, 2) k_jpeg_decode(const JpegHdr* __restric
                 pred[cpt] += t ? extend(br.take(t), t) : 0;
                 coef[0] = pred[cpt];
                 uint64_t mask = 1;
-                const int tac = (tap >> (8 * cpt)) & 0xff;
-                const uint32_t* fac = T.fac[tac - 4];
                 for (int kk = 1; kk < 64;) {
                     if (br.n < 32) br.refill();
-                    const uint32_t e = fac[br.buf >> 56];
-                    if (e & kFacFull) {  // run and value in one lookup
-                        const int len = e & 15;
-                        br.buf <<= len;
-                        br.n -= len;
-                        kk += (e >> 4) & 15;
-                        if (kk > 63) { bad = true; break; }
-                        const int z = zz[kk];
-                        coef[z * kDT] = (int)(int8_t)(uint8_t)(e >> 16);
-                        mask |= 1ull << z;
-                        ++kk;
-                        continue;
-                    }
-                    int rs;
-                    if (e & kFacSym) {
-                        const int len = e & 15;
-                        br.buf <<= len;
-                        br.n -= len;
-                        rs = (e >> 8) & 255;
-                    } else {
-                        rs = decode_long(br, T, tac, 9);
-                    }
+                    const int rs = decode_sym(br, T, (tap >> (8 * cpt)) & 0xff);
                     if (rs < 0) { bad = true; break; }
                     const int ss = rs & 15, rr = rs >> 4;
                     if (ss == 0) {
