@@ -49,6 +49,11 @@ def main():
     res["rows_equal"] = int(nr.item()) == n_raw
     res["decode_err"] = int(err.item())
     res["decode_jpeg_ms_incl_sync"] = timed(lambda: ctx.decode_jpeg(0, buf, out))
+    # the same pipeline on the decoded RGB tile already on the device: the difference to
+    # process_tile_jpeg is the ingest (copy + decode), the difference to process_tile is what
+    # the JPEG loss does to the later steps
+    dec = out.clone()
+    res["process_tile_on_decoded_ms"] = timed(lambda: ctx.process_tile(0, dec, lab, nob, tl, tf, tt, nr))
     res["decoded_equals_raw_within"] = int((out.cpu().numpy().astype(int) - rgb).__abs__().max())
     print(json.dumps(res))
     ctx.close()
