@@ -439,6 +439,10 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.wl.queue = (int32_t*)A(4 * (size_t)cap);
         s.wl.ctr = (unsigned long long*)A(8 * 8);
         s.wl.cap = cap;
+        // S4 CTAs per tile: with many tiles in flight each tile's reconstruction takes 3/8 of
+        // the SMs (r2, 12 slots: 48-64 CTAs 983-989 tiles/s, 111 955, 148 935); alone it takes
+        // 3/4 (the engine's default)
+        s.wl.ctas = cfg->n_slots >= 4 ? std::max(1, num_sms() * 3 / 8) : 0;
         s.obj_root = (int32_t*)A(4 * (size_t)mo);
         s.obj_rank = (int32_t*)A(4 * (size_t)mo);
         s.obj_bbox = (int32_t*)A(16 * (size_t)mo);

@@ -56,6 +56,7 @@ struct Worklist {
     unsigned long long* ctr;
     int32_t cap;      // ring capacity (>= ntiles + max warps)
     int32_t ntx, nty; // tile grid
+    int32_t ctas;     // region-engine CTAs per launch (0: the engine's single-tile default)
 };
 
 // header of a JPEG tile, parsed on the host (k_jpeg.cu jpeg_parse)

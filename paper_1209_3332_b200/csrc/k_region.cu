@@ -1538,7 +1538,7 @@ void launch_recon_u8_regions(const uint8_t* mask, uint8_t* R, int w, int h, cons
         }
         return std::max(1, nsm * 3 / 4);
     });
-    int b = std::max(1, std::min(blocks, n));
+    int b = std::max(1, std::min(wl.ctas > 0 ? wl.ctas : blocks, n));
     static const int grid_env = [] {  // HP_RG_GRID: absolute CTA count (experiments)
         const char* e = getenv("HP_RG_GRID");
         return e ? atoi(e) : 0;

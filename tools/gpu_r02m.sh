@@ -1,7 +1,7 @@
 #!/bin/bash
 O=gpurun_out/r02m; mkdir -p $O
 export CUDA_DEVICE_MAX_CONNECTIONS=32
-for g in 111 148 74 222; do
+for g in ${GRIDS:-111 148 74 222}; do
   HP_RG_GRID=$g timeout -s KILL 400 python bench.py --no-e2e --no-cpu-baseline > $O/bench_grid$g.json 2> $O/bench_grid$g.err
   python -c "import json;d=json.loads(open('$O/bench_grid$g.json').read().strip().splitlines()[-1]);print('grid $g',d['value'])"
 done
