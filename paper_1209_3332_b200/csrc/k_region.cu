@@ -410,8 +410,9 @@ __device__ void adi_close_region(SM& S, const uint8_t* sR, uint8_t* sRw, const u
                         if ((cm >> b) & 1) mark(S.coldirty, c0 - 1 + b - 1);
                 }
                 const unsigned lanes = __ballot_sync(FULL, chg != 0);
-                if ((lane & 7) == 0 && ((lanes >> lane) & 0xffu)) {
-                    const int sx = lane >> 3, sy = (y - 1) >> 5;
+                constexpr int LPS = SW / PXL;  // lanes per sub-tile column
+                if ((lane % LPS) == 0 && ((lanes >> lane) & (uint32_t)((1ull << LPS) - 1))) {
+                    const int sx = lane / LPS, sy = (y - 1) >> 5;
                     atomicOr(&S.subchg[sy * RX + sx], 1u << ((y - 1) & 31));
                 }
             }
