@@ -21,8 +21,9 @@
 //   J2  colour: JFIF YCbCr -> RGB, R = Y + 1.402 (Cr-128), G = Y - 0.34414 (Cb-128)
 //       - 0.71414 (Cr-128), B = Y + 1.772 (Cb-128), with the IJG 16-bit fixed-point
 //       rounding, clamped to 0..255.
-// Scope: 8-bit precision, 3 components, every sampling factor 1x1 (4:4:4), one interleaved
-// scan; anything else returns 5 (unsupported).  No blocking or reordering beyond this.
+// Scope: 8-bit precision, 3 components, 4:4:4 or 4:2:0 sampling, one interleaved scan;
+// anything else returns 5 (unsupported).  4:2:0 chroma is brought to full resolution by the
+// IJG "fancy" triangle filter (reading J4).  No blocking or reordering beyond this.
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -273,7 +274,10 @@ extern "C" int or_jpeg_decode(const uint8_t* data, int64_t n, int32_t* width, in
                 comp_h[i] = seg[7 + 3 * i] >> 4;
                 comp_v[i] = seg[7 + 3 * i] & 15;
                 comp_tq[i] = seg[8 + 3 * i];
-                if (comp_h[i] != 1 || comp_v[i] != 1) return 5;
+                // 4:4:4 (every component 1x1) or 4:2:0 (Y 2x2, Cb and Cr 1x1); reading J3
+                const bool ok = i == 0 ? ((comp_h[0] == 1 && comp_v[0] == 1) || (comp_h[0] == 2 && comp_v[0] == 2))
+                                       : (comp_h[i] == 1 && comp_v[i] == 1);
+                if (!ok) return 5;
                 if (comp_tq[i] > 3) return 1;
             }
             frame = true;
@@ -318,57 +322,117 @@ extern "C" int or_jpeg_decode(const uint8_t* data, int64_t n, int32_t* width, in
             *width = X;
             *height = Y;
             if (!rgb) return 0;  // size query
-            // F.2: MCUs of one block per component (all sampling factors 1), raster order
-            const int mx = (X + 7) / 8, my = (Y + 7) / 8;
+            // F.2 / A.2.3: MCUs in raster order; an MCU holds H x V blocks of Y (raster order
+            // inside the MCU), then one block of Cb and one of Cr.  4:4:4 (H = V = 1) or 4:2:0
+            // (H = V = 2).  The decoded samples go to component planes padded to whole MCUs.
+            const int Hy = comp_h[0], Vy = comp_v[0];
+            const int mw = 8 * Hy, mh = 8 * Vy;  // MCU size in pixels
+            const int mx = (X + mw - 1) / mw, my = (Y + mh - 1) / mh;
             const int64_t nmcu = (int64_t)mx * my;
+            const int yw = mx * mw, yh = my * mh, cw = mx * 8, chh = my * 8;  // plane sizes
+            std::vector<uint8_t> plane_y((size_t)yw * yh), plane_cb((size_t)cw * chh), plane_cr((size_t)cw * chh);
             Reader rd{data, n, p + 2 + L};
             int pred[3] = {0, 0, 0};
-            int32_t coef[3][64];
-            uint8_t smp[3][64];
+            int32_t coef[64];
+            uint8_t smp[64];
             for (int64_t mcu = 0; mcu < nmcu; ++mcu) {
                 if (Ri > 0 && mcu > 0 && mcu % Ri == 0) {  // F.2.1.3.1 restart
                     if (!rd.restart()) return 1;
                     pred[0] = pred[1] = pred[2] = 0;
                 }
+                const int mcx = (int)(mcu % mx), mcy = (int)(mcu / mx);
                 for (int c = 0; c < 3; ++c) {
-                    int zz[64] = {};
-                    // F.2.2.1 DC
-                    const int t = rd.decode(dc[comp_td[c]]);
-                    if (t < 0 || t > 11) return 1;
-                    const int diff = extend(rd.receive(t), t);
-                    pred[c] += diff;
-                    zz[0] = pred[c];
-                    // F.2.2.2 AC (Figure F.13)
-                    int k = 1;
-                    while (k < 64) {
-                        const int rs = rd.decode(ac[comp_ta[c]]);
-                        if (rs < 0) return 1;
-                        const int ssss = rs & 15, rrrr = rs >> 4;
-                        if (ssss == 0) {
-                            if (rrrr == 15) {
-                                k += 16;
-                                continue;
+                    const int nb = c == 0 ? Hy * Vy : 1;
+                    for (int bi = 0; bi < nb; ++bi) {
+                        int zz[64] = {};
+                        // F.2.2.1 DC
+                        const int t = rd.decode(dc[comp_td[c]]);
+                        if (t < 0 || t > 11) return 1;
+                        const int diff = extend(rd.receive(t), t);
+                        pred[c] += diff;
+                        zz[0] = pred[c];
+                        // F.2.2.2 AC (Figure F.13)
+                        int k = 1;
+                        while (k < 64) {
+                            const int rs = rd.decode(ac[comp_ta[c]]);
+                            if (rs < 0) return 1;
+                            const int ssss = rs & 15, rrrr = rs >> 4;
+                            if (ssss == 0) {
+                                if (rrrr == 15) {
+                                    k += 16;
+                                    continue;
+                                }
+                                break;  // EOB
                             }
-                            break;  // EOB
+                            k += rrrr;
+                            if (k > 63) return 1;
+                            zz[k] = extend(rd.receive(ssss), ssss);
+                            ++k;
                         }
-                        k += rrrr;
-                        if (k > 63) return 1;
-                        zz[k] = extend(rd.receive(ssss), ssss);
-                        ++k;
+                        // A.3.4 dequantisation, A.3.6 zig-zag -> natural order
+                        for (int kk = 0; kk < 64; ++kk) coef[ZZ[kk]] = zz[kk] * qt[comp_tq[c]][ZZ[kk]];
+                        idct_block(coef, smp);
+                        uint8_t* pl = c == 0 ? plane_y.data() : c == 1 ? plane_cb.data() : plane_cr.data();
+                        const int pw = c == 0 ? yw : cw;
+                        const int ox = c == 0 ? mcx * mw + 8 * (bi % Hy) : mcx * 8;
+                        const int oy = c == 0 ? mcy * mh + 8 * (bi / Hy) : mcy * 8;
+                        for (int r = 0; r < 8; ++r)
+                            for (int cc = 0; cc < 8; ++cc) pl[(size_t)(oy + r) * pw + ox + cc] = smp[r * 8 + cc];
                     }
-                    // A.3.4 dequantisation, A.3.6 zig-zag -> natural order
-                    for (int kk = 0; kk < 64; ++kk) coef[c][ZZ[kk]] = zz[kk] * qt[comp_tq[c]][ZZ[kk]];
-                    idct_block(coef[c], smp[c]);
                 }
-                const int bx = (int)(mcu % mx) * 8, by = (int)(mcu / mx) * 8;
-                for (int r = 0; r < 8; ++r)
-                    for (int cc = 0; cc < 8; ++cc) {
-                        const int x = bx + cc, y = by + r;
-                        if (x >= X || y >= Y) continue;  // partial MCU at the right / bottom edge
-                        ycc_to_rgb(smp[0][r * 8 + cc], smp[1][r * 8 + cc], smp[2][r * 8 + cc],
-                                   rgb + ((int64_t)y * X + x) * 3);
-                    }
             }
+            // chroma at full resolution: copied (4:4:4), or reading J4's triangle-filter
+            // ("fancy") upsampling of the IJG library for 4:2:0 -- per output row, the nearer
+            // chroma row weighted 3 and the next nearer 1 (the first / last real row repeated at
+            // the image edges), then the same 3:1 weights across columns with the rounding
+            // offsets 8 and 7 of the two output pixels of a chroma column
+            std::vector<uint8_t> up_cb((size_t)X * Y), up_cr((size_t)X * Y);
+            if (Hy == 1 || (X + 1) / 2 <= 2) {
+                // 4:4:4 copies; the IJG library filters only chroma wider than 2 samples and
+                // replicates each sample to 2 x 2 otherwise
+                const int sh = Hy == 1 ? 0 : 1;
+                for (int y = 0; y < Y; ++y)
+                    for (int x = 0; x < X; ++x) {
+                        up_cb[(size_t)y * X + x] = plane_cb[(size_t)(y >> sh) * cw + (x >> sh)];
+                        up_cr[(size_t)y * X + x] = plane_cr[(size_t)(y >> sh) * cw + (x >> sh)];
+                    }
+            } else {
+                const int dw = (X + 1) / 2, dh = (Y + 1) / 2;  // downsampled_width / height
+                std::vector<int> colsum(cw);
+                for (int pass = 0; pass < 2; ++pass) {
+                    const std::vector<uint8_t>& src = pass == 0 ? plane_cb : plane_cr;
+                    std::vector<uint8_t>& dst = pass == 0 ? up_cb : up_cr;
+                    std::vector<uint8_t> row((size_t)2 * cw + 2);
+                    for (int y = 0; y < Y; ++y) {
+                        const int ir = y / 2;
+                        int fr = (y % 2 == 0) ? ir - 1 : ir + 1;  // the next nearer row
+                        if (fr < 0) fr = 0;
+                        if (fr > dh - 1) fr = dh - 1;
+                        for (int c = 0; c < cw; ++c) colsum[c] = 3 * src[(size_t)ir * cw + c] + src[(size_t)fr * cw + c];
+                        // the IJG column loop: first column, dw - 2 general columns, last column
+                        int o = 0;
+                        int thiscol = colsum[0], nextcol = colsum[1 < cw ? 1 : 0], lastcol;
+                        row[o++] = (uint8_t)((thiscol * 4 + 8) >> 4);
+                        row[o++] = (uint8_t)((thiscol * 3 + nextcol + 7) >> 4);
+                        lastcol = thiscol;
+                        thiscol = nextcol;
+                        for (int c = 2; c < dw; ++c) {
+                            nextcol = colsum[c];
+                            row[o++] = (uint8_t)((thiscol * 3 + lastcol + 8) >> 4);
+                            row[o++] = (uint8_t)((thiscol * 3 + nextcol + 7) >> 4);
+                            lastcol = thiscol;
+                            thiscol = nextcol;
+                        }
+                        row[o++] = (uint8_t)((thiscol * 3 + lastcol + 8) >> 4);
+                        row[o++] = (uint8_t)((thiscol * 4 + 7) >> 4);
+                        for (int x = 0; x < X; ++x) dst[(size_t)y * X + x] = row[x];
+                    }
+                }
+            }
+            for (int y = 0; y < Y; ++y)
+                for (int x = 0; x < X; ++x)
+                    ycc_to_rgb(plane_y[(size_t)y * yw + x], up_cb[(size_t)y * X + x], up_cr[(size_t)y * X + x],
+                               rgb + ((int64_t)y * X + x) * 3);
             return 0;
         } else if (m == 0xD9) {
             return 1;  // EOI before a scan

@@ -53,10 +53,35 @@ def test_flat_grey_closed_form(v):
     assert np.array_equal(out, rgb)
 
 
+@pytest.mark.parametrize("shape,q,rst", [((64, 64), 90, 4), ((37, 53), 75, 1), ((300, 257), 95, 0),
+                                         ((512, 512), 90, 4), ((1, 300), 90, 2), ((301, 1), 85, 3),
+                                         ((2, 2), 90, 1), ((9, 3), 90, 1), ((7, 4), 90, 2), ((5, 5), 90, 1),
+                                         ((17, 33), 60, 2), ((2, 300), 90, 1)])
+def test_matches_cv2_420(shape, q, rst):
+    """4:2:0 (Y 2x2, chroma 1x1): reading J4's triangle-filter upsampling (the IJG "fancy"
+    path; chroma at most 2 samples wide is replicated instead), bit for bit with OpenCV --
+    ragged sizes exercise the first / last column and row special cases."""
+    rgb = make_tile(sum(shape) + q + 7, TileSpec(*shape))["rgb"]
+    buf = encode_tile(rgb, q, rst, sampling="420")
+    assert np.array_equal(oracle.jpeg_decode(buf), _cv2_rgb(buf))
+
+
+@pytest.mark.parametrize("rgbv", [(200, 30, 90), (12, 240, 7), (128, 128, 128)])
+def test_420_flat_colour_closed_form(rgbv):
+    """A flat colour has constant chroma planes; the filter's weights sum to 16 with rounding
+    offsets 8 / 7, so (16 c + 8) >> 4 = (16 c + 7) >> 4 = c: the upsampled chroma, hence the
+    decoded image, is uniform -- and equal to the 4:4:4 decode of the same colour."""
+    rgb = np.full((40, 56, 3), rgbv, np.uint8)
+    a = oracle.jpeg_decode(encode_tile(rgb, 95, 2, sampling="420"))
+    assert (a == a[0, 0]).all()
+    b = oracle.jpeg_decode(encode_tile(rgb, 95, 2, sampling="444"))
+    assert np.array_equal(a[0, 0], b[0, 0])
+
+
 def test_out_of_scope_refused():
     rgb = make_tile(3, TileSpec(64, 64))["rgb"]
     with pytest.raises(RuntimeError):
-        oracle.jpeg_decode(encode_tile(rgb, 90, 4, sampling="420"))
+        oracle.jpeg_decode(encode_tile(rgb, 90, 4, sampling="422"))
     with pytest.raises(RuntimeError):
         oracle.jpeg_decode(encode_tile(rgb, 90, 0, progressive=True))
     with pytest.raises(RuntimeError):
