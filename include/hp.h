@@ -193,7 +193,8 @@ hp_status hp_run_tiles(hp_ctx* ctx, const hp_tile_source* src, const hp_result_s
 
 /* Compressed ingest ("the main limiting factor and bottleneck
  * is the I/O overhead of reading image tiles", 716-726).  Tiles arrive as baseline JPEG files
- * (ITU-T T.81 sequential Huffman, 8-bit, 3 components, 4:4:4 sampling, one interleaved scan;
+ * (ITU-T T.81 sequential Huffman, 8-bit, 3 components, 4:4:4 or 4:2:0 sampling (the 4:2:0
+ * chroma upsampled by the IJG triangle filter, reading J4), one interleaved scan;
  * a restart interval (DRI) lets the GPU decode one interval per thread -- without one the
  * whole scan is a single serial interval).  Only the file crosses PCIe (~4 MB instead of
  * 50 MB for a quality-90 4K tile).  The host parses the marker segments (a few hundred

@@ -157,7 +157,7 @@ void ev(hp_ctx* ctx, Slot& sl, int k, cudaStream_t s) {
 // both uploaded by the caller) and decodes it inside S1 (k_jpeg.cu); rgb gives only the size.
 hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, int64_t lpitch,
                   int32_t* n_objects, cudaStream_t s, hp_feature_table* table = nullptr,
-                  bool* fused = nullptr, bool jpeg = false) {
+                  bool* fused = nullptr, int jpeg = 0) {
     if (fused) *fused = false;
     const hp_params& p = ctx->cfg.params;
     const int w = rgb->width, h = rgb->height;
@@ -165,8 +165,8 @@ hp_status segment(hp_ctx* ctx, Slot& sl, const hp_image* rgb, int32_t* labels, i
     if (jpeg) {                                                                                       // S0 + S1
         cudaMemsetAsync(sl.jerr, 0, sizeof(int32_t), s);
         const int64_t cap = 3LL * ctx->cfg.max_width * ctx->cfg.max_height;
-        launch_jpeg_decode(sl.jhdr_dev, sl.rgb_dev, cap, w, h, sl.jstarts, sl.jblk, ctx->lut, p, sl.g, sl.flags,
-                           &sl.counters[0], nullptr, 0, sl.jerr, s);
+        launch_jpeg_decode(sl.jhdr_dev, jpeg, sl.rgb_dev, cap, w, h, sl.jstarts, sl.jblk, sl.jplanes, ctx->lut, p,
+                           sl.g, sl.flags, &sl.counters[0], nullptr, 0, sl.jerr, s);
     } else {
         HP_DUP(1) launch_cd(rgb->data, w, h, rgb->pitch_bytes, ctx->lut, p, sl.g, sl.flags, &sl.counters[0], s);  // S1
     }
@@ -288,7 +288,7 @@ hp_status check_labels(hp_ctx* ctx, const hp_labels* l, int w) {
 // (stream s).  ring: stage the header in the slot's pinned ring (single-tile calls may be
 // issued back to back on one slot) instead of its one run_tiles staging entry.
 hp_status upload_jpeg(hp_ctx* ctx, Slot& sl, const uint8_t* host, int64_t nbytes, cudaStream_t s, bool ring,
-                      int* w, int* h) {
+                      int* w, int* h, int* sub) {
     const int64_t cap = 3LL * ctx->cfg.max_width * ctx->cfg.max_height;
     if (!host || nbytes < 4 || nbytes > cap) {
         set_err(ctx, "jpeg: null buffer or size %lld outside [4, %lld]", (long long)nbytes, (long long)cap);
@@ -321,6 +321,7 @@ hp_status upload_jpeg(hp_ctx* ctx, Slot& sl, const uint8_t* host, int64_t nbytes
     }
     *w = H->width;
     *h = H->height;
+    *sub = H->sub;
     return check_launch(ctx, "jpeg upload");
 }
 
@@ -467,6 +468,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.jstarts = (int32_t*)A(4 * (size_t)jpeg_max_intervals(N));
         s.jblk = (int32_t*)A(4 * (size_t)(3 * N / 8192 + 2));
         s.jerr = (int32_t*)A(16);
+        s.jplanes = (uint8_t*)A((size_t)jpeg_planes_bytes(cfg->max_width, cfg->max_height));
         s.jhdr_host = (JpegHdr*)halloc(sizeof(JpegHdr));
         s.jhdr_ring = (JpegHdr*)halloc(4 * sizeof(JpegHdr));
         s.h_jerr = (int32_t*)halloc(16);
@@ -484,7 +486,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
                        s.ML, s.d, s.L, s.dist, s.J, s.c, s.gcol, s.seg_top, s.seg_bot, s.wl.state, s.wl.inrows, s.wl.queue,
                        s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.cs_edge, s.cs_roots, s.cs_nroots, s.sc_root, s.sc_bbox, s.sc_area, s.sc_big, s.sc_huge, s.big_scratch, s.stg_label, s.stg_flags, s.stg_feat, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
                        s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows, s.h_arena,
-                       s.jhdr_dev, s.jstarts, s.jblk, s.jerr, s.jhdr_host, s.jhdr_ring, s.h_jerr};
+                       s.jhdr_dev, s.jstarts, s.jblk, s.jerr, s.jhdr_host, s.jhdr_ring, s.h_jerr, s.jplanes};
         for (void* p : all)
             if (!p) { hp_ctx_destroy(ctx); return HP_ERR_NOMEM; }
         int prio_lo = 0, prio_hi = 0;
@@ -578,15 +580,15 @@ hp_status hp_process_tile_jpeg(hp_ctx* ctx, int32_t slot, const uint8_t* host_jp
     if ((st = check_labels(ctx, lab, 1)) || (st = check_table(ctx, out))) return st;
     Slot& sl = ctx->slots[slot];
     cudaStream_t cs = (cudaStream_t)s;
-    int w = 0, h = 0;
-    if ((st = upload_jpeg(ctx, sl, host_jpeg, nbytes, cs, true, &w, &h))) return st;
+    int w = 0, h = 0, sub = 1;
+    if ((st = upload_jpeg(ctx, sl, host_jpeg, nbytes, cs, true, &w, &h, &sub))) return st;
     if (lab->labels_pitch_elems < w) {
         set_err(ctx, "labels pitch %lld < JPEG width %d", (long long)lab->labels_pitch_elems, w);
         return HP_ERR_INVALID;
     }
     hp_image im{sl.rgb_dev, w, h, 3LL * w};
     bool fused = false;
-    st = segment(ctx, sl, &im, lab->labels, lab->labels_pitch_elems, lab->n_objects_dev, cs, out, &fused, true);
+    st = segment(ctx, sl, &im, lab->labels, lab->labels_pitch_elems, lab->n_objects_dev, cs, out, &fused, sub);
     if (!st && !fused) st = features(ctx, sl, w, h, lab->labels, lab->labels_pitch_elems, out, cs);
     if (!st && decode_err_dev) cudaMemcpyAsync(decode_err_dev, sl.jerr, sizeof(int32_t), cudaMemcpyDeviceToDevice, cs);
     return st ? st : check_launch(ctx, "process_tile_jpeg");
@@ -602,15 +604,16 @@ hp_status hp_decode_jpeg(hp_ctx* ctx, int32_t slot, const uint8_t* host_jpeg, in
     }
     Slot& sl = ctx->slots[slot];
     cudaStream_t cs = (cudaStream_t)s;
-    int w = 0, h = 0;
-    if ((st = upload_jpeg(ctx, sl, host_jpeg, nbytes, cs, true, &w, &h))) return st;
+    int w = 0, h = 0, sub = 1;
+    if ((st = upload_jpeg(ctx, sl, host_jpeg, nbytes, cs, true, &w, &h, &sub))) return st;
     if (pitch_bytes < 3LL * w) {
         set_err(ctx, "hp_decode_jpeg: pitch < 3*width");
         return HP_ERR_INVALID;
     }
     cudaMemsetAsync(sl.jerr, 0, sizeof(int32_t), cs);
-    launch_jpeg_decode(sl.jhdr_dev, sl.rgb_dev, 3LL * ctx->cfg.max_width * ctx->cfg.max_height, w, h, sl.jstarts,
-                       sl.jblk, ctx->lut, ctx->cfg.params, nullptr, nullptr, nullptr, rgb_dev, pitch_bytes, sl.jerr, cs);
+    launch_jpeg_decode(sl.jhdr_dev, sub, sl.rgb_dev, 3LL * ctx->cfg.max_width * ctx->cfg.max_height, w, h, sl.jstarts,
+                       sl.jblk, sl.jplanes, ctx->lut, ctx->cfg.params, nullptr, nullptr, nullptr, rgb_dev, pitch_bytes,
+                       sl.jerr, cs);
     cudaMemcpyAsync(sl.h_jerr, sl.jerr, sizeof(int32_t), cudaMemcpyDeviceToHost, cs);
     cudaError_t e = cudaStreamSynchronize(cs);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "hp_decode_jpeg");
@@ -929,6 +932,7 @@ hp_status run_tiles_impl(hp_ctx* ctx, int w, int h, bool jpeg, Next next, const 
         cudaStream_t s = sl.stream;
         const uint8_t* host = nullptr;
         int64_t pitch = 0, tid = -1;
+        int jsub = 1;
         while (true) {  // until a tile is in flight on slot i or the source is drained
             host = nullptr;
             pitch = 0;
@@ -948,7 +952,7 @@ hp_status run_tiles_impl(hp_ctx* ctx, int w, int h, bool jpeg, Next next, const 
             // a JPEG the decoder cannot take (malformed, out of scope, wrong size) fails alone:
             // reported through done() with no rows, and the slot takes the next tile
             int jw = 0, jh = 0;
-            hp_status ps = upload_jpeg(ctx, sl, host, pitch, s, false, &jw, &jh);
+            hp_status ps = upload_jpeg(ctx, sl, host, pitch, s, false, &jw, &jh, &jsub);
             if (ps == HP_ERR_CUDA) return ps;
             if (!ps && (jw != w || jh != h)) {
                 set_err(ctx, "run_tiles_jpeg: tile %lld is %dx%d, the source says %dx%d", (long long)tid, jw, jh, w, h);
@@ -965,7 +969,7 @@ hp_status run_tiles_impl(hp_ctx* ctx, int w, int h, bool jpeg, Next next, const 
         // the tile's chain: segmentation + features on the slot's own buffers, rows D2H
         auto chain = [&]() -> hp_status {
             bool fused = false;
-            hp_status r = segment(ctx, sl, &im, sl.lab_dev, w, sl.cnt32 + 4, s, &tab, &fused, jpeg);
+            hp_status r = segment(ctx, sl, &im, sl.lab_dev, w, sl.cnt32 + 4, s, &tab, &fused, jpeg ? jsub : 0);
             if (!r && !fused) r = features(ctx, sl, w, h, sl.lab_dev, w, &tab, s);
             if (r) return r;
             cudaMemcpyAsync(sl.h_nrows, sl.tab_nrows, 4, cudaMemcpyDeviceToHost, s);
@@ -991,7 +995,8 @@ hp_status run_tiles_impl(hp_ctx* ctx, int w, int h, bool jpeg, Next next, const 
         const bool graphable = ctx->graphs && !ctx->timing && ctx->cfg.params.bg_skip_frac > 1.0f &&
                                ctx->prio == 0;
         hp_status r = HP_OK;
-        const bool same = sl.graph_w == w && sl.graph_h == h && sl.graph_jpeg == (int)jpeg && same_arena(sl.graph_arena);
+        const int gkey = jpeg ? jsub : 0;  // raw, JPEG 4:4:4 or JPEG 4:2:0: different chains
+        const bool same = sl.graph_w == w && sl.graph_h == h && sl.graph_jpeg == gkey && same_arena(sl.graph_arena);
         if (graphable && sl.gexec && same) {
             if (cudaGraphLaunch(sl.gexec, s) != cudaSuccess) return cuda_fail(ctx, cudaGetLastError(), "graph launch");
         } else if (graphable && same) {
@@ -1013,7 +1018,7 @@ hp_status run_tiles_impl(hp_ctx* ctx, int w, int h, bool jpeg, Next next, const 
             }
             sl.graph_w = w;
             sl.graph_h = h;
-            sl.graph_jpeg = (int)jpeg;
+            sl.graph_jpeg = gkey;
             sl.graph_arena = akey;
         }
         cudaEventRecord(sl.done_ev, s);

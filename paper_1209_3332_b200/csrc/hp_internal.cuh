@@ -62,13 +62,14 @@ struct Worklist {
 // header of a JPEG tile, parsed on the host (k_jpeg.cu jpeg_parse)
 struct JpegHdr {
     int32_t width, height;
-    int32_t mcux, mcuy;          // 8x8 MCUs per row / column (4:4:4)
+    int32_t mcux, mcuy;          // MCUs per row / column (8 x 8 px, or 16 x 16 px for 4:2:0)
     int32_t ri;                  // MCUs per restart interval (all MCUs when there is no DRI)
     int32_t n_intervals;
     int64_t scan_off, scan_len;  // the entropy-coded segment within the file
     uint16_t q[3][64];           // dequantisation factor per component, natural order
     uint8_t td[3], ta[3];        // DC table (0..3) and AC table (4..7) of each component
-    uint8_t pad[2];
+    uint8_t sub;                 // 1: 4:4:4; 2: 4:2:0 (Y sampled 2 x 2, MCU 16 x 16 px)
+    uint8_t pad;
     uint8_t bits[8][17];         // BITS[1..16] of tables 0..3 (DC) and 4..7 (AC)
     uint8_t vals[8][256];        // HUFFVAL
 };
@@ -116,6 +117,7 @@ struct Slot {
     int32_t* jstarts;            // restart-interval start offsets
     int32_t* jblk;               // per-chunk restart-marker counts
     int32_t* jerr;               // decode error word
+    uint8_t* jplanes;            // 4:2:0 component planes (Y, Cb, Cr) before upsampling
     int32_t* h_jerr;             // pinned copy of it, per delivered tile
     int32_t* lab_dev;
     int32_t *tab_label, *tab_flags, *tab_nrows;
@@ -185,15 +187,22 @@ void upload_od_lut(float* lut_dev, cudaStream_t s);
 hp_status jpeg_parse(const uint8_t* data, int64_t n, JpegHdr* out, const char** why);
 // Capacity of the per-slot restart-interval offset array for a tile of npx pixels.
 inline int64_t jpeg_max_intervals(int64_t npx) { return npx / 64 + 64; }
-// Decode the file (device copy `file`, header `hdr` on the device) of a w x h tile.
-// rgb == nullptr: S1 fused (g, flags, bg_count as launch_cd); else the decoded RGB tile
-// (pitch rgb_pitch) only -- the verification path.  starts / blkcnt: slot scratch
-// (jpeg_max_intervals entries; file_cap / 8192 + 2 entries).  err: device int, OR-ed with
-// 1 (restart-marker count mismatch) or 2 (invalid Huffman code); the caller zeroes it.
-void launch_jpeg_decode(const JpegHdr* hdr, const uint8_t* file, int64_t file_cap, int w, int h, int32_t* starts,
-                        int32_t* blkcnt, const float* lut, const hp_params& p, uint8_t* g, uint8_t* flags,
-                        unsigned long long* bg_count, uint8_t* rgb, int64_t rgb_pitch, int32_t* err,
-                        cudaStream_t s);
+// Decode the file (device copy `file`, header `hdr` on the device) of a w x h tile; sub is
+// the host-parsed sampling (1: 4:4:4, 2: 4:2:0).  rgb == nullptr: S1 fused (g, flags,
+// bg_count as launch_cd); else the decoded RGB tile (pitch rgb_pitch) only -- the
+// verification path.  4:4:4 decodes straight into S1; 4:2:0 decodes to component planes
+// (`planes`, jpeg_planes_bytes) and a second kernel upsamples (reading J4), converts and runs
+// S1.  starts / blkcnt: slot scratch (jpeg_max_intervals entries; file_cap / 8192 + 2
+// entries).  err: device int, OR-ed with 1 (restart-marker count mismatch) or 2 (invalid
+// Huffman code); the caller zeroes it.
+inline int64_t jpeg_planes_bytes(int w, int h) {
+    const int64_t yw = (w + 15) / 16 * 16, yh = (h + 15) / 16 * 16;
+    return yw * yh + 2 * (yw / 2) * (yh / 2);
+}
+void launch_jpeg_decode(const JpegHdr* hdr, int sub, const uint8_t* file, int64_t file_cap, int w, int h,
+                        int32_t* starts, int32_t* blkcnt, uint8_t* planes, const float* lut, const hp_params& p,
+                        uint8_t* g, uint8_t* flags, unsigned long long* bg_count, uint8_t* rgb, int64_t rgb_pitch,
+                        int32_t* err, cudaStream_t s);
 // S3
 void launch_open(const uint8_t* g, int w, int h, int diam, uint8_t* tmp, uint8_t* out,
                  cudaStream_t s);

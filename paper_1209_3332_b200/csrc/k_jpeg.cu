@@ -71,7 +71,9 @@ hp_status jpeg_parse(const uint8_t* d, int64_t n, JpegHdr* H, const char** why) 
                 if (s[5] != 3) return unsup("component count other than 3");
                 for (int i = 0; i < 3; ++i) {
                     cid[i] = s[6 + 3 * i];
-                    if (s[7 + 3 * i] != 0x11) return unsup("chroma subsampling (only 4:4:4)");
+                    // 4:4:4, or 4:2:0 (Y 2 x 2, chroma 1 x 1); reading J3
+                    if (i == 0 && s[7] == 0x22) H->sub = 2;
+                    else if (s[7 + 3 * i] != 0x11) return unsup("chroma sampling other than 4:4:4 / 4:2:0");
                     ctq[i] = s[8 + 3 * i];
                     if (ctq[i] > 3) return bad("SOF table");
                 }
@@ -108,8 +110,9 @@ hp_status jpeg_parse(const uint8_t* d, int64_t n, JpegHdr* H, const char** why) 
                 }
                 if (s[7] != 0 || s[8] != 63 || s[9] != 0) return unsup("progressive scan");
                 if (H->width < 1 || H->height < 1) return bad("frame size");
-                H->mcux = (H->width + 7) / 8;
-                H->mcuy = (H->height + 7) / 8;
+                if (H->sub == 0) H->sub = 1;
+                H->mcux = (H->width + 8 * H->sub - 1) / (8 * H->sub);
+                H->mcuy = (H->height + 8 * H->sub - 1) / (8 * H->sub);
                 const int64_t nmcu = (int64_t)H->mcux * H->mcuy;
                 H->ri = (ri > 0 && ri < nmcu) ? ri : (int32_t)nmcu;
                 H->n_intervals = (int32_t)((nmcu + H->ri - 1) / H->ri);
@@ -459,12 +462,14 @@ __device__ __forceinline__ void ycc_rgb(int y, int cb, int cr, int& R, int& G, i
     B = clamp255(y + ((116130 * xb + 32768) >> 16));
 }
 
-template <bool kRGB>
+// kMode 0: 4:4:4 fused into S1; 1: 4:4:4 to RGB (verification); 2: 4:2:0 to component planes
+template <int kMode>
 __global__ void __launch_bounds__(kDT, 2) k_jpeg_decode(const JpegHdr* __restrict__ H, const uint8_t* __restrict__ file,
                                                      const int32_t* __restrict__ starts, const float* __restrict__ lut_g,
                                                      CdConst k, uint8_t* __restrict__ g, uint8_t* __restrict__ flags,
                                                      unsigned long long* bg_count, uint8_t* __restrict__ rgb,
-                                                     int64_t rgb_pitch, int32_t* err) {
+                                                     int64_t rgb_pitch, uint8_t* __restrict__ planes, int32_t* err) {
+    constexpr bool kRGB = kMode == 1;
     __shared__ HuffSm T;
     __shared__ uint16_t q[3][64];
     __shared__ float od[256];
@@ -491,9 +496,11 @@ __global__ void __launch_bounds__(kDT, 2) k_jpeg_decode(const JpegHdr* __restric
         const int64_t m0 = (int64_t)iv * ri, m1 = min(m0 + ri, nmcu);
         bool bad = false;
         for (int64_t m = m0; m < m1 && !bad; ++m) {
-            const int bx = (int)(m % mcux) * 8, by = (int)(m / mcux) * 8;
+            const int bx = (int)(m % mcux) * 8 * (kMode == 2 ? 2 : 1), by = (int)(m / mcux) * 8 * (kMode == 2 ? 2 : 1);
 #pragma unroll 1
-            for (int cpt = 0; cpt < 3; ++cpt) {
+            for (int blk = 0; blk < (kMode == 2 ? 6 : 3); ++blk) {
+                // 4:2:0: four Y blocks (raster order inside the MCU), then Cb, Cr
+                const int cpt = kMode == 2 ? (blk < 4 ? 0 : blk - 3) : blk;
                 // --- F.2.2.1 / F.2.2.2: the block's coefficients, zig-zag -> natural order
                 br.refill();
                 int t = decode_sym(br, T, (tdp >> (8 * cpt)) & 0xff);
@@ -518,8 +525,24 @@ __global__ void __launch_bounds__(kDT, 2) k_jpeg_decode(const JpegHdr* __restric
                     ++kk;
                 }
                 if (bad) break;
-                // --- IDCT; Y and Cb samples parked, Cr rows converted and consumed at once
-                if (cpt < 2) {
+                // --- IDCT
+                if (kMode == 2) {  // into the component planes (Y pitch yw, chroma pitch yw / 2)
+                    const int yw = mcux * 16, cwp = mcux * 8;
+                    uint8_t* dst;
+                    if (cpt == 0) {
+                        dst = planes + (int64_t)(by + 8 * (blk >> 1)) * yw + bx + 8 * (blk & 1);
+                    } else {
+                        const int64_t cplane = (int64_t)cwp * H->mcuy * 8;
+                        dst = planes + (int64_t)yw * H->mcuy * 16 + (cpt - 1) * cplane + (int64_t)(by / 2) * cwp + bx / 2;
+                    }
+                    const int pitch = cpt == 0 ? yw : cwp;
+                    idct_block(coef, mask, q[cpt], [&](int r, const int* sm) {
+                        uint2 v;
+                        v.x = sm[0] | sm[1] << 8 | sm[2] << 16 | (uint32_t)sm[3] << 24;
+                        v.y = sm[4] | sm[5] << 8 | sm[6] << 16 | (uint32_t)sm[7] << 24;
+                        *reinterpret_cast<uint2*>(dst + (int64_t)r * pitch) = v;
+                    });
+                } else if (cpt < 2) {  // Y and Cb samples parked, Cr rows converted and consumed at once
                     uint8_t* dst = smp + cpt * 64 * kDT;
                     idct_block(coef, mask, q[cpt], [&](int r, const int* s) {
 #pragma unroll
@@ -573,15 +596,104 @@ __global__ void __launch_bounds__(kDT, 2) k_jpeg_decode(const JpegHdr* __restric
         }
         if (bad) atomicOr(err, 2);
     }
+    if (kMode == 0 && bg_count) block_count(nbg, bg_count);
+}
+
+// 4:2:0 -> full resolution (reading J4, the IJG triangle filter), JFIF colour, then S1 (or the
+// RGB tile for verification).  A thread makes 8 output pixels of a row from 8 Y samples and
+// the 6 chroma columns around them in the nearer and the next nearer chroma row.
+template <bool kRGB>
+__global__ void __launch_bounds__(256) k_jpeg_up_cd(const JpegHdr* __restrict__ H, const uint8_t* __restrict__ planes,
+                                                    const float* __restrict__ lut_g, CdConst k, uint8_t* __restrict__ g,
+                                                    uint8_t* __restrict__ flags, unsigned long long* bg_count,
+                                                    uint8_t* __restrict__ rgb, int64_t rgb_pitch) {
+    __shared__ float od[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) od[i] = lut_g[i];
+    __syncthreads();
+    const int w = H->width, h = H->height;
+    const int yw = H->mcux * 16, cwp = H->mcux * 8;
+    const int64_t cplane = (int64_t)cwp * H->mcuy * 8;
+    const uint8_t* Yp = planes;
+    const uint8_t* Cp[2] = {planes + (int64_t)yw * H->mcuy * 16, planes + (int64_t)yw * H->mcuy * 16 + cplane};
+    const int dw = (w + 1) / 2, dh = (h + 1) / 2;  // downsampled width / height
+    const int gpr = (w + 7) / 8;                   // 8-pixel groups per row
+    const int64_t ngroups = (int64_t)gpr * h;
+    const bool vec8 = (w & 7) == 0;
+    int nbg = 0;
+    for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < ngroups; gi += (int64_t)gridDim.x * blockDim.x) {
+        const int y = (int)(gi / gpr), x0 = (int)(gi % gpr) * 8;
+        const int ir = y >> 1;
+        const int fr = min(max((y & 1) ? ir + 1 : ir - 1, 0), dh - 1);  // next nearer chroma row
+        const int c0 = x0 >> 1;                                         // chroma columns c0 .. c0 + 3
+        int up[2][8];
+#pragma unroll
+        for (int pl = 0; pl < 2; ++pl) {
+            const uint8_t* rn = Cp[pl] + (int64_t)ir * cwp;
+            const uint8_t* rf = Cp[pl] + (int64_t)fr * cwp;
+            if (dw <= 2) {  // the IJG library replicates chroma of at most 2 samples per row
+#pragma unroll
+                for (int j = 0; j < 8; ++j) up[pl][j] = rn[min((x0 + j) >> 1, cwp - 1)];
+                continue;
+            }
+            int cs[6];  // column sums of chroma columns c0 - 1 .. c0 + 4
+#pragma unroll
+            for (int j = 0; j < 6; ++j) {
+                const int c = min(max(c0 - 1 + j, 0), cwp - 1);
+                cs[j] = 3 * rn[c] + rf[c];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = c0 + j;
+                up[pl][2 * j] = c == 0 ? (cs[j + 1] * 4 + 8) >> 4 : (cs[j + 1] * 3 + cs[j] + 8) >> 4;
+                up[pl][2 * j + 1] = c >= dw - 1 ? (cs[j + 1] * 4 + 7) >> 4 : (cs[j + 1] * 3 + cs[j + 2] + 7) >> 4;
+            }
+        }
+        const uint8_t* yr = Yp + (int64_t)y * yw + x0;
+        uint8_t gv[8], fv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            int R, G, B;
+            ycc_rgb(yr[j], up[0][j], up[1][j], R, G, B);
+            if (kRGB) {
+                if (x0 + j < w) {
+                    uint8_t* o = rgb + (int64_t)y * rgb_pitch + 3 * (x0 + j);
+                    o[0] = (uint8_t)R;
+                    o[1] = (uint8_t)G;
+                    o[2] = (uint8_t)B;
+                }
+            } else {
+                int nb = 0;
+                cd_pixel(R, G, B, od, k, gv[j], fv[j], nb);
+                if (x0 + j < w) nbg += nb;
+            }
+        }
+        if (!kRGB) {
+            const int64_t o = (int64_t)y * w + x0;
+            if (vec8) {
+                uint2 gw, fw;
+                gw.x = gv[0] | gv[1] << 8 | gv[2] << 16 | (uint32_t)gv[3] << 24;
+                gw.y = gv[4] | gv[5] << 8 | gv[6] << 16 | (uint32_t)gv[7] << 24;
+                fw.x = fv[0] | fv[1] << 8 | fv[2] << 16 | (uint32_t)fv[3] << 24;
+                fw.y = fv[4] | fv[5] << 8 | fv[6] << 16 | (uint32_t)fv[7] << 24;
+                *reinterpret_cast<uint2*>(g + o) = gw;
+                *reinterpret_cast<uint2*>(flags + o) = fw;
+            } else {
+                for (int j = 0; j < 8 && x0 + j < w; ++j) {
+                    g[o + j] = gv[j];
+                    flags[o + j] = fv[j];
+                }
+            }
+        }
+    }
     if (!kRGB && bg_count) block_count(nbg, bg_count);
 }
 
 }  // namespace
 
-void launch_jpeg_decode(const JpegHdr* hdr, const uint8_t* file, int64_t file_cap, int w, int h, int32_t* starts,
-                        int32_t* blkcnt, const float* lut, const hp_params& p, uint8_t* g, uint8_t* flags,
-                        unsigned long long* bg_count, uint8_t* rgb, int64_t rgb_pitch, int32_t* err,
-                        cudaStream_t s) {
+void launch_jpeg_decode(const JpegHdr* hdr, int sub, const uint8_t* file, int64_t file_cap, int w, int h,
+                        int32_t* starts, int32_t* blkcnt, uint8_t* planes, const float* lut, const hp_params& p,
+                        uint8_t* g, uint8_t* flags, unsigned long long* bg_count, uint8_t* rgb, int64_t rgb_pitch,
+                        int32_t* err, cudaStream_t s) {
     if (bg_count) cudaMemsetAsync(bg_count, 0, sizeof(unsigned long long), s);
     const int nsm = num_sms();
     const int64_t nch = file_cap / kChunk + 1;
@@ -591,19 +703,33 @@ void launch_jpeg_decode(const JpegHdr* hdr, const uint8_t* file, int64_t file_ca
     const size_t dyn = 64 * kDT * sizeof(int) + 2 * 64 * kDT;
     static PerDevice once;
     once.get([&] {
-        cudaFuncSetAttribute(k_jpeg_decode<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        cudaFuncSetAttribute(k_jpeg_decode<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k_jpeg_decode<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k_jpeg_decode<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k_jpeg_decode<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         return 0;
     });
-    const int64_t nint_max = ((int64_t)((w + 7) / 8) * ((h + 7) / 8));
+    const int mpx = 8 * sub;
+    const int64_t nint_max = ((int64_t)((w + mpx - 1) / mpx) * ((h + mpx - 1) / mpx));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nint_max + kDT - 1) / kDT, nsm * 2));
     const CdConst k = cd_const(p);
+    if (sub == 2) {
+        (note_launch(), k_jpeg_decode<2><<<grid, kDT, dyn, s>>>(hdr, file, starts, lut, k, nullptr, nullptr, nullptr,
+                                                               nullptr, 0, planes, err));
+        const int64_t ng = (int64_t)((w + 7) / 8) * h;
+        const int ug = (int)std::max<int64_t>(1, std::min<int64_t>((ng + 255) / 256, nsm * 8));
+        if (rgb)
+            (note_launch(), k_jpeg_up_cd<true><<<ug, 256, 0, s>>>(hdr, planes, lut, k, nullptr, nullptr, nullptr, rgb,
+                                                                rgb_pitch));
+        else
+            (note_launch(), k_jpeg_up_cd<false><<<ug, 256, 0, s>>>(hdr, planes, lut, k, g, flags, bg_count, nullptr, 0));
+        return;
+    }
     if (rgb)
-        (note_launch(), k_jpeg_decode<true><<<grid, kDT, dyn, s>>>(hdr, file, starts, lut, k, g, flags, nullptr, rgb,
-                                                                  rgb_pitch, err));
+        (note_launch(), k_jpeg_decode<1><<<grid, kDT, dyn, s>>>(hdr, file, starts, lut, k, g, flags, nullptr, rgb,
+                                                               rgb_pitch, nullptr, err));
     else
-        (note_launch(), k_jpeg_decode<false><<<grid, kDT, dyn, s>>>(hdr, file, starts, lut, k, g, flags, bg_count,
-                                                                   nullptr, 0, err));
+        (note_launch(), k_jpeg_decode<0><<<grid, kDT, dyn, s>>>(hdr, file, starts, lut, k, g, flags, bg_count,
+                                                               nullptr, 0, nullptr, err));
 }
 
 }  // namespace hp

@@ -41,6 +41,18 @@ def test_decode_tiles(ctx, shape, q, rst):
     assert np.array_equal(_decode(ctx, buf, *shape), oracle.jpeg_decode(buf))
 
 
+@pytest.mark.parametrize("shape,q,rst", [((64, 64), 90, 4), ((37, 53), 75, 1), ((300, 257), 95, 0),
+                                         ((512, 512), 90, 4), ((1, 300), 90, 2), ((301, 1), 85, 3),
+                                         ((2, 2), 90, 1), ((9, 3), 90, 1), ((7, 4), 90, 2), ((5, 5), 90, 1),
+                                         ((17, 33), 60, 2), ((2, 300), 90, 1), ((1000, 1016), 90, 16)])
+def test_decode_tiles_420(ctx, shape, q, rst):
+    """4:2:0: the decode kernel writes component planes, the upsampling kernel applies reading
+    J4's triangle filter (replication for chroma <= 2 samples wide) -- bit-exact with the oracle."""
+    rgb = make_tile(sum(shape) + q + 7, TileSpec(*shape))["rgb"]
+    buf = encode_tile(rgb, q, rst, sampling="420")
+    assert np.array_equal(_decode(ctx, buf, *shape), oracle.jpeg_decode(buf))
+
+
 @pytest.mark.parametrize("kind", ["noise", "checker", "flat"])
 @pytest.mark.parametrize("q", [60, 100])
 def test_decode_hard_images(ctx, kind, q):
@@ -64,9 +76,9 @@ def _tables(cap):
             torch.zeros((cap, 36), dtype=torch.float32, device="cuda"), torch.zeros(1, dtype=torch.int32, device="cuda"))
 
 
-def _check_tile_jpeg(ctx, rgb, q=90, rst=4):
+def _check_tile_jpeg(ctx, rgb, q=90, rst=4, sampling="444"):
     import torch
-    buf = encode_tile(rgb, q, rst)
+    buf = encode_tile(rgb, q, rst, sampling=sampling)
     dec = oracle.jpeg_decode(buf)
     h, w = rgb.shape[:2]
     cap = 65536
@@ -92,6 +104,16 @@ def test_process_tile_jpeg_config1(ctx):
 @pytest.mark.parametrize("seed,shape,rst", [(41, (300, 404), 3), (42, (257, 129), 0), (43, (512, 384), 1)])
 def test_process_tile_jpeg_ragged(ctx, seed, shape, rst):
     _check_tile_jpeg(ctx, make_tile(seed, TileSpec(*shape))["rgb"], 85, rst)
+
+
+@pytest.mark.parametrize("seed,shape,rst", [(44, (300, 404), 2), (45, (257, 129), 0)])
+def test_process_tile_jpeg_420(ctx, seed, shape, rst):
+    _check_tile_jpeg(ctx, make_tile(seed, TileSpec(*shape))["rgb"], 85, rst, sampling="420")
+
+
+@pytest.mark.slow
+def test_process_tile_jpeg_config2_420(ctx):
+    assert _check_tile_jpeg(ctx, make_config_tile(2), sampling="420") > 1000
 
 
 @pytest.mark.slow
@@ -126,7 +148,7 @@ def test_corrupt_and_unsupported_files(ctx):
         _decode(ctx, _corrupt_codes(buf), 128, 128)
     assert e.value.status == 1
     with pytest.raises(HPError) as e:
-        _decode(ctx, encode_tile(rgb, 90, 2, sampling="420"), 128, 128)
+        _decode(ctx, encode_tile(rgb, 90, 2, sampling="422"), 128, 128)
     assert e.value.status == 5
     with pytest.raises(HPError) as e:
         _decode(ctx, encode_tile(rgb, 90, 0, progressive=True), 128, 128)
@@ -140,14 +162,16 @@ def test_corrupt_and_unsupported_files(ctx):
 
 def test_run_tiles_jpeg(ctx):
     """hp_run_tiles_jpeg with per-slot graphs: 10 files over 4 slots (each slot captures and
-    replays), two of them bad -- the bad ones come back with a nonzero status and no rows,
+    replays), 4:4:4 and 4:2:0 files mixed (a slot rebuilds its graph when the sampling
+    changes), two of them bad -- the bad ones come back with a nonzero status and no rows,
     every other table equals the oracle's on the decoded tile."""
     import torch
     h, w = 256, 384
     tiles = [make_tile(900 + i, TileSpec(h, w))["rgb"] for i in range(4)]
-    bufs = [torch.from_numpy(encode_tile(t, 90, 4)).pin_memory() for t in tiles]
+    bufs = [torch.from_numpy(encode_tile(t, 90, 4, sampling="420" if i == 2 else "444")).pin_memory()
+            for i, t in enumerate(tiles)]
     bad = {3: torch.from_numpy(_corrupt_rst(bufs[1].numpy())).pin_memory(),
-           7: torch.from_numpy(encode_tile(tiles[2], 90, 4, sampling="420")).pin_memory()}
+           7: torch.from_numpy(encode_tile(tiles[2], 90, 4, sampling="422")).pin_memory()}
     ref = [oracle.process_tile(oracle.jpeg_decode(b.numpy()))[1:] for b in bufs]
     order = iter(range(10))
     got = {}
