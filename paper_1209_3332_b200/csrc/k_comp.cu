@@ -218,7 +218,71 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
     // step from q toward p lands in that disk, so q is 8-adjacent to the component: every
     // nearest background pixel is an in-tile non-member of the window touching a member.  No
     // such pixel = the component is the whole tile = no background: +inf.
-    {
+    if constexpr (St::kKO == CompGm::kKO) {
+        // windows too big for shared memory (a big component under non-default area bounds):
+        // the brute force below is O(members x boundary); use an exact separable EDT of the
+        // window instead (Meijster: per column the distance to the nearest background pixel,
+        // then per row the lower envelope of (x - i)^2 + g(i)^2 with integer separators).
+        // The window holds every nearest background pixel (see above), so the result is the
+        // same integer d2.  Background = in-tile non-member window pixels.
+        const int INF = WX + WY;  // larger than any in-window distance
+        int32_t* g = S.B;         // column distances
+        int32_t* sv = S.C;        // per row: envelope indices
+        int32_t* tv = reinterpret_cast<int32_t*>(S.A);  // per row: envelope starts
+        int anybg = 0;
+        for (int x = tr; x < WX; x += TS) {
+            int d = INF;
+            for (int y = 0; y < WY; ++y) {
+                const int li = y * WX + x;
+                if (!S.mem[li] && S.pm[li]) { d = 0; anybg = 1; }
+                else if (d < INF) ++d;
+                g[li] = d;
+            }
+            d = INF;
+            for (int y = WY - 1; y >= 0; --y) {
+                const int li = y * WX + x;
+                if (g[li] == 0) d = 0;
+                else if (d < INF) ++d;
+                if (d < g[li]) g[li] = d;
+            }
+        }
+        anybg = team.reduce(anybg, red.i, OpMax());
+        team.sync();
+        for (int y = tr; y < WY; y += TS) {
+            int32_t* srow = sv + y * WX;
+            int32_t* trow = tv + y * WX;
+            const int32_t* grow = g + y * WX;
+            auto f = [&](int x, int i) { return (int64_t)(x - i) * (x - i) + (int64_t)grow[i] * grow[i]; };
+            auto sep = [&](int i, int u) {
+                return (int)(((int64_t)u * u - (int64_t)i * i + (int64_t)grow[u] * grow[u] - (int64_t)grow[i] * grow[i]) /
+                             (2 * (int64_t)(u - i)));
+            };
+            int q = 0;
+            srow[0] = 0;
+            trow[0] = 0;
+            for (int u = 1; u < WX; ++u) {
+                while (q >= 0 && f(trow[q], srow[q]) > f(trow[q], u)) --q;
+                if (q < 0) {
+                    q = 0;
+                    srow[0] = u;
+                } else {
+                    const int wv = 1 + sep(srow[q], u);
+                    if (wv < WX) {
+                        ++q;
+                        srow[q] = u;
+                        trow[q] = wv;
+                    }
+                }
+            }
+            for (int u = WX - 1; u >= 0; --u) {
+                const int li = y * WX + u;
+                if (S.mem[li])
+                    S.dist[li] = anybg ? __fsqrt_rn(__uint2float_rn((uint32_t)f(u, srow[q]))) : INFINITY;
+                if (u == trow[q]) --q;
+            }
+        }
+        team.sync();
+    } else {
         int nb = 0;
         int32_t* bl = S.C;  // boundary pixels, (ly << 16) | lx
         for (int base = 0; base < NWIN; base += TS) {

@@ -950,3 +950,38 @@ def test_pipeline_ragged_and_max_width(hw):
     olab, ol, of, ot = oracle.process_tile(rgb)
     assert np.array_equal(lab, olab) and nobj == len(ol) > 0
     assert_features_equal(gl, gf, gt, ol, of, ot)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_components_big_windows_separable_edt(seed):
+    """Components whose windows exceed shared memory (> 2432 px) take the global-memory path,
+    whose S7 is the separable exact EDT (k_comp.cu); with area bounds up to 131072 the big
+    objects survive S10, so their EDT -> markers -> watershed -> labels -> features are all
+    observable: bit-exact labels, features within C18 (oracle chain on the same F)."""
+    import torch
+    from paper_1209_3332_b200 import Context
+    from paper_1209_3332_b200.hp import Params as HParams
+    rng = np.random.default_rng(seed)
+    h, w = 300, 360
+    yy, xx = np.indices((h, w))
+    F = np.zeros((h, w), bool)
+    for _ in range(4):  # overlapping big blobs (watershed splits) with notches and holes filled
+        cy, cx, a, b = rng.uniform(60, 240), rng.uniform(60, 300), rng.uniform(25, 60), rng.uniform(25, 60)
+        F |= ((yy - cy) / a) ** 2 + ((xx - cx) / b) ** 2 <= 1.0
+    F &= rng.random((h, w)) > 0.002  # pinholes, filled again below: S6 output has no holes
+    F = oracle.fill_holes(F.astype(U8))
+    g = rng.integers(0, 256, size=(h, w)).astype(U8)
+    p = oracle.default_params()
+    p.obj_max_area = p.cand_max_area = 131072
+    d2, dist = oracle.edt(F)
+    ML, _, _ = oracle.markers(dist, F, 1.0)
+    split, _, _, _ = oracle.watershed(dist, ML, F)
+    labels, nobj = oracle.bwlabel(split, p.obj_min_area, p.obj_max_area)
+    assert nobj >= 1 and np.bincount(labels[labels > 0]).max() > 2432
+    ol, of, ot = oracle.features(labels, g)
+    cap = 4096
+    with Context(0, w, h, n_slots=1, max_objects=cap, params=HParams.from_dict(p.to_dict())) as c:
+        lab, nob, lf, ft = stage(c, "COMPONENTS", [F, g], [((h, w), I32), ((1,), I32), ((2, cap), I32),
+                                                          ((cap, 36), F32)], w, h)
+    assert np.array_equal(lab, labels) and int(nob[0]) == nobj
+    assert_features_equal(lf[0, :nobj], lf[1, :nobj], ft[:nobj], ol, of, ot)
