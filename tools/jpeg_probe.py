@@ -54,6 +54,19 @@ def main():
     # the JPEG loss does to the later steps
     dec = out.clone()
     res["process_tile_on_decoded_ms"] = timed(lambda: ctx.process_tile(0, dec, lab, nob, tl, tf, tt, nr))
+    # per-stage times (S1..S11 events) of the raw and the decoded tile, and their object counts
+    names = ["S1", "S2", "S3", "S4", "S5", "S6", "S7", "S8-S11+Canny", "-", "-", "-"]
+    for tag, t in (("raw", dev), ("decoded", dec)):
+        ctx.set_stage_timing(True)
+        per = []
+        for _ in range(5):
+            ctx.process_tile(0, t, lab, nob, tl, tf, tt, nr)
+            torch.cuda.synchronize()
+            per.append(ctx.stage_times(0))
+        ctx.set_stage_timing(False)
+        med = [sorted(p[i] for p in per)[2] for i in range(11)]
+        res[f"stages_{tag}_ms"] = {names[i]: round(med[i], 4) for i in range(8)}
+        res[f"objects_{tag}"] = int(nob.item())
     res["decoded_equals_raw_within"] = int((out.cpu().numpy().astype(int) - rgb).__abs__().max())
     print(json.dumps(res))
     ctx.close()
