@@ -67,3 +67,7 @@ def test_hp_arm_line():
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 4 * 3 * 1024 * 1024
     assert d["e2e"]["d2h_bytes_per_step"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    j = d["e2e"]["jpeg"]  # NEXT-3 leg: JPEG files through hp_run_tiles_jpeg
+    assert j["value"] > 0 and 0 < j["h2d_bytes_per_step"] < 4 * 3 * 1024 * 1024
+    assert all({"ms_isolated", "ms_in_situ", "alg_bytes_per_tile"} <= set(p) for p in d["per_stage"])
+    assert d["per_stage"][-1]["alg_bytes_per_tile"] == 34 * 1024 * 1024  # S7-S11 at 34 B/px
