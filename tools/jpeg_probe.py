@@ -49,9 +49,16 @@ def main():
     res["rows_equal"] = int(nr.item()) == n_raw
     res["decode_err"] = int(err.item())
     res["decode_jpeg_ms_incl_sync"] = timed(lambda: ctx.decode_jpeg(0, buf, out))
+    # the same tile as 4:2:0 (decode to planes + upsampling / colour / S1 kernel)
+    b420 = torch.from_numpy(encode_tile(rgb, 90, 4, sampling="420")).pin_memory()
+    res["jpeg420_bytes"] = int(b420.numel())
+    res["process_tile_jpeg420_ms"] = timed(lambda: ctx.process_tile_jpeg(0, b420, lab, nob, tl, tf, tt, nr,
+                                                                        decode_err=err))
+    res["decode_jpeg420_ms_incl_sync"] = timed(lambda: ctx.decode_jpeg(0, b420, out))
     # the same pipeline on the decoded RGB tile already on the device: the difference to
     # process_tile_jpeg is the ingest (copy + decode), the difference to process_tile is what
     # the JPEG loss does to the later steps
+    ctx.decode_jpeg(0, buf, out)
     dec = out.clone()
     res["process_tile_on_decoded_ms"] = timed(lambda: ctx.process_tile(0, dec, lab, nob, tl, tf, tt, nr))
     # per-stage times (S1..S11 events) of the raw and the decoded tile, and their object counts
