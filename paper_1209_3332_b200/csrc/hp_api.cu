@@ -465,7 +465,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.stg_feat = (float*)A(4 * (size_t)mo * HP_NFEAT);
         s.rgb_dev = (uint8_t*)A(3 * N);
         s.jhdr_dev = (JpegHdr*)A(sizeof(JpegHdr));
-        s.jstarts = (int32_t*)A(4 * (size_t)jpeg_max_intervals(N));
+        s.jstarts = (int32_t*)A(4 * (size_t)jpeg_max_intervals(cfg->max_width, cfg->max_height));
         s.jblk = (int32_t*)A(4 * (size_t)(3 * N / 8192 + 2));
         s.jerr = (int32_t*)A(16);
         s.jplanes = (uint8_t*)A((size_t)jpeg_planes_bytes(cfg->max_width, cfg->max_height));

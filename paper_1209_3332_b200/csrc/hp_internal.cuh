@@ -186,7 +186,8 @@ void upload_od_lut(float* lut_dev, cudaStream_t s);
 // malformed stream; *why gets the reason.
 hp_status jpeg_parse(const uint8_t* data, int64_t n, JpegHdr* out, const char** why);
 // Capacity of the per-slot restart-interval offset array for a tile of npx pixels.
-inline int64_t jpeg_max_intervals(int64_t npx) { return npx / 64 + 64; }
+// (at most one interval per 8 x 8 MCU of the largest tile; 4:2:0 MCUs are larger)
+inline int64_t jpeg_max_intervals(int w, int h) { return (int64_t)((w + 7) / 8) * ((h + 7) / 8) + 1; }
 // Decode the file (device copy `file`, header `hdr` on the device) of a w x h tile; sub is
 // the host-parsed sampling (1: 4:4:4, 2: 4:2:0).  rgb == nullptr: S1 fused (g, flags,
 // bg_count as launch_cd); else the decoded RGB tile (pitch rgb_pitch) only -- the

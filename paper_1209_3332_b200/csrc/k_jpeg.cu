@@ -699,7 +699,7 @@ void launch_jpeg_decode(const JpegHdr* hdr, int sub, const uint8_t* file, int64_
     const int64_t nch = file_cap / kChunk + 1;
     const int gs = (int)std::min<int64_t>(nch, nsm * 4);
     (note_launch(), k_rst_count<<<gs, 256, 0, s>>>(hdr, file, blkcnt));
-    (note_launch(), k_rst_write<<<gs, 256, 0, s>>>(hdr, file, blkcnt, starts, jpeg_max_intervals((int64_t)w * h), err));
+    (note_launch(), k_rst_write<<<gs, 256, 0, s>>>(hdr, file, blkcnt, starts, jpeg_max_intervals(w, h), err));
     const size_t dyn = 64 * kDT * sizeof(int) + 2 * 64 * kDT;
     static PerDevice once;
     once.get([&] {
