@@ -1,6 +1,8 @@
 """Determinism / race stress: the bench's tiles processed REPS times each with S slots in
 flight (as in bench.py); every run's labels + feature table must be bit-identical to the first
-run of that tile.  usage: python tools/stress_determinism.py [REPS] [SLOTS]"""
+run of that tile.  With "jpeg" the tiles are first passed through a quality-90 JPEG round trip
+(smoother images: longer S4 propagation, more regions on the alternating-phase closure).
+usage: python tools/stress_determinism.py [REPS] [SLOTS] [jpeg]"""
 import hashlib
 import json
 import os
@@ -17,6 +19,10 @@ def main():
     reps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
     S = int(sys.argv[2]) if len(sys.argv) > 2 else 6
     tiles = [make_tile(1000 + i, TileSpec())["rgb"] for i in range(12)]
+    if len(sys.argv) > 3 and sys.argv[3] == "jpeg":
+        import cv2
+        from synth.jpeg import encode_tile
+        tiles = [np.ascontiguousarray(cv2.imdecode(encode_tile(t), cv2.IMREAD_COLOR)[:, :, ::-1]) for t in tiles]
     dev = [torch.from_numpy(t).cuda() for t in tiles]
     size, cap = 4096, 16384
     ctx = Context(0, size, size, n_slots=S, max_objects=cap)
@@ -46,7 +52,8 @@ def main():
                 elif ref[i] != d:
                     bad += 1
                     print(f"MISMATCH tile {i} rep {r}", flush=True)
-    print(json.dumps({"runs": runs, "mismatches": bad, "tiles": len(tiles), "slots": S}), flush=True)
+    print(json.dumps({"runs": runs, "mismatches": bad, "tiles": len(tiles), "slots": S,
+                      "input": sys.argv[3] if len(sys.argv) > 3 else "raw"}), flush=True)
     ctx.close()
     return 1 if bad else 0
 
