@@ -195,3 +195,57 @@ def test_run_tiles_jpeg(ctx):
         assert st == 0
         ol, of, ot = ref[tid % 4]
         assert_features_equal(l, f, ft, ol, of, ot)
+
+
+def _oracle_jpeg_rows(buf):
+    return oracle.process_tile(oracle.jpeg_decode(buf))[1:]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("sampling", ["444", "420"])
+def test_bench_jpeg_e2e_launch_config(sampling):
+    """bench.py's e2e.jpeg leg in its exact configuration at full size: the bench's 12 4K tiles
+    as quality-90 JPEG files (restart interval 4), hp_run_tiles_jpeg on 14 slots with per-slot
+    graphs, 32 hardware queues, the files twice each from a demand-driven queue -- every
+    delivered table equals the oracle's on the oracle's decode of the same file."""
+    import multiprocessing as mp
+    import os
+
+    import torch
+    from paper_1209_3332_b200 import Context
+    from paper_1209_3332_b200.dist import DistTileSource, TileQueue
+    from tests.test_gpu_parity import BENCH_BATCH, BENCH_E2E_SLOTS, BENCH_SLOTS, _pool_tile
+    K = BENCH_BATCH
+    with mp.get_context("fork").Pool(max(1, min(K, os.cpu_count() or 1))) as pool:
+        tiles = pool.map(_pool_tile, range(1000, 1000 + K))
+        bufs = [encode_tile(t, 90, 4, sampling=sampling) for t in tiles]
+        ref = pool.map(_oracle_jpeg_rows, bufs)
+    c = Context(0, 4096, 4096, n_slots=max(BENCH_SLOTS, BENCH_E2E_SLOTS), max_objects=8192)
+    try:
+        pinned = [torch.from_numpy(b).pin_memory() for b in bufs]
+        q = TileQueue(2 * K, block=BENCH_SLOTS, store=None)
+        ids = iter(())
+        got = {}
+
+        def nxt():
+            nonlocal ids
+            while True:
+                tid = next(ids, None)
+                if tid is not None:
+                    b = pinned[tid % K]
+                    return b.data_ptr(), b.numel(), tid
+                blk = q.grab()
+                if blk is None:
+                    return None
+                ids = iter(blk)
+
+        def done(tid, l, f, ft, st):
+            assert st == 0, f"tile {tid} status {st}"
+            got[tid] = (l, f, ft)
+
+        c.run_tiles_jpeg(nxt, done, 4096, 4096)
+        assert sorted(got) == list(range(2 * K))
+        for tid, (l, f, ft) in got.items():
+            assert_features_equal(l, f, ft, *ref[tid % K])
+    finally:
+        c.close()
