@@ -76,6 +76,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #define HP_RG_CHAIN 8  // ... and only from a region's HP_RG_CHAIN-th job on (a long chain).  r2: config 5
                        // serpentine 787 -> 422 ms, spiral 2348 -> 841 ms; config 2 and bench unchanged
 #endif
+#ifndef HP_RG_FIRSTROW
+#define HP_RG_FIRSTROW 0  // first jobs: a full-width row pass before the sub-tile sweeps
+#endif
 #ifndef HP_RG_INIT
 #define HP_RG_INIT 0  // raster + anti-raster initialisation sweep per region before the queue engine
 #endif
@@ -487,6 +490,7 @@ struct Smem {
     int first;  // HP_RG_FIRSTORDER: this job is the region's first
     int thin;   // HP_RG_THIN: this job's few dirty rows go to the alternating-phase closure
     int visits; // earlier jobs of this region in this launch
+    int allrows; // every sub-tile row of the job is dirty (a region's first job)
     uint32_t rowdirty[AROWS / 32], coldirty[ACOLS / 32], rowsnap[AROWS / 32], colsnap[ACOLS / 32];
     uint32_t subchg[NW];
 };
@@ -759,6 +763,7 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                     }
                     S.pend = np;
                     S.thin = nbits <= thin_rows && S.visits >= chain_visits;
+                    S.allrows = nbits == NW * 32;  // a region's first job: every row dirty
 #if HP_RG_PROFILE
                     S.tA = gtimer();
 #endif
@@ -776,6 +781,24 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                 int nrows = 0;
                 const int r = wr0 + lane + 1;
                 unsigned backoff = HP_POLL_NS;
+#if HP_RG_FIRSTROW
+                if (!S.thin && S.allrows) {
+                    // first job: one full-width closure of every region row (8 px per lane)
+                    // before the sub-tile sweeps, so values cross the sub-tile borders along
+                    // the rows at once; its changed rows join the write-back
+                    if (lane == 0) S.subchg[warp] = 0;
+                    __syncthreads();
+                    for (int y = 1 + warp; y <= AROWS; y += NW) {
+                        const uint32_t chg = adi_row_close(sR, sRw, sM, y, lane);
+                        constexpr int LPS = SW / PXL;
+                        const unsigned lanes = __ballot_sync(FULL, chg != 0);
+                        if ((lane % LPS) == 0 && ((lanes >> lane) & (uint32_t)((1ull << LPS) - 1)))
+                            atomicOr(&S.subchg[((y - 1) >> 5) * RX + lane / LPS], 1u << ((y - 1) & 31));
+                    }
+                    __syncthreads();
+                    mychg = S.subchg[warp];
+                }
+#endif
                 if (S.thin) {
                     // a thin job (a few dirty rows, e.g. a wave front crossing the region
                     // along a corridor): alternating full-width row / full-height column
