@@ -248,8 +248,10 @@ def gather_rows_device(rows: DeviceRows, device=None, stats: dict | None = None)
             parts.append(part)
         for w in (dist.batch_isend_irecv(ops) if ops else []):
             w.wait()
+    on_gpu = torch.device(dev).type == "cuda"
     if stats is not None:
-        torch.cuda.synchronize(dev) if torch.device(dev).type == "cuda" else None
+        if on_gpu:
+            torch.cuda.synchronize(dev)
         stats["transfer_s"] = time.perf_counter() - t0
         stats["received_bytes"] = sum(len(p) for p in parts[1:]) * ROW_BYTES
     t1 = time.perf_counter()
@@ -258,7 +260,8 @@ def gather_rows_device(rows: DeviceRows, device=None, stats: dict | None = None)
     out = DeviceRows(tile[order], torch.cat([p.label for p in parts])[order],
                      torch.cat([p.flags for p in parts])[order], torch.cat([p.feat for p in parts])[order])
     if stats is not None:
-        torch.cuda.synchronize(dev) if torch.device(dev).type == "cuda" else None
+        if on_gpu:
+            torch.cuda.synchronize(dev)
         stats["merge_s"] = time.perf_counter() - t1
     return out
 

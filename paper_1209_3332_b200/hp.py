@@ -375,17 +375,21 @@ class Context:
 
     @staticmethod
     def _host_buf(jpeg):
-        """(pointer, nbytes) of a host JPEG buffer: a numpy u8 array or a (pinned) CPU tensor."""
+        """(pointer, nbytes, owner) of a host JPEG buffer: a numpy u8 array or a (pinned) CPU
+        tensor; the caller keeps `owner` alive across the call (a contiguous copy of a strided
+        array lives only there)."""
         if hasattr(jpeg, "data_ptr"):
-            return jpeg.data_ptr(), jpeg.numel() * jpeg.element_size()
+            if not jpeg.is_contiguous():
+                jpeg = jpeg.contiguous()
+            return jpeg.data_ptr(), jpeg.numel() * jpeg.element_size(), jpeg
         a = np.ascontiguousarray(jpeg, dtype=np.uint8)
-        return a.ctypes.data, a.nbytes
+        return a.ctypes.data, a.nbytes, a
 
     def process_tile_jpeg(self, slot, jpeg, labels, n_objects, t_label, t_flags, t_feat, n_rows,
                           decode_err=None, stream=None):
         """hp_process_tile_jpeg: one JPEG tile (host bytes, kept alive until the stream is
         done) through both stages; decode_err: optional device int32 tensor."""
-        ptr, nb = self._host_buf(jpeg)
+        ptr, nb, _owner = self._host_buf(jpeg)
         lab = Labels(labels.data_ptr(), labels.stride(0), n_objects.data_ptr())
         tab = FeatureTable(t_label.data_ptr(), t_flags.data_ptr(), t_feat.data_ptr(),
                            t_label.shape[0], n_rows.data_ptr())
@@ -395,7 +399,7 @@ class Context:
 
     def decode_jpeg(self, slot, jpeg, rgb_out, stream=None):
         """hp_decode_jpeg: decoded RGB into the device tensor rgb_out [H, W, 3] (synchronises)."""
-        ptr, nb = self._host_buf(jpeg)
+        ptr, nb, _owner = self._host_buf(jpeg)
         self._chk(lib().hp_decode_jpeg(self._h, slot, C.c_void_p(ptr), nb, C.c_void_p(rgb_out.data_ptr()),
                                        rgb_out.stride(0) * rgb_out.element_size(), _stream(stream)),
                   "hp_decode_jpeg")
