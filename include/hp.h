@@ -225,6 +225,12 @@ hp_status hp_run_tiles_jpeg(hp_ctx* ctx, const hp_jpeg_source* src, const hp_res
 hp_status hp_process_tile_jpeg(hp_ctx* ctx, int32_t slot, const uint8_t* host_jpeg, int64_t nbytes,
                                hp_labels* lab, hp_feature_table* out, int32_t* decode_err_dev,
                                hp_stream s);
+/* Host-only header probe (no context, no GPU): the frame size, sampling (444 or 420), the
+ * restart interval in MCUs (0 = none) and the number of restart intervals of a JPEG file, or
+ * HP_ERR_UNSUPPORTED / HP_ERR_INVALID as the JPEG calls would report it.  sampling,
+ * restart_interval and n_intervals may be NULL. */
+hp_status hp_jpeg_info(const uint8_t* host_jpeg, int64_t nbytes, int32_t* width, int32_t* height,
+                       int32_t* sampling, int32_t* restart_interval, int32_t* n_intervals);
 /* Verification entry of the decoder alone: the decoded RGB tile (DEVICE rgb_dev, u8 R,G,B
  * interleaved, pitch_bytes >= 3*width).  Synchronises s; a corrupt scan -> HP_ERR_INVALID. */
 hp_status hp_decode_jpeg(hp_ctx* ctx, int32_t slot, const uint8_t* host_jpeg, int64_t nbytes,

@@ -594,6 +594,21 @@ hp_status hp_process_tile_jpeg(hp_ctx* ctx, int32_t slot, const uint8_t* host_jp
     return st ? st : check_launch(ctx, "process_tile_jpeg");
 }
 
+hp_status hp_jpeg_info(const uint8_t* host_jpeg, int64_t nbytes, int32_t* width, int32_t* height, int32_t* sampling,
+                       int32_t* restart_interval, int32_t* n_intervals) {
+    if (!host_jpeg || !width || !height) return HP_ERR_INVALID;
+    JpegHdr H;
+    const char* why = "";
+    const hp_status st = jpeg_parse(host_jpeg, nbytes, &H, &why);
+    if (st) return st;
+    *width = H.width;
+    *height = H.height;
+    if (sampling) *sampling = H.sub == 2 ? 420 : 444;
+    if (restart_interval) *restart_interval = H.n_intervals > 1 ? H.ri : 0;
+    if (n_intervals) *n_intervals = H.n_intervals;
+    return HP_OK;
+}
+
 hp_status hp_decode_jpeg(hp_ctx* ctx, int32_t slot, const uint8_t* host_jpeg, int64_t nbytes, uint8_t* rgb_dev,
                          int64_t pitch_bytes, hp_stream s) {
     hp_status st = enter(ctx, slot);

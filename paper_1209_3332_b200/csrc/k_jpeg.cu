@@ -64,11 +64,12 @@ hp_status jpeg_parse(const uint8_t* d, int64_t n, JpegHdr* H, const char** why) 
                 break;
             case 0xC0:
             case 0xC1:  // baseline / extended sequential, Huffman
-                if (sl < 15) return bad("SOF");
+                if (sl < 6) return bad("SOF");
                 if (s[0] != 8) return unsup("sample precision other than 8 bits");
                 H->height = be16(s + 1);
                 H->width = be16(s + 3);
                 if (s[5] != 3) return unsup("component count other than 3");
+                if (sl < 15) return bad("SOF");
                 for (int i = 0; i < 3; ++i) {
                     cid[i] = s[6 + 3 * i];
                     // 4:4:4, or 4:2:0 (Y 2 x 2, chroma 1 x 1); reading J3

@@ -41,7 +41,20 @@ EXPORTS = ["hp_default_params", "hp_ctx_create", "hp_ctx_destroy", "hp_status_st
            "hp_process_tile", "hp_run_tiles", "hp_stage_run", "hp_set_stage_timing",
            "hp_get_stage_times", "hp_stage_times_accum", "hp_launch_count", "hp_reduce_rows",
            "hp_group_center", "hp_group_std", "hp_run_tiles_jpeg", "hp_process_tile_jpeg",
-           "hp_decode_jpeg"]
+           "hp_decode_jpeg", "hp_jpeg_info"]
+
+
+def jpeg_info(jpeg):
+    """hp_jpeg_info (host only): {'width', 'height', 'sampling' (444 / 420), 'restart_interval'
+    (MCUs, 0 = none), 'n_intervals'} of a JPEG file; raises HPError (status 5 = outside the
+    decoder's scope, 1 = malformed)."""
+    a = np.ascontiguousarray(np.frombuffer(bytes(jpeg), np.uint8) if isinstance(jpeg, (bytes, bytearray))
+                             else jpeg, dtype=np.uint8)
+    v = [C.c_int32() for _ in range(5)]
+    st = lib().hp_jpeg_info(a.ctypes.data_as(C.c_void_p), a.nbytes, *[C.byref(x) for x in v])
+    if st != 0:
+        raise HPError(st, "hp_jpeg_info")
+    return dict(zip(["width", "height", "sampling", "restart_interval", "n_intervals"], [x.value for x in v]))
 
 
 class HPError(RuntimeError):
@@ -165,6 +178,7 @@ def lib():
             "hp_process_tile_jpeg": (C.c_int, [P, i32, P, C.c_int64, C.POINTER(Labels), C.POINTER(FeatureTable),
                                                P, P]),
             "hp_decode_jpeg": (C.c_int, [P, i32, P, C.c_int64, P, C.c_int64, P]),
+            "hp_jpeg_info": (C.c_int, [P, C.c_int64, P, P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
