@@ -369,9 +369,9 @@ __device__ __forceinline__ uint32_t adi_col_close(const uint8_t* sR, uint8_t* sR
 // One region closure by alternating phases (see k_region_adi); S holds the window and the
 // rowdirty / coldirty / rowsnap / colsnap / subchg words (rowdirty seeded by the caller, the
 // rest zero).  On return S.subchg[k] = the rows of sub-tile k that changed.
-template <class SM>
+template <class SM, class Ensure>
 __device__ void adi_close_region(SM& S, const uint8_t* sR, uint8_t* sRw, const uint8_t* sM, int warp, int lane,
-                                 int& phases, int& lines) {
+                                 int& phases, int& lines, Ensure ensure_full) {
     auto improves = [&](int pr, int pc, int qr, int qc) {
         return min((int)sR[bidx(pr, pc)], (int)sM[bidx(qr, qc)]) > (int)sR[bidx(qr, qc)];
     };
@@ -430,6 +430,7 @@ __device__ void adi_close_region(SM& S, const uint8_t* sR, uint8_t* sRw, const u
         int anyc = 0;
 #pragma unroll
         for (int k = 0; k < ACOLS / 32; ++k) anyc |= S.colsnap[k] != 0;
+        if (anyc) ensure_full();  // a column closure reads whole window columns
         if (anyc) {
             ++phases;
             for (int c = 1 + warp; c <= ACOLS; c += NW) {
@@ -491,6 +492,7 @@ struct Smem {
     int thin;   // HP_RG_THIN: this job's few dirty rows go to the alternating-phase closure
     int visits; // earlier jobs of this region in this launch
     int allrows; // every sub-tile row of the job is dirty (a region's first job)
+    uint32_t loaded[(ROWS + 31) / 32];  // thin jobs: window rows loaded so far
     uint32_t rowdirty[AROWS / 32], coldirty[ACOLS / 32], rowsnap[AROWS / 32], colsnap[ACOLS / 32];
     uint32_t subchg[NW];
 };
@@ -690,7 +692,56 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
             for (int k = 0; k < NW; ++k) any_in |= S.dirty[k] != 0;
             uint32_t mychg = 0;
             if (any_in) {
-                if (!have_window) {
+                if (threadIdx.x == 0) {
+                    int nbits = 0;
+                    for (int k = 0; k < NW; ++k) nbits += __popc(S.dirty[k]);
+                    S.thin = nbits <= thin_rows && S.visits >= chain_visits;
+                }
+                __syncthreads();
+                // thin jobs load their window lazily: first only the rows the dirty rows'
+                // closures read (each dirty row and its neighbours), the rest when a column
+                // phase needs whole columns (ensure_full)
+                auto load_rows = [&](bool partial) {
+                    for (int k = threadIdx.x; k < ROWS * RWW; k += NW * 32) {
+                        const int r = k / RWW, wi = k - r * RWW;
+                        if (partial && ((S.loaded[r >> 5] >> (r & 31)) & 1)) continue;
+                        const int gx = X0 - 4 + 4 * wi, gy = Y0 - 1 + r;
+                        if (inner) {
+                            const int64_t o = (int64_t)gy * w + gx;
+                            S.R[k] = __ldcg(reinterpret_cast<const unsigned int*>(R + o));
+                            S.M[k] = __ldcg(reinterpret_cast<const unsigned int*>(mask + o));
+                        } else {
+                            S.R[k] = load_word(R, w, h, gx, gy);
+                            S.M[k] = load_word(mask, w, h, gx, gy);
+                        }
+                    }
+                };
+                bool full = have_window;
+                auto ensure_full = [&]() {
+                    if (full) return;
+                    load_rows(true);  // the rows not loaded yet
+                    __syncthreads();
+                    full = true;
+                };
+                if (!have_window && S.thin) {
+                    if (threadIdx.x < (ROWS + 31) / 32) {
+                        uint32_t need[(ROWS + 31) / 32] = {};
+                        for (int sy = 0; sy < RY; ++sy) {
+                            uint32_t band = 0;
+                            for (int sx = 0; sx < RX; ++sx) band |= S.dirty[sy * RX + sx];
+                            for (int b = 0; b < 32; ++b)
+                                if ((band >> b) & 1)
+                                    for (int r = sy * 32 + b; r <= sy * 32 + b + 2; ++r) need[r >> 5] |= 1u << (r & 31);
+                        }
+                        // the loop marks loaded rows; invert so load_rows(true) loads the needed ones
+                        S.loaded[threadIdx.x] = ~need[threadIdx.x];
+                    }
+                    __syncthreads();
+                    load_rows(true);
+                    __syncthreads();
+                    if (threadIdx.x < (ROWS + 31) / 32) S.loaded[threadIdx.x] = ~S.loaded[threadIdx.x];
+                    __syncthreads();
+                } else if (!have_window) {
                     // the whole window: all of a thread's loads are issued before any store
                     constexpr int NIT = (ROWS * RWW + NW * 32 - 1) / (NW * 32);
                     uint32_t vr[NIT], vm[NIT];
@@ -762,7 +813,6 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                         nbits += __popc(S.dirty[k]);
                     }
                     S.pend = np;
-                    S.thin = nbits <= thin_rows && S.visits >= chain_visits;
                     S.allrows = nbits == NW * 32;  // a region's first job: every row dirty
 #if HP_RG_PROFILE
                     S.tA = gtimer();
@@ -809,8 +859,9 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                     __syncthreads();
                     if (lane == 0 && S.dirty[warp]) atomicOr(&S.rowdirty[warp / RX], S.dirty[warp]);
                     __syncthreads();
-                    adi_close_region(S, sR, sRw, sM, warp, lane, iters, nrows);
+                    adi_close_region(S, sR, sRw, sM, warp, lane, iters, nrows, ensure_full);
                     mychg = S.subchg[warp];
+                    have_window = full;
                 } else while (true) {
                     uint32_t dirty = 0;
                     if (lane == 0 && *reinterpret_cast<volatile uint32_t*>(&S.dirty[warp]))
@@ -972,23 +1023,27 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
 #pragma unroll
                         for (int j = 0; j < PPL; ++j) {
                             const int c = wc0 + PPL * lane + 1 + j;
-                            if (sy == 0 && improves(wr0 + 1, c, wr0, c + d)) {
+                            // only pixels of rows changed in this job can newly improve a
+                            // neighbour (an unchanged pixel's offer was delivered when it got its
+                            // value); thin jobs also hold only those rows' neighbourhoods
+                            if (sy == 0 && (mychg & 1u) && improves(wr0 + 1, c, wr0, c + d)) {
                                 if (c + d == wc0) m8[0] |= TOP;
                                 else if (c + d == wc0 + SW + 1) m8[2] |= TOP;
                                 else m8[1] |= TOP;
                             }
-                            if (sy == RY - 1 && improves(wr0 + kTile, c, wr0 + kTile + 1, c + d)) {
+                            if (sy == RY - 1 && (mychg >> 31) && improves(wr0 + kTile, c, wr0 + kTile + 1, c + d)) {
                                 if (c + d == wc0) m8[5] |= BOT;
                                 else if (c + d == wc0 + SW + 1) m8[7] |= BOT;
                                 else m8[6] |= BOT;
                             }
                         }
-                        if (sx == 0 && improves(r, wc0 + 1, r + d, wc0)) {
+                        const bool rowchg = (mychg >> lane) & 1u;
+                        if (sx == 0 && rowchg && improves(r, wc0 + 1, r + d, wc0)) {
                             if (r + d == wr0) m8[0] |= TOP;
                             else if (r + d == wr0 + kTile + 1) m8[5] |= BOT;
                             else m8[3] |= 1u << (lane + d);
                         }
-                        if (sx == RX - 1 && improves(r, wc0 + SW, r + d, wc0 + SW + 1)) {
+                        if (sx == RX - 1 && rowchg && improves(r, wc0 + SW, r + d, wc0 + SW + 1)) {
                             if (r + d == wr0) m8[2] |= TOP;
                             else if (r + d == wr0 + kTile + 1) m8[7] |= BOT;
                             else m8[4] |= 1u << (lane + d);
@@ -1303,7 +1358,7 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_adi(const uint8_
                 }
                 __syncthreads();
                 int phases = 0, lines = 0;
-                adi_close_region(S, sR, sRw, sM, warp, lane, phases, lines);
+                adi_close_region(S, sR, sRw, sM, warp, lane, phases, lines, [] {});
                 if (threadIdx.x == 0) {
                     atomicAdd(&wl.ctr[4], (unsigned long long)phases);
                 }
