@@ -492,7 +492,6 @@ struct Smem {
     int thin;   // HP_RG_THIN: this job's few dirty rows go to the alternating-phase closure
     int visits; // earlier jobs of this region in this launch
     int allrows; // every sub-tile row of the job is dirty (a region's first job)
-    uint32_t loaded[(ROWS + 31) / 32];  // thin jobs: window rows loaded so far
     uint32_t rowdirty[AROWS / 32], coldirty[ACOLS / 32], rowsnap[AROWS / 32], colsnap[ACOLS / 32];
     uint32_t subchg[NW];
 };
@@ -698,50 +697,7 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                     S.thin = nbits <= thin_rows && S.visits >= chain_visits;
                 }
                 __syncthreads();
-                // thin jobs load their window lazily: first only the rows the dirty rows'
-                // closures read (each dirty row and its neighbours), the rest when a column
-                // phase needs whole columns (ensure_full)
-                auto load_rows = [&](bool partial) {
-                    for (int k = threadIdx.x; k < ROWS * RWW; k += NW * 32) {
-                        const int r = k / RWW, wi = k - r * RWW;
-                        if (partial && ((S.loaded[r >> 5] >> (r & 31)) & 1)) continue;
-                        const int gx = X0 - 4 + 4 * wi, gy = Y0 - 1 + r;
-                        if (inner) {
-                            const int64_t o = (int64_t)gy * w + gx;
-                            S.R[k] = __ldcg(reinterpret_cast<const unsigned int*>(R + o));
-                            S.M[k] = __ldcg(reinterpret_cast<const unsigned int*>(mask + o));
-                        } else {
-                            S.R[k] = load_word(R, w, h, gx, gy);
-                            S.M[k] = load_word(mask, w, h, gx, gy);
-                        }
-                    }
-                };
-                bool full = have_window;
-                auto ensure_full = [&]() {
-                    if (full) return;
-                    load_rows(true);  // the rows not loaded yet
-                    __syncthreads();
-                    full = true;
-                };
-                if (!have_window && S.thin) {
-                    if (threadIdx.x < (ROWS + 31) / 32) {
-                        uint32_t need[(ROWS + 31) / 32] = {};
-                        for (int sy = 0; sy < RY; ++sy) {
-                            uint32_t band = 0;
-                            for (int sx = 0; sx < RX; ++sx) band |= S.dirty[sy * RX + sx];
-                            for (int b = 0; b < 32; ++b)
-                                if ((band >> b) & 1)
-                                    for (int r = sy * 32 + b; r <= sy * 32 + b + 2; ++r) need[r >> 5] |= 1u << (r & 31);
-                        }
-                        // the loop marks loaded rows; invert so load_rows(true) loads the needed ones
-                        S.loaded[threadIdx.x] = ~need[threadIdx.x];
-                    }
-                    __syncthreads();
-                    load_rows(true);
-                    __syncthreads();
-                    if (threadIdx.x < (ROWS + 31) / 32) S.loaded[threadIdx.x] = ~S.loaded[threadIdx.x];
-                    __syncthreads();
-                } else if (!have_window) {
+                if (!have_window) {
                     // the whole window: all of a thread's loads are issued before any store
                     constexpr int NIT = (ROWS * RWW + NW * 32 - 1) / (NW * 32);
                     uint32_t vr[NIT], vm[NIT];
@@ -859,9 +815,8 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                     __syncthreads();
                     if (lane == 0 && S.dirty[warp]) atomicOr(&S.rowdirty[warp / RX], S.dirty[warp]);
                     __syncthreads();
-                    adi_close_region(S, sR, sRw, sM, warp, lane, iters, nrows, ensure_full);
+                    adi_close_region(S, sR, sRw, sM, warp, lane, iters, nrows, [] {});
                     mychg = S.subchg[warp];
-                    have_window = full;
                 } else while (true) {
                     uint32_t dirty = 0;
                     if (lane == 0 && *reinterpret_cast<volatile uint32_t*>(&S.dirty[warp]))
