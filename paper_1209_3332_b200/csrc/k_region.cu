@@ -691,12 +691,6 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
             for (int k = 0; k < NW; ++k) any_in |= S.dirty[k] != 0;
             uint32_t mychg = 0;
             if (any_in) {
-                if (threadIdx.x == 0) {
-                    int nbits = 0;
-                    for (int k = 0; k < NW; ++k) nbits += __popc(S.dirty[k]);
-                    S.thin = nbits <= thin_rows && S.visits >= chain_visits;
-                }
-                __syncthreads();
                 if (!have_window) {
                     // the whole window: all of a thread's loads are issued before any store
                     constexpr int NIT = (ROWS * RWW + NW * 32 - 1) / (NW * 32);
@@ -769,6 +763,7 @@ __global__ void __launch_bounds__(NW * 32, HP_RG_MINB) k_region_mr8(const uint8_
                         nbits += __popc(S.dirty[k]);
                     }
                     S.pend = np;
+                    S.thin = nbits <= thin_rows && S.visits >= chain_visits;
                     S.allrows = nbits == NW * 32;  // a region's first job: every row dirty
 #if HP_RG_PROFILE
                     S.tA = gtimer();
