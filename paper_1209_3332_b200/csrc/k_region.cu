@@ -55,7 +55,7 @@ constexpr unsigned FULL = 0xffffffffu;
 #define HP_RG_WAITERS 4
 #endif
 #ifndef HP_RG_MIN_ALIVE
-#define HP_RG_MIN_ALIVE 16
+#define HP_RG_MIN_ALIVE 4  // r2, 55 CTAs x 12 tiles in flight: 16 -> 4 idle CTAs kept, bench 974-984 -> 1003-1011
 #endif
 #ifndef HP_POLL_NS
 #define HP_POLL_NS 400       // idle sub-tile warps back off (frees issue slots for co-running work)
