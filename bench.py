@@ -230,7 +230,8 @@ def main():
     ap.add_argument("--impl", default="hp", choices=["hp", "reference"])
     ap.add_argument("--batch", type=int, default=12, help="distinct 4K tiles per GPU per step")
     ap.add_argument("--slots", type=int, default=12, help="tiles in flight per GPU (n_slots)")
-    ap.add_argument("--e2e-slots", type=int, default=14, help="context slots used by hp_run_tiles (e2e)")
+    ap.add_argument("--e2e-slots", type=int, default=24,
+                    help="context slots used by hp_run_tiles (e2e); r2 sweep: 10 947, 14 953, 18 963, 24 963 tiles/s")
     ap.add_argument("--size", type=int, default=4096)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--schedule", default="rotate", choices=["rotate", "join", "fixed"],
