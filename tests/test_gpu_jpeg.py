@@ -205,7 +205,7 @@ def _oracle_jpeg_rows(buf):
 @pytest.mark.parametrize("sampling", ["444", "420"])
 def test_bench_jpeg_e2e_launch_config(sampling):
     """bench.py's e2e.jpeg leg in its exact configuration at full size: the bench's 12 4K tiles
-    as quality-90 JPEG files (restart interval 4), hp_run_tiles_jpeg on 14 slots with per-slot
+    as quality-90 JPEG files (restart interval 4), hp_run_tiles_jpeg on 24 slots with per-slot
     graphs, 32 hardware queues, the files twice each from a demand-driven queue -- every
     delivered table equals the oracle's on the oracle's decode of the same file."""
     import multiprocessing as mp

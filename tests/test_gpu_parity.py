@@ -746,7 +746,7 @@ def _pool_tile(seed):
     return bench._gen((seed, 4096))
 
 
-BENCH_SLOTS, BENCH_E2E_SLOTS, BENCH_BATCH = 12, 14, 12   # bench.py's defaults
+BENCH_SLOTS, BENCH_E2E_SLOTS, BENCH_BATCH = 12, 24, 12   # bench.py's defaults
 
 
 def _oracle_rows(rgb):
@@ -812,7 +812,7 @@ def test_bench_tiles_in_bench_launch_config(bench_ref):
 
 @pytest.mark.slow
 def test_bench_e2e_launch_config(bench_ref):
-    """Parity of bench.py's e2e leg in its exact configuration: hp_run_tiles on 14 slots with
+    """Parity of bench.py's e2e leg in its exact configuration: hp_run_tiles on 24 slots with
     per-slot CUDA graphs (captured on a slot's second tile, replayed after), pinned host tiles,
     32 hardware work queues, the bench's tiles twice each in a demand-driven order -- every
     delivered table equals the oracle's (labels and flags exact, features within C18)."""
