@@ -511,6 +511,19 @@ def test_iwpp_stress(ctx, kind, ramp):
     assert np.array_equal(rec, mask)
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("kind", ["serpentine", "spiral"])
+@pytest.mark.parametrize("ramp", [False, True])
+def test_iwpp_stress_4k(ctx, kind, ramp):
+    """BASELINE configs[4] at its real size: 4096^2 1-px corridors, one 8.4 M-pixel dependency
+    chain; regions re-entered many times go through the alternating-phase closure.  The
+    reconstruction of the single-pixel marker under the corridor mask is the mask itself."""
+    size = 4096
+    marker, mask, _ = make_stress(kind, size, ramp)
+    rec, st = stage(ctx, "IWPP_RAW", [marker, mask], [((size, size), U8), ((4,), I64)], size, size)
+    assert np.array_equal(rec, mask)
+
+
 def test_reduce_rows(ctx):
     """hp_reduce_rows (segmented fp64 sums) against numpy, with empty groups,
     and bit-identical run to run."""
