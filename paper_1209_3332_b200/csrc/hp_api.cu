@@ -451,6 +451,8 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.cs_edge = (int32_t*)A(4 * 4 * kTile * (size_t)ntiles);
         s.cs_roots = (int32_t*)A(4 * (size_t)kTile * kTile * ntiles);
         s.cs_nroots = (int32_t*)A(4 * (size_t)ntiles);
+        s.cs_lr = (uint16_t*)A(2 * N);
+        s.cs_kind = (uint8_t*)A((size_t)ntiles);
         s.sc_root = (int32_t*)A(4 * (size_t)s.comp_cap);
         s.sc_bbox = (int4*)A(16 * (size_t)s.comp_cap);
         s.sc_area = (int32_t*)A(4 * (size_t)s.comp_cap);
@@ -484,7 +486,7 @@ hp_status hp_ctx_create(const hp_config* cfg, hp_ctx** out) {
         s.h_arena = (int64_t*)halloc(16);
         void* all[] = {s.g, s.flags, s.rbc, s.u8a, s.u8b, s.cand, s.big0, s.F, s.split, s.pmask, s.lab, s.aux,
                        s.ML, s.d, s.L, s.dist, s.J, s.c, s.gcol, s.seg_top, s.seg_bot, s.wl.state, s.wl.inrows, s.wl.queue,
-                       s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.cs_edge, s.cs_roots, s.cs_nroots, s.sc_root, s.sc_bbox, s.sc_area, s.sc_big, s.sc_huge, s.big_scratch, s.stg_label, s.stg_flags, s.stg_feat, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
+                       s.wl.ctr, s.obj_root, s.obj_rank, s.obj_bbox, s.cs_edge, s.cs_roots, s.cs_nroots, s.cs_lr, s.cs_kind, s.sc_root, s.sc_bbox, s.sc_area, s.sc_big, s.sc_huge, s.big_scratch, s.stg_label, s.stg_flags, s.stg_feat, s.counters, s.cnt32, s.rgb_dev, s.lab_dev,
                        s.tab_label, s.tab_flags, s.tab_feat, s.tab_nrows, s.h_label, s.h_flags, s.h_feat, s.h_nrows, s.h_arena,
                        s.jhdr_dev, s.jstarts, s.jblk, s.jerr, s.jhdr_host, s.jhdr_ring, s.h_jerr, s.jplanes};
         for (void* p : all)

@@ -92,6 +92,8 @@ struct Slot {
     int32_t* cs_edge;    // k_ccls.cu: per 32x32 tile, the roots of its 4 x 32 edge pixels
     int32_t* cs_roots;   // k_ccls.cu: per tile, its local roots (up to 1024)
     int32_t* cs_nroots;  // k_ccls.cu: per tile, number of local roots
+    uint16_t* cs_lr;     // k_ccls.cu: per pixel, its local root within its 32x32 tile (0xffff: none)
+    uint8_t* cs_kind;    // k_ccls.cu: per tile, 0 no foreground / 1 general / 2 all foreground
     // S5 component list (k_ccls.cu listing; consumed by the per-component S6 / S7-S11 kernels)
     int32_t* sc_root;
     int4* sc_bbox;

@@ -11,14 +11,18 @@
 //                same scheme as k_ccl_local); per local component: area and property bits,
 //                reduced in shared memory and written ONLY at the component's root entry
 //                (global index of its minimum pixel); tile-edge pixels' roots to a compact
-//                edge array; the tile's local roots to a list;
+//                edge array; the tile's local roots to a list; the tile's kind (empty /
+//                general / full) to kinds and every pixel's local root (u16, within the
+//                tile) to lr;
 //   k_cs_merge   cross-tile unions from the edge arrays (CAS hooking of the larger root under
 //                the smaller on the sparse parent array, finds with CAS path halving);
 //   k_cs_accum   every non-root local root adds its area / ORs its bits into its global root
 //                and points straight at it (no unions run any more, so this is safe);
-//   k_cs_out     recomputes the tile's local union-find and writes the u8 output from the
-//                global root's property word.
-// HBM traffic per pixel: the input plane twice and the u8 output once (plus small arrays).
+//   k_cs_out     writes the u8 output from each pixel's lr and its global root's property
+//                word (one lookup per run); for S2 it re-runs the tile's union-find instead
+//                (lr_mode).
+// HBM traffic per pixel: the input plane once, lr written and read (2 B each way), the u8
+// output once (plus small arrays); S2: its flags plane twice and the output.
 // The property word packs the area (bits 0-28: images up to 2^29 - 1 px) with the OR-bits
 // HIT (bit 29) and TOUCH (bit 30); atomicAdd of areas never carries into the flag bits.
 #include <climits>
@@ -77,6 +81,14 @@ struct Sel {
         return f ? !(prop & kTouch) : 1;  // SEL_FILL: big0 | enclosed background
     }
 };
+
+// the output pass reads each pixel's local root from k_cs_local's lr plane, except for S2:
+// its sparse RBC_LO components make re-running the tile's union-find cheaper than the 2 B/px
+// plane (measured r2: k_cs_local<1> + k_cs_out<1> 42.5 -> 47.2 us per 4K tile with lr)
+template <int MODE>
+__host__ __device__ constexpr bool lr_mode() {
+    return MODE != SEL_RBC;
+}
 
 template <int MODE>
 __device__ __forceinline__ int32_t mode_bit() {
@@ -157,6 +169,10 @@ __device__ __forceinline__ unsigned span(int lo, int hi) {  // bits lo..hi
 }
 
 // loads + runs + unions; returns 0 (no foreground), 1 (general), 2 (all foreground)
+__device__ __forceinline__ bool is_run_start(unsigned fm, int lane) {
+    return ((fm >> lane) & 1) && !(lane > 0 && ((fm >> (lane - 1)) & 1));
+}
+
 template <int MODE>
 __device__ __forceinline__ int tile_uf(const Sel& sel, int conn, int tx0, int ty0, TileSm& T, uint8_t (&v)[4],
                                        unsigned (&fms)[4], bool clear_acc) {
@@ -212,14 +228,11 @@ __device__ __forceinline__ int tile_uf(const Sel& sel, int conn, int tx0, int ty
     return 1;
 }
 
-__device__ __forceinline__ bool is_run_start(unsigned fm, int lane) {
-    return ((fm >> lane) & 1) && !(lane > 0 && ((fm >> (lane - 1)) & 1));
-}
-
 template <int MODE>
 __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __restrict__ P, int32_t* __restrict__ X,
                                                   int32_t* __restrict__ E, int32_t* __restrict__ roots,
-                                                  int32_t* __restrict__ nroots) {
+                                                  int32_t* __restrict__ nroots, uint16_t* __restrict__ lr,
+                                                  uint8_t* __restrict__ kinds) {
     __shared__ TileSm T;
     constexpr bool BB = MODE == SEL_AREA_TH;  // bounding boxes per component
     __shared__ int bbs[BB ? 4 : 1][BB ? kT * kT : 1];
@@ -241,6 +254,7 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
     const int kind = tile_uf<MODE>(sel, conn, tx0, ty0, T, v, fms, true);  // (its barriers order bbs)
     int32_t* Et = E + (int64_t)t * 4 * kT;
     auto gidx = [&](int li) -> int32_t { return (int32_t)((int64_t)(ty0 + li / kT) * w + tx0 + li % kT); };
+    if (threadIdx.x == 0) kinds[t] = (uint8_t)kind;
     if (kind == 0) {
         if (threadIdx.x < 4 * kT) Et[threadIdx.x] = -1;
         if (threadIdx.x == 0) nroots[t] = 0;
@@ -266,14 +280,18 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
         }
         return;
     }
-    // per run: area and property bit at the run's root
+    // per run: area and property bit at the run's root; every pixel's local root to lr (the
+    // output pass reads it instead of re-running the tile's union-find)
+    int rk[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int ly = (threadIdx.x >> 5) + 8 * k;
         const unsigned fm = fms[k];
+        rk[k] = 0;
         if (!is_run_start(fm, lane)) continue;
         const int re = run_end(fm, lane);
         const int r = find_l(T.s, ly * kT + lane);
+        rk[k] = r;
         atomicAdd(&T.acc[r], re - lane + 1);
         if (T.bitm[ly] & span(lane, re)) atomicOr(&T.acc[r], mode_bit<MODE>());
         if constexpr (BB) {
@@ -282,6 +300,15 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
             atomicMax(&bbs[2][r], tx0 + re);
             atomicMax(&bbs[3][r], ty0 + ly);
         }
+    }
+#pragma unroll
+    for (int k = 0; k < 4 && lr_mode<MODE>(); ++k) {
+        const int ly = (threadIdx.x >> 5) + 8 * k;
+        const unsigned fm = fms[k];
+        const bool f = (fm >> lane) & 1;
+        const int r = __shfl_sync(0xffffffffu, rk[k], f ? run_start(fm, lane) : lane);
+        const int gx = tx0 + lane, gy = ty0 + ly;
+        if (gx < w && gy < h) lr[(int64_t)gy * w + gx] = f ? (uint16_t)r : (uint16_t)0xffff;
     }
     __syncthreads();
     // roots: run starts that are their own parent
@@ -386,40 +413,85 @@ __global__ void __launch_bounds__(256) k_cs_accum(int ntiles, const int32_t* __r
 }
 
 // every mode but SEL_FILL outputs 0 on a tile without foreground: the caller zeroes the plane
-// and such tiles (nroots == 0) skip the pass
+// and such tiles skip the pass.  A streaming pass: each pixel's local root from lr (written by
+// k_cs_local), the property word of its global root looked up once per run (r1-r2 re-ran the
+// tile's union-find here: 30-34 us per 4K tile, latency-bound on the shared-memory finds).
 template <int MODE>
 __global__ void __launch_bounds__(256) k_cs_out(Sel sel, int conn, const int32_t* __restrict__ P,
-                                                const int32_t* __restrict__ X, uint8_t* __restrict__ out,
-                                                const int32_t* __restrict__ nroots) {
-    __shared__ TileSm T;
+                                                const int32_t* __restrict__ X,
+                                                uint8_t* __restrict__ out, const uint16_t* __restrict__ lr,
+                                                const uint8_t* __restrict__ kinds) {
     if (sel.gate && *sel.gate == 0) return;
-    if (MODE != SEL_FILL && nroots[blockIdx.y * gridDim.x + blockIdx.x] == 0) return;
+    const int kind = kinds[blockIdx.y * gridDim.x + blockIdx.x];
+    if (MODE != SEL_FILL && kind == 0) return;
     const int tx0 = blockIdx.x * kT, ty0 = blockIdx.y * kT;
     const int lane = threadIdx.x & 31;
     const int w = sel.w, h = sel.h;
-    uint8_t v[4];
-    unsigned fms[4];
-    const int kind = tile_uf<MODE>(sel, conn, tx0, ty0, T, v, fms, false);
     const int gx = tx0 + lane;
-    int32_t prop0 = 0;
-    if (kind == 2) prop0 = __ldg(X + __ldg(P + (int32_t)((int64_t)ty0 * w + tx0)));
+    if constexpr (!lr_mode<MODE>()) {
+        __shared__ TileSm T;
+        uint8_t v[4];
+        unsigned fms[4];
+        const int kd = tile_uf<MODE>(sel, conn, tx0, ty0, T, v, fms, false);
+        int32_t prop0 = 0;
+        if (kd == 2) prop0 = __ldg(X + __ldg(P + (int32_t)((int64_t)ty0 * w + tx0)));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int ly = (threadIdx.x >> 5) + 8 * k;
+            const int gy = ty0 + ly;
+            const unsigned fm = fms[k];
+            const bool f = (fm >> lane) & 1;
+            int32_t prop = prop0;
+            if (kd == 1) {
+                const int st = f ? run_start(fm, lane) : lane;
+                int32_t pr = 0;
+                if (f && st == lane) {
+                    const int r = find_l(T.s, ly * kT + lane);
+                    pr = __ldg(X + __ldg(P + (int32_t)((int64_t)(ty0 + r / kT) * w + tx0 + r % kT)));
+                }
+                prop = __shfl_sync(0xffffffffu, pr, st);
+            }
+            if (gx < w && gy < h) out[(int64_t)gy * w + gx] = sel.out<MODE>(v[k], f, prop);
+        }
+        return;
+    }
+    // the four rows' loads and the run lookups are issued as independent batches (three
+    // dependent L2 round trips per thread instead of twelve)
+    int l[4], st[4];
+    uint8_t v[4];
+    bool in[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const int ly = (threadIdx.x >> 5) + 8 * k;
-        const int gy = ty0 + ly;
-        const unsigned fm = fms[k];
-        const bool f = (fm >> lane) & 1;
-        int32_t prop = prop0;
-        if (kind == 1) {
-            const int st = f ? run_start(fm, lane) : lane;
-            int32_t pr = 0;
-            if (f && st == lane) {
-                const int r = find_l(T.s, ly * kT + lane);
-                pr = __ldg(X + __ldg(P + (int32_t)((int64_t)(ty0 + r / kT) * w + tx0 + r % kT)));
-            }
-            prop = __shfl_sync(0xffffffffu, pr, st);
+        const int gy = ty0 + (threadIdx.x >> 5) + 8 * k;
+        in[k] = gx < w && gy < h;
+        const int64_t p = (int64_t)gy * w + gx;
+        l[k] = (kind == 1 && in[k]) ? (int)__ldg(lr + p) : 0xffff;
+        v[k] = (MODE == SEL_RBC && in[k]) ? __ldg(sel.plane + p) : (uint8_t)0;
+    }
+    int32_t q[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const bool f = l[k] != 0xffff;
+        const unsigned fm = __ballot_sync(0xffffffffu, f);
+        st[k] = f ? run_start(fm, lane) : lane;
+        q[k] = (f && st[k] == lane) ? __ldg(P + (int32_t)((int64_t)(ty0 + l[k] / kT) * w + tx0 + l[k] % kT)) : -1;
+    }
+    if (kind == 2) q[0] = __ldg(P + (int32_t)((int64_t)ty0 * w + tx0));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = q[k] >= 0 ? __ldg(X + q[k]) : 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int gy = ty0 + (threadIdx.x >> 5) + 8 * k;
+        bool f;
+        int32_t prop;
+        if (kind == 2) {  // an all-foreground tile lies inside the image
+            f = true;
+            prop = q[0];
+        } else {
+            f = l[k] != 0xffff;
+            prop = __shfl_sync(0xffffffffu, q[k], st[k]);
         }
-        if (gx < w && gy < h) out[(int64_t)gy * w + gx] = sel.out<MODE>(v[k], f, prop);
+        if (in[k]) out[(int64_t)gy * w + gx] = sel.out<MODE>(v[k], f, prop);
     }
 }
 
@@ -464,13 +536,14 @@ void run_select(Sel sel, int conn, Slot& sl, uint8_t* out, cudaStream_t s, const
     dim3 grid(ntx, nty);
     int32_t* P = sel.P ? sel.P : sl.lab;
     int32_t* X = sel.X ? sel.X : sl.aux;
-    (note_launch(), k_cs_local<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, sl.cs_edge, sl.cs_roots, sl.cs_nroots));
+    (note_launch(), k_cs_local<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, sl.cs_edge, sl.cs_roots, sl.cs_nroots,
+                                                           sl.cs_lr, sl.cs_kind));
     (note_launch(), k_cs_merge<<<(int)(((int64_t)ntiles * 2 * kT + 255) / 256), 256, 0, s>>>(conn, ntx, nty,
                                                                                            sl.cs_edge, P, sel.gate));
     (note_launch(), k_cs_accum<<<(ntiles + 7) / 8, 256, 0, s>>>(ntiles, sl.cs_roots, sl.cs_nroots, P, X, sel));
     if (out) {
         if (MODE != SEL_FILL) cudaMemsetAsync(out, 0, (size_t)w * h, s);
-        (note_launch(), k_cs_out<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, out, sl.cs_nroots));
+        (note_launch(), k_cs_out<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, out, sl.cs_lr, sl.cs_kind));
     }
     if (lo)
         (note_launch(), k_cs_list<<<(ntiles + 7) / 8, 256, 0, s>>>(ntiles, sl.cs_roots, sl.cs_nroots, P, X, sel,
