@@ -565,7 +565,8 @@ void run_select(Sel sel, int conn, Slot& sl, uint8_t* out, cudaStream_t s, const
 // keeps m = |dx| + |dy| and the biased dx, dy (int16 planes); the gradient sector is computed
 // in the suppression step only for pixels with m > low.
 constexpr int kNW = 64, kNH = 32;
-constexpr int kGWW = kNW / 4 + 2;  // staged g words per row: pixels [x0 - 4, x0 + kNW + 4)
+constexpr int kGWW = kNW / 4 + 2;  // Sobel groups per row: pixels [x0 - 4, x0 + kNW + 4)
+constexpr int kSW = kNW / 4 + 8;   // staged g words per row: pixels [x0 - 16, x0 + kNW + 16), 16-B aligned
 constexpr int kGR = kNH + 4;       // staged g rows: [y0 - 2, y0 + kNH + 2)
 constexpr int kMW = kNW + 8;       // magnitude columns [x0 - 4, x0 + kNW + 4) (x0-1 .. x0+kNW used)
 constexpr int kMR = kNH + 2;       // magnitude rows [y0 - 1, y0 + kNH]
@@ -596,25 +597,63 @@ __device__ __forceinline__ uint32_t absdiff2(uint32_t a, uint32_t b) { return __
 
 __global__ void __launch_bounds__(256) k_canny_nms(const uint8_t* __restrict__ g, int w, int h, int low, int high,
                                                    uint8_t* __restrict__ map) {
-    __shared__ uint32_t sg[kGR][kGWW];
+    __shared__ __align__(16) uint32_t sg[kGR][kSW];
+    __shared__ __align__(8) unsigned long long bar;
     __shared__ __align__(8) uint16_t sm[kMR][kMW];
     __shared__ __align__(8) uint16_t sdx[kMR][kMW];
     __shared__ __align__(8) uint16_t sdy[kMR][kMW];
     const int x0 = blockIdx.x * kNW, y0 = blockIdx.y * kNH;
     const bool aligned = (w & 3) == 0 && (((uintptr_t)g) & 3) == 0;
-    for (int i = threadIdx.x; i < kGR * kGWW; i += blockDim.x) {
-        const int r = i / kGWW, q = i - r * kGWW;
-        sg[r][q] = g_word(g, w, h, x0 - 4 + 4 * q, y0 - 2 + r, aligned);
+    // Stage the rows [y0 - 2, y0 + kNH + 2) (clamped: replicated borders).  Interior tiles of a
+    // 16-B-aligned plane: one bulk async copy (cp.async.bulk, the TMA engine) per 96-byte row,
+    // completing on an mbarrier -- no load / store instructions on the SMs (r2: the word loop
+    // issued a quarter of the kernel's instructions).  Tiles at the left / right edge replicate
+    // columns, so they keep the per-word loop.
+    const bool bulk = (w & 15) == 0 && (((uintptr_t)g) & 15) == 0 && x0 >= 16 && x0 + kNW + 16 <= w;
+    if (bulk) {
+        const uint32_t ba = (uint32_t)__cvta_generic_to_shared(&bar);
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ba) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            if (threadIdx.x == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ba), "r"(kGR * kSW * 4)
+                             : "memory");
+            __syncwarp();
+            for (int r = threadIdx.x; r < kGR; r += 32) {
+                const int gy = min(max(y0 - 2 + r, 0), h - 1);
+                const uint8_t* src = g + (int64_t)gy * w + x0 - 16;
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        (uint32_t)__cvta_generic_to_shared(&sg[r][0])),
+                    "l"(src), "r"(kSW * 4), "r"(ba)
+                    : "memory");
+            }
+        }
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                : "=r"(done)
+                : "r"(ba)
+                : "memory");
+    } else {
+        for (int i = threadIdx.x; i < kGR * kSW; i += blockDim.x) {
+            const int r = i / kSW, q = i - r * kSW;
+            sg[r][q] = g_word(g, w, h, x0 - 16 + 4 * q, y0 - 2 + r, aligned);
+        }
+        __syncthreads();
     }
-    __syncthreads();
     // Sobel of pixel groups (row gy = y0 - 1 + r, pixels x0 - 4 + 4q + k, k = 0..3)
     for (int i = threadIdx.x; i < kMR * kGWW; i += blockDim.x) {
         const int r = i / kGWW, q = i - r * kGWW;
-        const int ql = max(q - 1, 0), qr = min(q + 1, kGWW - 1);  // outermost pixels unused
+        const int qs = q + 3;  // staged word of group q (pixels x0 - 4 + 4q)
         uint32_t t[4], c[4], b[4];
-        col_pairs(sg[r][ql], sg[r][q], sg[r][qr], t);
-        col_pairs(sg[r + 1][ql], sg[r + 1][q], sg[r + 1][qr], c);
-        col_pairs(sg[r + 2][ql], sg[r + 2][q], sg[r + 2][qr], b);
+        col_pairs(sg[r][qs - 1], sg[r][qs], sg[r][qs + 1], t);
+        col_pairs(sg[r + 1][qs - 1], sg[r + 1][qs], sg[r + 1][qs + 1], c);
+        col_pairs(sg[r + 2][qs - 1], sg[r + 2][qs], sg[r + 2][qs + 1], b);
         uint32_t S[4], D[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {

@@ -274,7 +274,10 @@ def test_edt_random(ctx, shape, dens):
         assert np.array_equal(d2, e2)
 
 
-@pytest.mark.parametrize("shape,blur", [((37, 53), False), ((70, 300), True), ((129, 97), True), ((8, 8), False)])
+# (300, 512) and (96, 1024): 16-B-aligned rows, so interior tiles stage g by bulk async copies
+# (k_canny_nms) while edge tiles keep the per-word loop
+@pytest.mark.parametrize("shape,blur", [((37, 53), False), ((70, 300), True), ((129, 97), True), ((8, 8), False),
+                                        ((300, 512), True), ((96, 1024), False)])
 def test_canny_random(ctx, shape, blur):
     import cv2
     h, w = shape
