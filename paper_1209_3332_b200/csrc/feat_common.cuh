@@ -108,6 +108,8 @@ __device__ __forceinline__ int refl(int i, int n) {
 }
 
 struct FeatSmem {
+    double f[HP_NFEAT];  // team rank 0's 36 features (shared, not registers: r2 the per-thread
+                         // array cost k_comp_fused 484 B of spills at its 128-register cap)
     unsigned int hist[256];
     unsigned int glcm[64];
     float gmin, gmax;

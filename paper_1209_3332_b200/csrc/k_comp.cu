@@ -513,10 +513,9 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
                 const int li = ly * WX + lx;  // non-members hold stale values: test mem first
                 return S.mem[li] && S.B[li] == r;
             };
-            double f[HP_NFEAT];
             int border = 0;
-            object_features(team, inP, a.g, a.edge, w, h, bb.x, bb.y, bb.z, bb.w, S.fs, red, f, &border);
-            if (tr == 0) write_row(a, gidx(r) + 1, border, f);
+            object_features(team, inP, a.g, a.edge, w, h, bb.x, bb.y, bb.z, bb.w, S.fs, red, S.fs.f, &border);
+            if (tr == 0) write_row(a, gidx(r) + 1, border, S.fs.f);
             team.sync();
         }
     }

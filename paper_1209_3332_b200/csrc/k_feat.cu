@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(kFT, 3) k_obj_feat(const int32_t* __restrict__
         auto inP = [&](int x, int y) {
             return x >= 0 && y >= 0 && x < w && y < h && labels[(int64_t)y * lpitch + x] == lab;
         };
-        double f[HP_NFEAT];
+        double* f = fs.f;
         int border = 0;
         object_features(team, inP, g, edge, w, h, bbox[4 * obj], bbox[4 * obj + 1], bbox[4 * obj + 2],
                         bbox[4 * obj + 3], fs, red, f, &border);
