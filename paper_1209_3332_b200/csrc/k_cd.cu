@@ -35,9 +35,10 @@ __global__ void __launch_bounds__(256) k_cd_vec16(const uint8_t* __restrict__ rg
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
             int o = 3 * i;
-            int R = (wv[o >> 2] >> (8 * (o & 3))) & 0xff;
-            int G = (wv[(o + 1) >> 2] >> (8 * ((o + 1) & 3))) & 0xff;
-            int B = (wv[(o + 2) >> 2] >> (8 * ((o + 2) & 3))) & 0xff;
+            // one PRMT per channel byte (a shift + mask pair otherwise)
+            int R = (int)__byte_perm(wv[o >> 2], 0, 0x4440 | (o & 3));
+            int G = (int)__byte_perm(wv[(o + 1) >> 2], 0, 0x4440 | ((o + 1) & 3));
+            int B = (int)__byte_perm(wv[(o + 2) >> 2], 0, 0x4440 | ((o + 2) & 3));
             cd_pixel(R, G, B, lut, k, gb[i], fb[i], nbg);
         }
         uint4 go, fo;
