@@ -96,14 +96,30 @@ __global__ void __launch_bounds__(256) k_morph_r(const uint8_t* __restrict__ src
     uint32_t* H = smem + ROWS * IW;               // [ND][ROWS][32]
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const bool row_aligned = (w & 3) == 0 && (((uintptr_t)src) & 3) == 0;
+    const bool dst_aligned = (w & 1) == 0 && (((uintptr_t)dst) & 1) == 0;
     const int ntx = (w + TW2 - 1) / TW2, ntiles = ntx * ((h + TH2 - 1) / TH2);
 
     // Persistent over tiles: the global loads of the NEXT tile's input are issued into
     // registers before this tile's compute, so their latency hides behind stages 2-3.
     // stage 1 (per tile): pixels [x0 - 2RW, x0 + 64 + 2RW + 2) of rows [y0 - R, y0 + TH2 + R)
     uint32_t pre[NL];
-    auto load = [&](int tile) {
-        const int x0 = (tile % ntx) * TW2, y0 = (tile / ntx) * TH2;
+    // tile -> (tx, ty) advanced by the grid stride without a division per tile (r2 ncu: the
+    // runtime div / mod by ntx cost 12% of the kernel's instructions)
+    const int gsx = (int)gridDim.x % ntx, gsy = (int)gridDim.x / ntx;
+    auto load = [&](int tx_, int ty_) {
+        const int x0 = tx_ * TW2, y0 = ty_ * TH2;
+        if (row_aligned && x0 - 2 * RW >= 0 && x0 + TW2 + 2 * RW + 4 <= w && y0 - R >= 0 && y0 + TH2 + R <= h) {
+            // interior tile: every staged word is an aligned in-range load
+            const uint8_t* base = src + (int64_t)(y0 - R) * w + (x0 - 2 * RW);
+#pragma unroll
+            for (int l = 0; l < NL; ++l) {
+                const int i = threadIdx.x + 256 * l;
+                const int r = i / NQ, q = i - r * NQ;
+                pre[l] = (i < ROWS * NQ) ? __ldg(reinterpret_cast<const unsigned int*>(base + (int64_t)r * w + 4 * q))
+                                         : 0u;
+            }
+            return;
+        }
 #pragma unroll
         for (int l = 0; l < NL; ++l) {
             const int i = threadIdx.x + 256 * l;
@@ -131,9 +147,16 @@ __global__ void __launch_bounds__(256) k_morph_r(const uint8_t* __restrict__ src
         }
     };
     int tile = blockIdx.x;
-    if (tile < ntiles) load(tile);
+    int tx0 = (int)blockIdx.x % ntx, ty0 = (int)blockIdx.x / ntx;
+    if (tile < ntiles) load(tx0, ty0);
     for (; tile < ntiles; tile += gridDim.x) {
-        const int x0 = (tile % ntx) * TW2, y0 = (tile / ntx) * TH2;
+        const int x0 = tx0 * TW2, y0 = ty0 * TH2;
+        tx0 += gsx;
+        ty0 += gsy;
+        if (tx0 >= ntx) {
+            tx0 -= ntx;
+            ++ty0;
+        }
         __syncthreads();  // the previous tile's stages 2-3 are done with in[] and H[]
 #pragma unroll
         for (int l = 0; l < NL; ++l) {
@@ -145,7 +168,7 @@ __global__ void __launch_bounds__(256) k_morph_r(const uint8_t* __restrict__ src
             }
         }
         __syncthreads();
-        if (tile + (int)gridDim.x < ntiles) load(tile + gridDim.x);
+        if (tile + (int)gridDim.x < ntiles) load(tx0, ty0);
 
         // stage 2: horizontal running min/max for the distinct half-widths; one warp per row,
         // lane = output word (pixels 2j, 2j+1)
@@ -189,15 +212,16 @@ __global__ void __launch_bounds__(256) k_morph_r(const uint8_t* __restrict__ src
             for (int i = 0; i < ORW; ++i)
                 m[i] = vop3<IS_MIN>(m[i], H[(E.idx_of_dy[dy] * ROWS + oy0 + i + dy) * 32 + j],
                                     H[(E.idx_of_dy[dy + 1] * ROWS + oy0 + i + dy + 1) * 32 + j]);
+        uint8_t* o = dst + (int64_t)(y0 + oy0) * w + gx;
+        if (dst_aligned && gx + 1 < w && y0 + oy0 + ORW <= h) {
 #pragma unroll
-        for (int i = 0; i < ORW; ++i) {
-            const int gy = y0 + oy0 + i;
-            if (gy >= h || gx >= w) continue;
-            const uint32_t pk = __byte_perm(m[i], 0, 0x0020);  // u16 lanes -> 2 bytes
-            uint8_t* o = dst + (int64_t)gy * w + gx;
-            if (gx + 1 < w && (((uintptr_t)o) & 1) == 0) {
-                *reinterpret_cast<uint16_t*>(o) = (uint16_t)pk;
-            } else {
+            for (int i = 0; i < ORW; ++i, o += w)
+                *reinterpret_cast<uint16_t*>(o) = (uint16_t)__byte_perm(m[i], 0, 0x0020);  // u16 lanes -> 2 bytes
+        } else {
+#pragma unroll
+            for (int i = 0; i < ORW; ++i, o += w) {
+                if (y0 + oy0 + i >= h || gx >= w) continue;
+                const uint32_t pk = __byte_perm(m[i], 0, 0x0020);
                 o[0] = (uint8_t)pk;
                 if (gx + 1 < w) o[1] = (uint8_t)(pk >> 8);
             }
