@@ -170,28 +170,42 @@ __global__ void __launch_bounds__(256) k_morph_r(const uint8_t* __restrict__ src
         __syncthreads();
         if (tile + (int)gridDim.x < ntiles) load(tx0, ty0);
 
-        // stage 2: horizontal running min/max for the distinct half-widths; one warp per row,
-        // lane = output word (pixels 2j, 2j+1)
-        for (int r = ty; r < ROWS; r += 8) {
-            const uint32_t* rowp = in + r * IW;
-            const int j = tx;
-            uint32_t wv[2 * RW + 2];
+        // stage 2: horizontal running min/max for the distinct half-widths; a half-warp per
+        // row, lane -> output words 2l, 2l+1 (pixels 4l .. 4l+3): the 2RW+3 covering words
+        // come in as 8-byte shared loads, each funnel-shifted window serves both outputs (the
+        // second output's window k is the first's k + 2), H is written 8 bytes at a time
+        // (r2: a lane per word issued 12 of 36 M instructions in the covering-word loads)
+        {
+            constexpr int NWV = ((((2 * RW + R + 2) >> 1) + 2) + 1) & ~1;  // words 0 .. last used, even
+            static_assert(2 * 15 + NWV <= IW, "covering words inside the staged row");
+            const int l = tx & 15;
+            for (int r = 2 * ty + (tx >> 4); r < ROWS; r += 16) {
+                const uint32_t* rowp = in + r * IW + 2 * l;
+                uint32_t wv[NWV];
 #pragma unroll
-            for (int k = 0; k < 2 * RW + 2; ++k) wv[k] = rowp[j + k];
-            auto win = [&](int k) -> uint32_t {  // pixels (2j + k, 2j + 1 + k)
-                const int o = 2 * RW + k;
-                return (o & 1) ? __funnelshift_r(wv[o >> 1], wv[(o >> 1) + 1], 16) : wv[o >> 1];
-            };
-            uint32_t m = wv[RW];
-#pragma unroll
-            for (int q = 0; q < ND; ++q)
-                if (E.hw[q] == 0) H[(q * ROWS + r) * 32 + j] = m;
-#pragma unroll
-            for (int k = 1; k <= R; ++k) {
-                m = vop3<IS_MIN>(m, win(k), win(-k));
+                for (int k = 0; k + 1 < NWV; k += 2) {
+                    const uint2 v = *reinterpret_cast<const uint2*>(rowp + k);
+                    wv[k] = v.x;
+                    wv[k + 1] = v.y;
+                }
+                if (NWV & 1) wv[NWV - 1] = rowp[NWV - 1];
+                auto win = [&](int k) -> uint32_t {  // pixels (4l + k, 4l + 1 + k)
+                    const int o = 2 * RW + k;
+                    return (o & 1) ? __funnelshift_r(wv[o >> 1], wv[(o >> 1) + 1], 16) : wv[o >> 1];
+                };
+                uint32_t m0 = win(0), m1 = win(2);
+                uint2* Hr = reinterpret_cast<uint2*>(H + r * 32 + 2 * l);
 #pragma unroll
                 for (int q = 0; q < ND; ++q)
-                    if (E.hw[q] == k) H[(q * ROWS + r) * 32 + j] = m;
+                    if (E.hw[q] == 0) Hr[q * ROWS * 16] = make_uint2(m0, m1);
+#pragma unroll
+                for (int k = 1; k <= R; ++k) {
+                    m0 = vop3<IS_MIN>(m0, win(k), win(-k));
+                    m1 = vop3<IS_MIN>(m1, win(k + 2), win(2 - k));
+#pragma unroll
+                    for (int q = 0; q < ND; ++q)
+                        if (E.hw[q] == k) Hr[q * ROWS * 16] = make_uint2(m0, m1);
+                }
             }
         }
         __syncthreads();
