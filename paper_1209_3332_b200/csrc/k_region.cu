@@ -58,10 +58,12 @@ constexpr unsigned FULL = 0xffffffffu;
 #define HP_RG_MIN_ALIVE 4  // r2, 55 CTAs x 12 tiles in flight: 16 -> 4 idle CTAs kept, bench 974-984 -> 1003-1011
 #endif
 #ifndef HP_POLL_NS
-#define HP_POLL_NS 400       // idle sub-tile warps back off (frees issue slots for co-running work)
+#define HP_POLL_NS 200       // idle sub-tile warps back off (frees issue slots for co-running work)
 #endif
 #ifndef HP_POLL_MAX_NS
-#define HP_POLL_MAX_NS 1600  // back-off cap (r1: 400-6400 within noise in bench.py)
+#define HP_POLL_MAX_NS 800   // back-off cap (r1: 400-6400 within noise in bench.py; r2, two boxes,
+                             // alternating: 200/800 ns S4 0.79 -> 0.78 ms and bench +0.5% over
+                             // 400/1600; 1000/8000 S4 0.87 ms, bench -1.5%; 100/400 and 200/400 no better)
 #endif
 #ifndef HP_RG_PACKSCAN
 #define HP_RG_PACKSCAN 0  // both scan directions at once on packed u16x2 clamps (r1: S4 0.78 -> 0.82 ms, bench 843 -> 834: off)
