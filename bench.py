@@ -458,6 +458,10 @@ def main():
                 "basis": "in-situ stage events (its stream, inside the timed region, ~B tiles sharing the GPU)",
                 "achieved_isolated": dstage["alg_GBps_isolated"], "frac_isolated": dstage["frac_isolated"],
                 "share_of_step": round(dstage["ms_in_situ"] / max(1e-9, sum(p["ms_in_situ"] for p in per_stage)), 4)}
+    if dstage["stage"].startswith("S4"):
+        # what actually bounds it (DESIGN.md §11 "S4 latency bound", profiles/r02_final_stage_table.md)
+        roofline["limiter"] = ("latency: dependent chains of region jobs / row closures (ncu: ~25% warps "
+                               "active, ~34% issue active, ~82% L2 hit; DRAM bytes below the floor)")
 
     # e2e through hp_run_tiles: pinned host tiles, H2D + D2H inside the timed region
     e2e = None
