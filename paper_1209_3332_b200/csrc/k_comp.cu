@@ -23,6 +23,9 @@
 // Rows land in a staging table and k_rows_scatter orders them by label.  Every relaxation is
 // monotone toward a unique fixed point, so the result equals the oracle's.
 #include <climits>
+#ifdef HP_FILL_DBG
+#include <cstdio>
+#endif
 
 #include "feat_common.cuh"
 
@@ -82,6 +85,23 @@ __device__ __forceinline__ void cunion(int* P, int a, int b) {
             b = t;
         }
         if (atomicCAS(&P[a], a, b) == a) return;
+    }
+}
+
+// The window forests start from horizontal runs: every pixel of a set first points at its left
+// neighbour in the set, then ceil(log2 WX) pointer-jumping rounds make it point at the start of
+// its run (the run's minimum index, so min-index roots survive), and only then do the other
+// neighbours cunion.  (r1-r2 let every pixel cunion with its left neighbour: a warp's lanes
+// hooking consecutive pixels at once chained each run into a list that every later find walked
+// -- instrumented r2: 50-170 us for a 400-pixel S6 window.)  left(li): li - 1 is in li's set
+// and li is not the first column; each(fn): fn over the set.
+template <class Team, class Each, class Left>
+__device__ __forceinline__ void link_runs(const Team& team, int* P, int WX, Each each, Left left) {
+    each([&](int li) { P[li] = left(li) ? li - 1 : li; });
+    team.sync();
+    for (int r = 1; r < WX; r <<= 1) {
+        each([&](int li) { P[li] = P[P[li]]; });
+        team.sync();
     }
 }
 
@@ -338,13 +358,13 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
         if (nv > jp) { S.A[li] = nv; return true; }
         return false;
     });
-    // flat zones of J: union-find over N+ neighbours with equal J (min-index roots)
-    each([&](int li) { S.B[li] = li; });
-    team.sync();
+    // flat zones of J: union-find over N+ neighbours with equal J (min-index roots); members
+    // never sit in the ring, so li - 1 is in the window row
+    link_runs(team, S.B, WX, each, [&](int li) { return S.mem[li - 1] && S.A[li - 1] == S.A[li]; });
     each([&](int li) {
         float jp = S.A[li];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {  // (-1,-1) (0,-1) (1,-1) (-1,0)
+        for (int j = 0; j < 3; ++j) {  // (-1,-1) (0,-1) (1,-1); (-1,0) is the run
             int q = li + nbo[j];
             if (S.mem[q] && S.A[q] == jp) cunion(S.B, li, q);
         }
@@ -466,12 +486,11 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
     });
     team.sync();
     // ---- S10: objects = 8-components of split (union-find), area filter
-    each([&](int li) { S.B[li] = li; });
-    team.sync();
+    link_runs(team, S.B, WX, each, [&](int li) { return S.sp[li] && S.mem[li - 1] && S.sp[li - 1]; });
     each([&](int li) {
         if (!S.sp[li]) return;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 3; ++j) {  // (-1,-1) (0,-1) (1,-1); (-1,0) is the run
             int q = li + nbo[j];
             if (S.mem[q] && S.sp[q]) cunion(S.B, li, q);
         }
@@ -645,10 +664,15 @@ __device__ void fill_isolate(const Team& team, St& S, const FillArgs& a, int WX,
     auto win = [&](auto fn) {
         for (int li = tr; li < NWIN; li += TS) fn(li);
     };
+    auto each_mem = [&](auto fn) {
+        win([&](int li) {
+            if (S.mem[li]) fn(li);
+        });
+    };
+    link_runs(team, S.B, WX, each_mem, [&](int li) { return li % WX > 0 && S.mem[li - 1]; });
     win([&](int li) {
         if (!S.mem[li]) return;
         const int ly = li / WX, lx = li - ly * WX;
-        if (lx > 0 && S.mem[li - 1]) cunion(S.B, li, li - 1);
         if (ly > 0) {
             if (S.mem[li - WX]) cunion(S.B, li, li - WX);
             if (lx > 0 && S.mem[li - WX - 1]) cunion(S.B, li, li - WX - 1);
@@ -672,13 +696,21 @@ __device__ void fill_holes_window(const Team& team, St& S, const FillArgs& a, in
     auto win = [&](auto fn) {
         for (int li = tr; li < NWIN; li += TS) fn(li);
     };
-    win([&](int li) { S.C[li] = S.sp[li] ? -1 : li; });
-    team.sync();
+    win([&](int li) {
+        if (S.sp[li]) S.C[li] = -1;
+    });
+    auto each_bg = [&](auto fn) {
+        win([&](int li) {
+            if (!S.sp[li]) fn(li);
+        });
+    };
+    link_runs(team, S.C, WX, each_bg, [&](int li) { return li % WX > 0 && !S.sp[li - 1]; });
     win([&](int li) {
         if (S.sp[li]) return;
         const int ly = li / WX, lx = li - ly * WX;
-        if (lx > 0 && !S.sp[li - 1]) cunion(S.C, li, li - 1);
-        if (ly > 0 && !S.sp[li - WX]) cunion(S.C, li, li - WX);
+        // one union per touching pair of runs: skip when the left pixels (li - 1, li - 1 - WX)
+        // already joined the same two runs
+        if (ly > 0 && !S.sp[li - WX] && !(lx > 0 && !S.sp[li - 1] && !S.sp[li - WX - 1])) cunion(S.C, li, li - WX);
     });
     team.sync();
     win([&](int li) { S.B[li] = 0; });  // seed flags at the 4-roots
@@ -719,6 +751,18 @@ __device__ void fill_solve(const Team& team, St& S, TeamRed& red, const FillArgs
     auto win = [&](auto fn) {
         for (int li = tr; li < NWIN; li += TS) fn(li);
     };
+#ifdef HP_FILL_DBG
+    const long long t_start = clock64();
+    struct Rep {
+        long long t0; int ts, nwin, area, tr; long long t1 = 0, t2 = 0, t3 = 0; int path = 0;
+        __device__ ~Rep() {
+            const long long t4 = clock64(), dt = t4 - t0;
+            if (tr == 0 && dt > 50000)
+                printf("FILLDBG ts=%d nwin=%d area=%d path=%d cycles=%lld stage=%lld iso=%lld euler=%lld rest=%lld\n", ts,
+                       nwin, area, path, dt, t1 - t0, t2 - t1, t3 - t2, t4 - t3);
+        }
+    } rep_{t_start, TS, NWIN, area, tr};
+#endif
     // stage: candidate pixels (mem), in-tile flags (pm)
     int ncand = 0;
     win([&](int li) {
@@ -733,6 +777,10 @@ __device__ void fill_solve(const Team& team, St& S, TeamRed& red, const FillArgs
     });
     ncand = team.reduce(ncand, red.i, OpAdd());
     team.sync();
+#ifdef HP_FILL_DBG
+    rep_.t1 = clock64();
+    rep_.path = ncand == area ? 1 : 2;
+#endif
     // fast path 1: the window holds no other candidate, so A = every candidate pixel
     if (ncand == area) {
         win([&](int li) { S.sp[li] = S.mem[li]; });
@@ -740,6 +788,9 @@ __device__ void fill_solve(const Team& team, St& S, TeamRed& red, const FillArgs
     } else {
         fill_isolate(team, S, a, WX, NWIN, li_root);
     }
+#ifdef HP_FILL_DBG
+    rep_.t2 = clock64();
+#endif
     // fast path 2: holes of the one 8-component A from its Euler number (bit-quads, Gray 1971:
     // E8 = (n1 - n3 - 2 nD) / 4, holes = 1 - E8 for 4-connected background)
     int q = 0;
@@ -754,6 +805,10 @@ __device__ void fill_solve(const Team& team, St& S, TeamRed& red, const FillArgs
     }
     q = team.reduce(q, red.i, OpAdd());
     const bool holes = (4 - q) / 4 > 0;  // holes = 1 - q / 4
+#ifdef HP_FILL_DBG
+    rep_.t3 = clock64();
+    rep_.path += holes ? 10 : 0;
+#endif
     if (!holes) {
         win([&](int li) {
             if (S.sp[li]) mark_f(a, (int64_t)(wy0 + li / WX) * w + (wx0 + li % WX), root);

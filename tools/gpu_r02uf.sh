@@ -1,0 +1,6 @@
+set -e
+export CUDA_DEVICE_MAX_CONNECTIONS=32
+bash tools/gpu_r02fd.sh || true
+timeout -s KILL 900 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider 2>&1 | tail -2
+bash tools/gpu_ab_ncu.sh r02uf paper_1209_3332_b200/libhp_old.so paper_1209_3332_b200/libhp.so
+bash tools/gpu_ab.sh r02ufb paper_1209_3332_b200/libhp_old.so paper_1209_3332_b200/libhp.so
