@@ -550,6 +550,20 @@ constexpr int kWarpsPB = 4;
 constexpr int kCapB = HP_CAPB, kKoB = 160; // block team (4 warps): the same shared memory, one window
 static_assert(sizeof(CompSm<kCapB, kKoB>) <= kWarpsPB * sizeof(CompSm<kCapW, kKoW>), "block window too big");
 
+// S6 needs only 11 of the 21 B per window pixel (and no feature scratch): its own, smaller
+// per-team storage lets twice as many fill blocks share an SM (r2: the fill kernel's teams are
+// latency-bound on dependent shared-memory passes; 16 warps per SM left them exposed).
+template <int CAP>
+struct FillSm {
+    int32_t B[CAP];
+    int32_t C[CAP];
+    uint8_t mem[CAP];
+    uint8_t pm[CAP];
+    uint8_t sp[CAP];
+};
+constexpr size_t kFillSmem = sizeof(FillSm<kCapB>) > kWarpsPB * sizeof(FillSm<kCapW>) ? sizeof(FillSm<kCapB>)
+                                                                                          : kWarpsPB * sizeof(FillSm<kCapW>);
+
 __device__ __forceinline__ int win_px(int4 bb) { return (bb.z - bb.x + 3) * (bb.w - bb.y + 3); }
 
 __device__ __forceinline__ void to_global(const CompArgs& a, int ci) {
@@ -582,7 +596,7 @@ __global__ void k_comp_classify(CompArgs a, const int32_t* __restrict__ cnt, int
 #define HP_COMP_BPS 4
 #endif
 #ifndef HP_FILL_BPS
-#define HP_FILL_BPS 4
+#define HP_FILL_BPS 8  // fill blocks per SM (FillSm: ~27 KB each)
 #endif
 
 #ifndef HP_COMP_MINB
@@ -696,6 +710,23 @@ __device__ void fill_holes_window(const Team& team, St& S, const FillArgs& a, in
     auto win = [&](auto fn) {
         for (int li = tr; li < NWIN; li += TS) fn(li);
     };
+#ifdef HP_FILL_DBG
+    long long tt[6];
+    int ntt = 0;
+    tt[ntt++] = clock64();
+    struct RepH {
+        long long* tt; int* ntt; int tr, nwin;
+        __device__ ~RepH() {
+            const long long e = clock64();
+            if (tr == 0 && e - tt[0] > 40000)
+                printf("HOLESDBG nwin=%d total=%lld init=%lld jump=%lld union=%lld seed=%lld mark=%lld\n", nwin, e - tt[0],
+                       tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], e - tt[4]);
+        }
+    } reph_{tt, &ntt, tr, NWIN};
+#define HOLES_T() tt[ntt++] = clock64()
+#else
+#define HOLES_T()
+#endif
     win([&](int li) {
         if (S.sp[li]) S.C[li] = -1;
     });
@@ -704,7 +735,9 @@ __device__ void fill_holes_window(const Team& team, St& S, const FillArgs& a, in
             if (!S.sp[li]) fn(li);
         });
     };
+    HOLES_T();
     link_runs(team, S.C, WX, each_bg, [&](int li) { return li % WX > 0 && !S.sp[li - 1]; });
+    HOLES_T();
     win([&](int li) {
         if (S.sp[li]) return;
         const int ly = li / WX, lx = li - ly * WX;
@@ -713,6 +746,7 @@ __device__ void fill_holes_window(const Team& team, St& S, const FillArgs& a, in
         if (ly > 0 && !S.sp[li - WX] && !(lx > 0 && !S.sp[li - 1] && !S.sp[li - WX - 1])) cunion(S.C, li, li - WX);
     });
     team.sync();
+    HOLES_T();
     win([&](int li) { S.B[li] = 0; });  // seed flags at the 4-roots
     team.sync();
     win([&](int li) {
@@ -724,6 +758,7 @@ __device__ void fill_holes_window(const Team& team, St& S, const FillArgs& a, in
         if (seed) S.B[cfind(S.C, li)] = 1;
     });
     team.sync();
+    HOLES_T();
     win([&](int li) {
         if (!S.pm[li]) return;
         const int ly = li / WX, lx = li - ly * WX;
@@ -876,7 +911,7 @@ __global__ void __launch_bounds__(kWarpsPB * 32, 4) k_fill_fused(FillArgs a, con
     __shared__ TeamRed red;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     {
-        auto& S = *reinterpret_cast<CompSm<kCapB, kKoB>*>(smem_raw);
+        auto& S = *reinterpret_cast<FillSm<kCapB>*>(smem_raw);
         const TeamCTA<kWarpsPB * 32> team;
         const int nbig = *nbig_p;
         while (true) {
@@ -890,7 +925,7 @@ __global__ void __launch_bounds__(kWarpsPB * 32, 4) k_fill_fused(FillArgs a, con
         }
     }
     {
-        auto& S = reinterpret_cast<CompSm<kCapW, kKoW>*>(smem_raw)[warp];
+        auto& S = reinterpret_cast<FillSm<kCapW>*>(smem_raw)[warp];
         const TeamWarp team{lane};
         const int ncomp = min(*cnt, cap);
         while (true) {
@@ -1006,7 +1041,7 @@ void launch_fill_components(const uint8_t* big0, int w, int h, Slot& sl, const i
     cudaMemsetAsync(enc, 0, n, s);
     cudaMemsetAsync(sl.lab, 0xff, 4 * n, s);
     FillArgs a{big0, w, h, F, enc, reinterpret_cast<unsigned*>(sl.lab)};
-    const size_t smw = kWarpsPB * sizeof(CompSm<kCapW, kKoW>);
+    const size_t smw = kFillSmem;
     static PerDevice once;
     once.get([&] { return (int)cudaFuncSetAttribute(k_fill_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw); });
     const int32_t cap = sl.comp_cap;
