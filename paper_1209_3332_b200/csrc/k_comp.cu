@@ -23,7 +23,7 @@
 // Rows land in a staging table and k_rows_scatter orders them by label.  Every relaxation is
 // monotone toward a unique fixed point, so the result equals the oracle's.
 #include <climits>
-#ifdef HP_FILL_DBG
+#if defined(HP_FILL_DBG) || defined(HP_COMP_DBG)
 #include <cstdio>
 #endif
 
@@ -114,6 +114,11 @@ __device__ __forceinline__ void write_row(const CompArgs& a, int32_t label, int 
     }
 }
 
+#ifdef HP_COMP_DBG
+__device__ unsigned long long g_compdbg[13];
+__device__ unsigned int g_compdbg_done;
+#endif
+
 // ---------------------------------------------------------------- shared-memory path
 // Per-team window storage (4-byte planes first for alignment); 19 B per window pixel.
 template <int CAP, int KO>
@@ -199,6 +204,26 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
         int ly = li / WX, lx = li - ly * WX;
         return (int32_t)((int64_t)(wy0 + ly) * w + (wx0 + lx));
     };
+#ifdef HP_COMP_DBG  // experiment: clock64 per phase, summed over the launch (tools/gpu_r02cd2.sh)
+    long long ct[12];
+    int nct = 0;
+    struct RepC {
+        long long* ct; int* nct; int tr;
+        __device__ ~RepC() {
+            const long long e = clock64();
+            if (tr == 0 && *nct == 11) {
+                for (int k = 0; k < 10; ++k) atomicAdd(&g_compdbg[k], (unsigned long long)(ct[k + 1] - ct[k]));
+                atomicAdd(&g_compdbg[10], (unsigned long long)(e - ct[10]));
+                atomicAdd(&g_compdbg[11], (unsigned long long)(e - ct[0]));
+                atomicAdd(&g_compdbg[12], 1ull);
+            }
+        }
+    } repc_{ct, &nct, tr};
+#define COMP_T() ct[nct++] = clock64()
+#else
+#define COMP_T()
+#endif
+    COMP_T();
     // ---- stage the window (ring pixels are never members: no bounds checks later) and list
     // the members, so every later pass touches members only
     if (tr == 0) {
@@ -232,6 +257,7 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
     auto each = [&](auto fn) {
         for (int k = tr; k < nmem; k += TS) fn((int)S.list[k]);
     };
+    COMP_T();
     // ---- S7 EDT of the members, exactly, inside the window (reading C11).
     // For a member p at distance d from the nearest background pixel q, the open disk of
     // radius d around p is foreground and 8-connected, so it lies in p's component; one
@@ -346,6 +372,7 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
             if (!team.any(ch)) break;
         }
     };
+    COMP_T();
     // ---- S8: J = recon(dist - h, dist)
     each([&](int li) { S.A[li] = fminf(__fsub_rn(S.dist[li], a.hh), S.dist[li]); });
     team.sync();
@@ -386,6 +413,7 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
         }
     });
     team.sync();
+    COMP_T();
     // ---- markers -> L initial (ML = 1 + global min index of the zone, else inf) and W1 init
     each([&](int li) { S.pm[li] = S.C[S.B[li]] == 0; });  // staged: zone flags live at roots
     team.sync();
@@ -395,6 +423,7 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
         S.A[li] = ml != kInfI ? S.dist[li] : -INFINITY;
     });
     team.sync();
+    COMP_T();
     // ---- S9 W1: c = recon(dist on markers else -inf, dist)
     converge([&](int li) -> bool {
         float cp = S.A[li], b = cp;
@@ -405,6 +434,7 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
         if (nv > cp) { S.A[li] = nv; return true; }
         return false;
     });
+    COMP_T();
     // ---- W2: plateau distance (markers: B != inf)
     each([&](int li) {
         int32_t v = kInfI;
@@ -434,6 +464,7 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
         if (b < dp) { S.C[li] = b; return true; }
         return false;
     });
+    COMP_T();
     // ---- parents: argmin over neighbours with c(q) >= c(p) of (-c(q), d(q))
     each([&](int li) {
         uint8_t bits = 0;
@@ -462,6 +493,7 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
         S.pm[li] = bits;
     });
     team.sync();
+    COMP_T();
     // ---- W3: L = min over parents
     converge([&](int li) -> bool {
         int pmk = S.pm[li];
@@ -473,6 +505,7 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
         if (b < lp) { S.B[li] = b; return true; }
         return false;
     });
+    COMP_T();
     // ---- lines, split
     each([&](int li) {
         int32_t lp = S.B[li];
@@ -485,6 +518,7 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
         S.sp[li] = v;
     });
     team.sync();
+    COMP_T();
     // ---- S10: objects = 8-components of split (union-find), area filter
     link_runs(team, S.B, WX, each, [&](int li) { return S.sp[li] && S.mem[li - 1] && S.sp[li - 1]; });
     each([&](int li) {
@@ -522,6 +556,7 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
     });
     if (tr == 0 && nobj) atomicAdd(a.n_objects, nobj);
     team.sync();
+    COMP_T();
     // ---- S11: features of each kept object
     if (a.do_features) {
         for (int k = 0; k < nobj; ++k) {
@@ -643,6 +678,19 @@ __global__ void __launch_bounds__(kWarpsPB * 32, HP_COMP_MINB) k_comp_fused(Comp
             __syncwarp();
         }
     }
+#ifdef HP_COMP_DBG
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&g_compdbg_done, 1u) == gridDim.x - 1) {
+            unsigned long long* c = g_compdbg;
+            printf("COMPSUM n=%llu total=%llu stage=%llu edt=%llu J+zones+rmax=%llu mark=%llu W1=%llu W2=%llu par=%llu W3=%llu lines=%llu S10=%llu S11=%llu\n",
+                   c[12], c[11], c[0], c[1], c[2], c[3], c[4], c[5], c[6], c[7], c[8], c[9], c[10]);
+            for (int k = 0; k < 13; ++k) c[k] = 0;
+            g_compdbg_done = 0;
+        }
+    }
+#endif
 }
 
 // ---------------------------------------------------------------- S6 per S5 component
