@@ -157,8 +157,10 @@ __device__ void object_features(const Team& team, InP inP, const uint8_t* __rest
         int border = 0;
         double gs = 0.0;
         float gmin = INFINITY, gmax = -INFINITY;
-        for (int k = tr; k < nb; k += TS) {
-            int y = by0 + k / sw, x = bx0 + k % sw;
+        // the search box in team order: (x, y) advanced by the team size without a division
+        const int dsx = TS % sw, dsy = TS / sw;
+        for (int k = tr, x = bx0 + tr % sw, y = by0 + tr / sw; k < nb;
+             k += TS, x += dsx, y += dsy, (x > bx1 ? (x -= sw, ++y) : 0)) {
             if (!inP(x, y)) continue;
             ++A;
             oxmin = min(oxmin, x);
@@ -218,8 +220,8 @@ __device__ void object_features(const Team& team, InP inP, const uint8_t* __rest
         const double Ad = (double)A;
         const double gmean = gs / Ad;
         double g2 = 0.0, g3 = 0.0, g4 = 0.0;
-        for (int k = tr; k < nb; k += TS) {
-            int y = by0 + k / sw, x = bx0 + k % sw;
+        for (int k = tr, x = bx0 + tr % sw, y = by0 + tr / sw; k < nb;
+             k += TS, x += dsx, y += dsy, (x > bx1 ? (x -= sw, ++y) : 0)) {
             if (!inP(x, y)) continue;
             double dv = (double)sobel(x, y) - gmean;
             double d2 = dv * dv;

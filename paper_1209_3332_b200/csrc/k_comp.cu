@@ -561,10 +561,11 @@ __device__ bool comp_solve(const Team& team, St& S, TeamRed& red, const CompArgs
     if (a.do_features) {
         for (int k = 0; k < nobj; ++k) {
             const int r = S.objroot[k];
+            // object_features only asks about pixels of the component's bounding box and the
+            // 4- / 8-neighbours of object pixels, all inside the window (bbox + 1-px ring): no
+            // bounds checks
             auto inP = [&](int x, int y) -> bool {
-                int lx = x - wx0, ly = y - wy0;
-                if (lx < 0 || ly < 0 || lx >= WX || ly >= WY) return false;
-                const int li = ly * WX + lx;  // non-members hold stale values: test mem first
+                const int li = (y - wy0) * WX + (x - wx0);  // non-members hold stale values: test mem first
                 return S.mem[li] && S.B[li] == r;
             };
             int border = 0;
