@@ -632,7 +632,7 @@ __global__ void k_comp_classify(CompArgs a, const int32_t* __restrict__ cnt, int
 #define HP_COMP_BPS 4
 #endif
 #ifndef HP_FILL_BPS
-#define HP_FILL_BPS 8  // fill blocks per SM (FillSm: ~27 KB each)
+#define HP_FILL_BPS 4  // fill blocks per SM (FillSm: ~27 KB each; r2 sweep 2 / 3 / 4 / 8 within 1%, 4 ahead in 3 of 4 pairs)
 #endif
 
 #ifndef HP_COMP_MINB
