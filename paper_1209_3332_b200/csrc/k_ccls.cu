@@ -56,6 +56,31 @@ struct Sel {
         if (MODE == SEL_AREA_TH) return ((int)__ldg(plane + p) - (int)__ldg(R + p)) > g1 && !__ldg(rbc + p);
         return __ldg(plane + p);
     }
+    // the bytes of pixels x0 .. x0 + 3 of row y (x0 a multiple of 4, y < h): one 32-bit load per
+    // plane where the row is 4-byte aligned and the 4 pixels lie in the image, else per byte
+    // (out-of-image bytes 0)
+    template <int MODE>
+    __device__ __forceinline__ uint32_t load4(int y, int x0) const {
+        const int64_t p = (int64_t)y * w + x0;
+        if ((w & 3) == 0 && x0 + 3 < w) {
+            const uint32_t a = __ldg(reinterpret_cast<const unsigned int*>(plane + p));
+            if (MODE != SEL_AREA_TH) return a;
+            const uint32_t r = __ldg(reinterpret_cast<const unsigned int*>(R + p));
+            const uint32_t b = __ldg(reinterpret_cast<const unsigned int*>(rbc + p));
+            uint32_t o = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int gv = (a >> (8 * k)) & 0xff, rv = (r >> (8 * k)) & 0xff, bv = (b >> (8 * k)) & 0xff;
+                o |= (uint32_t)((gv - rv) > g1 && !bv) << (8 * k);
+            }
+            return o;
+        }
+        uint32_t o = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (x0 + k < w) o |= (uint32_t)load<MODE>(p + k) << (8 * k);
+        return o;
+    }
     template <int MODE>
     __device__ __forceinline__ bool fg(uint8_t v) const {
         if (MODE == SEL_AREA || MODE == SEL_AREA_TH || MODE == SEL_EDGE) return v != 0;
@@ -173,33 +198,79 @@ __device__ __forceinline__ bool is_run_start(unsigned fm, int lane) {
     return ((fm >> lane) & 1) && !(lane > 0 && ((fm >> (lane - 1)) & 1));
 }
 
+// rows of a thread (lane = column in every pass): S5's word set-up gives warp w the tile rows
+// 4w .. 4w + 3, the byte set-up the rows w + 8k
+template <int MODE>
+__device__ __forceinline__ int tile_row(int k) {
+    return MODE == SEL_AREA_TH ? 4 * (int)(threadIdx.x >> 5) + k : (int)(threadIdx.x >> 5) + 8 * k;
+}
+
 template <int MODE>
 __device__ __forceinline__ int tile_uf(const Sel& sel, int conn, int tx0, int ty0, TileSm& T, uint8_t (&v)[4],
                                        unsigned (&fms)[4], bool clear_acc) {
     const int lane = threadIdx.x & 31;
     const int w = sel.w, h = sel.h;
-    const int gx = tx0 + lane;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int gy = ty0 + (threadIdx.x >> 5) + 8 * k;
-        v[k] = (gx < w && gy < h) ? sel.load<MODE>((int64_t)gy * w + gx) : (uint8_t)0;
-    }
     int nfg = 0;
+    if constexpr (MODE != SEL_AREA_TH) {
+        const int gx = tx0 + lane;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int ly = (threadIdx.x >> 5) + 8 * k;
-        const int gy = ty0 + ly;
-        const bool f = gx < w && gy < h && sel.fg<MODE>(v[k]);
-        const unsigned fm = __ballot_sync(0xffffffffu, f);
-        const unsigned bm = __ballot_sync(0xffffffffu, f && sel.bit<MODE>(v[k], gx, gy));
-        fms[k] = fm;
-        if (lane == 0) {
-            T.rowm[ly] = fm;
-            T.bitm[ly] = bm;
+        for (int k = 0; k < 4; ++k) {
+            const int gy = ty0 + tile_row<MODE>(k);
+            v[k] = (gx < w && gy < h) ? sel.load<MODE>((int64_t)gy * w + gx) : (uint8_t)0;
         }
-        nfg += f;
-        T.s[ly * kT + lane] = f ? ly * kT + run_start(fm, lane) : -1;
-        if (clear_acc) T.acc[ly * kT + lane] = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int ly = tile_row<MODE>(k);
+            const int gy = ty0 + ly;
+            const bool f = gx < w && gy < h && sel.fg<MODE>(v[k]);
+            const unsigned fm = __ballot_sync(0xffffffffu, f);
+            const unsigned bm = __ballot_sync(0xffffffffu, f && sel.bit<MODE>(v[k], gx, gy));
+            fms[k] = fm;
+            if (lane == 0) {
+                T.rowm[ly] = fm;
+                T.bitm[ly] = bm;
+            }
+            nfg += f;
+            T.s[ly * kT + lane] = f ? ly * kT + run_start(fm, lane) : -1;
+            if (clear_acc) T.acc[ly * kT + lane] = 0;
+        }
+    } else {
+        // S5 sets up a word per thread: its candidate is a function of three planes (g, recon, rbc),
+        // so 3 word loads replace 12 byte loads (r2: k_cs_local<3> 67.4 -> 62.2 us per 4K tile; for
+        // the one-plane passes the shuffles cost more than they save).  lane -> row 4 * warp +
+        // (lane >> 3), pixels 4 * (lane & 7) .. + 3; the warp's four row masks by segmented ORs
+        const int wc = 4 * (lane & 7);
+        const int gyw = ty0 + tile_row<MODE>(lane >> 3), gxw = tx0 + wc;
+        const uint32_t word = gyw < h ? sel.load4<MODE>(gyw, gxw) : 0u;
+        unsigned xf = 0, xb = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const uint8_t vb = (uint8_t)(word >> (8 * b));
+            const bool f = gyw < h && gxw + b < w && sel.fg<MODE>(vb);
+            xf |= (unsigned)f << (wc + b);
+            xb |= (unsigned)(f && sel.bit<MODE>(vb, gxw + b, gyw)) << (wc + b);
+        }
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            xf |= __shfl_xor_sync(0xffffffffu, xf, o);
+            xb |= __shfl_xor_sync(0xffffffffu, xb, o);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int ly = tile_row<MODE>(k);
+            const unsigned fm = __shfl_sync(0xffffffffu, xf, 8 * k);
+            const unsigned bm = __shfl_sync(0xffffffffu, xb, 8 * k);
+            v[k] = 0;  // (read by the S2 output pass only)
+            fms[k] = fm;
+            if (lane == 0) {
+                T.rowm[ly] = fm;
+                T.bitm[ly] = bm;
+            }
+            const bool f = (fm >> lane) & 1;
+            nfg += f;
+            T.s[ly * kT + lane] = f ? ly * kT + run_start(fm, lane) : -1;
+            if (clear_acc) T.acc[ly * kT + lane] = 0;
+        }
     }
     if (threadIdx.x == 0) T.nr = 0;
     const int any_fg = __syncthreads_or(nfg > 0);
@@ -208,7 +279,7 @@ __device__ __forceinline__ int tile_uf(const Sel& sel, int conn, int tx0, int ty
     if (all_fg) return 2;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const int ly = (threadIdx.x >> 5) + 8 * k;
+        const int ly = tile_row<MODE>(k);
         const unsigned fm = fms[k];
         if (ly == 0 || !((fm >> lane) & 1) || (lane > 0 && ((fm >> (lane - 1)) & 1))) continue;  // run starts
         const unsigned above = T.rowm[ly - 1];
@@ -285,7 +356,7 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
     int rk[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const int ly = (threadIdx.x >> 5) + 8 * k;
+        const int ly = tile_row<MODE>(k);
         const unsigned fm = fms[k];
         rk[k] = 0;
         if (!is_run_start(fm, lane)) continue;
@@ -303,7 +374,7 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
     }
 #pragma unroll
     for (int k = 0; k < 4 && lr_mode<MODE>(); ++k) {
-        const int ly = (threadIdx.x >> 5) + 8 * k;
+        const int ly = tile_row<MODE>(k);
         const unsigned fm = fms[k];
         const bool f = (fm >> lane) & 1;
         const int r = __shfl_sync(0xffffffffu, rk[k], f ? run_start(fm, lane) : lane);
@@ -314,7 +385,7 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
     // roots: run starts that are their own parent
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        const int ly = (threadIdx.x >> 5) + 8 * k;
+        const int ly = tile_row<MODE>(k);
         const int li = ly * kT + lane;
         if (T.s[li] == li) {
             const int32_t G = gidx(li);
@@ -437,7 +508,7 @@ __global__ void __launch_bounds__(256) k_cs_out(Sel sel, int conn, const int32_t
         if (kd == 2) prop0 = __ldg(X + __ldg(P + (int32_t)((int64_t)ty0 * w + tx0)));
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const int ly = (threadIdx.x >> 5) + 8 * k;
+            const int ly = tile_row<MODE>(k);
             const int gy = ty0 + ly;
             const unsigned fm = fms[k];
             const bool f = (fm >> lane) & 1;
