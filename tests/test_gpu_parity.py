@@ -633,6 +633,45 @@ def test_run_tiles(ctx):
         assert_features_equal(got[i][0], got[i][1], got[i][2], ol, of, ot)
 
 
+@pytest.mark.parametrize("where", ["next_tile", "on_done"])
+def test_run_tiles_callback_errors_propagate(ctx, where):
+    """An exception raised in either Python callback of run_tiles is re-raised by run_tiles
+    itself once the driver returns (ctypes would print and swallow it: ADVICE r1), no further
+    tile is fed after it, and the context stays usable."""
+    import torch
+    tiles = [torch.from_numpy(make_tile(140 + i, TileSpec(256, 256))["rgb"]).pin_memory() for i in range(3)]
+    fed = []
+
+    def nxt():
+        k = len(fed)
+        if where == "next_tile" and k == 1:
+            raise ValueError("feeder failed")
+        if k >= len(tiles):
+            return None
+        fed.append(k)
+        return tiles[k].data_ptr(), 3 * 256, k
+
+    def done(tid, lab, fl, ft, st):
+        assert st == 0
+        if where == "on_done":
+            raise KeyError("sink failed")
+
+    with pytest.raises(ValueError if where == "next_tile" else KeyError):
+        ctx.run_tiles(nxt, done, 256, 256)
+    if where == "next_tile":
+        assert fed == [0]
+    # the context still runs tiles afterwards
+    got = []
+    it = iter(range(len(tiles)))
+
+    def nxt2():
+        k = next(it, None)
+        return None if k is None else (tiles[k].data_ptr(), 3 * 256, k)
+
+    ctx.run_tiles(nxt2, lambda tid, lab, fl, ft, st: got.append((tid, st)), 256, 256)
+    assert sorted(got) == [(k, 0) for k in range(len(tiles))]
+
+
 def _arena(torch, cap):
     from paper_1209_3332_b200.hp import NFEAT
     dev = "cuda"
