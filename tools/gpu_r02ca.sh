@@ -2,7 +2,7 @@
 # S4 register carry (HP_RG_CARRY=1 variant): parity, A/B bench + config 2 / config 5
 O=gpurun_out/${OUTN:-r02ca}; mkdir -p $O
 export CUDA_DEVICE_MAX_CONNECTIONS=32
-SO=$PWD/paper_1209_3332_b200/libhp_carry.so
+SO=$PWD/paper_1209_3332_b200/libhp_${VAR:-carry}.so
 HP_SO=$SO timeout -s KILL 900 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider -k "recon or iwpp or pipeline or hot_path or bench_tiles" > $O/pytest.log 2>&1; echo "rc=$?" >> $O/pytest.log; tail -2 $O/pytest.log
 for v in A B A B; do
   so=$PWD/paper_1209_3332_b200/libhp.so; [ $v = B ] && so=$SO
