@@ -211,6 +211,9 @@ __device__ __forceinline__ int tile_uf(const Sel& sel, int conn, int tx0, int ty
     const int lane = threadIdx.x & 31;
     const int w = sel.w, h = sel.h;
     int nfg = 0;
+    unsigned bms[4];
+    // phase 1: the row masks only (registers); an empty tile leaves after one vote without a
+    // shared-memory write (S2's RBC_LO and S5's candidates leave most tiles empty)
     if constexpr (MODE != SEL_AREA_TH) {
         const int gx = tx0 + lane;
 #pragma unroll
@@ -220,19 +223,11 @@ __device__ __forceinline__ int tile_uf(const Sel& sel, int conn, int tx0, int ty
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const int ly = tile_row<MODE>(k);
-            const int gy = ty0 + ly;
+            const int gy = ty0 + tile_row<MODE>(k);
             const bool f = gx < w && gy < h && sel.fg<MODE>(v[k]);
-            const unsigned fm = __ballot_sync(0xffffffffu, f);
-            const unsigned bm = __ballot_sync(0xffffffffu, f && sel.bit<MODE>(v[k], gx, gy));
-            fms[k] = fm;
-            if (lane == 0) {
-                T.rowm[ly] = fm;
-                T.bitm[ly] = bm;
-            }
+            fms[k] = __ballot_sync(0xffffffffu, f);
+            bms[k] = __ballot_sync(0xffffffffu, f && sel.bit<MODE>(v[k], gx, gy));
             nfg += f;
-            T.s[ly * kT + lane] = f ? ly * kT + run_start(fm, lane) : -1;
-            if (clear_acc) T.acc[ly * kT + lane] = 0;
         }
     } else {
         // S5 sets up a word per thread: its candidate is a function of three planes (g, recon, rbc),
@@ -257,25 +252,28 @@ __device__ __forceinline__ int tile_uf(const Sel& sel, int conn, int tx0, int ty
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const int ly = tile_row<MODE>(k);
-            const unsigned fm = __shfl_sync(0xffffffffu, xf, 8 * k);
-            const unsigned bm = __shfl_sync(0xffffffffu, xb, 8 * k);
+            fms[k] = __shfl_sync(0xffffffffu, xf, 8 * k);
+            bms[k] = __shfl_sync(0xffffffffu, xb, 8 * k);
             v[k] = 0;  // (read by the S2 output pass only)
-            fms[k] = fm;
-            if (lane == 0) {
-                T.rowm[ly] = fm;
-                T.bitm[ly] = bm;
-            }
-            const bool f = (fm >> lane) & 1;
-            nfg += f;
-            T.s[ly * kT + lane] = f ? ly * kT + run_start(fm, lane) : -1;
-            if (clear_acc) T.acc[ly * kT + lane] = 0;
+            nfg += (fms[k] >> lane) & 1;
         }
     }
-    if (threadIdx.x == 0) T.nr = 0;
-    const int any_fg = __syncthreads_or(nfg > 0);
+    if (!__syncthreads_or(nfg > 0)) return 0;
     const int all_fg = __syncthreads_and(nfg == 4);
-    if (!any_fg) return 0;
+    // phase 2: the tile's run pointers, masks and accumulators in shared memory
+    if (threadIdx.x == 0) T.nr = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int ly = tile_row<MODE>(k);
+        const unsigned fm = fms[k];
+        if (lane == 0) {
+            T.rowm[ly] = fm;
+            T.bitm[ly] = bms[k];
+        }
+        T.s[ly * kT + lane] = ((fm >> lane) & 1) ? ly * kT + run_start(fm, lane) : -1;
+        if (clear_acc) T.acc[ly * kT + lane] = 0;
+    }
+    __syncthreads();
     if (all_fg) return 2;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
