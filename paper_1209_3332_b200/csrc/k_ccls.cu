@@ -207,7 +207,7 @@ __device__ __forceinline__ int tile_row(int k) {
 
 template <int MODE>
 __device__ __forceinline__ int tile_uf(const Sel& sel, int conn, int tx0, int ty0, TileSm& T, uint8_t (&v)[4],
-                                       unsigned (&fms)[4], bool clear_acc) {
+                                       unsigned (&fms)[4], bool clear_acc, int (*bbs)[kT * kT] = nullptr) {
     const int lane = threadIdx.x & 31;
     const int w = sel.w, h = sel.h;
     int nfg = 0;
@@ -272,6 +272,13 @@ __device__ __forceinline__ int tile_uf(const Sel& sel, int conn, int tx0, int ty
         }
         T.s[ly * kT + lane] = ((fm >> lane) & 1) ? ly * kT + run_start(fm, lane) : -1;
         if (clear_acc) T.acc[ly * kT + lane] = 0;
+        if (bbs && is_run_start(fm, lane)) {  // S5's bounding boxes: only run starts can be roots
+            const int li = ly * kT + lane;
+            bbs[0][li] = INT_MAX;
+            bbs[1][li] = INT_MAX;
+            bbs[2][li] = -1;
+            bbs[3][li] = -1;
+        }
     }
     __syncthreads();
     if (all_fg) return 2;
@@ -310,17 +317,12 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
     const int t = blockIdx.y * gridDim.x + blockIdx.x;
     const int lane = threadIdx.x & 31;
     const int w = sel.w, h = sel.h;
-    if constexpr (BB) {
-        for (int i = threadIdx.x; i < kT * kT; i += blockDim.x) {
-            bbs[0][i] = INT_MAX;
-            bbs[1][i] = INT_MAX;
-            bbs[2][i] = -1;
-            bbs[3][i] = -1;
-        }
-    }
     uint8_t v[4];
     unsigned fms[4];
-    const int kind = tile_uf<MODE>(sel, conn, tx0, ty0, T, v, fms, true);  // (its barriers order bbs)
+    // (tile_uf initialises the bounding boxes of the run starts, before its last barrier)
+    int (*bbp)[kT * kT] = nullptr;
+    if constexpr (BB) bbp = bbs;
+    const int kind = tile_uf<MODE>(sel, conn, tx0, ty0, T, v, fms, true, bbp);
     int32_t* Et = E + (int64_t)t * 4 * kT;
     auto gidx = [&](int li) -> int32_t { return (int32_t)((int64_t)(ty0 + li / kT) * w + tx0 + li % kT); };
     if (threadIdx.x == 0) kinds[t] = (uint8_t)kind;
