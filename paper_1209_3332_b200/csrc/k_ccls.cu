@@ -326,8 +326,7 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
     int32_t* Et = E + (int64_t)t * 4 * kT;
     auto gidx = [&](int li) -> int32_t { return (int32_t)((int64_t)(ty0 + li / kT) * w + tx0 + li % kT); };
     if (threadIdx.x == 0) kinds[t] = (uint8_t)kind;
-    if (kind == 0) {
-        if (threadIdx.x < 4 * kT) Et[threadIdx.x] = -1;
+    if (kind == 0) {  // (its edge roots are not written: k_cs_merge reads the tile's kind first)
         if (threadIdx.x == 0) nroots[t] = 0;
         return;
     }
@@ -421,16 +420,20 @@ __global__ void __launch_bounds__(256) k_cs_local(Sel sel, int conn, int32_t* __
 // which also covers every right-column diagonal; 4-conn: i0 .. i1); the 8-conn corner
 // diagonals (up-left of (0,0), up-right of (31,0)) are taken by the top row's end lanes.
 __global__ void __launch_bounds__(256) k_cs_merge(int conn, int ntx, int nty, const int32_t* __restrict__ E,
-                                                  int32_t* __restrict__ P, const int32_t* __restrict__ gate) {
+                                                  int32_t* __restrict__ P, const int32_t* __restrict__ gate,
+                                                  const uint8_t* __restrict__ kinds) {
     if (gate && *gate == 0) return;
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gt >= (int64_t)ntx * nty * 2 * kT) return;  // (whole warps: 2 * kT per tile)
     const int t = (int)(gt / (2 * kT)), j = (int)(gt % (2 * kT));
+    if (__ldg(kinds + t) == 0) return;  // an empty tile has no edge roots (whole warps)
     const int bx = t % ntx, by = t / ntx;
     const int side = j >> 5, i = j & 31;
     auto e = [&](int tx, int ty, int sd, int k) -> int32_t {
         if (tx < 0 || ty < 0 || tx >= ntx || ty >= nty) return -1;
-        return __ldg(E + ((int64_t)(ty * ntx + tx)) * 4 * kT + sd * kT + k);
+        const int64_t tt = (int64_t)ty * ntx + tx;
+        if (__ldg(kinds + tt) == 0) return -1;
+        return __ldg(E + tt * 4 * kT + sd * kT + k);
     };
     const int ntxb = side == 0 ? bx : bx - 1, ntyb = side == 0 ? by - 1 : by;  // tile across the edge
     const int nside = side == 0 ? 1 : 3;                                       // its bottom row / right column
@@ -609,8 +612,8 @@ void run_select(Sel sel, int conn, Slot& sl, uint8_t* out, cudaStream_t s, const
     int32_t* X = sel.X ? sel.X : sl.aux;
     (note_launch(), k_cs_local<MODE><<<grid, 256, 0, s>>>(sel, conn, P, X, sl.cs_edge, sl.cs_roots, sl.cs_nroots,
                                                            sl.cs_lr, sl.cs_kind));
-    (note_launch(), k_cs_merge<<<(int)(((int64_t)ntiles * 2 * kT + 255) / 256), 256, 0, s>>>(conn, ntx, nty,
-                                                                                           sl.cs_edge, P, sel.gate));
+    (note_launch(), k_cs_merge<<<(int)(((int64_t)ntiles * 2 * kT + 255) / 256), 256, 0, s>>>(
+                        conn, ntx, nty, sl.cs_edge, P, sel.gate, sl.cs_kind));
     (note_launch(), k_cs_accum<<<(ntiles + 7) / 8, 256, 0, s>>>(ntiles, sl.cs_roots, sl.cs_nroots, P, X, sel));
     if (out) {
         if (MODE != SEL_FILL) cudaMemsetAsync(out, 0, (size_t)w * h, s);
